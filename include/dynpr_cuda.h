@@ -1,0 +1,236 @@
+/*
+ * dynpr_cuda.h -- C-ABI of the B200-native Static / DF-P PageRank engine.
+ *
+ * This is the drop-in boundary for the compute path of the reference C++
+ * library `dynpr` (/root/reference/proj).  The reference exposes a plain
+ * C++20 API in namespace `dynpr` and has no FFI of its own; every entry point
+ * below replaces one reference function (cited file:line) and keeps its
+ * argument meaning, its validation order and its exception message text
+ * (returned through dynpr_last_error()).  A C++ shim that restores the exact
+ * `dynpr::` signatures on top of this ABI is include/dynpr_b200.hpp; the
+ * Python mirror of the reference's pybind11 module is
+ * paper_2404_08299_b200/__init__.py.  INTEGRATION.md shows both bindings.
+ *
+ * Conventions
+ *  - Every function returns a dynpr_status; on failure the thread-local
+ *    dynpr_last_error() holds the message (the reference's exception text for
+ *    validation errors, e.g. "engine: empty graph").
+ *  - Plain pointers + sizes only.  Array arguments may be host memory
+ *    (pageable or pinned) or device memory of the context's GPU; the library
+ *    detects which with cudaPointerGetAttributes and copies as needed.
+ *  - Graph handles are immutable device CSR arrays ("snapshots"), exactly like
+ *    the reference's value-typed CsrGraph (graph.hpp:17-49).  Operations that
+ *    produce a new snapshot (add_self_loops, transpose, apply_batch) return a
+ *    new handle and never mutate their input.
+ *  - All calls are synchronous on return.  One context per host thread at a
+ *    time (reference SPEC: each engine call is single-caller).
+ *  - Types follow graph.hpp:9,47-48: vertex ids uint32, CSR offsets uint64,
+ *    ranks fp64, affected flags uint8 (frontier.hpp:16-17).
+ */
+#ifndef DYNPR_CUDA_H
+#define DYNPR_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum dynpr_status {
+  DYNPR_OK = 0,
+  DYNPR_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference */
+  DYNPR_CUDA_ERROR = 2,
+  DYNPR_NCCL_ERROR = 3,
+  DYNPR_OUT_OF_MEMORY = 4,
+  DYNPR_SIZING_ERROR = 5      /* dynpr::SizingError (workload.hpp:17-19) */
+} dynpr_status;
+
+/* rank.hpp:14-18 PartitionStrategy */
+enum {
+  DYNPR_DONT_PARTITION = 0,
+  DYNPR_PARTITION_TRANSPOSE = 1,
+  DYNPR_PARTITION_BOTH = 2
+};
+
+/* rank.hpp:23 RankMode */
+enum { DYNPR_RANK_PLAIN = 0, DYNPR_RANK_CLOSED_LOOP_PRUNE = 1 };
+
+/* rank.hpp:25-39 EngineConfig, field for field. */
+typedef struct dynpr_config {
+  double damping_factor;         /* alpha, default 0.85 */
+  double iteration_tolerance;    /* L-inf convergence threshold, 1e-10 */
+  double frontier_tolerance;     /* tau_f, 1e-6 */
+  double prune_tolerance;        /* tau_p, 1e-6 */
+  int32_t max_iterations;        /* 500 */
+  uint32_t low_degree_threshold; /* D_P, 32 */
+  int32_t partition_strategy;    /* DYNPR_PARTITION_BOTH */
+  int32_t convergence_check_disabled; /* 0 */
+} dynpr_config;
+
+/* engine.hpp:16-22 RankResult telemetry (ranks are returned separately). */
+typedef struct dynpr_stats {
+  int32_t iterations;
+  int32_t converged;
+  uint64_t affected_vertex_iterations;
+  double final_delta;
+  uint64_t processed_edges; /* sum of in-degree over processed vertices */
+  double device_ms;         /* CUDA-event time of the engine call */
+} dynpr_stats;
+
+/*
+ * Per-iteration observer (engine.hpp:24-27 IterationObserver).  `ranks` is a
+ * host copy of the latest iterate; `processed` is a host copy of the
+ * vertexAffected flags at the start of that sweep (the processed set), or
+ * NULL for the full-sweep engines.  Only honoured when non-NULL: it forces a
+ * device-to-host copy per iteration.
+ */
+typedef void (*dynpr_observer)(int iteration, const double* ranks,
+                               const uint8_t* processed, uint64_t n,
+                               void* user);
+
+typedef struct dynpr_context dynpr_context;
+typedef struct dynpr_graph dynpr_graph;
+
+/* ---- errors, config ----------------------------------------------------- */
+const char* dynpr_last_error(void);
+const char* dynpr_version(void);
+void dynpr_config_default(dynpr_config* cfg);
+/* EngineConfig::validate (rank.cpp:11-20), same messages. */
+dynpr_status dynpr_config_validate(const dynpr_config* cfg);
+
+/* ---- context ------------------------------------------------------------ */
+dynpr_status dynpr_context_create(int device, dynpr_context** out);
+dynpr_status dynpr_context_destroy(dynpr_context* ctx);
+/* Kernel-launch counter (every kernel this library launched). */
+uint64_t dynpr_context_launches(const dynpr_context* ctx);
+/*
+ * Profiling: when enabled the engines bracket every rank-update sweep with
+ * CUDA events on their stream; dynpr_context_sweep_times returns the summed
+ * sweep time (ms) and the number of sweeps since the last reset.
+ */
+dynpr_status dynpr_context_set_profiling(dynpr_context* ctx, int enable);
+dynpr_status dynpr_context_sweep_times(dynpr_context* ctx, double* total_ms,
+                                       uint64_t* sweeps, uint64_t* bytes);
+
+/* ---- graphs (graph.hpp:17-80) ------------------------------------------- */
+/* CsrGraph(vertexCount, offsets, targets) incl. validation (graph.cpp:30-49).
+ * offsets has n+1 entries, targets offsets[n] entries. */
+dynpr_status dynpr_graph_from_csr(dynpr_context* ctx, uint32_t n,
+                                  const uint64_t* offsets,
+                                  const uint32_t* targets, uint64_t m,
+                                  dynpr_graph** out);
+/* buildCsr (graph.cpp:56-68): sort + dedupe, throws on ids >= n. */
+dynpr_status dynpr_graph_build(dynpr_context* ctx, uint32_t n,
+                               const uint32_t* src, const uint32_t* dst,
+                               uint64_t count, dynpr_graph** out);
+/* addSelfLoops (graph.cpp:85-111). */
+dynpr_status dynpr_graph_add_self_loops(dynpr_context* ctx,
+                                        const dynpr_graph* g,
+                                        dynpr_graph** out);
+/* transpose (graph.cpp:70-83): slices in ascending source order. */
+dynpr_status dynpr_graph_transpose(dynpr_context* ctx, const dynpr_graph* g,
+                                   dynpr_graph** out);
+/* applyBatch (graph.cpp:113-203): (E \ dels) U ins, loops re-ensured.
+ * missing / duplicate may be NULL; otherwise they are ADDED to (like
+ * BatchApplyStats accumulation, graph.cpp:198-201). */
+dynpr_status dynpr_graph_apply_batch(dynpr_context* ctx, const dynpr_graph* g,
+                                     const uint32_t* del_src,
+                                     const uint32_t* del_dst, uint64_t n_del,
+                                     const uint32_t* ins_src,
+                                     const uint32_t* ins_dst, uint64_t n_ins,
+                                     dynpr_graph** out, uint64_t* missing,
+                                     uint64_t* duplicate);
+/* Batch ingest for a (forward, transpose) pair: applies the batch to gF and
+ * the reversed batch to gT, so out_gT == transpose(out_gF) byte for byte
+ * without a full re-transpose (replaces harness.cpp:203-204). */
+dynpr_status dynpr_graph_apply_batch_pair(
+    dynpr_context* ctx, const dynpr_graph* gF, const dynpr_graph* gT,
+    const uint32_t* del_src, const uint32_t* del_dst, uint64_t n_del,
+    const uint32_t* ins_src, const uint32_t* ins_dst, uint64_t n_ins,
+    dynpr_graph** out_gF, dynpr_graph** out_gT, uint64_t* missing,
+    uint64_t* duplicate);
+dynpr_status dynpr_graph_info(const dynpr_graph* g, uint32_t* n, uint64_t* m);
+/* Copies offsets (n+1) and targets (m) out (host or device pointers). */
+dynpr_status dynpr_graph_download(dynpr_context* ctx, const dynpr_graph* g,
+                                  uint64_t* offsets, uint32_t* targets);
+dynpr_status dynpr_graph_has_edge(dynpr_context* ctx, const dynpr_graph* g,
+                                  uint32_t source, uint32_t target, int* out);
+dynpr_status dynpr_graph_destroy(dynpr_graph* g);
+/* Synthetic RMAT/Kronecker generator (no reference counterpart):
+ * edge i draws `scale` quadrant choices from SplitMix64(deriveSeed(seed,i))
+ * (rng.hpp:10-47) with probabilities (a, b, c, 1-a-b-c); count =
+ * edge_factor << scale pairs, then buildCsr + addSelfLoops. */
+dynpr_status dynpr_graph_rmat(dynpr_context* ctx, uint32_t scale,
+                              uint32_t edge_factor, double a, double b,
+                              double c, uint64_t seed, dynpr_graph** out);
+
+/* ---- primitives (partition.hpp:20, rank.hpp:66-76, frontier.hpp:28-36) -- */
+/* partitionByDegree: order[n] (low group then high group, ascending ids). */
+dynpr_status dynpr_partition_by_degree(dynpr_context* ctx,
+                                       const dynpr_graph* g,
+                                       uint32_t threshold, uint32_t* order,
+                                       uint32_t* low_count);
+/* updateRanks (rank.cpp:79-140).  vertex_affected / neighbors_pending are
+ * either both NULL (full sweep, no flags) or both n-byte arrays that are
+ * read and updated in place.  previous is read, current written. */
+dynpr_status dynpr_update_ranks(dynpr_context* ctx, const dynpr_graph* gT,
+                                const dynpr_graph* gF,
+                                uint8_t* vertex_affected,
+                                uint8_t* neighbors_pending,
+                                const double* previous, double* current,
+                                const dynpr_config* cfg, int mode);
+/* linfNormDelta / l1NormDelta (rank.cpp:142-152). */
+dynpr_status dynpr_linf_norm_delta(dynpr_context* ctx, const double* a,
+                                   const double* b, uint64_t n, double* out);
+dynpr_status dynpr_l1_norm_delta(dynpr_context* ctx, const double* a,
+                                 const double* b, uint64_t n, double* out);
+/* initialAffected (frontier.cpp:33-53): writes both n-byte flag arrays. */
+dynpr_status dynpr_initial_affected(dynpr_context* ctx, const dynpr_graph* g,
+                                    const uint32_t* del_src,
+                                    const uint32_t* del_dst, uint64_t n_del,
+                                    const uint32_t* ins_src,
+                                    const uint32_t* ins_dst, uint64_t n_ins,
+                                    uint8_t* vertex_affected,
+                                    uint8_t* neighbors_pending);
+/* expandAffected (frontier.cpp:55-84): vertex_affected |= out(pending). */
+dynpr_status dynpr_expand_affected(dynpr_context* ctx, const dynpr_graph* g,
+                                   uint8_t* vertex_affected,
+                                   const uint8_t* neighbors_pending,
+                                   uint32_t threshold);
+
+/* ---- engines (engine.hpp:33-71) ---------------------------------------- */
+/* staticPageRank(gTranspose, gForward, cfg) -- engine.cpp:99-108. */
+dynpr_status dynpr_static_pagerank(dynpr_context* ctx, const dynpr_graph* gT,
+                                   const dynpr_graph* gF,
+                                   const dynpr_config* cfg, double* ranks_out,
+                                   dynpr_stats* stats, dynpr_observer observer,
+                                   void* observer_user);
+/* naiveDynamic(gTranspose, gForward, previousRanks, cfg) -- engine.cpp:110. */
+dynpr_status dynpr_naive_dynamic(dynpr_context* ctx, const dynpr_graph* gT,
+                                 const dynpr_graph* gF, const double* previous,
+                                 uint64_t n_previous, const dynpr_config* cfg,
+                                 double* ranks_out, dynpr_stats* stats,
+                                 dynpr_observer observer, void* observer_user);
+/* dynamicFrontier(gForward, gTranspose, dels, ins, prev, cfg, pruning) --
+ * engine.cpp:192-203.  DF-P when pruning != 0. */
+dynpr_status dynpr_dynamic_frontier(
+    dynpr_context* ctx, const dynpr_graph* gF, const dynpr_graph* gT,
+    const uint32_t* del_src, const uint32_t* del_dst, uint64_t n_del,
+    const uint32_t* ins_src, const uint32_t* ins_dst, uint64_t n_ins,
+    const double* previous, uint64_t n_previous, const dynpr_config* cfg,
+    int pruning, double* ranks_out, dynpr_stats* stats,
+    dynpr_observer observer, void* observer_user);
+/* dynamicFrontierFromFlags -- engine.cpp:178-190. */
+dynpr_status dynpr_dynamic_frontier_from_flags(
+    dynpr_context* ctx, const dynpr_graph* gF, const dynpr_graph* gT,
+    const uint8_t* vertex_affected, const uint8_t* neighbors_pending,
+    uint64_t n_flags, const double* previous, uint64_t n_previous,
+    const dynpr_config* cfg, int pruning, double* ranks_out,
+    dynpr_stats* stats, dynpr_observer observer, void* observer_user);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DYNPR_CUDA_H */

@@ -1,0 +1,488 @@
+"""B200-native Static and DF-P PageRank -- Python mirror of the reference's
+``dynpr`` module (proj/python/dynpr/__init__.py, bindings/module.cpp).
+
+Same names, argument order and meaning, and error behaviour as the
+reference's pybind11 bindings (module.cpp:22-166): invalid arguments raise
+``ValueError`` with the reference's message text.  Every graph is an
+immutable device-resident CSR snapshot (``CsrGraph``); ranks come back as
+numpy float64 arrays.  All compute runs in libdynpr_cuda.so's hand-written
+sm_100a kernels through the C-ABI of include/dynpr_cuda.h; there is no CPU
+fallback -- without the library or a GPU every call raises.
+
+Argument-order note (reference engine.hpp:33-62): ``static_pagerank`` and
+``naive_dynamic`` take ``(g_transpose, g_forward, ...)``; ``dynamic_frontier``
+takes ``(g_forward, g_transpose, ...)``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import weakref
+from dataclasses import dataclass, field
+from typing import Callable, Optional, Sequence
+
+import numpy as np
+
+from . import _native as N
+from ._native import NativeUnavailable
+
+__all__ = [
+    "BatchUpdate", "BatchApplyStats", "Context", "CsrGraph", "DegreePartition", "EngineConfig",
+    "PartitionStrategy", "RankMode", "RankResult", "SizingError", "NativeUnavailable",
+    "add_self_loops", "apply_batch", "apply_batch_pair", "build_csr", "default_context",
+    "dynamic_frontier", "dynamic_frontier_from_flags", "expand_affected", "initial_affected",
+    "l1_norm_delta", "linf_norm_delta", "naive_dynamic", "partition_by_degree", "rmat_graph",
+    "static_pagerank", "transpose", "update_ranks",
+]
+
+
+class SizingError(ValueError):
+    """dynpr::SizingError (workload.hpp:17-19); a ValueError like in module.cpp:165."""
+
+
+class PartitionStrategy(enum.IntEnum):  # rank.hpp:14-18
+    DONT_PARTITION = 0
+    PARTITION_TRANSPOSE = 1
+    PARTITION_BOTH = 2
+
+
+class RankMode(enum.IntEnum):  # rank.hpp:23
+    PLAIN = 0
+    CLOSED_LOOP_PRUNE = 1
+
+
+@dataclass
+class EngineConfig:  # rank.hpp:25-39, defaults
+    damping_factor: float = 0.85
+    iteration_tolerance: float = 1e-10
+    frontier_tolerance: float = 1e-6
+    prune_tolerance: float = 1e-6
+    max_iterations: int = 500
+    low_degree_threshold: int = 32
+    partition_strategy: PartitionStrategy = PartitionStrategy.PARTITION_BOTH
+    convergence_check_disabled: bool = False
+
+    def _c(self) -> N.Config:
+        return N.Config(float(self.damping_factor), float(self.iteration_tolerance),
+                        float(self.frontier_tolerance), float(self.prune_tolerance),
+                        int(self.max_iterations), int(self.low_degree_threshold),
+                        int(self.partition_strategy), int(bool(self.convergence_check_disabled)))
+
+    def validate(self) -> None:
+        """EngineConfig::validate (rank.cpp:11-20); raises ValueError."""
+        c = self._c()
+        _check(N.lib().dynpr_config_validate(C.byref(c)))
+
+
+@dataclass
+class RankResult:  # engine.hpp:16-22
+    ranks: np.ndarray
+    iterations: int
+    affected_vertex_iterations: int
+    converged: bool
+    final_delta: float
+    processed_edges: int = 0
+    device_ms: float = 0.0
+
+
+@dataclass
+class DegreePartition:  # partition.hpp:12-15
+    order: np.ndarray
+    low_count: int
+
+
+@dataclass
+class BatchUpdate:  # graph.hpp:54-57
+    deletions: object = field(default_factory=list)
+    insertions: object = field(default_factory=list)
+
+
+@dataclass
+class BatchApplyStats:  # graph.hpp:61-64
+    missing_deletions: int = 0
+    duplicate_insertions: int = 0
+
+
+def _check(rc: int) -> None:
+    if rc == N.DYNPR_OK:
+        return
+    msg = N.last_error()
+    if rc == N.DYNPR_INVALID_ARGUMENT:
+        raise ValueError(msg)
+    if rc == N.DYNPR_SIZING_ERROR:
+        raise SizingError(msg)
+    if rc == N.DYNPR_OUT_OF_MEMORY:
+        raise MemoryError(msg)
+    raise RuntimeError(msg)
+
+
+class Context:
+    """One CUDA device + stream + workspace (dynpr_context)."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        _check(N.lib().dynpr_context_create(int(device), C.byref(h)))
+        self.h = h.value
+        self.device = device
+        self._fin = weakref.finalize(self, N.lib().dynpr_context_destroy, C.c_void_p(self.h))
+
+    @property
+    def launches(self) -> int:
+        return int(N.lib().dynpr_context_launches(C.c_void_p(self.h)))
+
+    def set_profiling(self, enable: bool) -> None:
+        _check(N.lib().dynpr_context_set_profiling(C.c_void_p(self.h), int(enable)))
+
+    def sweep_times(self):
+        ms, sw, by = C.c_double(), C.c_uint64(), C.c_uint64()
+        _check(N.lib().dynpr_context_sweep_times(C.c_void_p(self.h), C.byref(ms), C.byref(sw), C.byref(by)))
+        return ms.value, sw.value, by.value
+
+
+_default_ctx: Optional[Context] = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(0)
+    return _default_ctx
+
+
+def _ctx(ctx: Optional[Context]) -> Context:
+    return ctx if ctx is not None else default_context()
+
+
+# ---- array plumbing ------------------------------------------------------------
+def _arr(a, dtype) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=dtype).reshape(-1))
+
+
+def _edges(edges):
+    """[(u, v), ...] | (src, dst) arrays | (k, 2) array -> uint32 src, dst."""
+    if isinstance(edges, tuple) and len(edges) == 2 and not np.isscalar(edges[0]) and \
+            isinstance(edges[0], np.ndarray):
+        return _arr(edges[0], np.uint32), _arr(edges[1], np.uint32)
+    if isinstance(edges, np.ndarray):
+        a = edges.reshape(-1, 2)
+    else:
+        lst = list(edges)
+        if not lst:
+            return np.zeros(0, np.uint32), np.zeros(0, np.uint32)
+        a = np.asarray(lst, dtype=np.int64).reshape(-1, 2)
+    if a.size and (a.min() < 0 or a.max() > 0xFFFFFFFF):
+        raise ValueError("vertex id out of uint32 range")
+    return _arr(a[:, 0], np.uint32), _arr(a[:, 1], np.uint32)
+
+
+def _p(a: Optional[np.ndarray]):
+    if a is None or a.size == 0:
+        return None
+    return C.c_void_p(a.ctypes.data)
+
+
+def _is_device_array(x) -> bool:
+    return hasattr(x, "data_ptr") and getattr(x, "is_cuda", False)
+
+
+class CsrGraph:
+    """Immutable device CSR snapshot (graph.hpp:17-49); host arrays are
+    downloaded lazily and cached."""
+
+    def __init__(self, handle: int, ctx: Context):
+        self.h = handle
+        self.ctx = ctx
+        n, m = C.c_uint32(), C.c_uint64()
+        _check(N.lib().dynpr_graph_info(C.c_void_p(handle), C.byref(n), C.byref(m)))
+        self._n, self._m = n.value, m.value
+        self._host = None
+        self._fin = weakref.finalize(self, N.lib().dynpr_graph_destroy, C.c_void_p(handle))
+
+    @classmethod
+    def from_csr(cls, vertex_count: int, offsets, targets, ctx: Optional[Context] = None) -> "CsrGraph":
+        """CsrGraph(vertexCount, offsets, targets) with full validation."""
+        ctx = _ctx(ctx)
+        off = _arr(offsets, np.uint64)
+        tgt = _arr(targets, np.uint32)
+        if len(off) != int(vertex_count) + 1:
+            raise ValueError("CsrGraph: malformed offsets array")
+        h = C.c_void_p()
+        _check(N.lib().dynpr_graph_from_csr(C.c_void_p(ctx.h), int(vertex_count), _p(off), _p(tgt),
+                                            len(tgt), C.byref(h)))
+        return cls(h.value, ctx)
+
+    @property
+    def vertex_count(self) -> int:
+        return self._n
+
+    @property
+    def edge_count(self) -> int:
+        return self._m
+
+    def _download(self):
+        if self._host is None:
+            off = np.zeros(self._n + 1, np.uint64)
+            tgt = np.zeros(max(self._m, 1), np.uint32)
+            _check(N.lib().dynpr_graph_download(C.c_void_p(self.ctx.h), C.c_void_p(self.h),
+                                                _p(off), _p(tgt)))
+            self._host = (off, tgt[: self._m])
+        return self._host
+
+    @property
+    def offsets(self) -> np.ndarray:
+        return self._download()[0]
+
+    @property
+    def targets(self) -> np.ndarray:
+        return self._download()[1]
+
+    def degree(self, v: int) -> int:
+        off = self.offsets
+        return int(off[v + 1] - off[v])
+
+    def degrees(self) -> np.ndarray:
+        return np.diff(self.offsets).astype(np.uint32)
+
+    def out(self, v: int) -> list:
+        off, tgt = self._download()
+        return tgt[int(off[v]):int(off[v + 1])].tolist()
+
+    def has_edge(self, source: int, target: int) -> bool:
+        out = C.c_int()
+        _check(N.lib().dynpr_graph_has_edge(C.c_void_p(self.ctx.h), C.c_void_p(self.h), int(source),
+                                            int(target), C.byref(out)))
+        return bool(out.value)
+
+    def has_self_loop(self, v: int) -> bool:
+        return self.has_edge(v, v)
+
+    def __eq__(self, other) -> bool:  # bytewise (graph.hpp:43)
+        if not isinstance(other, CsrGraph):
+            return NotImplemented
+        if self._n != other._n or self._m != other._m:
+            return False
+        return bool(np.array_equal(self.offsets, other.offsets) and np.array_equal(self.targets, other.targets))
+
+    def __repr__(self) -> str:
+        return f"<CsrGraph |V|={self._n} |E|={self._m}>"
+
+
+def _new_graph(fn, ctx: Context, *args) -> CsrGraph:
+    h = C.c_void_p()
+    _check(fn(C.c_void_p(ctx.h), *args, C.byref(h)))
+    return CsrGraph(h.value, ctx)
+
+
+# ---- graph construction (graph.hpp:66-80) -------------------------------------
+def build_csr(edges, vertex_count: int, ctx: Optional[Context] = None) -> CsrGraph:
+    ctx = _ctx(ctx)
+    s, d = _edges(edges)
+    return _new_graph(N.lib().dynpr_graph_build, ctx, int(vertex_count), _p(s), _p(d), len(s))
+
+
+def transpose(g: CsrGraph) -> CsrGraph:
+    return _new_graph(N.lib().dynpr_graph_transpose, g.ctx, C.c_void_p(g.h))
+
+
+def add_self_loops(g: CsrGraph) -> CsrGraph:
+    return _new_graph(N.lib().dynpr_graph_add_self_loops, g.ctx, C.c_void_p(g.h))
+
+
+def _batch_arrays(batch: BatchUpdate):
+    ds, dd = _edges(batch.deletions)
+    is_, id_ = _edges(batch.insertions)
+    return ds, dd, is_, id_
+
+
+def apply_batch(g: CsrGraph, batch: BatchUpdate, stats: Optional[BatchApplyStats] = None) -> CsrGraph:
+    ds, dd, is_, id_ = _batch_arrays(batch)
+    miss, dup = C.c_uint64(0), C.c_uint64(0)
+    h = C.c_void_p()
+    _check(N.lib().dynpr_graph_apply_batch(C.c_void_p(g.ctx.h), C.c_void_p(g.h), _p(ds), _p(dd), len(ds),
+                                           _p(is_), _p(id_), len(is_), C.byref(h), C.byref(miss), C.byref(dup)))
+    if stats is not None:
+        stats.missing_deletions += miss.value
+        stats.duplicate_insertions += dup.value
+    return CsrGraph(h.value, g.ctx)
+
+
+def apply_batch_pair(g: CsrGraph, gt: CsrGraph, batch: BatchUpdate,
+                     stats: Optional[BatchApplyStats] = None):
+    """Device batch ingest of a (forward, transpose) pair: returns
+    (applyBatch(g), transpose(applyBatch(g))) without a re-transpose."""
+    ds, dd, is_, id_ = _batch_arrays(batch)
+    miss, dup = C.c_uint64(0), C.c_uint64(0)
+    hf, ht = C.c_void_p(), C.c_void_p()
+    _check(N.lib().dynpr_graph_apply_batch_pair(C.c_void_p(g.ctx.h), C.c_void_p(g.h), C.c_void_p(gt.h),
+                                                _p(ds), _p(dd), len(ds), _p(is_), _p(id_), len(is_),
+                                                C.byref(hf), C.byref(ht), C.byref(miss), C.byref(dup)))
+    if stats is not None:
+        stats.missing_deletions += miss.value
+        stats.duplicate_insertions += dup.value
+    return CsrGraph(hf.value, g.ctx), CsrGraph(ht.value, g.ctx)
+
+
+def rmat_graph(scale: int, edge_factor: int = 16, a: float = 0.57, b: float = 0.19, c: float = 0.19,
+               seed: int = 42, ctx: Optional[Context] = None) -> CsrGraph:
+    """Self-loop-augmented RMAT/Kronecker graph generated on the device
+    (Graph500 parameters; counter-based SplitMix64 seeding)."""
+    ctx = _ctx(ctx)
+    return _new_graph(N.lib().dynpr_graph_rmat, ctx, int(scale), int(edge_factor), float(a), float(b),
+                      float(c), int(seed))
+
+
+# ---- primitives ------------------------------------------------------------------
+def partition_by_degree(g: CsrGraph, threshold: int) -> DegreePartition:
+    order = np.zeros(max(g.vertex_count, 1), np.uint32)
+    low = C.c_uint32()
+    _check(N.lib().dynpr_partition_by_degree(C.c_void_p(g.ctx.h), C.c_void_p(g.h), int(threshold),
+                                             _p(order), C.byref(low)))
+    return DegreePartition(order[: g.vertex_count], low.value)
+
+
+def update_ranks(gt: CsrGraph, g: CsrGraph, previous, current=None, vertex_affected=None,
+                 neighbors_pending=None, config: Optional[EngineConfig] = None,
+                 mode: RankMode = RankMode.PLAIN):
+    """One sweep of updateRanks (rank.cpp:79-140).  Returns
+    (current, vertex_affected, neighbors_pending) (flags None when not given)."""
+    cfg = (config or EngineConfig())._c()
+    n = gt.vertex_count
+    prev = _arr(previous, np.float64)
+    cur = np.array(prev if current is None else _arr(current, np.float64), dtype=np.float64)
+    va = np_ = None
+    if vertex_affected is not None:
+        va = _arr(vertex_affected, np.uint8).copy()
+        np_ = _arr(neighbors_pending if neighbors_pending is not None else np.zeros(n, np.uint8),
+                   np.uint8).copy()
+    if len(prev) != n:
+        raise ValueError("updateRanks: previous length mismatch")
+    _check(N.lib().dynpr_update_ranks(C.c_void_p(gt.ctx.h), C.c_void_p(gt.h), C.c_void_p(g.h), _p(va), _p(np_),
+                                      _p(prev), _p(cur), C.byref(cfg), int(mode)))
+    return cur, va, np_
+
+
+def linf_norm_delta(a, b, ctx: Optional[Context] = None) -> float:
+    a, b = _arr(a, np.float64), _arr(b, np.float64)
+    if len(a) != len(b):
+        raise ValueError("linfNormDelta: length mismatch")
+    out = C.c_double()
+    _check(N.lib().dynpr_linf_norm_delta(C.c_void_p(_ctx(ctx).h), _p(a), _p(b), len(a), C.byref(out)))
+    return out.value
+
+
+def l1_norm_delta(a, b, ctx: Optional[Context] = None) -> float:
+    a, b = _arr(a, np.float64), _arr(b, np.float64)
+    if len(a) != len(b):
+        raise ValueError("l1NormDelta: length mismatch")
+    out = C.c_double()
+    _check(N.lib().dynpr_l1_norm_delta(C.c_void_p(_ctx(ctx).h), _p(a), _p(b), len(a), C.byref(out)))
+    return out.value
+
+
+def initial_affected(g: CsrGraph, deletions, insertions):
+    """initialAffected (frontier.cpp:33-53) -> (vertex_affected, neighbors_pending)."""
+    ds, dd = _edges(deletions)
+    is_, id_ = _edges(insertions)
+    n = g.vertex_count
+    va = np.zeros(max(n, 1), np.uint8)
+    np_ = np.zeros(max(n, 1), np.uint8)
+    _check(N.lib().dynpr_initial_affected(C.c_void_p(g.ctx.h), C.c_void_p(g.h), _p(ds), _p(dd), len(ds),
+                                          _p(is_), _p(id_), len(is_), _p(va), _p(np_)))
+    return va[:n], np_[:n]
+
+
+def expand_affected(g: CsrGraph, vertex_affected, neighbors_pending, threshold: int = 32) -> np.ndarray:
+    """expandAffected (frontier.cpp:55-84): returns the expanded vertexAffected."""
+    va = _arr(vertex_affected, np.uint8).copy()
+    np_ = _arr(neighbors_pending, np.uint8)
+    if len(va) != g.vertex_count or len(np_) != g.vertex_count:
+        raise ValueError("expandAffected: flags length mismatch")
+    _check(N.lib().dynpr_expand_affected(C.c_void_p(g.ctx.h), C.c_void_p(g.h), _p(va), _p(np_),
+                                         int(threshold)))
+    return va
+
+
+# ---- engines (engine.hpp:33-71) --------------------------------------------------
+def _observer(cb: Optional[Callable]):
+    if cb is None:
+        return N.OBSERVER(0), None
+
+    def obs(it, ranks, processed, n, user):
+        r = np.ctypeslib.as_array(ranks, shape=(n,)).copy()
+        if processed:
+            cb(it, r, np.ctypeslib.as_array(processed, shape=(n,)).copy())
+        else:
+            cb(it, r)
+
+    fn = N.OBSERVER(obs)
+    return fn, fn
+
+
+def _result(ranks: np.ndarray, st: N.Stats) -> RankResult:
+    return RankResult(ranks, st.iterations, st.affected_vertex_iterations, bool(st.converged),
+                      st.final_delta, st.processed_edges, st.device_ms)
+
+
+def static_pagerank(g_transpose: CsrGraph, g_forward: CsrGraph, config: Optional[EngineConfig] = None,
+                    observer: Optional[Callable] = None) -> RankResult:
+    """staticPageRank(gTranspose, gForward, cfg) -- engine.cpp:99-108."""
+    cfg = (config or EngineConfig())._c()
+    ranks = np.zeros(max(g_transpose.vertex_count, 1), np.float64)
+    st = N.Stats()
+    obs, keep = _observer(observer)
+    _check(N.lib().dynpr_static_pagerank(C.c_void_p(g_transpose.ctx.h), C.c_void_p(g_transpose.h),
+                                         C.c_void_p(g_forward.h), C.byref(cfg), _p(ranks), C.byref(st), obs,
+                                         None))
+    return _result(ranks[: g_transpose.vertex_count], st)
+
+
+def naive_dynamic(g_transpose: CsrGraph, g_forward: CsrGraph, previous_ranks,
+                  config: Optional[EngineConfig] = None, observer: Optional[Callable] = None) -> RankResult:
+    """naiveDynamic(gTranspose, gForward, previousRanks, cfg) -- engine.cpp:110-122."""
+    cfg = (config or EngineConfig())._c()
+    prev = _arr(previous_ranks, np.float64)
+    ranks = np.zeros(max(g_transpose.vertex_count, 1), np.float64)
+    st = N.Stats()
+    obs, keep = _observer(observer)
+    _check(N.lib().dynpr_naive_dynamic(C.c_void_p(g_transpose.ctx.h), C.c_void_p(g_transpose.h),
+                                       C.c_void_p(g_forward.h), _p(prev), len(prev), C.byref(cfg), _p(ranks),
+                                       C.byref(st), obs, None))
+    return _result(ranks[: g_transpose.vertex_count], st)
+
+
+def dynamic_frontier(g_forward: CsrGraph, g_transpose: CsrGraph, deletions, insertions, previous_ranks,
+                     config: Optional[EngineConfig] = None, pruning: bool = False,
+                     observer: Optional[Callable] = None) -> RankResult:
+    """dynamicFrontier(gForward, gTranspose, dels, ins, prev, cfg, pruning) --
+    engine.cpp:192-203 (DF-P with pruning=True).  The observer, when given,
+    receives (iteration, ranks, processed_flags)."""
+    cfg = (config or EngineConfig())._c()
+    ds, dd = _edges(deletions)
+    is_, id_ = _edges(insertions)
+    prev = _arr(previous_ranks, np.float64)
+    ranks = np.zeros(max(g_transpose.vertex_count, 1), np.float64)
+    st = N.Stats()
+    obs, keep = _observer(observer)
+    _check(N.lib().dynpr_dynamic_frontier(C.c_void_p(g_forward.ctx.h), C.c_void_p(g_forward.h),
+                                          C.c_void_p(g_transpose.h), _p(ds), _p(dd), len(ds), _p(is_), _p(id_),
+                                          len(is_), _p(prev), len(prev), C.byref(cfg), int(bool(pruning)),
+                                          _p(ranks), C.byref(st), obs, None))
+    return _result(ranks[: g_transpose.vertex_count], st)
+
+
+def dynamic_frontier_from_flags(g_forward: CsrGraph, g_transpose: CsrGraph, vertex_affected,
+                                neighbors_pending, previous_ranks, config: Optional[EngineConfig] = None,
+                                pruning: bool = False, observer: Optional[Callable] = None) -> RankResult:
+    """dynamicFrontierFromFlags -- engine.cpp:178-190."""
+    cfg = (config or EngineConfig())._c()
+    va = _arr(vertex_affected, np.uint8)
+    np_ = _arr(neighbors_pending, np.uint8)
+    prev = _arr(previous_ranks, np.float64)
+    ranks = np.zeros(max(g_transpose.vertex_count, 1), np.float64)
+    st = N.Stats()
+    obs, keep = _observer(observer)
+    _check(N.lib().dynpr_dynamic_frontier_from_flags(C.c_void_p(g_forward.ctx.h), C.c_void_p(g_forward.h),
+                                                     C.c_void_p(g_transpose.h), _p(va), _p(np_), len(va),
+                                                     _p(prev), len(prev), C.byref(cfg), int(bool(pruning)),
+                                                     _p(ranks), C.byref(st), obs, None))
+    return _result(ranks[: g_transpose.vertex_count], st)

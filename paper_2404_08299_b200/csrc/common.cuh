@@ -1,0 +1,227 @@
+// Shared host/device plumbing of libdynpr_cuda.so: error model, context,
+// grow-only device workspace, host<->device argument staging.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "dynpr_cuda.h"
+
+namespace dynpr_b200 {
+
+// ---- error model -----------------------------------------------------------
+// Internal code throws; every extern "C" entry point converts to a status and
+// stores the message for dynpr_last_error().
+struct Error : std::runtime_error {
+  dynpr_status code;
+  Error(dynpr_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] inline void invalid(const std::string& m) {
+  throw Error(DYNPR_INVALID_ARGUMENT, m);
+}
+
+void set_last_error(const std::string& m);
+
+#define DYNPR_CK(call)                                                        \
+  do {                                                                        \
+    cudaError_t e__ = (call);                                                 \
+    if (e__ != cudaSuccess) {                                                 \
+      throw ::dynpr_b200::Error(                                              \
+          e__ == cudaErrorMemoryAllocation ? DYNPR_OUT_OF_MEMORY              \
+                                           : DYNPR_CUDA_ERROR,                \
+          std::string(#call) + ": " + cudaGetErrorString(e__));               \
+    }                                                                         \
+  } while (0)
+
+template <class F>
+dynpr_status api_guard(F&& f) {
+  try {
+    f();
+    return DYNPR_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_last_error("host allocation failed");
+    return DYNPR_OUT_OF_MEMORY;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return DYNPR_CUDA_ERROR;
+  }
+}
+
+// ---- device buffers ----------------------------------------------------------
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  void* ensure(size_t bytes) {
+    if (bytes <= cap && p) return p;
+    if (p) DYNPR_CK(cudaFree(p));
+    p = nullptr;
+    cap = 0;
+    size_t want = bytes < 256 ? 256 : bytes;
+    DYNPR_CK(cudaMalloc(&p, want));
+    cap = want;
+    return p;
+  }
+  template <class T>
+  T* as(size_t count) {
+    return static_cast<T*>(ensure(count * sizeof(T)));
+  }
+};
+
+// Per-solve reduction slot (device), read back once per sweep.
+struct SweepRed {
+  unsigned long long delta_bits;  // max |r - prev| as IEEE bits (>= 0)
+  unsigned long long processed;   // vertices processed (affected count)
+  unsigned long long edges;       // in-edges gathered
+  unsigned int pend_low;          // pending vertices with out-degree <= T
+  unsigned int pend_high;         // pending vertices with out-degree  > T
+};
+
+}  // namespace dynpr_b200
+
+struct dynpr_context {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  uint64_t launches = 0;
+  // profiling of rank sweeps
+  bool profiling = false;
+  double sweep_ms = 0.0;
+  uint64_t sweeps = 0;
+  uint64_t sweep_bytes = 0;
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_s0 = nullptr, ev_s1 = nullptr;
+  // pinned host scratch for small readbacks
+  void* pinned = nullptr;
+  // workspace (grow-only; the engines never allocate inside the timed loop)
+  dynpr_b200::DevBuf rank[2], contrib[2], flags_va, flags_np, flags_written,
+      pend_low, pend_high, sched_high, sched_chunks, sched_multi, partials,
+      tile_counts, red, stage_a, stage_b, stage_c, stage_d, stage_e, stage_f,
+      cub_tmp, scratch64a, scratch64b, scratch32a, scratch32b, scratch8a, batch[4];
+};
+
+struct dynpr_graph {
+  dynpr_context* ctx = nullptr;
+  uint32_t n = 0;
+  uint64_t m = 0;
+  uint64_t* off = nullptr;  // n+1, device
+  uint32_t* tgt = nullptr;  // m, device
+  bool all_loops = false;   // every vertex known to carry its self-loop
+};
+
+namespace dynpr_b200 {
+
+constexpr int kWarp = 32;
+
+inline unsigned grid_for(uint64_t items, unsigned per_block,
+                         unsigned cap = 1u << 30) {
+  uint64_t g = (items + per_block - 1) / per_block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return static_cast<unsigned>(g);
+}
+
+inline void count_launch(dynpr_context* ctx, uint64_t k = 1) {
+  ctx->launches += k;
+}
+inline void check_launch() { DYNPR_CK(cudaGetLastError()); }
+
+// ---- host/device argument staging ---------------------------------------------
+bool is_device_ptr(const void* p);
+
+// Makes `count` elements of a caller array available on the device.
+template <class T>
+const T* stage_in(dynpr_context* ctx, DevBuf& buf, const T* p, uint64_t count) {
+  if (count == 0) return static_cast<const T*>(buf.ensure(sizeof(T)));
+  if (p == nullptr) invalid("null array argument");
+  if (is_device_ptr(p)) return p;
+  T* d = buf.as<T>(count);
+  DYNPR_CK(cudaMemcpyAsync(d, p, count * sizeof(T), cudaMemcpyHostToDevice,
+                           ctx->stream));
+  return d;
+}
+
+// Output staging: returns a device pointer to write; commit() copies back.
+template <class T>
+struct StageOut {
+  dynpr_context* ctx;
+  T* user;
+  T* dev;
+  uint64_t count;
+  bool host;
+  StageOut(dynpr_context* c, DevBuf& buf, T* p, uint64_t n)
+      : ctx(c), user(p), count(n) {
+    if (n && p == nullptr) invalid("null output array");
+    host = n && !is_device_ptr(p);
+    dev = host ? buf.as<T>(n) : p;
+  }
+  void commit() {
+    if (host && count)
+      DYNPR_CK(cudaMemcpyAsync(user, dev, count * sizeof(T),
+                               cudaMemcpyDeviceToHost, ctx->stream));
+    DYNPR_CK(cudaStreamSynchronize(ctx->stream));
+  }
+};
+
+inline void sync(dynpr_context* ctx) {
+  DYNPR_CK(cudaStreamSynchronize(ctx->stream));
+}
+
+inline void bind_device(dynpr_context* ctx) { DYNPR_CK(cudaSetDevice(ctx->device)); }
+
+// ---- device helpers ------------------------------------------------------------
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+template <class T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Binary search: first index in [lo, hi) with a[i] >= key.
+template <class T, class I>
+__device__ __forceinline__ I lower_bound_dev(const T* a, I lo, I hi, T key) {
+  while (lo < hi) {
+    I mid = lo + (hi - lo) / 2;
+    if (a[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// Number of bits needed to represent x (0 -> 0).
+inline int bits_for(uint64_t x) {
+  int b = 0;
+  while (x) { ++b; x >>= 1; }
+  return b;
+}
+
+// ---- shared internals used across translation units ------------------------
+// graph.cu
+dynpr_graph* make_graph(dynpr_context* ctx, uint32_t n, uint64_t m);
+void destroy_graph(dynpr_graph* g);
+void graph_apply_batch_impl(dynpr_context* ctx, const dynpr_graph* g,
+                            const uint32_t* d_ds, const uint32_t* d_dd,
+                            uint64_t nd, const uint32_t* d_is,
+                            const uint32_t* d_id, uint64_t ni, bool validate,
+                            const uint32_t* h_ds, const uint32_t* h_dd,
+                            const uint32_t* h_is, const uint32_t* h_id,
+                            dynpr_graph** out, uint64_t* missing,
+                            uint64_t* duplicate);
+
+}  // namespace dynpr_b200

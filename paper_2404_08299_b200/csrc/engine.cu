@@ -1,0 +1,560 @@
+// Engines and the extern "C" boundary of libdynpr_cuda.so.
+//
+//   staticPageRank            engine.cpp:99-108   -> dynpr_static_pagerank
+//   naiveDynamic              engine.cpp:110-122  -> dynpr_naive_dynamic
+//   dynamicFrontier           engine.cpp:192-203  -> dynpr_dynamic_frontier
+//   dynamicFrontierFromFlags  engine.cpp:178-190  -> dynpr_dynamic_frontier_from_flags
+//   convergeLoop              engine.cpp:61-95    -> solve() below
+//   updateRanks / linfNormDelta / l1NormDelta     rank.cpp:79-152
+//   initialAffected / expandAffected              frontier.cpp:33-84
+//   partitionByDegree                             partition.cpp:7-61
+//   EngineConfig::validate                        rank.cpp:11-20
+//
+// The host loop mirrors convergeLoop's order exactly (count -> clear pending
+// -> update -> L-inf -> swap -> record -> observer -> convergence test ->
+// expand); the count, the pending clear and the L-inf are fused into the
+// sweep kernels, and the only per-iteration host traffic is one 32-byte
+// readback (delta, processed, edges, pending-list sizes).
+#include <algorithm>
+#include <cmath>
+#include <string>
+
+#include "sweep.cuh"
+
+namespace dynpr_b200 {
+
+thread_local std::string g_last_error;
+void set_last_error(const std::string& m) { g_last_error = m; }
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes attr;
+  if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
+}
+
+bool any_bad_ids(dynpr_context* ctx, const uint32_t* d_s, const uint32_t* d_d, uint64_t cnt, uint32_t n);
+
+namespace {
+
+void validate_config(const dynpr_config* c) {  // rank.cpp:11-20
+  if (!c) invalid("null config");
+  if (!(c->damping_factor > 0.0 && c->damping_factor < 1.0))
+    invalid("EngineConfig: dampingFactor must be in (0,1)");
+  if (!(c->iteration_tolerance > 0.0)) invalid("EngineConfig: iterationTolerance must be > 0");
+  if (c->frontier_tolerance < 0.0 || c->prune_tolerance < 0.0)
+    invalid("EngineConfig: tolerances must be >= 0");
+  if (c->max_iterations <= 0) invalid("EngineConfig: maxIterations must be positive");
+}
+
+void check_pair(const dynpr_graph* gT, const dynpr_graph* gF) {  // engine.cpp:15-23
+  if (!gT || !gF) invalid("null graph");
+  if (gT->n != gF->n || gT->m != gF->m)
+    invalid("engine: graph pair is not mutually transposed (count mismatch)");
+  if (gT->n == 0) invalid("engine: empty graph");
+}
+
+double bits_to_double(unsigned long long b) {
+  double d;
+  std::memcpy(&d, &b, 8);
+  return d;
+}
+
+SweepRed read_red(dynpr_context* ctx, const SweepRed* d) {
+  DYNPR_CK(cudaMemcpyAsync(ctx->pinned, d, sizeof(SweepRed), cudaMemcpyDeviceToHost, ctx->stream));
+  sync(ctx);
+  SweepRed h;
+  std::memcpy(&h, ctx->pinned, sizeof h);
+  return h;
+}
+
+struct SolveSpec {
+  const dynpr_graph* gT = nullptr;
+  const dynpr_graph* gF = nullptr;
+  const dynpr_config* cfg = nullptr;
+  const double* prev = nullptr;  // device, or null for the uniform start
+  bool flagged = false;          // DF / DF-P frontier loop
+  bool closed = false;           // ClosedLoopPrune formula (DF-P)
+  // frontier seeds: batch (device arrays) or explicit flags (device)
+  const uint32_t* ds = nullptr;
+  const uint32_t* dd = nullptr;
+  uint64_t nd = 0;
+  const uint32_t* is = nullptr;
+  uint64_t ni = 0;
+  const uint8_t* flags_in = nullptr;
+};
+
+// convergeLoop (engine.cpp:61-95) on the device.
+void solve(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynpr_stats* stats,
+           dynpr_observer obs, void* user) {
+  const dynpr_graph* gT = sp.gT;
+  const dynpr_graph* gF = sp.gF;
+  const dynpr_config& c = *sp.cfg;
+  const uint32_t n = gT->n;
+  cudaStream_t st = ctx->stream;
+  // workspace (allocation is excluded from the timed region)
+  double* R[2] = {ctx->rank[0].as<double>(n), ctx->rank[1].as<double>(n)};
+  double* CB[2] = {ctx->contrib[0].as<double>(n), ctx->contrib[1].as<double>(n)};
+  SweepRed* red = ctx->red.as<SweepRed>(2);
+  uint8_t* va = nullptr;
+  uint8_t* written = nullptr;
+  uint32_t *pl = nullptr, *ph = nullptr;
+  if (sp.flagged) {
+    const uint64_t cap = std::max<uint64_t>(n, sp.nd + sp.ni) + 1;
+    va = ctx->flags_va.as<uint8_t>(n);
+    written = ctx->flags_written.as<uint8_t>(n);
+    pl = ctx->pend_low.as<uint32_t>(cap);
+    ph = ctx->pend_high.as<uint32_t>(cap);
+  }
+  std::vector<double> h_ranks;
+  std::vector<uint8_t> h_flags;
+  if (obs) {
+    h_ranks.resize(n);
+    if (sp.flagged) h_flags.resize(n);
+  }
+
+  DYNPR_CK(cudaEventRecord(ctx->ev_a, st));
+  // makePartitions (engine.cpp:40-56): the in-degree schedule.  The
+  // out-degree split of PartitionBoth is applied on the fly when pending
+  // vertices are appended to the low/high expansion lists.
+  const Schedule s = build_schedule(ctx, gT, c.low_degree_threshold, nullptr, true);
+  // initRanksUniform / initRanksFrom (rank.cpp:22-37) + contributions
+  launch_init_ranks(ctx, gF, sp.prev, 1.0 / (double)n, R[0], R[1], CB[0], CB[1]);
+  if (sp.flagged) {
+    DYNPR_CK(cudaMemsetAsync(written, 0, n, st));
+    if (sp.flags_in) {
+      DYNPR_CK(cudaMemcpyAsync(va, sp.flags_in, n, cudaMemcpyDeviceToDevice, st));
+    } else {
+      // initialAffected + the one expandAffected before the loop
+      // (engine.cpp:199-200)
+      DYNPR_CK(cudaMemsetAsync(va, 0, n, st));
+      DYNPR_CK(cudaMemsetAsync(red + 1, 0, sizeof(SweepRed), st));
+      launch_init_affected(ctx, gF, sp.ds, sp.dd, sp.nd, sp.is, sp.ni, va, nullptr, c.low_degree_threshold, pl,
+                           ph, red + 1);
+      const SweepRed r0 = read_red(ctx, red + 1);
+      launch_expand(ctx, gF, va, pl, r0.pend_low, ph, r0.pend_high);
+    }
+  }
+
+  SweepArgs a{};
+  a.offT = gT->off;
+  a.idxT = gT->tgt;
+  a.offF = gF->off;
+  a.n = n;
+  a.T = c.low_degree_threshold;
+  a.alpha = c.damping_factor;
+  a.teleport = (1.0 - c.damping_factor) / (double)n;  // rank.cpp:85
+  a.tf = c.frontier_tolerance;
+  a.tp = c.prune_tolerance;
+  a.va = va;
+  a.np = nullptr;
+  a.written = written;
+  a.pend_low = pl;
+  a.pend_high = ph;
+  a.red = red;
+  a.chunks = s.chunks;
+  a.n_chunks = s.n_chunks;
+  a.multi = s.multi;
+  a.n_multi = s.n_multi;
+  a.partials = s.partials;
+
+  dynpr_stats res{};
+  int cur = 0;  // R[cur] holds the latest iterate ("previous")
+  for (int iter = 0; iter < c.max_iterations; ++iter) {
+    DYNPR_CK(cudaMemsetAsync(red, 0, sizeof(SweepRed), st));
+    if (obs && sp.flagged) {
+      DYNPR_CK(cudaMemcpyAsync(h_flags.data(), va, n, cudaMemcpyDeviceToHost, st));
+    }
+    a.rank_prev = R[cur];
+    a.rank_cur = R[cur ^ 1];
+    a.contrib_prev = CB[cur];
+    a.contrib_cur = CB[cur ^ 1];
+    if (ctx->profiling) DYNPR_CK(cudaEventRecord(ctx->ev_s0, st));
+    launch_sweep(ctx, a, sp.flagged, sp.closed, s.n_low);
+    if (ctx->profiling) DYNPR_CK(cudaEventRecord(ctx->ev_s1, st));
+    const SweepRed r = read_red(ctx, red);
+    if (ctx->profiling) {
+      float ms = 0.f;
+      DYNPR_CK(cudaEventElapsedTime(&ms, ctx->ev_s0, ctx->ev_s1));
+      ctx->sweep_ms += ms;
+      ctx->sweeps += 1;
+      // algorithmic bytes of the sweep: 4 B per gathered in-edge
+      // id + 28 B per processed vertex (8 offset, 4 out-degree, 8 R_prev,
+      // 8 R_new) [+ 1 B flag read per vertex in frontier mode]
+      ctx->sweep_bytes += 4ull * r.edges + 28ull * r.processed + 8ull + (sp.flagged ? (uint64_t)n : 0ull);
+    }
+    const double delta = bits_to_double(r.delta_bits);
+    cur ^= 1;  // swap (engine.cpp:80)
+    res.iterations = iter + 1;
+    res.affected_vertex_iterations += sp.flagged ? r.processed : (uint64_t)n;
+    res.processed_edges += r.edges;
+    res.final_delta = delta;
+    if (obs) {
+      DYNPR_CK(cudaMemcpyAsync(h_ranks.data(), R[cur], (size_t)n * 8, cudaMemcpyDeviceToHost, st));
+      sync(ctx);
+      obs(res.iterations, h_ranks.data(), sp.flagged ? h_flags.data() : nullptr, n, user);
+    }
+    if (!c.convergence_check_disabled && delta <= c.iteration_tolerance) {
+      res.converged = 1;
+      break;
+    }
+    if (sp.flagged) launch_expand(ctx, gF, va, pl, r.pend_low, ph, r.pend_high);  // engine.cpp:91
+  }
+  DYNPR_CK(cudaEventRecord(ctx->ev_b, st));
+  DYNPR_CK(cudaMemcpyAsync(ranks_out, R[cur], (size_t)n * 8, cudaMemcpyDefault, st));
+  sync(ctx);
+  float ms = 0.f;
+  DYNPR_CK(cudaEventElapsedTime(&ms, ctx->ev_a, ctx->ev_b));
+  res.device_ms = ms;
+  if (stats) *stats = res;
+}
+
+}  // namespace
+}  // namespace dynpr_b200
+
+using namespace dynpr_b200;
+
+extern "C" {
+
+const char* dynpr_last_error(void) { return g_last_error.c_str(); }
+const char* dynpr_version(void) { return "dynpr_b200 0.1 (sm_100a)"; }
+
+void dynpr_config_default(dynpr_config* c) {
+  if (!c) return;
+  c->damping_factor = 0.85;
+  c->iteration_tolerance = 1e-10;
+  c->frontier_tolerance = 1e-6;
+  c->prune_tolerance = 1e-6;
+  c->max_iterations = 500;
+  c->low_degree_threshold = 32;
+  c->partition_strategy = DYNPR_PARTITION_BOTH;
+  c->convergence_check_disabled = 0;
+}
+
+dynpr_status dynpr_config_validate(const dynpr_config* c) {
+  return api_guard([&] { validate_config(c); });
+}
+
+dynpr_status dynpr_context_create(int device, dynpr_context** out) {
+  return api_guard([&] {
+    if (!out) invalid("null argument");
+    int count = 0;
+    DYNPR_CK(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count) invalid("dynpr_context_create: no such CUDA device");
+    DYNPR_CK(cudaSetDevice(device));
+    auto* ctx = new dynpr_context();
+    ctx->device = device;
+    try {
+      DYNPR_CK(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
+      DYNPR_CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+      DYNPR_CK(cudaEventCreate(&ctx->ev_a));
+      DYNPR_CK(cudaEventCreate(&ctx->ev_b));
+      DYNPR_CK(cudaEventCreate(&ctx->ev_s0));
+      DYNPR_CK(cudaEventCreate(&ctx->ev_s1));
+      DYNPR_CK(cudaMallocHost(&ctx->pinned, 4096));
+    } catch (...) {
+      dynpr_context_destroy(ctx);
+      throw;
+    }
+    *out = ctx;
+  });
+}
+
+dynpr_status dynpr_context_destroy(dynpr_context* ctx) {
+  return api_guard([&] {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    if (ctx->ev_a) cudaEventDestroy(ctx->ev_a);
+    if (ctx->ev_b) cudaEventDestroy(ctx->ev_b);
+    if (ctx->ev_s0) cudaEventDestroy(ctx->ev_s0);
+    if (ctx->ev_s1) cudaEventDestroy(ctx->ev_s1);
+    if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+  });
+}
+
+uint64_t dynpr_context_launches(const dynpr_context* ctx) { return ctx ? ctx->launches : 0; }
+
+dynpr_status dynpr_context_set_profiling(dynpr_context* ctx, int enable) {
+  return api_guard([&] {
+    if (!ctx) invalid("null context");
+    ctx->profiling = enable != 0;
+    ctx->sweep_ms = 0.0;
+    ctx->sweeps = 0;
+    ctx->sweep_bytes = 0;
+  });
+}
+
+dynpr_status dynpr_context_sweep_times(dynpr_context* ctx, double* total_ms, uint64_t* sweeps, uint64_t* bytes) {
+  return api_guard([&] {
+    if (!ctx) invalid("null context");
+    if (total_ms) *total_ms = ctx->sweep_ms;
+    if (sweeps) *sweeps = ctx->sweeps;
+    if (bytes) *bytes = ctx->sweep_bytes;
+  });
+}
+
+// ---- primitives ---------------------------------------------------------------
+dynpr_status dynpr_partition_by_degree(dynpr_context* ctx, const dynpr_graph* g, uint32_t threshold,
+                                       uint32_t* order, uint32_t* low_count) {
+  return api_guard([&] {
+    if (!ctx || !g || !low_count) invalid("null argument");
+    bind_device(ctx);
+    StageOut<uint32_t> o(ctx, ctx->stage_a, order, g->n);
+    Schedule s = build_schedule(ctx, g, threshold, g->n ? o.dev : nullptr, false);
+    o.commit();
+    *low_count = s.n_low;
+  });
+}
+
+dynpr_status dynpr_update_ranks(dynpr_context* ctx, const dynpr_graph* gT, const dynpr_graph* gF,
+                                uint8_t* vertex_affected, uint8_t* neighbors_pending, const double* previous,
+                                double* current, const dynpr_config* cfg, int mode) {
+  return api_guard([&] {
+    if (!ctx || !gT || !gF || !cfg) invalid("null argument");
+    if ((vertex_affected == nullptr) != (neighbors_pending == nullptr))
+      invalid("updateRanks: pass both flag arrays or neither");
+    bind_device(ctx);
+    const uint32_t n = gT->n;
+    if (n == 0) return;
+    const double* prev = stage_in(ctx, ctx->stage_b, previous, n);
+    double* R0 = ctx->rank[0].as<double>(n);
+    double* C0 = ctx->contrib[0].as<double>(n);
+    DYNPR_CK(cudaMemcpyAsync(R0, prev, (size_t)n * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+    launch_init_ranks(ctx, gF, R0, 0.0, R0, nullptr, C0, nullptr);
+    StageOut<double> out(ctx, ctx->rank[1], current, n);
+    const bool flagged = vertex_affected != nullptr;
+    uint8_t *va = nullptr, *np = nullptr;
+    bool host_flags = false;
+    if (flagged) {
+      host_flags = !is_device_ptr(vertex_affected);
+      if (host_flags) {
+        va = ctx->flags_va.as<uint8_t>(n);
+        np = ctx->flags_np.as<uint8_t>(n);
+        DYNPR_CK(cudaMemcpyAsync(va, vertex_affected, n, cudaMemcpyHostToDevice, ctx->stream));
+        DYNPR_CK(cudaMemcpyAsync(np, neighbors_pending, n, cudaMemcpyHostToDevice, ctx->stream));
+      } else {
+        va = vertex_affected;
+        np = neighbors_pending;
+      }
+    }
+    const Schedule s = build_schedule(ctx, gT, cfg->low_degree_threshold, nullptr, true);
+    SweepRed* red = ctx->red.as<SweepRed>(2);
+    DYNPR_CK(cudaMemsetAsync(red, 0, sizeof(SweepRed), ctx->stream));
+    SweepArgs a{};
+    a.offT = gT->off;
+    a.idxT = gT->tgt;
+    a.offF = gF->off;
+    a.n = n;
+    a.T = cfg->low_degree_threshold;
+    a.alpha = cfg->damping_factor;
+    a.teleport = (1.0 - cfg->damping_factor) / (double)n;
+    a.tf = cfg->frontier_tolerance;
+    a.tp = cfg->prune_tolerance;
+    a.rank_prev = R0;
+    a.rank_cur = out.dev;
+    a.contrib_prev = C0;
+    a.contrib_cur = nullptr;
+    a.va = va;
+    a.np = np;
+    a.written = nullptr;
+    a.red = red;
+    a.chunks = s.chunks;
+    a.n_chunks = s.n_chunks;
+    a.multi = s.multi;
+    a.n_multi = s.n_multi;
+    a.partials = s.partials;
+    a.np_accumulate = 1;
+    a.copy_all = 1;
+    launch_sweep(ctx, a, flagged, mode == DYNPR_RANK_CLOSED_LOOP_PRUNE, s.n_low);
+    if (flagged && host_flags) {
+      DYNPR_CK(cudaMemcpyAsync(vertex_affected, va, n, cudaMemcpyDeviceToHost, ctx->stream));
+      DYNPR_CK(cudaMemcpyAsync(neighbors_pending, np, n, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    out.commit();
+  });
+}
+
+dynpr_status dynpr_linf_norm_delta(dynpr_context* ctx, const double* a, const double* b, uint64_t n, double* out) {
+  return api_guard([&] {
+    if (!ctx || !out) invalid("null argument");
+    bind_device(ctx);
+    const double* da = stage_in(ctx, ctx->stage_a, a, n);
+    const double* db = stage_in(ctx, ctx->stage_b, b, n);
+    auto* bits = ctx->scratch64a.as<unsigned long long>(1);
+    launch_linf(ctx, da, db, n, bits);
+    DYNPR_CK(cudaMemcpyAsync(ctx->pinned, bits, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+    unsigned long long h;
+    std::memcpy(&h, ctx->pinned, 8);
+    *out = bits_to_double(h);
+  });
+}
+
+dynpr_status dynpr_l1_norm_delta(dynpr_context* ctx, const double* a, const double* b, uint64_t n, double* out) {
+  return api_guard([&] {
+    if (!ctx || !out) invalid("null argument");
+    bind_device(ctx);
+    const double* da = stage_in(ctx, ctx->stage_a, a, n);
+    const double* db = stage_in(ctx, ctx->stage_b, b, n);
+    double* part = ctx->stage_c.as<double>((n + 4095) / 4096 + 2);
+    double* res = part + (n + 4095) / 4096 + 1;
+    launch_l1(ctx, da, db, n, part, res);
+    DYNPR_CK(cudaMemcpyAsync(ctx->pinned, res, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+    std::memcpy(out, ctx->pinned, 8);
+  });
+}
+
+dynpr_status dynpr_initial_affected(dynpr_context* ctx, const dynpr_graph* g, const uint32_t* del_src,
+                                    const uint32_t* del_dst, uint64_t n_del, const uint32_t* ins_src,
+                                    const uint32_t* ins_dst, uint64_t n_ins, uint8_t* vertex_affected,
+                                    uint8_t* neighbors_pending) {
+  return api_guard([&] {
+    if (!ctx || !g) invalid("null argument");
+    bind_device(ctx);
+    const uint32_t n = g->n;
+    const uint32_t* ds = stage_in(ctx, ctx->batch[0], del_src, n_del);
+    const uint32_t* dd = stage_in(ctx, ctx->batch[1], del_dst, n_del);
+    const uint32_t* is = stage_in(ctx, ctx->batch[2], ins_src, n_ins);
+    const uint32_t* id = stage_in(ctx, ctx->batch[3], ins_dst, n_ins);
+    if (any_bad_ids(ctx, ds, dd, n_del, n)) invalid("initialAffected deletions: vertex id out of range");
+    if (any_bad_ids(ctx, is, id, n_ins, n)) invalid("initialAffected insertions: vertex id out of range");
+    StageOut<uint8_t> va(ctx, ctx->flags_va, vertex_affected, n);
+    StageOut<uint8_t> np(ctx, ctx->flags_np, neighbors_pending, n);
+    if (n) {
+      DYNPR_CK(cudaMemsetAsync(va.dev, 0, n, ctx->stream));
+      DYNPR_CK(cudaMemsetAsync(np.dev, 0, n, ctx->stream));
+    }
+    launch_init_affected(ctx, g, ds, dd, n_del, is, n_ins, va.dev, np.dev, 0, nullptr, nullptr, nullptr);
+    va.commit();
+    np.commit();
+  });
+}
+
+dynpr_status dynpr_expand_affected(dynpr_context* ctx, const dynpr_graph* g, uint8_t* vertex_affected,
+                                   const uint8_t* neighbors_pending, uint32_t threshold) {
+  return api_guard([&] {
+    if (!ctx || !g) invalid("null argument");
+    bind_device(ctx);
+    const uint32_t n = g->n;
+    if (!n) return;
+    const uint8_t* np = stage_in(ctx, ctx->flags_np, neighbors_pending, n);
+    StageOut<uint8_t> va(ctx, ctx->flags_va, vertex_affected, n);
+    if (va.host)
+      DYNPR_CK(cudaMemcpyAsync(va.dev, vertex_affected, n, cudaMemcpyHostToDevice, ctx->stream));
+    uint32_t* pl = ctx->pend_low.as<uint32_t>(n);
+    uint32_t* ph = ctx->pend_high.as<uint32_t>(n);
+    SweepRed* red = ctx->red.as<SweepRed>(2);
+    DYNPR_CK(cudaMemsetAsync(red, 0, sizeof(SweepRed), ctx->stream));
+    launch_collect_pending(ctx, g, np, threshold, pl, ph, red);
+    const SweepRed r = read_red(ctx, red);
+    launch_expand(ctx, g, va.dev, pl, r.pend_low, ph, r.pend_high);
+    va.commit();
+  });
+}
+
+// ---- engines -------------------------------------------------------------------
+dynpr_status dynpr_static_pagerank(dynpr_context* ctx, const dynpr_graph* gT, const dynpr_graph* gF,
+                                   const dynpr_config* cfg, double* ranks_out, dynpr_stats* stats,
+                                   dynpr_observer observer, void* observer_user) {
+  return api_guard([&] {
+    if (!ctx) invalid("null context");
+    validate_config(cfg);
+    check_pair(gT, gF);
+    if (!ranks_out) invalid("null output array");
+    bind_device(ctx);
+    SolveSpec sp;
+    sp.gT = gT;
+    sp.gF = gF;
+    sp.cfg = cfg;
+    solve(ctx, sp, ranks_out, stats, observer, observer_user);
+  });
+}
+
+dynpr_status dynpr_naive_dynamic(dynpr_context* ctx, const dynpr_graph* gT, const dynpr_graph* gF,
+                                 const double* previous, uint64_t n_previous, const dynpr_config* cfg,
+                                 double* ranks_out, dynpr_stats* stats, dynpr_observer observer,
+                                 void* observer_user) {
+  return api_guard([&] {
+    if (!ctx) invalid("null context");
+    validate_config(cfg);
+    check_pair(gT, gF);
+    if (n_previous != gT->n) invalid("naiveDynamic: previousRanks length mismatch");
+    if (!ranks_out) invalid("null output array");
+    bind_device(ctx);
+    SolveSpec sp;
+    sp.gT = gT;
+    sp.gF = gF;
+    sp.cfg = cfg;
+    sp.prev = stage_in(ctx, ctx->stage_b, previous, n_previous);
+    solve(ctx, sp, ranks_out, stats, observer, observer_user);
+  });
+}
+
+dynpr_status dynpr_dynamic_frontier(dynpr_context* ctx, const dynpr_graph* gF, const dynpr_graph* gT,
+                                    const uint32_t* del_src, const uint32_t* del_dst, uint64_t n_del,
+                                    const uint32_t* ins_src, const uint32_t* ins_dst, uint64_t n_ins,
+                                    const double* previous, uint64_t n_previous, const dynpr_config* cfg,
+                                    int pruning, double* ranks_out, dynpr_stats* stats, dynpr_observer observer,
+                                    void* observer_user) {
+  return api_guard([&] {
+    if (!ctx) invalid("null context");
+    // checkFrontierInputs (engine.cpp:155-162)
+    validate_config(cfg);
+    check_pair(gT, gF);
+    if (n_previous != gT->n) invalid("dynamicFrontier: previousRanks length mismatch");
+    if (!ranks_out) invalid("null output array");
+    bind_device(ctx);
+    SolveSpec sp;
+    sp.gT = gT;
+    sp.gF = gF;
+    sp.cfg = cfg;
+    sp.prev = stage_in(ctx, ctx->stage_b, previous, n_previous);
+    sp.ds = stage_in(ctx, ctx->batch[0], del_src, n_del);
+    sp.dd = stage_in(ctx, ctx->batch[1], del_dst, n_del);
+    sp.is = stage_in(ctx, ctx->batch[2], ins_src, n_ins);
+    const uint32_t* id = stage_in(ctx, ctx->batch[3], ins_dst, n_ins);
+    sp.nd = n_del;
+    sp.ni = n_ins;
+    // initialAffected range checks (frontier.cpp:36-37)
+    if (any_bad_ids(ctx, sp.ds, sp.dd, n_del, gT->n)) invalid("initialAffected deletions: vertex id out of range");
+    if (any_bad_ids(ctx, sp.is, id, n_ins, gT->n)) invalid("initialAffected insertions: vertex id out of range");
+    sp.flagged = true;
+    sp.closed = pruning != 0;
+    solve(ctx, sp, ranks_out, stats, observer, observer_user);
+  });
+}
+
+dynpr_status dynpr_dynamic_frontier_from_flags(dynpr_context* ctx, const dynpr_graph* gF, const dynpr_graph* gT,
+                                               const uint8_t* vertex_affected, const uint8_t* neighbors_pending,
+                                               uint64_t n_flags, const double* previous, uint64_t n_previous,
+                                               const dynpr_config* cfg, int pruning, double* ranks_out,
+                                               dynpr_stats* stats, dynpr_observer observer, void* observer_user) {
+  return api_guard([&] {
+    if (!ctx) invalid("null context");
+    validate_config(cfg);
+    check_pair(gT, gF);
+    if (n_previous != gT->n) invalid("dynamicFrontier: previousRanks length mismatch");
+    if (n_flags != gT->n) invalid("dynamicFrontier: flags length mismatch");
+    if (!ranks_out) invalid("null output array");
+    (void)neighbors_pending;  // cleared by the first sweep before any expansion (engine.cpp:74-76)
+    bind_device(ctx);
+    SolveSpec sp;
+    sp.gT = gT;
+    sp.gF = gF;
+    sp.cfg = cfg;
+    sp.prev = stage_in(ctx, ctx->stage_b, previous, n_previous);
+    sp.flags_in = stage_in(ctx, ctx->stage_a, vertex_affected, n_flags);
+    sp.flagged = true;
+    sp.closed = pruning != 0;
+    solve(ctx, sp, ranks_out, stats, observer, observer_user);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,170 @@
+"""Device CSR build / transpose / self-loops / batch ingest vs the reference.
+
+Known answers restate proj/tests/unit/test_graph.cpp; random cases compare the
+device CSR bytes with the oracle (the reference library when oracle/_ref is
+built) -- CsrGraph equality is byte equality (graph.hpp:43).
+"""
+import numpy as np
+import pytest
+
+from helpers import rand_pair, same_csr, to_dev
+
+pytestmark = pytest.mark.gpu
+
+
+def test_build_csr_empty_graph(dp):  # test_graph.cpp:12-17
+    g = dp.build_csr([], 0)
+    assert g.vertex_count == 0 and g.edge_count == 0
+    assert g.offsets.tolist() == [0]
+
+
+def test_build_csr_collapses_duplicates(dp):  # test_graph.cpp:19-23
+    g = dp.build_csr([(0, 1), (0, 1), (1, 0)], 2)
+    assert g.offsets.tolist() == [0, 1, 2]
+    assert g.targets.tolist() == [1, 0]
+
+
+def test_build_csr_rejects_out_of_range(dp):  # test_graph.cpp:25-28
+    with pytest.raises(ValueError, match=r"buildCsr: vertex id out of range \(0,5\) for \|V\|=3"):
+        dp.build_csr([(0, 1), (0, 5), (7, 7)], 3)
+    with pytest.raises(ValueError):
+        dp.build_csr([(0, 0)], 0)
+
+
+@pytest.mark.parametrize("n,pairs,seed", [(20, 100, 11), (1000, 8000, 3), (70000, 500000, 5)])
+def test_build_csr_matches_oracle(dp, oracle_lib, n, pairs, seed):
+    rng = np.random.default_rng(seed)
+    src = rng.integers(0, n, pairs, dtype=np.uint32)
+    dst = rng.integers(0, n, pairs, dtype=np.uint32)
+    g = dp.build_csr((src, dst), n)
+    assert same_csr(g, oracle_lib.build_csr((src, dst), n))
+
+
+def test_transpose_reverses_a_path(dp):  # test_graph.cpp:48-53
+    t = dp.transpose(dp.build_csr([(0, 1), (1, 2)], 3))
+    assert t.offsets.tolist() == [0, 0, 1, 2]
+    assert t.targets.tolist() == [0, 1]
+
+
+def test_transpose_fixes_self_loop_only_graphs(dp):  # test_graph.cpp:55-58
+    g = dp.build_csr([(0, 0), (1, 1), (2, 2)], 3)
+    assert dp.transpose(g) == g
+
+
+@pytest.mark.parametrize("seed,n,pairs", [(5, 50, 300), (9, 3000, 40000)])
+def test_transpose_matches_oracle_and_is_involutive(dp, oracle_lib, seed, n, pairs):
+    g, gt = rand_pair(oracle_lib, seed, n, pairs)
+    dg = to_dev(dp, g)
+    dt = dp.transpose(dg)
+    assert same_csr(dt, gt)
+    assert dp.transpose(dt) == dg  # test_graph.cpp:60-67
+
+
+def test_add_self_loops(dp):  # test_graph.cpp:69-80
+    g = dp.add_self_loops(dp.build_csr([], 3))
+    assert g.edge_count == 3 and all(g.has_self_loop(v) for v in range(3))
+    bare = dp.build_csr([(0, 1), (1, 1), (2, 0)], 3)
+    a = dp.add_self_loops(bare)
+    assert a.edge_count == bare.edge_count + 2
+    assert dp.add_self_loops(a) == a
+
+
+def test_add_self_loops_matches_oracle(dp, oracle_lib):
+    rng = np.random.default_rng(1)
+    src = rng.integers(0, 5000, 30000, dtype=np.uint32)
+    dst = rng.integers(0, 5000, 30000, dtype=np.uint32)
+    og = oracle_lib.add_self_loops(oracle_lib.build_csr((src, dst), 5000))
+    assert same_csr(dp.add_self_loops(dp.build_csr((src, dst), 5000)), og)
+
+
+def test_apply_batch_replaces_an_edge(dp):  # test_graph.cpp:82-90
+    g = dp.add_self_loops(dp.build_csr([(0, 1)], 2))
+    nxt = dp.apply_batch(g, dp.BatchUpdate(deletions=[(0, 1)], insertions=[(1, 0)]))
+    assert nxt.offsets.tolist() == [0, 1, 3]
+    assert nxt.targets.tolist() == [0, 0, 1]
+
+
+def test_apply_batch_with_empty_batch_equals_add_self_loops(dp):  # test_graph.cpp:92-97
+    bare = dp.build_csr([(0, 1), (2, 1)], 3)
+    assert dp.apply_batch(bare, dp.BatchUpdate()) == dp.add_self_loops(bare)
+    aug = dp.add_self_loops(bare)
+    assert dp.apply_batch(aug, dp.BatchUpdate()) == aug
+
+
+def test_apply_batch_matches_the_reference(dp, oracle_lib):  # test_graph.cpp:99-121
+    rng = oracle_lib.rng(99)
+    for _ in range(50):
+        g = oracle_lib.random_graph(rng, 30, 150)
+        dels, ins, used = [], [], set()
+        for _ in range(14):
+            u, v = rng.bounded(30), rng.bounded(30)
+            if u == v or (u, v) in used:
+                continue
+            used.add((u, v))
+            if oracle_lib.has_edge(g, u, v):
+                dels.append((u, v))
+            elif rng.bounded(3) == 0:
+                dels.append((u, v))
+            else:
+                ins.append((u, v))
+        ref, miss, dup = oracle_lib.apply_batch(g, dels, ins)
+        st = dp.BatchApplyStats()
+        nxt = dp.apply_batch(to_dev(dp, g), dp.BatchUpdate(dels, ins), st)
+        assert same_csr(nxt, ref)
+        assert (st.missing_deletions, st.duplicate_insertions) == (miss, dup)
+
+
+def test_apply_batch_tallies_noops(dp):  # test_graph.cpp:123-134
+    g = dp.add_self_loops(dp.build_csr([(0, 1)], 3))
+    st = dp.BatchApplyStats()
+    nxt = dp.apply_batch(g, dp.BatchUpdate([(1, 2), (1, 2)], [(0, 1), (0, 2)]), st)
+    assert st.missing_deletions == 2 and st.duplicate_insertions == 1
+    assert nxt.has_edge(0, 2) and nxt.has_edge(0, 1)
+
+
+def test_apply_batch_validates(dp):  # test_graph.cpp:136-150
+    g = dp.add_self_loops(dp.build_csr([(0, 1)], 2))
+    with pytest.raises(ValueError, match="self-loops cannot be deleted"):
+        dp.apply_batch(g, dp.BatchUpdate(deletions=[(1, 1)]))
+    with pytest.raises(ValueError, match="appears in both deletions and insertions"):
+        dp.apply_batch(g, dp.BatchUpdate([(0, 1)], [(0, 1)]))
+    with pytest.raises(ValueError, match=r"applyBatch insertions: vertex id out of range \(0,7\) for \|V\|=2"):
+        dp.apply_batch(g, dp.BatchUpdate(insertions=[(0, 7)]))
+    # range errors in the deletions come before self-loop errors (graph.cpp:116-120)
+    with pytest.raises(ValueError, match="applyBatch deletions: vertex id out of range"):
+        dp.apply_batch(g, dp.BatchUpdate(deletions=[(1, 1), (5, 0)]))
+
+
+@pytest.mark.parametrize("scale,size,seed", [(12, 200, 3), (14, 3000, 8)])
+def test_random_batch_ingest_pair_matches_reference(dp, oracle_lib, scale, size, seed):
+    """generateRandomBatch (80/20) -> applyBatch + transpose, on RMAT."""
+    src, dst = oracle_lib.rmat_edges(scale, 16 << scale)
+    g = oracle_lib.add_self_loops(oracle_lib.build_csr((src, dst), 1 << scale))
+    gt = oracle_lib.transpose(g)
+    dels, ins = oracle_lib.generate_random_batch(g, size, 0.8, seed)
+    g2, miss, dup = oracle_lib.apply_batch(g, dels, ins)
+    gt2 = oracle_lib.transpose(g2)
+    st = dp.BatchApplyStats()
+    dg2, dgt2 = dp.apply_batch_pair(to_dev(dp, g), to_dev(dp, gt), dp.BatchUpdate(dels, ins), st)
+    assert same_csr(dg2, g2) and same_csr(dgt2, gt2)
+    assert (st.missing_deletions, st.duplicate_insertions) == (miss, dup)
+
+
+@pytest.mark.parametrize("scale", [8, 12, 16])
+def test_rmat_generator_matches_oracle(dp, oracle_lib, scale):
+    src, dst = oracle_lib.rmat_edges(scale, 16 << scale)
+    og = oracle_lib.add_self_loops(oracle_lib.build_csr((src, dst), 1 << scale))
+    assert same_csr(dp.rmat_graph(scale), og)
+
+
+def test_from_csr_validation(dp):  # graph.cpp:30-49
+    with pytest.raises(ValueError, match="malformed offsets"):
+        dp.CsrGraph.from_csr(2, [0, 1, 3], [1, 0])
+    with pytest.raises(ValueError, match="non-decreasing"):
+        dp.CsrGraph.from_csr(3, [0, 2, 1, 2], [1, 0])
+    with pytest.raises(ValueError, match="target id out of range"):
+        dp.CsrGraph.from_csr(2, [0, 1, 2], [1, 5])
+    with pytest.raises(ValueError, match="sorted and deduplicated"):
+        dp.CsrGraph.from_csr(2, [0, 2, 2], [1, 1])
+    g = dp.CsrGraph.from_csr(2, [0, 1, 2], [1, 0])
+    assert g.out(0) == [1] and g.out(1) == [0] and g.degree(0) == 1
