@@ -1,0 +1,455 @@
+#!/usr/bin/env python
+"""Benchmark: Static and DF-P PageRank on synthetic RMAT graphs (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload rmat24|rmat20|rmat18] [--batch-frac 1e-4]
+
+Default workload (N=1): BASELINE configs[2] -- Static PageRank on RMAT
+scale-24 (Graph500 a,b,c = .57,.19,.19, edge factor 16, dedup + self-loops,
+alpha 0.85, tol 1e-10), the single-B200 roofline run.  One step follows the
+reference harness's random-batch protocol (harness.cpp:184-212, configs[1]):
+a fresh 80/20 batch of 1e-4|E| from the reference generator is ingested into
+the base graph on the device (timed separately), then Static PageRank and
+DF-P PageRank (warm-started from the base ranks) solve the updated graph.
+
+  value      Static GTEPS = |E| x iterations / solve time (CUDA events on the
+             library's stream around the engine call -- partition, init,
+             sweeps, convergence checks; graph resident in HBM, 1.4 GB > L2)
+  e2e        same metric through the public C-ABI with HOST buffers: upload
+             of the step's CSR pair from pinned memory + solve + ranks D2H
+  dfp        DF-P ms/solve on the same updated graph and its speed-up
+  roofline   the rank-update sweep vs measured HBM bandwidth
+  cpu_baseline  the reference library (oracle/_ref, OpenMP, all host cores)
+             on a bounded sample of the same workload
+
+--impl reference runs the unmodified reference CPU library through its own
+public API (staticPageRank) on the box's host cores, same metric and unit.
+"""
+from __future__ import annotations
+
+import argparse
+import gc
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    "rmat24": (24, "configs[2]: Static PageRank on RMAT scale-24 (edge factor 16, self-loops), "
+                   "alpha=0.85, tol=1e-10, single-B200 roofline run; per step a 1e-4|E| 80/20 random batch "
+                   "(configs[1] protocol) is ingested and Static + DF-P solve the updated graph"),
+    "rmat20": (20, "configs[1]: DF-P PageRank on RMAT scale-20 with 80/20 random batches; Static on the same "
+                   "updated graph"),
+    "rmat18": (18, "configs[0]: Static PageRank on RMAT scale-18 (edge factor 16, self-loops), alpha=0.85, "
+                   "tol=1e-10"),
+}
+
+
+def baseline_metric():
+    with open(os.path.join(ROOT, "BASELINE.json")) as f:
+        return json.load(f)["metric"]
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(prefix="clocks_", suffix=".csv")
+        os.close(fd)
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-i", str(self.device), "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.f.close()
+
+    def summary(self):
+        if not self.path or not os.path.exists(self.path):
+            return None
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as f:
+            for line in f:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 6:
+                    continue
+                try:
+                    sm.append(float(parts[0]))
+                    mx = max(mx, float(parts[1]))
+                except ValueError:
+                    continue
+                for name, val in zip(names, parts[2:6]):
+                    if val.lower().startswith("active"):
+                        reasons.add(name)
+        os.unlink(self.path)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup(backend: str):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group(backend)
+    return world, rank, local
+
+
+def max_over_ranks(x: float, world: int, device=None) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x: float, world: int, device=None) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def barrier(world: int):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# ---------------------------------------------------------------------------
+def cpu_reference_static(gF_host, gT_host, sweeps: int, threads: int):
+    """The reference library on host cores: `sweeps` static sweeps of
+    staticPageRank (maxIterations bounds the sample).  Returns
+    (GTEPS, ms, kind, ranks)."""
+    import oracle
+    kind = "reference" if oracle.available("ref") else "port"
+    O = oracle.Oracle("ref" if kind == "reference" else "port")
+    O.set_threads(threads)
+    n = len(gF_host[0]) - 1
+    gF = O.graph_from_csr(n, *gF_host)
+    gT = O.graph_from_csr(n, *gT_host)
+    cfg = oracle.default_config(max_iterations=sweeps, convergence_check_disabled=1)
+    O.static(gT, gF, cfg)  # warm-up (page-in)
+    t0 = time.perf_counter()
+    r = O.static(gT, gF, cfg)
+    ms = (time.perf_counter() - t0) * 1e3
+    gteps = gF.m * r.iterations / (ms * 1e-3) / 1e9
+    return gteps, ms, kind, r.ranks, (threads if kind == "reference" else 1)
+
+
+def run_reference(args, world, rank, local):
+    """--impl reference: the unmodified reference CPU library, rank 0 only."""
+    if rank != 0:
+        return
+    import numpy as np
+
+    import oracle
+    import paper_2404_08299_b200 as dp
+    scale, desc = WORKLOADS[args.workload]
+    threads = os.cpu_count() or 1
+    # Input preparation only (not timed, not the reference's code path): the
+    # RMAT graph is generated on the device and handed over through the
+    # reference's validating CsrGraph(n, offsets, targets) constructor
+    # (BASELINE.md "Kronecker-27 CPU run": hand the graph over from the GPU).
+    ctx = dp.Context(local)
+    g = dp.rmat_graph(scale, seed=args.seed, ctx=ctx)
+    gt = dp.transpose(g)
+    gF_host = (g.offsets.copy(), g.targets.copy())
+    gT_host = (gt.offsets.copy(), gt.targets.copy())
+    n, m = g.vertex_count, g.edge_count
+    del g, gt
+    gc.collect()
+    kind = "reference" if oracle.available("ref") else "port"
+    O = oracle.Oracle("ref" if kind == "reference" else "port")
+    O.set_threads(threads)
+    gF = O.graph_from_csr(n, *gF_host)
+    gT = O.graph_from_csr(n, *gT_host)
+    cfg = oracle.default_config(max_iterations=args.ref_sweeps, convergence_check_disabled=1)
+    times, iters = [], []
+    for step in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        r = O.static(gT, gF, cfg)  # staticPageRank, harness.cpp:222-224 style timing
+        ms = (time.perf_counter() - t0) * 1e3
+        if step >= args.warmup:
+            times.append(ms)
+            iters.append(r.iterations)
+    total_ms = sum(times)
+    value = m * sum(iters) / (total_ms * 1e-3) / 1e9
+    sample = (f"{args.ref_sweeps} static sweeps per step (staticPageRank, maxIterations={args.ref_sweeps}, "
+              f"convergence check disabled) on the base RMAT-{scale} graph")
+    line = {
+        "impl": "reference", "metric": baseline_metric(), "value": value, "unit": "GTEPS", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic RMAT (Graph500 a=.57 b=c=.19, edge factor 16, seed %d, dedup + self-loops)" % args.seed,
+        "config": {"workload": desc, "scale": scale, "n": n, "m": m, "alpha": 0.85, "tol": 1e-10},
+        "cpu_baseline": {"value": value, "unit": "GTEPS", "cores": threads if kind == "reference" else 1,
+                         "kind": kind, "sample": sample},
+        "e2e": {"value": value, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# ---------------------------------------------------------------------------
+def run_ours(args, world, rank, local):
+    import numpy as np
+    import torch
+
+    import paper_2404_08299_b200 as dp
+    from paper_2404_08299_b200 import _native as N
+
+    torch.cuda.set_device(local)
+    scale, desc = WORKLOADS[args.workload]
+    ctx = dp.Context(local)
+    L = N.lib()
+
+    # ---- setup (untimed): base graph pair, base ranks, batches ---------------
+    g0 = dp.rmat_graph(scale, seed=args.seed, ctx=ctx)
+    gt0 = dp.transpose(g0)
+    n, m0 = g0.vertex_count, g0.edge_count
+    base = dp.static_pagerank(gt0, g0)
+    base_dev = torch.from_numpy(base.ranks).to(f"cuda:{local}")
+    size = dp.batch_size_from_fraction(args.batch_frac, m0)
+    total = args.warmup + args.steps
+    batches = [dp.generate_random_batch(g0, size, 0.8, dp.derive_seed(args.seed + rank, 1000003 + k))
+               for k in range(total)]
+    ranks_dev = torch.empty(n, dtype=torch.float64, device=f"cuda:{local}")
+    cfg = dp.EngineConfig()._c()
+
+    def static_dev(gT, gF, max_iter=None):
+        c = dp.EngineConfig(max_iterations=max_iter or 500, convergence_check_disabled=bool(max_iter))._c()
+        st = N.Stats()
+        dp._check(L.dynpr_static_pagerank(N.C.c_void_p(ctx.h), N.C.c_void_p(gT.h), N.C.c_void_p(gF.h),
+                                          N.C.byref(c), N.C.c_void_p(ranks_dev.data_ptr()), N.C.byref(st),
+                                          N.OBSERVER(0), None))
+        return st
+
+    def dfp_dev(gF, gT, b):
+        (ds, dd), (is_, id_) = b.deletions, b.insertions
+        st = N.Stats()
+        dp._check(L.dynpr_dynamic_frontier(
+            N.C.c_void_p(ctx.h), N.C.c_void_p(gF.h), N.C.c_void_p(gT.h), dp._p(ds), dp._p(dd), len(ds),
+            dp._p(is_), dp._p(id_), len(is_), N.C.c_void_p(base_dev.data_ptr()), n, N.C.byref(cfg), 1,
+            N.C.c_void_p(ranks_dev.data_ptr()), N.C.byref(st), N.OBSERVER(0), None))
+        return st
+
+    rec = {"static_ms": [], "static_it": [], "static_edges": [], "dfp_ms": [], "dfp_it": [], "dfp_aff": [],
+           "dfp_edges": [], "ingest_ms": []}
+    sweep0 = None
+    launches0 = 0
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        for k in range(total):
+            timed = k >= args.warmup
+            if k == args.warmup:
+                barrier(world)
+                torch.cuda.synchronize()
+                ctx.set_profiling(True)
+                launches0 = ctx.launches
+            t0 = time.perf_counter()
+            g, gt = dp.apply_batch_pair(g0, gt0, batches[k])  # device batch ingest
+            ingest_ms = (time.perf_counter() - t0) * 1e3
+            st = static_dev(gt, g)
+            sweep_s = ctx.sweep_times()
+            sd = dfp_dev(g, gt, batches[k])
+            if timed:
+                if sweep0 is None:
+                    sweep0 = (0.0, 0, 0)
+                rec["static_ms"].append(st.device_ms)
+                rec["static_it"].append(st.iterations)
+                rec["static_edges"].append(g.edge_count * st.iterations)
+                rec["dfp_ms"].append(sd.device_ms)
+                rec["dfp_it"].append(sd.iterations)
+                rec["dfp_aff"].append(sd.affected_vertex_iterations)
+                rec["dfp_edges"].append(sd.processed_edges)
+                rec["ingest_ms"].append(ingest_ms)
+                # static-only sweep accounting (profiling counters since warm-up)
+                rec.setdefault("sweep_static", []).append(sweep_s)
+                ctx.set_profiling(True)  # reset counters so the next step's static is isolated
+            if k < total - 1:
+                del g, gt
+                gc.collect()
+        torch.cuda.synchronize()
+        launches = ctx.launches - launches0
+        barrier(world)
+    clock = clocks.summary()
+
+    static_ms_total = sum(rec["static_ms"])
+    static_edges = sum(rec["static_edges"])
+    local_gteps = static_edges / (static_ms_total * 1e-3) / 1e9
+    t_max = max_over_ranks(static_ms_total, world, f"cuda:{local}")
+    value = sum_over_ranks(static_edges, world, f"cuda:{local}") / (t_max * 1e-3) / 1e9
+    ms_per_step = t_max / args.steps
+
+    # roofline of the rank-update sweep (k_sweep_low + k_sweep_chunks + k_sweep_multi)
+    sw_ms = sum(s[0] for s in rec["sweep_static"])
+    sw_n = sum(s[1] for s in rec["sweep_static"])
+    sw_bytes = sum(s[2] for s in rec["sweep_static"])
+    peak, peak_kind = measured_peaks()
+    achieved = (sw_bytes / sw_n) / ((sw_ms / sw_n) * 1e-3) / 1e9 if sw_n else 0.0
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f).get(args.workload, {}).get("sweep_dram_bytes_per_launch")
+    except Exception:
+        pass
+
+    out = None
+    if rank == 0:
+        dfp_ms = statistics.mean(rec["dfp_ms"])
+        st_ms = statistics.mean(rec["static_ms"])
+        out = {
+            "metric": baseline_metric(), "value": value, "unit": "GTEPS", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic RMAT (Graph500 a=.57 b=c=.19, edge factor 16, seed %d, dedup + self-loops, "
+                    "generated on device); random 80/20 batches from the reference generateRandomBatch "
+                    "algorithm" % args.seed,
+            "config": {"workload": desc, "scale": scale, "n": n, "m_base": m0, "alpha": 0.85, "tol": 1e-10,
+                       "batch_fraction": args.batch_frac, "batch_size": size,
+                       "l2": "inputs larger than L2 (graph pair %.2f GB vs 126 MB L2); no flush needed"
+                             % ((2 * (8 * (n + 1) + 4 * m0)) / 1e9),
+                       "parallelism": "single GPU" if world == 1 else
+                       "replicas (one graph per GPU; range-partitioned NCCL path: see DESIGN.md)"},
+            "static": {"ms_per_solve": st_ms, "iterations": statistics.mean(rec["static_it"]),
+                       "gteps": local_gteps},
+            "dfp": {"ms_per_solve": dfp_ms, "iterations": statistics.mean(rec["dfp_it"]),
+                    "affected_vertex_iterations": statistics.mean(rec["dfp_aff"]),
+                    "processed_gteps": sum(rec["dfp_edges"]) / (sum(rec["dfp_ms"]) * 1e-3) / 1e9,
+                    "speedup_vs_static": st_ms / dfp_ms},
+            "ingest": {"ms_per_batch_pair": statistics.mean(rec["ingest_ms"]),
+                       "note": "applyBatch on forward + transpose, host wall clock incl. batch H2D"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "rank-update sweep (k_sweep_low+k_sweep_chunks+k_sweep_multi), "
+                                   "algorithmic bytes 4*edges + 28*vertices + 8 per sweep",
+                         "peak_source": peak_kind, "sweeps": sw_n},
+            "gpu_launches": launches,
+            "clocks": clock,
+        }
+
+    # ---- e2e: same metric through the C-ABI with host buffers ------------------
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    off_t = torch.from_numpy(gt.offsets).pin_memory()
+    tgt_t = torch.from_numpy(gt.targets).pin_memory()
+    off_f = torch.from_numpy(g.offsets).pin_memory()
+    tgt_f = torch.from_numpy(g.targets).pin_memory()
+    ranks_host = torch.empty(n, dtype=torch.float64).pin_memory()
+    m = g.edge_count
+    e2e_t, e2e_e = 0.0, 0
+    for k in range(e2e_steps + 1):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        hT, hF = N.C.c_void_p(), N.C.c_void_p()
+        dp._check(L.dynpr_graph_from_csr(N.C.c_void_p(ctx.h), n, N.C.c_void_p(off_t.data_ptr()),
+                                         N.C.c_void_p(tgt_t.data_ptr()), m, N.C.byref(hT)))
+        dp._check(L.dynpr_graph_from_csr(N.C.c_void_p(ctx.h), n, N.C.c_void_p(off_f.data_ptr()),
+                                         N.C.c_void_p(tgt_f.data_ptr()), m, N.C.byref(hF)))
+        st = N.Stats()
+        dp._check(L.dynpr_static_pagerank(N.C.c_void_p(ctx.h), hT, hF, N.C.byref(cfg),
+                                          N.C.c_void_p(ranks_host.data_ptr()), N.C.byref(st), N.OBSERVER(0),
+                                          None))
+        L.dynpr_graph_destroy(hT)
+        L.dynpr_graph_destroy(hF)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if k > 0:  # first pass warms the workspace
+            e2e_t += dt
+            e2e_e += m * st.iterations
+    e2e_tmax = max_over_ranks(e2e_t, world, f"cuda:{local}")
+    e2e_value = sum_over_ranks(e2e_e, world, f"cuda:{local}") / e2e_tmax / 1e9
+
+    if rank == 0:
+        h2d = 2 * (8 * (n + 1) + 4 * m)
+        out["e2e"] = {"value": e2e_value, "unit": "GTEPS", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8 * n,
+                      "note": "per step: dynpr_graph_from_csr x2 (CSR pair from pinned host memory, validated) + "
+                              "dynpr_static_pagerank with a pinned host ranks buffer; wall clock, %d steps" % e2e_steps}
+
+    # ---- CPU baseline: the reference library on the host cores (rank 0, N=1) ---
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        gteps, ms, kind, ref_ranks, cores = cpu_reference_static(
+            (g.offsets, g.targets), (gt.offsets, gt.targets), args.ref_sweeps, threads)
+        out["cpu_baseline"] = {"value": gteps, "unit": "GTEPS", "cores": cores, "kind": kind,
+                               "sample": f"{args.ref_sweeps} static sweeps (staticPageRank, maxIterations="
+                                         f"{args.ref_sweeps}) on the last step's updated RMAT-{scale} graph, "
+                                         f"{ms:.0f} ms"}
+        st = static_dev(gt, g, max_iter=args.ref_sweeps)
+        mine = ranks_dev.cpu().numpy()
+        out["parity_sample"] = {"sweeps": args.ref_sweeps, "ranks_bitwise_equal": bool(np.array_equal(mine, ref_ranks)),
+                                "linf": float(np.max(np.abs(mine - ref_ranks)))}
+    if rank == 0:
+        print(json.dumps(out))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="rmat24")
+    ap.add_argument("--batch-frac", type=float, default=1e-4)
+    ap.add_argument("--seed", type=int, default=42)
+    ap.add_argument("--ref-sweeps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    world, rank, local = dist_setup("gloo" if args.impl == "reference" else "nccl")
+    if args.impl == "reference":
+        run_reference(args, world, rank, local)
+    else:
+        run_ours(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -165,6 +165,26 @@ dynpr_status dynpr_graph_rmat(dynpr_context* ctx, uint32_t scale,
                               uint32_t edge_factor, double a, double b,
                               double c, uint64_t seed, dynpr_graph** out);
 
+/* ---- workload (workload.hpp:189-197, rng.hpp:44-47) --------------------- */
+/* batchSizeFromFraction (workload.cpp:245-249): round half up, floor 1. */
+uint64_t dynpr_batch_size_from_fraction(double fraction, uint64_t total);
+/* deriveSeed (rng.hpp:44-47). */
+uint64_t dynpr_derive_seed(uint64_t seed, uint64_t stream);
+/* generateRandomBatch (workload.cpp:183-243), same draws and order: the
+ * insertions (ceil(insert_fraction * total) uniform non-existing,
+ * non-self, distinct pairs) then the deletions (uniform without
+ * replacement from the non-loop edges, partial Fisher-Yates).  Host-side
+ * (the RNG stream is sequential); outputs are host arrays of capacity
+ * total_size.  Errors: SizingError / invalid_argument texts of the
+ * reference. */
+dynpr_status dynpr_generate_random_batch(dynpr_context* ctx,
+                                         const dynpr_graph* g,
+                                         uint64_t total_size,
+                                         double insert_fraction, uint64_t seed,
+                                         uint32_t* ins_src, uint32_t* ins_dst,
+                                         uint64_t* n_ins, uint32_t* del_src,
+                                         uint32_t* del_dst, uint64_t* n_del);
+
 /* ---- primitives (partition.hpp:20, rank.hpp:66-76, frontier.hpp:28-36) -- */
 /* partitionByDegree: order[n] (low group then high group, ascending ids). */
 dynpr_status dynpr_partition_by_degree(dynpr_context* ctx,

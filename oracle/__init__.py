@@ -238,8 +238,8 @@ class Oracle:
     # ---- graphs --------------------------------------------------------------
     def graph_from_csr(self, n: int, off, tgt) -> Graph:
         off = np.ascontiguousarray(np.asarray(off, dtype=np.uint64))
+        m = len(tgt)  # targets.size(), checked against offsets.back() (graph.cpp:35-37)
         tgt = _u32(tgt) if len(tgt) else np.zeros(1, np.uint32)
-        m = int(off[-1]) if len(off) else 0
         return self._graph_out(getattr(self.L, self.p + "graph_from_csr"), C.c_uint32(n),
                                _ptr(off, _u64p), _ptr(tgt, _u32p), C.c_uint64(m))
 

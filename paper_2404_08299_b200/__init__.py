@@ -32,7 +32,8 @@ __all__ = [
     "add_self_loops", "apply_batch", "apply_batch_pair", "build_csr", "default_context",
     "dynamic_frontier", "dynamic_frontier_from_flags", "expand_affected", "initial_affected",
     "l1_norm_delta", "linf_norm_delta", "naive_dynamic", "partition_by_degree", "rmat_graph",
-    "static_pagerank", "transpose", "update_ranks",
+    "static_pagerank", "transpose", "update_ranks", "generate_random_batch", "batch_size_from_fraction",
+    "derive_seed",
 ]
 
 
@@ -329,6 +330,30 @@ def rmat_graph(scale: int, edge_factor: int = 16, a: float = 0.57, b: float = 0.
     ctx = _ctx(ctx)
     return _new_graph(N.lib().dynpr_graph_rmat, ctx, int(scale), int(edge_factor), float(a), float(b),
                       float(c), int(seed))
+
+
+# ---- workload (workload.hpp:189-197) --------------------------------------------
+def batch_size_from_fraction(fraction: float, total: int) -> int:
+    return int(N.lib().dynpr_batch_size_from_fraction(float(fraction), int(total)))
+
+
+def derive_seed(seed: int, stream: int) -> int:
+    return int(N.lib().dynpr_derive_seed(int(seed), int(stream)))
+
+
+def generate_random_batch(g: CsrGraph, total_size: int, insert_fraction: float = 0.8,
+                          seed: int = 1) -> BatchUpdate:
+    """generateRandomBatch (workload.cpp:183-243): identical draws to the
+    reference; deletions/insertions come back as (src, dst) uint32 arrays."""
+    cap = max(int(total_size), 1)
+    is_, id_ = np.zeros(cap, np.uint32), np.zeros(cap, np.uint32)
+    ds, dd = np.zeros(cap, np.uint32), np.zeros(cap, np.uint32)
+    ni, nd = C.c_uint64(), C.c_uint64()
+    _check(N.lib().dynpr_generate_random_batch(C.c_void_p(g.ctx.h), C.c_void_p(g.h), int(total_size),
+                                               float(insert_fraction), int(seed), _p(is_), _p(id_),
+                                               C.byref(ni), _p(ds), _p(dd), C.byref(nd)))
+    return BatchUpdate(deletions=(ds[: nd.value].copy(), dd[: nd.value].copy()),
+                       insertions=(is_[: ni.value].copy(), id_[: ni.value].copy()))
 
 
 # ---- primitives ------------------------------------------------------------------

@@ -7,6 +7,8 @@ built) -- CsrGraph equality is byte equality (graph.hpp:43).
 import numpy as np
 import pytest
 
+import oracle
+
 from helpers import rand_pair, same_csr, to_dev
 
 pytestmark = pytest.mark.gpu
@@ -157,14 +159,47 @@ def test_rmat_generator_matches_oracle(dp, oracle_lib, scale):
     assert same_csr(dp.rmat_graph(scale), og)
 
 
-def test_from_csr_validation(dp):  # graph.cpp:30-49
-    with pytest.raises(ValueError, match="malformed offsets"):
-        dp.CsrGraph.from_csr(2, [0, 1, 3], [1, 0])
-    with pytest.raises(ValueError, match="non-decreasing"):
-        dp.CsrGraph.from_csr(3, [0, 2, 1, 2], [1, 0])
-    with pytest.raises(ValueError, match="target id out of range"):
-        dp.CsrGraph.from_csr(2, [0, 1, 2], [1, 5])
-    with pytest.raises(ValueError, match="sorted and deduplicated"):
-        dp.CsrGraph.from_csr(2, [0, 2, 2], [1, 1])
+@pytest.mark.parametrize("n,off,tgt,msg", [
+    (2, [0, 1, 3], [1, 0], "malformed offsets"),
+    (3, [0, 1, 0, 2], [1, 0], "non-decreasing"),
+    (3, [0, 2, 1, 2], [1, 0], "sorted and deduplicated"),  # vertex 0 fails first
+    (2, [0, 1, 2], [1, 5], "target id out of range"),
+    (2, [0, 2, 2], [1, 1], "sorted and deduplicated"),
+    (3, [0, 2, 2, 3], [2, 9, 0], "target id out of range"),
+])
+def test_from_csr_validation(dp, oracle_lib, n, off, tgt, msg):  # graph.cpp:30-49
+    with pytest.raises(oracle.OracleError) as ref_err:
+        oracle_lib.graph_from_csr(n, off, tgt)
+    assert msg in str(ref_err.value)
+    with pytest.raises(ValueError) as err:
+        dp.CsrGraph.from_csr(n, off, tgt)
+    assert str(err.value) == str(ref_err.value)
+
+
+def test_from_csr_accessors(dp):
     g = dp.CsrGraph.from_csr(2, [0, 1, 2], [1, 0])
     assert g.out(0) == [1] and g.out(1) == [0] and g.degree(0) == 1
+
+
+@pytest.mark.parametrize("scale,frac,ins,seed", [(10, 1e-3, 0.8, 1), (14, 1e-4, 0.8, 42), (12, 1e-2, 0.5, 9),
+                                                 (10, 1e-3, 1.0, 3), (10, 1e-3, 0.0, 4)])
+def test_generate_random_batch_matches_reference(dp, oracle_lib, scale, frac, ins, seed):
+    """workload.cpp:183-243 -- identical draws (virtual Fisher-Yates)."""
+    src, dst = oracle_lib.rmat_edges(scale, 16 << scale)
+    og = oracle_lib.add_self_loops(oracle_lib.build_csr((src, dst), 1 << scale))
+    size = oracle_lib.batch_size_from_fraction(frac, og.m)
+    assert dp.batch_size_from_fraction(frac, og.m) == size
+    s = oracle_lib.derive_seed(seed, 5)
+    assert dp.derive_seed(seed, 5) == s
+    dels, inss = oracle_lib.generate_random_batch(og, size, ins, s)
+    b = dp.generate_random_batch(dp.rmat_graph(scale), size, ins, s)
+    assert np.array_equal(b.deletions[0], dels[0]) and np.array_equal(b.deletions[1], dels[1])
+    assert np.array_equal(b.insertions[0], inss[0]) and np.array_equal(b.insertions[1], inss[1])
+
+
+def test_generate_random_batch_errors(dp):
+    g = dp.add_self_loops(dp.build_csr([(0, 1)], 2))
+    with pytest.raises(dp.SizingError, match="requested 3 deletions but only 1 non-loop edges exist"):
+        dp.generate_random_batch(g, 3, 0.0, 1)
+    with pytest.raises(ValueError, match="insertFraction must be in"):
+        dp.generate_random_batch(g, 3, 1.5, 1)
