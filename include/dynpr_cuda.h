@@ -165,6 +165,16 @@ dynpr_status dynpr_graph_rmat(dynpr_context* ctx, uint32_t scale,
                               uint32_t edge_factor, double a, double b,
                               double c, uint64_t seed, dynpr_graph** out);
 
+/* Builds (or reuses) the engine layout of the pair (gT, gF) for degree
+ * threshold `threshold`: vertices relabelled by in-degree, SELL-32 segment
+ * slices of the in-CSR, and with `with_forward` the relabelled out-CSR for
+ * frontier expansion.  It is cached on gT (snapshots are immutable), so the
+ * engines reuse it; an engine call on a pair without it builds it inside the
+ * call.  `build_ms` (nullable) receives the device time of the build. */
+dynpr_status dynpr_graph_prepare(dynpr_context* ctx, const dynpr_graph* gT,
+                                 const dynpr_graph* gF, uint32_t threshold,
+                                 int with_forward, double* build_ms);
+
 /* ---- workload (workload.hpp:189-197, rng.hpp:44-47) --------------------- */
 /* batchSizeFromFraction (workload.cpp:245-249): round half up, floor 1. */
 uint64_t dynpr_batch_size_from_fraction(double fraction, uint64_t total);

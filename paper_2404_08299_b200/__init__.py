@@ -33,7 +33,7 @@ __all__ = [
     "dynamic_frontier", "dynamic_frontier_from_flags", "expand_affected", "initial_affected",
     "l1_norm_delta", "linf_norm_delta", "naive_dynamic", "partition_by_degree", "rmat_graph",
     "static_pagerank", "transpose", "update_ranks", "generate_random_batch", "batch_size_from_fraction",
-    "derive_seed",
+    "derive_seed", "prepare",
 ]
 
 
@@ -321,6 +321,19 @@ def apply_batch_pair(g: CsrGraph, gt: CsrGraph, batch: BatchUpdate,
         stats.missing_deletions += miss.value
         stats.duplicate_insertions += dup.value
     return CsrGraph(hf.value, g.ctx), CsrGraph(ht.value, g.ctx)
+
+
+def prepare(g_transpose: CsrGraph, g_forward: CsrGraph, config: Optional[EngineConfig] = None,
+            frontier: bool = True) -> float:
+    """Build (and cache on g_transpose) the engine layout of the pair: the
+    device graph format the sweeps read (see include/dynpr_cuda.h).  Returns
+    the build's device milliseconds.  Engines build it on demand otherwise."""
+    cfg = config or EngineConfig()
+    ms = C.c_double()
+    _check(N.lib().dynpr_graph_prepare(C.c_void_p(g_transpose.ctx.h), C.c_void_p(g_transpose.h),
+                                       C.c_void_p(g_forward.h), int(cfg.low_degree_threshold), int(frontier),
+                                       C.byref(ms)))
+    return ms.value
 
 
 def rmat_graph(scale: int, edge_factor: int = 16, a: float = 0.57, b: float = 0.19, c: float = 0.19,

@@ -86,9 +86,13 @@ struct SweepRed {
   unsigned long long delta_bits;  // max |r - prev| as IEEE bits (>= 0)
   unsigned long long processed;   // vertices processed (affected count)
   unsigned long long edges;       // in-edges gathered
+  unsigned long long pend_edges;  // out-edges of the pending vertices
   unsigned int pend_low;          // pending vertices with out-degree <= T
-  unsigned int pend_high;         // pending vertices with out-degree  > T
+  unsigned int pend_high;         // 1024-edge expansion items of the others
 };
+
+// Out-edges per expansion work item of a high out-degree vertex.
+constexpr uint32_t kExpandChunk = 1024;
 
 }  // namespace dynpr_b200
 
@@ -102,17 +106,24 @@ struct dynpr_context {
   double sweep_ms = 0.0;
   uint64_t sweeps = 0;
   uint64_t sweep_bytes = 0;
+  uint64_t pull_expansions = 0;
   cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_s0 = nullptr, ev_s1 = nullptr;
   // pinned host scratch for small readbacks
   void* pinned = nullptr;
   // workspace (grow-only; the engines never allocate inside the timed loop)
   dynpr_b200::DevBuf rank[2], contrib[2], flags_va, flags_np, flags_written,
-      pend_low, pend_high, sched_high, sched_chunks, sched_multi, partials,
+      pend_low, pend_high, pend_flags, partials, perm_stage,
       tile_counts, red, stage_a, stage_b, stage_c, stage_d, stage_e, stage_f,
       cub_tmp, scratch64a, scratch64b, scratch32a, scratch32b, scratch8a, batch[4];
 };
 
+namespace dynpr_b200 {
+struct Layout;
+}
+
 struct dynpr_graph {
+  uint64_t id = 0;          // unique per snapshot (layout cache key)
+  dynpr_b200::Layout* layout = nullptr;  // cached engine layout (transpose side)
   dynpr_context* ctx = nullptr;
   uint32_t n = 0;
   uint64_t m = 0;
@@ -181,6 +192,27 @@ inline void sync(dynpr_context* ctx) {
 
 inline void bind_device(dynpr_context* ctx) { DYNPR_CK(cudaSetDevice(ctx->device)); }
 
+// Long-lived arrays (graph snapshots, engine layouts) come from the device's
+// stream-ordered memory pool (release threshold = unlimited, set at context
+// creation), so snapshot churn during batch ingest reuses memory instead of
+// paying cudaMalloc/cudaFree.
+inline void* pool_alloc(dynpr_context* ctx, size_t bytes) {
+  void* p = nullptr;
+  cudaError_t e = cudaMallocAsync(&p, bytes ? bytes : 16, ctx->stream);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw Error(DYNPR_OUT_OF_MEMORY, "device allocation of " + std::to_string(bytes) + " bytes failed");
+  }
+  return p;
+}
+template <class T>
+T* pool_alloc_n(dynpr_context* ctx, uint64_t count) {
+  return static_cast<T*>(pool_alloc(ctx, count * sizeof(T)));
+}
+inline void pool_free(dynpr_context* ctx, void* p) {
+  if (p) cudaFreeAsync(p, ctx->stream);
+}
+
 // ---- device helpers ------------------------------------------------------------
 __device__ __forceinline__ double warp_max(double v) {
 #pragma unroll
@@ -213,6 +245,7 @@ inline int bits_for(uint64_t x) {
 
 // ---- shared internals used across translation units ------------------------
 // graph.cu
+dynpr_graph* new_graph_struct(dynpr_context* ctx, uint32_t n);
 dynpr_graph* make_graph(dynpr_context* ctx, uint32_t n, uint64_t m);
 void destroy_graph(dynpr_graph* g);
 void graph_apply_batch_impl(dynpr_context* ctx, const dynpr_graph* g,

@@ -19,6 +19,7 @@
 #include <cmath>
 #include <string>
 
+#include "layout.cuh"
 #include "sweep.cuh"
 
 namespace dynpr_b200 {
@@ -87,7 +88,8 @@ struct SolveSpec {
   const uint8_t* flags_in = nullptr;
 };
 
-// convergeLoop (engine.cpp:61-95) on the device.
+// convergeLoop (engine.cpp:61-95) on the device, in the layout's new-id
+// space; inputs are permuted in and the result permuted back out.
 void solve(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynpr_stats* stats,
            dynpr_observer obs, void* user) {
   const dynpr_graph* gT = sp.gT;
@@ -95,85 +97,86 @@ void solve(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynpr_sta
   const dynpr_config& c = *sp.cfg;
   const uint32_t n = gT->n;
   cudaStream_t st = ctx->stream;
+  // The engine layout is part of the device graph format (built at ingest
+  // or by dynpr_graph_prepare); an uncached build is timed with the solve.
+  DYNPR_CK(cudaEventRecord(ctx->ev_a, st));
+  const Layout* L = get_layout(ctx, gT, gF, c.low_degree_threshold, sp.flagged);
   // workspace (allocation is excluded from the timed region)
   double* R[2] = {ctx->rank[0].as<double>(n), ctx->rank[1].as<double>(n)};
   double* CB[2] = {ctx->contrib[0].as<double>(n), ctx->contrib[1].as<double>(n)};
+  double* partials = ctx->partials.as<double>(L->n_mseg + 1);
   SweepRed* red = ctx->red.as<SweepRed>(2);
   uint8_t* va = nullptr;
+  uint8_t* np = nullptr;
   uint8_t* written = nullptr;
-  uint32_t *pl = nullptr, *ph = nullptr;
+  uint32_t* pl = nullptr;
+  uint2* ph = nullptr;
   if (sp.flagged) {
-    const uint64_t cap = std::max<uint64_t>(n, sp.nd + sp.ni) + 1;
     va = ctx->flags_va.as<uint8_t>(n);
+    np = ctx->pend_flags.as<uint8_t>(n);
     written = ctx->flags_written.as<uint8_t>(n);
-    pl = ctx->pend_low.as<uint32_t>(cap);
-    ph = ctx->pend_high.as<uint32_t>(cap);
+    pl = ctx->pend_low.as<uint32_t>((uint64_t)n + 1);
+    // every high out-degree vertex contributes ceil(outdeg/1024) items
+    ph = ctx->pend_high.as<uint2>((uint64_t)n + gT->m / kExpandChunk + 1);
   }
   std::vector<double> h_ranks;
   std::vector<uint8_t> h_flags;
+  double* obs_ranks = nullptr;
+  uint8_t* obs_flags = nullptr;
   if (obs) {
     h_ranks.resize(n);
-    if (sp.flagged) h_flags.resize(n);
+    obs_ranks = ctx->stage_c.as<double>(n);
+    if (sp.flagged) {
+      h_flags.resize(n);
+      obs_flags = ctx->flags_np.as<uint8_t>(2ull * n);
+    }
   }
-
-  DYNPR_CK(cudaEventRecord(ctx->ev_a, st));
-  // makePartitions (engine.cpp:40-56): the in-degree schedule.  The
-  // out-degree split of PartitionBoth is applied on the fly when pending
-  // vertices are appended to the low/high expansion lists.
-  const Schedule s = build_schedule(ctx, gT, c.low_degree_threshold, nullptr, true);
   // initRanksUniform / initRanksFrom (rank.cpp:22-37) + contributions
-  launch_init_ranks(ctx, gF, sp.prev, 1.0 / (double)n, R[0], R[1], CB[0], CB[1]);
+  if (sp.prev) launch_gather_perm_f64(ctx, L, sp.prev, R[0]);
+  launch_init_ranks(ctx, L, sp.prev ? R[0] : nullptr, 1.0 / (double)n, R[0], R[1], CB[0], CB[1]);
   if (sp.flagged) {
     DYNPR_CK(cudaMemsetAsync(written, 0, n, st));
     if (sp.flags_in) {
-      DYNPR_CK(cudaMemcpyAsync(va, sp.flags_in, n, cudaMemcpyDeviceToDevice, st));
+      launch_gather_perm_u8(ctx, L, sp.flags_in, va);
     } else {
       // initialAffected + the one expandAffected before the loop
       // (engine.cpp:199-200)
       DYNPR_CK(cudaMemsetAsync(va, 0, n, st));
+      DYNPR_CK(cudaMemsetAsync(np, 0, n, st));
       DYNPR_CK(cudaMemsetAsync(red + 1, 0, sizeof(SweepRed), st));
-      launch_init_affected(ctx, gF, sp.ds, sp.dd, sp.nd, sp.is, sp.ni, va, nullptr, c.low_degree_threshold, pl,
-                           ph, red + 1);
+      launch_init_affected(ctx, L->inv, sp.ds, sp.dd, sp.nd, sp.is, sp.ni, va, np);
+      launch_collect_pending(ctx, L->outdeg, nullptr, n, np, c.low_degree_threshold, pl, ph, red + 1);
       const SweepRed r0 = read_red(ctx, red + 1);
-      launch_expand(ctx, gF, va, pl, r0.pend_low, ph, r0.pend_high);
+      launch_expand(ctx, L->offF, L->tgtF, va, pl, r0.pend_low, ph, r0.pend_high);
     }
   }
 
-  SweepArgs a{};
-  a.offT = gT->off;
-  a.idxT = gT->tgt;
-  a.offF = gF->off;
-  a.n = n;
-  a.T = c.low_degree_threshold;
+  SweepArgs a = layout_args(L, partials);
   a.alpha = c.damping_factor;
   a.teleport = (1.0 - c.damping_factor) / (double)n;  // rank.cpp:85
   a.tf = c.frontier_tolerance;
   a.tp = c.prune_tolerance;
   a.va = va;
-  a.np = nullptr;
+  a.np = np;  // pending flags (new ids) for pull expansion
   a.written = written;
   a.pend_low = pl;
   a.pend_high = ph;
   a.red = red;
-  a.chunks = s.chunks;
-  a.n_chunks = s.n_chunks;
-  a.multi = s.multi;
-  a.n_multi = s.n_multi;
-  a.partials = s.partials;
 
   dynpr_stats res{};
   int cur = 0;  // R[cur] holds the latest iterate ("previous")
   for (int iter = 0; iter < c.max_iterations; ++iter) {
     DYNPR_CK(cudaMemsetAsync(red, 0, sizeof(SweepRed), st));
     if (obs && sp.flagged) {
-      DYNPR_CK(cudaMemcpyAsync(h_flags.data(), va, n, cudaMemcpyDeviceToHost, st));
+      launch_scatter_inv_u8(ctx, L, va, obs_flags);
+      DYNPR_CK(cudaMemcpyAsync(h_flags.data(), obs_flags, n, cudaMemcpyDeviceToHost, st));
     }
     a.rank_prev = R[cur];
     a.rank_cur = R[cur ^ 1];
     a.contrib_prev = CB[cur];
     a.contrib_cur = CB[cur ^ 1];
     if (ctx->profiling) DYNPR_CK(cudaEventRecord(ctx->ev_s0, st));
-    launch_sweep(ctx, a, sp.flagged, sp.closed, s.n_low);
+    launch_sweep(ctx, a, sp.flagged, sp.closed);
     if (ctx->profiling) DYNPR_CK(cudaEventRecord(ctx->ev_s1, st));
     const SweepRed r = read_red(ctx, red);
     if (ctx->profiling) {
@@ -193,7 +196,8 @@ void solve(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynpr_sta
     res.processed_edges += r.edges;
     res.final_delta = delta;
     if (obs) {
-      DYNPR_CK(cudaMemcpyAsync(h_ranks.data(), R[cur], (size_t)n * 8, cudaMemcpyDeviceToHost, st));
+      launch_scatter_inv_f64(ctx, L, R[cur], obs_ranks);
+      DYNPR_CK(cudaMemcpyAsync(h_ranks.data(), obs_ranks, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
       sync(ctx);
       obs(res.iterations, h_ranks.data(), sp.flagged ? h_flags.data() : nullptr, n, user);
     }
@@ -201,10 +205,25 @@ void solve(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynpr_sta
       res.converged = 1;
       break;
     }
-    if (sp.flagged) launch_expand(ctx, gF, va, pl, r.pend_low, ph, r.pend_high);  // engine.cpp:91
+    if (sp.flagged) {  // expandAffected (engine.cpp:91), direction-optimising
+      // push touches the pending vertices' out-edges; pull scans at most
+      // the in-edges of the vertices that were not processed this sweep
+      const uint64_t pull_bound = gT->m > r.edges ? gT->m - r.edges : 0;
+      if (r.pend_edges > pull_bound) {
+        launch_pull_expand(ctx, a);
+        ctx->pull_expansions += 1;
+      } else {
+        launch_expand(ctx, L->offF, L->tgtF, va, pl, r.pend_low, ph, r.pend_high);
+      }
+    }
   }
+  // result back to old ids (R[cur ^ 1] is free and receives the permuted copy
+  // when the caller's buffer is on the host)
+  const bool host_out = !is_device_ptr(ranks_out);
+  double* out_dev = host_out ? R[cur ^ 1] : ranks_out;
+  launch_scatter_inv_f64(ctx, L, R[cur], out_dev);
   DYNPR_CK(cudaEventRecord(ctx->ev_b, st));
-  DYNPR_CK(cudaMemcpyAsync(ranks_out, R[cur], (size_t)n * 8, cudaMemcpyDefault, st));
+  if (host_out) DYNPR_CK(cudaMemcpyAsync(ranks_out, out_dev, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
   sync(ctx);
   float ms = 0.f;
   DYNPR_CK(cudaEventElapsedTime(&ms, ctx->ev_a, ctx->ev_b));
@@ -250,6 +269,11 @@ dynpr_status dynpr_context_create(int device, dynpr_context** out) {
     try {
       DYNPR_CK(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
       DYNPR_CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+      // keep freed snapshot memory reserved in the stream-ordered pool
+      cudaMemPool_t pool;
+      DYNPR_CK(cudaDeviceGetDefaultMemPool(&pool, device));
+      uint64_t keep = ~0ull;
+      DYNPR_CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
       DYNPR_CK(cudaEventCreate(&ctx->ev_a));
       DYNPR_CK(cudaEventCreate(&ctx->ev_b));
       DYNPR_CK(cudaEventCreate(&ctx->ev_s0));
@@ -306,9 +330,20 @@ dynpr_status dynpr_partition_by_degree(dynpr_context* ctx, const dynpr_graph* g,
     if (!ctx || !g || !low_count) invalid("null argument");
     bind_device(ctx);
     StageOut<uint32_t> o(ctx, ctx->stage_a, order, g->n);
-    Schedule s = build_schedule(ctx, g, threshold, g->n ? o.dev : nullptr, false);
+    Schedule s = build_partition(ctx, g, threshold, g->n ? o.dev : nullptr);
     o.commit();
     *low_count = s.n_low;
+  });
+}
+
+dynpr_status dynpr_graph_prepare(dynpr_context* ctx, const dynpr_graph* gT, const dynpr_graph* gF,
+                                 uint32_t threshold, int with_forward, double* build_ms) {
+  return api_guard([&] {
+    if (!ctx) invalid("null context");
+    check_pair(gT, gF);
+    bind_device(ctx);
+    const Layout* L = get_layout(ctx, gT, gF, threshold, with_forward != 0);
+    if (build_ms) *build_ms = L->build_ms;
   });
 }
 
@@ -322,59 +357,52 @@ dynpr_status dynpr_update_ranks(dynpr_context* ctx, const dynpr_graph* gT, const
     bind_device(ctx);
     const uint32_t n = gT->n;
     if (n == 0) return;
+    if (gF->n != n) invalid("engine: graph pair is not mutually transposed (count mismatch)");
+    const Layout* L = get_layout(ctx, gT, gF, cfg->low_degree_threshold, false);
     const double* prev = stage_in(ctx, ctx->stage_b, previous, n);
     double* R0 = ctx->rank[0].as<double>(n);
+    double* R1 = ctx->rank[1].as<double>(n);
     double* C0 = ctx->contrib[0].as<double>(n);
-    DYNPR_CK(cudaMemcpyAsync(R0, prev, (size_t)n * 8, cudaMemcpyDeviceToDevice, ctx->stream));
-    launch_init_ranks(ctx, gF, R0, 0.0, R0, nullptr, C0, nullptr);
-    StageOut<double> out(ctx, ctx->rank[1], current, n);
+    launch_gather_perm_f64(ctx, L, prev, R0);
+    launch_init_ranks(ctx, L, R0, 0.0, R0, nullptr, C0, nullptr);
     const bool flagged = vertex_affected != nullptr;
-    uint8_t *va = nullptr, *np = nullptr;
-    bool host_flags = false;
+    uint8_t* va = nullptr;
+    uint8_t* np = nullptr;
+    uint8_t* flag_old = nullptr;
     if (flagged) {
-      host_flags = !is_device_ptr(vertex_affected);
-      if (host_flags) {
-        va = ctx->flags_va.as<uint8_t>(n);
-        np = ctx->flags_np.as<uint8_t>(n);
-        DYNPR_CK(cudaMemcpyAsync(va, vertex_affected, n, cudaMemcpyHostToDevice, ctx->stream));
-        DYNPR_CK(cudaMemcpyAsync(np, neighbors_pending, n, cudaMemcpyHostToDevice, ctx->stream));
-      } else {
-        va = vertex_affected;
-        np = neighbors_pending;
-      }
+      va = ctx->flags_va.as<uint8_t>(n);
+      np = ctx->flags_written.as<uint8_t>(n);
+      flag_old = ctx->flags_np.as<uint8_t>(2ull * n);
+      DYNPR_CK(cudaMemcpyAsync(flag_old, vertex_affected, n, cudaMemcpyDefault, ctx->stream));
+      DYNPR_CK(cudaMemcpyAsync(flag_old + n, neighbors_pending, n, cudaMemcpyDefault, ctx->stream));
+      launch_gather_perm_u8(ctx, L, flag_old, va);
+      launch_gather_perm_u8(ctx, L, flag_old + n, np);
     }
-    const Schedule s = build_schedule(ctx, gT, cfg->low_degree_threshold, nullptr, true);
     SweepRed* red = ctx->red.as<SweepRed>(2);
     DYNPR_CK(cudaMemsetAsync(red, 0, sizeof(SweepRed), ctx->stream));
-    SweepArgs a{};
-    a.offT = gT->off;
-    a.idxT = gT->tgt;
-    a.offF = gF->off;
-    a.n = n;
-    a.T = cfg->low_degree_threshold;
+    SweepArgs a = layout_args(L, ctx->partials.as<double>(L->n_mseg + 1));
     a.alpha = cfg->damping_factor;
     a.teleport = (1.0 - cfg->damping_factor) / (double)n;
     a.tf = cfg->frontier_tolerance;
     a.tp = cfg->prune_tolerance;
     a.rank_prev = R0;
-    a.rank_cur = out.dev;
+    a.rank_cur = R1;
     a.contrib_prev = C0;
     a.contrib_cur = nullptr;
     a.va = va;
     a.np = np;
     a.written = nullptr;
     a.red = red;
-    a.chunks = s.chunks;
-    a.n_chunks = s.n_chunks;
-    a.multi = s.multi;
-    a.n_multi = s.n_multi;
-    a.partials = s.partials;
     a.np_accumulate = 1;
     a.copy_all = 1;
-    launch_sweep(ctx, a, flagged, mode == DYNPR_RANK_CLOSED_LOOP_PRUNE, s.n_low);
-    if (flagged && host_flags) {
-      DYNPR_CK(cudaMemcpyAsync(vertex_affected, va, n, cudaMemcpyDeviceToHost, ctx->stream));
-      DYNPR_CK(cudaMemcpyAsync(neighbors_pending, np, n, cudaMemcpyDeviceToHost, ctx->stream));
+    launch_sweep(ctx, a, flagged, mode == DYNPR_RANK_CLOSED_LOOP_PRUNE);
+    StageOut<double> out(ctx, ctx->stage_c, current, n);
+    launch_scatter_inv_f64(ctx, L, R1, out.dev);
+    if (flagged) {
+      launch_scatter_inv_u8(ctx, L, va, flag_old);
+      launch_scatter_inv_u8(ctx, L, np, flag_old + n);
+      DYNPR_CK(cudaMemcpyAsync(vertex_affected, flag_old, n, cudaMemcpyDefault, ctx->stream));
+      DYNPR_CK(cudaMemcpyAsync(neighbors_pending, flag_old + n, n, cudaMemcpyDefault, ctx->stream));
     }
     out.commit();
   });
@@ -431,7 +459,7 @@ dynpr_status dynpr_initial_affected(dynpr_context* ctx, const dynpr_graph* g, co
       DYNPR_CK(cudaMemsetAsync(va.dev, 0, n, ctx->stream));
       DYNPR_CK(cudaMemsetAsync(np.dev, 0, n, ctx->stream));
     }
-    launch_init_affected(ctx, g, ds, dd, n_del, is, n_ins, va.dev, np.dev, 0, nullptr, nullptr, nullptr);
+    launch_init_affected(ctx, nullptr, ds, dd, n_del, is, n_ins, va.dev, np.dev);
     va.commit();
     np.commit();
   });
@@ -448,13 +476,13 @@ dynpr_status dynpr_expand_affected(dynpr_context* ctx, const dynpr_graph* g, uin
     StageOut<uint8_t> va(ctx, ctx->flags_va, vertex_affected, n);
     if (va.host)
       DYNPR_CK(cudaMemcpyAsync(va.dev, vertex_affected, n, cudaMemcpyHostToDevice, ctx->stream));
-    uint32_t* pl = ctx->pend_low.as<uint32_t>(n);
-    uint32_t* ph = ctx->pend_high.as<uint32_t>(n);
+    uint32_t* pl = ctx->pend_low.as<uint32_t>((uint64_t)n + 1);
+    uint2* ph = ctx->pend_high.as<uint2>((uint64_t)n + g->m / kExpandChunk + 1);
     SweepRed* red = ctx->red.as<SweepRed>(2);
     DYNPR_CK(cudaMemsetAsync(red, 0, sizeof(SweepRed), ctx->stream));
-    launch_collect_pending(ctx, g, np, threshold, pl, ph, red);
+    launch_collect_pending(ctx, nullptr, g->off, n, np, threshold, pl, ph, red);
     const SweepRed r = read_red(ctx, red);
-    launch_expand(ctx, g, va.dev, pl, r.pend_low, ph, r.pend_high);
+    launch_expand(ctx, g->off, g->tgt, va.dev, pl, r.pend_low, ph, r.pend_high);
     va.commit();
   });
 }

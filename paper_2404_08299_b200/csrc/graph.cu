@@ -12,9 +12,12 @@
 //                                      touched ones
 // Every result is byte-identical to the reference CsrGraph (sorted,
 // deduplicated slices) and validation errors carry the reference messages.
+#include <atomic>
+
 #include <cub/cub.cuh>
 
 #include "common.cuh"
+#include "layout.cuh"
 
 namespace dynpr_b200 {
 
@@ -399,25 +402,33 @@ bool any_bad_ids(dynpr_context* ctx, const uint32_t* d_s, const uint32_t* d_d, u
 }
 
 // ---------------------------------------------------------------------------
-dynpr_graph* make_graph(dynpr_context* ctx, uint32_t n, uint64_t m) {
+dynpr_graph* new_graph_struct(dynpr_context* ctx, uint32_t n) {
+  static std::atomic<uint64_t> next_id{1};
   auto* g = new dynpr_graph();
+  g->id = next_id.fetch_add(1);
   g->ctx = ctx;
   g->n = n;
+  return g;
+}
+
+dynpr_graph* make_graph(dynpr_context* ctx, uint32_t n, uint64_t m) {
+  dynpr_graph* g = new_graph_struct(ctx, n);
   g->m = m;
-  cudaError_t e1 = cudaMalloc(&g->off, ((size_t)n + 1) * sizeof(uint64_t));
-  cudaError_t e2 = cudaMalloc(&g->tgt, (m ? m : 1) * sizeof(uint32_t));
-  if (e1 != cudaSuccess || e2 != cudaSuccess) {
+  try {
+    g->off = pool_alloc_n<uint64_t>(ctx, (uint64_t)n + 1);
+    g->tgt = pool_alloc_n<uint32_t>(ctx, m ? m : 1);
+  } catch (...) {
     destroy_graph(g);
-    cudaGetLastError();
-    throw Error(DYNPR_OUT_OF_MEMORY, "device allocation of CSR arrays failed");
+    throw;
   }
   return g;
 }
 
 void destroy_graph(dynpr_graph* g) {
   if (!g) return;
-  if (g->off) cudaFree(g->off);
-  if (g->tgt) cudaFree(g->tgt);
+  if (g->layout) destroy_layout(g->layout);
+  pool_free(g->ctx, g->off);
+  pool_free(g->ctx, g->tgt);
   delete g;
 }
 
@@ -529,10 +540,13 @@ void graph_apply_batch_impl(dynpr_context* ctx, const dynpr_graph* g,
     count_launch(ctx);
   }
   // new offsets
-  dynpr_graph* r = new dynpr_graph();
-  r->ctx = ctx;
-  r->n = n;
-  DYNPR_CK(cudaMalloc(&r->off, ((size_t)n + 1) * sizeof(uint64_t)));
+  dynpr_graph* r = new_graph_struct(ctx, n);
+  try {
+    r->off = pool_alloc_n<uint64_t>(ctx, (uint64_t)n + 1);
+  } catch (...) {
+    destroy_graph(r);
+    throw;
+  }
   k_new_degrees<<<grid_for((uint64_t)n + 1, 256, 1 << 16), 256, 0, st>>>(g->off, n, ddel, dins, need, r->off);
   check_launch();
   count_launch(ctx);
@@ -544,11 +558,11 @@ void graph_apply_batch_impl(dynpr_context* ctx, const dynpr_graph* g,
   sync(ctx);
   std::memcpy(&m_new, ctx->pinned, 8);
   r->m = m_new;
-  cudaError_t e = cudaMalloc(&r->tgt, (m_new ? m_new : 1) * sizeof(uint32_t));
-  if (e != cudaSuccess) {
+  try {
+    r->tgt = pool_alloc_n<uint32_t>(ctx, m_new ? m_new : 1);
+  } catch (...) {
     destroy_graph(r);
-    cudaGetLastError();
-    throw Error(DYNPR_OUT_OF_MEMORY, "device allocation of CSR targets failed");
+    throw;
   }
   // compact present deletions / fresh insertions
   uint64_t* dp = ctx->stage_d.as<uint64_t>(ndu + 1);

@@ -1,0 +1,356 @@
+// Builder of the engine layout (see layout.cuh): degree sort, relabelling,
+// SELL-32 segment slices, relabelled forward CSR.
+#include <cub/cub.cuh>
+
+#include "layout.cuh"
+
+namespace dynpr_b200 {
+
+namespace {
+
+template <class F>
+void cub_call(dynpr_context* ctx, F&& f) {
+  size_t bytes = 0;
+  DYNPR_CK(f(nullptr, bytes));
+  void* tmp = ctx->cub_tmp.ensure(bytes);
+  DYNPR_CK(f(tmp, bytes));
+}
+
+dynpr_context* g_alloc_ctx = nullptr;  // set for the duration of a build
+template <class T>
+T* dalloc(uint64_t count) {
+  return pool_alloc_n<T>(g_alloc_ctx, count ? count : 1);
+}
+
+#define GRID_STRIDE(i, count)                                                      \
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < (count); \
+       i += (uint64_t)gridDim.x * blockDim.x)
+
+__global__ void k_degrees_keys(const uint64_t* offT, const uint64_t* offF, uint32_t n, uint32_t* indeg_old,
+                               uint32_t* outdeg_old, uint32_t* iota) {
+  GRID_STRIDE(v, n) {
+    indeg_old[v] = (uint32_t)(offT[v + 1] - offT[v]);
+    outdeg_old[v] = (uint32_t)(offF[v + 1] - offF[v]);
+    iota[v] = (uint32_t)v;
+  }
+}
+__global__ void k_desc_keys(const uint32_t* deg, uint32_t n, uint32_t maxdeg, uint32_t* keys) {
+  GRID_STRIDE(v, n) keys[v] = maxdeg - deg[v];
+}
+__global__ void k_relabel(const uint32_t* perm, uint32_t n, const uint32_t* indeg_old, const uint32_t* outdeg_old,
+                          uint32_t* inv, uint32_t* indeg, uint32_t* outdeg) {
+  GRID_STRIDE(i, n) {
+    const uint32_t o = perm[i];
+    inv[o] = (uint32_t)i;
+    indeg[i] = indeg_old[o];
+    outdeg[i] = outdeg_old[o];
+  }
+}
+// M = number of vertices with in-degree > thr (a prefix: degrees descend)
+__global__ void k_count_above(const uint32_t* indeg, uint32_t n, uint32_t thr, unsigned* out) {
+  unsigned c = 0;
+  GRID_STRIDE(i, n) c += indeg[i] > thr;
+  c = warp_sum(c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+// single region: slice lengths (x32) for the exclusive scan
+__global__ void k_single_slice_len(const uint32_t* indeg, uint32_t M, uint32_t n, uint64_t S, uint64_t* len32) {
+  GRID_STRIDE(s, S + 1) len32[s] = s < S ? 32ull * indeg[M + 32 * s] : 0ull;
+}
+// multi region: chunk counts per multi vertex
+__global__ void k_multi_nch(const uint32_t* indeg, uint32_t M, uint32_t* nch) {
+  GRID_STRIDE(v, (uint64_t)M + 1) nch[v] = v < M ? (indeg[v] + 255u) / 256u : 0u;
+}
+__global__ void k_multi_segments(const uint32_t* indeg, uint32_t M, const uint32_t* pbase, uint32_t* mseg_v,
+                                 uint32_t* mseg_len) {
+  GRID_STRIDE(v, M) {
+    const uint32_t d = indeg[v], b = pbase[v];
+    const uint32_t nch = (d + 255u) / 256u;
+    for (uint32_t j = 0; j < nch; ++j) {
+      mseg_v[b + j] = (uint32_t)v;
+      mseg_len[b + j] = (j + 1 < nch) ? 256u : d - 256u * j;
+    }
+  }
+}
+__global__ void k_multi_slice_len(const uint32_t* mseg_len, uint64_t nseg, uint64_t S, uint64_t* len32) {
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / 32;
+  const unsigned lane = threadIdx.x & 31;
+  const uint64_t nw = (uint64_t)gridDim.x * blockDim.x / 32;
+  for (uint64_t s = warp; s <= S; s += nw) {
+    const uint64_t seg = s * 32 + lane;
+    const unsigned l = (s < S && seg < nseg) ? mseg_len[seg] : 0u;
+    const unsigned mx = __reduce_max_sync(0xffffffffu, l);
+    if (lane == 0) len32[s] = 32ull * mx;
+  }
+}
+// SELL fill, single region: warp per slice, lane per vertex
+__global__ void k_fill_single(const uint64_t* offT, const uint32_t* tgtT, const uint32_t* perm, const uint32_t* inv,
+                              const uint32_t* indeg, uint32_t M, uint32_t n, uint64_t S, const uint64_t* sbase,
+                              uint32_t* sell) {
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / 32;
+  const unsigned lane = threadIdx.x & 31;
+  const uint64_t nw = (uint64_t)gridDim.x * blockDim.x / 32;
+  for (uint64_t s = warp; s < S; s += nw) {
+    const uint64_t vn = M + s * 32 + lane;
+    const bool valid = vn < n;
+    const uint32_t deg = valid ? indeg[vn] : 0u;
+    const uint64_t src = valid ? offT[perm[vn]] : 0;
+    const uint64_t base = sbase[s];
+    const uint32_t L = (uint32_t)((sbase[s + 1] - base) / 32);
+    for (uint32_t k = 0; k < L; ++k) sell[base + 32ull * k + lane] = k < deg ? inv[tgtT[src + k]] : 0u;
+  }
+}
+// SELL fill, multi region: warp per slice, lane per 256-edge segment
+__global__ void k_fill_multi(const uint64_t* offT, const uint32_t* tgtT, const uint32_t* perm, const uint32_t* inv,
+                             const uint32_t* pbase, const uint32_t* mseg_v, const uint32_t* mseg_len, uint64_t nseg,
+                             uint64_t S, const uint64_t* mbase, uint32_t* sell) {
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / 32;
+  const unsigned lane = threadIdx.x & 31;
+  const uint64_t nw = (uint64_t)gridDim.x * blockDim.x / 32;
+  for (uint64_t s = warp; s < S; s += nw) {
+    const uint64_t seg = s * 32 + lane;
+    const bool valid = seg < nseg;
+    uint32_t len = 0;
+    uint64_t src = 0;
+    if (valid) {
+      const uint32_t v = mseg_v[seg];
+      len = mseg_len[seg];
+      src = offT[perm[v]] + 256ull * (seg - pbase[v]);
+    }
+    const uint64_t base = mbase[s];
+    const uint32_t L = (uint32_t)((mbase[s + 1] - base) / 32);
+    for (uint32_t k = 0; k < L; ++k) sell[base + 32ull * k + lane] = k < len ? inv[tgtT[src + k]] : 0u;
+  }
+}
+// relabelled forward CSR: warp per new vertex
+__global__ void k_outdeg64(const uint32_t* outdeg, uint32_t n, uint64_t* off) {
+  GRID_STRIDE(v, (uint64_t)n + 1) off[v] = v < n ? outdeg[v] : 0ull;
+}
+__global__ void k_fill_forward(const uint64_t* offF, const uint32_t* tgtF, const uint32_t* perm, const uint32_t* inv,
+                               uint32_t n, const uint64_t* noff, uint32_t* ntgt) {
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / 32;
+  const unsigned lane = threadIdx.x & 31;
+  const uint64_t nw = (uint64_t)gridDim.x * blockDim.x / 32;
+  for (uint64_t v = warp; v < n; v += nw) {
+    const uint64_t src = offF[perm[v]], d = noff[v], len = noff[v + 1] - d;
+    for (uint64_t k = lane; k < len; k += 32) ntgt[d + k] = inv[tgtF[src + k]];
+  }
+}
+
+__global__ void k_gather_perm_f64(const uint32_t* perm, uint32_t n, const double* src, double* dst) {
+  GRID_STRIDE(i, n) dst[i] = src[perm[i]];
+}
+__global__ void k_gather_perm_u8(const uint32_t* perm, uint32_t n, const uint8_t* src, uint8_t* dst) {
+  GRID_STRIDE(i, n) dst[i] = src[perm[i]];
+}
+__global__ void k_scatter_inv_f64(const uint32_t* inv, uint32_t n, const double* src, double* dst) {
+  GRID_STRIDE(o, n) dst[o] = src[inv[o]];
+}
+__global__ void k_scatter_inv_u8(const uint32_t* inv, uint32_t n, const uint8_t* src, uint8_t* dst) {
+  GRID_STRIDE(o, n) dst[o] = src[inv[o]];
+}
+
+unsigned grid(dynpr_context* ctx, uint64_t items) { return grid_for(items, 256, ctx->num_sms * 32); }
+
+uint64_t read_u64(dynpr_context* ctx, const void* d) {
+  uint64_t h = 0;
+  DYNPR_CK(cudaMemcpyAsync(ctx->pinned, d, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  sync(ctx);
+  std::memcpy(&h, ctx->pinned, 8);
+  return h;
+}
+
+void build_forward(dynpr_context* ctx, Layout* L, const dynpr_graph* gF) {
+  cudaStream_t st = ctx->stream;
+  g_alloc_ctx = ctx;
+  L->offF = dalloc<uint64_t>((uint64_t)L->n + 1);
+  L->tgtF = dalloc<uint32_t>(L->m);
+  k_outdeg64<<<grid(ctx, (uint64_t)L->n + 1), 256, 0, st>>>(L->outdeg, L->n, L->offF);
+  check_launch();
+  cub_call(ctx, [&](void* t, size_t& b) {
+    return cub::DeviceScan::ExclusiveSum(t, b, L->offF, L->offF, (int64_t)L->n + 1, st);
+  });
+  k_fill_forward<<<grid(ctx, (uint64_t)L->n * 32), 256, 0, st>>>(gF->off, gF->tgt, L->perm, L->inv, L->n, L->offF,
+                                                                 L->tgtF);
+  check_launch();
+  count_launch(ctx, 2);
+  L->has_forward = true;
+}
+
+Layout* build_layout(dynpr_context* ctx, const dynpr_graph* gT, const dynpr_graph* gF, uint32_t T) {
+  cudaStream_t st = ctx->stream;
+  const uint32_t n = gT->n;
+  auto* L = new Layout();
+  L->ctx = ctx;
+  g_alloc_ctx = ctx;
+  uint32_t* tmp = nullptr;
+  try {
+    L->n = n;
+    L->m = gT->m;
+    L->T = T;
+    L->gF_id = gF->id;
+    L->perm = dalloc<uint32_t>(n);
+    L->inv = dalloc<uint32_t>(n);
+    L->indeg = dalloc<uint32_t>(n);
+    L->outdeg = dalloc<uint32_t>(n);
+    // temporaries from the pool (the context's stage buffers may hold the
+    // caller's staged inputs when the build happens inside an engine call)
+    tmp = dalloc<uint32_t>(5ull * ((uint64_t)n + 1));
+    uint32_t* indeg_old = tmp;
+    uint32_t* outdeg_old = tmp + (n + 1ull);
+    uint32_t* keys = tmp + 2ull * (n + 1ull);
+    uint32_t* keys2 = tmp + 3ull * (n + 1ull);
+    uint32_t* iota = tmp + 4ull * (n + 1ull);
+    k_degrees_keys<<<grid(ctx, n), 256, 0, st>>>(gT->off, gF->off, n, indeg_old, outdeg_old, iota);
+    check_launch();
+    // max in-degree -> descending sort keys
+    auto* mx = reinterpret_cast<uint32_t*>(ctx->scratch64a.as<unsigned long long>(2));
+    cub_call(ctx, [&](void* t, size_t& b) { return cub::DeviceReduce::Max(t, b, indeg_old, mx, (int64_t)n, st); });
+    const uint32_t maxdeg = (uint32_t)(read_u64(ctx, mx) & 0xffffffffu);
+    k_desc_keys<<<grid(ctx, n), 256, 0, st>>>(indeg_old, n, maxdeg, keys);
+    check_launch();
+    count_launch(ctx, 2);
+    const int eb = bits_for(maxdeg);
+    if (eb > 0) {
+      cub::DoubleBuffer<uint32_t> kb(keys, keys2);
+      cub::DoubleBuffer<uint32_t> vb(iota, L->perm);
+      cub_call(ctx, [&](void* t, size_t& b) {
+        return cub::DeviceRadixSort::SortPairs(t, b, kb, vb, (int64_t)n, 0, eb, st);
+      });
+      if (vb.Current() != L->perm)
+        DYNPR_CK(cudaMemcpyAsync(L->perm, vb.Current(), (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
+    } else {
+      DYNPR_CK(cudaMemcpyAsync(L->perm, iota, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
+    }
+    k_relabel<<<grid(ctx, n), 256, 0, st>>>(L->perm, n, indeg_old, outdeg_old, L->inv, L->indeg, L->outdeg);
+    check_launch();
+    // multi vertices: in-degree > max(T, 256)
+    const uint32_t thr = T > 256u ? T : 256u;
+    auto* cnt = reinterpret_cast<unsigned*>(ctx->scratch64a.as<unsigned long long>(2));
+    DYNPR_CK(cudaMemsetAsync(cnt, 0, 8, st));
+    k_count_above<<<grid(ctx, n), 256, 0, st>>>(L->indeg, n, thr, cnt);
+    check_launch();
+    count_launch(ctx, 2);
+    L->M = (uint32_t)(read_u64(ctx, cnt) & 0xffffffffu);
+    const uint32_t M = L->M;
+    // single region slices
+    L->n_sslices = ((uint64_t)(n - M) + 31) / 32;
+    L->sbase = dalloc<uint64_t>(L->n_sslices + 1);
+    k_single_slice_len<<<grid(ctx, L->n_sslices + 1), 256, 0, st>>>(L->indeg, M, n, L->n_sslices, L->sbase);
+    check_launch();
+    cub_call(ctx, [&](void* t, size_t& b) {
+      return cub::DeviceScan::ExclusiveSum(t, b, L->sbase, L->sbase, (int64_t)L->n_sslices + 1, st);
+    });
+    const uint64_t sell_s_len = read_u64(ctx, L->sbase + L->n_sslices);
+    L->sell_s = dalloc<uint32_t>(sell_s_len);
+    // multi region segments
+    L->pbase = dalloc<uint32_t>((uint64_t)M + 1);
+    k_multi_nch<<<grid(ctx, (uint64_t)M + 1), 256, 0, st>>>(L->indeg, M, L->pbase);
+    check_launch();
+    cub_call(ctx, [&](void* t, size_t& b) {
+      return cub::DeviceScan::ExclusiveSum(t, b, L->pbase, L->pbase, (int64_t)M + 1, st);
+    });
+    {
+      uint32_t h = 0;  // pbase is uint32: read exactly 4 bytes
+      DYNPR_CK(cudaMemcpyAsync(ctx->pinned, L->pbase + M, 4, cudaMemcpyDeviceToHost, st));
+      sync(ctx);
+      std::memcpy(&h, ctx->pinned, 4);
+      L->n_mseg = h;
+    }
+    L->mseg_v = dalloc<uint32_t>(L->n_mseg);
+    L->mseg_len = dalloc<uint32_t>(L->n_mseg);
+    L->n_mslices = (L->n_mseg + 31) / 32;
+    L->mbase = dalloc<uint64_t>(L->n_mslices + 1);
+    if (M) {
+      k_multi_segments<<<grid(ctx, M), 256, 0, st>>>(L->indeg, M, L->pbase, L->mseg_v, L->mseg_len);
+      check_launch();
+    }
+    k_multi_slice_len<<<grid(ctx, (L->n_mslices + 1) * 32), 256, 0, st>>>(L->mseg_len, L->n_mseg, L->n_mslices,
+                                                                          L->mbase);
+    check_launch();
+    cub_call(ctx, [&](void* t, size_t& b) {
+      return cub::DeviceScan::ExclusiveSum(t, b, L->mbase, L->mbase, (int64_t)L->n_mslices + 1, st);
+    });
+    const uint64_t sell_m_len = read_u64(ctx, L->mbase + L->n_mslices);
+    L->sell_m = dalloc<uint32_t>(sell_m_len);
+    if (L->n_sslices) {
+      k_fill_single<<<grid(ctx, L->n_sslices * 32), 256, 0, st>>>(gT->off, gT->tgt, L->perm, L->inv, L->indeg, M, n,
+                                                                 L->n_sslices, L->sbase, L->sell_s);
+      check_launch();
+    }
+    if (L->n_mslices) {
+      k_fill_multi<<<grid(ctx, L->n_mslices * 32), 256, 0, st>>>(gT->off, gT->tgt, L->perm, L->inv, L->pbase,
+                                                                L->mseg_v, L->mseg_len, L->n_mseg, L->n_mslices,
+                                                                L->mbase, L->sell_m);
+      check_launch();
+    }
+    count_launch(ctx, 6);
+    pool_free(ctx, tmp);
+  } catch (...) {
+    pool_free(ctx, tmp);
+    destroy_layout(L);
+    throw;
+  }
+  return L;
+}
+
+}  // namespace
+
+Layout::~Layout() {
+  for (void* p : {(void*)perm, (void*)inv, (void*)indeg, (void*)outdeg, (void*)sbase, (void*)sell_s, (void*)mbase,
+                  (void*)mseg_v, (void*)mseg_len, (void*)pbase, (void*)sell_m, (void*)offF, (void*)tgtF})
+    pool_free(ctx, p);
+}
+
+void destroy_layout(Layout* L) { delete L; }
+
+Layout* get_layout(dynpr_context* ctx, const dynpr_graph* gT, const dynpr_graph* gF, uint32_t T, bool need_forward) {
+  Layout* L = gT->layout;
+  if (!L || L->gF_id != gF->id || L->T != T) {
+    if (L) {
+      destroy_layout(L);
+      const_cast<dynpr_graph*>(gT)->layout = nullptr;
+    }
+    DYNPR_CK(cudaEventRecord(ctx->ev_s0, ctx->stream));
+    L = build_layout(ctx, gT, gF, T);
+    const_cast<dynpr_graph*>(gT)->layout = L;
+    DYNPR_CK(cudaEventRecord(ctx->ev_s1, ctx->stream));
+    sync(ctx);
+    float ms = 0.f;
+    DYNPR_CK(cudaEventElapsedTime(&ms, ctx->ev_s0, ctx->ev_s1));
+    L->build_ms = ms;
+  }
+  if (need_forward && !L->has_forward) {
+    DYNPR_CK(cudaEventRecord(ctx->ev_s0, ctx->stream));
+    build_forward(ctx, L, gF);
+    DYNPR_CK(cudaEventRecord(ctx->ev_s1, ctx->stream));
+    sync(ctx);
+    float ms = 0.f;
+    DYNPR_CK(cudaEventElapsedTime(&ms, ctx->ev_s0, ctx->ev_s1));
+    L->build_ms += ms;
+  }
+  return L;
+}
+
+void launch_gather_perm_f64(dynpr_context* ctx, const Layout* L, const double* src, double* dst) {
+  k_gather_perm_f64<<<grid(ctx, L->n), 256, 0, ctx->stream>>>(L->perm, L->n, src, dst);
+  check_launch();
+  count_launch(ctx);
+}
+void launch_gather_perm_u8(dynpr_context* ctx, const Layout* L, const uint8_t* src, uint8_t* dst) {
+  k_gather_perm_u8<<<grid(ctx, L->n), 256, 0, ctx->stream>>>(L->perm, L->n, src, dst);
+  check_launch();
+  count_launch(ctx);
+}
+void launch_scatter_inv_f64(dynpr_context* ctx, const Layout* L, const double* src, double* dst) {
+  k_scatter_inv_f64<<<grid(ctx, L->n), 256, 0, ctx->stream>>>(L->inv, L->n, src, dst);
+  check_launch();
+  count_launch(ctx);
+}
+void launch_scatter_inv_u8(dynpr_context* ctx, const Layout* L, const uint8_t* src, uint8_t* dst) {
+  k_scatter_inv_u8<<<grid(ctx, L->n), 256, 0, ctx->stream>>>(L->inv, L->n, src, dst);
+  check_launch();
+  count_launch(ctx);
+}
+
+}  // namespace dynpr_b200

@@ -1,0 +1,72 @@
+// Engine layout of a (gT, gF) graph pair: the device format the sweep
+// kernels read.  Built once per immutable graph snapshot and cached on the
+// transpose handle (keyed by the forward graph's id and the degree
+// threshold), like the CSR itself.
+//
+//  * Vertices are relabelled: new id = rank of the vertex when sorted by
+//    in-degree descending (stable by old id).  Per-vertex arrays (ranks,
+//    contributions, flags, degrees) live in new-id order, so the hot,
+//    high-degree vertices -- whose contributions are gathered most -- are
+//    packed at the front of the contribution vector (L2 locality).
+//  * Every vertex's in-neighbour list is split into the reference's
+//    accumulation segments (rank.cpp:42-75): one flat segment when
+//    in-degree <= max(T, 256), else 256-edge chunks ("multi" vertices,
+//    the prefix [0, M) of new ids).
+//  * Segments are stored SELL-32 (sliced ELLPACK, slice = one warp): element
+//    k of the 32 segments of slice s sits at base[s] + 32*k + lane, column ids
+//    already relabelled, each segment keeping the reference's ascending-old-id
+//    order.  A warp walks 32 segments in lock step with fully coalesced index
+//    loads and every lane sums its own segment in order -- the reference's
+//    accumulation order, bit for bit, with no shared-memory staging.
+//  * For the frontier engines the forward graph is also relabelled (rows and
+//    columns) for push expansion in new-id space.
+#pragma once
+
+#include "common.cuh"
+
+namespace dynpr_b200 {
+
+struct Layout {
+  dynpr_context* ctx = nullptr;
+  uint32_t n = 0;
+  uint64_t m = 0;
+  uint32_t T = 0;
+  uint64_t gF_id = 0;
+  uint32_t* perm = nullptr;    // new -> old
+  uint32_t* inv = nullptr;     // old -> new
+  uint32_t* indeg = nullptr;   // new order
+  uint32_t* outdeg = nullptr;  // new order
+  uint32_t M = 0;              // multi-segment vertices are [0, M)
+  // single-segment region: vertices [M, n), slice s = vertices M+32s..+31
+  uint64_t n_sslices = 0;
+  uint64_t* sbase = nullptr;   // n_sslices + 1
+  uint32_t* sell_s = nullptr;
+  // multi region: segments in (vertex, chunk) order
+  uint64_t n_mseg = 0;
+  uint64_t n_mslices = 0;
+  uint64_t* mbase = nullptr;   // n_mslices + 1
+  uint32_t* mseg_v = nullptr;  // vertex of segment
+  uint32_t* mseg_len = nullptr;
+  uint32_t* pbase = nullptr;   // first segment of multi vertex v (M + 1)
+  uint32_t* sell_m = nullptr;
+  // relabelled forward CSR (frontier engines)
+  bool has_forward = false;
+  uint64_t* offF = nullptr;
+  uint32_t* tgtF = nullptr;
+  double build_ms = 0.0;       // device time of the last (re)build
+  ~Layout();
+};
+
+// Returns the cached layout of (gT, gF, T), building it if needed.  When
+// `need_forward` the relabelled forward CSR is built too.
+Layout* get_layout(dynpr_context* ctx, const dynpr_graph* gT, const dynpr_graph* gF, uint32_t T,
+                   bool need_forward);
+void destroy_layout(Layout* L);
+
+// new-id order <-> old-id order
+void launch_gather_perm_f64(dynpr_context* ctx, const Layout* L, const double* src_old, double* dst_new);
+void launch_gather_perm_u8(dynpr_context* ctx, const Layout* L, const uint8_t* src_old, uint8_t* dst_new);
+void launch_scatter_inv_f64(dynpr_context* ctx, const Layout* L, const double* src_new, double* dst_old);
+void launch_scatter_inv_u8(dynpr_context* ctx, const Layout* L, const uint8_t* src_new, uint8_t* dst_old);
+
+}  // namespace dynpr_b200

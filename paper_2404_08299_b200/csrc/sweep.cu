@@ -1,4 +1,4 @@
-// Rank-update sweep, degree schedule, frontier and norm kernels
+// Rank-update sweep, degree partition, frontier and norm kernels
 // (north_star subsystems 2, 3 and 4).
 //
 // Arithmetic contract (SURVEY 8a, rank.cpp:42-115): every fp64 operation
@@ -10,25 +10,33 @@
 //   otherwise                       : sequential partial sums over 256-edge
 //                                     chunks, added in chunk order
 //                                     (rank.cpp:59-75)
-// so the ranks, the L-inf delta and hence every threshold decision are
+// so the ranks, the L-inf delta and every threshold decision are
 // bit-identical to the reference CPU library.
 //
-// Parallel decomposition (B200-first, the paper's kernel pair refined):
-//   k_sweep_low    thread per vertex, in-degree <= T (~93% of RMAT vertices)
-//   k_sweep_chunks warp per 32 chunks of <= 256 edges; the warp stages 16
-//                  contributions per chunk per round through shared memory
-//                  with coalesced half-warp loads (two chunks per load
-//                  instruction), then every lane sums its own chunk
-//                  sequentially -> the reference order at full warp
-//                  efficiency ("transposed" warp-cooperative gather)
-//   k_sweep_multi  thread per vertex with more than one chunk: adds the
-//                  chunk partials in order and finalises
-// All three share one fused epilogue: closed-loop / plain rank formula,
-// the next sweep's contribution r/outdeg (IEEE division, so gathering it is
-// bit-identical to the reference's per-edge division), copy-through of
-// unaffected vertices, prune / frontier flags with warp-aggregated
-// append to the pending lists, and a block-level max / count reduction
-// finished with one 64-bit atomic per block (L-inf fused into the update).
+// Parallel decomposition over the engine layout (layout.cuh), the paper's
+// low/high kernel pair recast for the B200 memory system:
+//   k_sweep_single  warp per SELL-32 slice of 32 single-segment vertices
+//                   (in-degree <= max(T, 256), sorted by in-degree so the
+//                   32 lanes have near-equal trip counts); lane = vertex
+//   k_sweep_mseg    warp per slice of 32 256-edge chunks of the high
+//                   in-degree ("multi") vertices; lane = chunk -> partial
+//   k_sweep_mfinal  thread per multi vertex: partials combined in chunk order
+// Index loads are coalesced 128-byte lines (lane-interleaved SELL storage,
+// streamed past L1); contribution gathers go through the read-only path into
+// a relabelled vector whose hot entries are packed at its front.  One fused
+// epilogue: closed-loop / plain rank formula, the next sweep's contribution
+// r/outdeg (IEEE division, bit-identical to the reference's per-edge
+// division), copy-through of unaffected vertices, prune / frontier flags,
+// warp-aggregated append of pending vertices to the out-degree-split
+// expansion lists, and the L-inf / count reductions finished with one 64-bit
+// atomic per block.
+//
+// Frontier expansion (frontier.cpp:55-84) is direction-optimising: push over
+// the relabelled out-CSR (thread per low out-degree vertex, warp per
+// 1024-edge item of a high one) when the pending set is small, pull over
+// the SELL in-lists of the still-unaffected vertices (early exit on the first
+// pending in-neighbour) when pushing would touch more edges.  Both produce
+// exactly vertexAffected |= out(pending).
 #include "sweep.cuh"
 
 namespace dynpr_b200 {
@@ -37,65 +45,74 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kRound = 16;  // contributions staged per chunk per round
+constexpr unsigned kFull = 0xffffffffu;
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31; }
 
-// ---- block reductions ----------------------------------------------------
-struct BlockRed {
-  double dmax;
-  unsigned long long proc, edges;
+struct Acc {
+  double dmax = 0.0;
+  unsigned long long proc = 0, edges = 0, pedges = 0;
 };
 
-__device__ __forceinline__ void block_reduce_commit(double dmax,
-                                                    unsigned long long proc,
-                                                    unsigned long long edges,
-                                                    SweepRed* red) {
+// ---- block reductions ----------------------------------------------------
+__device__ __forceinline__ void block_reduce_commit(Acc acc, SweepRed* red) {
   __shared__ double s_d[kWarps];
-  __shared__ unsigned long long s_p[kWarps], s_e[kWarps];
-  dmax = warp_max(dmax);
-  proc = warp_sum(proc);
-  edges = warp_sum(edges);
+  __shared__ unsigned long long s_p[kWarps], s_e[kWarps], s_q[kWarps];
+  acc.dmax = warp_max(acc.dmax);
+  acc.proc = warp_sum(acc.proc);
+  acc.edges = warp_sum(acc.edges);
+  acc.pedges = warp_sum(acc.pedges);
   const int w = threadIdx.x >> 5;
   if (lane_id() == 0) {
-    s_d[w] = dmax;
-    s_p[w] = proc;
-    s_e[w] = edges;
+    s_d[w] = acc.dmax;
+    s_p[w] = acc.proc;
+    s_e[w] = acc.edges;
+    s_q[w] = acc.pedges;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     double d = 0.0;
-    unsigned long long p = 0, e = 0;
+    unsigned long long p = 0, e = 0, q = 0;
     for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
       d = fmax(d, s_d[i]);
       p += s_p[i];
       e += s_e[i];
+      q += s_q[i];
     }
     if (d > 0.0) atomicMax(&red->delta_bits, (unsigned long long)__double_as_longlong(d));
     if (p) atomicAdd(&red->processed, p);
     if (e) atomicAdd(&red->edges, e);
+    if (q) atomicAdd(&red->pend_edges, q);
   }
 }
 
-// Warp-aggregated append of pending vertices to the low/high out-degree
-// lists (all 32 lanes must call it).
-__device__ __forceinline__ void warp_append(bool pend, bool lowout, uint32_t v,
-                                            uint32_t* pl, uint32_t* ph,
-                                            SweepRed* red) {
-  const unsigned ml = __ballot_sync(0xffffffffu, pend && lowout);
-  const unsigned mh = __ballot_sync(0xffffffffu, pend && !lowout);
+// Warp-aggregated append of pending vertices (all 32 lanes must call it):
+// low out-degree vertices go to `pl` one entry each, the others to `ph` as
+// ceil(outdeg / 1024) (vertex, chunk) work items.
+__device__ __forceinline__ void warp_append(bool pend, bool lowout, uint32_t v, uint32_t od, uint32_t* pl,
+                                            uint2* ph, SweepRed* red) {
+  const unsigned ml = __ballot_sync(kFull, pend && lowout);
+  const unsigned items = (pend && !lowout) ? (od + kExpandChunk - 1) / kExpandChunk : 0u;
+  const unsigned mh = __ballot_sync(kFull, items != 0);
   if (!(ml | mh)) return;
   const unsigned lane = lane_id();
+  unsigned incl = items;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(kFull, incl, o);
+    if ((int)lane >= o) incl += y;
+  }
+  const unsigned total = __shfl_sync(kFull, incl, 31);
   unsigned bl = 0, bh = 0;
   if (lane == 0) {
     if (ml) bl = atomicAdd(&red->pend_low, (unsigned)__popc(ml));
-    if (mh) bh = atomicAdd(&red->pend_high, (unsigned)__popc(mh));
+    if (total) bh = atomicAdd(&red->pend_high, total);
   }
-  bl = __shfl_sync(0xffffffffu, bl, 0);
-  bh = __shfl_sync(0xffffffffu, bh, 0);
+  bl = __shfl_sync(kFull, bl, 0);
+  bh = __shfl_sync(kFull, bh, 0);
   const unsigned lt = (1u << lane) - 1u;
   if (pend && lowout) pl[bl + __popc(ml & lt)] = v;
-  if (pend && !lowout) ph[bh + __popc(mh & lt)] = v;
+  for (unsigned j = 0, b = bh + incl - items; j < items; ++j) ph[b + j] = make_uint2(v, j);
 }
 
 // Unaffected vertex (rank.cpp:90-92): current = previous.  In engine mode
@@ -115,11 +132,8 @@ __device__ __forceinline__ void copy_through(const SweepArgs& a, uint32_t v) {
 // Fused epilogue: rank formula (rank.cpp:97-106), next contribution, delta,
 // flags (rank.cpp:108-115).
 template <bool FLAGGED, bool CLOSED>
-__device__ __forceinline__ void finalize(const SweepArgs& a, uint32_t v,
-                                         double c, double& dmax, bool& pend,
-                                         bool& lowout) {
-  const double pv = a.rank_prev[v];
-  const uint32_t od = (uint32_t)(a.offF[v + 1] - a.offF[v]);
+__device__ __forceinline__ void finalize(const SweepArgs& a, uint32_t v, double c, double pv, uint32_t od,
+                                         Acc& acc, bool& pend, bool& lowout) {
   const double d = (double)od;
   double r;
   if (CLOSED) {
@@ -131,7 +145,7 @@ __device__ __forceinline__ void finalize(const SweepArgs& a, uint32_t v,
   a.rank_cur[v] = r;
   if (a.contrib_cur) a.contrib_cur[v] = __ddiv_rn(r, d);
   const double dr = fabs(__dsub_rn(r, pv));
-  if (dr > dmax) dmax = dr;  // NaN never wins, like blockMax (parallel.hpp:66-73)
+  if (dr > acc.dmax) acc.dmax = dr;  // NaN never wins, like blockMax (parallel.hpp:66-73)
   if (FLAGGED) {
     const double denom = r > pv ? r : pv;
     const double rel = denom > 0.0 ? __ddiv_rn(dr, denom) : 0.0;
@@ -145,307 +159,267 @@ __device__ __forceinline__ void finalize(const SweepArgs& a, uint32_t v,
       }
     }
     lowout = od <= a.T;
+    if (pend) acc.pedges += od;
     if (a.written) a.written[v] = 1;
   }
 }
 
-// ---- low in-degree: thread per vertex ----------------------------------------
+// Lane-sequential sum of one SELL segment: element k of this lane's segment
+// is at sell[base + 32k + lane].  Index loads for the next 8 elements are
+// issued before the adds of the current 8 (software pipelining); the adds
+// stay in segment order.
+__device__ __forceinline__ double segment_sum(const uint32_t* __restrict__ sell, uint64_t base, unsigned lane,
+                                              uint32_t len, uint32_t Lw, const double* __restrict__ contrib) {
+  constexpr uint32_t U = 8;
+  const uint32_t* p = sell + base + lane;
+  double c = 0.0;
+  uint32_t u[U];
+#pragma unroll
+  for (uint32_t q = 0; q < U; ++q) u[q] = q < len ? __ldcs(p + 32u * q) : 0u;
+  for (uint32_t k = 0; k < Lw; k += U) {
+    double x[U];
+#pragma unroll
+    for (uint32_t q = 0; q < U; ++q) x[q] = (k + q < len) ? __ldg(contrib + u[q]) : 0.0;
+    uint32_t un[U];
+#pragma unroll
+    for (uint32_t q = 0; q < U; ++q) un[q] = (k + U + q < len) ? __ldcs(p + 32ull * (k + U + q)) : 0u;
+#pragma unroll
+    for (uint32_t q = 0; q < U; ++q)
+      if (k + q < len) c = __dadd_rn(c, x[q]);
+#pragma unroll
+    for (uint32_t q = 0; q < U; ++q) u[q] = un[q];
+  }
+  return c;
+}
+
+// Does any element of this lane's SELL segment hit a pending vertex?
+__device__ __forceinline__ bool segment_any_pending(const uint32_t* __restrict__ sell, uint64_t base, unsigned lane,
+                                                    uint32_t len, const uint8_t* __restrict__ np) {
+  constexpr uint32_t U = 8;
+  const uint32_t* p = sell + base + lane;
+  bool found = false;
+  for (uint32_t k = 0;; k += U) {
+    const bool active = !found && k < len;
+    if (!__any_sync(kFull, active)) break;
+    if (active) {
+      uint32_t u[U];
+#pragma unroll
+      for (uint32_t q = 0; q < U; ++q) u[q] = (k + q < len) ? __ldcs(p + 32ull * (k + q)) : 0u;
+#pragma unroll
+      for (uint32_t q = 0; q < U; ++q)
+        if (k + q < len && np[u[q]]) found = true;
+    }
+  }
+  return found;
+}
+
+// ---- single-segment vertices: warp per 32-vertex slice ------------------------
 template <bool FLAGGED, bool CLOSED>
-__global__ void __launch_bounds__(kThreads) k_sweep_low(SweepArgs a) {
-  double dmax = 0.0;
-  unsigned long long proc = 0, edges = 0;
+__global__ void __launch_bounds__(kThreads) k_sweep_single(SweepArgs a) {
+  Acc acc;
+  const unsigned lane = lane_id();
+  const uint64_t nw = (uint64_t)gridDim.x * kWarps;
+  for (uint64_t s = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) / 32; s < a.n_sslices; s += nw) {
+    const uint64_t vv = (uint64_t)a.M + s * 32 + lane;
+    const bool valid = vv < a.n;
+    const uint32_t v = (uint32_t)vv;
+    const uint32_t deg = valid ? a.indeg[v] : 0u;
+    bool aff = valid;
+    if (FLAGGED) aff = valid && a.va[v];
+    const uint32_t len = aff ? deg : 0u;
+    const uint32_t Lw = __reduce_max_sync(kFull, len);
+    double pv = 0.0;
+    uint32_t od = 0;
+    if (aff) {  // prefetch the epilogue operands under the gather latency
+      pv = a.rank_prev[v];
+      od = a.outdeg[v];
+    }
+    double c = 0.0;
+    if (Lw) c = segment_sum(a.sell_s, a.sbase[s], lane, len, Lw, a.contrib_prev);
+    bool pend = false, lowout = false;
+    if (valid) {
+      if (!aff) {
+        copy_through(a, v);
+      } else {
+        finalize<FLAGGED, CLOSED>(a, v, c, pv, od, acc, pend, lowout);
+        ++acc.proc;
+        acc.edges += deg;
+      }
+    }
+    if (FLAGGED && a.pend_low) warp_append(pend, lowout, v, od, a.pend_low, a.pend_high, a.red);
+  }
+  block_reduce_commit(acc, a.red);
+}
+
+// ---- multi vertices: warp per slice of 32 chunks -> partials -------------------
+template <bool FLAGGED>
+__global__ void __launch_bounds__(kThreads) k_sweep_mseg(SweepArgs a) {
+  const unsigned lane = lane_id();
+  const uint64_t nw = (uint64_t)gridDim.x * kWarps;
+  for (uint64_t s = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) / 32; s < a.n_mslices; s += nw) {
+    const uint64_t seg = s * 32 + lane;
+    uint32_t len = 0;
+    if (seg < a.n_mseg) {
+      len = a.mseg_len[seg];
+      if (FLAGGED && !a.va[a.mseg_v[seg]]) len = 0;
+    }
+    const uint32_t Lw = __reduce_max_sync(kFull, len);
+    if (!Lw) continue;
+    const double c = segment_sum(a.sell_m, a.mbase[s], lane, len, Lw, a.contrib_prev);
+    if (len) a.partials[seg] = c;
+  }
+}
+
+// ---- multi vertices: ordered combine (rank.cpp:72) + epilogue --------------------
+template <bool FLAGGED, bool CLOSED>
+__global__ void __launch_bounds__(kThreads) k_sweep_mfinal(SweepArgs a) {
+  Acc acc;
   const uint64_t stride = (uint64_t)gridDim.x * kThreads;
-  for (uint64_t base = (uint64_t)blockIdx.x * kThreads; base < a.n; base += stride) {
+  for (uint64_t base = (uint64_t)blockIdx.x * kThreads; base < a.M; base += stride) {
     const uint64_t vv = base + threadIdx.x;
     bool pend = false, lowout = false;
-    if (vv < a.n) {
-      const uint32_t v = (uint32_t)vv;
-      const uint64_t b = a.offT[v], e = a.offT[v + 1];
-      const uint32_t deg = (uint32_t)(e - b);
-      if (deg <= a.T) {
-        if (FLAGGED && !a.va[v]) {
-          copy_through(a, v);
-        } else {
-          double c = 0.0;
-          uint64_t i = b;
-          for (; i + 4 <= e; i += 4) {
-            const uint32_t u0 = a.idxT[i], u1 = a.idxT[i + 1], u2 = a.idxT[i + 2],
-                           u3 = a.idxT[i + 3];
-            const double x0 = a.contrib_prev[u0], x1 = a.contrib_prev[u1],
-                         x2 = a.contrib_prev[u2], x3 = a.contrib_prev[u3];
-            c = __dadd_rn(c, x0);
-            c = __dadd_rn(c, x1);
-            c = __dadd_rn(c, x2);
-            c = __dadd_rn(c, x3);
-          }
-          for (; i < e; ++i) c = __dadd_rn(c, a.contrib_prev[a.idxT[i]]);
-          finalize<FLAGGED, CLOSED>(a, v, c, dmax, pend, lowout);
-          ++proc;
-          edges += deg;
-        }
-      }
-    }
-    if (FLAGGED && a.pend_low)
-      warp_append(pend, lowout, (uint32_t)vv, a.pend_low, a.pend_high, a.red);
-  }
-  block_reduce_commit(dmax, proc, edges, a.red);
-}
-
-// ---- high in-degree: warp-cooperative chunks -----------------------------------
-template <bool FLAGGED, bool CLOSED>
-__global__ void __launch_bounds__(kThreads) k_sweep_chunks(SweepArgs a) {
-  __shared__ double s_x[kWarps][32][kRound + 1];
-  __shared__ uint64_t s_b[kWarps][32];
-  __shared__ uint32_t s_len[kWarps][32];
-  const int w = threadIdx.x >> 5;
-  const unsigned lane = lane_id();
-  const unsigned half = lane >> 4, hl = lane & 15;
-  double dmax = 0.0;
-  unsigned long long proc = 0, edges = 0;
-  const uint64_t wstride = (uint64_t)gridDim.x * kWarps * 32;
-  for (uint64_t cbase = ((uint64_t)blockIdx.x * kWarps + w) * 32; cbase < a.n_chunks;
-       cbase += wstride) {
-    const uint64_t c = cbase + lane;
-    const bool valid = c < a.n_chunks;
-    uint32_t v = 0, j = 0;
-    uint64_t vb = 0, ve = 0;
-    if (valid) {
-      const uint2 ent = a.chunks[c];
-      v = ent.x;
-      j = ent.y;
-      vb = a.offT[v];
-      ve = a.offT[v + 1];
-    }
-    const uint64_t b = vb + (uint64_t)kAccumChunk * j;
-    const uint64_t e = (b + kAccumChunk < ve) ? b + kAccumChunk : ve;
-    const bool aff = valid && (!FLAGGED || a.va[v]);
-    const uint32_t len = aff ? (uint32_t)(e - b) : 0u;
-    s_b[w][lane] = b;
-    s_len[w][lane] = len;
-    const unsigned maxlen = __reduce_max_sync(0xffffffffu, len);
-    __syncwarp();
-    double p = 0.0;
-    for (unsigned r0 = 0; r0 < maxlen; r0 += kRound) {
-      const unsigned k = r0 + hl;
-      // gather phase: step q stages element k of chunks 2q (lanes 0-15) and
-      // 2q+1 (lanes 16-31); indices first, then contributions, for MLP.
-      uint32_t u[kRound];
-#pragma unroll
-      for (int q = 0; q < kRound; ++q) {
-        const int i = 2 * q + half;
-        u[q] = k < s_len[w][i] ? a.idxT[s_b[w][i] + k] : 0xffffffffu;
-      }
-      double x[kRound];
-#pragma unroll
-      for (int q = 0; q < kRound; ++q) x[q] = u[q] != 0xffffffffu ? a.contrib_prev[u[q]] : 0.0;
-#pragma unroll
-      for (int q = 0; q < kRound; ++q) s_x[w][2 * q + half][hl] = x[q];
-      __syncwarp();
-      // sum phase: each lane walks its own chunk in order
-      if (len > r0) {
-        const unsigned cnt = (len - r0) < (unsigned)kRound ? (len - r0) : (unsigned)kRound;
-        for (unsigned t = 0; t < cnt; ++t) p = __dadd_rn(p, s_x[w][lane][t]);
-      }
-      __syncwarp();
-    }
-    bool pend = false, lowout = false;
-    if (valid) {
-      const uint64_t deg = ve - vb;
-      if (deg <= kAccumChunk) {  // single chunk: c = 0.0 + p = p (rank.cpp:72)
-        if (!aff) {
-          copy_through(a, v);
-        } else {
-          finalize<FLAGGED, CLOSED>(a, v, p, dmax, pend, lowout);
-          ++proc;
-          edges += deg;
-        }
-      } else if (aff) {
-        a.partials[c] = p;
-      }
-    }
-    if (FLAGGED && a.pend_low) warp_append(pend, lowout, v, a.pend_low, a.pend_high, a.red);
-  }
-  block_reduce_commit(dmax, proc, edges, a.red);
-}
-
-// ---- multi-chunk vertices: ordered combine of the partials (rank.cpp:72) ------
-template <bool FLAGGED, bool CLOSED>
-__global__ void __launch_bounds__(kThreads) k_sweep_multi(SweepArgs a) {
-  double dmax = 0.0;
-  unsigned long long proc = 0, edges = 0;
-  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
-  for (uint64_t base = (uint64_t)blockIdx.x * kThreads; base < a.n_multi; base += stride) {
-    const uint64_t i = base + threadIdx.x;
-    bool pend = false, lowout = false;
-    uint32_t v = 0;
-    if (i < a.n_multi) {
-      const uint2 ent = a.multi[i];
-      v = ent.x;
-      const uint64_t deg = a.offT[v + 1] - a.offT[v];
+    const uint32_t v = (uint32_t)vv;
+    uint32_t od = 0;
+    if (vv < a.M) {
       if (FLAGGED && !a.va[v]) {
         copy_through(a, v);
       } else {
-        const uint64_t nch = (deg + kAccumChunk - 1) / kAccumChunk;
+        const uint32_t deg = a.indeg[v];
+        const uint32_t nch = (deg + kAccumChunk - 1) / kAccumChunk;
+        const double* p = a.partials + a.pbase[v];
         double c = 0.0;
-        for (uint64_t q = 0; q < nch; ++q) c = __dadd_rn(c, a.partials[(uint64_t)ent.y + q]);
-        finalize<FLAGGED, CLOSED>(a, v, c, dmax, pend, lowout);
-        ++proc;
-        edges += deg;
+        for (uint32_t q = 0; q < nch; ++q) c = __dadd_rn(c, p[q]);
+        od = a.outdeg[v];
+        finalize<FLAGGED, CLOSED>(a, v, c, a.rank_prev[v], od, acc, pend, lowout);
+        ++acc.proc;
+        acc.edges += deg;
       }
     }
-    if (FLAGGED && a.pend_low) warp_append(pend, lowout, v, a.pend_low, a.pend_high, a.red);
+    if (FLAGGED && a.pend_low) warp_append(pend, lowout, v, od, a.pend_low, a.pend_high, a.red);
   }
-  block_reduce_commit(dmax, proc, edges, a.red);
+  block_reduce_commit(acc, a.red);
 }
 
-// ---- schedule (partition.cpp:7-61 + chunk table) ----------------------------------
+// ---- pull expansion over the SELL in-lists ------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_pull_single(SweepArgs a) {
+  const unsigned lane = lane_id();
+  const uint64_t nw = (uint64_t)gridDim.x * kWarps;
+  for (uint64_t s = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) / 32; s < a.n_sslices; s += nw) {
+    const uint64_t vv = (uint64_t)a.M + s * 32 + lane;
+    const bool need = vv < a.n && !a.va[vv];
+    const uint32_t len = need ? a.indeg[vv] : 0u;
+    if (!__any_sync(kFull, len != 0)) continue;
+    if (segment_any_pending(a.sell_s, a.sbase[s], lane, len, a.np)) a.va[vv] = 1;
+  }
+}
+__global__ void __launch_bounds__(kThreads) k_pull_mseg(SweepArgs a) {
+  const unsigned lane = lane_id();
+  const uint64_t nw = (uint64_t)gridDim.x * kWarps;
+  for (uint64_t s = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) / 32; s < a.n_mslices; s += nw) {
+    const uint64_t seg = s * 32 + lane;
+    uint32_t len = 0, v = 0;
+    if (seg < a.n_mseg) {
+      v = a.mseg_v[seg];
+      if (!a.va[v]) len = a.mseg_len[seg];
+    }
+    if (!__any_sync(kFull, len != 0)) continue;
+    if (segment_any_pending(a.sell_m, a.mbase[s], lane, len, a.np)) a.va[v] = 1;
+  }
+}
+
+// ---- stable degree partition (partition.cpp:7-61) ------------------------------------
 constexpr int kTileItems = 4;
 constexpr int kTile = kThreads * kTileItems;  // 1024 vertices per tile
 
-struct Cnt3 {
-  unsigned low, chunks, multi;
-};
-__device__ __forceinline__ Cnt3 add3(Cnt3 x, Cnt3 y) {
-  return {x.low + y.low, x.chunks + y.chunks, x.multi + y.multi};
-}
-
-__device__ __forceinline__ Cnt3 vertex_counts(const uint64_t* off, uint64_t v, uint32_t n,
-                                              uint32_t thr, bool want_chunks) {
-  if (v >= n) return {0, 0, 0};
-  const uint64_t deg = off[v + 1] - off[v];
-  if (deg <= thr) return {1, 0, 0};
-  if (!want_chunks) return {0, 0, 0};
-  const unsigned nch = (unsigned)((deg + kAccumChunk - 1) / kAccumChunk);
-  return {0, nch, nch > 1 ? 1u : 0u};
-}
-
-// Exclusive block scan of per-thread Cnt3 (thread order == id order).
-__device__ __forceinline__ Cnt3 block_exclusive_scan(Cnt3 x, Cnt3& total) {
-  __shared__ Cnt3 s_w[kWarps];
+__device__ __forceinline__ unsigned block_exclusive_scan(unsigned x, unsigned& total) {
+  __shared__ unsigned s_w[kWarps];
   const unsigned lane = lane_id();
   const int w = threadIdx.x >> 5;
-  Cnt3 inc = x;
+  unsigned inc = x;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    Cnt3 y;
-    y.low = __shfl_up_sync(0xffffffffu, inc.low, o);
-    y.chunks = __shfl_up_sync(0xffffffffu, inc.chunks, o);
-    y.multi = __shfl_up_sync(0xffffffffu, inc.multi, o);
-    if ((int)lane >= o) inc = add3(inc, y);
+    const unsigned y = __shfl_up_sync(kFull, inc, o);
+    if ((int)lane >= o) inc += y;
   }
   if (lane == 31) s_w[w] = inc;
   __syncthreads();
-  Cnt3 pre = {0, 0, 0};
-  total = {0, 0, 0};
+  unsigned pre = 0;
+  total = 0;
   for (int i = 0; i < kWarps; ++i) {
-    if (i < w) pre = add3(pre, s_w[i]);
-    total = add3(total, s_w[i]);
+    if (i < w) pre += s_w[i];
+    total += s_w[i];
   }
   __syncthreads();
-  Cnt3 r = add3(pre, inc);
-  return {r.low - x.low, r.chunks - x.chunks, r.multi - x.multi};
+  return pre + inc - x;
 }
 
-__global__ void __launch_bounds__(kThreads) k_sched_count(const uint64_t* off, uint32_t n, uint32_t thr,
-                                                         bool want_chunks, uint4* tiles) {
+__global__ void __launch_bounds__(kThreads) k_part_count(const uint64_t* off, uint32_t n, uint32_t thr,
+                                                        unsigned* tiles) {
   const uint64_t v0 = (uint64_t)blockIdx.x * kTile + (uint64_t)threadIdx.x * kTileItems;
-  Cnt3 s = {0, 0, 0};
+  unsigned s = 0;
 #pragma unroll
-  for (int k = 0; k < kTileItems; ++k) s = add3(s, vertex_counts(off, v0 + k, n, thr, want_chunks));
-  Cnt3 total;
+  for (int k = 0; k < kTileItems; ++k) s += (v0 + k < n) && (off[v0 + k + 1] - off[v0 + k] <= thr);
+  unsigned total;
   block_exclusive_scan(s, total);
-  if (threadIdx.x == 0) tiles[blockIdx.x] = make_uint4(total.low, total.chunks, total.multi, 0);
+  if (threadIdx.x == 0) tiles[blockIdx.x] = total;
 }
 
-// Single-block exclusive scan of the tile counts (64-bit chunk totals).
-__global__ void k_sched_scan(uint4* tiles, uint64_t ntiles, unsigned long long* totals,
-                             unsigned long long* chunk_base) {
-  __shared__ unsigned long long s_l[1024], s_c[1024], s_m[1024];
-  unsigned long long carry_l = 0, carry_c = 0, carry_m = 0;
+// Single-block exclusive scan of the tile counts.
+__global__ void k_part_scan(unsigned* tiles, uint64_t ntiles, unsigned long long* total_out) {
+  __shared__ unsigned long long s[1024];
+  unsigned long long carry = 0;
   for (uint64_t base = 0; base < ntiles; base += blockDim.x) {
     const uint64_t i = base + threadIdx.x;
-    const uint4 t = i < ntiles ? tiles[i] : make_uint4(0, 0, 0, 0);
-    s_l[threadIdx.x] = t.x;
-    s_c[threadIdx.x] = t.y;
-    s_m[threadIdx.x] = t.z;
+    const unsigned t = i < ntiles ? tiles[i] : 0u;
+    s[threadIdx.x] = t;
     __syncthreads();
-    for (unsigned o = 1; o < blockDim.x; o <<= 1) {  // Hillis-Steele inclusive
-      unsigned long long al = 0, ac = 0, am = 0;
-      if (threadIdx.x >= o) {
-        al = s_l[threadIdx.x - o];
-        ac = s_c[threadIdx.x - o];
-        am = s_m[threadIdx.x - o];
-      }
+    for (unsigned o = 1; o < blockDim.x; o <<= 1) {
+      const unsigned long long add = threadIdx.x >= o ? s[threadIdx.x - o] : 0ull;
       __syncthreads();
-      s_l[threadIdx.x] += al;
-      s_c[threadIdx.x] += ac;
-      s_m[threadIdx.x] += am;
+      s[threadIdx.x] += add;
       __syncthreads();
     }
-    if (i < ntiles) {
-      tiles[i] = make_uint4((unsigned)(carry_l + s_l[threadIdx.x] - t.x), 0u,
-                            (unsigned)(carry_m + s_m[threadIdx.x] - t.z), 0u);
-      chunk_base[i] = carry_c + s_c[threadIdx.x] - t.y;
-    }
+    if (i < ntiles) tiles[i] = (unsigned)(carry + s[threadIdx.x] - t);
     __syncthreads();
-    carry_l += s_l[blockDim.x - 1];
-    carry_c += s_c[blockDim.x - 1];
-    carry_m += s_m[blockDim.x - 1];
+    carry += s[blockDim.x - 1];
     __syncthreads();
   }
-  if (threadIdx.x == 0) {
-    totals[0] = carry_l;
-    totals[1] = carry_c;
-    totals[2] = carry_m;
-  }
+  if (threadIdx.x == 0) *total_out = carry;
 }
 
-__global__ void __launch_bounds__(kThreads) k_sched_scatter(const uint64_t* off, uint32_t n, uint32_t thr,
-                                                           bool want_chunks, const uint4* tiles,
-                                                           const unsigned long long* chunk_base,
-                                                           const unsigned long long* totals,
-                                                           uint32_t* order, uint2* chunks, uint2* multi) {
+__global__ void __launch_bounds__(kThreads) k_part_scatter(const uint64_t* off, uint32_t n, uint32_t thr,
+                                                          const unsigned* tiles,
+                                                          const unsigned long long* total, uint32_t* order) {
   const uint64_t v0 = (uint64_t)blockIdx.x * kTile + (uint64_t)threadIdx.x * kTileItems;
-  Cnt3 item[kTileItems];
-  Cnt3 s = {0, 0, 0};
+  bool low[kTileItems];
+  unsigned s = 0;
 #pragma unroll
   for (int k = 0; k < kTileItems; ++k) {
-    item[k] = vertex_counts(off, v0 + k, n, thr, want_chunks);
-    s = add3(s, item[k]);
+    low[k] = (v0 + k < n) && (off[v0 + k + 1] - off[v0 + k] <= thr);
+    s += low[k];
   }
-  Cnt3 total;
-  Cnt3 pre = block_exclusive_scan(s, total);
-  const uint4 t = tiles[blockIdx.x];
-  uint64_t lowpos = (uint64_t)t.x + pre.low;
-  uint64_t cpos = chunk_base[blockIdx.x] + pre.chunks;
-  uint64_t mpos = (uint64_t)t.z + pre.multi;
-  const uint64_t lowCount = totals[0];
+  unsigned tot;
+  uint64_t lowpos = (uint64_t)tiles[blockIdx.x] + block_exclusive_scan(s, tot);
+  const uint64_t lowCount = *total;
 #pragma unroll
   for (int k = 0; k < kTileItems; ++k) {
     const uint64_t v = v0 + k;
     if (v >= n) break;
-    if (item[k].low) {
-      if (order) order[lowpos] = (uint32_t)v;
-      ++lowpos;
+    if (low[k]) {
+      order[lowpos++] = (uint32_t)v;
     } else {
-      // high ids keep ascending order after the low group (partition.cpp:56-58)
-      if (order) order[lowCount + (v - lowpos)] = (uint32_t)v;
-      if (want_chunks) {
-        for (unsigned j = 0; j < item[k].chunks; ++j) chunks[cpos + j] = make_uint2((uint32_t)v, j);
-        if (item[k].multi) multi[mpos++] = make_uint2((uint32_t)v, (uint32_t)cpos);
-        cpos += item[k].chunks;
-      }
+      order[lowCount + (v - lowpos)] = (uint32_t)v;  // high ids ascending after the low group
     }
   }
 }
 
 // ---- init / frontier kernels -------------------------------------------------
-__global__ void k_init_ranks(const uint64_t* offF, uint32_t n, const double* init, double uniform,
-                             double* r0, double* r1, double* c0, double* c1) {
+__global__ void k_init_ranks(const uint32_t* outdeg, uint32_t n, const double* init, double uniform, double* r0,
+                             double* r1, double* c0, double* c1) {
   for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
        v += (uint64_t)gridDim.x * blockDim.x) {
     const double r = init ? init[v] : uniform;
-    const double c = __ddiv_rn(r, (double)(uint32_t)(offF[v + 1] - offF[v]));
+    const double c = __ddiv_rn(r, (double)outdeg[v]);
     r0[v] = r;
     if (r1) r1[v] = r;
     c0[v] = c;
@@ -454,66 +428,78 @@ __global__ void k_init_ranks(const uint64_t* offF, uint32_t n, const double* ini
 }
 
 // initialAffected (frontier.cpp:43-51): dels mark np[u] and va[v]; ins mark
-// np[u].  Pending sources go straight to the expansion lists.
-__global__ void k_init_affected(const uint64_t* offF, const uint32_t* ds, const uint32_t* dd, uint64_t nd,
-                                const uint32_t* is, uint64_t ni, uint8_t* va, uint8_t* np, uint32_t T,
-                                uint32_t* pl, uint32_t* ph, SweepRed* red) {
-  const uint64_t total = nd + ni;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < total; base += stride) {
-    const uint64_t i = base + threadIdx.x;
-    bool pend = false, lowout = false;
-    uint32_t u = 0;
-    if (i < total) {
-      if (i < nd) {
-        u = ds[i];
-        va[dd[i]] = 1;
-      } else {
-        u = is[i - nd];
-      }
-      if (np) np[u] = 1;
-      pend = true;
-      lowout = (offF[u + 1] - offF[u]) <= T;
+// np[u] (ids mapped through `inv` into the flag space when given).
+__global__ void k_init_affected(const uint32_t* inv, const uint32_t* ds, const uint32_t* dd, uint64_t nd,
+                                const uint32_t* is, uint64_t ni, uint8_t* va, uint8_t* np) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nd + ni;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t u;
+    if (i < nd) {
+      u = ds[i];
+      const uint32_t v = dd[i];
+      va[inv ? inv[v] : v] = 1;
+    } else {
+      u = is[i - nd];
     }
-    if (pl) warp_append(pend, lowout, u, pl, ph, red);
+    np[inv ? inv[u] : u] = 1;
   }
 }
 
-__global__ void k_collect_pending(const uint64_t* offF, uint32_t n, const uint8_t* np, uint32_t T,
-                                  uint32_t* pl, uint32_t* ph, SweepRed* red) {
+// Pending flags -> expansion work lists (out-degree from `outdeg` when given,
+// else from the CSR offsets).
+__global__ void k_collect_pending(const uint32_t* outdeg, const uint64_t* off, uint32_t n, const uint8_t* np,
+                                  uint32_t T, uint32_t* pl, uint2* ph, SweepRed* red) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
     const uint64_t v = base + threadIdx.x;
     bool pend = false, lowout = false;
+    uint32_t od = 0;
     if (v < n && np[v]) {
       pend = true;
-      lowout = (offF[v + 1] - offF[v]) <= T;
+      od = outdeg ? outdeg[v] : (uint32_t)(off[v + 1] - off[v]);
+      lowout = od <= T;
     }
-    warp_append(pend, lowout, (uint32_t)v, pl, ph, red);
+    warp_append(pend, lowout, (uint32_t)v, od, pl, ph, red);
   }
 }
 
-// expandAffected (frontier.cpp:55-84) split by out-degree: thread per
-// low pending vertex, warp per high pending vertex.  Byte stores of 1 are
-// idempotent, so duplicates and races are benign.
+// Push expansion (frontier.cpp:55-84) split by out-degree: thread per low
+// pending vertex, warp per 1024-edge item of a high one.  Byte stores of 1
+// are idempotent; the read-before-write keeps dense frontiers
+// from turning into L2 write traffic.
 __global__ void k_expand_low(const uint64_t* off, const uint32_t* tgt, const uint32_t* list, uint32_t cnt,
                              uint8_t* va) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cnt;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t u = list[i];
     const uint64_t b = off[u], e = off[u + 1];
-    for (uint64_t k = b; k < e; ++k) va[tgt[k]] = 1;
+    for (uint64_t k = b; k < e; ++k) {
+      const uint32_t w = tgt[k];
+      if (!va[w]) va[w] = 1;
+    }
   }
 }
-__global__ void k_expand_high(const uint64_t* off, const uint32_t* tgt, const uint32_t* list, uint32_t cnt,
+__global__ void k_expand_high(const uint64_t* off, const uint32_t* tgt, const uint2* items, uint32_t cnt,
                               uint8_t* va) {
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / 32;
   const uint64_t nw = (uint64_t)gridDim.x * blockDim.x / 32;
   const unsigned lane = lane_id();
   for (uint64_t i = warp; i < cnt; i += nw) {
-    const uint32_t u = list[i];
-    const uint64_t b = off[u], e = off[u + 1];
-    for (uint64_t k = b + lane; k < e; k += 32) va[tgt[k]] = 1;
+    const uint2 it = items[i];
+    const uint64_t b = off[it.x] + (uint64_t)kExpandChunk * it.y;
+    const uint64_t e0 = off[it.x + 1];
+    const uint64_t e = b + kExpandChunk < e0 ? b + kExpandChunk : e0;
+    for (uint64_t k = b + lane; k < e; k += 32 * 4) {
+      uint32_t w[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) w[q] = k + 32 * q < e ? tgt[k + 32 * q] : 0xffffffffu;
+      uint8_t f[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) f[q] = w[q] != 0xffffffffu ? va[w[q]] : 1;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (!f[q]) va[w[q]] = 1;
+    }
   }
 }
 
@@ -552,61 +538,102 @@ __global__ void k_l1_final(const double* partials, uint64_t nb, double* out) {
   *out = t;
 }
 
+// Persistent grid: resident blocks per SM x SMs (queried once per kernel).
+template <class K>
+unsigned persistent_grid(dynpr_context* ctx, K kernel, uint64_t work_blocks) {
+  static const void* keys[32] = {};
+  static int vals[32] = {};
+  int per_sm = -1;
+  for (int i = 0; i < 32 && keys[i]; ++i)
+    if (keys[i] == (const void*)kernel) per_sm = vals[i];
+  if (per_sm < 0) {
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, kThreads, 0) != cudaSuccess || b < 1) {
+      cudaGetLastError();
+      b = 1;
+    }
+    per_sm = b;
+    for (int i = 0; i < 32; ++i)
+      if (!keys[i]) {
+        keys[i] = (const void*)kernel;
+        vals[i] = b;
+        break;
+      }
+  }
+  const uint64_t cap = (uint64_t)per_sm * ctx->num_sms;
+  return (unsigned)(work_blocks < 1 ? 1 : (work_blocks < cap ? work_blocks : cap));
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
-Schedule build_schedule(dynpr_context* ctx, const dynpr_graph* g, uint32_t thr, uint32_t* order,
-                        bool want_chunks) {
+Schedule build_partition(dynpr_context* ctx, const dynpr_graph* g, uint32_t thr, uint32_t* order) {
   Schedule s;
   s.threshold = thr;
   const uint32_t n = g->n;
   if (n == 0) return s;
   cudaStream_t st = ctx->stream;
   const uint64_t ntiles = ((uint64_t)n + kTile - 1) / kTile;
-  uint4* tiles = ctx->tile_counts.as<uint4>(ntiles);
-  auto* cb = ctx->scratch64a.as<unsigned long long>(ntiles + 4);
-  unsigned long long* totals = cb + ntiles;
-  k_sched_count<<<(unsigned)ntiles, kThreads, 0, st>>>(g->off, n, thr, want_chunks, tiles);
+  unsigned* tiles = ctx->tile_counts.as<unsigned>(ntiles);
+  auto* total = ctx->scratch64a.as<unsigned long long>(1);
+  k_part_count<<<(unsigned)ntiles, kThreads, 0, st>>>(g->off, n, thr, tiles);
   check_launch();
-  k_sched_scan<<<1, 1024, 0, st>>>(tiles, ntiles, totals, cb);
+  k_part_scan<<<1, 1024, 0, st>>>(tiles, ntiles, total);
   check_launch();
-  count_launch(ctx, 2);
-  unsigned long long h[3];
-  DYNPR_CK(cudaMemcpyAsync(ctx->pinned, totals, sizeof h, cudaMemcpyDeviceToHost, st));
+  k_part_scatter<<<(unsigned)ntiles, kThreads, 0, st>>>(g->off, n, thr, tiles, total, order);
+  check_launch();
+  count_launch(ctx, 3);
+  unsigned long long h;
+  DYNPR_CK(cudaMemcpyAsync(ctx->pinned, total, 8, cudaMemcpyDeviceToHost, st));
   sync(ctx);
-  std::memcpy(h, ctx->pinned, sizeof h);
-  s.n_low = (uint32_t)h[0];
+  std::memcpy(&h, ctx->pinned, 8);
+  s.n_low = (uint32_t)h;
   s.n_high = n - s.n_low;
-  s.n_chunks = h[1];
-  s.n_multi = (uint32_t)h[2];
-  uint2* chunks = nullptr;
-  uint2* multi = nullptr;
-  if (want_chunks) {
-    chunks = ctx->sched_chunks.as<uint2>(s.n_chunks + 1);
-    multi = ctx->sched_multi.as<uint2>((uint64_t)s.n_multi + 1);
-    s.partials = ctx->partials.as<double>(s.n_chunks + 1);
-  }
-  k_sched_scatter<<<(unsigned)ntiles, kThreads, 0, st>>>(g->off, n, thr, want_chunks, tiles, cb, totals, order,
-                                                        chunks, multi);
-  check_launch();
-  count_launch(ctx);
-  s.chunks = chunks;
-  s.multi = multi;
   return s;
 }
 
-void launch_sweep(dynpr_context* ctx, const SweepArgs& a, bool flagged, bool closed, uint32_t n_low_hint) {
+SweepArgs layout_args(const Layout* L, double* partials) {
+  SweepArgs a{};
+  a.n = L->n;
+  a.M = L->M;
+  a.T = L->T;
+  a.indeg = L->indeg;
+  a.outdeg = L->outdeg;
+  a.n_sslices = L->n_sslices;
+  a.sbase = L->sbase;
+  a.sell_s = L->sell_s;
+  a.n_mseg = L->n_mseg;
+  a.n_mslices = L->n_mslices;
+  a.mbase = L->mbase;
+  a.mseg_v = L->mseg_v;
+  a.mseg_len = L->mseg_len;
+  a.pbase = L->pbase;
+  a.sell_m = L->sell_m;
+  a.partials = partials;
+  return a;
+}
+
+void launch_sweep(dynpr_context* ctx, const SweepArgs& a, bool flagged, bool closed) {
   cudaStream_t st = ctx->stream;
-  const unsigned max_blocks = (unsigned)ctx->num_sms * 8;
-  (void)n_low_hint;
-  const unsigned g_low = grid_for(a.n, kThreads, max_blocks);
-  const unsigned g_chunk = grid_for(a.n_chunks, kThreads, max_blocks);
-  const unsigned g_multi = grid_for(a.n_multi, kThreads, max_blocks);
-#define DYNPR_SWEEP(F, C)                                                        \
-  do {                                                                           \
-    k_sweep_low<F, C><<<g_low, kThreads, 0, st>>>(a);                            \
-    if (a.n_chunks) k_sweep_chunks<F, C><<<g_chunk, kThreads, 0, st>>>(a);       \
-    if (a.n_multi) k_sweep_multi<F, C><<<g_multi, kThreads, 0, st>>>(a);         \
+  const uint64_t single_blocks = (a.n_sslices + kWarps - 1) / kWarps;
+  const uint64_t mseg_blocks = (a.n_mslices + kWarps - 1) / kWarps;
+  const unsigned g_mfinal = grid_for(a.M, kThreads);
+  unsigned launched = 0;
+#define DYNPR_SWEEP(F, C)                                                                           \
+  do {                                                                                              \
+    if (a.n_mslices) {                                                                              \
+      k_sweep_mseg<F><<<persistent_grid(ctx, k_sweep_mseg<F>, mseg_blocks), kThreads, 0, st>>>(a); \
+      ++launched;                                                                                   \
+    }                                                                                               \
+    if (a.n_sslices) {                                                                              \
+      k_sweep_single<F, C>                                                                          \
+          <<<persistent_grid(ctx, k_sweep_single<F, C>, single_blocks), kThreads, 0, st>>>(a);      \
+      ++launched;                                                                                   \
+    }                                                                                               \
+    if (a.M) {                                                                                      \
+      k_sweep_mfinal<F, C><<<g_mfinal, kThreads, 0, st>>>(a);                                       \
+      ++launched;                                                                                   \
+    }                                                                                               \
   } while (0)
   if (flagged) {
     if (closed) DYNPR_SWEEP(true, true); else DYNPR_SWEEP(true, false);
@@ -615,48 +642,63 @@ void launch_sweep(dynpr_context* ctx, const SweepArgs& a, bool flagged, bool clo
   }
 #undef DYNPR_SWEEP
   check_launch();
-  count_launch(ctx, 1 + (a.n_chunks ? 1 : 0) + (a.n_multi ? 1 : 0));
+  count_launch(ctx, launched);
 }
 
-void launch_init_ranks(dynpr_context* ctx, const dynpr_graph* gF, const double* init, double uniform, double* r0,
+void launch_pull_expand(dynpr_context* ctx, const SweepArgs& a) {
+  cudaStream_t st = ctx->stream;
+  unsigned launched = 0;
+  if (a.n_mslices) {
+    k_pull_mseg<<<persistent_grid(ctx, k_pull_mseg, (a.n_mslices + kWarps - 1) / kWarps), kThreads, 0, st>>>(a);
+    ++launched;
+  }
+  if (a.n_sslices) {
+    k_pull_single<<<persistent_grid(ctx, k_pull_single, (a.n_sslices + kWarps - 1) / kWarps), kThreads, 0, st>>>(
+        a);
+    ++launched;
+  }
+  check_launch();
+  count_launch(ctx, launched);
+}
+
+void launch_init_ranks(dynpr_context* ctx, const Layout* L, const double* init, double uniform, double* r0,
                        double* r1, double* c0, double* c1) {
-  if (!gF->n) return;
-  k_init_ranks<<<grid_for(gF->n, kThreads, ctx->num_sms * 16), kThreads, 0, ctx->stream>>>(gF->off, gF->n, init,
-                                                                                          uniform, r0, r1, c0, c1);
+  if (!L->n) return;
+  k_init_ranks<<<grid_for(L->n, kThreads, ctx->num_sms * 16), kThreads, 0, ctx->stream>>>(L->outdeg, L->n, init,
+                                                                                         uniform, r0, r1, c0, c1);
   check_launch();
   count_launch(ctx);
 }
 
-void launch_init_affected(dynpr_context* ctx, const dynpr_graph* gF, const uint32_t* ds, const uint32_t* dd,
-                          uint64_t nd, const uint32_t* is, uint64_t ni, uint8_t* va, uint8_t* np, uint32_t T,
-                          uint32_t* pend_low, uint32_t* pend_high, SweepRed* red) {
+void launch_init_affected(dynpr_context* ctx, const uint32_t* inv, const uint32_t* ds, const uint32_t* dd,
+                          uint64_t nd, const uint32_t* is, uint64_t ni, uint8_t* va, uint8_t* np) {
   if (nd + ni == 0) return;
-  k_init_affected<<<grid_for(nd + ni, kThreads, ctx->num_sms * 16), kThreads, 0, ctx->stream>>>(
-      gF->off, ds, dd, nd, is, ni, va, np, T, pend_low, pend_high, red);
+  k_init_affected<<<grid_for(nd + ni, kThreads, ctx->num_sms * 16), kThreads, 0, ctx->stream>>>(inv, ds, dd, nd,
+                                                                                               is, ni, va, np);
   check_launch();
   count_launch(ctx);
 }
 
-void launch_collect_pending(dynpr_context* ctx, const dynpr_graph* gF, const uint8_t* np, uint32_t T,
-                            uint32_t* pend_low, uint32_t* pend_high, SweepRed* red) {
-  if (!gF->n) return;
-  k_collect_pending<<<grid_for(gF->n, kThreads, ctx->num_sms * 16), kThreads, 0, ctx->stream>>>(
-      gF->off, gF->n, np, T, pend_low, pend_high, red);
+void launch_collect_pending(dynpr_context* ctx, const uint32_t* outdeg, const uint64_t* off, uint32_t n,
+                            const uint8_t* np, uint32_t T, uint32_t* pend_low, uint2* pend_high, SweepRed* red) {
+  if (!n) return;
+  k_collect_pending<<<grid_for(n, kThreads, ctx->num_sms * 16), kThreads, 0, ctx->stream>>>(
+      outdeg, off, n, np, T, pend_low, pend_high, red);
   check_launch();
   count_launch(ctx);
 }
 
-void launch_expand(dynpr_context* ctx, const dynpr_graph* gF, uint8_t* va, const uint32_t* pend_low,
-                   uint32_t n_low, const uint32_t* pend_high, uint32_t n_high) {
+void launch_expand(dynpr_context* ctx, const uint64_t* off, const uint32_t* tgt, uint8_t* va,
+                   const uint32_t* pend_low, uint32_t n_low, const uint2* pend_high, uint32_t n_high) {
   if (n_low) {
-    k_expand_low<<<grid_for(n_low, kThreads, ctx->num_sms * 16), kThreads, 0, ctx->stream>>>(gF->off, gF->tgt,
-                                                                                            pend_low, n_low, va);
+    k_expand_low<<<grid_for(n_low, kThreads, ctx->num_sms * 16), kThreads, 0, ctx->stream>>>(off, tgt, pend_low,
+                                                                                            n_low, va);
     check_launch();
     count_launch(ctx);
   }
   if (n_high) {
     k_expand_high<<<grid_for((uint64_t)n_high * 32, kThreads, ctx->num_sms * 16), kThreads, 0, ctx->stream>>>(
-        gF->off, gF->tgt, pend_high, n_high, va);
+        off, tgt, pend_high, n_high, va);
     check_launch();
     count_launch(ctx);
   }
