@@ -55,7 +55,7 @@ __global__ void k_count_above(const uint32_t* indeg, uint32_t n, uint32_t thr, u
 }
 // single region: slice lengths (x32) for the exclusive scan
 __global__ void k_single_slice_len(const uint32_t* indeg, uint32_t M, uint32_t n, uint64_t S, uint64_t* len32) {
-  GRID_STRIDE(s, S + 1) len32[s] = s < S ? 32ull * indeg[M + 32 * s] : 0ull;
+  GRID_STRIDE(s, S + 1) len32[s] = s < S ? 32ull * ((indeg[M + 32 * s] + 3u) & ~3u) : 0ull;
 }
 // multi region: chunk counts per multi vertex
 __global__ void k_multi_nch(const uint32_t* indeg, uint32_t M, uint32_t* nch) {
@@ -80,9 +80,23 @@ __global__ void k_multi_slice_len(const uint32_t* mseg_len, uint64_t nseg, uint6
     const uint64_t seg = s * 32 + lane;
     const unsigned l = (s < S && seg < nseg) ? mseg_len[seg] : 0u;
     const unsigned mx = __reduce_max_sync(0xffffffffu, l);
-    if (lane == 0) len32[s] = 32ull * mx;
+    if (lane == 0) len32[s] = 32ull * ((mx + 3u) & ~3u);
   }
 }
+// One lane's segment into SELL-32x4: 4 consecutive elements per 16-byte
+// store, so each warp store covers 512 contiguous bytes.
+__device__ __forceinline__ void fill_lane(uint32_t* sell, uint64_t base, unsigned lane, uint32_t L, uint32_t len,
+                                          const uint32_t* src, const uint32_t* inv) {
+  for (uint32_t k = 0; k < L; k += 4) {
+    uint4 w;
+    w.x = k < len ? inv[src[k]] : 0u;
+    w.y = k + 1 < len ? inv[src[k + 1]] : 0u;
+    w.z = k + 2 < len ? inv[src[k + 2]] : 0u;
+    w.w = k + 3 < len ? inv[src[k + 3]] : 0u;
+    *reinterpret_cast<uint4*>(sell + sell_pos(base, lane, k)) = w;
+  }
+}
+
 // SELL fill, single region: warp per slice, lane per vertex
 __global__ void k_fill_single(const uint64_t* offT, const uint32_t* tgtT, const uint32_t* perm, const uint32_t* inv,
                               const uint32_t* indeg, uint32_t M, uint32_t n, uint64_t S, const uint64_t* sbase,
@@ -97,7 +111,7 @@ __global__ void k_fill_single(const uint64_t* offT, const uint32_t* tgtT, const 
     const uint64_t src = valid ? offT[perm[vn]] : 0;
     const uint64_t base = sbase[s];
     const uint32_t L = (uint32_t)((sbase[s + 1] - base) / 32);
-    for (uint32_t k = 0; k < L; ++k) sell[base + 32ull * k + lane] = k < deg ? inv[tgtT[src + k]] : 0u;
+    fill_lane(sell, base, lane, L, deg, tgtT + src, inv);
   }
 }
 // SELL fill, multi region: warp per slice, lane per 256-edge segment
@@ -119,7 +133,7 @@ __global__ void k_fill_multi(const uint64_t* offT, const uint32_t* tgtT, const u
     }
     const uint64_t base = mbase[s];
     const uint32_t L = (uint32_t)((mbase[s + 1] - base) / 32);
-    for (uint32_t k = 0; k < L; ++k) sell[base + 32ull * k + lane] = k < len ? inv[tgtT[src + k]] : 0u;
+    fill_lane(sell, base, lane, L, len, tgtT + src, inv);
   }
 }
 // relabelled forward CSR: warp per new vertex

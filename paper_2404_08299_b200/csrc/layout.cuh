@@ -26,6 +26,14 @@
 
 namespace dynpr_b200 {
 
+// SELL-32x4 interleave: element k of lane i of a slice starting at `base`
+// lives at base + 128*(k/4) + 4*i + k%4, so a lane fetches 4 consecutive
+// elements with one 16-byte load and a warp load covers 512 contiguous bytes.
+// Slice lengths are padded to a multiple of 4.
+__host__ __device__ __forceinline__ uint64_t sell_pos(uint64_t base, uint32_t lane, uint32_t k) {
+  return base + 128ull * (k >> 2) + 4u * lane + (k & 3u);
+}
+
 struct Layout {
   dynpr_context* ctx = nullptr;
   uint32_t n = 0;

@@ -37,6 +37,8 @@
 // the SELL in-lists of the still-unaffected vertices (early exit on the first
 // pending in-neighbour) when pushing would touch more edges.  Both produce
 // exactly vertexAffected |= out(pending).
+#include <cstdlib>
+
 #include "sweep.cuh"
 
 namespace dynpr_b200 {
@@ -56,8 +58,8 @@ struct Acc {
 
 // ---- block reductions ----------------------------------------------------
 __device__ __forceinline__ void block_reduce_commit(Acc acc, SweepRed* red) {
-  __shared__ double s_d[kWarps];
-  __shared__ unsigned long long s_p[kWarps], s_e[kWarps], s_q[kWarps];
+  __shared__ double s_d[32];
+  __shared__ unsigned long long s_p[32], s_e[32], s_q[32];
   acc.dmax = warp_max(acc.dmax);
   acc.proc = warp_sum(acc.proc);
   acc.edges = warp_sum(acc.edges);
@@ -164,30 +166,51 @@ __device__ __forceinline__ void finalize(const SweepArgs& a, uint32_t v, double 
   }
 }
 
-// Lane-sequential sum of one SELL segment: element k of this lane's segment
-// is at sell[base + 32k + lane].  Index loads for the next 8 elements are
-// issued before the adds of the current 8 (software pipelining); the adds
-// stay in segment order.
+// Cache-policy loads.  Index streams and cold contributions bypass L1
+// (L1::no_allocate); the hot prefix of the relabelled contribution vector
+// (new ids < a.hot, the most-gathered vertices) is loaded evict_last so it
+// stays resident in L1 and its gathers never reach L2.
+__device__ __forceinline__ uint4 ld_idx4(const uint32_t* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+// A contribution: the vertex's own (self-loop) value from a register, the
+// hot prefix (new ids < hot, the most-gathered vertices) from the CTA's
+// shared-memory copy, everything else from global memory.  Random 8-byte
+// reads: shared memory 1415 G/s vs L2-resident global 288 G/s on B200
+// (profiles/microbench_gather.cu).
+__device__ __forceinline__ double ld_contrib(const double* __restrict__ contrib, const double* s_hot, uint32_t u,
+                                             uint32_t hot, uint32_t self, double cself) {
+  if (u == self) return cself;
+  return u < hot ? s_hot[u] : __ldg(contrib + u);
+}
+
+// Lane-sequential sum of one SELL-32x4 segment (layout.cuh sell_pos):
+// elements 4j..4j+3 of this lane arrive with one 16-byte load.  Index loads
+// for the next 8 elements are issued before the adds of the current 8
+// (software pipelining); the adds stay in segment order.
 __device__ __forceinline__ double segment_sum(const uint32_t* __restrict__ sell, uint64_t base, unsigned lane,
-                                              uint32_t len, uint32_t Lw, const double* __restrict__ contrib) {
-  constexpr uint32_t U = 8;
-  const uint32_t* p = sell + base + lane;
+                                              uint32_t len, uint32_t Lw, const double* __restrict__ contrib,
+                                              const double* s_hot, uint32_t hot, uint32_t self, double cself) {
+  const uint32_t* p = sell + base + 4u * lane;  // element k at p + 32*k (k % 4 == 0)
+  const uint4 z = make_uint4(0, 0, 0, 0);
   double c = 0.0;
-  uint32_t u[U];
+  uint4 a = len > 0 ? ld_idx4(p) : z;
+  uint4 b = len > 4 ? ld_idx4(p + 128) : z;
+  for (uint32_t k = 0; k < Lw; k += 8) {
+    const uint32_t u[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    double x[8];
 #pragma unroll
-  for (uint32_t q = 0; q < U; ++q) u[q] = q < len ? __ldcs(p + 32u * q) : 0u;
-  for (uint32_t k = 0; k < Lw; k += U) {
-    double x[U];
+    for (uint32_t q = 0; q < 8; ++q)
+      x[q] = (k + q < len) ? ld_contrib(contrib, s_hot, u[q], hot, self, cself) : 0.0;
+    a = (k + 8 < len) ? ld_idx4(p + 32ull * (k + 8)) : z;
+    b = (k + 12 < len) ? ld_idx4(p + 32ull * (k + 12)) : z;
 #pragma unroll
-    for (uint32_t q = 0; q < U; ++q) x[q] = (k + q < len) ? __ldg(contrib + u[q]) : 0.0;
-    uint32_t un[U];
-#pragma unroll
-    for (uint32_t q = 0; q < U; ++q) un[q] = (k + U + q < len) ? __ldcs(p + 32ull * (k + U + q)) : 0u;
-#pragma unroll
-    for (uint32_t q = 0; q < U; ++q)
+    for (uint32_t q = 0; q < 8; ++q)
       if (k + q < len) c = __dadd_rn(c, x[q]);
-#pragma unroll
-    for (uint32_t q = 0; q < U; ++q) u[q] = un[q];
   }
   return c;
 }
@@ -195,31 +218,44 @@ __device__ __forceinline__ double segment_sum(const uint32_t* __restrict__ sell,
 // Does any element of this lane's SELL segment hit a pending vertex?
 __device__ __forceinline__ bool segment_any_pending(const uint32_t* __restrict__ sell, uint64_t base, unsigned lane,
                                                     uint32_t len, const uint8_t* __restrict__ np) {
-  constexpr uint32_t U = 8;
-  const uint32_t* p = sell + base + lane;
+  const uint32_t* p = sell + base + 4u * lane;
+  const uint4 z = make_uint4(0, 0, 0, 0);
   bool found = false;
-  for (uint32_t k = 0;; k += U) {
+  for (uint32_t k = 0;; k += 8) {
     const bool active = !found && k < len;
     if (!__any_sync(kFull, active)) break;
     if (active) {
-      uint32_t u[U];
+      const uint4 a = ld_idx4(p + 32ull * k);
+      const uint4 b = (k + 4 < len) ? ld_idx4(p + 32ull * (k + 4)) : z;
+      const uint32_t u[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
-      for (uint32_t q = 0; q < U; ++q) u[q] = (k + q < len) ? __ldcs(p + 32ull * (k + q)) : 0u;
-#pragma unroll
-      for (uint32_t q = 0; q < U; ++q)
+      for (uint32_t q = 0; q < 8; ++q)
         if (k + q < len && np[u[q]]) found = true;
     }
   }
   return found;
 }
 
+// The sweep kernels run one 1024-thread CTA per SM (persistent); each CTA
+// first copies the hot prefix of the previous contributions into its shared
+// memory (coalesced, L2-resident: hot vertices were just written).
+constexpr int kSweepThreads = 1024;
+constexpr int kSweepWarps = kSweepThreads / 32;
+
+__device__ __forceinline__ void load_hot(double* s_hot, const double* __restrict__ contrib, uint32_t hot) {
+  for (uint32_t i = threadIdx.x; i < hot; i += kSweepThreads) s_hot[i] = __ldg(contrib + i);
+  __syncthreads();
+}
+
 // ---- single-segment vertices: warp per 32-vertex slice ------------------------
 template <bool FLAGGED, bool CLOSED>
-__global__ void __launch_bounds__(kThreads) k_sweep_single(SweepArgs a) {
+__global__ void __launch_bounds__(kSweepThreads, 1) k_sweep_single(SweepArgs a) {
+  extern __shared__ double s_hot[];
+  load_hot(s_hot, a.contrib_prev, a.hot);
   Acc acc;
   const unsigned lane = lane_id();
-  const uint64_t nw = (uint64_t)gridDim.x * kWarps;
-  for (uint64_t s = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) / 32; s < a.n_sslices; s += nw) {
+  const uint64_t nw = (uint64_t)gridDim.x * kSweepWarps;
+  for (uint64_t s = ((uint64_t)blockIdx.x * kSweepThreads + threadIdx.x) / 32; s < a.n_sslices; s += nw) {
     const uint64_t vv = (uint64_t)a.M + s * 32 + lane;
     const bool valid = vv < a.n;
     const uint32_t v = (uint32_t)vv;
@@ -228,14 +264,15 @@ __global__ void __launch_bounds__(kThreads) k_sweep_single(SweepArgs a) {
     if (FLAGGED) aff = valid && a.va[v];
     const uint32_t len = aff ? deg : 0u;
     const uint32_t Lw = __reduce_max_sync(kFull, len);
-    double pv = 0.0;
+    double pv = 0.0, cself = 0.0;
     uint32_t od = 0;
-    if (aff) {  // prefetch the epilogue operands under the gather latency
+    if (aff) {  // prefetch the epilogue operands (and the self-loop term)
       pv = a.rank_prev[v];
       od = a.outdeg[v];
+      cself = a.contrib_prev[v];
     }
     double c = 0.0;
-    if (Lw) c = segment_sum(a.sell_s, a.sbase[s], lane, len, Lw, a.contrib_prev);
+    if (Lw) c = segment_sum(a.sell_s, a.sbase[s], lane, len, Lw, a.contrib_prev, s_hot, a.hot, v, cself);
     bool pend = false, lowout = false;
     if (valid) {
       if (!aff) {
@@ -253,19 +290,25 @@ __global__ void __launch_bounds__(kThreads) k_sweep_single(SweepArgs a) {
 
 // ---- multi vertices: warp per slice of 32 chunks -> partials -------------------
 template <bool FLAGGED>
-__global__ void __launch_bounds__(kThreads) k_sweep_mseg(SweepArgs a) {
+__global__ void __launch_bounds__(kSweepThreads, 1) k_sweep_mseg(SweepArgs a) {
+  extern __shared__ double s_hot[];
+  load_hot(s_hot, a.contrib_prev, a.hot);
   const unsigned lane = lane_id();
-  const uint64_t nw = (uint64_t)gridDim.x * kWarps;
-  for (uint64_t s = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) / 32; s < a.n_mslices; s += nw) {
+  const uint64_t nw = (uint64_t)gridDim.x * kSweepWarps;
+  for (uint64_t s = ((uint64_t)blockIdx.x * kSweepThreads + threadIdx.x) / 32; s < a.n_mslices; s += nw) {
     const uint64_t seg = s * 32 + lane;
-    uint32_t len = 0;
+    uint32_t len = 0, v = 0xffffffffu;
     if (seg < a.n_mseg) {
       len = a.mseg_len[seg];
-      if (FLAGGED && !a.va[a.mseg_v[seg]]) len = 0;
+      v = a.mseg_v[seg];
+      if (FLAGGED && !a.va[v]) len = 0;
     }
     const uint32_t Lw = __reduce_max_sync(kFull, len);
     if (!Lw) continue;
-    const double c = segment_sum(a.sell_m, a.mbase[s], lane, len, Lw, a.contrib_prev);
+    // multi vertices are hubs (new ids < M <= hot in practice): their own
+    // contribution is already served from shared memory
+    const double c = segment_sum(a.sell_m, a.mbase[s], lane, len, Lw, a.contrib_prev, s_hot, a.hot, 0xffffffffu,
+                                 0.0);
     if (len) a.partials[seg] = c;
   }
 }
@@ -548,6 +591,10 @@ unsigned persistent_grid(dynpr_context* ctx, K kernel, uint64_t work_blocks) {
     if (keys[i] == (const void*)kernel) per_sm = vals[i];
   if (per_sm < 0) {
     int b = 0;
+    // these kernels use ~200 B of shared memory: give the SM's unified
+    // L1/shared SRAM to L1 (it holds the hot contribution prefix)
+    cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+    cudaGetLastError();
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, kThreads, 0) != cudaSuccess || b < 1) {
       cudaGetLastError();
       b = 1;
@@ -610,24 +657,51 @@ SweepArgs layout_args(const Layout* L, double* partials) {
   a.pbase = L->pbase;
   a.sell_m = L->sell_m;
   a.partials = partials;
+  // Hot prefix held in L1: ~200 KB of L1 per SM (shared-memory carveout 0)
+  // = 25,600 contributions; DYNPR_HOT overrides for tuning.
+  static const uint32_t hot_default = [] {
+    const char* e = std::getenv("DYNPR_HOT");
+    return e ? (uint32_t)std::strtoul(e, nullptr, 10) : 24576u;
+  }();
+  a.hot = L->n < hot_default ? L->n : hot_default;
   return a;
+}
+
+// Grid for the 1024-thread smem-cached sweep kernels: one CTA per SM (fewer
+// when the work is small); raises the dynamic shared-memory limit once.
+template <class K>
+unsigned sweep_grid(dynpr_context* ctx, K kernel, uint64_t slices, size_t smem) {
+  static const void* done[16] = {};
+  bool seen = false;
+  for (int i = 0; i < 16 && done[i]; ++i) seen |= done[i] == (const void*)kernel;
+  if (!seen) {
+    DYNPR_CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    for (int i = 0; i < 16; ++i)
+      if (!done[i]) {
+        done[i] = (const void*)kernel;
+        break;
+      }
+  }
+  (void)smem;
+  const uint64_t blocks = (slices + kSweepWarps - 1) / kSweepWarps;
+  return (unsigned)(blocks < 1 ? 1 : (blocks < (uint64_t)ctx->num_sms ? blocks : (uint64_t)ctx->num_sms));
 }
 
 void launch_sweep(dynpr_context* ctx, const SweepArgs& a, bool flagged, bool closed) {
   cudaStream_t st = ctx->stream;
-  const uint64_t single_blocks = (a.n_sslices + kWarps - 1) / kWarps;
-  const uint64_t mseg_blocks = (a.n_mslices + kWarps - 1) / kWarps;
   const unsigned g_mfinal = grid_for(a.M, kThreads);
+  const size_t smem = (size_t)(a.hot ? a.hot : 1) * sizeof(double);
   unsigned launched = 0;
 #define DYNPR_SWEEP(F, C)                                                                           \
   do {                                                                                              \
     if (a.n_mslices) {                                                                              \
-      k_sweep_mseg<F><<<persistent_grid(ctx, k_sweep_mseg<F>, mseg_blocks), kThreads, 0, st>>>(a); \
+      k_sweep_mseg<F><<<sweep_grid(ctx, k_sweep_mseg<F>, a.n_mslices, smem), kSweepThreads, smem,   \
+                        st>>>(a);                                                                   \
       ++launched;                                                                                   \
     }                                                                                               \
     if (a.n_sslices) {                                                                              \
-      k_sweep_single<F, C>                                                                          \
-          <<<persistent_grid(ctx, k_sweep_single<F, C>, single_blocks), kThreads, 0, st>>>(a);      \
+      k_sweep_single<F, C><<<sweep_grid(ctx, k_sweep_single<F, C>, a.n_sslices, smem), kSweepThreads, \
+                             smem, st>>>(a);                                                        \
       ++launched;                                                                                   \
     }                                                                                               \
     if (a.M) {                                                                                      \

@@ -34,6 +34,7 @@ struct SweepArgs {
   const uint32_t* pbase;
   const uint32_t* sell_m;
   double* partials;
+  uint32_t hot;  // new ids < hot: contributions kept L1-resident (evict_last)
   // iteration state
   double alpha, teleport, tf, tp;
   const double* rank_prev;
