@@ -113,6 +113,28 @@ dynpr_status dynpr_context_set_profiling(dynpr_context* ctx, int enable);
 dynpr_status dynpr_context_sweep_times(dynpr_context* ctx, double* total_ms,
                                        uint64_t* sweeps, uint64_t* bytes);
 
+/* ---- multi-GPU (the reference is single-node CPU only) -------- */
+/* One process per GPU: rank 0 obtains a 128-byte NCCL unique id, shares it
+ * (e.g. torch.distributed broadcast), every rank creates its context.  The
+ * engines are then called SPMD with identical (replicated) graphs and
+ * inputs: each rank sweeps its edge-balanced vertex range, contributions and
+ * pending flags are all-gathered over NVLink after every sweep, and every
+ * rank returns the full result.  NCCL is loaded at run time (dlopen). */
+dynpr_status dynpr_nccl_get_unique_id(uint8_t* id128);
+dynpr_status dynpr_context_create_nccl(int device, int rank, int world,
+                                       const uint8_t* id128,
+                                       dynpr_context** out);
+/* The same partitioned engine with `world` virtual ranks on host threads of
+ * one process (any devices, typically one): the test harness of the
+ * multi-GPU path on a single GPU. */
+typedef struct dynpr_team dynpr_team;
+dynpr_status dynpr_team_create(int world, dynpr_team** out);
+dynpr_status dynpr_team_destroy(dynpr_team* team);
+dynpr_status dynpr_context_create_team(int device, dynpr_team* team, int rank,
+                                       dynpr_context** out);
+dynpr_status dynpr_context_rank(const dynpr_context* ctx, int* rank,
+                                int* world);
+
 /* ---- graphs (graph.hpp:17-80) ------------------------------------------- */
 /* CsrGraph(vertexCount, offsets, targets) incl. validation (graph.cpp:30-49).
  * offsets has n+1 entries, targets offsets[n] entries. */

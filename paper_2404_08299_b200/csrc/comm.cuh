@@ -1,0 +1,46 @@
+// Multi-GPU exchange for the range-partitioned engine.
+//
+// One process (or, for LocalComm, one host thread) per rank; every rank
+// holds the full graph and layout, owns a contiguous edge-balanced range of
+// the relabelled vertex space, and per sweep exchanges
+//   * allgatherv of the owned slice of the contribution vector (8 B/vertex),
+//   * allreduce of the 40-byte SweepRed (max of the L-inf bits, sums),
+//   * (DF/DF-P) allgatherv of the owned pending flags (1 B/vertex).
+// NcclComm implements this with NCCL over NVLink (grouped ncclBroadcast =
+// allgatherv, ncclAllReduce), NCCL resolved at run time with dlopen so the
+// library has no link-time NCCL dependency.  LocalComm runs P virtual ranks
+// on threads of one process (same device or not) with the identical engine
+// code path, which is how the partitioned engine is tested bit-exactly on a
+// single GPU.
+#pragma once
+
+#include <memory>
+
+#include "common.cuh"
+
+namespace dynpr_b200 {
+
+class Comm {
+ public:
+  virtual ~Comm() = default;
+  int rank = 0;
+  int world = 1;
+  // In place on `buf` (device): rank r's bytes are [off[r], off[r+1]).
+  virtual void allgatherv(void* buf, const uint64_t* off, cudaStream_t st) = 0;
+  // In place on a device SweepRed: delta_bits max, the counters summed.
+  virtual void allreduce_red(SweepRed* red, cudaStream_t st) = 0;
+  virtual void barrier() = 0;
+};
+
+// 128-byte NCCL unique id (ncclUniqueId) from the rank-0 process.
+dynpr_status nccl_unique_id(void* out128);
+std::unique_ptr<Comm> make_nccl_comm(int rank, int world, const void* id128);
+
+// P virtual ranks in one process: a shared rendezvous the P rank contexts
+// attach to.
+struct LocalTeam;
+std::shared_ptr<LocalTeam> make_local_team(int world);
+int local_team_world(const LocalTeam& t);
+std::unique_ptr<Comm> make_local_comm(std::shared_ptr<LocalTeam> team, int rank, int device);
+
+}  // namespace dynpr_b200

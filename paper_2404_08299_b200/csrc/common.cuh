@@ -94,10 +94,12 @@ struct SweepRed {
 // Out-edges per expansion work item of a high out-degree vertex.
 constexpr uint32_t kExpandChunk = 1024;
 
+class Comm;
 }  // namespace dynpr_b200
 
 struct dynpr_context {
   int device = 0;
+  dynpr_b200::Comm* comm = nullptr;  // owned; null = single GPU
   int num_sms = 148;
   cudaStream_t stream = nullptr;
   uint64_t launches = 0;

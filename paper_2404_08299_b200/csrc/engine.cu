@@ -20,6 +20,7 @@
 #include <string>
 
 #include "layout.cuh"
+#include "comm.cuh"
 #include "sweep.cuh"
 
 namespace dynpr_b200 {
@@ -163,12 +164,41 @@ void solve(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynpr_sta
   a.pend_high = ph;
   a.red = red;
 
+  // Multi-GPU: this rank sweeps only its edge-balanced vertex
+  // range; contributions (and DF pending flags) are all-gathered after
+  // every sweep and the reduction record all-reduced, so every rank takes
+  // the same convergence / expansion decisions.
+  Comm* comm = ctx->comm;
+  const bool dist = comm && comm->world > 1;
+  std::vector<uint64_t> off_c, off_f;  // allgatherv byte offsets: f64 / u8 per vertex
+  if (dist) {
+    const std::vector<RankRange> plan = plan_ranges(ctx, const_cast<Layout*>(L), comm->world);
+    const RankRange& me = plan[comm->rank];
+    a.v_lo = me.v_lo;
+    a.v_hi = me.v_hi;
+    a.ss_lo = me.ss_lo;
+    a.ss_hi = me.ss_hi;
+    a.ms_lo = me.ms_lo;
+    a.ms_hi = me.ms_hi;
+    off_c.resize(comm->world + 1);
+    off_f.resize(comm->world + 1);
+    for (int r = 0; r < comm->world; ++r) {
+      off_c[r] = 8ull * plan[r].v_lo;
+      off_f[r] = plan[r].v_lo;
+    }
+    off_c[comm->world] = 8ull * n;
+    off_f[comm->world] = n;
+  }
+
   dynpr_stats res{};
   int cur = 0;  // R[cur] holds the latest iterate ("previous")
   for (int iter = 0; iter < c.max_iterations; ++iter) {
     DYNPR_CK(cudaMemsetAsync(red, 0, sizeof(SweepRed), st));
     if (obs && sp.flagged) {
-      launch_scatter_inv_u8(ctx, L, va, obs_flags);
+      uint8_t* snap = obs_flags + n;  // owned entries are current on each rank
+      DYNPR_CK(cudaMemcpyAsync(snap, va, n, cudaMemcpyDeviceToDevice, st));
+      if (dist) comm->allgatherv(snap, off_f.data(), st);
+      launch_scatter_inv_u8(ctx, L, snap, obs_flags);
       DYNPR_CK(cudaMemcpyAsync(h_flags.data(), obs_flags, n, cudaMemcpyDeviceToHost, st));
     }
     a.rank_prev = R[cur];
@@ -178,6 +208,12 @@ void solve(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynpr_sta
     if (ctx->profiling) DYNPR_CK(cudaEventRecord(ctx->ev_s0, st));
     launch_sweep(ctx, a, sp.flagged, sp.closed);
     if (ctx->profiling) DYNPR_CK(cudaEventRecord(ctx->ev_s1, st));
+    if (dist) {
+      comm->allreduce_red(red, st);
+      comm->allgatherv(CB[cur ^ 1], off_c.data(), st);
+      if (sp.flagged) comm->allgatherv(np, off_f.data(), st);
+      if (obs) comm->allgatherv(R[cur ^ 1], off_c.data(), st);
+    }
     const SweepRed r = read_red(ctx, red);
     if (ctx->profiling) {
       float ms = 0.f;
@@ -209,7 +245,9 @@ void solve(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynpr_sta
       // push touches the pending vertices' out-edges; pull scans at most
       // the in-edges of the vertices that were not processed this sweep
       const uint64_t pull_bound = gT->m > r.edges ? gT->m - r.edges : 0;
-      if (r.pend_edges > pull_bound) {
+      // multi-GPU: pending flags are replicated, each rank pulls into its
+      // own rows (no remote writes)
+      if (dist || r.pend_edges > pull_bound) {
         launch_pull_expand(ctx, a);
         ctx->pull_expansions += 1;
       } else {
@@ -221,6 +259,7 @@ void solve(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynpr_sta
   // when the caller's buffer is on the host)
   const bool host_out = !is_device_ptr(ranks_out);
   double* out_dev = host_out ? R[cur ^ 1] : ranks_out;
+  if (dist) comm->allgatherv(R[cur], off_c.data(), st);  // every rank returns the full vector
   launch_scatter_inv_f64(ctx, L, R[cur], out_dev);
   DYNPR_CK(cudaEventRecord(ctx->ev_b, st));
   if (host_out) DYNPR_CK(cudaMemcpyAsync(ranks_out, out_dev, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
@@ -287,11 +326,74 @@ dynpr_status dynpr_context_create(int device, dynpr_context** out) {
   });
 }
 
+// ---- multi-GPU contexts ------------------------------------------------------------
+struct dynpr_team {
+  std::shared_ptr<dynpr_b200::LocalTeam> team;
+};
+
+dynpr_status dynpr_nccl_get_unique_id(uint8_t* id128) {
+  if (!id128) {
+    set_last_error("null argument");
+    return DYNPR_INVALID_ARGUMENT;
+  }
+  return nccl_unique_id(id128);
+}
+
+dynpr_status dynpr_context_create_nccl(int device, int rank, int world, const uint8_t* id128,
+                                       dynpr_context** out) {
+  dynpr_status st = dynpr_context_create(device, out);
+  if (st != DYNPR_OK) return st;
+  st = api_guard([&] {
+    if (world < 1 || rank < 0 || rank >= world || !id128) invalid("dynpr_context_create_nccl: bad rank/world");
+    (*out)->comm = make_nccl_comm(rank, world, id128).release();
+  });
+  if (st != DYNPR_OK) {
+    dynpr_context_destroy(*out);
+    *out = nullptr;
+  }
+  return st;
+}
+
+dynpr_status dynpr_team_create(int world, dynpr_team** out) {
+  return api_guard([&] {
+    if (!out || world < 1) invalid("dynpr_team_create: bad world size");
+    *out = new dynpr_team{make_local_team(world)};
+  });
+}
+
+dynpr_status dynpr_team_destroy(dynpr_team* t) {
+  return api_guard([&] { delete t; });
+}
+
+dynpr_status dynpr_context_create_team(int device, dynpr_team* team, int rank, dynpr_context** out) {
+  dynpr_status st = dynpr_context_create(device, out);
+  if (st != DYNPR_OK) return st;
+  st = api_guard([&] {
+    if (!team || rank < 0 || rank >= local_team_world(*team->team)) invalid("dynpr_context_create_team: bad rank");
+    (*out)->comm = make_local_comm(team->team, rank, device).release();
+  });
+  if (st != DYNPR_OK) {
+    dynpr_context_destroy(*out);
+    *out = nullptr;
+  }
+  return st;
+}
+
+dynpr_status dynpr_context_rank(const dynpr_context* ctx, int* rank, int* world) {
+  return api_guard([&] {
+    if (!ctx) invalid("null context");
+    if (rank) *rank = ctx->comm ? ctx->comm->rank : 0;
+    if (world) *world = ctx->comm ? ctx->comm->world : 1;
+  });
+}
+
 dynpr_status dynpr_context_destroy(dynpr_context* ctx) {
   return api_guard([&] {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    delete ctx->comm;
+    ctx->comm = nullptr;
     if (ctx->ev_a) cudaEventDestroy(ctx->ev_a);
     if (ctx->ev_b) cudaEventDestroy(ctx->ev_b);
     if (ctx->ev_s0) cudaEventDestroy(ctx->ev_s0);

@@ -34,6 +34,13 @@ __host__ __device__ __forceinline__ uint64_t sell_pos(uint64_t base, uint32_t la
   return base + 128ull * (k >> 2) + 4u * lane + (k & 3u);
 }
 
+// One rank's share of the sweep work (multi-GPU): vertices [v_lo, v_hi),
+// single-region slices [ss_lo, ss_hi), multi-region slices [ms_lo, ms_hi).
+struct RankRange {
+  uint32_t v_lo, v_hi;
+  uint64_t ss_lo, ss_hi, ms_lo, ms_hi;
+};
+
 struct Layout {
   dynpr_context* ctx = nullptr;
   uint32_t n = 0;
@@ -62,6 +69,9 @@ struct Layout {
   uint64_t* offF = nullptr;
   uint32_t* tgtF = nullptr;
   double build_ms = 0.0;       // device time of the last (re)build
+  // multi-GPU partition cache (sweep.cu plan_ranges)
+  int plan_world = 0;
+  std::vector<RankRange> plan;
   ~Layout();
 };
 

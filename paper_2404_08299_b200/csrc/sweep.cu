@@ -177,15 +177,18 @@ __device__ __forceinline__ uint4 ld_idx4(const uint32_t* p) {
                : "l"(p));
   return v;
 }
-// A contribution: the vertex's own (self-loop) value from a register, the
-// hot prefix (new ids < hot, the most-gathered vertices) from the CTA's
-// shared-memory copy, everything else from global memory.  Random 8-byte
-// reads: shared memory 1415 G/s vs L2-resident global 288 G/s on B200
-// (profiles/microbench_gather.cu).
+// A contribution: the vertex's own (self-loop) value from a register (it
+// was loaded coalesced with the vertex's other operands), everything else
+// through the read-only path.  A shared-memory cache of the hottest
+// contributions was measured and rejected (profiles/r01/README.md): it
+// served only ~15% of RMAT-24 gathers and its 1024-thread CTAs halved
+// occupancy; random 8-byte gathers top out near 288 G/s from L2
+// (profiles/microbench_gather.cu), which is what bounds this sweep.
 __device__ __forceinline__ double ld_contrib(const double* __restrict__ contrib, const double* s_hot, uint32_t u,
                                              uint32_t hot, uint32_t self, double cself) {
-  if (u == self) return cself;
-  return u < hot ? s_hot[u] : __ldg(contrib + u);
+  (void)s_hot;
+  (void)hot;
+  return u == self ? cself : __ldg(contrib + u);
 }
 
 // Lane-sequential sum of one SELL-32x4 segment (layout.cuh sell_pos):
@@ -236,26 +239,18 @@ __device__ __forceinline__ bool segment_any_pending(const uint32_t* __restrict__
   return found;
 }
 
-// The sweep kernels run one 1024-thread CTA per SM (persistent); each CTA
-// first copies the hot prefix of the previous contributions into its shared
-// memory (coalesced, L2-resident: hot vertices were just written).
-constexpr int kSweepThreads = 1024;
+// Sweep kernels: persistent grids of 256-thread CTAs at full occupancy.
+constexpr int kSweepThreads = kThreads;
 constexpr int kSweepWarps = kSweepThreads / 32;
-
-__device__ __forceinline__ void load_hot(double* s_hot, const double* __restrict__ contrib, uint32_t hot) {
-  for (uint32_t i = threadIdx.x; i < hot; i += kSweepThreads) s_hot[i] = __ldg(contrib + i);
-  __syncthreads();
-}
 
 // ---- single-segment vertices: warp per 32-vertex slice ------------------------
 template <bool FLAGGED, bool CLOSED>
-__global__ void __launch_bounds__(kSweepThreads, 1) k_sweep_single(SweepArgs a) {
-  extern __shared__ double s_hot[];
-  load_hot(s_hot, a.contrib_prev, a.hot);
+__global__ void __launch_bounds__(kSweepThreads, 5) k_sweep_single(SweepArgs a) {
+  const double* s_hot = nullptr;
   Acc acc;
   const unsigned lane = lane_id();
   const uint64_t nw = (uint64_t)gridDim.x * kSweepWarps;
-  for (uint64_t s = ((uint64_t)blockIdx.x * kSweepThreads + threadIdx.x) / 32; s < a.n_sslices; s += nw) {
+  for (uint64_t s = a.ss_lo + ((uint64_t)blockIdx.x * kSweepThreads + threadIdx.x) / 32; s < a.ss_hi; s += nw) {
     const uint64_t vv = (uint64_t)a.M + s * 32 + lane;
     const bool valid = vv < a.n;
     const uint32_t v = (uint32_t)vv;
@@ -290,23 +285,22 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep_single(SweepArgs a) 
 
 // ---- multi vertices: warp per slice of 32 chunks -> partials -------------------
 template <bool FLAGGED>
-__global__ void __launch_bounds__(kSweepThreads, 1) k_sweep_mseg(SweepArgs a) {
-  extern __shared__ double s_hot[];
-  load_hot(s_hot, a.contrib_prev, a.hot);
+__global__ void __launch_bounds__(kSweepThreads) k_sweep_mseg(SweepArgs a) {
+  const double* s_hot = nullptr;
   const unsigned lane = lane_id();
   const uint64_t nw = (uint64_t)gridDim.x * kSweepWarps;
-  for (uint64_t s = ((uint64_t)blockIdx.x * kSweepThreads + threadIdx.x) / 32; s < a.n_mslices; s += nw) {
+  for (uint64_t s = a.ms_lo + ((uint64_t)blockIdx.x * kSweepThreads + threadIdx.x) / 32; s < a.ms_hi; s += nw) {
     const uint64_t seg = s * 32 + lane;
     uint32_t len = 0, v = 0xffffffffu;
     if (seg < a.n_mseg) {
       len = a.mseg_len[seg];
       v = a.mseg_v[seg];
+      if (v < a.v_lo || v >= a.v_hi) len = 0;  // another rank's vertex
       if (FLAGGED && !a.va[v]) len = 0;
     }
     const uint32_t Lw = __reduce_max_sync(kFull, len);
     if (!Lw) continue;
-    // multi vertices are hubs (new ids < M <= hot in practice): their own
-    // contribution is already served from shared memory
+    // (a multi vertex's self-loop is one gather among >256: not special-cased)
     const double c = segment_sum(a.sell_m, a.mbase[s], lane, len, Lw, a.contrib_prev, s_hot, a.hot, 0xffffffffu,
                                  0.0);
     if (len) a.partials[seg] = c;
@@ -318,12 +312,13 @@ template <bool FLAGGED, bool CLOSED>
 __global__ void __launch_bounds__(kThreads) k_sweep_mfinal(SweepArgs a) {
   Acc acc;
   const uint64_t stride = (uint64_t)gridDim.x * kThreads;
-  for (uint64_t base = (uint64_t)blockIdx.x * kThreads; base < a.M; base += stride) {
+  const uint64_t vend = a.M < a.v_hi ? a.M : a.v_hi;
+  for (uint64_t base = a.v_lo + (uint64_t)blockIdx.x * kThreads; base < vend; base += stride) {
     const uint64_t vv = base + threadIdx.x;
     bool pend = false, lowout = false;
     const uint32_t v = (uint32_t)vv;
     uint32_t od = 0;
-    if (vv < a.M) {
+    if (vv < vend) {
       if (FLAGGED && !a.va[v]) {
         copy_through(a, v);
       } else {
@@ -347,7 +342,7 @@ __global__ void __launch_bounds__(kThreads) k_sweep_mfinal(SweepArgs a) {
 __global__ void __launch_bounds__(kThreads) k_pull_single(SweepArgs a) {
   const unsigned lane = lane_id();
   const uint64_t nw = (uint64_t)gridDim.x * kWarps;
-  for (uint64_t s = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) / 32; s < a.n_sslices; s += nw) {
+  for (uint64_t s = a.ss_lo + ((uint64_t)blockIdx.x * kThreads + threadIdx.x) / 32; s < a.ss_hi; s += nw) {
     const uint64_t vv = (uint64_t)a.M + s * 32 + lane;
     const bool need = vv < a.n && !a.va[vv];
     const uint32_t len = need ? a.indeg[vv] : 0u;
@@ -358,12 +353,12 @@ __global__ void __launch_bounds__(kThreads) k_pull_single(SweepArgs a) {
 __global__ void __launch_bounds__(kThreads) k_pull_mseg(SweepArgs a) {
   const unsigned lane = lane_id();
   const uint64_t nw = (uint64_t)gridDim.x * kWarps;
-  for (uint64_t s = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) / 32; s < a.n_mslices; s += nw) {
+  for (uint64_t s = a.ms_lo + ((uint64_t)blockIdx.x * kThreads + threadIdx.x) / 32; s < a.ms_hi; s += nw) {
     const uint64_t seg = s * 32 + lane;
     uint32_t len = 0, v = 0;
     if (seg < a.n_mseg) {
       v = a.mseg_v[seg];
-      if (!a.va[v]) len = a.mseg_len[seg];
+      if (v >= a.v_lo && v < a.v_hi && !a.va[v]) len = a.mseg_len[seg];
     }
     if (!__any_sync(kFull, len != 0)) continue;
     if (segment_any_pending(a.sell_m, a.mbase[s], lane, len, a.np)) a.va[v] = 1;
@@ -664,47 +659,84 @@ SweepArgs layout_args(const Layout* L, double* partials) {
     return e ? (uint32_t)std::strtoul(e, nullptr, 10) : 24576u;
   }();
   a.hot = L->n < hot_default ? L->n : hot_default;
+  a.v_lo = 0;
+  a.v_hi = L->n;
+  a.ss_lo = 0;
+  a.ss_hi = L->n_sslices;
+  a.ms_lo = 0;
+  a.ms_hi = L->n_mslices;
   return a;
 }
 
-// Grid for the 1024-thread smem-cached sweep kernels: one CTA per SM (fewer
-// when the work is small); raises the dynamic shared-memory limit once.
+std::vector<RankRange> plan_ranges(dynpr_context* ctx, Layout* L, int world) {
+  if (L->plan_world == world) return L->plan;
+  const uint32_t n = L->n, M = L->M;
+  std::vector<uint32_t> indeg(n), pbase((size_t)M + 1);
+  DYNPR_CK(cudaMemcpy(indeg.data(), L->indeg, (size_t)n * 4, cudaMemcpyDeviceToHost));
+  DYNPR_CK(cudaMemcpy(pbase.data(), L->pbase, ((size_t)M + 1) * 4, cudaMemcpyDeviceToHost));
+  (void)ctx;
+  // boundaries at equal shares of the in-edges (each owned edge is one gather)
+  std::vector<uint32_t> cut(world + 1, 0);
+  cut[world] = n;
+  uint64_t acc = 0;
+  int r = 1;
+  for (uint32_t v = 0; v < n && r < world; ++v) {
+    acc += indeg[v];
+    while (r < world && acc * (uint64_t)world >= L->m * (uint64_t)r) {
+      uint32_t c = v + 1;
+      if (c > M) c = M + ((c - M + 31) / 32) * 32;  // whole single-region slices
+      if (c > n) c = n;
+      cut[r++] = c;
+    }
+  }
+  while (r < world) cut[r++] = n;
+  for (int i = 1; i <= world; ++i)
+    if (cut[i] < cut[i - 1]) cut[i] = cut[i - 1];
+  std::vector<RankRange> plan(world);
+  for (int i = 0; i < world; ++i) {
+    RankRange& p = plan[i];
+    p.v_lo = cut[i];
+    p.v_hi = cut[i + 1];
+    p.ss_lo = p.v_lo <= M ? 0 : (p.v_lo - M) / 32;
+    p.ss_hi = p.v_hi <= M ? 0 : (p.v_hi - M + 31) / 32;
+    if (p.ss_hi < p.ss_lo) p.ss_hi = p.ss_lo;
+    const uint32_t mlo = p.v_lo < M ? p.v_lo : M, mhi = p.v_hi < M ? p.v_hi : M;
+    p.ms_lo = pbase[mlo] / 32;
+    p.ms_hi = (pbase[mhi] + 31) / 32;
+    if (mhi <= mlo) p.ms_lo = p.ms_hi = 0;
+  }
+  L->plan = plan;
+  L->plan_world = world;
+  return plan;
+}
+
+// Persistent grid for the sweep kernels (resident CTAs per SM x SMs).
 template <class K>
 unsigned sweep_grid(dynpr_context* ctx, K kernel, uint64_t slices, size_t smem) {
-  static const void* done[16] = {};
-  bool seen = false;
-  for (int i = 0; i < 16 && done[i]; ++i) seen |= done[i] == (const void*)kernel;
-  if (!seen) {
-    DYNPR_CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    for (int i = 0; i < 16; ++i)
-      if (!done[i]) {
-        done[i] = (const void*)kernel;
-        break;
-      }
-  }
   (void)smem;
-  const uint64_t blocks = (slices + kSweepWarps - 1) / kSweepWarps;
-  return (unsigned)(blocks < 1 ? 1 : (blocks < (uint64_t)ctx->num_sms ? blocks : (uint64_t)ctx->num_sms));
+  return persistent_grid(ctx, kernel, (slices + kSweepWarps - 1) / kSweepWarps);
 }
 
 void launch_sweep(dynpr_context* ctx, const SweepArgs& a, bool flagged, bool closed) {
   cudaStream_t st = ctx->stream;
-  const unsigned g_mfinal = grid_for(a.M, kThreads);
-  const size_t smem = (size_t)(a.hot ? a.hot : 1) * sizeof(double);
+  const uint64_t mv = (a.M < a.v_hi ? a.M : a.v_hi) > a.v_lo ? (a.M < a.v_hi ? a.M : a.v_hi) - a.v_lo : 0;
+  const unsigned g_mfinal = grid_for(mv, kThreads);
+  const uint64_t n_ms = a.ms_hi - a.ms_lo, n_ss = a.ss_hi - a.ss_lo;
+  const size_t smem = 0;
   unsigned launched = 0;
 #define DYNPR_SWEEP(F, C)                                                                           \
   do {                                                                                              \
-    if (a.n_mslices) {                                                                              \
-      k_sweep_mseg<F><<<sweep_grid(ctx, k_sweep_mseg<F>, a.n_mslices, smem), kSweepThreads, smem,   \
+    if (n_ms) {                                                                                     \
+      k_sweep_mseg<F><<<sweep_grid(ctx, k_sweep_mseg<F>, n_ms, smem), kSweepThreads, smem,          \
                         st>>>(a);                                                                   \
       ++launched;                                                                                   \
     }                                                                                               \
-    if (a.n_sslices) {                                                                              \
-      k_sweep_single<F, C><<<sweep_grid(ctx, k_sweep_single<F, C>, a.n_sslices, smem), kSweepThreads, \
+    if (n_ss) {                                                                                     \
+      k_sweep_single<F, C><<<sweep_grid(ctx, k_sweep_single<F, C>, n_ss, smem), kSweepThreads,      \
                              smem, st>>>(a);                                                        \
       ++launched;                                                                                   \
     }                                                                                               \
-    if (a.M) {                                                                                      \
+    if (mv) {                                                                                       \
       k_sweep_mfinal<F, C><<<g_mfinal, kThreads, 0, st>>>(a);                                       \
       ++launched;                                                                                   \
     }                                                                                               \
@@ -722,13 +754,13 @@ void launch_sweep(dynpr_context* ctx, const SweepArgs& a, bool flagged, bool clo
 void launch_pull_expand(dynpr_context* ctx, const SweepArgs& a) {
   cudaStream_t st = ctx->stream;
   unsigned launched = 0;
-  if (a.n_mslices) {
-    k_pull_mseg<<<persistent_grid(ctx, k_pull_mseg, (a.n_mslices + kWarps - 1) / kWarps), kThreads, 0, st>>>(a);
+  const uint64_t n_ms = a.ms_hi - a.ms_lo, n_ss = a.ss_hi - a.ss_lo;
+  if (n_ms) {
+    k_pull_mseg<<<persistent_grid(ctx, k_pull_mseg, (n_ms + kWarps - 1) / kWarps), kThreads, 0, st>>>(a);
     ++launched;
   }
-  if (a.n_sslices) {
-    k_pull_single<<<persistent_grid(ctx, k_pull_single, (a.n_sslices + kWarps - 1) / kWarps), kThreads, 0, st>>>(
-        a);
+  if (n_ss) {
+    k_pull_single<<<persistent_grid(ctx, k_pull_single, (n_ss + kWarps - 1) / kWarps), kThreads, 0, st>>>(a);
     ++launched;
   }
   check_launch();

@@ -49,7 +49,16 @@ struct SweepArgs {
   SweepRed* red;
   int np_accumulate;  // updateRanks primitive: np |= pend, untouched otherwise
   int copy_all;       // updateRanks primitive: copy-through every unaffected
+  // owned work (multi-GPU rank; the whole graph on one GPU): vertices
+  // [v_lo, v_hi), single slices [ss_lo, ss_hi), multi slices [ms_lo, ms_hi)
+  uint32_t v_lo, v_hi;
+  uint64_t ss_lo, ss_hi, ms_lo, ms_hi;
 };
+
+// Edge-balanced partition of the layout's vertex space over `world` ranks
+// (SURVEY 8e): contiguous new-id ranges, aligned to 32-vertex slices in the
+// single region; computed on the host once per (layout, world) and cached.
+std::vector<RankRange> plan_ranges(dynpr_context* ctx, Layout* L, int world);
 
 SweepArgs layout_args(const Layout* L, double* partials);
 
