@@ -75,6 +75,12 @@ PROTOTYPES = {
     "dynpr_context_launches": (_u64, [_vp]),
     "dynpr_context_set_profiling": (_i, [_vp, _i]),
     "dynpr_context_sweep_times": (_i, [_vp, _dp, _u64p, _u64p]),
+    "dynpr_nccl_get_unique_id": (_i, [_vp]),
+    "dynpr_context_create_nccl": (_i, [_i, _i, _i, _vp, _pvp]),
+    "dynpr_team_create": (_i, [_i, _pvp]),
+    "dynpr_team_destroy": (_i, [_vp]),
+    "dynpr_context_create_team": (_i, [_i, _vp, _i, _pvp]),
+    "dynpr_context_rank": (_i, [_vp, _ip, _ip]),
     "dynpr_graph_from_csr": (_i, [_vp, _u32, _vp, _vp, _u64, _pvp]),
     "dynpr_graph_build": (_i, [_vp, _u32, _vp, _vp, _u64, _pvp]),
     "dynpr_graph_add_self_loops": (_i, [_vp, _vp, _pvp]),
