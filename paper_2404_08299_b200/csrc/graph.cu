@@ -125,26 +125,65 @@ __global__ void k_has_edge(const uint64_t* off, const uint32_t* tgt,
 // CsrGraph ctor validation (graph.cpp:38-48): per vertex, the first failing
 // check in the reference's order; the global answer is the lowest vertex.
 // Also records whether every vertex carries its self-loop.
-__global__ void k_validate_csr(const uint64_t* off, const uint32_t* tgt,
-                               uint32_t n, unsigned long long* err,
-                               int* all_loops) {
-  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
+// CsrGraph constructor validation (graph.cpp:30-49), edge-parallel.
+// Pass 1 (vertex per thread, vertices < vlim): first vertex with decreasing
+// offsets -> err[0]; marks the first edge of every non-empty row in a bitmap;
+// self-loop presence by binary search.  Pass 2 (edges < elim, 4 per thread,
+// coalesced): first edge whose target is out of range (code 2) or not above
+// its in-row predecessor (code 3) -> err[1] = i << 2 | code.  The reference
+// reports the first violation in (vertex, edge) order; the host combines the
+// two passes into exactly that one.
+__global__ void k_validate_rows(const uint64_t* off, const uint32_t* tgt, uint32_t vlim, uint64_t m,
+                                unsigned* rowstart, unsigned long long* err, int* all_loops) {
+  bool loops = true;
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < vlim;
        v += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t b = off[v], e = off[v + 1];
-    int code = 0;
-    bool loop = false;
     if (b > e) {
-      code = 1;
+      atomicMin(err, v);
+      loops = false;
+      continue;
+    }
+    if (e > m || b == e) {
+      loops = false;
+      continue;
+    }
+    atomicOr(rowstart + (b >> 5), 1u << (b & 31));
+    uint64_t lo = b, hi = e;  // lower_bound of v
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (tgt[mid] < (uint32_t)v) lo = mid + 1; else hi = mid;
+    }
+    if (lo == e || tgt[lo] != (uint32_t)v) loops = false;
+  }
+  if (!__all_sync(0xffffffffu, loops) && (threadIdx.x & 31) == 0) atomicExch(all_loops, 0);
+}
+
+__global__ void k_validate_edges(const uint32_t* tgt, uint64_t elim, uint32_t n, const unsigned* rowstart,
+                                 unsigned long long* err) {
+  const uint64_t nq = (elim + 3) / 4;
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < nq;
+       q += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i0 = 4 * q;
+    uint32_t t[5];
+    t[0] = i0 ? tgt[i0 - 1] : 0u;
+    if (i0 + 4 <= elim) {
+      const uint4 w = *reinterpret_cast<const uint4*>(tgt + i0);
+      t[1] = w.x; t[2] = w.y; t[3] = w.z; t[4] = w.w;
     } else {
-      for (uint64_t i = b; i < e; ++i) {
-        const uint32_t t = tgt[i];
-        if (t >= n) { code = 2; break; }
-        if (i > b && tgt[i - 1] >= t) { code = 3; break; }
-        loop |= (t == v);
+      for (int k = 0; k < 4; ++k) t[k + 1] = i0 + k < elim ? tgt[i0 + k] : 0u;
+    }
+    const unsigned rs = (rowstart[i0 >> 5] >> (i0 & 31)) & 0xfu;  // i0 % 4 == 0: same word
+    for (int k = 0; k < 4 && i0 + k < elim; ++k) {
+      const uint64_t i = i0 + k;
+      int code = 0;
+      if (t[k + 1] >= n) code = 2;
+      else if (i > 0 && !((rs >> k) & 1u) && t[k] >= t[k + 1]) code = 3;
+      if (code) {
+        atomicMin(err, (i << 2) | code);
+        break;
       }
     }
-    if (code) atomicMin(err, ((unsigned long long)v << 2) | code);
-    if (!loop) atomicExch(all_loops, 0);
   }
 }
 
@@ -646,26 +685,55 @@ dynpr_status dynpr_graph_from_csr(dynpr_context* ctx, uint32_t n,
     try {
       DYNPR_CK(cudaMemcpyAsync(g->off, offsets, ((size_t)n + 1) * 8, cudaMemcpyDefault, ctx->stream));
       if (m) DYNPR_CK(cudaMemcpyAsync(g->tgt, targets, m * 4, cudaMemcpyDefault, ctx->stream));
-      auto* err = scratch_u64(ctx, ctx->scratch64b, 2, kNone);
-      int* loops = reinterpret_cast<int*>(err + 1);
-      const unsigned long long init[2] = {kNone, 1ull};  // loops flag = 1
-      DYNPR_CK(cudaMemcpy(err, init, sizeof init, cudaMemcpyHostToDevice));
-      if (n) {
-        k_validate_csr<<<grid_for(n, 128, 1 << 16), 128, 0, ctx->stream>>>(g->off, g->tgt, n, err, loops);
-        check_launch();
-        count_launch(ctx);
+      // err[0]: first bad vertex (offsets), err[1]: first bad edge, err[2]: loops flag
+      auto* err = scratch_u64(ctx, ctx->scratch64b, 3, kNone);
+      int* loops = reinterpret_cast<int*>(err + 2);
+      const uint64_t words = (m + 31) / 32 + 1;
+      unsigned* rowstart = pool_alloc_n<unsigned>(ctx, words);
+      unsigned long long h[3];
+      auto run = [&](uint32_t vlim, uint64_t elim) {
+        const unsigned long long init[3] = {kNone, kNone, 1ull};  // loops flag = 1
+        DYNPR_CK(cudaMemcpyAsync(ctx->pinned, init, sizeof init, cudaMemcpyHostToDevice, ctx->stream));
+        DYNPR_CK(cudaMemcpyAsync(err, ctx->pinned, sizeof init, cudaMemcpyHostToDevice, ctx->stream));
+        DYNPR_CK(cudaMemsetAsync(rowstart, 0, words * 4, ctx->stream));
+        if (vlim) {
+          k_validate_rows<<<grid_for(vlim, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(g->off, g->tgt, vlim, m,
+                                                                                          rowstart, err, loops);
+          check_launch();
+          count_launch(ctx);
+        }
+        if (elim) {
+          k_validate_edges<<<grid_for((elim + 3) / 4, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
+              g->tgt, elim, n, rowstart, err + 1);
+          check_launch();
+          count_launch(ctx);
+        }
+        DYNPR_CK(cudaMemcpyAsync(ctx->pinned, err, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+        sync(ctx);
+        std::memcpy(h, ctx->pinned, sizeof h);
+      };
+      try {
+        run(n, m);
+        if (h[0] != kNone) {
+          // offsets decrease at v0: the reference scanned only the rows
+          // before it, whose edges are [0, off[v0]); rescan exactly those
+          const uint32_t v0 = (uint32_t)h[0];
+          uint64_t lim = 0;
+          DYNPR_CK(cudaMemcpy(&lim, g->off + v0, 8, cudaMemcpyDeviceToHost));
+          run(v0, lim < m ? lim : m);
+          h[0] = v0;
+        }
+      } catch (...) {
+        pool_free(ctx, rowstart);
+        throw;
       }
-      unsigned long long h[2];
-      DYNPR_CK(cudaMemcpyAsync(ctx->pinned, err, 16, cudaMemcpyDeviceToHost, ctx->stream));
-      sync(ctx);
-      std::memcpy(h, ctx->pinned, 16);
-      if (h[0] != kNone) {
-        const int code = (int)(h[0] & 3);
-        if (code == 1) invalid("CsrGraph: offsets must be non-decreasing");
-        if (code == 2) invalid("CsrGraph: target id out of range");
+      pool_free(ctx, rowstart);
+      if (h[1] != kNone) {
+        if ((h[1] & 3) == 2) invalid("CsrGraph: target id out of range");
         invalid("CsrGraph: target slices must be sorted and deduplicated");
       }
-      g->all_loops = n == 0 || (int)(h[1] & 0xffffffffu) == 1;
+      if (h[0] != kNone) invalid("CsrGraph: offsets must be non-decreasing");
+      g->all_loops = n == 0 || (int)(h[2] & 0xffffffffu) == 1;
     } catch (...) {
       destroy_graph(g);
       throw;
