@@ -25,8 +25,15 @@ def main():
     gt = dp.transpose(g)
     cfg = dp.EngineConfig(max_iterations=a.static_iters, convergence_check_disabled=True) \
         if a.static_iters else dp.EngineConfig()
+    dp.prepare(gt, g)
+    base = dp.static_pagerank(gt, g, cfg)  # warms the workspace
+    ctx = dp.default_context()
+    ctx.set_profiling(True)
     base = dp.static_pagerank(gt, g, cfg)
-    print(f"static: {base.iterations} it, {base.device_ms:.3f} ms")
+    ms, sweeps, nbytes = ctx.sweep_times()
+    ctx.set_profiling(False)
+    print(f"static: {base.iterations} it, {base.device_ms:.3f} ms; sweep {ms / max(sweeps, 1):.3f} ms, "
+          f"{nbytes / max(sweeps, 1) / (ms / max(sweeps, 1)) / 1e6:.0f} GB/s algorithmic")
     if a.dfp:
         b = dp.generate_random_batch(g, dp.batch_size_from_fraction(a.frac, g.edge_count), 0.8, 7)
         g2, gt2 = dp.apply_batch_pair(g, gt, b)
