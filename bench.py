@@ -153,6 +153,31 @@ def sum_over_ranks(x: float, world: int, device=None) -> float:
     return float(t.item())
 
 
+def gather_ceiling(bytes_per_sweep: float, edges_per_sweep: float, achieved: float, world: int = 1):
+    """The sweep's second roofline (profiles/r01/README.md): every in-edge is
+    one random 8-byte gather and each SM retires ~0.98 random global requests
+    per clock (measured, microbench_gather3), so a sweep cannot beat
+    edges / (SMs x clock x 0.98).  Reported beside the HBM roofline."""
+    try:
+        import torch
+        p = torch.cuda.get_device_properties(torch.cuda.current_device())
+        sms = p.multi_processor_count * world
+        clk = 1.965e9
+        try:
+            with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+                clk = float(json.load(f).get("sm_max_mhz", 1965.0)) * 1e6
+        except Exception:
+            pass
+    except Exception:
+        return None
+    if not edges_per_sweep:
+        return None
+    t = edges_per_sweep / (sms * clk * 0.98)
+    bound = bytes_per_sweep / t / 1e9
+    return {"requests_per_sm_clk": 0.98, "sweep_ms_floor": t * 1e3, "achieved_bound_gbs": bound,
+            "frac": achieved / bound if bound else None}
+
+
 def barrier(world: int):
     if world > 1:
         import torch.distributed as dist
@@ -243,7 +268,12 @@ def run_ours(args, world, rank, local):
 
     torch.cuda.set_device(local)
     scale, desc = WORKLOADS[args.workload]
-    ctx = dp.Context(local)
+    # N = 1: one GPU.  N > 1: an NCCL team over the torch.distributed group --
+    # every rank holds the (replicated) graph and sweeps its edge-balanced
+    # vertex range; contributions / pending flags are all-gathered over
+    # NVLink after every sweep.  Same graph for every N: strong
+    # scaling.
+    ctx = dp.Context(local) if world == 1 else dp.context_from_process_group(local)
     L = N.lib()
 
     # ---- setup (untimed): base graph pair, base ranks, batches ---------------
@@ -321,10 +351,10 @@ def run_ours(args, world, rank, local):
     clock = clocks.summary()
 
     static_ms_total = sum(rec["static_ms"])
-    static_edges = sum(rec["static_edges"])
+    static_edges = sum(rec["static_edges"])  # the whole graph's edges: ranks share one graph
     local_gteps = static_edges / (static_ms_total * 1e-3) / 1e9
     t_max = max_over_ranks(static_ms_total, world, f"cuda:{local}")
-    value = sum_over_ranks(static_edges, world, f"cuda:{local}") / (t_max * 1e-3) / 1e9
+    value = static_edges / (t_max * 1e-3) / 1e9
     ms_per_step = t_max / args.steps
 
     # roofline of the rank-update sweep (k_sweep_low + k_sweep_chunks + k_sweep_multi)
@@ -332,6 +362,9 @@ def run_ours(args, world, rank, local):
     sw_n = sum(s[1] for s in rec["sweep_static"])
     sw_bytes = sum(s[2] for s in rec["sweep_static"])
     peak, peak_kind = measured_peaks()
+    if world > 1:  # the sweep record is all-reduced: bytes of the whole sweep over the team
+        peak *= world
+        peak_kind += " x %d GPUs" % world
     achieved = (sw_bytes / sw_n) / ((sw_ms / sw_n) * 1e-3) / 1e9 if sw_n else 0.0
     traffic = None
     try:
@@ -347,7 +380,7 @@ def run_ours(args, world, rank, local):
         out = {
             "metric": baseline_metric(), "value": value, "unit": "GTEPS", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic RMAT (Graph500 a=.57 b=c=.19, edge factor 16, seed %d, dedup + self-loops, "
                     "generated on device); random 80/20 batches from the reference generateRandomBatch "
                     "algorithm" % args.seed,
@@ -356,7 +389,8 @@ def run_ours(args, world, rank, local):
                        "l2": "inputs larger than L2 (graph pair %.2f GB vs 126 MB L2); no flush needed"
                              % ((2 * (8 * (n + 1) + 4 * m0)) / 1e9),
                        "parallelism": "single GPU" if world == 1 else
-                       "replicas (one graph per GPU; range-partitioned NCCL path: see DESIGN.md)"},
+                       "vertex-range partitioned over %d GPUs (edge-balanced; NCCL allgather of "
+                       "contributions + allreduce of the sweep record per iteration)" % world},
             "static": {"ms_per_solve": st_ms, "iterations": statistics.mean(rec["static_it"]),
                        "gteps": local_gteps},
             "dfp": {"ms_per_solve": dfp_ms, "iterations": statistics.mean(rec["dfp_it"]),
@@ -370,9 +404,12 @@ def run_ours(args, world, rank, local):
                                "device time"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "rank-update sweep (k_sweep_low+k_sweep_chunks+k_sweep_multi), "
+                         "kernel": "rank-update sweep (k_sweep_mseg + k_sweep_single + k_sweep_mfinal), "
                                    "algorithmic bytes 4*edges + 28*vertices + 8 per sweep",
-                         "peak_source": peak_kind, "sweeps": sw_n},
+                         "peak_source": peak_kind, "sweeps": sw_n,
+                         "gather_ceiling": gather_ceiling(sw_bytes / sw_n if sw_n else 0.0,
+                                                          sum(rec["static_edges"]) / max(1, sum(rec["static_it"])),
+                                                          achieved, world)},
             "gpu_launches": launches,
             "clocks": clock,
         }

@@ -33,7 +33,8 @@ __all__ = [
     "dynamic_frontier", "dynamic_frontier_from_flags", "expand_affected", "initial_affected",
     "l1_norm_delta", "linf_norm_delta", "naive_dynamic", "partition_by_degree", "rmat_graph",
     "static_pagerank", "transpose", "update_ranks", "generate_random_batch", "batch_size_from_fraction",
-    "derive_seed", "prepare",
+    "derive_seed", "prepare", "LocalTeam", "nccl_unique_id", "share_nccl_unique_id",
+    "context_from_process_group",
 ]
 
 
@@ -118,14 +119,48 @@ def _check(rc: int) -> None:
 
 
 class Context:
-    """One CUDA device + stream + workspace (dynpr_context)."""
+    """One CUDA device + stream + workspace (dynpr_context).
 
-    def __init__(self, device: int = 0):
-        h = C.c_void_p()
-        _check(N.lib().dynpr_context_create(int(device), C.byref(h)))
-        self.h = h.value
+    A plain context solves on its own GPU.  `Context.nccl(...)` (one process
+    per GPU) and `LocalTeam(world).context(...)` (virtual ranks on host
+    threads of one process) create contexts of a range-partitioned team: the
+    engines are then called SPMD with the same graphs and inputs on every
+    rank, each rank sweeps its edge-balanced vertex range, and the
+    contributions / pending flags are all-gathered after every sweep
+    (SURVEY 8e).  Every rank returns the full result."""
+
+    def __init__(self, device: int = 0, _handle: Optional[int] = None, _keep=None):
+        if _handle is None:
+            h = C.c_void_p()
+            _check(N.lib().dynpr_context_create(int(device), C.byref(h)))
+            _handle = h.value
+        self.h = _handle
         self.device = device
+        self._keep = _keep  # a LocalTeam must outlive its contexts
         self._fin = weakref.finalize(self, N.lib().dynpr_context_destroy, C.c_void_p(self.h))
+
+    @classmethod
+    def nccl(cls, device: int, rank: int, world: int, unique_id: bytes) -> "Context":
+        """Rank `rank` of a `world`-GPU team joined through NCCL (unique_id
+        from nccl_unique_id() on rank 0, shared out of band)."""
+        if len(unique_id) != 128:
+            raise ValueError("NCCL unique id must be 128 bytes")
+        h = C.c_void_p()
+        buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+        _check(N.lib().dynpr_context_create_nccl(int(device), int(rank), int(world), buf, C.byref(h)))
+        return cls(device, _handle=h.value)
+
+    @property
+    def rank(self) -> int:
+        r, w = C.c_int(), C.c_int()
+        _check(N.lib().dynpr_context_rank(C.c_void_p(self.h), C.byref(r), C.byref(w)))
+        return r.value
+
+    @property
+    def world(self) -> int:
+        r, w = C.c_int(), C.c_int()
+        _check(N.lib().dynpr_context_rank(C.c_void_p(self.h), C.byref(r), C.byref(w)))
+        return w.value
 
     @property
     def launches(self) -> int:
@@ -138,6 +173,49 @@ class Context:
         ms, sw, by = C.c_double(), C.c_uint64(), C.c_uint64()
         _check(N.lib().dynpr_context_sweep_times(C.c_void_p(self.h), C.byref(ms), C.byref(sw), C.byref(by)))
         return ms.value, sw.value, by.value
+
+
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId on this process (rank 0 of an NCCL team)."""
+    buf = (C.c_uint8 * 128)()
+    _check(N.lib().dynpr_nccl_get_unique_id(buf))
+    return bytes(buf)
+
+
+def share_nccl_unique_id(group=None) -> bytes:
+    """Rank 0 of a torch.distributed process group (any backend) creates the
+    NCCL unique id and broadcasts it; every rank returns the same 128 bytes."""
+    import torch.distributed as dist
+    obj = [nccl_unique_id() if dist.get_rank(group) == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    return obj[0]
+
+
+def context_from_process_group(device: int, group=None) -> Context:
+    """One process per GPU (torchrun): this process's rank of an NCCL team
+    spanning the torch.distributed process group."""
+    import torch.distributed as dist
+    uid = share_nccl_unique_id(group)
+    return Context.nccl(device, dist.get_rank(group), dist.get_world_size(group), uid)
+
+
+class LocalTeam:
+    """`world` virtual ranks of the partitioned engine inside one process
+    (any devices, typically one GPU): the single-GPU test harness of the
+    multi-GPU path.  Each rank's engine call must run on its own host
+    thread (the calls meet at barriers)."""
+
+    def __init__(self, world: int):
+        h = C.c_void_p()
+        _check(N.lib().dynpr_team_create(int(world), C.byref(h)))
+        self.h = h.value
+        self.world = world
+        self._fin = weakref.finalize(self, N.lib().dynpr_team_destroy, C.c_void_p(self.h))
+
+    def context(self, device: int, rank: int) -> Context:
+        h = C.c_void_p()
+        _check(N.lib().dynpr_context_create_team(int(device), C.c_void_p(self.h), int(rank), C.byref(h)))
+        return Context(device, _handle=h.value, _keep=self)
 
 
 _default_ctx: Optional[Context] = None

@@ -1,0 +1,124 @@
+"""The range-partitioned multi-GPU engine on one B200.
+
+A LocalTeam runs P virtual ranks of the partitioned engine on host threads
+of this process, all on cuda:0, through the same engine code path as the
+NCCL team (each rank sweeps its edge-balanced vertex range; contributions,
+pending flags and the reduction record are exchanged after every sweep).
+Every rank must return exactly the single-GPU result, which itself equals
+the reference's (tests/test_gpu_engine.py).  NCCL cannot put two ranks on
+one GPU, so the NCCL transport itself is exercised only on multi-GPU boxes
+(bench.py --gpus N).
+"""
+import threading
+
+import numpy as np
+import pytest
+
+from helpers import rand_pair
+
+pytestmark = pytest.mark.gpu
+
+
+def run_team(dp, world, fn):
+    """fn(ctx, rank) on `world` threads with virtual-rank contexts."""
+    team = dp.LocalTeam(world)
+    ctxs = [team.context(0, r) for r in range(world)]
+    out, errs = [None] * world, []
+
+    def body(r):
+        try:
+            out[r] = fn(ctxs[r], r)
+        except BaseException as e:  # pragma: no cover - reported below
+            errs.append(e)
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert not errs, errs
+    assert all(o is not None for o in out)
+    return out, ctxs
+
+
+def same(a, b):
+    assert a.iterations == b.iterations
+    assert a.converged == b.converged
+    assert a.affected_vertex_iterations == b.affected_vertex_iterations
+    assert a.final_delta == b.final_delta
+    assert np.array_equal(a.ranks, b.ranks)
+
+
+def test_team_reports_rank_and_world(dp):
+    team = dp.LocalTeam(3)
+    ctxs = [team.context(0, r) for r in range(3)]
+    assert [(c.rank, c.world) for c in ctxs] == [(0, 3), (1, 3), (2, 3)]
+    assert (dp.default_context().rank, dp.default_context().world) == (0, 1)
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("scale", [10, 13])
+def test_partitioned_static_and_dfp_equal_single_gpu(dp, oracle_lib, world, scale):
+    O = oracle_lib
+    src, dst = O.rmat_edges(scale, 16 << scale)
+    og = O.add_self_loops(O.build_csr((src, dst), 1 << scale))
+    off, tgt = og.csr()
+    n = og.n
+    dels, ins = O.generate_random_batch(og, O.batch_size_from_fraction(1e-3, og.m), 0.8, 5)
+    og2, _, _ = O.apply_batch(og, dels, ins)
+    off2, tgt2 = og2.csr()
+
+    g = dp.CsrGraph.from_csr(n, off, tgt)
+    gt = dp.transpose(g)
+    base = dp.static_pagerank(gt, g)
+    g2 = dp.CsrGraph.from_csr(n, off2, tgt2)
+    gt2 = dp.transpose(g2)
+    single = {
+        "static": base,
+        "nd": dp.naive_dynamic(gt2, g2, base.ranks),
+        "df": dp.dynamic_frontier(g2, gt2, dels, ins, base.ranks, pruning=False),
+        "dfp": dp.dynamic_frontier(g2, gt2, dels, ins, base.ranks, pruning=True),
+    }
+    # the checker agrees with the single-GPU engine (bitwise)
+    ref = O.dynamic_frontier(og2, O.transpose(og2), dels, ins, O.static(O.transpose(og), og).ranks,
+                             pruning=True)
+    assert np.array_equal(single["dfp"].ranks, ref.ranks)
+
+    def fn(ctx, r):
+        h = dp.CsrGraph.from_csr(n, off, tgt, ctx=ctx)
+        ht = dp.transpose(h)
+        b = dp.static_pagerank(ht, h)
+        h2 = dp.CsrGraph.from_csr(n, off2, tgt2, ctx=ctx)
+        ht2 = dp.transpose(h2)
+        return {
+            "static": b,
+            "nd": dp.naive_dynamic(ht2, h2, b.ranks),
+            "df": dp.dynamic_frontier(h2, ht2, dels, ins, b.ranks, pruning=False),
+            "dfp": dp.dynamic_frontier(h2, ht2, dels, ins, b.ranks, pruning=True),
+        }
+
+    out, _ = run_team(dp, world, fn)
+    for r in range(world):
+        for k in single:
+            same(out[r][k], single[k])
+
+
+def test_partitioned_observer_sees_full_iterates(dp, oracle_lib):
+    O = oracle_lib
+    og, ogt = rand_pair(O, 23, 3000, 40000)
+    off, tgt = og.csr()
+    seen_single = []
+    g = dp.CsrGraph.from_csr(og.n, off, tgt)
+    dp.static_pagerank(dp.transpose(g), g, observer=lambda it, r: seen_single.append(r.copy()))
+
+    def fn(ctx, r):
+        seen = []
+        h = dp.CsrGraph.from_csr(og.n, off, tgt, ctx=ctx)
+        dp.static_pagerank(dp.transpose(h), h, observer=lambda it, x: seen.append(x.copy()))
+        return seen
+
+    out, _ = run_team(dp, 2, fn)
+    for seen in out:
+        assert len(seen) == len(seen_single)
+        for a, b in zip(seen, seen_single):
+            assert np.array_equal(a, b)
