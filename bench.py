@@ -280,6 +280,19 @@ def run_ours(args, world, rank, local):
     g0 = dp.rmat_graph(scale, seed=args.seed, ctx=ctx)
     gt0 = dp.transpose(g0)
     n, m0 = g0.vertex_count, g0.edge_count
+    exchange = "none (single GPU)"
+    symm_keep = None
+    if world > 1:
+        # fused exchange: contributions stored straight into every rank's
+        # peer-mapped buffer by the sweep epilogue (torch symmetric memory
+        # for the IPC plumbing); the NCCL all-gather is the fallback
+        exchange = "NCCL all-gather of contributions per sweep"
+        if os.environ.get("DYNPR_EXCHANGE", "fused") == "fused":
+            try:
+                symm_keep = dp.attach_symmetric_exchange(ctx, n)
+                exchange = "fused: sweep epilogue stores contributions into all peers over NVLink"
+            except Exception as e:  # plumbing unavailable: keep the all-gather transport
+                exchange += " (fused exchange unavailable: %s)" % str(e).splitlines()[0][:120]
     base = dp.static_pagerank(gt0, g0)
     base_dev = torch.from_numpy(base.ranks).to(f"cuda:{local}")
     size = dp.batch_size_from_fraction(args.batch_frac, m0)
@@ -389,8 +402,9 @@ def run_ours(args, world, rank, local):
                        "l2": "inputs larger than L2 (graph pair %.2f GB vs 126 MB L2); no flush needed"
                              % ((2 * (8 * (n + 1) + 4 * m0)) / 1e9),
                        "parallelism": "single GPU" if world == 1 else
-                       "vertex-range partitioned over %d GPUs (edge-balanced; NCCL allgather of "
-                       "contributions + allreduce of the sweep record per iteration)" % world},
+                       "vertex-range partitioned over %d GPUs (edge-balanced; NCCL all-reduce of the "
+                       "sweep record per iteration)" % world,
+                       "exchange": exchange},
             "static": {"ms_per_solve": st_ms, "iterations": statistics.mean(rec["static_it"]),
                        "gteps": local_gteps},
             "dfp": {"ms_per_solve": dfp_ms, "iterations": statistics.mean(rec["dfp_it"]),

@@ -134,6 +134,17 @@ dynpr_status dynpr_context_create_team(int device, dynpr_team* team, int rank,
                                        dynpr_context** out);
 dynpr_status dynpr_context_rank(const dynpr_context* ctx, int* rank,
                                 int* world);
+/* Fused exchange: ptrs0[r] / ptrs1[r] are rank r's two contribution buffers
+ * (`capacity` doubles each) mapped into this process -- CUDA IPC / torch
+ * symmetric memory across processes, plain device pointers for a LocalTeam.
+ * With them attached, every sweep's epilogue stores each new contribution
+ * straight into all ranks' copies over NVLink (the transfer overlaps the
+ * sweep), replacing the per-sweep all-gather; the sweep-record all-reduce
+ * remains as the team barrier.  world = 0 detaches. */
+dynpr_status dynpr_context_attach_peers(dynpr_context* ctx, int world,
+                                        const uint64_t* ptrs0,
+                                        const uint64_t* ptrs1,
+                                        uint64_t capacity);
 
 /* ---- graphs (graph.hpp:17-80) ------------------------------------------- */
 /* CsrGraph(vertexCount, offsets, targets) incl. validation (graph.cpp:30-49).

@@ -34,7 +34,7 @@ __all__ = [
     "l1_norm_delta", "linf_norm_delta", "naive_dynamic", "partition_by_degree", "rmat_graph",
     "static_pagerank", "transpose", "update_ranks", "generate_random_batch", "batch_size_from_fraction",
     "derive_seed", "prepare", "LocalTeam", "nccl_unique_id", "share_nccl_unique_id",
-    "context_from_process_group",
+    "context_from_process_group", "attach_symmetric_exchange",
 ]
 
 
@@ -150,6 +150,15 @@ class Context:
         _check(N.lib().dynpr_context_create_nccl(int(device), int(rank), int(world), buf, C.byref(h)))
         return cls(device, _handle=h.value)
 
+    def attach_peers(self, ptrs0: Sequence[int], ptrs1: Sequence[int], capacity: int) -> None:
+        """Fused exchange: every rank's two contribution buffers (device
+        addresses valid in this process, `capacity` doubles each); [] detaches.
+        See dynpr_context_attach_peers."""
+        world = len(ptrs0)
+        a0 = (C.c_uint64 * max(world, 1))(*[int(p) for p in ptrs0])
+        a1 = (C.c_uint64 * max(world, 1))(*[int(p) for p in ptrs1])
+        _check(N.lib().dynpr_context_attach_peers(C.c_void_p(self.h), world, a0, a1, int(capacity)))
+
     @property
     def rank(self) -> int:
         r, w = C.c_int(), C.c_int()
@@ -189,6 +198,27 @@ def share_nccl_unique_id(group=None) -> bytes:
     obj = [nccl_unique_id() if dist.get_rank(group) == 0 else None]
     dist.broadcast_object_list(obj, src=0, group=group)
     return obj[0]
+
+
+def attach_symmetric_exchange(ctx: Context, n: int, group=None):
+    """Allocates the two n-double contribution buffers of every rank in
+    torch symmetric memory (CUDA IPC handles exchanged over the process
+    group), maps all peers' buffers and attaches them to `ctx` (fused
+    NVLink exchange).  Returns the tensors/handles, which must stay alive
+    while the context solves."""
+    import torch
+    import torch.distributed as dist
+    import torch.distributed._symmetric_memory as symm_mem
+    group = group or dist.group.WORLD
+    keep = []
+    ptrs = []
+    for _ in range(2):
+        t = symm_mem.empty(max(n, 1), dtype=torch.float64, device=f"cuda:{ctx.device}")
+        h = symm_mem.rendezvous(t, group)
+        keep.append((t, h))
+        ptrs.append([int(p) for p in h.buffer_ptrs])
+    ctx.attach_peers(ptrs[0], ptrs[1], max(n, 1))
+    return keep
 
 
 def context_from_process_group(device: int, group=None) -> Context:

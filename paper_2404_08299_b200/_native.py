@@ -81,6 +81,7 @@ PROTOTYPES = {
     "dynpr_team_destroy": (_i, [_vp]),
     "dynpr_context_create_team": (_i, [_i, _vp, _i, _pvp]),
     "dynpr_context_rank": (_i, [_vp, _ip, _ip]),
+    "dynpr_context_attach_peers": (_i, [_vp, _i, _vp, _vp, _u64]),
     "dynpr_graph_from_csr": (_i, [_vp, _u32, _vp, _vp, _u64, _pvp]),
     "dynpr_graph_build": (_i, [_vp, _u32, _vp, _vp, _u64, _pvp]),
     "dynpr_graph_add_self_loops": (_i, [_vp, _vp, _pvp]),

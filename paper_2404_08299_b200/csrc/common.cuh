@@ -109,6 +109,10 @@ struct dynpr_context {
   uint64_t sweeps = 0;
   uint64_t sweep_bytes = 0;
   uint64_t pull_expansions = 0;
+  // fused multi-GPU exchange: every rank's two contribution buffers, mapped
+  // into this process (dynpr_context_attach_peers); empty = all-gather path
+  std::vector<double*> peer_cb[2];
+  uint64_t peer_capacity = 0;
   cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_s0 = nullptr, ev_s1 = nullptr;
   // pinned host scratch for small readbacks
   void* pinned = nullptr;

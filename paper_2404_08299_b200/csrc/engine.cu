@@ -104,7 +104,14 @@ void solve(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynpr_sta
   const Layout* L = get_layout(ctx, gT, gF, c.low_degree_threshold, sp.flagged);
   // workspace (allocation is excluded from the timed region)
   double* R[2] = {ctx->rank[0].as<double>(n), ctx->rank[1].as<double>(n)};
-  double* CB[2] = {ctx->contrib[0].as<double>(n), ctx->contrib[1].as<double>(n)};
+  // Multi-GPU with attached peer buffers: contributions live in the
+  // peer-mapped buffers and each sweep stores its new values straight into
+  // every rank's copy (fused exchange); otherwise they are all-gathered.
+  Comm* comm = ctx->comm;
+  const bool dist = comm && comm->world > 1;
+  const bool fused = dist && (int)ctx->peer_cb[0].size() == comm->world && ctx->peer_capacity >= n;
+  double* CB[2] = {fused ? ctx->peer_cb[0][comm->rank] : ctx->contrib[0].as<double>(n),
+                   fused ? ctx->peer_cb[1][comm->rank] : ctx->contrib[1].as<double>(n)};
   double* partials = ctx->partials.as<double>(L->n_mseg + 1);
   SweepRed* red = ctx->red.as<SweepRed>(2);
   uint8_t* va = nullptr;
@@ -168,8 +175,6 @@ void solve(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynpr_sta
   // range; contributions (and DF pending flags) are all-gathered after
   // every sweep and the reduction record all-reduced, so every rank takes
   // the same convergence / expansion decisions.
-  Comm* comm = ctx->comm;
-  const bool dist = comm && comm->world > 1;
   std::vector<uint64_t> off_c, off_f;  // allgatherv byte offsets: f64 / u8 per vertex
   if (dist) {
     const std::vector<RankRange> plan = plan_ranges(ctx, const_cast<Layout*>(L), comm->world);
@@ -190,6 +195,14 @@ void solve(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynpr_sta
     off_f[comm->world] = n;
   }
 
+  if (fused) {
+    // Team barrier: no rank may store into a peer's buffers before that
+    // peer has initialised them (an all-reduce of a zeroed record is
+    // stream-ordered after this rank's init on every rank).
+    DYNPR_CK(cudaMemsetAsync(red, 0, sizeof(SweepRed), st));
+    comm->allreduce_red(red, st);
+  }
+
   dynpr_stats res{};
   int cur = 0;  // R[cur] holds the latest iterate ("previous")
   for (int iter = 0; iter < c.max_iterations; ++iter) {
@@ -205,12 +218,17 @@ void solve(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynpr_sta
     a.rank_cur = R[cur ^ 1];
     a.contrib_prev = CB[cur];
     a.contrib_cur = CB[cur ^ 1];
+    a.npeers = 0;
+    if (fused) {
+      for (int r = 0; r < comm->world; ++r)
+        if (r != comm->rank) a.peer_cur[a.npeers++] = ctx->peer_cb[cur ^ 1][r];
+    }
     if (ctx->profiling) DYNPR_CK(cudaEventRecord(ctx->ev_s0, st));
     launch_sweep(ctx, a, sp.flagged, sp.closed);
     if (ctx->profiling) DYNPR_CK(cudaEventRecord(ctx->ev_s1, st));
     if (dist) {
-      comm->allreduce_red(red, st);
-      comm->allgatherv(CB[cur ^ 1], off_c.data(), st);
+      comm->allreduce_red(red, st);  // also the team barrier of the fused exchange
+      if (!fused) comm->allgatherv(CB[cur ^ 1], off_c.data(), st);
       if (sp.flagged) comm->allgatherv(np, off_f.data(), st);
       if (obs) comm->allgatherv(R[cur ^ 1], off_c.data(), st);
     }
@@ -377,6 +395,26 @@ dynpr_status dynpr_context_create_team(int device, dynpr_team* team, int rank, d
     *out = nullptr;
   }
   return st;
+}
+
+dynpr_status dynpr_context_attach_peers(dynpr_context* ctx, int world, const uint64_t* ptrs0, const uint64_t* ptrs1,
+                                        uint64_t capacity) {
+  return api_guard([&] {
+    if (!ctx) invalid("null context");
+    ctx->peer_cb[0].clear();
+    ctx->peer_cb[1].clear();
+    ctx->peer_capacity = 0;
+    if (world == 0) return;  // detach
+    const int team = ctx->comm ? ctx->comm->world : 1;
+    if (world != team || !ptrs0 || !ptrs1) invalid("dynpr_context_attach_peers: world does not match the team");
+    if (world - 1 > kMaxPeers) invalid("dynpr_context_attach_peers: team larger than kMaxPeers + 1");
+    for (int r = 0; r < world; ++r) {
+      if (!ptrs0[r] || !ptrs1[r]) invalid("dynpr_context_attach_peers: null buffer");
+      ctx->peer_cb[0].push_back(reinterpret_cast<double*>(ptrs0[r]));
+      ctx->peer_cb[1].push_back(reinterpret_cast<double*>(ptrs1[r]));
+    }
+    ctx->peer_capacity = capacity;
+  });
 }
 
 dynpr_status dynpr_context_rank(const dynpr_context* ctx, int* rank, int* world) {

@@ -117,6 +117,14 @@ __device__ __forceinline__ void warp_append(bool pend, bool lowout, uint32_t v, 
   for (unsigned j = 0, b = bh + incl - items; j < items; ++j) ph[b + j] = make_uint2(v, j);
 }
 
+// A new contribution of vertex v: the local buffer and, in a multi-GPU team
+// with peer-mapped buffers, every peer's copy (NVLink stores issued from the
+// epilogue, so the exchange overlaps the sweep instead of following it).
+__device__ __forceinline__ void store_contrib(const SweepArgs& a, uint32_t v, double c) {
+  a.contrib_cur[v] = c;
+  for (int p = 0; p < a.npeers; ++p) a.peer_cur[p][v] = c;
+}
+
 // Unaffected vertex (rank.cpp:90-92): current = previous.  In engine mode
 // only vertices written by the previous sweep differ between the buffers.
 __device__ __forceinline__ void copy_through(const SweepArgs& a, uint32_t v) {
@@ -125,7 +133,7 @@ __device__ __forceinline__ void copy_through(const SweepArgs& a, uint32_t v) {
     if (a.contrib_cur) a.contrib_cur[v] = a.contrib_prev[v];
   } else if (a.written[v]) {
     a.rank_cur[v] = a.rank_prev[v];
-    a.contrib_cur[v] = a.contrib_prev[v];
+    store_contrib(a, v, a.contrib_prev[v]);
     a.written[v] = 0;
   }
   if (a.np && !a.np_accumulate) a.np[v] = 0;
@@ -145,7 +153,7 @@ __device__ __forceinline__ void finalize(const SweepArgs& a, uint32_t v, double 
     r = __dadd_rn(a.teleport, __dmul_rn(a.alpha, c));
   }
   a.rank_cur[v] = r;
-  if (a.contrib_cur) a.contrib_cur[v] = __ddiv_rn(r, d);
+  if (a.contrib_cur) store_contrib(a, v, __ddiv_rn(r, d));
   const double dr = fabs(__dsub_rn(r, pv));
   if (dr > acc.dmax) acc.dmax = dr;  // NaN never wins, like blockMax (parallel.hpp:66-73)
   if (FLAGGED) {
@@ -280,6 +288,7 @@ __global__ void __launch_bounds__(kSweepThreads, 5) k_sweep_single(SweepArgs a) 
     }
     if (FLAGGED && a.pend_low) warp_append(pend, lowout, v, od, a.pend_low, a.pend_high, a.red);
   }
+  if (a.npeers) __threadfence_system();  // peer stores visible before the team barrier
   block_reduce_commit(acc, a.red);
 }
 
@@ -335,6 +344,7 @@ __global__ void __launch_bounds__(kThreads) k_sweep_mfinal(SweepArgs a) {
     }
     if (FLAGGED && a.pend_low) warp_append(pend, lowout, v, od, a.pend_low, a.pend_high, a.red);
   }
+  if (a.npeers) __threadfence_system();  // peer stores visible before the team barrier
   block_reduce_commit(acc, a.red);
 }
 

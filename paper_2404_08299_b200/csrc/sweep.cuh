@@ -10,6 +10,9 @@ namespace dynpr_b200 {
 // Edges per partial sum for high in-degree vertices (rank.cpp:42 kAccumChunk).
 constexpr uint32_t kAccumChunk = 256;
 
+// Largest team whose peer buffers the sweep epilogue writes (one B200 box).
+constexpr int kMaxPeers = 8;
+
 // Stable degree partition of one graph (partition.cpp:7-61), used by the
 // partitionByDegree entry point.
 struct Schedule {
@@ -53,6 +56,10 @@ struct SweepArgs {
   // [v_lo, v_hi), single slices [ss_lo, ss_hi), multi slices [ms_lo, ms_hi)
   uint32_t v_lo, v_hi;
   uint64_t ss_lo, ss_hi, ms_lo, ms_hi;
+  // fused exchange (multi-GPU team with peer-mapped contribution buffers):
+  // the other ranks' copies of contrib_cur, written alongside the local one
+  int npeers;
+  double* peer_cur[kMaxPeers];
 };
 
 // Edge-balanced partition of the layout's vertex space over `world` ranks

@@ -19,10 +19,19 @@ from helpers import rand_pair
 pytestmark = pytest.mark.gpu
 
 
-def run_team(dp, world, fn):
-    """fn(ctx, rank) on `world` threads with virtual-rank contexts."""
+def run_team(dp, world, fn, fused_n=0):
+    """fn(ctx, rank) on `world` threads with virtual-rank contexts; with
+    fused_n > 0 the ranks get peer contribution buffers (fused exchange:
+    each sweep stores into every rank's copy, no all-gather)."""
     team = dp.LocalTeam(world)
     ctxs = [team.context(0, r) for r in range(world)]
+    if fused_n:
+        import torch
+        bufs = [[torch.empty(fused_n, dtype=torch.float64, device="cuda:0") for _ in range(world)] for _ in range(2)]
+        ptrs = [[b.data_ptr() for b in bufs[k]] for k in range(2)]
+        for c in ctxs:
+            c.attach_peers(ptrs[0], ptrs[1], fused_n)
+        ctxs.append(bufs)  # keep the buffers alive with the contexts
     out, errs = [None] * world, []
 
     def body(r):
@@ -49,6 +58,14 @@ def same(a, b):
     assert np.array_equal(a.ranks, b.ranks)
 
 
+def test_attach_peers_validates(dp):
+    team = dp.LocalTeam(2)
+    c = team.context(0, 0)
+    with pytest.raises(ValueError, match="world does not match"):
+        c.attach_peers([1, 2, 3], [4, 5, 6], 10)
+    c.attach_peers([], [], 0)  # detach is always allowed
+
+
 def test_team_reports_rank_and_world(dp):
     team = dp.LocalTeam(3)
     ctxs = [team.context(0, r) for r in range(3)]
@@ -58,7 +75,8 @@ def test_team_reports_rank_and_world(dp):
 
 @pytest.mark.parametrize("world", [2, 3, 4])
 @pytest.mark.parametrize("scale", [10, 13])
-def test_partitioned_static_and_dfp_equal_single_gpu(dp, oracle_lib, world, scale):
+@pytest.mark.parametrize("fused", [False, True], ids=["allgather", "fused-peer-stores"])
+def test_partitioned_static_and_dfp_equal_single_gpu(dp, oracle_lib, world, scale, fused):
     O = oracle_lib
     src, dst = O.rmat_edges(scale, 16 << scale)
     og = O.add_self_loops(O.build_csr((src, dst), 1 << scale))
@@ -97,7 +115,7 @@ def test_partitioned_static_and_dfp_equal_single_gpu(dp, oracle_lib, world, scal
             "dfp": dp.dynamic_frontier(h2, ht2, dels, ins, b.ranks, pruning=True),
         }
 
-    out, _ = run_team(dp, world, fn)
+    out, _ = run_team(dp, world, fn, fused_n=n if fused else 0)
     for r in range(world):
         for k in single:
             same(out[r][k], single[k])
