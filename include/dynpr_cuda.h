@@ -284,6 +284,22 @@ dynpr_status dynpr_dynamic_frontier(
     const double* previous, uint64_t n_previous, const dynpr_config* cfg,
     int pruning, double* ranks_out, dynpr_stats* stats,
     dynpr_observer observer, void* observer_user);
+/* dynamicTraversal(gForward, gTranspose, dels, ins, prev, cfg) --
+ * engine.cpp:124-151: the affected set is everything reachable (device BFS,
+ * markReachable frontier.cpp:86-121) from the update sources and the
+ * deletion targets, fixed for the solve; plain rank formula, no expansion. */
+dynpr_status dynpr_dynamic_traversal(
+    dynpr_context* ctx, const dynpr_graph* gF, const dynpr_graph* gT,
+    const uint32_t* del_src, const uint32_t* del_dst, uint64_t n_del,
+    const uint32_t* ins_src, const uint32_t* ins_dst, uint64_t n_ins,
+    const double* previous, uint64_t n_previous, const dynpr_config* cfg,
+    double* ranks_out, dynpr_stats* stats, dynpr_observer observer,
+    void* observer_user);
+/* markReachable(g, seeds) -- frontier.cpp:86-121: vertex_affected[v] = 1 for
+ * every v reachable from a seed (n bytes out; neighborsPending stays 0). */
+dynpr_status dynpr_mark_reachable(dynpr_context* ctx, const dynpr_graph* g,
+                                  const uint32_t* seeds, uint64_t n_seeds,
+                                  uint8_t* vertex_affected);
 /* dynamicFrontierFromFlags -- engine.cpp:178-190. */
 dynpr_status dynpr_dynamic_frontier_from_flags(
     dynpr_context* ctx, const dynpr_graph* gF, const dynpr_graph* gT,

@@ -471,6 +471,35 @@ class Oracle:
             _ptr(ranks, _dp), C.byref(st), obs, None))
         return self._result(ranks[: gT.n], st, trace)
 
+    def dynamic_traversal(self, gF: Graph, gT: Graph, dels, ins, prev, cfg: Config = None,
+                          trace: Optional[list] = None) -> Result:
+        """dynamicTraversal (engine.cpp:124-151)."""
+        cfg = cfg or default_config()
+        ds, dd = split_edges(dels)
+        is_, id_ = split_edges(ins)
+        nd, ni = len(ds), len(is_)
+        z = np.zeros(1, np.uint32)
+        ds, dd = (ds, dd) if nd else (z, z)
+        is_, id_ = (is_, id_) if ni else (z, z)
+        prev = _f64(prev)
+        ranks = np.zeros(max(gT.n, 1), np.float64)
+        st = Stats()
+        obs, keep = self._observer(trace, False)
+        self._check(getattr(self.L, self.p + "dynamic_traversal")(
+            C.c_void_p(gF.h), C.c_void_p(gT.h), _ptr(ds, _u32p), _ptr(dd, _u32p), C.c_uint64(nd),
+            _ptr(is_, _u32p), _ptr(id_, _u32p), C.c_uint64(ni), _ptr(prev, _dp), C.c_uint64(len(prev)),
+            C.byref(cfg), _ptr(ranks, _dp), C.byref(st), obs, None))
+        return self._result(ranks[: gT.n], st, trace)
+
+    def mark_reachable(self, g: Graph, seeds) -> np.ndarray:
+        """markReachable (frontier.cpp:86-121): vertexAffected bytes."""
+        sd = np.ascontiguousarray(np.asarray(seeds, dtype=np.uint32).reshape(-1))
+        z = sd if len(sd) else np.zeros(1, np.uint32)
+        va = np.zeros(max(g.n, 1), np.uint8)
+        self._check(getattr(self.L, self.p + "mark_reachable")(
+            C.c_void_p(g.h), _ptr(z, _u32p), C.c_uint64(len(sd)), _ptr(va, _u8p)))
+        return va[: g.n]
+
     def compute_reference_ranks(self, gT: Graph, gF: Graph, cfg: Config = None):
         cfg = cfg or default_config()
         ranks = np.zeros(max(gT.n, 1), np.float64)

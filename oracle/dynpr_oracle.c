@@ -583,6 +583,75 @@ int orc_dynamic_frontier_from_flags(const orc_graph* gF, const orc_graph* gT,
   return rc;
 }
 
+/* markReachable (frontier.cpp:86-121): every vertex reachable from a seed
+ * over g's out-slices.  Sequential BFS; only the visited set is observable
+ * (frontier.cpp:96-98), so the visit order does not matter. */
+int orc_mark_reachable(const orc_graph* g, const uint32_t* seeds, uint64_t ns,
+                       uint8_t* va) {
+  const uint32_t n = g->n;
+  for (uint64_t i = 0; i < ns; ++i)
+    if (seeds[i] >= n) return set_err(1, "markReachable: seed out of range");
+  memset(va, 0, n);
+  uint32_t* q = (uint32_t*)malloc(((size_t)n + 1) * sizeof(uint32_t));
+  uint64_t head = 0, tail = 0;
+  for (uint64_t i = 0; i < ns; ++i)
+    if (!va[seeds[i]]) {
+      va[seeds[i]] = 1;
+      q[tail++] = seeds[i];
+    }
+  while (head < tail) {
+    const uint32_t u = q[head++];
+    for (uint64_t k = g->off[u]; k < g->off[u + 1]; ++k) {
+      const uint32_t w = g->tgt[k];
+      if (!va[w]) {
+        va[w] = 1;
+        q[tail++] = w;
+      }
+    }
+  }
+  free(q);
+  return 0;
+}
+
+/* dynamicTraversal (engine.cpp:124-151): seeds = update sources + deletion
+ * targets, affected = markReachable(gForward, seeds), plain formula, no
+ * expansion. */
+int orc_dynamic_traversal(const orc_graph* gF, const orc_graph* gT,
+                          const uint32_t* ds, const uint32_t* dd, uint64_t nd,
+                          const uint32_t* is, const uint32_t* id, uint64_t ni,
+                          const double* prevRanks, uint64_t nprev,
+                          const dynpr_config* cfg, double* ranks,
+                          dynpr_stats* st, dynpr_observer obs, void* user) {
+  (void)id;
+  if (orc_validate_config(cfg) || check_pair(gT, gF)) return 1;
+  if (nprev != gT->n)
+    return set_err(1, "dynamicTraversal: previousRanks length mismatch");
+  const uint32_t n = gT->n;
+  const uint64_t ns = 2 * nd + ni;
+  uint32_t* seeds = (uint32_t*)malloc((ns + 1) * sizeof(uint32_t));
+  for (uint64_t i = 0; i < nd; ++i) {
+    seeds[2 * i] = ds[i];
+    seeds[2 * i + 1] = dd[i];
+  }
+  for (uint64_t i = 0; i < ni; ++i) seeds[2 * nd + i] = is[i];
+  uint8_t* va = (uint8_t*)malloc((size_t)n + 1);
+  uint8_t* np = (uint8_t*)calloc((size_t)n + 1, 1);
+  int rc = orc_mark_reachable(gF, seeds, ns, va);
+  free(seeds);
+  if (rc) {
+    free(va); free(np);
+    return rc;
+  }
+  double* a = (double*)malloc((size_t)n * sizeof(double));
+  double* b = (double*)malloc((size_t)n * sizeof(double));
+  memcpy(a, prevRanks, (size_t)n * sizeof(double));
+  memcpy(b, prevRanks, (size_t)n * sizeof(double));
+  converge_loop(gT, gF, a, b, va, np, 0, DYNPR_RANK_PLAIN, cfg, ranks, st, obs,
+                user);
+  free(a); free(b); free(va); free(np);
+  return 0;
+}
+
 /* computeReferenceRanks (harness.cpp:340-349): static, check disabled. */
 int orc_compute_reference_ranks(const orc_graph* gT, const orc_graph* gF,
                                 const dynpr_config* cfg, double* ranks) {

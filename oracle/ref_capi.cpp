@@ -303,6 +303,30 @@ int ref_dynamic_frontier(const void* gF, const void* gT, const uint32_t* ds,
     fillStats(r, st, ms);
   });
 }
+int ref_dynamic_traversal(const void* gF, const void* gT, const uint32_t* ds,
+                          const uint32_t* dd, uint64_t nd, const uint32_t* is,
+                          const uint32_t* id, uint64_t ni, const double* prev,
+                          uint64_t nprev, const dynpr_config* c, double* ranks,
+                          dynpr_stats* st, dynpr_observer obs, void* user) {
+  return guard([&] {
+    EdgeList dels = toEdges(ds, dd, nd), ins = toEdges(is, id, ni);
+    auto t0 = std::chrono::steady_clock::now();
+    RankResult r = dynamicTraversal(*CG(gF), *CG(gT), dels, ins,
+                                    std::span<const double>(prev, nprev),
+                                    toCfg(c), wrapObserver(obs, user));
+    double ms = std::chrono::duration<double, std::milli>(
+                    std::chrono::steady_clock::now() - t0).count();
+    std::memcpy(ranks, r.ranks.data(), r.ranks.size() * sizeof(double));
+    fillStats(r, st, ms);
+  });
+}
+int ref_mark_reachable(const void* g, const uint32_t* seeds, uint64_t ns,
+                       uint8_t* va) {
+  return guard([&] {
+    AffectedFlags f = markReachable(*CG(g), std::span<const Vertex>(seeds, ns));
+    std::memcpy(va, f.vertexAffected.data(), f.vertexAffected.size());
+  });
+}
 int ref_dynamic_frontier_from_flags(const void* gF, const void* gT,
                                     const uint8_t* va, const uint8_t* np,
                                     uint64_t nflags, const double* prev,

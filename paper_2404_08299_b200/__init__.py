@@ -34,7 +34,7 @@ __all__ = [
     "l1_norm_delta", "linf_norm_delta", "naive_dynamic", "partition_by_degree", "rmat_graph",
     "static_pagerank", "transpose", "update_ranks", "generate_random_batch", "batch_size_from_fraction",
     "derive_seed", "prepare", "LocalTeam", "nccl_unique_id", "share_nccl_unique_id",
-    "context_from_process_group", "attach_symmetric_exchange",
+    "context_from_process_group", "attach_symmetric_exchange", "dynamic_traversal", "mark_reachable",
 ]
 
 
@@ -614,6 +614,34 @@ def dynamic_frontier(g_forward: CsrGraph, g_transpose: CsrGraph, deletions, inse
                                           len(is_), _p(prev), len(prev), C.byref(cfg), int(bool(pruning)),
                                           _p(ranks), C.byref(st), obs, None))
     return _result(ranks[: g_transpose.vertex_count], st)
+
+
+def dynamic_traversal(g_forward: CsrGraph, g_transpose: CsrGraph, deletions, insertions, previous_ranks,
+                      config: Optional[EngineConfig] = None, observer: Optional[Callable] = None) -> RankResult:
+    """dynamicTraversal(gForward, gTranspose, dels, ins, prev, cfg) --
+    engine.cpp:124-151: every vertex reachable from an update endpoint
+    (device BFS) is processed every sweep; no expansion, no pruning."""
+    cfg = (config or EngineConfig())._c()
+    ds, dd = _edges(deletions)
+    is_, id_ = _edges(insertions)
+    prev = _arr(previous_ranks, np.float64)
+    ranks = np.zeros(max(g_transpose.vertex_count, 1), np.float64)
+    st = N.Stats()
+    obs, keep = _observer(observer)
+    _check(N.lib().dynpr_dynamic_traversal(C.c_void_p(g_forward.ctx.h), C.c_void_p(g_forward.h),
+                                           C.c_void_p(g_transpose.h), _p(ds), _p(dd), len(ds), _p(is_), _p(id_),
+                                           len(is_), _p(prev), len(prev), C.byref(cfg), _p(ranks), C.byref(st),
+                                           obs, None))
+    return _result(ranks[: g_transpose.vertex_count], st)
+
+
+def mark_reachable(g: CsrGraph, seeds) -> np.ndarray:
+    """markReachable(g, seeds) -- frontier.cpp:86-121: the vertexAffected
+    bytes of every vertex reachable from a seed (device BFS)."""
+    sd = _arr(seeds, np.uint32)
+    va = np.zeros(max(g.vertex_count, 1), np.uint8)
+    _check(N.lib().dynpr_mark_reachable(C.c_void_p(g.ctx.h), C.c_void_p(g.h), _p(sd), len(sd), _p(va)))
+    return va[: g.vertex_count]
 
 
 def dynamic_frontier_from_flags(g_forward: CsrGraph, g_transpose: CsrGraph, vertex_affected,

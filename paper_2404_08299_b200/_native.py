@@ -108,6 +108,9 @@ PROTOTYPES = {
     "dynpr_naive_dynamic": (_i, [_vp, _vp, _vp, _vp, _u64, _cfgp, _vp, _stp, OBSERVER, _vp]),
     "dynpr_dynamic_frontier": (_i, [_vp, _vp, _vp, _vp, _vp, _u64, _vp, _vp, _u64, _vp, _u64, _cfgp, _i,
                                     _vp, _stp, OBSERVER, _vp]),
+    "dynpr_dynamic_traversal": (_i, [_vp, _vp, _vp, _vp, _vp, _u64, _vp, _vp, _u64, _vp, _u64, _cfgp, _vp, _stp,
+                                     OBSERVER, _vp]),
+    "dynpr_mark_reachable": (_i, [_vp, _vp, _vp, _u64, _vp]),
     "dynpr_dynamic_frontier_from_flags": (_i, [_vp, _vp, _vp, _vp, _vp, _u64, _vp, _u64, _cfgp, _i, _vp,
                                                _stp, OBSERVER, _vp]),
 }

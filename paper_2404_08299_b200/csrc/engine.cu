@@ -87,6 +87,11 @@ struct SolveSpec {
   const uint32_t* is = nullptr;
   uint64_t ni = 0;
   const uint8_t* flags_in = nullptr;
+  // dynamicTraversal (engine.cpp:124-151): the affected set is everything
+  // reachable from the seeds, fixed for the whole solve (no expansion)
+  bool traversal = false;
+  const uint32_t* seeds = nullptr;
+  uint64_t nseeds = 0;
 };
 
 // convergeLoop (engine.cpp:61-95) on the device, in the layout's new-id
@@ -120,7 +125,7 @@ void solve(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynpr_sta
   uint32_t* pl = nullptr;
   uint2* ph = nullptr;
   if (sp.flagged) {
-    va = ctx->flags_va.as<uint8_t>(n);
+    va = ctx->flags_va.as<uint8_t>((uint64_t)n + 4);  // +4: word-wide claims (markReachable)
     np = ctx->pend_flags.as<uint8_t>(n);
     written = ctx->flags_written.as<uint8_t>(n);
     pl = ctx->pend_low.as<uint32_t>((uint64_t)n + 1);
@@ -146,6 +151,11 @@ void solve(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynpr_sta
     DYNPR_CK(cudaMemsetAsync(written, 0, n, st));
     if (sp.flags_in) {
       launch_gather_perm_u8(ctx, L, sp.flags_in, va);
+    } else if (sp.traversal) {
+      // markReachable over the relabelled forward CSR (frontier.cpp:86-121)
+      DYNPR_CK(cudaMemsetAsync(va, 0, n, st));
+      uint32_t* fb = ctx->perm_stage.as<uint32_t>((uint64_t)n + 1);
+      mark_reachable(ctx, L->offF, L->tgtF, n, L->inv, sp.seeds, sp.nseeds, va, pl, fb);
     } else {
       // initialAffected + the one expandAffected before the loop
       // (engine.cpp:199-200)
@@ -165,10 +175,10 @@ void solve(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynpr_sta
   a.tf = c.frontier_tolerance;
   a.tp = c.prune_tolerance;
   a.va = va;
-  a.np = np;  // pending flags (new ids) for pull expansion
+  a.np = sp.traversal ? nullptr : np;  // pending flags (new ids) for pull expansion
   a.written = written;
-  a.pend_low = pl;
-  a.pend_high = ph;
+  a.pend_low = sp.traversal ? nullptr : pl;
+  a.pend_high = sp.traversal ? nullptr : ph;
   a.red = red;
 
   // Multi-GPU: this rank sweeps only its edge-balanced vertex
@@ -229,7 +239,7 @@ void solve(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynpr_sta
     if (dist) {
       comm->allreduce_red(red, st);  // also the team barrier of the fused exchange
       if (!fused) comm->allgatherv(CB[cur ^ 1], off_c.data(), st);
-      if (sp.flagged) comm->allgatherv(np, off_f.data(), st);
+      if (sp.flagged && !sp.traversal) comm->allgatherv(np, off_f.data(), st);
       if (obs) comm->allgatherv(R[cur ^ 1], off_c.data(), st);
     }
     const SweepRed r = read_red(ctx, red);
@@ -259,7 +269,7 @@ void solve(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynpr_sta
       res.converged = 1;
       break;
     }
-    if (sp.flagged) {  // expandAffected (engine.cpp:91), direction-optimising
+    if (sp.flagged && !sp.traversal) {  // expandAffected (engine.cpp:91), direction-optimising
       // push touches the pending vertices' out-edges; pull scans at most
       // the in-edges of the vertices that were not processed this sweep
       const uint64_t pull_bound = gT->m > r.edges ? gT->m - r.edges : 0;
@@ -696,6 +706,64 @@ dynpr_status dynpr_dynamic_frontier(dynpr_context* ctx, const dynpr_graph* gF, c
     sp.flagged = true;
     sp.closed = pruning != 0;
     solve(ctx, sp, ranks_out, stats, observer, observer_user);
+  });
+}
+
+dynpr_status dynpr_dynamic_traversal(dynpr_context* ctx, const dynpr_graph* gF, const dynpr_graph* gT,
+                                     const uint32_t* del_src, const uint32_t* del_dst, uint64_t n_del,
+                                     const uint32_t* ins_src, const uint32_t* ins_dst, uint64_t n_ins,
+                                     const double* previous, uint64_t n_previous, const dynpr_config* cfg,
+                                     double* ranks_out, dynpr_stats* stats, dynpr_observer observer,
+                                     void* observer_user) {
+  return api_guard([&] {
+    if (!ctx) invalid("null context");
+    validate_config(cfg);
+    check_pair(gT, gF);
+    if (n_previous != gT->n) invalid("dynamicTraversal: previousRanks length mismatch");
+    if (!ranks_out) invalid("null output array");
+    bind_device(ctx);
+    // seeds: sources of all updates + targets of deletions (engine.cpp:138-145)
+    const uint64_t ns = 2 * n_del + n_ins;
+    uint32_t* seeds = ctx->stage_d.as<uint32_t>(ns + 1);
+    auto put = [&](const uint32_t* p, uint64_t cnt, uint64_t at) {
+      if (cnt) DYNPR_CK(cudaMemcpyAsync(seeds + at, p, cnt * 4, cudaMemcpyDefault, ctx->stream));
+    };
+    if (n_del && (!del_src || !del_dst)) invalid("null array argument");
+    if (n_ins && !ins_src) invalid("null array argument");
+    put(del_src, n_del, 0);
+    put(del_dst, n_del, n_del);
+    put(ins_src, n_ins, 2 * n_del);
+    if (any_bad_ids(ctx, seeds, seeds, ns, gT->n)) invalid("markReachable: seed out of range");
+    (void)ins_dst;
+    SolveSpec sp;
+    sp.gT = gT;
+    sp.gF = gF;
+    sp.cfg = cfg;
+    sp.prev = stage_in(ctx, ctx->stage_b, previous, n_previous);
+    sp.flagged = true;
+    sp.closed = false;
+    sp.traversal = true;
+    sp.seeds = seeds;
+    sp.nseeds = ns;
+    solve(ctx, sp, ranks_out, stats, observer, observer_user);
+  });
+}
+
+dynpr_status dynpr_mark_reachable(dynpr_context* ctx, const dynpr_graph* g, const uint32_t* seeds, uint64_t n_seeds,
+                                  uint8_t* vertex_affected) {
+  return api_guard([&] {
+    if (!ctx || !g) invalid("null argument");
+    bind_device(ctx);
+    const uint32_t n = g->n;
+    const uint32_t* s = stage_in(ctx, ctx->stage_d, seeds, n_seeds);
+    if (any_bad_ids(ctx, s, s, n_seeds, n)) invalid("markReachable: seed out of range");
+    uint8_t* flags = ctx->flags_va.as<uint8_t>((uint64_t)n + 4);
+    DYNPR_CK(cudaMemsetAsync(flags, 0, (size_t)n + 4, ctx->stream));
+    uint32_t* fa = ctx->pend_low.as<uint32_t>((uint64_t)n + 1);
+    uint32_t* fb = ctx->perm_stage.as<uint32_t>((uint64_t)n + 1);
+    mark_reachable(ctx, g->off, g->tgt, n, nullptr, s, n_seeds, flags, fa, fb);
+    if (n) DYNPR_CK(cudaMemcpyAsync(vertex_affected, flags, n, cudaMemcpyDefault, ctx->stream));
+    sync(ctx);
   });
 }
 

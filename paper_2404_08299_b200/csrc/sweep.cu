@@ -38,6 +38,7 @@
 // pending in-neighbour) when pushing would touch more edges.  Both produce
 // exactly vertexAffected |= out(pending).
 #include <cstdlib>
+#include <utility>
 
 #include "sweep.cuh"
 
@@ -551,6 +552,62 @@ __global__ void k_expand_high(const uint64_t* off, const uint32_t* tgt, const ui
   }
 }
 
+// ---- markReachable (frontier.cpp:86-121): level-synchronous BFS -------------------
+// Claims a flag byte exactly once (the containing 32-bit word is or-ed, the
+// byte's old value decides the winner); newly claimed vertices are appended
+// to the next frontier with warp-aggregated atomics.
+__device__ __forceinline__ bool claim_byte(uint8_t* flags, uint32_t w) {
+  if (flags[w]) return false;
+  unsigned* word = reinterpret_cast<unsigned*>(flags + (w & ~3u));
+  const unsigned sh = (w & 3u) * 8u;
+  const unsigned old = atomicOr(word, 1u << sh);
+  return ((old >> sh) & 0xffu) == 0u;
+}
+
+__device__ __forceinline__ void warp_push(bool take, uint32_t v, uint32_t* out, unsigned* cnt) {
+  const unsigned mask = __ballot_sync(kFull, take);
+  if (!mask) return;
+  unsigned base = 0;
+  if (lane_id() == 0) base = atomicAdd(cnt, (unsigned)__popc(mask));
+  base = __shfl_sync(kFull, base, 0);
+  if (take) out[base + __popc(mask & ((1u << lane_id()) - 1u))] = v;
+}
+
+__global__ void k_bfs_seed(const uint32_t* inv, const uint32_t* seeds, uint64_t ns, uint8_t* flags, uint32_t* out,
+                           unsigned* cnt) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x; b < ns; b += stride) {
+    const uint64_t i = b + threadIdx.x;
+    uint32_t v = 0;
+    bool take = false;
+    if (i < ns) {
+      v = inv ? inv[seeds[i]] : seeds[i];
+      take = claim_byte(flags, v);
+    }
+    warp_push(take, v, out, cnt);
+  }
+}
+
+// warp per frontier vertex, lanes stride over its out-edges
+__global__ void k_bfs_level(const uint64_t* off, const uint32_t* tgt, const uint32_t* fr, uint32_t nf, uint8_t* flags,
+                            uint32_t* out, unsigned* cnt) {
+  const uint64_t nw = (uint64_t)gridDim.x * blockDim.x / 32;
+  for (uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; i < nf; i += nw) {
+    const uint32_t u = fr[i];
+    const uint64_t b = off[u], e = off[u + 1];
+    for (uint64_t k0 = b; k0 < e; k0 += 32) {
+      const uint64_t k = k0 + lane_id();
+      uint32_t w = 0;
+      bool take = false;
+      if (k < e) {
+        w = tgt[k];
+        take = claim_byte(flags, w);
+      }
+      warp_push(take, w, out, cnt);
+    }
+  }
+}
+
 // ---- norms ------------------------------------------------------------------
 __global__ void k_linf(const double* a, const double* b, uint64_t n, unsigned long long* out) {
   double m = 0.0;
@@ -818,6 +875,33 @@ void launch_expand(dynpr_context* ctx, const uint64_t* off, const uint32_t* tgt,
     check_launch();
     count_launch(ctx);
   }
+}
+
+uint64_t mark_reachable(dynpr_context* ctx, const uint64_t* off, const uint32_t* tgt, uint32_t n, const uint32_t* inv,
+                        const uint32_t* seeds, uint64_t ns, uint8_t* flags, uint32_t* fa, uint32_t* fb) {
+  cudaStream_t st = ctx->stream;
+  auto* cnt = reinterpret_cast<unsigned*>(ctx->scratch32a.as<unsigned>(2));
+  uint64_t reached = 0;
+  if (!ns || !n) return 0;
+  DYNPR_CK(cudaMemsetAsync(cnt, 0, 4, st));
+  k_bfs_seed<<<grid_for(ns, kThreads, ctx->num_sms * 16), kThreads, 0, st>>>(inv, seeds, ns, flags, fa, cnt);
+  check_launch();
+  count_launch(ctx);
+  for (;;) {
+    unsigned nf = 0;
+    DYNPR_CK(cudaMemcpyAsync(ctx->pinned, cnt, 4, cudaMemcpyDeviceToHost, st));
+    sync(ctx);
+    std::memcpy(&nf, ctx->pinned, 4);
+    reached += nf;
+    if (!nf) break;
+    DYNPR_CK(cudaMemsetAsync(cnt, 0, 4, st));
+    k_bfs_level<<<grid_for((uint64_t)nf * 32, kThreads, ctx->num_sms * 16), kThreads, 0, st>>>(off, tgt, fa, nf, flags,
+                                                                                           fb, cnt);
+    check_launch();
+    count_launch(ctx);
+    std::swap(fa, fb);
+  }
+  return reached;
 }
 
 void launch_linf(dynpr_context* ctx, const double* a, const double* b, uint64_t n, unsigned long long* out_bits) {

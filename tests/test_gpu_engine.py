@@ -225,3 +225,50 @@ def test_rmat_static_and_dfp_bitwise(dp, oracle_lib, scale, frac):
     assert_same_result(d, ref)
     for f, (_, _, rf) in zip(got, trace):
         assert np.array_equal(f, rf)
+
+
+# ---- dynamicTraversal / markReachable (engine.cpp:124-151, frontier.cpp:86-121) ----
+@pytest.mark.parametrize("case", [(131, 400, 4000, 8, 0.8, 2024), (137, 300, 1200, 3, 1.0, 77),
+                                  (139, 150, 2500, 6, 0.8, 5), (3, 20000, 200000, 200, 0.8, 9)])
+def test_dynamic_traversal_bitwise_vs_reference(dp, oracle_lib, case):
+    og2, ogt2, dels, ins, prev = batch_case(oracle_lib, *case)
+    g, gt = dev_pair(dp, og2, ogt2)
+    ref = oracle_lib.dynamic_traversal(og2, ogt2, dels, ins, prev)
+    assert_same_result(dp.dynamic_traversal(g, gt, dels, ins, prev), ref)
+
+
+def test_dynamic_traversal_on_rmat(dp, oracle_lib):
+    O = oracle_lib
+    src, dst = O.rmat_edges(14, 16 << 14)
+    og = O.add_self_loops(O.build_csr((src, dst), 1 << 14))
+    base = O.static(O.transpose(og), og)
+    dels, ins = O.generate_random_batch(og, O.batch_size_from_fraction(1e-4, og.m), 0.8, 3)
+    og2, _, _ = O.apply_batch(og, dels, ins)
+    ogt2 = O.transpose(og2)
+    g, gt = dev_pair(dp, og2, ogt2)
+    ref = O.dynamic_traversal(og2, ogt2, dels, ins, base.ranks)
+    assert_same_result(dp.dynamic_traversal(g, gt, dels, ins, base.ranks), ref)
+
+
+def test_dynamic_traversal_errors_and_empty_batch(dp, oracle_lib):
+    og, ogt = rand_pair(oracle_lib, 151, 50, 200)
+    g, gt = dev_pair(dp, og, ogt)
+    prev = np.full(50, 1.0 / 50)
+    r = dp.dynamic_traversal(g, gt, [], [], prev)
+    assert r.converged and r.iterations == 1 and r.affected_vertex_iterations == 0
+    assert np.array_equal(r.ranks, prev)
+    with pytest.raises(ValueError, match="dynamicTraversal: previousRanks length mismatch"):
+        dp.dynamic_traversal(g, gt, [], [], [1.0])
+    with pytest.raises(ValueError, match="markReachable: seed out of range"):
+        dp.dynamic_traversal(g, gt, [], [(70, 1)], prev)
+
+
+@pytest.mark.parametrize("seed,n,pairs,nseeds", [(157, 300, 900, 1), (163, 2000, 5000, 7), (167, 5000, 60000, 40)])
+def test_mark_reachable_vs_reference(dp, oracle_lib, seed, n, pairs, nseeds):
+    og, _ = rand_pair(oracle_lib, seed, n, pairs)
+    g = to_dev(dp, og)
+    seeds = np.random.default_rng(seed).integers(0, n, nseeds).astype(np.uint32)
+    assert np.array_equal(dp.mark_reachable(g, seeds), oracle_lib.mark_reachable(og, seeds))
+    assert not dp.mark_reachable(g, []).any()
+    with pytest.raises(ValueError, match="markReachable: seed out of range"):
+        dp.mark_reachable(g, [n])
