@@ -43,7 +43,9 @@ typedef enum dynpr_status {
   DYNPR_CUDA_ERROR = 2,
   DYNPR_NCCL_ERROR = 3,
   DYNPR_OUT_OF_MEMORY = 4,
-  DYNPR_SIZING_ERROR = 5      /* dynpr::SizingError (workload.hpp:17-19) */
+  DYNPR_SIZING_ERROR = 5,     /* dynpr::SizingError (workload.hpp:17-19) */
+  DYNPR_PARSE_ERROR = 6,      /* dynpr::ParseError (workload.hpp:12-15) */
+  DYNPR_RUNTIME_ERROR = 7     /* std::runtime_error (e.g. "cannot open <path>") */
 } dynpr_status;
 
 /* rank.hpp:14-18 PartitionStrategy */
@@ -307,6 +309,116 @@ dynpr_status dynpr_dynamic_frontier_from_flags(
     uint64_t n_flags, const double* previous, uint64_t n_previous,
     const dynpr_config* cfg, int pruning, double* ranks_out,
     dynpr_stats* stats, dynpr_observer observer, void* observer_user);
+
+/* ---- input formats (workload.hpp:22-64, workload.cpp:43-181) ------------ */
+/* A host edge list: MatrixMarket pairs, or a compacted, timestamp-sorted
+ * temporal stream (TemporalEdgeList).  Parsed from a memory map of the file;
+ * the messages of ParseError ("<path>:<line>: <what>") and of the
+ * "cannot open <path>" runtime_error are the reference's. */
+typedef struct dynpr_edge_list dynpr_edge_list;
+/* loadMatrixMarket (workload.cpp:43-107): general or symmetric coordinate
+ * files, 1-based ids, symmetric off-diagonal entries expanded to both
+ * directions, weights ignored; vertex_count = max(rows, cols). */
+dynpr_status dynpr_load_matrix_market(const char* path, dynpr_edge_list** out);
+/* loadTemporalEdgeList (workload.cpp:109-136): `src dst timestamp` lines,
+ * `#` comments, ids compacted to first-appearance order, entries stably
+ * sorted by timestamp, duplicates kept. */
+dynpr_status dynpr_load_temporal_edge_list(const char* path,
+                                           dynpr_edge_list** out);
+/* splitTemporal (workload.cpp:138-181): `base` = the first
+ * floor(base_fraction * count) entries, sorted and deduplicated; batch b is
+ * entries [base_count + b*batch_size, base_count + (b+1)*batch_size) of the
+ * stream, as insertions.  SizingError text of the reference when short. */
+dynpr_status dynpr_split_temporal(const dynpr_edge_list* stream,
+                                  double base_fraction, int32_t batch_count,
+                                  uint64_t batch_size, dynpr_edge_list** base,
+                                  uint64_t* base_count);
+dynpr_status dynpr_edge_list_info(const dynpr_edge_list* e,
+                                  uint32_t* vertex_count, uint64_t* count,
+                                  int* has_timestamps);
+/* Copies entries [first, first+count) out; ts may be NULL. */
+dynpr_status dynpr_edge_list_copy(const dynpr_edge_list* e, uint64_t first,
+                                  uint64_t count, uint32_t* src, uint32_t* dst,
+                                  int64_t* ts);
+dynpr_status dynpr_edge_list_destroy(dynpr_edge_list* e);
+
+/* ---- experiment harness (harness.hpp:12-79, harness.cpp:68-399) --------- */
+/* computeReferenceRanks (harness.cpp:340-349): Static with the convergence
+ * check disabled, exactly cfg->max_iterations sweeps, on the device. */
+dynpr_status dynpr_compute_reference_ranks(dynpr_context* ctx,
+                                           const dynpr_graph* gT,
+                                           const dynpr_graph* gF,
+                                           const dynpr_config* cfg,
+                                           double* ranks_out);
+
+/* harness.hpp:12 Approach, harness.hpp:16 ExperimentMode, harness.hpp:20-23
+ * ChainMode, harness.hpp:55 ReportFormat. */
+enum {
+  DYNPR_APPROACH_STATIC = 0,
+  DYNPR_APPROACH_ND = 1,
+  DYNPR_APPROACH_DT = 2,
+  DYNPR_APPROACH_DF = 3,
+  DYNPR_APPROACH_DFP = 4
+};
+enum { DYNPR_MODE_STATIC = 0, DYNPR_MODE_TEMPORAL = 1, DYNPR_MODE_RANDOM = 2 };
+enum { DYNPR_CHAIN_PER_APPROACH = 0, DYNPR_CHAIN_SHARED_REFERENCE = 1 };
+enum { DYNPR_REPORT_CSV = 0, DYNPR_REPORT_JSON = 1 };
+
+/* ExperimentSpec (harness.hpp:41-53), field for field. */
+typedef struct dynpr_experiment_spec {
+  const char* graph_path;
+  const char* graph_name;            /* NULL or "" = file stem */
+  int32_t mode;                      /* DYNPR_MODE_* */
+  const char* const* batch_size_specs; /* fraction strings, e.g. "1e-3" */
+  int32_t n_batch_size_specs;
+  const int32_t* approaches;         /* DYNPR_APPROACH_* */
+  int32_t n_approaches;
+  uint64_t seed;                     /* 1 */
+  int32_t repetitions;               /* 1 */
+  double base_fraction;              /* 0.9 (temporal) */
+  int32_t batch_count;               /* 100 (temporal) */
+  double insert_fraction;            /* 0.8 */
+  int32_t chain_mode;                /* DYNPR_CHAIN_PER_APPROACH */
+  int32_t threads;                   /* accepted, ignored: one GPU context */
+  int32_t record_timing;             /* 1; 0 writes deterministic zeros */
+  dynpr_config config;
+} dynpr_experiment_spec;
+void dynpr_experiment_spec_default(dynpr_experiment_spec* spec);
+
+/* ExperimentRow (harness.hpp:29-39).  The strings belong to the report. */
+typedef struct dynpr_experiment_row {
+  const char* graph_name;
+  const char* approach; /* "static" | "nd" | "dt" | "df" | "dfp" */
+  const char* batch_size_spec;
+  int64_t batch_index;  /* -1 = summary row */
+  double runtime_millis;
+  int64_t iterations;
+  uint64_t affected_vertex_iterations;
+  double l1_error_vs_reference; /* NaN when absent */
+  int32_t converged;
+} dynpr_experiment_row;
+
+typedef struct dynpr_report dynpr_report;
+/* runExperiment (harness.cpp:351-381): per-batch rows then one summary row
+ * per (approach, batch size).  Graphs are built, batches ingested and the
+ * 500-sweep reference ranks computed on the device; runtime_millis is the
+ * host wall clock of the engine call alone (harness.cpp:133-135). */
+dynpr_status dynpr_run_experiment(dynpr_context* ctx,
+                                  const dynpr_experiment_spec* spec,
+                                  dynpr_report** out);
+dynpr_status dynpr_report_create(dynpr_report** out);
+dynpr_status dynpr_report_append(dynpr_report* r, const dynpr_experiment_row* row);
+dynpr_status dynpr_report_size(const dynpr_report* r, uint64_t* rows);
+dynpr_status dynpr_report_row(const dynpr_report* r, uint64_t i,
+                              dynpr_experiment_row* out);
+/* summarizeRows (harness.cpp:68-113): geometric means of runtime and error,
+ * rounded arithmetic means of the counters, AND of converged. */
+dynpr_status dynpr_report_summarize(const dynpr_report* r, dynpr_report** out);
+/* emitReport (harness.cpp:287-396): CSV (fixed header) or JSON array, %.17g
+ * floats, NaN -> empty field / null; path "-" = stdout. */
+dynpr_status dynpr_report_emit(const dynpr_report* r, int32_t format,
+                               const char* path);
+dynpr_status dynpr_report_destroy(dynpr_report* r);
 
 #ifdef __cplusplus
 }

@@ -103,6 +103,7 @@ class OracleError(Exception):
     def __init__(self, code: int, msg: str):
         super().__init__(msg)
         self.code = code
+        self.msg = msg
 
 
 @dataclass
@@ -506,6 +507,66 @@ class Oracle:
         self._check(getattr(self.L, self.p + "compute_reference_ranks")(
             C.c_void_p(gT.h), C.c_void_p(gF.h), C.byref(cfg), _ptr(ranks, _dp)))
         return ranks[: gT.n]
+
+    # ---- input formats + harness (reference library only) ------------------
+    def _edges_out(self, h):
+        L = self.L
+        L.ref_edges_count.restype = C.c_uint64
+        L.ref_edges_vertex_count.restype = C.c_uint32
+        for nm in ("ref_edges_count", "ref_edges_vertex_count", "ref_edges_free"):
+            getattr(L, nm).argtypes = [_vp]
+        L.ref_edges_copy.argtypes = [_vp, _vp, _vp, _vp]
+        cnt = L.ref_edges_count(h)
+        n = L.ref_edges_vertex_count(h)
+        s = np.empty(max(cnt, 1), np.uint32)
+        d = np.empty(max(cnt, 1), np.uint32)
+        t = np.empty(max(cnt, 1), np.int64)
+        L.ref_edges_copy(h, s.ctypes.data, d.ctypes.data, t.ctypes.data)
+        L.ref_edges_free(h)
+        return s[:cnt], d[:cnt], t[:cnt], n
+
+    def _load(self, fn, path):
+        fn.argtypes = [C.c_char_p, C.POINTER(_vp)]
+        h = _vp()
+        self._check(fn(str(path).encode(), C.byref(h)))
+        return h.value
+
+    def load_matrix_market(self, path):
+        """loadMatrixMarket -> (src, dst, vertex_count)."""
+        s, d, _, n = self._edges_out(self._load(self.L.ref_load_matrix_market, path))
+        return s, d, n
+
+    def load_temporal(self, path):
+        """loadTemporalEdgeList -> (src, dst, timestamps, vertex_count)."""
+        return self._edges_out(self._load(self.L.ref_load_temporal, path))
+
+    def split_temporal(self, path, base_fraction, batch_count, batch_size):
+        """splitTemporal -> ((base_src, base_dst), (batch_src, batch_dst) concatenated)."""
+        h = self._load(self.L.ref_load_temporal, path)
+        base, batches = _vp(), _vp()
+        self.L.ref_split_temporal.argtypes = [_vp, C.c_double, C.c_int, C.c_uint64, C.POINTER(_vp),
+                                              C.POINTER(_vp)]
+        try:
+            self._check(self.L.ref_split_temporal(h, base_fraction, batch_count, batch_size, C.byref(base),
+                                                  C.byref(batches)))
+        finally:
+            self.L.ref_edges_free(h)
+        bs, bd, _, _ = self._edges_out(base.value)
+        s, d, _, _ = self._edges_out(batches.value)
+        return (bs, bd), (s, d)
+
+    def run_experiment(self, spec_struct, fmt: int, out_path: str):
+        """runExperiment + emitReport; spec_struct is a dynpr_experiment_spec
+        ctypes structure (paper_2404_08299_b200._native.ExperimentSpec)."""
+        self.L.ref_run_experiment.argtypes = [_vp, C.c_int, C.c_char_p]
+        self._check(self.L.ref_run_experiment(C.addressof(spec_struct), fmt, str(out_path).encode()))
+
+    def summarize_emit(self, rows_array, count: int, summarize: bool, fmt: int, out_path: str):
+        """summarizeRows (optional) + emitReport over a ctypes array of
+        dynpr_experiment_row."""
+        self.L.ref_summarize_emit.argtypes = [_vp, C.c_uint64, C.c_int, C.c_int, C.c_char_p]
+        self._check(self.L.ref_summarize_emit(C.addressof(rows_array), count, int(summarize), fmt,
+                                              str(out_path).encode()))
 
 
 class PortRng:

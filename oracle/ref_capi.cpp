@@ -39,6 +39,8 @@ int fail(const std::exception& e) {
   g_error = e.what();
   if (dynamic_cast<const std::invalid_argument*>(&e)) return 1;
   if (dynamic_cast<const SizingError*>(&e)) return 5;
+  if (dynamic_cast<const ParseError*>(&e)) return 6;
+  if (dynamic_cast<const std::runtime_error*>(&e)) return 7;
   return 2;
 }
 
@@ -430,6 +432,122 @@ uint64_t ref_batch_size_from_fraction(double f, uint64_t total) {
 }
 int ref_validate_config(const dynpr_config* c) {
   return guard([&] { toCfg(c).validate(); });
+}
+
+// ---- input formats + harness (workload.cpp:43-181, harness.cpp) ------------
+// Loaders return a heap EdgeBuf the caller reads with ref_edges_* and frees.
+struct EdgeBuf {
+  std::vector<uint32_t> s, d;
+  std::vector<int64_t> t;
+  uint32_t n = 0;
+};
+int ref_load_matrix_market(const char* path, void** out) {
+  return guard([&] {
+    auto mm = loadMatrixMarket(path);
+    auto* b = new EdgeBuf;
+    b->n = mm.vertexCount;
+    for (auto& e : mm.edges) {
+      b->s.push_back(e.first);
+      b->d.push_back(e.second);
+    }
+    *out = b;
+  });
+}
+int ref_load_temporal(const char* path, void** out) {
+  return guard([&] {
+    auto t = loadTemporalEdgeList(path);
+    auto* b = new EdgeBuf;
+    b->n = t.vertexCount;
+    for (auto& e : t.entries) {
+      b->s.push_back(e.source);
+      b->d.push_back(e.target);
+      b->t.push_back(e.timestamp);
+    }
+    *out = b;
+  });
+}
+// splitTemporal of a loaded stream: base edges into a new EdgeBuf, batches
+// concatenated into another (batch_count * batch_size insertions).
+int ref_split_temporal(const void* stream, double baseFraction, int batchCount,
+                       uint64_t batchSize, void** base, void** batches) {
+  return guard([&] {
+    const auto* b = static_cast<const EdgeBuf*>(stream);
+    TemporalEdgeList t;
+    t.vertexCount = b->n;
+    for (size_t i = 0; i < b->s.size(); ++i) t.entries.push_back({b->s[i], b->d[i], b->t[i]});
+    auto sp = splitTemporal(t, baseFraction, batchCount, batchSize);
+    auto* bb = new EdgeBuf;
+    bb->n = b->n;
+    for (auto& e : sp.baseEdges) {
+      bb->s.push_back(e.first);
+      bb->d.push_back(e.second);
+    }
+    auto* ba = new EdgeBuf;
+    ba->n = b->n;
+    for (auto& batch : sp.batches)
+      for (auto& e : batch.insertions) {
+        ba->s.push_back(e.first);
+        ba->d.push_back(e.second);
+      }
+    *base = bb;
+    *batches = ba;
+  });
+}
+uint64_t ref_edges_count(const void* e) { return static_cast<const EdgeBuf*>(e)->s.size(); }
+uint32_t ref_edges_vertex_count(const void* e) { return static_cast<const EdgeBuf*>(e)->n; }
+void ref_edges_copy(const void* e, uint32_t* s, uint32_t* d, int64_t* t) {
+  const auto* b = static_cast<const EdgeBuf*>(e);
+  std::memcpy(s, b->s.data(), b->s.size() * 4);
+  std::memcpy(d, b->d.data(), b->d.size() * 4);
+  if (t && !b->t.empty()) std::memcpy(t, b->t.data(), b->t.size() * 8);
+}
+void ref_edges_free(void* e) { delete static_cast<EdgeBuf*>(e); }
+
+// runExperiment + emitReport (harness.hpp:41-79) with the fields of
+// dynpr_experiment_spec; the report is written to `out_path`.
+int ref_run_experiment(const dynpr_experiment_spec* s, int format, const char* out_path) {
+  return guard([&] {
+    ExperimentSpec spec;
+    spec.graphPath = s->graph_path ? s->graph_path : "";
+    spec.graphName = s->graph_name ? s->graph_name : "";
+    spec.mode = static_cast<ExperimentMode>(s->mode);
+    for (int i = 0; i < s->n_batch_size_specs; ++i) spec.batchSizeSpecs.push_back(s->batch_size_specs[i]);
+    for (int i = 0; i < s->n_approaches; ++i) spec.approaches.push_back(static_cast<Approach>(s->approaches[i]));
+    spec.seed = s->seed;
+    spec.repetitions = s->repetitions;
+    spec.baseFraction = s->base_fraction;
+    spec.batchCount = s->batch_count;
+    spec.insertFraction = s->insert_fraction;
+    spec.chainMode = static_cast<ChainMode>(s->chain_mode);
+    spec.threads = s->threads;
+    spec.recordTiming = s->record_timing != 0;
+    spec.config = toCfg(&s->config);
+    auto rows = runExperiment(spec);
+    emitReport(rows, format ? ReportFormat::Json : ReportFormat::Csv, out_path);
+  });
+}
+
+// summarizeRows + emitReport over caller rows (dynpr_experiment_row layout).
+int ref_summarize_emit(const dynpr_experiment_row* in, uint64_t count, int summarize, int format,
+                       const char* out_path) {
+  return guard([&] {
+    std::vector<ExperimentRow> rows;
+    for (uint64_t i = 0; i < count; ++i) {
+      ExperimentRow r;
+      r.graphName = in[i].graph_name;
+      r.approach = in[i].approach;
+      r.batchSizeSpec = in[i].batch_size_spec;
+      r.batchIndex = in[i].batch_index;
+      r.runtimeMillis = in[i].runtime_millis;
+      r.iterations = in[i].iterations;
+      r.affectedVertexIterations = in[i].affected_vertex_iterations;
+      r.l1ErrorVsReference = in[i].l1_error_vs_reference;
+      r.converged = in[i].converged != 0;
+      rows.push_back(r);
+    }
+    if (summarize) rows = summarizeRows(rows);
+    emitReport(rows, format ? ReportFormat::Json : ReportFormat::Csv, out_path);
+  });
 }
 
 }  // extern "C"

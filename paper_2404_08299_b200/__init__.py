@@ -35,6 +35,10 @@ __all__ = [
     "static_pagerank", "transpose", "update_ranks", "generate_random_batch", "batch_size_from_fraction",
     "derive_seed", "prepare", "LocalTeam", "nccl_unique_id", "share_nccl_unique_id",
     "context_from_process_group", "attach_symmetric_exchange", "dynamic_traversal", "mark_reachable",
+    "ParseError", "Approach", "ExperimentMode", "ChainMode", "ReportFormat", "ExperimentRow", "ExperimentSpec",
+    "approach_name", "approach_from_name", "load_matrix_market", "load_matrix_market_arrays",
+    "load_temporal_edge_list", "load_temporal_edge_list_arrays", "split_temporal", "compute_reference_ranks",
+    "run_experiment", "summarize_rows", "emit_report",
 ]
 
 
@@ -660,3 +664,11 @@ def dynamic_frontier_from_flags(g_forward: CsrGraph, g_transpose: CsrGraph, vert
                                                      _p(prev), len(prev), C.byref(cfg), int(bool(pruning)),
                                                      _p(ranks), C.byref(st), obs, None))
     return _result(ranks[: g_transpose.vertex_count], st)
+
+
+from ._harness import (  # noqa: E402  (input formats + experiment harness)
+    Approach, ChainMode, ExperimentMode, ExperimentRow, ExperimentSpec, ParseError, ReportFormat,
+    approach_from_name, approach_name, compute_reference_ranks, emit_report, load_matrix_market,
+    load_matrix_market_arrays, load_temporal_edge_list, load_temporal_edge_list_arrays, run_experiment,
+    split_temporal, summarize_rows,
+)

@@ -21,6 +21,8 @@ DYNPR_CUDA_ERROR = 2
 DYNPR_NCCL_ERROR = 3
 DYNPR_OUT_OF_MEMORY = 4
 DYNPR_SIZING_ERROR = 5
+DYNPR_PARSE_ERROR = 6
+DYNPR_RUNTIME_ERROR = 7
 
 
 class Config(C.Structure):
@@ -44,6 +46,41 @@ class Stats(C.Structure):
         ("final_delta", C.c_double),
         ("processed_edges", C.c_uint64),
         ("device_ms", C.c_double),
+    ]
+
+
+class ExperimentSpec(C.Structure):  # dynpr_experiment_spec
+    _fields_ = [
+        ("graph_path", C.c_char_p),
+        ("graph_name", C.c_char_p),
+        ("mode", C.c_int32),
+        ("batch_size_specs", C.POINTER(C.c_char_p)),
+        ("n_batch_size_specs", C.c_int32),
+        ("approaches", C.POINTER(C.c_int32)),
+        ("n_approaches", C.c_int32),
+        ("seed", C.c_uint64),
+        ("repetitions", C.c_int32),
+        ("base_fraction", C.c_double),
+        ("batch_count", C.c_int32),
+        ("insert_fraction", C.c_double),
+        ("chain_mode", C.c_int32),
+        ("threads", C.c_int32),
+        ("record_timing", C.c_int32),
+        ("config", Config),
+    ]
+
+
+class ExperimentRow(C.Structure):  # dynpr_experiment_row
+    _fields_ = [
+        ("graph_name", C.c_char_p),
+        ("approach", C.c_char_p),
+        ("batch_size_spec", C.c_char_p),
+        ("batch_index", C.c_int64),
+        ("runtime_millis", C.c_double),
+        ("iterations", C.c_int64),
+        ("affected_vertex_iterations", C.c_uint64),
+        ("l1_error_vs_reference", C.c_double),
+        ("converged", C.c_int32),
     ]
 
 
@@ -113,6 +150,22 @@ PROTOTYPES = {
     "dynpr_mark_reachable": (_i, [_vp, _vp, _vp, _u64, _vp]),
     "dynpr_dynamic_frontier_from_flags": (_i, [_vp, _vp, _vp, _vp, _vp, _u64, _vp, _u64, _cfgp, _i, _vp,
                                                _stp, OBSERVER, _vp]),
+    "dynpr_load_matrix_market": (_i, [C.c_char_p, _pvp]),
+    "dynpr_load_temporal_edge_list": (_i, [C.c_char_p, _pvp]),
+    "dynpr_split_temporal": (_i, [_vp, _d, C.c_int32, _u64, _pvp, _u64p]),
+    "dynpr_edge_list_info": (_i, [_vp, _u32p, _u64p, _ip]),
+    "dynpr_edge_list_copy": (_i, [_vp, _u64, _u64, _vp, _vp, _vp]),
+    "dynpr_edge_list_destroy": (_i, [_vp]),
+    "dynpr_compute_reference_ranks": (_i, [_vp, _vp, _vp, _cfgp, _vp]),
+    "dynpr_experiment_spec_default": (None, [C.POINTER(ExperimentSpec)]),
+    "dynpr_run_experiment": (_i, [_vp, C.POINTER(ExperimentSpec), _pvp]),
+    "dynpr_report_create": (_i, [_pvp]),
+    "dynpr_report_append": (_i, [_vp, C.POINTER(ExperimentRow)]),
+    "dynpr_report_size": (_i, [_vp, _u64p]),
+    "dynpr_report_row": (_i, [_vp, _u64, C.POINTER(ExperimentRow)]),
+    "dynpr_report_summarize": (_i, [_vp, _pvp]),
+    "dynpr_report_emit": (_i, [_vp, C.c_int32, C.c_char_p]),
+    "dynpr_report_destroy": (_i, [_vp]),
 }
 
 _lib = None

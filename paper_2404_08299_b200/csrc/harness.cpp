@@ -1,0 +1,891 @@
+// Input formats and the experiment harness: the callers either side of the
+// hot path.
+//
+//  * loadMatrixMarket / loadTemporalEdgeList / splitTemporal
+//    (workload.cpp:43-181): the file is memory-mapped and tokenised in place
+//    with std::from_chars -- same token rules as the reference's
+//    getline + istringstream (whitespace = C-locale isspace, one trailing
+//    '\r' chomped, comment tests on the raw first byte), same ParseError
+//    texts and line numbers -- instead of a stringstream per line.
+//  * runExperiment / summarizeRows / emitReport (harness.cpp:68-399): the
+//    static, random-batch and temporal protocols driven through this
+//    library's device engines.  Every graph lives on the device: the base
+//    CSR pair is built there (buildCsr + addSelfLoops + transpose), each
+//    batch is ingested with apply_batch_pair (forward and transpose updated
+//    together, byte-identical to applyBatch + transpose), the 500-sweep
+//    reference ranks (computeReferenceRanks) and the L1 errors are computed
+//    on the device, and the chained warm-start ranks never leave it.  Only
+//    the report rows come back to the host.
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <charconv>
+#include <chrono>
+#include <cerrno>
+#include <cmath>
+#include <cstdio>
+#include <fstream>
+#include <iostream>
+#include <map>
+#include <memory>
+#include <string>
+#include <unordered_map>
+#include <utility>
+#include <vector>
+
+#include "common.cuh"
+
+struct dynpr_edge_list {
+  uint32_t n = 0;
+  std::vector<uint32_t> src, dst;
+  std::vector<int64_t> ts;  // empty unless a temporal stream
+  bool temporal = false;
+};
+
+struct dynpr_report {
+  struct Row {
+    std::string graph, approach, spec;
+    int64_t batch_index = 0;
+    double runtime = 0.0;
+    int64_t iterations = 0;
+    uint64_t affected = 0;
+    double l1 = 0.0;
+    bool converged = false;
+  };
+  std::vector<Row> rows;
+};
+
+namespace dynpr_b200 {
+namespace {
+
+[[noreturn]] void parse_error(const std::string& path, uint64_t line, const std::string& what) {
+  throw Error(DYNPR_PARSE_ERROR, path + ":" + std::to_string(line) + ": " + what);
+}
+
+// Read-only memory map of a whole file (empty files map to nothing).
+struct MappedFile {
+  const char* data = nullptr;
+  size_t size = 0;
+  explicit MappedFile(const std::string& path) {
+    int fd = ::open(path.c_str(), O_RDONLY);
+    if (fd < 0) throw Error(DYNPR_RUNTIME_ERROR, "cannot open " + path);
+    struct stat st;
+    if (::fstat(fd, &st) != 0 || S_ISDIR(st.st_mode)) {
+      ::close(fd);
+      throw Error(DYNPR_RUNTIME_ERROR, "cannot open " + path);
+    }
+    size = static_cast<size_t>(st.st_size);
+    if (size) {
+      void* p = ::mmap(nullptr, size, PROT_READ, MAP_PRIVATE, fd, 0);
+      if (p == MAP_FAILED) {
+        ::close(fd);
+        throw Error(DYNPR_RUNTIME_ERROR, "cannot open " + path);
+      }
+      ::madvise(p, size, MADV_SEQUENTIAL);
+      data = static_cast<const char*>(p);
+    }
+    ::close(fd);
+  }
+  ~MappedFile() {
+    if (data) ::munmap(const_cast<char*>(data), size);
+  }
+};
+
+// std::getline over the mapped bytes: yields [b, e) without the '\n', then
+// chomps one '\r' (workload.cpp:34-36).  A final line without '\n' counts;
+// an empty file yields no line.
+struct LineReader {
+  const char* p;
+  const char* end;
+  LineReader(const MappedFile& f) : p(f.data), end(f.data + f.size) {}
+  bool next(const char*& b, const char*& e) {
+    if (p >= end) return false;
+    b = p;
+    const char* nl = static_cast<const char*>(memchr(p, '\n', static_cast<size_t>(end - p)));
+    e = nl ? nl : end;
+    p = nl ? nl + 1 : end;
+    if (e > b && e[-1] == '\r') --e;
+    return true;
+  }
+};
+
+inline bool is_space(char c) {  // isspace in the "C" locale
+  return c == ' ' || c == '\t' || c == '\n' || c == '\v' || c == '\f' || c == '\r';
+}
+
+// istream >> std::string: skip whitespace, take the next non-space run
+// (empty when the line is exhausted).
+struct Tokens {
+  const char* p;
+  const char* e;
+  std::pair<const char*, const char*> next() {
+    while (p < e && is_space(*p)) ++p;
+    const char* b = p;
+    while (p < e && !is_space(*p)) ++p;
+    return {b, p};
+  }
+};
+
+template <class T>
+bool parse_num(std::pair<const char*, const char*> tok, T& out) {  // workload.cpp:22-30
+  auto [p, ec] = std::from_chars(tok.first, tok.second, out);
+  return ec == std::errc() && p == tok.second;
+}
+
+std::string lower(std::pair<const char*, const char*> tok) {
+  std::string s(tok.first, tok.second);
+  for (char& c : s) c = static_cast<char>(std::tolower(static_cast<unsigned char>(c)));
+  return s;
+}
+
+// loadMatrixMarket -- workload.cpp:43-107.
+dynpr_edge_list* load_matrix_market(const std::string& path) {
+  MappedFile f(path);
+  LineReader lines(f);
+  const char *b, *e;
+  uint64_t line_no = 0;
+  if (!lines.next(b, e)) parse_error(path, 1, "empty file");
+  ++line_no;
+  Tokens header{b, e};
+  const std::string banner = lower(header.next()), object = lower(header.next()),
+                    format = lower(header.next());
+  header.next();  // field
+  const std::string symmetry = lower(header.next());
+  if (banner != "%%matrixmarket") parse_error(path, line_no, "missing %%MatrixMarket banner");
+  if (object != "matrix" || format != "coordinate")
+    parse_error(path, line_no, "only 'matrix coordinate' files are supported");
+  const bool symmetric = symmetry == "symmetric" || symmetry == "skew-symmetric" || symmetry == "hermitian";
+
+  uint64_t rows = 0, cols = 0, declared = 0;
+  for (;;) {
+    if (!lines.next(b, e)) parse_error(path, line_no + 1, "missing size line");
+    ++line_no;
+    if (e == b || *b == '%') continue;
+    Tokens t{b, e};
+    auto r = t.next(), c = t.next(), z = t.next();
+    if (!parse_num(r, rows) || !parse_num(c, cols) || !parse_num(z, declared))
+      parse_error(path, line_no, "malformed size line");
+    break;
+  }
+  auto out = std::make_unique<dynpr_edge_list>();
+  out->n = static_cast<uint32_t>(std::max(rows, cols));
+  // Reserve from the file size, not the declared count (a lying header must
+  // not allocate): every entry line takes at least 4 bytes.
+  const size_t guess = std::min<uint64_t>(symmetric ? declared * 2 : declared, f.size / 2 + 16);
+  out->src.reserve(guess);
+  out->dst.reserve(guess);
+  uint64_t seen = 0;
+  while (seen < declared) {
+    if (!lines.next(b, e))
+      parse_error(path, line_no + 1,
+                  "expected " + std::to_string(declared) + " entries, got " + std::to_string(seen));
+    ++line_no;
+    if (e == b || *b == '%') continue;
+    Tokens t{b, e};
+    auto si = t.next(), sj = t.next();  // any weight column is ignored
+    uint64_t i = 0, j = 0;
+    if (!parse_num(si, i) || !parse_num(sj, j)) parse_error(path, line_no, "malformed entry");
+    if (i < 1 || i > rows || j < 1 || j > cols) parse_error(path, line_no, "index out of declared bounds");
+    ++seen;
+    const auto u = static_cast<uint32_t>(i - 1), v = static_cast<uint32_t>(j - 1);
+    out->src.push_back(u);
+    out->dst.push_back(v);
+    if (symmetric && u != v) {
+      out->src.push_back(v);
+      out->dst.push_back(u);
+    }
+  }
+  return out.release();
+}
+
+// loadTemporalEdgeList -- workload.cpp:109-136.  Ids are compacted in
+// first-appearance order (source before target within a line); the entries
+// are then stably sorted by timestamp (a stable permutation sort on the
+// 64-bit keys).
+dynpr_edge_list* load_temporal(const std::string& path) {
+  MappedFile f(path);
+  LineReader lines(f);
+  auto out = std::make_unique<dynpr_edge_list>();
+  out->temporal = true;
+  std::unordered_map<uint64_t, uint32_t> compact;
+  compact.reserve(1024);
+  auto compact_id = [&](uint64_t raw) {
+    return compact.emplace(raw, static_cast<uint32_t>(compact.size())).first->second;
+  };
+  std::vector<uint32_t> s, d;
+  std::vector<int64_t> ts;
+  const char *b, *e;
+  uint64_t line_no = 0;
+  while (lines.next(b, e)) {
+    ++line_no;
+    if (e == b || *b == '#') continue;
+    Tokens t{b, e};
+    auto a = t.next(), c = t.next(), z = t.next();
+    uint64_t src = 0, dst = 0;
+    int64_t stamp = 0;
+    if (!parse_num(a, src) || !parse_num(c, dst) || !parse_num(z, stamp))
+      parse_error(path, line_no, "expected 'src dst timestamp'");
+    const uint32_t cs = compact_id(src);
+    const uint32_t cd = compact_id(dst);
+    s.push_back(cs);
+    d.push_back(cd);
+    ts.push_back(stamp);
+  }
+  out->n = static_cast<uint32_t>(compact.size());
+  const size_t cnt = ts.size();
+  bool sorted = std::is_sorted(ts.begin(), ts.end());
+  if (sorted) {
+    out->src = std::move(s);
+    out->dst = std::move(d);
+    out->ts = std::move(ts);
+  } else {
+    std::vector<uint64_t> perm(cnt);
+    for (size_t i = 0; i < cnt; ++i) perm[i] = i;
+    std::stable_sort(perm.begin(), perm.end(), [&](uint64_t x, uint64_t y) { return ts[x] < ts[y]; });
+    out->src.resize(cnt);
+    out->dst.resize(cnt);
+    out->ts.resize(cnt);
+    for (size_t i = 0; i < cnt; ++i) {
+      out->src[i] = s[perm[i]];
+      out->dst[i] = d[perm[i]];
+      out->ts[i] = ts[perm[i]];
+    }
+  }
+  return out.release();
+}
+
+// splitTemporal -- workload.cpp:138-181 (base part; the batches are ranges
+// of the stream).
+uint64_t split_base_count(const dynpr_edge_list* t, double base_fraction, int32_t batch_count,
+                          uint64_t batch_size) {
+  if (!(base_fraction > 0.0 && base_fraction < 1.0))
+    invalid("splitTemporal: baseFraction must be in (0,1)");
+  if (batch_count < 1 || batch_size < 1) invalid("splitTemporal: batchCount and batchSize must be >= 1");
+  const uint64_t total = t->src.size();
+  const auto base = static_cast<uint64_t>(std::floor(base_fraction * static_cast<double>(total)));
+  const uint64_t needed = base + static_cast<uint64_t>(batch_count) * batch_size;
+  if (needed > total) {
+    const uint64_t fit = (total - std::min(base, total)) / batch_size;
+    throw Error(DYNPR_SIZING_ERROR, "splitTemporal: stream has " + std::to_string(total) + " entries; only " +
+                                        std::to_string(fit) + " of " + std::to_string(batch_count) +
+                                        " batches of size " + std::to_string(batch_size) + " fit after the base");
+  }
+  return base;
+}
+
+dynpr_edge_list* split_base(const dynpr_edge_list* t, uint64_t base) {
+  auto out = std::make_unique<dynpr_edge_list>();
+  out->n = t->n;
+  std::vector<uint64_t> keys(base);
+  for (uint64_t i = 0; i < base; ++i) keys[i] = (uint64_t(t->src[i]) << 32) | t->dst[i];
+  std::sort(keys.begin(), keys.end());
+  keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+  out->src.resize(keys.size());
+  out->dst.resize(keys.size());
+  for (size_t i = 0; i < keys.size(); ++i) {
+    out->src[i] = static_cast<uint32_t>(keys[i] >> 32);
+    out->dst[i] = static_cast<uint32_t>(keys[i]);
+  }
+  return out.release();
+}
+
+// ---- harness ----------------------------------------------------------------
+
+using Clock = std::chrono::steady_clock;
+
+const char* approach_name(int32_t a) {  // harness.cpp:318-327
+  switch (a) {
+    case DYNPR_APPROACH_STATIC: return "static";
+    case DYNPR_APPROACH_ND: return "nd";
+    case DYNPR_APPROACH_DT: return "dt";
+    case DYNPR_APPROACH_DF: return "df";
+    case DYNPR_APPROACH_DFP: return "dfp";
+  }
+  invalid("unknown approach");
+}
+
+std::string file_stem(const std::string& path) {  // harness.cpp:26-32
+  const auto slash = path.find_last_of("/\\");
+  std::string name = slash == std::string::npos ? path : path.substr(slash + 1);
+  const auto dot = name.find_last_of('.');
+  if (dot != std::string::npos && dot > 0) name = name.substr(0, dot);
+  return name;
+}
+
+double stod_like(const std::string& s) {  // std::stod: leading space, prefix parse
+  const char* b = s.c_str();
+  char* end = nullptr;
+  errno = 0;
+  const double v = std::strtod(b, &end);
+  if (end == b) invalid("stod");
+  if (errno == ERANGE && (v == HUGE_VAL || v == -HUGE_VAL)) invalid("stod");
+  return v;
+}
+
+// Status -> exception, keeping the library's message.
+void ck(dynpr_status st) {
+  if (st != DYNPR_OK) throw Error(st, dynpr_last_error());
+}
+
+struct Graph {  // owning handle
+  dynpr_graph* g = nullptr;
+  Graph() = default;
+  explicit Graph(dynpr_graph* h) : g(h) {}
+  Graph(Graph&& o) noexcept : g(o.g) { o.g = nullptr; }
+  Graph& operator=(Graph&& o) noexcept {
+    if (this != &o) {
+      if (g) dynpr_graph_destroy(g);
+      g = o.g;
+      o.g = nullptr;
+    }
+    return *this;
+  }
+  ~Graph() {
+    if (g) dynpr_graph_destroy(g);
+  }
+  uint64_t m() const {
+    uint32_t n;
+    uint64_t m;
+    dynpr_graph_info(g, &n, &m);
+    return m;
+  }
+  uint32_t n() const {
+    uint32_t n;
+    uint64_t m;
+    dynpr_graph_info(g, &n, &m);
+    return n;
+  }
+};
+
+struct Pair {  // harness.cpp:117-127 LoadedGraph
+  Graph forward, transposed;
+};
+
+Pair augment_and_transpose(dynpr_context* ctx, const std::vector<uint32_t>& s, const std::vector<uint32_t>& d,
+                           uint32_t n) {
+  dynpr_graph *raw = nullptr, *loops = nullptr, *t = nullptr;
+  ck(dynpr_graph_build(ctx, n, s.data(), d.data(), s.size(), &raw));
+  Graph graw(raw);
+  ck(dynpr_graph_add_self_loops(ctx, raw, &loops));
+  Pair p;
+  p.forward = Graph(loops);
+  ck(dynpr_graph_transpose(ctx, loops, &t));
+  p.transposed = Graph(t);
+  return p;
+}
+
+// Host batch (edge-list pairs) staged once to the device for the engines.
+struct Batch {
+  std::vector<uint32_t> ds, dd, is, id;
+};
+
+struct Runner {
+  dynpr_context* ctx;
+  const dynpr_experiment_spec& spec;
+  const std::string graph_name;
+  dynpr_report* rep;
+  uint32_t n = 0;
+
+  // Chain ranks per approach (harness.cpp:140-149), device-resident.
+  std::map<int32_t, std::unique_ptr<DevBuf>> chain;
+  DevBuf reference, result, scratch;
+
+  double* chain_of(int32_t a) { return chain.at(a)->as<double>(n); }
+
+  void reset_chains(const double* from) {
+    for (int i = 0; i < spec.n_approaches; ++i) {
+      auto& slot = chain[spec.approaches[i]];
+      if (!slot) slot = std::make_unique<DevBuf>();
+      DYNPR_CK(cudaMemcpyAsync(slot->as<double>(n), from, n * sizeof(double), cudaMemcpyDeviceToDevice,
+                               ctx->stream));
+    }
+    sync(ctx);
+  }
+
+  // harness.cpp:34-54 runApproach
+  void run_approach(int32_t a, const Pair& p, const Batch& b, const double* prev, double* out, dynpr_stats* st) {
+    const dynpr_config* c = &spec.config;
+    switch (a) {
+      case DYNPR_APPROACH_STATIC:
+        ck(dynpr_static_pagerank(ctx, p.transposed.g, p.forward.g, c, out, st, nullptr, nullptr));
+        return;
+      case DYNPR_APPROACH_ND:
+        ck(dynpr_naive_dynamic(ctx, p.transposed.g, p.forward.g, prev, n, c, out, st, nullptr, nullptr));
+        return;
+      case DYNPR_APPROACH_DT:
+        ck(dynpr_dynamic_traversal(ctx, p.forward.g, p.transposed.g, b.ds.data(), b.dd.data(), b.ds.size(),
+                                   b.is.data(), b.id.data(), b.is.size(), prev, n, c, out, st, nullptr, nullptr));
+        return;
+      case DYNPR_APPROACH_DF:
+      case DYNPR_APPROACH_DFP:
+        ck(dynpr_dynamic_frontier(ctx, p.forward.g, p.transposed.g, b.ds.data(), b.dd.data(), b.ds.size(),
+                                  b.is.data(), b.id.data(), b.is.size(), prev, n, c, a == DYNPR_APPROACH_DFP, out,
+                                  st, nullptr, nullptr));
+        return;
+    }
+    invalid("unknown approach");
+  }
+
+  void reference_ranks(const Pair& p, double* out) {  // harness.cpp:340-349
+    ck(dynpr_compute_reference_ranks(ctx, p.transposed.g, p.forward.g, &spec.config, out));
+  }
+
+  dynpr_report::Row row(int32_t a, const std::string& size_spec, int64_t index, double ms, const dynpr_stats& st,
+                        double l1) {
+    dynpr_report::Row r;
+    r.graph = graph_name;
+    r.approach = approach_name(a);
+    r.spec = size_spec;
+    r.batch_index = index;
+    r.runtime = spec.record_timing ? ms : 0.0;
+    r.iterations = st.iterations;
+    r.affected = st.affected_vertex_iterations;
+    r.l1 = l1;
+    r.converged = st.converged != 0;
+    return r;
+  }
+
+  // harness.cpp:129-155 runBatchStep
+  void batch_step(const Pair& p, const Batch& b, const std::string& size_spec, int64_t index) {
+    double* ref = reference.as<double>(n);
+    reference_ranks(p, ref);
+    double* out = result.as<double>(n);
+    for (int i = 0; i < spec.n_approaches; ++i) {
+      const int32_t a = spec.approaches[i];
+      const double* prev = chain_of(a);
+      dynpr_stats st{};
+      const auto t0 = Clock::now();
+      run_approach(a, p, b, prev, out, &st);
+      const double ms = std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
+      double l1 = 0.0;
+      ck(dynpr_l1_norm_delta(ctx, out, ref, n, &l1));
+      rep->rows.push_back(row(a, size_spec, index, ms, st, l1));
+      if (a != DYNPR_APPROACH_STATIC) {
+        const double* keep = spec.chain_mode == DYNPR_CHAIN_SHARED_REFERENCE ? ref : out;
+        DYNPR_CK(cudaMemcpyAsync(chain_of(a), keep, n * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+        sync(ctx);
+      }
+    }
+  }
+
+  // Snapshots are immutable; the engine layout is built once per ingested
+  // pair here (like the reference's transpose, outside the timed region).
+  void prepare(const Pair& p, bool forward) {
+    ck(dynpr_graph_prepare(ctx, p.transposed.g, p.forward.g, spec.config.low_degree_threshold, forward ? 1 : 0,
+                           nullptr));
+  }
+
+  bool needs_forward() const {
+    for (int i = 0; i < spec.n_approaches; ++i)
+      if (spec.approaches[i] != DYNPR_APPROACH_STATIC && spec.approaches[i] != DYNPR_APPROACH_ND) return true;
+    return false;
+  }
+
+  Pair apply(const Pair& p, const Batch& b) {
+    dynpr_graph *gf = nullptr, *gt = nullptr;
+    ck(dynpr_graph_apply_batch_pair(ctx, p.forward.g, p.transposed.g, b.ds.data(), b.dd.data(), b.ds.size(),
+                                    b.is.data(), b.id.data(), b.is.size(), &gf, &gt, nullptr, nullptr));
+    Pair q;
+    q.forward = Graph(gf);
+    q.transposed = Graph(gt);
+    return q;
+  }
+
+  // harness.cpp:241-270 runStatic
+  void run_static() {
+    std::unique_ptr<dynpr_edge_list> mm(load_matrix_market(spec.graph_path));
+    n = mm->n;
+    Pair p = augment_and_transpose(ctx, mm->src, mm->dst, mm->n);
+    n = p.forward.n();
+    double* ref = reference.as<double>(n);
+    reference_ranks(p, ref);
+    double* out = result.as<double>(n);
+    for (int rep_i = 0; rep_i < spec.repetitions; ++rep_i) {
+      dynpr_stats st{};
+      const auto t0 = Clock::now();
+      ck(dynpr_static_pagerank(ctx, p.transposed.g, p.forward.g, &spec.config, out, &st, nullptr, nullptr));
+      const double ms = std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
+      double l1 = 0.0;
+      ck(dynpr_l1_norm_delta(ctx, out, ref, n, &l1));
+      rep->rows.push_back(row(DYNPR_APPROACH_STATIC, "0", rep_i, ms, st, l1));
+    }
+  }
+
+  // harness.cpp:211-239 runRandomBatch
+  void run_random() {
+    std::unique_ptr<dynpr_edge_list> mm(load_matrix_market(spec.graph_path));
+    Pair base = augment_and_transpose(ctx, mm->src, mm->dst, mm->n);
+    mm.reset();
+    n = base.forward.n();
+    const uint64_t m = base.forward.m();
+    DevBuf base_ranks;
+    ck(dynpr_static_pagerank(ctx, base.transposed.g, base.forward.g, &spec.config, base_ranks.as<double>(n),
+                             nullptr, nullptr, nullptr));
+    for (int si = 0; si < spec.n_batch_size_specs; ++si) {
+      const std::string size_spec = spec.batch_size_specs[si];
+      const uint64_t size = dynpr_batch_size_from_fraction(stod_like(size_spec), m);
+      for (int r = 0; r < spec.repetitions; ++r) {
+        const uint64_t sub = dynpr_derive_seed(spec.seed, uint64_t(si) * 1000003ULL + uint64_t(r));
+        Batch b;
+        b.is.resize(size);
+        b.id.resize(size);
+        b.ds.resize(size);
+        b.dd.resize(size);
+        uint64_t ni = 0, nd = 0;
+        ck(dynpr_generate_random_batch(ctx, base.forward.g, size, spec.insert_fraction, sub, b.is.data(),
+                                       b.id.data(), &ni, b.ds.data(), b.dd.data(), &nd));
+        b.is.resize(ni);
+        b.id.resize(ni);
+        b.ds.resize(nd);
+        b.dd.resize(nd);
+        Pair p = apply(base, b);
+        prepare(p, needs_forward());
+        reset_chains(base_ranks.as<double>(n));
+        batch_step(p, b, size_spec, r);
+      }
+    }
+  }
+
+  // harness.cpp:157-182 runTemporal
+  void run_temporal() {
+    std::unique_ptr<dynpr_edge_list> stream(load_temporal(spec.graph_path));
+    for (int si = 0; si < spec.n_batch_size_specs; ++si) {
+      const std::string size_spec = spec.batch_size_specs[si];
+      const uint64_t size = dynpr_batch_size_from_fraction(stod_like(size_spec), stream->src.size());
+      const uint64_t base_count = split_base_count(stream.get(), spec.base_fraction, spec.batch_count, size);
+      std::unique_ptr<dynpr_edge_list> base(split_base(stream.get(), base_count));
+      Pair p = augment_and_transpose(ctx, base->src, base->dst, stream->n);
+      base.reset();
+      n = p.forward.n();
+      DevBuf initial;
+      ck(dynpr_static_pagerank(ctx, p.transposed.g, p.forward.g, &spec.config, initial.as<double>(n), nullptr,
+                               nullptr, nullptr));
+      reset_chains(initial.as<double>(n));
+      for (int bi = 0; bi < spec.batch_count; ++bi) {
+        Batch b;
+        const uint64_t first = base_count + uint64_t(bi) * size;
+        b.is.assign(stream->src.begin() + first, stream->src.begin() + first + size);
+        b.id.assign(stream->dst.begin() + first, stream->dst.begin() + first + size);
+        Pair q = apply(p, b);
+        p = std::move(q);
+        prepare(p, needs_forward());
+        batch_step(p, b, size_spec, bi);
+      }
+    }
+  }
+};
+
+// harness.cpp:56-66
+double geometric_mean(const std::vector<double>& values) {
+  if (values.empty()) return 0.0;
+  double log_sum = 0.0;
+  for (double v : values) {
+    if (!(v > 0.0)) return 0.0;
+    log_sum += std::log(v);
+  }
+  return std::exp(log_sum / static_cast<double>(values.size()));
+}
+
+// harness.cpp:68-113 summarizeRows
+std::vector<dynpr_report::Row> summarize(const std::vector<dynpr_report::Row>& rows) {
+  std::vector<std::pair<std::string, std::string>> order;
+  std::map<std::pair<std::string, std::string>, std::vector<const dynpr_report::Row*>> groups;
+  for (const auto& r : rows) {
+    auto key = std::make_pair(r.approach, r.spec);
+    auto [it, inserted] = groups.emplace(key, std::vector<const dynpr_report::Row*>{});
+    if (inserted) order.push_back(key);
+    it->second.push_back(&r);
+  }
+  std::vector<dynpr_report::Row> out;
+  for (const auto& key : order) {
+    const auto& g = groups[key];
+    dynpr_report::Row s;
+    s.graph = g.front()->graph;
+    s.approach = key.first;
+    s.spec = key.second;
+    s.batch_index = -1;
+    std::vector<double> runtimes, errors;
+    double iter_sum = 0.0, affected_sum = 0.0;
+    bool all = true;
+    for (const auto* r : g) {
+      runtimes.push_back(r->runtime);
+      if (!std::isnan(r->l1)) errors.push_back(r->l1);
+      iter_sum += static_cast<double>(r->iterations);
+      affected_sum += static_cast<double>(r->affected);
+      all = all && r->converged;
+    }
+    s.runtime = geometric_mean(runtimes);
+    s.l1 = errors.empty() ? std::nan("") : geometric_mean(errors);
+    s.iterations = static_cast<int64_t>(std::llround(iter_sum / static_cast<double>(g.size())));
+    s.affected = static_cast<uint64_t>(std::llround(affected_sum / static_cast<double>(g.size())));
+    s.converged = all;
+    out.push_back(std::move(s));
+  }
+  return out;
+}
+
+void fmt_double(std::string& out, double v) {  // harness.cpp:272-276
+  char buf[64];
+  std::snprintf(buf, sizeof buf, "%.17g", v);
+  out += buf;
+}
+
+std::string escape_json(const std::string& s) {
+  std::string out;
+  for (char c : s) {
+    if (c == '"' || c == '\\') out += '\\';
+    out += c;
+  }
+  return out;
+}
+
+// harness.cpp:287-316 writeCsv / 318-352 writeJson
+std::string render(const std::vector<dynpr_report::Row>& rows, int32_t format) {
+  std::string out;
+  if (format == DYNPR_REPORT_CSV) {
+    out += "graphName,approach,batchSizeSpec,batchIndex,runtimeMillis,"
+           "iterations,affectedVertexIterations,l1ErrorVsReference,converged\n";
+    for (const auto& r : rows) {
+      out += r.graph;
+      out += ',';
+      out += r.approach;
+      out += ',';
+      out += r.spec;
+      out += ',';
+      out += std::to_string(r.batch_index);
+      out += ',';
+      fmt_double(out, r.runtime);
+      out += ',';
+      out += std::to_string(r.iterations);
+      out += ',';
+      out += std::to_string(r.affected);
+      out += ',';
+      if (!std::isnan(r.l1)) fmt_double(out, r.l1);
+      out += ',';
+      out += r.converged ? "true" : "false";
+      out += '\n';
+    }
+  } else {
+    out += "[\n";
+    for (size_t i = 0; i < rows.size(); ++i) {
+      const auto& r = rows[i];
+      out += "  {\"graphName\":\"" + escape_json(r.graph) + "\",\"approach\":\"" + escape_json(r.approach) +
+             "\",\"batchSizeSpec\":\"" + escape_json(r.spec) + "\",\"batchIndex\":" +
+             std::to_string(r.batch_index) + ",\"runtimeMillis\":";
+      fmt_double(out, r.runtime);
+      out += ",\"iterations\":" + std::to_string(r.iterations) +
+             ",\"affectedVertexIterations\":" + std::to_string(r.affected) + ",\"l1ErrorVsReference\":";
+      if (std::isnan(r.l1))
+        out += "null";
+      else
+        fmt_double(out, r.l1);
+      out += ",\"converged\":";
+      out += r.converged ? "true" : "false";
+      out += i + 1 < rows.size() ? "},\n" : "}\n";
+    }
+    out += "]\n";
+  }
+  return out;
+}
+
+}  // namespace
+}  // namespace dynpr_b200
+
+using namespace dynpr_b200;
+
+extern "C" {
+
+dynpr_status dynpr_load_matrix_market(const char* path, dynpr_edge_list** out) {
+  return api_guard([&] {
+    if (!path || !out) invalid("null argument");
+    *out = load_matrix_market(path);
+  });
+}
+
+dynpr_status dynpr_load_temporal_edge_list(const char* path, dynpr_edge_list** out) {
+  return api_guard([&] {
+    if (!path || !out) invalid("null argument");
+    *out = load_temporal(path);
+  });
+}
+
+dynpr_status dynpr_split_temporal(const dynpr_edge_list* stream, double base_fraction, int32_t batch_count,
+                                  uint64_t batch_size, dynpr_edge_list** base, uint64_t* base_count) {
+  return api_guard([&] {
+    if (!stream || !base || !base_count) invalid("null argument");
+    const uint64_t bc = split_base_count(stream, base_fraction, batch_count, batch_size);
+    *base = split_base(stream, bc);
+    *base_count = bc;
+  });
+}
+
+dynpr_status dynpr_edge_list_info(const dynpr_edge_list* e, uint32_t* vertex_count, uint64_t* count,
+                                  int* has_timestamps) {
+  return api_guard([&] {
+    if (!e) invalid("null edge list");
+    if (vertex_count) *vertex_count = e->n;
+    if (count) *count = e->src.size();
+    if (has_timestamps) *has_timestamps = e->temporal ? 1 : 0;
+  });
+}
+
+dynpr_status dynpr_edge_list_copy(const dynpr_edge_list* e, uint64_t first, uint64_t count, uint32_t* src,
+                                  uint32_t* dst, int64_t* ts) {
+  return api_guard([&] {
+    if (!e) invalid("null edge list");
+    if (first > e->src.size() || count > e->src.size() - first) invalid("edge list range out of bounds");
+    if (count && (!src || !dst)) invalid("null output array");
+    std::memcpy(src, e->src.data() + first, count * sizeof(uint32_t));
+    std::memcpy(dst, e->dst.data() + first, count * sizeof(uint32_t));
+    if (ts && count) {
+      if (!e->temporal) invalid("edge list has no timestamps");
+      std::memcpy(ts, e->ts.data() + first, count * sizeof(int64_t));
+    }
+  });
+}
+
+dynpr_status dynpr_edge_list_destroy(dynpr_edge_list* e) {
+  delete e;
+  return DYNPR_OK;
+}
+
+dynpr_status dynpr_compute_reference_ranks(dynpr_context* ctx, const dynpr_graph* gT, const dynpr_graph* gF,
+                                           const dynpr_config* cfg, double* ranks_out) {
+  return api_guard([&] {
+    if (!cfg) invalid("null config");
+    dynpr_config c = *cfg;  // harness.cpp:340-349
+    c.convergence_check_disabled = 1;
+    ck(dynpr_static_pagerank(ctx, gT, gF, &c, ranks_out, nullptr, nullptr, nullptr));
+  });
+}
+
+void dynpr_experiment_spec_default(dynpr_experiment_spec* s) {
+  if (!s) return;
+  std::memset(s, 0, sizeof *s);
+  s->mode = DYNPR_MODE_STATIC;
+  s->seed = 1;
+  s->repetitions = 1;
+  s->base_fraction = 0.9;
+  s->batch_count = 100;
+  s->insert_fraction = 0.8;
+  s->chain_mode = DYNPR_CHAIN_PER_APPROACH;
+  s->record_timing = 1;
+  dynpr_config_default(&s->config);
+}
+
+// harness.cpp:351-381 runExperiment
+dynpr_status dynpr_run_experiment(dynpr_context* ctx, const dynpr_experiment_spec* spec, dynpr_report** out) {
+  return api_guard([&] {
+    if (!ctx || !spec || !out) invalid("null argument");
+    ck(dynpr_config_validate(&spec->config));
+    const std::string path = spec->graph_path ? spec->graph_path : "";
+    const std::string name =
+        spec->graph_name && spec->graph_name[0] ? std::string(spec->graph_name) : file_stem(path);
+    if (spec->n_approaches < 1 || !spec->approaches) invalid("runExperiment: no approaches requested");
+    for (int i = 0; i < spec->n_approaches; ++i) approach_name(spec->approaches[i]);
+    if (spec->mode != DYNPR_MODE_STATIC && (spec->n_batch_size_specs < 1 || !spec->batch_size_specs))
+      invalid("runExperiment: no batch sizes requested");
+    if (spec->repetitions < 1) invalid("runExperiment: repetitions must be >= 1");
+    if (spec->mode != DYNPR_MODE_STATIC && spec->mode != DYNPR_MODE_TEMPORAL && spec->mode != DYNPR_MODE_RANDOM)
+      invalid("runExperiment: unknown mode");
+    bind_device(ctx);
+    auto rep = std::make_unique<dynpr_report>();
+    Runner r{ctx, *spec, name, rep.get()};
+    switch (spec->mode) {
+      case DYNPR_MODE_STATIC: r.run_static(); break;
+      case DYNPR_MODE_TEMPORAL: r.run_temporal(); break;
+      case DYNPR_MODE_RANDOM: r.run_random(); break;
+    }
+    auto sums = summarize(rep->rows);
+    rep->rows.insert(rep->rows.end(), sums.begin(), sums.end());
+    *out = rep.release();
+  });
+}
+
+dynpr_status dynpr_report_create(dynpr_report** out) {
+  return api_guard([&] {
+    if (!out) invalid("null argument");
+    *out = new dynpr_report();
+  });
+}
+
+dynpr_status dynpr_report_append(dynpr_report* r, const dynpr_experiment_row* row) {
+  return api_guard([&] {
+    if (!r || !row) invalid("null argument");
+    dynpr_report::Row x;
+    x.graph = row->graph_name ? row->graph_name : "";
+    x.approach = row->approach ? row->approach : "";
+    x.spec = row->batch_size_spec ? row->batch_size_spec : "";
+    x.batch_index = row->batch_index;
+    x.runtime = row->runtime_millis;
+    x.iterations = row->iterations;
+    x.affected = row->affected_vertex_iterations;
+    x.l1 = row->l1_error_vs_reference;
+    x.converged = row->converged != 0;
+    r->rows.push_back(std::move(x));
+  });
+}
+
+dynpr_status dynpr_report_size(const dynpr_report* r, uint64_t* rows) {
+  return api_guard([&] {
+    if (!r || !rows) invalid("null argument");
+    *rows = r->rows.size();
+  });
+}
+
+dynpr_status dynpr_report_row(const dynpr_report* r, uint64_t i, dynpr_experiment_row* out) {
+  return api_guard([&] {
+    if (!r || !out) invalid("null argument");
+    if (i >= r->rows.size()) invalid("report row out of range");
+    const auto& x = r->rows[i];
+    out->graph_name = x.graph.c_str();
+    out->approach = x.approach.c_str();
+    out->batch_size_spec = x.spec.c_str();
+    out->batch_index = x.batch_index;
+    out->runtime_millis = x.runtime;
+    out->iterations = x.iterations;
+    out->affected_vertex_iterations = x.affected;
+    out->l1_error_vs_reference = x.l1;
+    out->converged = x.converged ? 1 : 0;
+  });
+}
+
+dynpr_status dynpr_report_summarize(const dynpr_report* r, dynpr_report** out) {
+  return api_guard([&] {
+    if (!r || !out) invalid("null argument");
+    auto s = std::make_unique<dynpr_report>();
+    s->rows = summarize(r->rows);
+    *out = s.release();
+  });
+}
+
+// harness.cpp:380-396 emitReport
+dynpr_status dynpr_report_emit(const dynpr_report* r, int32_t format, const char* path) {
+  return api_guard([&] {
+    if (!r || !path) invalid("null argument");
+    if (r->rows.empty()) invalid("emitReport: no rows");
+    if (format != DYNPR_REPORT_CSV && format != DYNPR_REPORT_JSON) invalid("emitReport: unknown format");
+    const std::string text = render(r->rows, format);
+    const std::string p = path;
+    if (p == "-") {
+      std::cout << text;
+      std::cout.flush();
+      if (!std::cout) throw Error(DYNPR_RUNTIME_ERROR, "emitReport: write failed");
+      return;
+    }
+    std::ofstream f(p);
+    if (!f) throw Error(DYNPR_RUNTIME_ERROR, "emitReport: cannot open " + p);
+    f << text;
+    if (!f) throw Error(DYNPR_RUNTIME_ERROR, "emitReport: write failed");
+  });
+}
+
+dynpr_status dynpr_report_destroy(dynpr_report* r) {
+  delete r;
+  return DYNPR_OK;
+}
+
+}  // extern "C"
