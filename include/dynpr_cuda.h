@@ -420,6 +420,12 @@ dynpr_status dynpr_report_emit(const dynpr_report* r, int32_t format,
                                const char* path);
 dynpr_status dynpr_report_destroy(dynpr_report* r);
 
+/* ---- debug ---------------------------------------------------------------- */
+/* With DYNPR_TRACE set in the environment the fused sweep records, per warp,
+ * {smid, start ns, end ns, heavy items | light items << 32, first heavy item,
+ * end of heavy phase ns} of the latest sweep; copies up to `cap` words. */
+dynpr_status dynpr_debug_sweep_trace(uint64_t* out, uint64_t cap, uint64_t* count);
+
 #ifdef __cplusplus
 }
 #endif

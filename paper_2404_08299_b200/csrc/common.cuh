@@ -70,7 +70,10 @@ struct DevBuf {
     if (p) DYNPR_CK(cudaFree(p));
     p = nullptr;
     cap = 0;
-    size_t want = bytes < 256 ? 256 : bytes;
+    // 25% headroom: snapshots of a batch stream grow by a few edges at a
+    // time, and a re-allocation (cudaFree synchronises the device) must not
+    // land inside an engine call's timed region on every batch
+    size_t want = bytes < 256 ? 256 : bytes + bytes / 4;
     DYNPR_CK(cudaMalloc(&p, want));
     cap = want;
     return p;
@@ -89,6 +92,8 @@ struct SweepRed {
   unsigned long long pend_edges;  // out-edges of the pending vertices
   unsigned int pend_low;          // pending vertices with out-degree <= T
   unsigned int pend_high;         // 1024-edge expansion items of the others
+  unsigned int ticket_heavy;      // fused sweep work queues (dynamic scheduling)
+  unsigned int ticket_light;
 };
 
 // Out-edges per expansion work item of a high out-degree vertex.
@@ -120,7 +125,7 @@ struct dynpr_context {
   dynpr_b200::DevBuf rank[2], contrib[2], flags_va, flags_np, flags_written,
       pend_low, pend_high, pend_flags, partials, perm_stage,
       tile_counts, red, stage_a, stage_b, stage_c, stage_d, stage_e, stage_f,
-      cub_tmp, scratch64a, scratch64b, scratch32a, scratch32b, scratch8a, batch[4];
+      cub_tmp, tick, scratch64a, scratch64b, scratch32a, scratch32b, scratch8a, batch[4];
 };
 
 namespace dynpr_b200 {

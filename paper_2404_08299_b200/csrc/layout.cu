@@ -247,6 +247,16 @@ Layout* build_layout(dynpr_context* ctx, const dynpr_graph* gT, const dynpr_grap
     count_launch(ctx, 2);
     L->M = (uint32_t)(read_u64(ctx, cnt) & 0xffffffffu);
     const uint32_t M = L->M;
+    DYNPR_CK(cudaMemsetAsync(cnt, 0, 8, st));
+    k_count_above<<<grid(ctx, n), 256, 0, st>>>(L->indeg, n, kHeavyDeg < thr ? kHeavyDeg : thr, cnt);
+    check_launch();
+    count_launch(ctx);
+    {
+      const uint32_t nh = (uint32_t)(read_u64(ctx, cnt) & 0xffffffffu);
+      L->n_hslices = nh > M ? ((uint64_t)(nh - M) + 31) / 32 : 0;
+    }
+    L->mcount = dalloc<uint32_t>((uint64_t)M + 1);
+    DYNPR_CK(cudaMemsetAsync(L->mcount, 0, ((size_t)M + 1) * 4, st));
     // single region slices
     L->n_sslices = ((uint64_t)(n - M) + 31) / 32;
     L->sbase = dalloc<uint64_t>(L->n_sslices + 1);
@@ -312,7 +322,7 @@ Layout* build_layout(dynpr_context* ctx, const dynpr_graph* gT, const dynpr_grap
 
 Layout::~Layout() {
   for (void* p : {(void*)perm, (void*)inv, (void*)indeg, (void*)outdeg, (void*)sbase, (void*)sell_s, (void*)mbase,
-                  (void*)mseg_v, (void*)mseg_len, (void*)pbase, (void*)sell_m, (void*)offF, (void*)tgtF})
+                  (void*)mseg_v, (void*)mseg_len, (void*)pbase, (void*)sell_m, (void*)mcount, (void*)offF, (void*)tgtF})
     pool_free(ctx, p);
 }
 

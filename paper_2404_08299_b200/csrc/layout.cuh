@@ -41,6 +41,11 @@ struct RankRange {
   uint64_t ss_lo, ss_hi, ms_lo, ms_hi;
 };
 
+// Single-region slices whose first (largest) segment is longer than this are
+// "heavy": the fused sweep schedules them one at a time, first, together with
+// the multi-vertex chunk slices (their lane chains set the sweep's latency).
+constexpr uint32_t kHeavyDeg = 64;
+
 struct Layout {
   dynpr_context* ctx = nullptr;
   uint32_t n = 0;
@@ -54,6 +59,7 @@ struct Layout {
   uint32_t M = 0;              // multi-segment vertices are [0, M)
   // single-segment region: vertices [M, n), slice s = vertices M+32s..+31
   uint64_t n_sslices = 0;
+  uint64_t n_hslices = 0;      // leading single slices with in-degree > kHeavyDeg
   uint64_t* sbase = nullptr;   // n_sslices + 1
   uint32_t* sell_s = nullptr;
   // multi region: segments in (vertex, chunk) order
@@ -64,6 +70,7 @@ struct Layout {
   uint32_t* mseg_len = nullptr;
   uint32_t* pbase = nullptr;   // first segment of multi vertex v (M + 1)
   uint32_t* sell_m = nullptr;
+  uint32_t* mcount = nullptr;  // per multi vertex: chunks finished this sweep (0 between sweeps)
   // relabelled forward CSR (frontier engines)
   bool has_forward = false;
   uint64_t* offF = nullptr;

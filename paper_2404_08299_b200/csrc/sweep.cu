@@ -38,6 +38,7 @@
 // pending in-neighbour) when pushing would touch more edges.  Both produce
 // exactly vertexAffected |= out(pending).
 #include <cstdlib>
+#include <string>
 #include <utility>
 
 #include "sweep.cuh"
@@ -347,6 +348,228 @@ __global__ void __launch_bounds__(kThreads) k_sweep_mfinal(SweepArgs a) {
   }
   if (a.npeers) __threadfence_system();  // peer stores visible before the team barrier
   block_reduce_commit(acc, a.red);
+}
+
+// ---- fused sweep: one kernel, dynamically scheduled ----------------------------
+// The three-kernel sweep above serialises the multi-chunk slices, the
+// single-vertex slices and the ordered combine; on graphs that do not fill
+// the GPU many times over the sweep time is then the sum of the longest lane
+// chains of each kernel (a 256-edge segment is 32 dependent gather rounds).
+// The fused kernel runs all of it in one launch:
+//  * heavy items first -- every multi-chunk slice, then the single slices whose
+//    largest segment exceeds kHeavyDeg -- dealt round-robin to the resident
+//    blocks (per-block counters), so the long chains start together at the
+//    beginning of the sweep, spread over all SMs (a per-warp trace showed
+//    that first-come grabbing piled several hub chains onto one SM, whose
+//    request queue then set the sweep time), and gather with a 16-deep
+//    pipeline; then the light single slices in global grabs of kLightGrab;
+//  * a multi vertex is finished by the warp that completes its last chunk
+//    (per-vertex completion counter, threadfence + atomic), which combines
+//    the partials in chunk order (rank.cpp:72) with a warp-wide load and a
+//    shuffle-broadcast sequential sum, and runs the epilogue.
+// Every vertex's sum and epilogue are exactly those of the split kernels.
+constexpr unsigned kLightGrab = 4;
+// Above this many slices per resident warp the sweep is throughput-bound and
+// the split kernels are used.
+constexpr uint64_t kSplitSlicesPerWarp = 64;
+constexpr unsigned kMaxBlocks = 4096;  // persistent grids are <= 8 x SMs
+
+// Debug timeline (DYNPR_TRACE=1): per warp of the last fused sweep, {smid,
+// start, end, heavy items | light items << 32, first heavy item, end of the
+// heavy phase} in globaltimer ns; read with dynpr_debug_sweep_trace.
+constexpr int kTraceWarps = 148 * 64;
+__device__ unsigned long long g_trace[kTraceWarps * 6];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(r));
+  return r;
+}
+
+template <int Q>
+__device__ __forceinline__ double segment_sum_deep(const uint32_t* __restrict__ sell, uint64_t base, unsigned lane,
+                                                   uint32_t len, uint32_t Lw, const double* __restrict__ contrib,
+                                                   uint32_t self, double cself) {
+  constexpr uint32_t D = 4 * Q;  // elements in flight per lane
+  const uint32_t* p = sell + base + 4u * lane;
+  const uint4 z = make_uint4(0, 0, 0, 0);
+  double c = 0.0;
+  uint4 ix[Q];
+#pragma unroll
+  for (int j = 0; j < Q; ++j) ix[j] = (4u * j < len) ? ld_idx4(p + 128ull * j) : z;
+  for (uint32_t k = 0; k < Lw; k += D) {
+    double x[D];
+#pragma unroll
+    for (int j = 0; j < Q; ++j) {
+      const uint32_t u[4] = {ix[j].x, ix[j].y, ix[j].z, ix[j].w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        x[4 * j + q] = (k + 4 * j + q < len) ? ld_contrib(contrib, nullptr, u[q], 0, self, cself) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < Q; ++j) ix[j] = (k + D + 4 * j < len) ? ld_idx4(p + 32ull * (k + D + 4 * j)) : z;
+#pragma unroll
+    for (uint32_t q = 0; q < D; ++q)
+      if (k + q < len) c = __dadd_rn(c, x[q]);
+  }
+  return c;
+}
+
+// One single-region slice (the body of k_sweep_single).
+template <bool FLAGGED, bool CLOSED, int Q>
+__device__ __forceinline__ void single_slice(const SweepArgs& a, uint64_t s, unsigned lane, Acc& acc) {
+  const uint64_t vv = (uint64_t)a.M + s * 32 + lane;
+  const bool valid = vv < a.n;
+  const uint32_t v = (uint32_t)vv;
+  const uint32_t deg = valid ? a.indeg[v] : 0u;
+  bool aff = valid;
+  if (FLAGGED) aff = valid && a.va[v];
+  const uint32_t len = aff ? deg : 0u;
+  const uint32_t Lw = __reduce_max_sync(kFull, len);
+  double pv = 0.0, cself = 0.0;
+  uint32_t od = 0;
+  if (aff) {
+    pv = a.rank_prev[v];
+    od = a.outdeg[v];
+    cself = a.contrib_prev[v];
+  }
+  double c = 0.0;
+  if (Lw) c = segment_sum_deep<Q>(a.sell_s, a.sbase[s], lane, len, Lw, a.contrib_prev, v, cself);
+  bool pend = false, lowout = false;
+  if (valid) {
+    if (!aff) {
+      copy_through(a, v);
+    } else {
+      finalize<FLAGGED, CLOSED>(a, v, c, pv, od, acc, pend, lowout);
+      ++acc.proc;
+      acc.edges += deg;
+    }
+  }
+  if (FLAGGED && a.pend_low) warp_append(pend, lowout, v, od, a.pend_low, a.pend_high, a.red);
+}
+
+// One multi-chunk slice: 32 chunk partials; the warp that completes a
+// vertex's last chunk combines and finalises it.
+template <bool FLAGGED, bool CLOSED, int Q>
+__device__ __forceinline__ void multi_slice(const SweepArgs& a, uint64_t s, unsigned lane, Acc& acc) {
+  const uint64_t seg = s * 32 + lane;
+  uint32_t len = 0, v = 0xffffffffu;
+  if (seg < a.n_mseg) {
+    v = a.mseg_v[seg];
+    len = a.mseg_len[seg];
+    if (v < a.v_lo || v >= a.v_hi) {
+      len = 0;  // another rank's vertex
+    } else if (FLAGGED && !a.va[v]) {
+      len = 0;
+      if (seg == a.pbase[v]) copy_through(a, v);  // first chunk's lane does the copy-through
+    }
+  }
+  const uint32_t Lw = __reduce_max_sync(kFull, len);
+  if (!Lw) return;
+  const double c = segment_sum_deep<Q>(a.sell_m, a.mbase[s], lane, len, Lw, a.contrib_prev, 0xffffffffu, 0.0);
+  bool last = false;
+  if (len) {
+    __stcg(a.partials + seg, c);
+    __threadfence();
+    const uint32_t nch = (a.indeg[v] + kAccumChunk - 1) / kAccumChunk;
+    last = atomicAdd(a.mcount + v, 1u) == nch - 1;
+    if (last) __threadfence();
+  }
+  unsigned lm = __ballot_sync(kFull, last);
+  if (!lm) return;
+  __syncwarp();
+  double cfin = 0.0;
+  while (lm) {
+    const int L = __ffs(lm) - 1;
+    lm &= lm - 1;
+    const uint32_t w = __shfl_sync(kFull, v, L);
+    const uint32_t pb = a.pbase[w], nch = a.pbase[w + 1] - pb;
+    double sum = 0.0;
+    for (uint32_t g = 0; g < nch; g += 32) {
+      const double x = (g + lane < nch) ? __ldcg(a.partials + pb + g + lane) : 0.0;
+      const uint32_t cnt = nch - g < 32 ? nch - g : 32;
+      for (uint32_t j = 0; j < cnt; ++j) sum = __dadd_rn(sum, __shfl_sync(kFull, x, j));
+    }
+    if ((int)lane == L) {
+      cfin = sum;
+      a.mcount[w] = 0;  // ready for the next sweep
+    }
+  }
+  bool pend = false, lowout = false;
+  uint32_t od = 0;
+  if (last) {
+    od = a.outdeg[v];
+    finalize<FLAGGED, CLOSED>(a, v, cfin, a.rank_prev[v], od, acc, pend, lowout);
+    ++acc.proc;
+    acc.edges += a.indeg[v];
+  }
+  if (FLAGGED && a.pend_low) warp_append(pend, lowout, v, od, a.pend_low, a.pend_high, a.red);
+}
+
+template <bool FLAGGED, bool CLOSED, int QH>
+__device__ __forceinline__ void fused_body(const SweepArgs& a) {
+  Acc acc;
+  const unsigned lane = lane_id();
+  const uint64_t n_ms = a.ms_hi - a.ms_lo;
+  const uint64_t hs_hi = a.ss_heavy < a.ss_hi ? a.ss_heavy : a.ss_hi;
+  const uint64_t n_hs = hs_hi > a.ss_lo ? hs_hi - a.ss_lo : 0;
+  const uint64_t n_heavy = n_ms + n_hs;
+  const unsigned long long t0 = a.trace ? gtimer() : 0ull;
+  unsigned long long nh = 0, nl = 0, first = ~0ull, th = 0;
+  // heavy items are dealt round-robin to the (all resident) blocks -- item =
+  // block + grid * k, k from a per-block counter -- so the long chains are
+  // spread over the SMs instead of piling onto whichever warps grab first
+  for (;;) {
+    unsigned k = 0;
+    if (lane == 0) k = atomicAdd(a.tick_sm + blockIdx.x, 1u);
+    k = __shfl_sync(kFull, k, 0);
+    const uint64_t t = (uint64_t)blockIdx.x + (uint64_t)gridDim.x * k;
+    if (t >= n_heavy) break;
+    ++nh;
+    if (first == ~0ull) first = t;
+    if (t < n_ms)
+      multi_slice<FLAGGED, CLOSED, QH>(a, a.ms_lo + t, lane, acc);
+    else
+      single_slice<FLAGGED, CLOSED, QH>(a, a.ss_lo + (t - n_ms), lane, acc);
+  }
+  if (a.trace) th = gtimer();
+  const uint64_t l_lo = a.ss_lo + n_hs;
+  const uint64_t n_light = a.ss_hi > l_lo ? a.ss_hi - l_lo : 0;
+  for (;;) {
+    unsigned t = 0;
+    if (lane == 0) t = atomicAdd(&a.red->ticket_light, kLightGrab);
+    t = __shfl_sync(kFull, t, 0);
+    if (t >= n_light) break;
+    const uint64_t e = t + kLightGrab < n_light ? t + kLightGrab : n_light;
+    nl += e - t;
+    for (uint64_t i = t; i < e; ++i) single_slice<FLAGGED, CLOSED, 2>(a, l_lo + i, lane, acc);
+  }
+  if (a.trace && lane == 0) {
+    const uint64_t w = ((uint64_t)blockIdx.x * kSweepThreads + threadIdx.x) / 32;
+    if (w < kTraceWarps) {
+      unsigned long long* r = g_trace + 6 * w;
+      r[0] = smid();
+      r[1] = t0;
+      r[2] = gtimer();
+      r[3] = nh | (nl << 32);
+      r[4] = first;
+      r[5] = th;
+    }
+  }
+  if (a.npeers) __threadfence_system();  // peer stores visible before the team barrier
+  block_reduce_commit(acc, a.red);
+}
+
+// 16-deep heavy chains at 4 CTAs per SM.  (A 5-CTA, 8-deep variant was
+// measured: it spills and is no faster on large graphs, where the split
+// kernels win -- profiles/ab_probe.py.)
+template <bool FLAGGED, bool CLOSED>
+__global__ void __launch_bounds__(kSweepThreads, 4) k_sweep_fused(SweepArgs a) {
+  fused_body<FLAGGED, CLOSED, 4>(a);
 }
 
 // ---- pull expansion over the SELL in-lists ------------------------------------------
@@ -719,6 +942,10 @@ SweepArgs layout_args(const Layout* L, double* partials) {
   a.pbase = L->pbase;
   a.sell_m = L->sell_m;
   a.partials = partials;
+  static const int trace = std::getenv("DYNPR_TRACE") != nullptr;
+  a.trace = trace;
+  a.mcount = L->mcount;
+  a.ss_heavy = L->n_hslices;
   // Hot prefix held in L1: ~200 KB of L1 per SM (shared-memory carveout 0)
   // = 25,600 contributions; DYNPR_HOT overrides for tuning.
   static const uint32_t hot_default = [] {
@@ -808,7 +1035,33 @@ void launch_sweep(dynpr_context* ctx, const SweepArgs& a, bool flagged, bool clo
       ++launched;                                                                                   \
     }                                                                                               \
   } while (0)
-  if (flagged) {
+  // Latency-bound graphs (few slices per resident warp) take the fused
+  // kernel; throughput-bound ones the split kernels (measured A/B,
+  // profiles/ab_probe.py: fused wins 1.2-1.5x on RMAT-18..22, split wins
+  // ~3% on RMAT-24).  DYNPR_SWEEP=split|fused overrides.
+  const char* mode = std::getenv("DYNPR_SWEEP");
+  const std::string m = mode ? mode : "";
+  const uint64_t resident_warps = (uint64_t)ctx->num_sms * 32;
+  const bool big = (n_ms + n_ss) > kSplitSlicesPerWarp * resident_warps;
+  const bool split = m == "split" || (m != "fused" && big);
+  if (!split) {
+    // one persistent launch; the work counters live in the (zeroed) record
+    SweepArgs af = a;
+    af.tick_sm = ctx->tick.as<uint32_t>(kMaxBlocks);
+    DYNPR_CK(cudaMemsetAsync(af.tick_sm, 0, kMaxBlocks * sizeof(uint32_t), st));
+    const uint64_t wb = (n_ms + n_ss + kSweepWarps - 1) / kSweepWarps;
+#define DYNPR_FUSED(F, C) \
+  k_sweep_fused<F, C><<<persistent_grid(ctx, k_sweep_fused<F, C>, wb), kSweepThreads, 0, st>>>(af)
+    if (n_ms + n_ss) {
+      if (flagged) {
+        if (closed) DYNPR_FUSED(true, true); else DYNPR_FUSED(true, false);
+      } else {
+        if (closed) DYNPR_FUSED(false, true); else DYNPR_FUSED(false, false);
+      }
+      ++launched;
+    }
+#undef DYNPR_FUSED
+  } else if (flagged) {
     if (closed) DYNPR_SWEEP(true, true); else DYNPR_SWEEP(true, false);
   } else {
     if (closed) DYNPR_SWEEP(false, true); else DYNPR_SWEEP(false, false);
@@ -924,3 +1177,11 @@ void launch_l1(dynpr_context* ctx, const double* a, const double* b, uint64_t n,
 }
 
 }  // namespace dynpr_b200
+
+extern "C" dynpr_status dynpr_debug_sweep_trace(uint64_t* out, uint64_t cap, uint64_t* count) {
+  return dynpr_b200::api_guard([&] {
+    const uint64_t n = 6ull * dynpr_b200::kTraceWarps;
+    if (count) *count = n;
+    if (out && cap) DYNPR_CK(cudaMemcpyFromSymbol(out, dynpr_b200::g_trace, (cap < n ? cap : n) * 8));
+  });
+}

@@ -37,6 +37,10 @@ struct SweepArgs {
   const uint32_t* pbase;
   const uint32_t* sell_m;
   double* partials;
+  uint32_t* tick_sm;     // fused sweep: per-block heavy-item counters (zeroed before each sweep)
+  uint32_t* mcount;      // per multi vertex chunk-completion counters (fused sweep)
+  uint64_t ss_heavy;     // single slices [0, ss_heavy) are heavy (layout n_hslices)
+  int trace;     // debug: record per-warp timelines of the fused sweep (DYNPR_TRACE)
   uint32_t hot;  // new ids < hot: contributions kept L1-resident (evict_last)
   // iteration state
   double alpha, teleport, tf, tp;
