@@ -121,11 +121,14 @@ struct dynpr_context {
   cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_s0 = nullptr, ev_s1 = nullptr;
   // pinned host scratch for small readbacks
   void* pinned = nullptr;
+  // instantiated device-loop graphs (engine.cu LoopGraphCache), keyed by
+  // sweep plan; owned
+  void* loop_graphs = nullptr;
   // workspace (grow-only; the engines never allocate inside the timed loop)
   dynpr_b200::DevBuf rank[2], contrib[2], flags_va, flags_np, flags_written,
       pend_low, pend_high, pend_flags, partials, perm_stage,
       tile_counts, red, stage_a, stage_b, stage_c, stage_d, stage_e, stage_f,
-      cub_tmp, tick, scratch64a, scratch64b, scratch32a, scratch32b, scratch8a, batch[4];
+      cub_tmp, tick, loopctl, scratch64a, scratch64b, scratch32a, scratch32b, scratch8a, batch[4];
 };
 
 namespace dynpr_b200 {

@@ -16,8 +16,13 @@
 // sweep kernels, and the only per-iteration host traffic is one 32-byte
 // readback (delta, processed, edges, pending-list sizes).
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
+#include <cstdlib>
 #include <string>
+#include <mutex>
+#include <vector>
 
 #include "layout.cuh"
 #include "comm.cuh"
@@ -94,7 +99,153 @@ struct SolveSpec {
   uint64_t nseeds = 0;
 };
 
-// convergeLoop (engine.cpp:61-95) on the device, in the layout's new-id
+bool host_loop_forced() {
+  const char* e = std::getenv("DYNPR_HOST_LOOP");
+  return e && e[0] && e[0] != '0';
+}
+
+// convergeLoop (engine.cpp:61-95) run entirely on the device: one CUDA graph
+// whose WHILE node repeats a two-iteration body (even sweep R0->R1, odd
+// sweep R1->R0, so the ping-pong buffers are baked in) --
+//   zero record -> sweep -> k_loop_end -> [push expand | pull expand]
+// -- where k_loop_end does the count / delta / convergence / max-iterations
+// bookkeeping of engine.cpp:79-91 on the device, picks the expansion
+// direction, and sets the loop condition.  Kernels of an iteration after
+// convergence return immediately (done flag), so the odd half of the last
+// body is free.  The host waits once, at the end.
+//
+// The kernels read their SweepArgs from constant-bank slots written per solve,
+// so an instantiated graph depends only on the sweep plan (kernel choice and
+// grids) and is cached on the context: a solve costs one ~1 KB upload and a
+// graph launch, not a capture + instantiate (~0.2 ms).
+struct LoopGraph {
+  SweepPlan plan;
+  int frontier;
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  uint64_t launches_per_body = 0;
+};
+struct LoopGraphCache {
+  std::vector<LoopGraph> items;
+  ~LoopGraphCache() {
+    for (auto& x : items) {
+      if (x.exec) cudaGraphExecDestroy(x.exec);
+      if (x.g) cudaGraphDestroy(x.g);
+    }
+  }
+};
+constexpr size_t kLoopCacheMax = 16;
+
+LoopGraph& loop_graph(dynpr_context* ctx, const SweepPlan& plan, int frontier, LoopCtl* dc, SweepRed* red) {
+  auto* cache = static_cast<LoopGraphCache*>(ctx->loop_graphs);
+  if (!cache) ctx->loop_graphs = cache = new LoopGraphCache();
+  for (auto& x : cache->items)
+    if (x.frontier == frontier && std::memcmp(&x.plan, &plan, sizeof plan) == 0) return x;
+  if (cache->items.size() >= kLoopCacheMax) {
+    LoopGraph& old = cache->items.front();
+    cudaGraphExecDestroy(old.exec);
+    cudaGraphDestroy(old.g);
+    cache->items.erase(cache->items.begin());
+  }
+  cudaStream_t st = ctx->stream;
+  LoopGraph lg;
+  lg.plan = plan;
+  lg.frontier = frontier;
+  const uint64_t launches0 = ctx->launches;
+  uint32_t* tick = sweep_tick(ctx);
+  DYNPR_CK(cudaGraphCreate(&lg.g, 0));
+  cudaGraphConditionalHandle cond;
+  DYNPR_CK(cudaGraphConditionalHandleCreate(&cond, lg.g, 1u, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams np{};
+  np.type = cudaGraphNodeTypeConditional;
+  np.conditional.handle = cond;
+  np.conditional.type = cudaGraphCondTypeWhile;
+  np.conditional.size = 1;
+  cudaGraphNode_t node;
+  DYNPR_CK(cudaGraphAddNode(&node, lg.g, nullptr, 0, &np));
+  cudaGraph_t body = np.conditional.phGraph_out[0];
+  DYNPR_CK(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  try {
+    for (int k = 0; k < 2; ++k) {
+      DYNPR_CK(cudaMemsetAsync(red, 0, sizeof(SweepRed), st));
+      launch_sweep_ind(ctx, plan, k, tick);
+      launch_loop_end(ctx, dc, red, cond, k == 1);
+      if (frontier) {
+        launch_expand_ind(ctx, k, &dc->pend_low, &dc->expand);
+        launch_pull_ind(ctx, plan, k);
+      }
+    }
+  } catch (...) {
+    cudaGraph_t junk = nullptr;
+    cudaStreamEndCapture(st, &junk);
+    cudaGetLastError();
+    throw;  // (the half-built graph is leaked: destroying it crashes in the driver)
+  }
+  cudaGraph_t captured = nullptr;
+  DYNPR_CK(cudaStreamEndCapture(st, &captured));
+  DYNPR_CK(cudaGraphInstantiate(&lg.exec, lg.g, 0));
+  lg.launches_per_body = ctx->launches - launches0;
+  ctx->launches = launches0;
+  cache->items.push_back(lg);
+  return cache->items.back();
+}
+
+void run_device_loop(dynpr_context* ctx, const SolveSpec& sp, const SweepArgs& a_in, double* const R[2],
+                     double* const CB[2], const Layout* L, SweepRed* red, dynpr_stats& res) {
+  const dynpr_config& c = *sp.cfg;
+  cudaStream_t st = ctx->stream;
+  LoopCtl h{};
+  h.max_iter = c.max_iterations;
+  h.check = c.convergence_check_disabled ? 0 : 1;
+  h.frontier = sp.flagged && !sp.traversal;
+  h.flagged = sp.flagged;
+  h.tol = c.iteration_tolerance;
+  h.m = sp.gT->m;
+  h.n = sp.gT->n;
+  LoopCtl* dc = ctx->loopctl.as<LoopCtl>(1);
+  // the constant-bank argument slots are per device: one device-loop solve
+  // at a time per GPU in this process
+  static std::mutex slot_lock[64];
+  std::lock_guard<std::mutex> guard(slot_lock[ctx->device & 63]);
+  prepare_sweep_launch(ctx);  // allocations / attributes must not happen inside a capture
+
+  SweepArgs half[2] = {a_in, a_in};
+  for (int k = 0; k < 2; ++k) {
+    half[k].rank_prev = R[k];
+    half[k].rank_cur = R[k ^ 1];
+    half[k].contrib_prev = CB[k];
+    half[k].contrib_cur = CB[k ^ 1];
+    half[k].npeers = 0;
+    half[k].done = &dc->done;
+    half[k].expand = &dc->expand;
+    half[k].offF = L->offF;
+    half[k].tgtF = L->tgtF;
+    half[k].tick_sm = sweep_tick(ctx);
+  }
+  const SweepPlan plan = plan_sweep(ctx, half[0], sp.flagged, sp.closed);
+  LoopGraph& lg = loop_graph(ctx, plan, h.frontier, dc, red);
+
+  // per-solve state: loop control + both halves' arguments, one upload
+  static_assert(sizeof(LoopCtl) <= 1024 && 2 * sizeof(SweepArgs) <= 2048, "pinned staging layout");
+  char* stage = static_cast<char*>(ctx->pinned);
+  std::memcpy(stage + 1024, &h, sizeof h);
+  std::memcpy(stage + 2048, half, sizeof half);
+  DYNPR_CK(cudaMemcpyAsync(dc, stage + 1024, sizeof h, cudaMemcpyHostToDevice, st));
+  upload_loop_args(ctx, reinterpret_cast<const SweepArgs*>(stage + 2048));
+  DYNPR_CK(cudaGraphLaunch(lg.exec, st));
+  DYNPR_CK(cudaMemcpyAsync(stage + 1024, dc, sizeof h, cudaMemcpyDeviceToHost, st));
+  sync(ctx);
+  std::memcpy(&h, stage + 1024, sizeof h);
+  // launches: the captured body (two iterations) ran once per two sweeps
+  ctx->launches += lg.launches_per_body * (uint64_t)((h.iterations + 1) / 2);
+  res.iterations = h.iterations;
+  res.converged = h.converged;
+  res.affected_vertex_iterations = h.affected;
+  res.processed_edges = h.edges;
+  res.final_delta = h.final_delta;
+}
+
+// convergeLoop (engine.cu:61-95) on the device, in the layout's new-id
 // space; inputs are permuted in and the result permuted back out.
 void solve(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynpr_stats* stats,
            dynpr_observer obs, void* user) {
@@ -117,6 +268,10 @@ void solve(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynpr_sta
   const bool fused = dist && (int)ctx->peer_cb[0].size() == comm->world && ctx->peer_capacity >= n;
   double* CB[2] = {fused ? ctx->peer_cb[0][comm->rank] : ctx->contrib[0].as<double>(n),
                    fused ? ctx->peer_cb[1][comm->rank] : ctx->contrib[1].as<double>(n)};
+  // Device-driven loop (CUDA graph WHILE node, no host round trip per
+  // iteration) unless the caller needs the host in the loop: an observer,
+  // a multi-GPU team (host-orchestrated collectives), per-sweep profiling.
+  const bool device_loop = !obs && !dist && !ctx->profiling && !host_loop_forced();
   double* partials = ctx->partials.as<double>(L->n_mseg + 1);
   SweepRed* red = ctx->red.as<SweepRed>(2);
   uint8_t* va = nullptr;
@@ -164,8 +319,12 @@ void solve(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynpr_sta
       DYNPR_CK(cudaMemsetAsync(red + 1, 0, sizeof(SweepRed), st));
       launch_init_affected(ctx, L->inv, sp.ds, sp.dd, sp.nd, sp.is, sp.ni, va, np);
       launch_collect_pending(ctx, L->outdeg, nullptr, n, np, c.low_degree_threshold, pl, ph, red + 1);
-      const SweepRed r0 = read_red(ctx, red + 1);
-      launch_expand(ctx, L->offF, L->tgtF, va, pl, r0.pend_low, ph, r0.pend_high);
+      if (device_loop) {  // list sizes stay on the device
+        launch_expand_dev(ctx, L->offF, L->tgtF, va, pl, ph, &red[1].pend_low, nullptr);
+      } else {
+        const SweepRed r0 = read_red(ctx, red + 1);
+        launch_expand(ctx, L->offF, L->tgtF, va, pl, r0.pend_low, ph, r0.pend_high);
+      }
     }
   }
 
@@ -215,7 +374,11 @@ void solve(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynpr_sta
 
   dynpr_stats res{};
   int cur = 0;  // R[cur] holds the latest iterate ("previous")
-  for (int iter = 0; iter < c.max_iterations; ++iter) {
+  if (device_loop) {
+    run_device_loop(ctx, sp, a, R, CB, L, red, res);
+    cur = res.iterations & 1;
+  }
+  for (int iter = 0; !device_loop && iter < c.max_iterations; ++iter) {
     DYNPR_CK(cudaMemsetAsync(red, 0, sizeof(SweepRed), st));
     if (obs && sp.flagged) {
       uint8_t* snap = obs_flags + n;  // owned entries are current on each rank
@@ -446,6 +609,8 @@ dynpr_status dynpr_context_destroy(dynpr_context* ctx) {
     if (ctx->ev_b) cudaEventDestroy(ctx->ev_b);
     if (ctx->ev_s0) cudaEventDestroy(ctx->ev_s0);
     if (ctx->ev_s1) cudaEventDestroy(ctx->ev_s1);
+    delete static_cast<LoopGraphCache*>(ctx->loop_graphs);
+    ctx->loop_graphs = nullptr;
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;

@@ -249,13 +249,22 @@ __device__ __forceinline__ bool segment_any_pending(const uint32_t* __restrict__
   return found;
 }
 
+// Device-loop arguments (the cached loop graph, engine.cu): the SweepArgs of
+// the solve's two half-iterations live in the constant bank, rewritten per
+// solve (stream-ordered), so one instantiated graph serves every snapshot of
+// the same launch shape and the kernels still read their arguments as
+// constant operands, exactly like by-value kernel parameters.  (Arguments
+// staged through shared memory were measured 8-15% slower on RMAT-22/24.)
+__constant__ SweepArgs c_loop_args[2];
+
 // Sweep kernels: persistent grids of 256-thread CTAs at full occupancy.
 constexpr int kSweepThreads = kThreads;
 constexpr int kSweepWarps = kSweepThreads / 32;
 
 // ---- single-segment vertices: warp per 32-vertex slice ------------------------
 template <bool FLAGGED, bool CLOSED>
-__global__ void __launch_bounds__(kSweepThreads, 5) k_sweep_single(SweepArgs a) {
+__device__ __forceinline__ void b_sweep_single(const SweepArgs& a) {
+  if (a.done && *a.done) return;
   const double* s_hot = nullptr;
   Acc acc;
   const unsigned lane = lane_id();
@@ -293,10 +302,19 @@ __global__ void __launch_bounds__(kSweepThreads, 5) k_sweep_single(SweepArgs a) 
   if (a.npeers) __threadfence_system();  // peer stores visible before the team barrier
   block_reduce_commit(acc, a.red);
 }
+template <bool FLAGGED, bool CLOSED>
+__global__ void __launch_bounds__(kSweepThreads, 5) k_sweep_single(SweepArgs a) {
+  b_sweep_single<FLAGGED, CLOSED>(a);
+}
+template <bool FLAGGED, bool CLOSED, int H>
+__global__ void __launch_bounds__(kSweepThreads, 5) k_sweep_single_c() {
+  b_sweep_single<FLAGGED, CLOSED>(c_loop_args[H]);
+}
 
 // ---- multi vertices: warp per slice of 32 chunks -> partials -------------------
 template <bool FLAGGED>
-__global__ void __launch_bounds__(kSweepThreads) k_sweep_mseg(SweepArgs a) {
+__device__ __forceinline__ void b_sweep_mseg(const SweepArgs& a) {
+  if (a.done && *a.done) return;
   const double* s_hot = nullptr;
   const unsigned lane = lane_id();
   const uint64_t nw = (uint64_t)gridDim.x * kSweepWarps;
@@ -317,10 +335,19 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_mseg(SweepArgs a) {
     if (len) a.partials[seg] = c;
   }
 }
+template <bool FLAGGED>
+__global__ void __launch_bounds__(kSweepThreads) k_sweep_mseg(SweepArgs a) {
+  b_sweep_mseg<FLAGGED>(a);
+}
+template <bool FLAGGED, int H>
+__global__ void __launch_bounds__(kSweepThreads) k_sweep_mseg_c() {
+  b_sweep_mseg<FLAGGED>(c_loop_args[H]);
+}
 
 // ---- multi vertices: ordered combine (rank.cpp:72) + epilogue --------------------
 template <bool FLAGGED, bool CLOSED>
-__global__ void __launch_bounds__(kThreads) k_sweep_mfinal(SweepArgs a) {
+__device__ __forceinline__ void b_sweep_mfinal(const SweepArgs& a) {
+  if (a.done && *a.done) return;
   Acc acc;
   const uint64_t stride = (uint64_t)gridDim.x * kThreads;
   const uint64_t vend = a.M < a.v_hi ? a.M : a.v_hi;
@@ -348,6 +375,14 @@ __global__ void __launch_bounds__(kThreads) k_sweep_mfinal(SweepArgs a) {
   }
   if (a.npeers) __threadfence_system();  // peer stores visible before the team barrier
   block_reduce_commit(acc, a.red);
+}
+template <bool FLAGGED, bool CLOSED>
+__global__ void __launch_bounds__(kThreads) k_sweep_mfinal(SweepArgs a) {
+  b_sweep_mfinal<FLAGGED, CLOSED>(a);
+}
+template <bool FLAGGED, bool CLOSED, int H>
+__global__ void __launch_bounds__(kThreads) k_sweep_mfinal_c() {
+  b_sweep_mfinal<FLAGGED, CLOSED>(c_loop_args[H]);
 }
 
 // ---- fused sweep: one kernel, dynamically scheduled ----------------------------
@@ -512,6 +547,7 @@ __device__ __forceinline__ void multi_slice(const SweepArgs& a, uint64_t s, unsi
 
 template <bool FLAGGED, bool CLOSED, int QH>
 __device__ __forceinline__ void fused_body(const SweepArgs& a) {
+  if (a.done && *a.done) return;
   Acc acc;
   const unsigned lane = lane_id();
   const uint64_t n_ms = a.ms_hi - a.ms_lo;
@@ -571,9 +607,14 @@ template <bool FLAGGED, bool CLOSED>
 __global__ void __launch_bounds__(kSweepThreads, 4) k_sweep_fused(SweepArgs a) {
   fused_body<FLAGGED, CLOSED, 4>(a);
 }
+template <bool FLAGGED, bool CLOSED, int H>
+__global__ void __launch_bounds__(kSweepThreads, 4) k_sweep_fused_c() {
+  fused_body<FLAGGED, CLOSED, 4>(c_loop_args[H]);
+}
 
 // ---- pull expansion over the SELL in-lists ------------------------------------------
-__global__ void __launch_bounds__(kThreads) k_pull_single(SweepArgs a) {
+__device__ __forceinline__ void b_pull_single(const SweepArgs& a) {
+  if (a.expand && *a.expand != kExpandPull) return;
   const unsigned lane = lane_id();
   const uint64_t nw = (uint64_t)gridDim.x * kWarps;
   for (uint64_t s = a.ss_lo + ((uint64_t)blockIdx.x * kThreads + threadIdx.x) / 32; s < a.ss_hi; s += nw) {
@@ -584,7 +625,13 @@ __global__ void __launch_bounds__(kThreads) k_pull_single(SweepArgs a) {
     if (segment_any_pending(a.sell_s, a.sbase[s], lane, len, a.np)) a.va[vv] = 1;
   }
 }
-__global__ void __launch_bounds__(kThreads) k_pull_mseg(SweepArgs a) {
+__global__ void __launch_bounds__(kThreads) k_pull_single(SweepArgs a) { b_pull_single(a); }
+template <int H>
+__global__ void __launch_bounds__(kThreads) k_pull_single_c() {
+  b_pull_single(c_loop_args[H]);
+}
+__device__ __forceinline__ void b_pull_mseg(const SweepArgs& a) {
+  if (a.expand && *a.expand != kExpandPull) return;
   const unsigned lane = lane_id();
   const uint64_t nw = (uint64_t)gridDim.x * kWarps;
   for (uint64_t s = a.ms_lo + ((uint64_t)blockIdx.x * kThreads + threadIdx.x) / 32; s < a.ms_hi; s += nw) {
@@ -597,6 +644,11 @@ __global__ void __launch_bounds__(kThreads) k_pull_mseg(SweepArgs a) {
     if (!__any_sync(kFull, len != 0)) continue;
     if (segment_any_pending(a.sell_m, a.mbase[s], lane, len, a.np)) a.va[v] = 1;
   }
+}
+__global__ void __launch_bounds__(kThreads) k_pull_mseg(SweepArgs a) { b_pull_mseg(a); }
+template <int H>
+__global__ void __launch_bounds__(kThreads) k_pull_mseg_c() {
+  b_pull_mseg(c_loop_args[H]);
 }
 
 // ---- stable degree partition (partition.cpp:7-61) ------------------------------------
@@ -740,7 +792,9 @@ __global__ void k_collect_pending(const uint32_t* outdeg, const uint64_t* off, u
 // are idempotent; the read-before-write keeps dense frontiers
 // from turning into L2 write traffic.
 __global__ void k_expand_low(const uint64_t* off, const uint32_t* tgt, const uint32_t* list, uint32_t cnt,
-                             uint8_t* va) {
+                             uint8_t* va, const unsigned* dcnt, const int* gate) {
+  if (gate && *gate != kExpandPush) return;
+  if (dcnt) cnt = dcnt[0];
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cnt;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t u = list[i];
@@ -752,7 +806,9 @@ __global__ void k_expand_low(const uint64_t* off, const uint32_t* tgt, const uin
   }
 }
 __global__ void k_expand_high(const uint64_t* off, const uint32_t* tgt, const uint2* items, uint32_t cnt,
-                              uint8_t* va) {
+                              uint8_t* va, const unsigned* dcnt, const int* gate) {
+  if (gate && *gate != kExpandPush) return;
+  if (dcnt) cnt = dcnt[1];
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / 32;
   const uint64_t nw = (uint64_t)gridDim.x * blockDim.x / 32;
   const unsigned lane = lane_id();
@@ -773,6 +829,81 @@ __global__ void k_expand_high(const uint64_t* off, const uint32_t* tgt, const ui
         if (!f[q]) va[w[q]] = 1;
     }
   }
+}
+template <int H>
+__global__ void k_expand_low_c(const unsigned* counts, const int* gate) {
+  const SweepArgs* ap = &c_loop_args[H];
+  if (gate && *gate != kExpandPush) return;
+  const unsigned cnt = counts[0];
+  const uint64_t* off = ap->offF;
+  const uint32_t* tgt = ap->tgtF;
+  const uint32_t* list = ap->pend_low;
+  uint8_t* va = ap->va;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cnt;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t u = list[i];
+    const uint64_t b = off[u], e = off[u + 1];
+    for (uint64_t k = b; k < e; ++k) {
+      const uint32_t w = tgt[k];
+      if (!va[w]) va[w] = 1;
+    }
+  }
+}
+template <int H>
+__global__ void k_expand_high_c(const unsigned* counts, const int* gate) {
+  const SweepArgs* ap = &c_loop_args[H];
+  if (gate && *gate != kExpandPush) return;
+  const unsigned cnt = counts[1];
+  const uint64_t* off = ap->offF;
+  const uint32_t* tgt = ap->tgtF;
+  const uint2* items = ap->pend_high;
+  uint8_t* va = ap->va;
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / 32;
+  const uint64_t nw = (uint64_t)gridDim.x * blockDim.x / 32;
+  const unsigned lane = lane_id();
+  for (uint64_t i = warp; i < cnt; i += nw) {
+    const uint2 it = items[i];
+    const uint64_t b = off[it.x] + (uint64_t)kExpandChunk * it.y;
+    const uint64_t e0 = off[it.x + 1];
+    const uint64_t e = b + kExpandChunk < e0 ? b + kExpandChunk : e0;
+    for (uint64_t k = b + lane; k < e; k += 32 * 4) {
+      uint32_t w[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) w[q] = k + 32 * q < e ? tgt[k + 32 * q] : 0xffffffffu;
+      uint8_t f[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) f[q] = w[q] != 0xffffffffu ? va[w[q]] : 1;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (!f[q]) va[w[q]] = 1;
+    }
+  }
+}
+
+// ---- device-driven loop bookkeeping (engine.cpp:71-92) --------------------------------
+__global__ void k_loop_end(LoopCtl* c, const SweepRed* red, cudaGraphConditionalHandle h, int set_cond) {
+  if (!c->done) {
+    const SweepRed r = *red;
+    const double delta = __longlong_as_double((long long)r.delta_bits);
+    c->iterations += 1;
+    c->affected += c->flagged ? r.processed : c->n;
+    c->edges += r.edges;
+    c->final_delta = delta;
+    c->expand = kExpandNone;
+    if (c->check && delta <= c->tol) {
+      c->converged = 1;
+      c->done = 1;
+    } else if (c->iterations >= c->max_iter) {
+      c->done = 1;  // the reference's trailing expansion cannot change the ranks
+    } else if (c->frontier) {
+      // direction-optimising expandAffected (same rule as the host loop)
+      const unsigned long long pull_bound = c->m > r.edges ? c->m - r.edges : 0ull;
+      c->expand = r.pend_edges > pull_bound ? kExpandPull : kExpandPush;
+      c->pend_low = r.pend_low;
+      c->pend_high = r.pend_high;
+    }
+  }
+  if (set_cond) cudaGraphSetConditional(h, c->done ? 0u : 1u);
 }
 
 // ---- markReachable (frontier.cpp:86-121): level-synchronous BFS -------------------
@@ -1071,6 +1202,131 @@ void launch_sweep(dynpr_context* ctx, const SweepArgs& a, bool flagged, bool clo
   count_launch(ctx, launched);
 }
 
+
+// ---- indirect launches for the cached device-loop graph ------------------------------
+// Same kernel choice as launch_sweep; every grid is fixed here (before any
+// capture), so a plan plus the device argument buffer fully describe the
+// launches and equal plans can share one instantiated graph.
+template <class K>
+static unsigned pgrid(dynpr_context* ctx, K k, uint64_t work_blocks) {
+  return persistent_grid(ctx, k, work_blocks);
+}
+
+SweepPlan plan_sweep(dynpr_context* ctx, const SweepArgs& a, bool flagged, bool closed) {
+  SweepPlan p{};
+  p.flagged = flagged;
+  p.closed = closed;
+  const uint64_t mv = (a.M < a.v_hi ? a.M : a.v_hi) > a.v_lo ? (a.M < a.v_hi ? a.M : a.v_hi) - a.v_lo : 0;
+  const uint64_t n_ms = a.ms_hi - a.ms_lo, n_ss = a.ss_hi - a.ss_lo;
+  const char* mode = std::getenv("DYNPR_SWEEP");
+  const std::string m = mode ? mode : "";
+  const uint64_t resident_warps = (uint64_t)ctx->num_sms * 32;
+  const bool big = (n_ms + n_ss) > kSplitSlicesPerWarp * resident_warps;
+  p.split = m == "split" || (m != "fused" && big);
+  const uint64_t wms = (n_ms + kSweepWarps - 1) / kSweepWarps, wss = (n_ss + kSweepWarps - 1) / kSweepWarps;
+#define DYNPR_PLAN(F, C)                                                                 \
+  do {                                                                                   \
+    if (!p.split) {                                                                      \
+      if (n_ms + n_ss) p.g_fused = pgrid(ctx, k_sweep_fused_c<F, C, 0>, (n_ms + n_ss + kSweepWarps - 1) / kSweepWarps); \
+    } else {                                                                             \
+      if (n_ms) p.g_mseg = pgrid(ctx, k_sweep_mseg_c<F, 0>, wms);                        \
+      if (n_ss) p.g_single = pgrid(ctx, k_sweep_single_c<F, C, 0>, wss);                 \
+      if (mv) p.g_mfinal = grid_for(mv, kThreads);                                       \
+    }                                                                                    \
+  } while (0)
+  if (flagged) {
+    if (closed) DYNPR_PLAN(true, true); else DYNPR_PLAN(true, false);
+  } else {
+    if (closed) DYNPR_PLAN(false, true); else DYNPR_PLAN(false, false);
+  }
+#undef DYNPR_PLAN
+  if (n_ms) p.g_pull_m = pgrid(ctx, k_pull_mseg_c<0>, (n_ms + kWarps - 1) / kWarps);
+  if (n_ss) p.g_pull_s = pgrid(ctx, k_pull_single_c<0>, (n_ss + kWarps - 1) / kWarps);
+  return p;
+}
+
+template <int H>
+static void launch_sweep_c(dynpr_context* ctx, const SweepPlan& p, uint32_t* tick) {
+  cudaStream_t st = ctx->stream;
+  unsigned launched = 0;
+#define DYNPR_IND(F, C)                                                                          \
+  do {                                                                                           \
+    if (!p.split) {                                                                              \
+      if (p.g_fused) {                                                                           \
+        DYNPR_CK(cudaMemsetAsync(tick, 0, kMaxBlocks * sizeof(uint32_t), st));                   \
+        k_sweep_fused_c<F, C, H><<<p.g_fused, kSweepThreads, 0, st>>>();                         \
+        ++launched;                                                                              \
+      }                                                                                          \
+    } else {                                                                                     \
+      if (p.g_mseg) { k_sweep_mseg_c<F, H><<<p.g_mseg, kSweepThreads, 0, st>>>(); ++launched; }   \
+      if (p.g_single) { k_sweep_single_c<F, C, H><<<p.g_single, kSweepThreads, 0, st>>>(); ++launched; } \
+      if (p.g_mfinal) { k_sweep_mfinal_c<F, C, H><<<p.g_mfinal, kThreads, 0, st>>>(); ++launched; } \
+    }                                                                                            \
+  } while (0)
+  if (p.flagged) {
+    if (p.closed) DYNPR_IND(true, true); else DYNPR_IND(true, false);
+  } else {
+    if (p.closed) DYNPR_IND(false, true); else DYNPR_IND(false, false);
+  }
+#undef DYNPR_IND
+  check_launch();
+  count_launch(ctx, launched);
+}
+void launch_sweep_ind(dynpr_context* ctx, const SweepPlan& p, int half, uint32_t* tick) {
+  if (half) launch_sweep_c<1>(ctx, p, tick); else launch_sweep_c<0>(ctx, p, tick);
+}
+
+void launch_pull_ind(dynpr_context* ctx, const SweepPlan& p, int half) {
+  cudaStream_t st = ctx->stream;
+  unsigned launched = 0;
+  if (p.g_pull_m) {
+    if (half) k_pull_mseg_c<1><<<p.g_pull_m, kThreads, 0, st>>>(); else k_pull_mseg_c<0><<<p.g_pull_m, kThreads, 0, st>>>();
+    ++launched;
+  }
+  if (p.g_pull_s) {
+    if (half) k_pull_single_c<1><<<p.g_pull_s, kThreads, 0, st>>>(); else k_pull_single_c<0><<<p.g_pull_s, kThreads, 0, st>>>();
+    ++launched;
+  }
+  check_launch();
+  count_launch(ctx, launched);
+}
+
+void launch_expand_ind(dynpr_context* ctx, int half, const unsigned* counts, const int* gate) {
+  const unsigned g = (unsigned)ctx->num_sms * 16;
+  if (half) {
+    k_expand_low_c<1><<<g, kThreads, 0, ctx->stream>>>(counts, gate);
+    k_expand_high_c<1><<<g, kThreads, 0, ctx->stream>>>(counts, gate);
+  } else {
+    k_expand_low_c<0><<<g, kThreads, 0, ctx->stream>>>(counts, gate);
+    k_expand_high_c<0><<<g, kThreads, 0, ctx->stream>>>(counts, gate);
+  }
+  check_launch();
+  count_launch(ctx, 2);
+}
+
+void upload_loop_args(dynpr_context* ctx, const SweepArgs* host_pinned_half2) {
+  DYNPR_CK(cudaMemcpyToSymbolAsync(c_loop_args, host_pinned_half2, 2 * sizeof(SweepArgs), 0, cudaMemcpyHostToDevice,
+                                   ctx->stream));
+}
+
+uint32_t* sweep_tick(dynpr_context* ctx) { return ctx->tick.as<uint32_t>(kMaxBlocks); }
+
+void prepare_sweep_launch(dynpr_context* ctx) {
+  ctx->tick.as<uint32_t>(kMaxBlocks);
+  persistent_grid(ctx, k_sweep_fused<false, false>, 1);
+  persistent_grid(ctx, k_sweep_fused<true, false>, 1);
+  persistent_grid(ctx, k_sweep_fused<false, true>, 1);
+  persistent_grid(ctx, k_sweep_fused<true, true>, 1);
+  persistent_grid(ctx, k_sweep_mseg<false>, 1);
+  persistent_grid(ctx, k_sweep_mseg<true>, 1);
+  persistent_grid(ctx, k_sweep_single<false, false>, 1);
+  persistent_grid(ctx, k_sweep_single<true, false>, 1);
+  persistent_grid(ctx, k_sweep_single<false, true>, 1);
+  persistent_grid(ctx, k_sweep_single<true, true>, 1);
+  persistent_grid(ctx, k_pull_mseg, 1);
+  persistent_grid(ctx, k_pull_single, 1);
+}
+
 void launch_pull_expand(dynpr_context* ctx, const SweepArgs& a) {
   cudaStream_t st = ctx->stream;
   unsigned launched = 0;
@@ -1118,16 +1374,34 @@ void launch_expand(dynpr_context* ctx, const uint64_t* off, const uint32_t* tgt,
                    const uint32_t* pend_low, uint32_t n_low, const uint2* pend_high, uint32_t n_high) {
   if (n_low) {
     k_expand_low<<<grid_for(n_low, kThreads, ctx->num_sms * 16), kThreads, 0, ctx->stream>>>(off, tgt, pend_low,
-                                                                                            n_low, va);
+                                                                                            n_low, va, nullptr,
+                                                                                            nullptr);
     check_launch();
     count_launch(ctx);
   }
   if (n_high) {
     k_expand_high<<<grid_for((uint64_t)n_high * 32, kThreads, ctx->num_sms * 16), kThreads, 0, ctx->stream>>>(
-        off, tgt, pend_high, n_high, va);
+        off, tgt, pend_high, n_high, va, nullptr, nullptr);
     check_launch();
     count_launch(ctx);
   }
+}
+
+void launch_loop_end(dynpr_context* ctx, LoopCtl* c, const SweepRed* red, cudaGraphConditionalHandle h,
+                     int set_cond) {
+  k_loop_end<<<1, 1, 0, ctx->stream>>>(c, red, h, set_cond);
+  check_launch();
+  count_launch(ctx);
+}
+
+void launch_expand_dev(dynpr_context* ctx, const uint64_t* off, const uint32_t* tgt, uint8_t* va,
+                       const uint32_t* pend_low, const uint2* pend_high, const unsigned* counts, const int* gate) {
+  const unsigned g = (unsigned)ctx->num_sms * 16;
+  k_expand_low<<<g, kThreads, 0, ctx->stream>>>(off, tgt, pend_low, 0, va, counts, gate);
+  check_launch();
+  k_expand_high<<<g, kThreads, 0, ctx->stream>>>(off, tgt, pend_high, 0, va, counts, gate);
+  check_launch();
+  count_launch(ctx, 2);
 }
 
 uint64_t mark_reachable(dynpr_context* ctx, const uint64_t* off, const uint32_t* tgt, uint32_t n, const uint32_t* inv,

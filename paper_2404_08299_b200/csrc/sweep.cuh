@@ -64,7 +64,35 @@ struct SweepArgs {
   // the other ranks' copies of contrib_cur, written alongside the local one
   int npeers;
   double* peer_cur[kMaxPeers];
+  // device-driven loop (engine.cu run_device_loop): every kernel of an
+  // iteration returns at once when *done is set; the pull kernels run only
+  // when *expand == kExpandPull.  Null in the host-driven loop.
+  const int* done;
+  const int* expand;
+  // relabelled forward CSR for the device loop's push expansion
+  const uint64_t* offF;
+  const uint32_t* tgtF;
 };
+
+// Device-driven convergence loop state (convergeLoop's bookkeeping,
+// engine.cpp:71-92, kept on the device so no iteration waits on the host).
+enum { kExpandNone = 0, kExpandPush = 1, kExpandPull = 2 };
+struct LoopCtl {
+  int done, converged, iterations, max_iter;
+  int check, frontier, flagged, expand;
+  unsigned pend_low, pend_high;  // push-expansion list sizes of the last sweep
+  double tol, final_delta;
+  unsigned long long affected, edges, m, n;
+};
+// One iteration's bookkeeping (single thread): count, delta, convergence,
+// max-iterations, expansion direction; `set_cond` also sets the WHILE
+// node's condition to !done.
+void launch_loop_end(dynpr_context* ctx, LoopCtl* c, const SweepRed* red, cudaGraphConditionalHandle h,
+                     int set_cond);
+// Push expansion with device-resident list sizes (counts[0] low, counts[1]
+// high), optionally gated on *gate == kExpandPush; fixed grids.
+void launch_expand_dev(dynpr_context* ctx, const uint64_t* off, const uint32_t* tgt, uint8_t* va,
+                       const uint32_t* pend_low, const uint2* pend_high, const unsigned* counts, const int* gate);
 
 // Edge-balanced partition of the layout's vertex space over `world` ranks
 // (SURVEY 8e): contiguous new-id ranges, aligned to 32-vertex slices in the
@@ -76,6 +104,24 @@ SweepArgs layout_args(const Layout* L, double* partials);
 // One synchronous sweep: single-segment slices, multi-segment slices,
 // ordered combine of the multi-vertex partials.
 void launch_sweep(dynpr_context* ctx, const SweepArgs& a, bool flagged, bool closed);
+// Launch plan of one sweep for the cached device-loop graph: kernel choice
+// (fused / split) and every grid.  Plans compare bytewise.
+struct SweepPlan {
+  int flagged, closed, split;
+  unsigned g_fused, g_mseg, g_single, g_mfinal, g_pull_m, g_pull_s;
+};
+SweepPlan plan_sweep(dynpr_context* ctx, const SweepArgs& a, bool flagged, bool closed);
+// The sweep / pull / push-expansion launches of a plan for half-iteration
+// `half` (0: R0->R1, 1: R1->R0), reading their SweepArgs from the constant
+// bank (upload_loop_args, stream-ordered), for capture into the loop graph.
+void launch_sweep_ind(dynpr_context* ctx, const SweepPlan& p, int half, uint32_t* tick);
+void launch_pull_ind(dynpr_context* ctx, const SweepPlan& p, int half);
+void launch_expand_ind(dynpr_context* ctx, int half, const unsigned* counts, const int* gate);
+void upload_loop_args(dynpr_context* ctx, const SweepArgs* host_pinned_half2);
+uint32_t* sweep_tick(dynpr_context* ctx);
+// Allocates the sweep launch workspace and resolves every kernel's persistent
+// grid, so launch_sweep / launch_pull_expand can be stream-captured.
+void prepare_sweep_launch(dynpr_context* ctx);
 
 // rank / contribution initialisation in new-id order: r = init (already in
 // new order) or `uniform`; c = r / outdeg.
