@@ -1,0 +1,89 @@
+"""The device-driven convergence loop (cached CUDA graph with a WHILE node,
+engine.cu run_device_loop) against the host-driven loop and the reference:
+same iterations, affected-vertex counts, converged flag, final delta and
+ranks, bit for bit, for every engine, both sweep kernels (fused latency
+mode / split throughput mode), odd and even iteration counts and the
+max-iterations / check-disabled exits."""
+import numpy as np
+import pytest
+
+from helpers import rand_pair, to_dev
+
+pytestmark = pytest.mark.gpu
+
+
+def _same(a, b):
+    assert a.iterations == b.iterations
+    assert a.converged == b.converged
+    assert a.affected_vertex_iterations == b.affected_vertex_iterations
+    assert a.final_delta == b.final_delta
+    assert np.array_equal(a.ranks, b.ranks)
+
+
+def _both(monkeypatch, fn):
+    monkeypatch.setenv("DYNPR_HOST_LOOP", "1")
+    host = fn()
+    monkeypatch.setenv("DYNPR_HOST_LOOP", "0")
+    dev = fn()
+    dev2 = fn()  # cached graph reused
+    _same(dev, host)
+    _same(dev2, host)
+    return dev
+
+
+@pytest.mark.parametrize("sweep", ["fused", "split"])
+@pytest.mark.parametrize("case", [(5, 3000, 40000, 60, 0.8, 3), (17, 20000, 300000, 2000, 0.8, 4),
+                                  (23, 800, 9000, 5, 1.0, 8)])
+def test_device_loop_all_engines(dp, oracle_lib, monkeypatch, sweep, case):
+    monkeypatch.setenv("DYNPR_SWEEP", sweep)
+    O = oracle_lib
+    seed, n, pairs, size, insf, bseed = case
+    og, ogt = rand_pair(O, seed, n, pairs)
+    base = O.static(ogt, og)
+    dels, ins = O.generate_random_batch(og, size, insf, bseed)
+    og2, _, _ = O.apply_batch(og, dels, ins)
+    ogt2 = O.transpose(og2)
+    g, gt = to_dev(dp, og2), to_dev(dp, ogt2)
+    _same(_both(monkeypatch, lambda: dp.static_pagerank(gt, g)), O.static(ogt2, og2))
+    _same(_both(monkeypatch, lambda: dp.naive_dynamic(gt, g, base.ranks)), O.naive_dynamic(ogt2, og2, base.ranks))
+    for pruning in (False, True):
+        _same(_both(monkeypatch, lambda: dp.dynamic_frontier(g, gt, dels, ins, base.ranks, pruning=pruning)),
+              O.dynamic_frontier(og2, ogt2, dels, ins, base.ranks, pruning=pruning))
+    _same(_both(monkeypatch, lambda: dp.dynamic_traversal(g, gt, dels, ins, base.ranks)),
+          O.dynamic_traversal(og2, ogt2, dels, ins, base.ranks))
+
+
+@pytest.mark.parametrize("max_it", [1, 2, 3, 7, 8])
+@pytest.mark.parametrize("check_disabled", [False, True])
+def test_device_loop_iteration_limits(dp, oracle_lib, monkeypatch, max_it, check_disabled):
+    O = oracle_lib
+    og, ogt = rand_pair(O, 41, 2000, 20000)
+    g, gt = to_dev(dp, og), to_dev(dp, ogt)
+    cfg = dp.EngineConfig(max_iterations=max_it, convergence_check_disabled=check_disabled)
+    import oracle
+    ocfg = oracle.default_config(max_iterations=max_it, convergence_check_disabled=int(check_disabled))
+    r = _both(monkeypatch, lambda: dp.static_pagerank(gt, g, cfg))
+    assert r.iterations == max_it and not r.converged
+    _same(r, O.static(ogt, og, ocfg))
+    dels, ins = O.generate_random_batch(og, 40, 0.8, 6)
+    og2, _, _ = O.apply_batch(og, dels, ins)
+    ogt2 = O.transpose(og2)
+    g2, gt2 = to_dev(dp, og2), to_dev(dp, ogt2)
+    prev = O.static(ogt, og).ranks
+    d = _both(monkeypatch, lambda: dp.dynamic_frontier(g2, gt2, dels, ins, prev, cfg, True))
+    _same(d, O.dynamic_frontier(og2, ogt2, dels, ins, prev, ocfg, pruning=True))
+
+
+def test_device_loop_converges_on_odd_and_even_iterations(dp, oracle_lib, monkeypatch):
+    """Tolerances chosen so the solve stops in the even and in the odd half
+    of the two-iteration graph body."""
+    O = oracle_lib
+    og, ogt = rand_pair(O, 43, 1500, 15000)
+    g, gt = to_dev(dp, og), to_dev(dp, ogt)
+    seen = set()
+    import oracle
+    for tol in (1e-4, 3e-5, 1e-5, 3e-6, 1e-6, 1e-8):
+        r = _both(monkeypatch, lambda: dp.static_pagerank(gt, g, dp.EngineConfig(iteration_tolerance=tol)))
+        _same(r, O.static(ogt, og, oracle.default_config(iteration_tolerance=tol)))
+        seen.add(r.iterations % 2)
+    assert seen == {0, 1}
