@@ -5,7 +5,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import paper_2404_08299_b200 as dp
 frac = float(sys.argv[1]) if len(sys.argv) > 1 else 1e-7
-g = dp.rmat_graph(20); gt = dp.transpose(g)
+scale = int(os.environ.get("SCALE", "20"))
+g = dp.rmat_graph(scale); gt = dp.transpose(g)
 base = dp.static_pagerank(gt, g)
 b = dp.generate_random_batch(g, dp.batch_size_from_fraction(frac, g.edge_count), 0.8, 5)
 g2, gt2 = dp.apply_batch_pair(g, gt, b)
