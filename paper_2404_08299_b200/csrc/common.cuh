@@ -3,6 +3,9 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 
 #include <cstdint>
 #include <cstring>
@@ -128,7 +131,7 @@ struct dynpr_context {
   dynpr_b200::DevBuf rank[2], contrib[2], flags_va, flags_np, flags_written,
       pend_low, pend_high, pend_flags, partials, perm_stage,
       tile_counts, red, stage_a, stage_b, stage_c, stage_d, stage_e, stage_f,
-      cub_tmp, tick, loopctl, scratch64a, scratch64b, scratch32a, scratch32b, scratch8a, batch[4];
+      cub_tmp, tick, loopctl, layout_tmp, scratch64a, scratch64b, scratch32a, scratch32b, scratch8a, batch[4];
 };
 
 namespace dynpr_b200 {
@@ -212,7 +215,21 @@ inline void bind_device(dynpr_context* ctx) { DYNPR_CK(cudaSetDevice(ctx->device
 // paying cudaMalloc/cudaFree.
 inline void* pool_alloc(dynpr_context* ctx, size_t bytes) {
   void* p = nullptr;
+  // Large arrays are over-allocated by ~3% and rounded to 2 MiB: the next
+  // snapshot of a batch stream is a few edges larger, and without slack its
+  // arrays could not reuse the blocks the previous snapshot returned to the
+  // pool (new physical memory is mapped on such a miss: tens of ms per GB).
+  if (bytes >= (size_t(1) << 21)) {
+    const size_t slack = bytes + bytes / 32;
+    bytes = (slack + (size_t(1) << 21) - 1) & ~((size_t(1) << 21) - 1);
+  }
+  static const bool dbg = std::getenv("DYNPR_ALLOC_DEBUG") != nullptr;
+  const auto t0 = dbg ? std::chrono::steady_clock::now() : std::chrono::steady_clock::time_point{};
   cudaError_t e = cudaMallocAsync(&p, bytes ? bytes : 16, ctx->stream);
+  if (dbg) {
+    const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+    if (us > 1000.0) std::fprintf(stderr, "pool_alloc %zu bytes: %.1f us\n", bytes, us);
+  }
   if (e != cudaSuccess) {
     cudaGetLastError();
     throw Error(DYNPR_OUT_OF_MEMORY, "device allocation of " + std::to_string(bytes) + " bytes failed");
@@ -246,6 +263,16 @@ __device__ __forceinline__ I lower_bound_dev(const T* a, I lo, I hi, T key) {
   while (lo < hi) {
     I mid = lo + (hi - lo) / 2;
     if (a[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// First index in [0, len) with a[i] > x (a ascending).
+__device__ __forceinline__ uint64_t upper_bound_u32(const uint32_t* a, uint64_t len, uint32_t x) {
+  uint64_t lo = 0, hi = len;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (a[mid] <= x) lo = mid + 1; else hi = mid;
   }
   return lo;
 }

@@ -275,6 +275,23 @@ __global__ void k_list_touched(const uint8_t* touched, uint32_t n,
 // Untouched slices keep their content and only shift: a warp per 32-vertex
 // tile copies the whole contiguous range when no vertex of the tile is
 // touched (the common case), else slice by slice skipping touched ones.
+// Copy of one CSR row range [b, e) to d.. with 8 loads in flight per lane
+// (the source and destination offsets differ by an arbitrary shift, so the
+// copy stays 4-byte granular; the depth gives the memory-level parallelism).
+__device__ __forceinline__ void warp_copy_range(const uint32_t* __restrict__ tgt, uint32_t* __restrict__ ntgt,
+                                                uint64_t b, uint64_t e, uint64_t d, unsigned lane) {
+  for (uint64_t i = b + lane; i < e; i += 32 * 8) {
+    uint32_t x[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) x[q] = i + 32 * q < e ? __ldcs(tgt + i + 32 * q) : 0u;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (i + 32 * q < e) __stcs(ntgt + d + (i + 32 * q - b), x[q]);
+  }
+}
+
+// Rows without batch entries keep their slices: warp per 32-vertex tile,
+// one contiguous copy when the whole tile is untouched.
 __global__ void k_copy_untouched(const uint64_t* off, const uint32_t* tgt,
                                  const uint64_t* noff, uint32_t* ntgt,
                                  uint32_t n, const uint8_t* touched) {
@@ -289,22 +306,38 @@ __global__ void k_copy_untouched(const uint64_t* off, const uint32_t* tgt,
     const bool mine = v < v1 && touched[v];
     const unsigned any = __ballot_sync(0xffffffffu, mine);
     if (!any) {
-      const uint64_t b = off[v0], e = off[v1], d = noff[v0];
-      for (uint64_t i = b + lane; i < e; i += 32) ntgt[d + (i - b)] = tgt[i];
+      warp_copy_range(tgt, ntgt, off[v0], off[v1], noff[v0], lane);
     } else {
       for (uint64_t w = v0; w < v1; ++w) {
         if ((any >> (w - v0)) & 1u) continue;
-        const uint64_t b = off[w], e = off[w + 1], d = noff[w];
-        for (uint64_t i = b + lane; i < e; i += 32) ntgt[d + (i - b)] = tgt[i];
+        warp_copy_range(tgt, ntgt, off[w], off[w + 1], noff[w], lane);
       }
     }
   }
 }
 
-// Warp per touched vertex u: every output element's position is computed
-// independently (sorted merge of (S \ Dp) U N U {u if loop needed}, where Dp
-// are the present deletions and N the fresh insertions of u).
-__global__ void k_merge_touched(const uint32_t* list, const unsigned* count,
+// Merge work items of the touched rows: a row of old degree d is split into
+// max(1, ceil(d / kMergeChunk)) items so a touched hub (RMAT-24: ~4e5 edges)
+// is spread over many warps instead of serialising one.
+constexpr uint64_t kMergeChunk = 2048;
+__global__ void k_merge_items(const uint8_t* touched, const uint64_t* off, uint32_t n, uint32_t* items) {
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v <= n;
+       v += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t c = 0;
+    if (v < n && touched[v]) {
+      const uint64_t d = off[v + 1] - off[v];
+      c = d > kMergeChunk ? (uint32_t)((d + kMergeChunk - 1) / kMergeChunk) : 1u;
+    }
+    items[v] = c;
+  }
+}
+
+// Rows with batch entries: every surviving old target and every fresh
+// insertion is written at its final position (old index - deletions before
+// it + insertions before it + the re-ensured self-loop when it precedes),
+// so the items of one row are independent.  Item t -> row through the
+// exclusive scan `istart` (n + 1 entries, istart[n] = total items).
+__global__ void k_merge_touched(const uint32_t* istart, uint32_t n,
                                 const uint64_t* off, const uint32_t* tgt,
                                 const uint64_t* noff, uint32_t* ntgt,
                                 const uint64_t* dp, uint64_t ndp,
@@ -313,24 +346,28 @@ __global__ void k_merge_touched(const uint32_t* list, const unsigned* count,
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / 32;
   const unsigned lane = threadIdx.x & 31;
   const uint64_t nwarps = (uint64_t)gridDim.x * blockDim.x / 32;
-  const unsigned total = *count;
-  for (uint64_t w = warp; w < total; w += nwarps) {
-    const uint32_t u = list[w];
+  const uint32_t total = istart[n];
+  for (uint64_t t = warp; t < total; t += nwarps) {
+    // row u: the last u with istart[u] <= t (rows with no items share a start)
+    const uint32_t u = (uint32_t)(upper_bound_u32(istart, (uint64_t)n + 1, (uint32_t)t) - 1);
+    const uint64_t c = t - istart[u];
     const uint64_t so = off[u], se = off[u + 1], base = noff[u];
+    const uint64_t cb = so + c * kMergeChunk, ce = cb + kMergeChunk < se ? cb + kMergeChunk : se;
     const uint64_t klo = (uint64_t)u << sb, khi = ((uint64_t)u + 1) << sb;
     const uint64_t dlo = lower_bound_dev<uint64_t, uint64_t>(dp, 0, ndp, klo);
     const uint64_t dhi = lower_bound_dev<uint64_t, uint64_t>(dp, dlo, ndp, khi);
     const uint64_t nlo = lower_bound_dev<uint64_t, uint64_t>(nw, 0, nnw, klo);
     const uint64_t nhi = lower_bound_dev<uint64_t, uint64_t>(nw, nlo, nnw, khi);
     const bool nl = need[u];
-    for (uint64_t k = lane; k < se - so; k += 32) {
-      const uint32_t t = tgt[so + k];
-      const uint64_t key = klo | t;
+    for (uint64_t k = cb - so + lane; k < ce - so; k += 32) {
+      const uint32_t x = tgt[so + k];
+      const uint64_t key = klo | x;
       const uint64_t q = lower_bound_dev<uint64_t, uint64_t>(dp, dlo, dhi, key);
       if (q < dhi && dp[q] == key) continue;
       const uint64_t r = lower_bound_dev<uint64_t, uint64_t>(nw, nlo, nhi, key) - nlo;
-      ntgt[base + k - (q - dlo) + r + ((nl && u < t) ? 1 : 0)] = t;
+      ntgt[base + k - (q - dlo) + r + ((nl && u < x) ? 1 : 0)] = x;
     }
+    if (c != 0) continue;
     for (uint64_t k = lane; k < nhi - nlo; k += 32) {
       const uint64_t key = nw[nlo + k];
       const uint32_t x = (uint32_t)(key & mask);
@@ -628,22 +665,22 @@ void graph_apply_batch_impl(dynpr_context* ctx, const dynpr_graph* g,
     });
     nnw = read_u64(ctx, nsel + 1);
   }
-  // touched list + copies
-  uint32_t* tlist = ctx->scratch32b.as<uint32_t>((uint64_t)n + 1);
-  unsigned* tcount = reinterpret_cast<unsigned*>(counters + 2);
+  // copies of the untouched rows + chunked merge of the touched ones
   if (n) {
-    k_list_touched<<<grid_for(n, 256, 1 << 16), 256, 0, st>>>(touched, n, tlist, tcount);
+    uint32_t* istart = ctx->scratch32b.as<uint32_t>((uint64_t)n + 1);
+    k_merge_items<<<grid_for((uint64_t)n + 1, 256, 1 << 16), 256, 0, st>>>(touched, g->off, n, istart);
     check_launch();
+    cub_call(ctx, [&](void* t, size_t& b) {
+      return cub::DeviceScan::ExclusiveSum(t, b, istart, istart, (int64_t)n + 1, st);
+    });
     const uint64_t tiles = ((uint64_t)n + 31) / 32;
     k_copy_untouched<<<grid_for(tiles * 32, 256, 1 << 16), 256, 0, st>>>(g->off, g->tgt, r->off, r->tgt, n,
                                                                           touched);
     check_launch();
-    k_merge_touched<<<grid_for((uint64_t)(ndp + nnw + 1) * 32 + (g->all_loops ? 0 : (uint64_t)n * 32), 256,
-                               1 << 16),
-                      256, 0, st>>>(tlist, tcount, g->off, g->tgt, r->off, r->tgt, dp, ndp, nw, nnw, sb, mask,
-                                    need);
+    k_merge_touched<<<(unsigned)ctx->num_sms * 16, 256, 0, st>>>(istart, n, g->off, g->tgt, r->off, r->tgt, dp,
+                                                                 ndp, nw, nnw, sb, mask, need);
     check_launch();
-    count_launch(ctx, 3);
+    count_launch(ctx, 4);
   }
   unsigned long long hc[2];
   DYNPR_CK(cudaMemcpyAsync(ctx->pinned, counters, 16, cudaMemcpyDeviceToHost, st));

@@ -140,14 +140,52 @@ __global__ void k_fill_multi(const uint64_t* offT, const uint32_t* tgtT, const u
 __global__ void k_outdeg64(const uint32_t* outdeg, uint32_t n, uint64_t* off) {
   GRID_STRIDE(v, (uint64_t)n + 1) off[v] = v < n ? outdeg[v] : 0ull;
 }
+// Relabelled forward CSR (rows and columns in new ids): the output is cut
+// into fixed 1024-element chunks, warp per chunk, so a hub row (RMAT-24:
+// ~4e5 out-edges) is spread over hundreds of warps and a run of short rows
+// keeps all 32 lanes busy.  The row of output element `pos` is found by a
+// binary search of the new offsets restricted to the chunk's row range (a
+// few L1-resident probes); 4 elements in flight per lane.
+constexpr uint64_t kFillChunk = 1024;
+__device__ __forceinline__ uint64_t last_le(const uint64_t* off, uint64_t lo, uint64_t hi, uint64_t pos) {
+  // last w in [lo, hi] with off[w] <= pos (off[lo] <= pos guaranteed)
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi + 1) >> 1;
+    if (off[mid] <= pos) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
 __global__ void k_fill_forward(const uint64_t* offF, const uint32_t* tgtF, const uint32_t* perm, const uint32_t* inv,
                                uint32_t n, const uint64_t* noff, uint32_t* ntgt) {
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / 32;
   const unsigned lane = threadIdx.x & 31;
   const uint64_t nw = (uint64_t)gridDim.x * blockDim.x / 32;
-  for (uint64_t v = warp; v < n; v += nw) {
-    const uint64_t src = offF[perm[v]], d = noff[v], len = noff[v + 1] - d;
-    for (uint64_t k = lane; k < len; k += 32) ntgt[d + k] = inv[tgtF[src + k]];
+  const uint64_t m = noff[n];
+  const uint64_t nchunks = (m + kFillChunk - 1) / kFillChunk;
+  for (uint64_t c = warp; c < nchunks; c += nw) {
+    const uint64_t p0 = c * kFillChunk, p1 = p0 + kFillChunk < m ? p0 + kFillChunk : m;
+    uint64_t w0 = 0, w1 = 0;
+    if (lane == 0) w0 = last_le(noff, 0, n - 1, p0);
+    if (lane == 1) w1 = last_le(noff, 0, n - 1, p1 - 1);
+    w0 = __shfl_sync(0xffffffffu, w0, 0);
+    w1 = __shfl_sync(0xffffffffu, w1, 1);
+    for (uint64_t base = p0; base < p1; base += 128) {
+      uint32_t x[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint64_t pos = base + 32 * q + lane;
+        x[q] = 0;
+        if (pos < p1) {
+          const uint64_t w = last_le(noff, w0, w1, pos);
+          x[q] = tgtF[offF[perm[w]] + (pos - noff[w])];
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint64_t pos = base + 32 * q + lane;
+        if (pos < p1) ntgt[pos] = inv[x[q]];
+      }
+    }
   }
 }
 
@@ -184,8 +222,8 @@ void build_forward(dynpr_context* ctx, Layout* L, const dynpr_graph* gF) {
   cub_call(ctx, [&](void* t, size_t& b) {
     return cub::DeviceScan::ExclusiveSum(t, b, L->offF, L->offF, (int64_t)L->n + 1, st);
   });
-  k_fill_forward<<<grid(ctx, (uint64_t)L->n * 32), 256, 0, st>>>(gF->off, gF->tgt, L->perm, L->inv, L->n, L->offF,
-                                                                 L->tgtF);
+  k_fill_forward<<<grid(ctx, (L->m + kFillChunk - 1) / kFillChunk * 32), 256, 0, st>>>(
+      gF->off, gF->tgt, L->perm, L->inv, L->n, L->offF, L->tgtF);
   check_launch();
   count_launch(ctx, 2);
   L->has_forward = true;
@@ -209,7 +247,10 @@ Layout* build_layout(dynpr_context* ctx, const dynpr_graph* gT, const dynpr_grap
     L->outdeg = dalloc<uint32_t>(n);
     // temporaries from the pool (the context's stage buffers may hold the
     // caller's staged inputs when the build happens inside an engine call)
-    tmp = dalloc<uint32_t>(5ull * ((uint64_t)n + 1));
+    // temporaries in a context-owned grow-only buffer: a pool allocation of
+    // this size per snapshot occasionally had to map fresh memory (measured
+    // up to 74 ms inside the ingest)
+    tmp = ctx->layout_tmp.as<uint32_t>(5ull * ((uint64_t)n + 1));
     uint32_t* indeg_old = tmp;
     uint32_t* outdeg_old = tmp + (n + 1ull);
     uint32_t* keys = tmp + 2ull * (n + 1ull);
@@ -309,9 +350,7 @@ Layout* build_layout(dynpr_context* ctx, const dynpr_graph* gT, const dynpr_grap
       check_launch();
     }
     count_launch(ctx, 6);
-    pool_free(ctx, tmp);
   } catch (...) {
-    pool_free(ctx, tmp);
     destroy_layout(L);
     throw;
   }

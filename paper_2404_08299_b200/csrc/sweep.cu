@@ -345,13 +345,75 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_mseg_c() {
 }
 
 // ---- multi vertices: ordered combine (rank.cpp:72) + epilogue --------------------
+// Ordered sum of n partials by a whole warp (rank.cpp:72): one coalesced load
+// per 32 partials, then a shuffle-broadcast sequential sum whose shuffles are
+// independent of the add chain (full groups unrolled), so the critical path
+// is n dependent DADDs instead of n dependent loads.
+__device__ __forceinline__ double warp_ordered_sum(const double* __restrict__ p, uint32_t n) {
+  const unsigned lane = lane_id();
+  double sum = 0.0;
+  uint32_t g = 0;
+  for (; g + 32 <= n; g += 32) {
+    const double x = p[g + lane];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) sum = __dadd_rn(sum, __shfl_sync(kFull, x, j));
+  }
+  if (g < n) {
+    const double x = g + lane < n ? p[g + lane] : 0.0;
+    for (uint32_t j = 0; j < n - g; ++j) sum = __dadd_rn(sum, __shfl_sync(kFull, x, j));
+  }
+  return sum;
+}
+
+constexpr uint32_t kWarpCombineChunks = 32;  // multi vertices with more partials are combined by a warp
+
 template <bool FLAGGED, bool CLOSED>
 __device__ __forceinline__ void b_sweep_mfinal(const SweepArgs& a) {
   if (a.done && *a.done) return;
   Acc acc;
-  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
   const uint64_t vend = a.M < a.v_hi ? a.M : a.v_hi;
-  for (uint64_t base = a.v_lo + (uint64_t)blockIdx.x * kThreads; base < vend; base += stride) {
+  // the multi vertices are sorted by in-degree (descending): [0, Mb) have
+  // more than kWarpCombineChunks partials
+  __shared__ uint32_t s_mb;
+  if (threadIdx.x == 0) {
+    uint32_t lo = 0, hi = a.M;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (a.indeg[mid] > kWarpCombineChunks * kAccumChunk) lo = mid + 1; else hi = mid;
+    }
+    s_mb = lo;
+  }
+  __syncthreads();
+  const uint64_t mb = s_mb;
+  // phase 1: warp per heavy multi vertex
+  {
+    const uint64_t lo = a.v_lo, hi = mb < vend ? mb : vend;
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+    const uint64_t nw = (uint64_t)gridDim.x * blockDim.x / 32;
+    for (uint64_t vv = lo + warp; vv < hi; vv += nw) {
+      const uint32_t v = (uint32_t)vv;
+      bool pend = false, lowout = false;
+      uint32_t od = 0;
+      if (FLAGGED && !a.va[v]) {
+        if (lane_id() == 0) copy_through(a, v);
+      } else {
+        const uint32_t deg = a.indeg[v];
+        const uint32_t pb = a.pbase[v];
+        const double c = warp_ordered_sum(a.partials + pb, (deg + kAccumChunk - 1) / kAccumChunk);
+        if (lane_id() == 0) {
+          od = a.outdeg[v];
+          finalize<FLAGGED, CLOSED>(a, v, c, a.rank_prev[v], od, acc, pend, lowout);
+          ++acc.proc;
+          acc.edges += deg;
+        }
+      }
+      if (FLAGGED && a.pend_low) warp_append(pend, lowout, v, od, a.pend_low, a.pend_high, a.red);
+    }
+  }
+  // phase 2: thread per remaining multi vertex, partials loaded 8 ahead
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+  const uint64_t first = a.v_lo > mb ? a.v_lo : mb;
+  for (uint64_t base = first + (uint64_t)blockIdx.x * kThreads; base < vend; base += stride) {
     const uint64_t vv = base + threadIdx.x;
     bool pend = false, lowout = false;
     const uint32_t v = (uint32_t)vv;
@@ -364,7 +426,14 @@ __device__ __forceinline__ void b_sweep_mfinal(const SweepArgs& a) {
         const uint32_t nch = (deg + kAccumChunk - 1) / kAccumChunk;
         const double* p = a.partials + a.pbase[v];
         double c = 0.0;
-        for (uint32_t q = 0; q < nch; ++q) c = __dadd_rn(c, p[q]);
+        for (uint32_t q = 0; q < nch; q += 8) {
+          double x[8];
+#pragma unroll
+          for (uint32_t j = 0; j < 8; ++j) x[j] = q + j < nch ? p[q + j] : 0.0;
+#pragma unroll
+          for (uint32_t j = 0; j < 8; ++j)
+            if (q + j < nch) c = __dadd_rn(c, x[j]);
+        }
         od = a.outdeg[v];
         finalize<FLAGGED, CLOSED>(a, v, c, a.rank_prev[v], od, acc, pend, lowout);
         ++acc.proc;
