@@ -143,8 +143,15 @@ def config3(O, kind, cores, scale=27, seed=42, ref_sweeps=3):
     g, gt = dp.apply_batch_pair(g0, gt0, b)
     lay = dp.prepare(gt, g)
     ingest_ms = (time.perf_counter() - t0) * 1e3
-    s = dp.static_pagerank(gt, g)
-    d = dp.dynamic_frontier(g, gt, b.deletions, b.insertions, base.ranks, pruning=True)
+    # warm (first calls on a new graph size allocate workspace / instantiate
+    # the loop graph); report the median of 3 warm solves each
+    prev_dev = base.ranks
+    dp.static_pagerank(gt, g)
+    dp.dynamic_frontier(g, gt, b.deletions, b.insertions, prev_dev, pruning=True)
+    ss = sorted((dp.static_pagerank(gt, g) for _ in range(3)), key=lambda r: r.device_ms)
+    ds = sorted((dp.dynamic_frontier(g, gt, b.deletions, b.insertions, prev_dev, pruning=True) for _ in range(3)),
+                key=lambda r: r.device_ms)
+    s, d = ss[1], ds[1]
     out = {"workload": "configs[3] Kronecker-%d on one B200" % scale, "n": n, "m": m,
            "build_s": build_s, "ingest_ms": ingest_ms, "layout_ms": lay,
            "static": {"ms_per_solve": s.device_ms, "iterations": s.iterations,

@@ -11,7 +11,9 @@ base = dp.static_pagerank(gt, g)
 b = dp.generate_random_batch(g, dp.batch_size_from_fraction(frac, g.edge_count), 0.8, 5)
 g2, gt2 = dp.apply_batch_pair(g, gt, b)
 dp.prepare(gt2, g2)
-for _ in range(3):
+if os.environ.get("HOSTLOOP_DFP"):
+    os.environ["DYNPR_HOST_LOOP"] = "1"
+for _ in range(int(os.environ.get("REPS", "3"))):
     t0 = time.perf_counter()
     d = dp.dynamic_frontier(g2, gt2, b.deletions, b.insertions, base.ranks, pruning=True)
     print("dfp device_ms %.3f wall_ms %.3f it %d affected %d" % (d.device_ms, (time.perf_counter() - t0) * 1e3,
