@@ -33,6 +33,8 @@
 #include <memory>
 #include <string>
 #include <unordered_map>
+#include <exception>
+#include <thread>
 #include <utility>
 #include <vector>
 
@@ -141,6 +143,108 @@ std::string lower(std::pair<const char*, const char*> tok) {
   return s;
 }
 
+// ---- parallel body parsing ----------------------------------------------------
+// Files above kParallelBytes are split into line-aligned chunks parsed by
+// host threads; every chunk reports its line count and its first error, and
+// the chunks are stitched in file order, so the result -- arrays, error
+// class, message and line number -- is exactly the sequential reading's.
+// DYNPR_PARSE_THREADS overrides the thread count (tests force the parallel
+// path on small files with it).
+constexpr size_t kParallelBytes = size_t(8) << 20;
+
+unsigned parse_threads(size_t body_bytes) {
+  if (const char* e = std::getenv("DYNPR_PARSE_THREADS")) {
+    const long t = std::strtol(e, nullptr, 10);
+    if (t >= 1) return (unsigned)std::min<long>(t, 256);
+  }
+  if (body_bytes < kParallelBytes) return 1;
+  const unsigned hc = std::thread::hardware_concurrency();
+  return std::max(1u, std::min(hc ? hc : 1u, 64u));
+}
+
+// [b, e) cut into up to `t` pieces, each ending just after a '\n' (the last
+// at e).
+std::vector<const char*> split_lines(const char* b, const char* e, unsigned t) {
+  std::vector<const char*> cuts{b};
+  const size_t len = static_cast<size_t>(e - b);
+  for (unsigned k = 1; k < t; ++k) {
+    const char* p = b + len * k / t;
+    if (p <= cuts.back()) continue;
+    const char* nl = static_cast<const char*>(memchr(p, '\n', static_cast<size_t>(e - p)));
+    if (!nl) break;
+    if (nl + 1 > cuts.back() && nl + 1 < e) cuts.push_back(nl + 1);
+  }
+  cuts.push_back(e);
+  return cuts;
+}
+
+template <class F>
+void parallel_for(size_t n, F&& f) {
+  if (n <= 1) {
+    if (n) f(0);
+    return;
+  }
+  std::vector<std::thread> th;
+  std::vector<std::exception_ptr> errs(n);
+  for (size_t k = 0; k < n; ++k)
+    th.emplace_back([&, k] {
+      try {
+        f(k);
+      } catch (...) {
+        errs[k] = std::current_exception();
+      }
+    });
+  for (auto& x : th) x.join();
+  for (auto& x : errs)
+    if (x) std::rethrow_exception(x);
+}
+
+// Lines of [b, e) as LineReader yields them.
+struct ChunkLines {
+  const char* p;
+  const char* end;
+  bool next(const char*& b, const char*& e) {
+    if (p >= end) return false;
+    b = p;
+    const char* nl = static_cast<const char*>(memchr(p, '\n', static_cast<size_t>(end - p)));
+    e = nl ? nl : end;
+    p = nl ? nl + 1 : end;
+    if (e > b && e[-1] == '\r') --e;
+    return true;
+  }
+};
+
+struct MMChunk {
+  std::vector<uint32_t> u, v;  // entries (before symmetric expansion)
+  uint64_t lines = 0;
+  uint64_t err_line = 0;       // 1-based within the chunk; 0 = none
+  const char* err_what = nullptr;
+};
+
+void parse_mm_chunk(const char* b0, const char* e0, uint64_t rows, uint64_t cols, MMChunk& out) {
+  ChunkLines lines{b0, e0};
+  const char *b, *e;
+  while (lines.next(b, e)) {
+    ++out.lines;
+    if (e == b || *b == '%') continue;
+    Tokens t{b, e};
+    auto si = t.next(), sj = t.next();
+    uint64_t i = 0, j = 0;
+    if (!parse_num(si, i) || !parse_num(sj, j)) {
+      out.err_line = out.lines;
+      out.err_what = "malformed entry";
+      return;
+    }
+    if (i < 1 || i > rows || j < 1 || j > cols) {
+      out.err_line = out.lines;
+      out.err_what = "index out of declared bounds";
+      return;
+    }
+    out.u.push_back(static_cast<uint32_t>(i - 1));
+    out.v.push_back(static_cast<uint32_t>(j - 1));
+  }
+}
+
 // loadMatrixMarket -- workload.cpp:43-107.
 dynpr_edge_list* load_matrix_market(const std::string& path) {
   MappedFile f(path);
@@ -172,72 +276,228 @@ dynpr_edge_list* load_matrix_market(const std::string& path) {
   }
   auto out = std::make_unique<dynpr_edge_list>();
   out->n = static_cast<uint32_t>(std::max(rows, cols));
-  // Reserve from the file size, not the declared count (a lying header must
-  // not allocate): every entry line takes at least 4 bytes.
-  const size_t guess = std::min<uint64_t>(symmetric ? declared * 2 : declared, f.size / 2 + 16);
-  out->src.reserve(guess);
-  out->dst.reserve(guess);
-  uint64_t seen = 0;
-  while (seen < declared) {
-    if (!lines.next(b, e))
-      parse_error(path, line_no + 1,
-                  "expected " + std::to_string(declared) + " entries, got " + std::to_string(seen));
-    ++line_no;
-    if (e == b || *b == '%') continue;
-    Tokens t{b, e};
-    auto si = t.next(), sj = t.next();  // any weight column is ignored
-    uint64_t i = 0, j = 0;
-    if (!parse_num(si, i) || !parse_num(sj, j)) parse_error(path, line_no, "malformed entry");
-    if (i < 1 || i > rows || j < 1 || j > cols) parse_error(path, line_no, "index out of declared bounds");
-    ++seen;
-    const auto u = static_cast<uint32_t>(i - 1), v = static_cast<uint32_t>(j - 1);
-    out->src.push_back(u);
-    out->dst.push_back(v);
-    if (symmetric && u != v) {
-      out->src.push_back(v);
-      out->dst.push_back(u);
+  // body: chunks parsed in parallel, stitched in order up to `declared`
+  // entries (the reference never reads past them, so a bad line after the
+  // last declared entry is not an error)
+  const char* body = lines.p;
+  const char* end = lines.end;
+  const auto cuts = split_lines(body, end, parse_threads(static_cast<size_t>(end - body)));
+  std::vector<MMChunk> ch(cuts.size() - 1);
+  parallel_for(ch.size(), [&](size_t k) { parse_mm_chunk(cuts[k], cuts[k + 1], rows, cols, ch[k]); });
+  uint64_t seen = 0, take_chunks = 0, last_take = 0;
+  for (size_t k = 0; k < ch.size(); ++k) {
+    const uint64_t need = declared - seen;
+    if (ch[k].u.size() >= need) {  // the declared count is reached inside this chunk
+      take_chunks = k + 1;
+      last_take = need;
+      seen = declared;
+      break;
     }
+    if (ch[k].err_line) parse_error(path, line_no + ch[k].err_line, ch[k].err_what);
+    seen += ch[k].u.size();
+    line_no += ch[k].lines;
+    take_chunks = k + 1;
+    last_take = ch[k].u.size();
   }
+  if (seen < declared)
+    parse_error(path, line_no + 1,
+                "expected " + std::to_string(declared) + " entries, got " + std::to_string(seen));
+  // output offsets per chunk (symmetric off-diagonal entries emit both
+  // directions, in entry order)
+  std::vector<uint64_t> base(take_chunks + 1, 0);
+  for (size_t k = 0; k < take_chunks; ++k) {
+    const uint64_t cnt = k + 1 == take_chunks ? last_take : ch[k].u.size();
+    uint64_t edges = cnt;
+    if (symmetric)
+      for (uint64_t i = 0; i < cnt; ++i) edges += ch[k].u[i] != ch[k].v[i];
+    base[k + 1] = base[k] + edges;
+  }
+  out->src.resize(base[take_chunks]);
+  out->dst.resize(base[take_chunks]);
+  parallel_for(take_chunks, [&](size_t k) {
+    const uint64_t cnt = k + 1 == take_chunks ? last_take : ch[k].u.size();
+    uint64_t o = base[k];
+    for (uint64_t i = 0; i < cnt; ++i) {
+      const uint32_t u = ch[k].u[i], v = ch[k].v[i];
+      out->src[o] = u;
+      out->dst[o++] = v;
+      if (symmetric && u != v) {
+        out->src[o] = v;
+        out->dst[o++] = u;
+      }
+    }
+  });
   return out.release();
 }
 
-// loadTemporalEdgeList -- workload.cpp:109-136.  Ids are compacted in
-// first-appearance order (source before target within a line); the entries
-// are then stably sorted by timestamp (a stable permutation sort on the
-// 64-bit keys).
-dynpr_edge_list* load_temporal(const std::string& path) {
-  MappedFile f(path);
-  LineReader lines(f);
-  auto out = std::make_unique<dynpr_edge_list>();
-  out->temporal = true;
-  std::unordered_map<uint64_t, uint32_t> compact;
-  compact.reserve(1024);
-  auto compact_id = [&](uint64_t raw) {
-    return compact.emplace(raw, static_cast<uint32_t>(compact.size())).first->second;
-  };
-  std::vector<uint32_t> s, d;
+// Open-addressing hash map uint64 -> uint64 (linear probing, power-of-two
+// capacity, grows at 1/2 load) -- the id compaction's hot structure.
+struct U64Map {
+  static constexpr uint64_t kEmpty = ~0ull;
+  std::vector<uint64_t> keys, vals;
+  uint64_t mask = 0, size = 0;
+  explicit U64Map(uint64_t cap = 1024) { init(cap); }
+  void init(uint64_t cap) {
+    uint64_t c = 16;
+    while (c < cap) c <<= 1;
+    keys.assign(c, kEmpty);
+    vals.assign(c, 0);
+    mask = c - 1;
+    size = 0;
+  }
+  static uint64_t hash(uint64_t k) {
+    k ^= k >> 33;
+    k *= 0xff51afd7ed558ccdULL;
+    k ^= k >> 33;
+    return k;
+  }
+  // inserts (k, v) if k is absent (the raw id ~0 is kept aside: never a key)
+  void emplace(uint64_t k, uint64_t v) {
+    if ((size + 1) * 2 > mask + 1) grow();
+    uint64_t i = hash(k) & mask;
+    while (keys[i] != kEmpty) {
+      if (keys[i] == k) return;
+      i = (i + 1) & mask;
+    }
+    keys[i] = k;
+    vals[i] = v;
+    ++size;
+  }
+  uint64_t at(uint64_t k) const {
+    uint64_t i = hash(k) & mask;
+    while (keys[i] != k) i = (i + 1) & mask;
+    return vals[i];
+  }
+  void grow() {
+    std::vector<uint64_t> ok = std::move(keys), ov = std::move(vals);
+    init((mask + 1) * 2);
+    for (size_t i = 0; i < ok.size(); ++i)
+      if (ok[i] != kEmpty) emplace(ok[i], ov[i]);
+  }
+};
+
+struct TChunk {
+  std::vector<uint64_t> s, d;
   std::vector<int64_t> ts;
+  uint64_t lines = 0;
+  uint64_t err_line = 0;
+};
+
+void parse_temporal_chunk(const char* b0, const char* e0, TChunk& out) {
+  ChunkLines lines{b0, e0};
   const char *b, *e;
-  uint64_t line_no = 0;
   while (lines.next(b, e)) {
-    ++line_no;
+    ++out.lines;
     if (e == b || *b == '#') continue;
     Tokens t{b, e};
     auto a = t.next(), c = t.next(), z = t.next();
     uint64_t src = 0, dst = 0;
     int64_t stamp = 0;
-    if (!parse_num(a, src) || !parse_num(c, dst) || !parse_num(z, stamp))
-      parse_error(path, line_no, "expected 'src dst timestamp'");
-    const uint32_t cs = compact_id(src);
-    const uint32_t cd = compact_id(dst);
-    s.push_back(cs);
-    d.push_back(cd);
-    ts.push_back(stamp);
+    if (!parse_num(a, src) || !parse_num(c, dst) || !parse_num(z, stamp)) {
+      out.err_line = out.lines;
+      return;
+    }
+    out.s.push_back(src);
+    out.d.push_back(dst);
+    out.ts.push_back(stamp);
   }
-  out->n = static_cast<uint32_t>(compact.size());
+}
+
+// loadTemporalEdgeList -- workload.cpp:109-136.  Raw ids are compacted in
+// first-appearance order (source before target within a line): the
+// (raw id, position) pairs are hash-partitioned into buckets, each bucket
+// keeps the first position of its ids (chunks visited in file order), the
+// distinct ids are ranked by first position, and the entries mapped in
+// parallel.  The entries are then stably sorted by timestamp.
+dynpr_edge_list* load_temporal(const std::string& path) {
+  MappedFile f(path);
+  const char* body = f.data;
+  const char* end = f.data + f.size;
+  const unsigned T = parse_threads(f.size);
+  const auto cuts = split_lines(body, end, T);
+  std::vector<TChunk> ch(cuts.size() - 1);
+  const bool dbg = std::getenv("DYNPR_PARSE_DEBUG") != nullptr;
+  auto tick = [&, t0 = std::chrono::steady_clock::now()](const char* what) mutable {
+    if (!dbg) return;
+    const auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "load_temporal %-10s %.1f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  };
+  parallel_for(ch.size(), [&](size_t k) { parse_temporal_chunk(cuts[k], cuts[k + 1], ch[k]); });
+  tick("parse");
+  uint64_t line_no = 0, total = 0;
+  std::vector<uint64_t> first(ch.size() + 1, 0);
+  for (size_t k = 0; k < ch.size(); ++k) {
+    if (ch[k].err_line) parse_error(path, line_no + ch[k].err_line, "expected 'src dst timestamp'");
+    line_no += ch[k].lines;
+    first[k] = total;
+    total += ch[k].s.size();
+  }
+  first[ch.size()] = total;
+
+  auto out = std::make_unique<dynpr_edge_list>();
+  out->temporal = true;
+  const size_t P = ch.size();
+  auto bucket_of = [P](uint64_t raw) {
+    return P == 1 ? size_t(0) : static_cast<size_t>((raw * 0x9E3779B97F4A7C15ULL) >> 32) % P;
+  };
+  // per-bucket maps raw -> first position (2 * entry + {0 src, 1 dst});
+  // every bucket thread walks the chunks in file order and keeps its ids.
+  // The raw id ~0 (the maps' empty marker) is tracked on the side.
+  std::vector<U64Map> firstpos(P);
+  uint64_t max_first = ~0ull;  // first position of raw id ~0, if present
+  parallel_for(P, [&](size_t bkt) {
+    auto& mp = firstpos[bkt];
+    for (size_t k = 0; k < ch.size(); ++k)
+      for (uint64_t i = 0; i < ch[k].s.size(); ++i) {
+        const uint64_t pos = 2 * (first[k] + i);
+        const uint64_t a = ch[k].s[i], c = ch[k].d[i];
+        if (a != U64Map::kEmpty && bucket_of(a) == bkt) mp.emplace(a, pos);
+        if (c != U64Map::kEmpty && bucket_of(c) == bkt) mp.emplace(c, pos + 1);
+      }
+  });
+  tick("firstpos");
+  for (size_t k = 0; k < ch.size() && max_first == ~0ull; ++k)
+    for (uint64_t i = 0; i < ch[k].s.size(); ++i) {
+      const uint64_t pos = 2 * (first[k] + i);
+      if (ch[k].s[i] == U64Map::kEmpty) { max_first = pos; break; }
+      if (ch[k].d[i] == U64Map::kEmpty) { max_first = pos + 1; break; }
+    }
+  // dense ids in first-appearance order
+  std::vector<std::pair<uint64_t, uint64_t>> order;  // (first pos, raw)
+  for (const auto& mp : firstpos)
+    for (size_t i = 0; i < mp.keys.size(); ++i)
+      if (mp.keys[i] != U64Map::kEmpty) order.emplace_back(mp.vals[i], mp.keys[i]);
+  if (max_first != ~0ull) order.emplace_back(max_first, U64Map::kEmpty);
+  std::sort(order.begin(), order.end());
+  uint32_t id_of_max = 0;
+  for (size_t i = 0; i < order.size(); ++i) {
+    if (order[i].second == U64Map::kEmpty) {
+      id_of_max = (uint32_t)i;
+      continue;
+    }
+    auto& mp = firstpos[bucket_of(order[i].second)];  // reuse: value := dense id
+    uint64_t j = U64Map::hash(order[i].second) & mp.mask;
+    while (mp.keys[j] != order[i].second) j = (j + 1) & mp.mask;
+    mp.vals[j] = i;
+  }
+  tick("order");
+  out->n = static_cast<uint32_t>(order.size());
+  std::vector<uint32_t> s(total), d(total);
+  std::vector<int64_t> ts(total);
+  auto dense = [&](uint64_t raw) -> uint32_t {
+    return raw == U64Map::kEmpty ? id_of_max : (uint32_t)firstpos[bucket_of(raw)].at(raw);
+  };
+  parallel_for(ch.size(), [&](size_t k) {
+    for (uint64_t i = 0; i < ch[k].s.size(); ++i) {
+      s[first[k] + i] = dense(ch[k].s[i]);
+      d[first[k] + i] = dense(ch[k].d[i]);
+      ts[first[k] + i] = ch[k].ts[i];
+    }
+  });
+  tick("map");
   const size_t cnt = ts.size();
-  bool sorted = std::is_sorted(ts.begin(), ts.end());
-  if (sorted) {
+  if (std::is_sorted(ts.begin(), ts.end())) {
     out->src = std::move(s);
     out->dst = std::move(d);
     out->ts = std::move(ts);

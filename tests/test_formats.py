@@ -22,6 +22,14 @@ def ref():
     return oracle.Oracle("ref")
 
 
+@pytest.fixture(autouse=True, params=["1", "3", "7"], ids=["seq", "par3", "par7"])
+def parse_threads(request, monkeypatch):
+    """Run every loader test on the sequential path and on the parallel
+    chunked parser (forced on small files)."""
+    monkeypatch.setenv("DYNPR_PARSE_THREADS", request.param)
+    return request.param
+
+
 def _write(tmp_path, name, text):
     p = tmp_path / name
     p.write_bytes(text.encode() if isinstance(text, str) else text)
@@ -68,6 +76,12 @@ MM_CASES = {
     "space_before_comment": "%%MatrixMarket matrix coordinate pattern general\n3 3 1\n  % not a comment\n1 2\n",
     "whitespace_line": "%%MatrixMarket matrix coordinate pattern general\n3 3 1\n   \n1 2\n",
     "zero_entries": "%%MatrixMarket matrix coordinate pattern general\n5 2 0\n",
+    "late_garbage_ignored": "%%MatrixMarket matrix coordinate pattern general\n4 4 3\n1 2\n2 3\n3 4\n"
+                            + "".join(f"{i % 4 + 1} {i % 3 + 1}\n" for i in range(40)) + "bad line\n",
+    "late_error_counts": "%%MatrixMarket matrix coordinate pattern general\n4 4 40\n"
+                         + "".join(f"{i % 4 + 1} {i % 3 + 1}\n" for i in range(30)) + "x y\n",
+    "short_many": "%%MatrixMarket matrix coordinate pattern symmetric\n9 9 50\n"
+                  + "".join(f"{i % 9 + 1} {(i * 7) % 9 + 1}\n" for i in range(45)),
 }
 
 
@@ -117,6 +131,9 @@ T_CASES = {
     "space_hash": "1 2 3\n # comment?\n",
     "no_final_newline": "1 2 3\n3 4 1",
     "empty": "",
+    "many_lines_late_error": "".join(f"{i * 31 % 97} {i * 17 % 89} {1000 - i}\n" for i in range(200)) + "1 2\n",
+    "many_lines_unsorted": "# x\n" + "".join(f"{i * 31 % 97} {i * 17 % 89} {(i * 7919) % 13}\n"
+                                            for i in range(300)),
 }
 
 
