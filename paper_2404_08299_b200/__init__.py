@@ -295,7 +295,43 @@ def _p(a: Optional[np.ndarray]):
 
 
 def _is_device_array(x) -> bool:
-    return hasattr(x, "data_ptr") and getattr(x, "is_cuda", False)
+    return getattr(x, "__cuda_array_interface__", None) is not None
+
+
+_TYPESTR = {np.float64: "<f8", np.uint8: "|u1", np.uint32: "<u4"}
+
+
+def _in_array(x, dtype):
+    """(pointer, length, keep-alive) of an input array.  Device arrays
+    (anything exposing __cuda_array_interface__: torch CUDA tensors, CuPy)
+    are passed to the C-ABI as device pointers -- no host round trip; the
+    library detects device memory itself (dynpr_cuda.h conventions)."""
+    cai = getattr(x, "__cuda_array_interface__", None)
+    if cai is not None:
+        if cai.get("typestr") != _TYPESTR[dtype]:
+            raise ValueError(f"device array must have dtype {np.dtype(dtype).name}")
+        if cai.get("strides") not in (None, ()):
+            shape = cai["shape"]
+            itemsize = np.dtype(dtype).itemsize
+            if len(shape) != 1 or cai["strides"][0] != itemsize:
+                raise ValueError("device array must be contiguous")
+        n = int(np.prod(cai["shape"])) if cai["shape"] else 1
+        return (C.c_void_p(cai["data"][0]) if n else None), n, x
+    a = _arr(x, dtype)
+    return _p(a), len(a), a
+
+
+def _out_ranks(out, n: int):
+    """(pointer, result array) for an engine's ranks: a fresh numpy array, or
+    the caller's device array `out` (n float64) so chained solves never
+    leave the GPU."""
+    if out is None:
+        r = np.zeros(max(n, 1), np.float64)
+        return _p(r), r
+    ptr, length, keep = _in_array(out, np.float64)
+    if length != n:
+        raise ValueError("out must hold exactly vertex_count float64 values")
+    return ptr, keep
 
 
 class CsrGraph:
@@ -574,67 +610,71 @@ def _result(ranks: np.ndarray, st: N.Stats) -> RankResult:
 
 
 def static_pagerank(g_transpose: CsrGraph, g_forward: CsrGraph, config: Optional[EngineConfig] = None,
-                    observer: Optional[Callable] = None) -> RankResult:
-    """staticPageRank(gTranspose, gForward, cfg) -- engine.cpp:99-108."""
+                    observer: Optional[Callable] = None, out=None) -> RankResult:
+    """staticPageRank(gTranspose, gForward, cfg) -- engine.cpp:99-108.
+    `out`: optional device array (n float64) that receives the ranks."""
     cfg = (config or EngineConfig())._c()
-    ranks = np.zeros(max(g_transpose.vertex_count, 1), np.float64)
+    rp, ranks = _out_ranks(out, g_transpose.vertex_count)
     st = N.Stats()
     obs, keep = _observer(observer)
     _check(N.lib().dynpr_static_pagerank(C.c_void_p(g_transpose.ctx.h), C.c_void_p(g_transpose.h),
-                                         C.c_void_p(g_forward.h), C.byref(cfg), _p(ranks), C.byref(st), obs,
+                                         C.c_void_p(g_forward.h), C.byref(cfg), rp, C.byref(st), obs,
                                          None))
     return _result(ranks[: g_transpose.vertex_count], st)
 
 
 def naive_dynamic(g_transpose: CsrGraph, g_forward: CsrGraph, previous_ranks,
-                  config: Optional[EngineConfig] = None, observer: Optional[Callable] = None) -> RankResult:
-    """naiveDynamic(gTranspose, gForward, previousRanks, cfg) -- engine.cpp:110-122."""
+                  config: Optional[EngineConfig] = None, observer: Optional[Callable] = None,
+                  out=None) -> RankResult:
+    """naiveDynamic(gTranspose, gForward, previousRanks, cfg) -- engine.cpp:110-122.
+    previous_ranks / out may be device arrays."""
     cfg = (config or EngineConfig())._c()
-    prev = _arr(previous_ranks, np.float64)
-    ranks = np.zeros(max(g_transpose.vertex_count, 1), np.float64)
+    pp, plen, pkeep = _in_array(previous_ranks, np.float64)
+    rp, ranks = _out_ranks(out, g_transpose.vertex_count)
     st = N.Stats()
     obs, keep = _observer(observer)
     _check(N.lib().dynpr_naive_dynamic(C.c_void_p(g_transpose.ctx.h), C.c_void_p(g_transpose.h),
-                                       C.c_void_p(g_forward.h), _p(prev), len(prev), C.byref(cfg), _p(ranks),
+                                       C.c_void_p(g_forward.h), pp, plen, C.byref(cfg), rp,
                                        C.byref(st), obs, None))
     return _result(ranks[: g_transpose.vertex_count], st)
 
 
 def dynamic_frontier(g_forward: CsrGraph, g_transpose: CsrGraph, deletions, insertions, previous_ranks,
                      config: Optional[EngineConfig] = None, pruning: bool = False,
-                     observer: Optional[Callable] = None) -> RankResult:
+                     observer: Optional[Callable] = None, out=None) -> RankResult:
     """dynamicFrontier(gForward, gTranspose, dels, ins, prev, cfg, pruning) --
     engine.cpp:192-203 (DF-P with pruning=True).  The observer, when given,
     receives (iteration, ranks, processed_flags)."""
     cfg = (config or EngineConfig())._c()
     ds, dd = _edges(deletions)
     is_, id_ = _edges(insertions)
-    prev = _arr(previous_ranks, np.float64)
-    ranks = np.zeros(max(g_transpose.vertex_count, 1), np.float64)
+    pp, plen, pkeep = _in_array(previous_ranks, np.float64)
+    rp, ranks = _out_ranks(out, g_transpose.vertex_count)
     st = N.Stats()
     obs, keep = _observer(observer)
     _check(N.lib().dynpr_dynamic_frontier(C.c_void_p(g_forward.ctx.h), C.c_void_p(g_forward.h),
                                           C.c_void_p(g_transpose.h), _p(ds), _p(dd), len(ds), _p(is_), _p(id_),
-                                          len(is_), _p(prev), len(prev), C.byref(cfg), int(bool(pruning)),
-                                          _p(ranks), C.byref(st), obs, None))
+                                          len(is_), pp, plen, C.byref(cfg), int(bool(pruning)),
+                                          rp, C.byref(st), obs, None))
     return _result(ranks[: g_transpose.vertex_count], st)
 
 
 def dynamic_traversal(g_forward: CsrGraph, g_transpose: CsrGraph, deletions, insertions, previous_ranks,
-                      config: Optional[EngineConfig] = None, observer: Optional[Callable] = None) -> RankResult:
+                      config: Optional[EngineConfig] = None, observer: Optional[Callable] = None,
+                      out=None) -> RankResult:
     """dynamicTraversal(gForward, gTranspose, dels, ins, prev, cfg) --
     engine.cpp:124-151: every vertex reachable from an update endpoint
     (device BFS) is processed every sweep; no expansion, no pruning."""
     cfg = (config or EngineConfig())._c()
     ds, dd = _edges(deletions)
     is_, id_ = _edges(insertions)
-    prev = _arr(previous_ranks, np.float64)
-    ranks = np.zeros(max(g_transpose.vertex_count, 1), np.float64)
+    pp, plen, pkeep = _in_array(previous_ranks, np.float64)
+    rp, ranks = _out_ranks(out, g_transpose.vertex_count)
     st = N.Stats()
     obs, keep = _observer(observer)
     _check(N.lib().dynpr_dynamic_traversal(C.c_void_p(g_forward.ctx.h), C.c_void_p(g_forward.h),
                                            C.c_void_p(g_transpose.h), _p(ds), _p(dd), len(ds), _p(is_), _p(id_),
-                                           len(is_), _p(prev), len(prev), C.byref(cfg), _p(ranks), C.byref(st),
+                                           len(is_), pp, plen, C.byref(cfg), rp, C.byref(st),
                                            obs, None))
     return _result(ranks[: g_transpose.vertex_count], st)
 

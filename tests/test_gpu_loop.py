@@ -87,3 +87,30 @@ def test_device_loop_converges_on_odd_and_even_iterations(dp, oracle_lib, monkey
         _same(r, O.static(ogt, og, oracle.default_config(iteration_tolerance=tol)))
         seen.add(r.iterations % 2)
     assert seen == {0, 1}
+
+
+def test_device_resident_arrays(dp, oracle_lib):
+    """previous_ranks / out as CUDA tensors (__cuda_array_interface__):
+    same results as host arrays, no host round trip of the rank vectors."""
+    import torch
+    O = oracle_lib
+    og, ogt = rand_pair(O, 51, 3000, 30000)
+    dels, ins = O.generate_random_batch(og, 30, 0.8, 2)
+    og2, _, _ = O.apply_batch(og, dels, ins)
+    g, gt = to_dev(dp, og), to_dev(dp, ogt)
+    g2, gt2 = to_dev(dp, og2), to_dev(dp, O.transpose(og2))
+    base = dp.static_pagerank(gt, g)
+    out = torch.empty(3000, dtype=torch.float64, device="cuda")
+    b2 = dp.static_pagerank(gt, g, out=out)
+    assert b2.ranks.data_ptr() == out.data_ptr() and np.array_equal(out.cpu().numpy(), base.ranks)
+    host = dp.dynamic_frontier(g2, gt2, dels, ins, base.ranks, pruning=True)
+    out2 = torch.empty_like(out)
+    dev = dp.dynamic_frontier(g2, gt2, dels, ins, out, pruning=True, out=out2)
+    _same(type(host)(out2.cpu().numpy(), dev.iterations, dev.affected_vertex_iterations, dev.converged,
+                     dev.final_delta), host)
+    nd = dp.naive_dynamic(gt2, g2, out, out=out2)
+    assert np.array_equal(out2.cpu().numpy(), dp.naive_dynamic(gt2, g2, base.ranks).ranks)
+    with pytest.raises(ValueError, match="dtype float64"):
+        dp.naive_dynamic(gt2, g2, out.float())
+    with pytest.raises(ValueError, match="exactly vertex_count"):
+        dp.static_pagerank(gt, g, out=out[:10])
