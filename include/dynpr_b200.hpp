@@ -35,10 +35,21 @@
 
 namespace dynpr_b200 {
 
+// SizingError / ParseError (workload.hpp:12-21) as thrown by this shim when
+// the caller does not supply the reference's own classes (see check<>).
+struct SizingError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct ParseError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
 inline void check(dynpr_status st) {
   if (st == DYNPR_OK) return;
   const std::string msg = dynpr_last_error();
   if (st == DYNPR_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+  if (st == DYNPR_SIZING_ERROR) throw SizingError(msg);
+  if (st == DYNPR_PARSE_ERROR) throw ParseError(msg);
   throw std::runtime_error(msg);
 }
 
@@ -253,6 +264,105 @@ inline double linfNormDelta(std::span<const double> a, std::span<const double> b
   double out = 0.0;
   check(dynpr_linf_norm_delta(ctx.get(), a.data(), b.data(), a.size(), &out));
   return out;
+}
+
+
+// ---- input formats + harness (workload.hpp:43-64, harness.hpp:12-79) -------
+
+// loadMatrixMarket -- workload.hpp:45-48.  MMGraph = {EdgeList edges;
+// Vertex vertexCount;} (the reference's MatrixMarketGraph).
+template <class MMGraph>
+MMGraph loadMatrixMarket(const std::string& path) {
+  dynpr_edge_list* e = nullptr;
+  check(dynpr_load_matrix_market(path.c_str(), &e));
+  std::unique_ptr<dynpr_edge_list, dynpr_status (*)(dynpr_edge_list*)> guard(e, &dynpr_edge_list_destroy);
+  uint32_t n = 0;
+  uint64_t cnt = 0;
+  int ts = 0;
+  check(dynpr_edge_list_info(e, &n, &cnt, &ts));
+  std::vector<uint32_t> s(cnt), d(cnt);
+  check(dynpr_edge_list_copy(e, 0, cnt, s.data(), d.data(), nullptr));
+  MMGraph out;
+  out.vertexCount = n;
+  out.edges.reserve(cnt);
+  for (uint64_t i = 0; i < cnt; ++i) out.edges.emplace_back(s[i], d[i]);
+  return out;
+}
+
+// computeReferenceRanks -- harness.hpp:57-61 (500 sweeps on the device).
+template <class Graph, class Cfg>
+std::vector<double> computeReferenceRanks(const Graph& gT, const Graph& gF, const Cfg& cfg,
+                                          Context& ctx = Context::instance()) {
+  const DeviceGraph dT = DeviceGraph::upload(gT, ctx), dF = DeviceGraph::upload(gF, ctx);
+  const dynpr_config c = toConfig(cfg);
+  std::vector<double> r(gT.vertexCount());
+  check(dynpr_compute_reference_ranks(ctx.get(), dT.get(), dF.get(), &c, r.data()));
+  return r;
+}
+
+// runExperiment -- harness.hpp:63-65, on the device engines.  Spec / Row are
+// the reference's ExperimentSpec / ExperimentRow (field for field); the
+// enums convert through their underlying values, which match
+// DYNPR_APPROACH_* / DYNPR_MODE_* / DYNPR_CHAIN_*.
+template <class Row, class Spec>
+std::vector<Row> runExperiment(const Spec& spec, Context& ctx = Context::instance()) {
+  dynpr_experiment_spec c;
+  dynpr_experiment_spec_default(&c);
+  std::vector<const char*> sizes;
+  for (const auto& x : spec.batchSizeSpecs) sizes.push_back(x.c_str());
+  std::vector<int32_t> approaches;
+  for (auto a : spec.approaches) approaches.push_back(static_cast<int32_t>(a));
+  c.graph_path = spec.graphPath.c_str();
+  c.graph_name = spec.graphName.c_str();
+  c.mode = static_cast<int32_t>(spec.mode);
+  c.batch_size_specs = sizes.data();
+  c.n_batch_size_specs = static_cast<int32_t>(sizes.size());
+  c.approaches = approaches.data();
+  c.n_approaches = static_cast<int32_t>(approaches.size());
+  c.seed = spec.seed;
+  c.repetitions = spec.repetitions;
+  c.base_fraction = spec.baseFraction;
+  c.batch_count = spec.batchCount;
+  c.insert_fraction = spec.insertFraction;
+  c.chain_mode = static_cast<int32_t>(spec.chainMode);
+  c.threads = spec.threads;
+  c.record_timing = spec.recordTiming ? 1 : 0;
+  c.config = toConfig(spec.config);
+  dynpr_report* rep = nullptr;
+  check(dynpr_run_experiment(ctx.get(), &c, &rep));
+  std::unique_ptr<dynpr_report, dynpr_status (*)(dynpr_report*)> guard(rep, &dynpr_report_destroy);
+  uint64_t cnt = 0;
+  check(dynpr_report_size(rep, &cnt));
+  std::vector<Row> rows(cnt);
+  for (uint64_t i = 0; i < cnt; ++i) {
+    dynpr_experiment_row r;
+    check(dynpr_report_row(rep, i, &r));
+    rows[i].graphName = r.graph_name;
+    rows[i].approach = r.approach;
+    rows[i].batchSizeSpec = r.batch_size_spec;
+    rows[i].batchIndex = r.batch_index;
+    rows[i].runtimeMillis = r.runtime_millis;
+    rows[i].iterations = r.iterations;
+    rows[i].affectedVertexIterations = r.affected_vertex_iterations;
+    rows[i].l1ErrorVsReference = r.l1_error_vs_reference;
+    rows[i].converged = r.converged != 0;
+  }
+  return rows;
+}
+
+// emitReport -- harness.hpp:77-79 (format: 0 CSV, 1 JSON).
+template <class Row>
+void emitReport(const std::vector<Row>& rows, int format, const std::string& path) {
+  dynpr_report* rep = nullptr;
+  check(dynpr_report_create(&rep));
+  std::unique_ptr<dynpr_report, dynpr_status (*)(dynpr_report*)> guard(rep, &dynpr_report_destroy);
+  for (const auto& r : rows) {
+    dynpr_experiment_row c{r.graphName.c_str(), r.approach.c_str(), r.batchSizeSpec.c_str(), r.batchIndex,
+                           r.runtimeMillis, r.iterations, r.affectedVertexIterations, r.l1ErrorVsReference,
+                           r.converged ? 1 : 0};
+    check(dynpr_report_append(rep, &c));
+  }
+  check(dynpr_report_emit(rep, format, path.c_str()));
 }
 
 }  // namespace dynpr_b200

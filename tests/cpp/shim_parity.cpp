@@ -9,8 +9,13 @@
 #include <span>
 #include <vector>
 
+#include <fstream>
+#include <sstream>
+#include <string>
+
 #include "dynpr/engine.hpp"
 #include "dynpr/graph.hpp"
+#include "dynpr/harness.hpp"
 #include "dynpr/partition.hpp"
 #include "dynpr/rng.hpp"
 #include "dynpr/workload.hpp"
@@ -86,6 +91,62 @@ int main() {
   } catch (const std::invalid_argument& e) {
     expect(std::string(e.what()) == "EngineConfig: dampingFactor must be in (0,1)",
            "invalid config throws std::invalid_argument with the reference text");
+  }
+  // harness: the reference's runExperiment + emitReport vs the same spec
+  // through the shim (device engines) -- report bytes (criterion 9 shape)
+  {
+    const std::string stream = "/tmp/dynpr_shim_stream.txt";
+    {
+      std::ofstream f(stream);
+      f << "# synthetic temporal stream\n";
+      SplitMix64 r(99);
+      for (int i = 0; i < 4000; ++i)
+        f << r.bounded(600) * 7 << ' ' << r.bounded(600) * 7 << ' ' << (1000 + i / 3) << '\n';
+    }
+    ExperimentSpec spec;
+    spec.graphPath = stream;
+    spec.mode = ExperimentMode::Temporal;
+    spec.batchSizeSpecs = {"1e-3"};
+    spec.approaches = {Approach::Static, Approach::NaiveDynamic, Approach::DynamicTraversal,
+                       Approach::DynamicFrontier, Approach::DynamicFrontierPrune};
+    spec.batchCount = 50;
+    spec.recordTiming = false;
+    const auto want = runExperiment(spec);
+    emitReport(want, ReportFormat::Csv, "/tmp/dynpr_shim_ref.csv");
+    const auto got = dynpr_b200::runExperiment<ExperimentRow>(spec);
+    dynpr_b200::emitReport(got, 0, "/tmp/dynpr_shim_dev.csv");
+    auto slurp = [](const char* p) {
+      std::ifstream f(p);
+      std::stringstream ss;
+      ss << f.rdbuf();
+      return ss.str();
+    };
+    const std::string a = slurp("/tmp/dynpr_shim_ref.csv"), b = slurp("/tmp/dynpr_shim_dev.csv");
+    expect(!a.empty() && a == b, "runExperiment (temporal, 5 approaches): report bytes identical");
+    expect(want.size() == got.size() && want.size() == 255, "runExperiment: 250 rows + 5 summaries");
+    // computeReferenceRanks on the device, bitwise
+    const auto r1 = computeReferenceRanks(gt, g, cfg);
+    const auto r2 = dynpr_b200::computeReferenceRanks(gt, g, cfg);
+    expect(r1 == r2, "computeReferenceRanks: bitwise equal");
+    // loadMatrixMarket
+    {
+      std::ofstream f("/tmp/dynpr_shim.mtx");
+      f << "%%MatrixMarket matrix coordinate real symmetric\n% c\n50 50 120\n";
+      SplitMix64 q(5);
+      for (int i = 0; i < 120; ++i) f << 1 + q.bounded(50) << ' ' << 1 + q.bounded(50) << " 1.0\n";
+    }
+    const auto m1 = loadMatrixMarket("/tmp/dynpr_shim.mtx");
+    const auto m2 = dynpr_b200::loadMatrixMarket<MatrixMarketGraph>("/tmp/dynpr_shim.mtx");
+    expect(m1.edges == m2.edges && m1.vertexCount == m2.vertexCount, "loadMatrixMarket: edges equal");
+    try {
+      ExperimentSpec bad = spec;
+      bad.batchSizeSpecs = {"1e-1"};
+      dynpr_b200::runExperiment<ExperimentRow>(bad);
+      expect(false, "sizing error raised");
+    } catch (const dynpr_b200::SizingError& e) {
+      expect(std::string(e.what()).rfind("splitTemporal: stream has 4000 entries", 0) == 0,
+             "runExperiment: SizingError with the reference text");
+    }
   }
   std::printf("%d failure(s)\n", failures);
   return failures ? 1 : 0;
