@@ -193,7 +193,19 @@ Result dynamicFrontier(const DeviceGraph& gF, const DeviceGraph& gT, const EdgeL
 template <class Result, class Graph, class Cfg,
           class Observer = std::function<void(int, std::span<const double>)>>
 Result staticPageRank(const Graph& gT, const Graph& gF, const Cfg& cfg, const Observer& obs = {}) {
-  return staticPageRank<Result>(DeviceGraph::upload(gT), DeviceGraph::upload(gF), cfg, obs);
+  // one call: gF's targets (unused by Static) upload and validate while the
+  // solve runs (dynpr_static_pagerank_csr)
+  Context& ctx = Context::instance();
+  const dynpr_config c = toConfig(cfg);
+  if (gT.vertexCount() != gF.vertexCount() || gT.targets().size() != gF.targets().size())
+    return staticPageRank<Result>(DeviceGraph::upload(gT), DeviceGraph::upload(gF), cfg, obs);
+  std::vector<double> ranks(gT.vertexCount());
+  dynpr_stats st{};
+  detail::ObserverBox box{std::function<void(int, std::span<const double>)>(obs)};
+  check(dynpr_static_pagerank_csr(ctx.get(), gT.vertexCount(), gT.offsets().data(), gT.targets().data(),
+                                  gF.offsets().data(), gF.targets().data(), gT.targets().size(), &c, ranks.data(),
+                                  &st, box.fn ? &detail::ObserverBox::trampoline : nullptr, &box));
+  return detail::makeResult<Result>(std::move(ranks), st);
 }
 
 // dynamicFrontier(gForward, gTranspose, dels, ins, prev, cfg, pruning) -- engine.hpp:58-62

@@ -271,6 +271,21 @@ dynpr_status dynpr_static_pagerank(dynpr_context* ctx, const dynpr_graph* gT,
                                    const dynpr_config* cfg, double* ranks_out,
                                    dynpr_stats* stats, dynpr_observer observer,
                                    void* observer_user);
+/* staticPageRank on host (or device) CSR arrays -- the reference's call with
+ * freshly constructed CsrGraph values (graph.cpp:30-49 + engine.cpp:99-108):
+ * gT is uploaded and validated, then gF's offsets; gF's targets, which Static
+ * does not read, are uploaded and validated on a side stream while the solve
+ * runs.  Same errors as constructing the two graphs then calling
+ * dynpr_static_pagerank. */
+dynpr_status dynpr_static_pagerank_csr(dynpr_context* ctx, uint32_t n,
+                                       const uint64_t* offsets_t,
+                                       const uint32_t* targets_t,
+                                       const uint64_t* offsets_f,
+                                       const uint32_t* targets_f, uint64_t m,
+                                       const dynpr_config* cfg,
+                                       double* ranks_out, dynpr_stats* stats,
+                                       dynpr_observer observer,
+                                       void* observer_user);
 /* naiveDynamic(gTranspose, gForward, previousRanks, cfg) -- engine.cpp:110. */
 dynpr_status dynpr_naive_dynamic(dynpr_context* ctx, const dynpr_graph* gT,
                                  const dynpr_graph* gF, const double* previous,

@@ -142,6 +142,7 @@ PROTOTYPES = {
     "dynpr_initial_affected": (_i, [_vp, _vp, _vp, _vp, _u64, _vp, _vp, _u64, _vp, _vp]),
     "dynpr_expand_affected": (_i, [_vp, _vp, _vp, _vp, _u32]),
     "dynpr_static_pagerank": (_i, [_vp, _vp, _vp, _cfgp, _vp, _stp, OBSERVER, _vp]),
+    "dynpr_static_pagerank_csr": (_i, [_vp, _u32, _vp, _vp, _vp, _vp, _u64, _cfgp, _vp, _stp, OBSERVER, _vp]),
     "dynpr_naive_dynamic": (_i, [_vp, _vp, _vp, _vp, _u64, _cfgp, _vp, _stp, OBSERVER, _vp]),
     "dynpr_dynamic_frontier": (_i, [_vp, _vp, _vp, _vp, _vp, _u64, _vp, _vp, _u64, _vp, _u64, _cfgp, _i,
                                     _vp, _stp, OBSERVER, _vp]),

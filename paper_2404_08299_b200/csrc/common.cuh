@@ -124,6 +124,8 @@ struct dynpr_context {
   cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_s0 = nullptr, ev_s1 = nullptr;
   // pinned host scratch for small readbacks
   void* pinned = nullptr;
+  cudaStream_t side = nullptr;  // deferred uploads / validation (created on first use)
+  cudaEvent_t ev_side = nullptr;
   // instantiated device-loop graphs (engine.cu LoopGraphCache), keyed by
   // sweep plan; owned
   void* loop_graphs = nullptr;
@@ -131,7 +133,7 @@ struct dynpr_context {
   dynpr_b200::DevBuf rank[2], contrib[2], flags_va, flags_np, flags_written,
       pend_low, pend_high, pend_flags, partials, perm_stage,
       tile_counts, red, stage_a, stage_b, stage_c, stage_d, stage_e, stage_f,
-      cub_tmp, tick, loopctl, layout_tmp, scratch64a, scratch64b, scratch32a, scratch32b, scratch8a, batch[4];
+      cub_tmp, tick, loopctl, layout_tmp, side_err, scratch64a, scratch64b, scratch32a, scratch32b, scratch8a, batch[4];
 };
 
 namespace dynpr_b200 {
@@ -289,6 +291,23 @@ inline int bits_for(uint64_t x) {
 dynpr_graph* new_graph_struct(dynpr_context* ctx, uint32_t n);
 dynpr_graph* make_graph(dynpr_context* ctx, uint32_t n, uint64_t m);
 void destroy_graph(dynpr_graph* g);
+
+// A host CSR uploaded with its targets' transfer + validation deferred to
+// the context's side stream (dynpr_static_pagerank_csr): the graph is usable
+// for anything that reads only its offsets until finish() has joined.
+struct DeferredCsr {
+  dynpr_context* ctx = nullptr;
+  dynpr_graph* g = nullptr;
+  unsigned* rowstart = nullptr;
+  unsigned long long* err = nullptr;
+  unsigned long long* host = nullptr;
+  bool pending = false;
+  void finish();
+  ~DeferredCsr();
+};
+cudaStream_t side_stream(dynpr_context* ctx);
+void upload_csr_deferred(dynpr_context* ctx, uint32_t n, const uint64_t* offsets, const uint32_t* targets,
+                         uint64_t m, cudaEvent_t after, DeferredCsr& d);
 void graph_apply_batch_impl(dynpr_context* ctx, const dynpr_graph* g,
                             const uint32_t* d_ds, const uint32_t* d_dd,
                             uint64_t nd, const uint32_t* d_is,

@@ -603,6 +603,7 @@ dynpr_status dynpr_context_destroy(dynpr_context* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    if (ctx->side) cudaStreamSynchronize(ctx->side);
     delete ctx->comm;
     ctx->comm = nullptr;
     if (ctx->ev_a) cudaEventDestroy(ctx->ev_a);
@@ -612,6 +613,8 @@ dynpr_status dynpr_context_destroy(dynpr_context* ctx) {
     delete static_cast<LoopGraphCache*>(ctx->loop_graphs);
     ctx->loop_graphs = nullptr;
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    if (ctx->side) cudaStreamDestroy(ctx->side);
+    if (ctx->ev_side) cudaEventDestroy(ctx->ev_side);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
   });
@@ -817,6 +820,45 @@ dynpr_status dynpr_static_pagerank(dynpr_context* ctx, const dynpr_graph* gT, co
     sp.gF = gF;
     sp.cfg = cfg;
     solve(ctx, sp, ranks_out, stats, observer, observer_user);
+  });
+}
+
+// staticPageRank(gT, gF, cfg) on host CSR arrays (the reference's by-value
+// call with freshly constructed graphs): gT is uploaded and validated first;
+// gF's offsets follow, and its targets -- which Static never reads -- are
+// uploaded and validated on the side stream while the solve runs.  Errors
+// keep the reference's order: graph construction (gT, then gF), then the
+// engine's own checks.
+dynpr_status dynpr_static_pagerank_csr(dynpr_context* ctx, uint32_t n, const uint64_t* offT, const uint32_t* tgtT,
+                                       const uint64_t* offF, const uint32_t* tgtF, uint64_t m,
+                                       const dynpr_config* cfg, double* ranks_out, dynpr_stats* stats,
+                                       dynpr_observer observer, void* observer_user) {
+  dynpr_graph* gT = nullptr;
+  const dynpr_status st = dynpr_graph_from_csr(ctx, n, offT, tgtT, m, &gT);
+  if (st != DYNPR_OK) return st;
+  struct Own {
+    dynpr_graph* g;
+    ~Own() { dynpr_graph_destroy(g); }
+  } own{gT};
+  return api_guard([&] {
+    bind_device(ctx);
+    if (!ctx->ev_side) DYNPR_CK(cudaEventCreateWithFlags(&ctx->ev_side, cudaEventDisableTiming));
+    DeferredCsr gF;
+    upload_csr_deferred(ctx, n, offF, tgtF, m, ctx->ev_side, gF);
+    try {
+      validate_config(cfg);
+      check_pair(gT, gF.g);
+      if (!ranks_out) invalid("null output array");
+    } catch (...) {
+      gF.finish();  // an invalid gF would have failed at construction, first
+      throw;
+    }
+    SolveSpec sp;
+    sp.gT = gT;
+    sp.gF = gF.g;
+    sp.cfg = cfg;
+    solve(ctx, sp, ranks_out, stats, observer, observer_user);
+    gF.finish();
   });
 }
 

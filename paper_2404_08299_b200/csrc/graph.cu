@@ -700,6 +700,121 @@ using namespace dynpr_b200;
 
 extern "C" {
 
+}  // extern "C"
+
+namespace dynpr_b200 {
+
+// CsrGraph constructor validation (graph.cpp:30-49) of a snapshot whose
+// arrays are (being) uploaded on stream `s`: err[0] first row whose offset
+// decreases, err[1] first bad edge, err[2] every-row-has-its-loop flag.
+// enqueue_csr_validation queues the kernels and the readback into `host`;
+// finish_csr_validation waits on `s` and throws the reference's messages
+// (re-scanning exactly the rows the reference would have scanned when the
+// offsets decrease).
+void enqueue_csr_validation(dynpr_context* ctx, dynpr_graph* g, uint32_t vlim, uint64_t elim, cudaStream_t s,
+                            unsigned long long* err, unsigned* rowstart, unsigned long long* host) {
+  const uint64_t m = g->m;
+  const uint64_t words = (m + 31) / 32 + 1;
+  const unsigned long long init[3] = {kNone, kNone, 1ull};  // loops flag = 1
+  std::memcpy(host, init, sizeof init);
+  DYNPR_CK(cudaMemcpyAsync(err, host, sizeof init, cudaMemcpyHostToDevice, s));
+  DYNPR_CK(cudaMemsetAsync(rowstart, 0, words * 4, s));
+  int* loops = reinterpret_cast<int*>(err + 2);
+  if (vlim) {
+    k_validate_rows<<<grid_for(vlim, 256, ctx->num_sms * 16), 256, 0, s>>>(g->off, g->tgt, vlim, m, rowstart, err,
+                                                                          loops);
+    check_launch();
+    count_launch(ctx);
+  }
+  if (elim) {
+    k_validate_edges<<<grid_for((elim + 3) / 4, 256, ctx->num_sms * 16), 256, 0, s>>>(g->tgt, elim, g->n, rowstart,
+                                                                                      err + 1);
+    check_launch();
+    count_launch(ctx);
+  }
+  DYNPR_CK(cudaMemcpyAsync(host, err, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+}
+
+void finish_csr_validation(dynpr_context* ctx, dynpr_graph* g, cudaStream_t s, unsigned long long* err,
+                           unsigned* rowstart, unsigned long long* host) {
+  DYNPR_CK(cudaStreamSynchronize(s));
+  unsigned long long h[3];
+  std::memcpy(h, host, sizeof h);
+  if (h[0] != kNone) {
+    // offsets decrease at v0: the reference scanned only the rows before it,
+    // whose edges are [0, off[v0]); rescan exactly those
+    const uint32_t v0 = (uint32_t)h[0];
+    uint64_t lim = 0;
+    DYNPR_CK(cudaMemcpy(&lim, g->off + v0, 8, cudaMemcpyDeviceToHost));
+    enqueue_csr_validation(ctx, g, v0, lim < g->m ? lim : g->m, s, err, rowstart, host);
+    DYNPR_CK(cudaStreamSynchronize(s));
+    std::memcpy(h, host, sizeof h);
+    h[0] = v0;
+  }
+  if (h[1] != kNone) {
+    if ((h[1] & 3) == 2) invalid("CsrGraph: target id out of range");
+    invalid("CsrGraph: target slices must be sorted and deduplicated");
+  }
+  if (h[0] != kNone) invalid("CsrGraph: offsets must be non-decreasing");
+  g->all_loops = g->n == 0 || (int)(h[2] & 0xffffffffu) == 1;
+}
+
+// Host-side part of the constructor checks: offsets.front() == 0 and
+// offsets.back() == targets.size().
+void check_csr_ends(uint32_t n, const uint64_t* offsets, uint64_t m) {
+  uint64_t first = 0, last = 0;
+  if (!offsets) invalid("CsrGraph: malformed offsets array");
+  if (is_device_ptr(offsets)) {
+    DYNPR_CK(cudaMemcpy(&first, offsets, 8, cudaMemcpyDeviceToHost));
+    DYNPR_CK(cudaMemcpy(&last, offsets + n, 8, cudaMemcpyDeviceToHost));
+  } else {
+    first = offsets[0];
+    last = offsets[n];
+  }
+  if (first != 0 || last != m) invalid("CsrGraph: malformed offsets array");
+}
+
+DeferredCsr::~DeferredCsr() {
+  if (pending && ctx && ctx->side) cudaStreamSynchronize(ctx->side);  // error path: the side work must end first
+  if (rowstart) pool_free(ctx, rowstart);
+  if (g) destroy_graph(g);
+}
+
+// Upload of a host CSR whose targets travel and are validated on the
+// context's side stream (after `after` fires), overlapping whatever the
+// main stream runs next; finish() joins and throws on invalid input.
+void upload_csr_deferred(dynpr_context* ctx, uint32_t n, const uint64_t* offsets, const uint32_t* targets,
+                         uint64_t m, cudaEvent_t after, DeferredCsr& d) {
+  check_csr_ends(n, offsets, m);
+  d.ctx = ctx;
+  d.g = make_graph(ctx, n, m);
+  d.rowstart = pool_alloc_n<unsigned>(ctx, (m + 31) / 32 + 1);
+  d.err = ctx->side_err.as<unsigned long long>(3);
+  d.host = reinterpret_cast<unsigned long long*>(static_cast<char*>(ctx->pinned) + 3072);
+  DYNPR_CK(cudaMemcpyAsync(d.g->off, offsets, ((size_t)n + 1) * 8, cudaMemcpyDefault, ctx->stream));
+  DYNPR_CK(cudaEventRecord(after, ctx->stream));  // the allocations and offsets are ordered before the side work
+  cudaStream_t side = side_stream(ctx);
+  DYNPR_CK(cudaStreamWaitEvent(side, after, 0));
+  if (m) DYNPR_CK(cudaMemcpyAsync(d.g->tgt, targets, m * 4, cudaMemcpyDefault, side));
+  enqueue_csr_validation(ctx, d.g, n, m, side, d.err, d.rowstart, d.host);
+  d.pending = true;
+}
+
+void DeferredCsr::finish() {
+  if (!pending) return;
+  pending = false;
+  finish_csr_validation(ctx, g, side_stream(ctx), err, rowstart, host);
+}
+
+cudaStream_t side_stream(dynpr_context* ctx) {
+  if (!ctx->side) DYNPR_CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+  return ctx->side;
+}
+
+}  // namespace dynpr_b200
+
+extern "C" {
+
 dynpr_status dynpr_graph_from_csr(dynpr_context* ctx, uint32_t n,
                                   const uint64_t* offsets,
                                   const uint32_t* targets, uint64_t m,
@@ -707,70 +822,22 @@ dynpr_status dynpr_graph_from_csr(dynpr_context* ctx, uint32_t n,
   return api_guard([&] {
     if (!ctx || !out) invalid("null argument");
     bind_device(ctx);
-    // offsets.front() == 0 && offsets.back() == targets.size()
-    uint64_t first = 0, last = 0;
-    if (!offsets) invalid("CsrGraph: malformed offsets array");
-    if (is_device_ptr(offsets)) {
-      DYNPR_CK(cudaMemcpy(&first, offsets, 8, cudaMemcpyDeviceToHost));
-      DYNPR_CK(cudaMemcpy(&last, offsets + n, 8, cudaMemcpyDeviceToHost));
-    } else {
-      first = offsets[0];
-      last = offsets[n];
-    }
-    if (first != 0 || last != m) invalid("CsrGraph: malformed offsets array");
+    check_csr_ends(n, offsets, m);
     dynpr_graph* g = make_graph(ctx, n, m);
     try {
       DYNPR_CK(cudaMemcpyAsync(g->off, offsets, ((size_t)n + 1) * 8, cudaMemcpyDefault, ctx->stream));
       if (m) DYNPR_CK(cudaMemcpyAsync(g->tgt, targets, m * 4, cudaMemcpyDefault, ctx->stream));
-      // err[0]: first bad vertex (offsets), err[1]: first bad edge, err[2]: loops flag
-      auto* err = scratch_u64(ctx, ctx->scratch64b, 3, kNone);
-      int* loops = reinterpret_cast<int*>(err + 2);
-      const uint64_t words = (m + 31) / 32 + 1;
-      unsigned* rowstart = pool_alloc_n<unsigned>(ctx, words);
-      unsigned long long h[3];
-      auto run = [&](uint32_t vlim, uint64_t elim) {
-        const unsigned long long init[3] = {kNone, kNone, 1ull};  // loops flag = 1
-        DYNPR_CK(cudaMemcpyAsync(ctx->pinned, init, sizeof init, cudaMemcpyHostToDevice, ctx->stream));
-        DYNPR_CK(cudaMemcpyAsync(err, ctx->pinned, sizeof init, cudaMemcpyHostToDevice, ctx->stream));
-        DYNPR_CK(cudaMemsetAsync(rowstart, 0, words * 4, ctx->stream));
-        if (vlim) {
-          k_validate_rows<<<grid_for(vlim, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(g->off, g->tgt, vlim, m,
-                                                                                          rowstart, err, loops);
-          check_launch();
-          count_launch(ctx);
-        }
-        if (elim) {
-          k_validate_edges<<<grid_for((elim + 3) / 4, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
-              g->tgt, elim, n, rowstart, err + 1);
-          check_launch();
-          count_launch(ctx);
-        }
-        DYNPR_CK(cudaMemcpyAsync(ctx->pinned, err, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
-        sync(ctx);
-        std::memcpy(h, ctx->pinned, sizeof h);
-      };
+      auto* err = ctx->scratch64b.as<unsigned long long>(3);
+      unsigned* rowstart = pool_alloc_n<unsigned>(ctx, (m + 31) / 32 + 1);
+      auto* host = static_cast<unsigned long long*>(ctx->pinned);
       try {
-        run(n, m);
-        if (h[0] != kNone) {
-          // offsets decrease at v0: the reference scanned only the rows
-          // before it, whose edges are [0, off[v0]); rescan exactly those
-          const uint32_t v0 = (uint32_t)h[0];
-          uint64_t lim = 0;
-          DYNPR_CK(cudaMemcpy(&lim, g->off + v0, 8, cudaMemcpyDeviceToHost));
-          run(v0, lim < m ? lim : m);
-          h[0] = v0;
-        }
+        enqueue_csr_validation(ctx, g, n, m, ctx->stream, err, rowstart, host);
+        finish_csr_validation(ctx, g, ctx->stream, err, rowstart, host);
       } catch (...) {
         pool_free(ctx, rowstart);
         throw;
       }
       pool_free(ctx, rowstart);
-      if (h[1] != kNone) {
-        if ((h[1] & 3) == 2) invalid("CsrGraph: target id out of range");
-        invalid("CsrGraph: target slices must be sorted and deduplicated");
-      }
-      if (h[0] != kNone) invalid("CsrGraph: offsets must be non-decreasing");
-      g->all_loops = n == 0 || (int)(h[2] & 0xffffffffu) == 1;
     } catch (...) {
       destroy_graph(g);
       throw;

@@ -203,3 +203,48 @@ def test_generate_random_batch_errors(dp):
         dp.generate_random_batch(g, 3, 0.0, 1)
     with pytest.raises(ValueError, match="insertFraction must be in"):
         dp.generate_random_batch(g, 3, 1.5, 1)
+
+
+def test_static_pagerank_csr_host_pair(dp, oracle_lib):
+    """dynpr_static_pagerank_csr: one call on a host CSR pair (gF's targets
+    uploaded + validated on a side stream during the solve) -- same ranks and
+    counters as constructing both graphs and calling the engine, and the
+    reference's error order (graph construction first, engine checks next)."""
+    import ctypes as C
+    from paper_2404_08299_b200 import _native as N
+    O = oracle_lib
+    from helpers import rand_pair
+    og, ogt = rand_pair(O, 61, 5000, 50000)
+    offF, tgtF = og.csr()
+    offT, tgtT = ogt.csr()
+    n, m = og.n, og.m
+    ctx = dp.default_context()
+    L = N.lib()
+
+    def run(oT, tT, oF, tF, cfg=None, nn=n, mm=m):
+        c = (cfg or dp.EngineConfig())._c()
+        r = np.zeros(max(nn, 1), np.float64)
+        st = N.Stats()
+        rc = L.dynpr_static_pagerank_csr(C.c_void_p(ctx.h), nn, oT.ctypes.data, tT.ctypes.data, oF.ctypes.data,
+                                         tF.ctypes.data, mm, C.byref(c), r.ctypes.data, C.byref(st), N.OBSERVER(0),
+                                         None)
+        return rc, r, st
+
+    rc, r, st = run(offT, tgtT, offF, tgtF)
+    assert rc == 0
+    ref = O.static(ogt, og)
+    assert st.iterations == ref.iterations and np.array_equal(r[:n], ref.ranks)
+    bad = tgtF.copy()
+    bad[offF[10]], bad[offF[10] + 1] = bad[offF[10] + 1], bad[offF[10]]  # unsorted slice in gF
+    rc, _, _ = run(offT, tgtT, offF, bad)
+    assert rc == N.DYNPR_INVALID_ARGUMENT and "sorted and deduplicated" in N.last_error()
+    rc, _, _ = run(offT, tgtT, offF, bad, cfg=dp.EngineConfig(damping_factor=2.0))
+    assert rc == N.DYNPR_INVALID_ARGUMENT and "sorted and deduplicated" in N.last_error()  # construction first
+    rc, _, _ = run(offT, tgtT, offF, tgtF, cfg=dp.EngineConfig(damping_factor=2.0))
+    assert rc == N.DYNPR_INVALID_ARGUMENT and "dampingFactor" in N.last_error()
+    badT = tgtT.copy()
+    badT[5] = n + 3
+    rc, _, _ = run(offT, badT, offF, tgtF)
+    assert rc == N.DYNPR_INVALID_ARGUMENT and "out of range" in N.last_error()
+    rc, r2, _ = run(offT, tgtT, offF, tgtF)  # the context is still healthy
+    assert rc == 0 and np.array_equal(r2[:n], ref.ranks)
