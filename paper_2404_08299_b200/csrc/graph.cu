@@ -265,12 +265,6 @@ __global__ void k_new_degrees(const uint64_t* off, uint32_t n,
     noff[v] = (off[v + 1] - off[v]) - ddel[v] + dins[v] + need[v];
   }
 }
-__global__ void k_list_touched(const uint8_t* touched, uint32_t n,
-                               uint32_t* list, unsigned* count) {
-  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
-       v += (uint64_t)gridDim.x * blockDim.x)
-    if (touched[v]) list[atomicAdd(count, 1u)] = (uint32_t)v;
-}
 
 // Untouched slices keep their content and only shift: a warp per 32-vertex
 // tile copies the whole contiguous range when no vertex of the tile is

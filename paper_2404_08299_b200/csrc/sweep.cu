@@ -176,10 +176,8 @@ __device__ __forceinline__ void finalize(const SweepArgs& a, uint32_t v, double 
   }
 }
 
-// Cache-policy loads.  Index streams and cold contributions bypass L1
-// (L1::no_allocate); the hot prefix of the relabelled contribution vector
-// (new ids < a.hot, the most-gathered vertices) is loaded evict_last so it
-// stays resident in L1 and its gathers never reach L2.
+// Index streams bypass L1 (L1::no_allocate) so the gathered contributions
+// -- the hot ones packed at the front of the relabelled vector -- keep it.
 __device__ __forceinline__ uint4 ld_idx4(const uint32_t* p) {
   uint4 v;
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -194,10 +192,8 @@ __device__ __forceinline__ uint4 ld_idx4(const uint32_t* p) {
 // served only ~15% of RMAT-24 gathers and its 1024-thread CTAs halved
 // occupancy; random 8-byte gathers top out near 288 G/s from L2
 // (profiles/microbench_gather.cu), which is what bounds this sweep.
-__device__ __forceinline__ double ld_contrib(const double* __restrict__ contrib, const double* s_hot, uint32_t u,
-                                             uint32_t hot, uint32_t self, double cself) {
-  (void)s_hot;
-  (void)hot;
+__device__ __forceinline__ double ld_contrib(const double* __restrict__ contrib, uint32_t u, uint32_t self,
+                                             double cself) {
   return u == self ? cself : __ldg(contrib + u);
 }
 
@@ -207,7 +203,7 @@ __device__ __forceinline__ double ld_contrib(const double* __restrict__ contrib,
 // (software pipelining); the adds stay in segment order.
 __device__ __forceinline__ double segment_sum(const uint32_t* __restrict__ sell, uint64_t base, unsigned lane,
                                               uint32_t len, uint32_t Lw, const double* __restrict__ contrib,
-                                              const double* s_hot, uint32_t hot, uint32_t self, double cself) {
+                                              uint32_t self, double cself) {
   const uint32_t* p = sell + base + 4u * lane;  // element k at p + 32*k (k % 4 == 0)
   const uint4 z = make_uint4(0, 0, 0, 0);
   double c = 0.0;
@@ -218,7 +214,7 @@ __device__ __forceinline__ double segment_sum(const uint32_t* __restrict__ sell,
     double x[8];
 #pragma unroll
     for (uint32_t q = 0; q < 8; ++q)
-      x[q] = (k + q < len) ? ld_contrib(contrib, s_hot, u[q], hot, self, cself) : 0.0;
+      x[q] = (k + q < len) ? ld_contrib(contrib, u[q], self, cself) : 0.0;
     a = (k + 8 < len) ? ld_idx4(p + 32ull * (k + 8)) : z;
     b = (k + 12 < len) ? ld_idx4(p + 32ull * (k + 12)) : z;
 #pragma unroll
@@ -265,7 +261,6 @@ constexpr int kSweepWarps = kSweepThreads / 32;
 template <bool FLAGGED, bool CLOSED>
 __device__ __forceinline__ void b_sweep_single(const SweepArgs& a) {
   if (a.done && *a.done) return;
-  const double* s_hot = nullptr;
   Acc acc;
   const unsigned lane = lane_id();
   const uint64_t nw = (uint64_t)gridDim.x * kSweepWarps;
@@ -286,7 +281,7 @@ __device__ __forceinline__ void b_sweep_single(const SweepArgs& a) {
       cself = a.contrib_prev[v];
     }
     double c = 0.0;
-    if (Lw) c = segment_sum(a.sell_s, a.sbase[s], lane, len, Lw, a.contrib_prev, s_hot, a.hot, v, cself);
+    if (Lw) c = segment_sum(a.sell_s, a.sbase[s], lane, len, Lw, a.contrib_prev, v, cself);
     bool pend = false, lowout = false;
     if (valid) {
       if (!aff) {
@@ -315,7 +310,6 @@ __global__ void __launch_bounds__(kSweepThreads, 5) k_sweep_single_c() {
 template <bool FLAGGED>
 __device__ __forceinline__ void b_sweep_mseg(const SweepArgs& a) {
   if (a.done && *a.done) return;
-  const double* s_hot = nullptr;
   const unsigned lane = lane_id();
   const uint64_t nw = (uint64_t)gridDim.x * kSweepWarps;
   for (uint64_t s = a.ms_lo + ((uint64_t)blockIdx.x * kSweepThreads + threadIdx.x) / 32; s < a.ms_hi; s += nw) {
@@ -330,7 +324,7 @@ __device__ __forceinline__ void b_sweep_mseg(const SweepArgs& a) {
     const uint32_t Lw = __reduce_max_sync(kFull, len);
     if (!Lw) continue;
     // (a multi vertex's self-loop is one gather among >256: not special-cased)
-    const double c = segment_sum(a.sell_m, a.mbase[s], lane, len, Lw, a.contrib_prev, s_hot, a.hot, 0xffffffffu,
+    const double c = segment_sum(a.sell_m, a.mbase[s], lane, len, Lw, a.contrib_prev, 0xffffffffu,
                                  0.0);
     if (len) a.partials[seg] = c;
   }
@@ -512,7 +506,7 @@ __device__ __forceinline__ double segment_sum_deep(const uint32_t* __restrict__ 
       const uint32_t u[4] = {ix[j].x, ix[j].y, ix[j].z, ix[j].w};
 #pragma unroll
       for (int q = 0; q < 4; ++q)
-        x[4 * j + q] = (k + 4 * j + q < len) ? ld_contrib(contrib, nullptr, u[q], 0, self, cself) : 0.0;
+        x[4 * j + q] = (k + 4 * j + q < len) ? ld_contrib(contrib, u[q], self, cself) : 0.0;
     }
 #pragma unroll
     for (int j = 0; j < Q; ++j) ix[j] = (k + D + 4 * j < len) ? ld_idx4(p + 32ull * (k + D + 4 * j)) : z;
@@ -1146,13 +1140,6 @@ SweepArgs layout_args(const Layout* L, double* partials) {
   a.trace = trace;
   a.mcount = L->mcount;
   a.ss_heavy = L->n_hslices;
-  // Hot prefix held in L1: ~200 KB of L1 per SM (shared-memory carveout 0)
-  // = 25,600 contributions; DYNPR_HOT overrides for tuning.
-  static const uint32_t hot_default = [] {
-    const char* e = std::getenv("DYNPR_HOT");
-    return e ? (uint32_t)std::strtoul(e, nullptr, 10) : 24576u;
-  }();
-  a.hot = L->n < hot_default ? L->n : hot_default;
   a.v_lo = 0;
   a.v_hi = L->n;
   a.ss_lo = 0;

@@ -41,7 +41,6 @@ struct SweepArgs {
   uint32_t* mcount;      // per multi vertex chunk-completion counters (fused sweep)
   uint64_t ss_heavy;     // single slices [0, ss_heavy) are heavy (layout n_hslices)
   int trace;     // debug: record per-warp timelines of the fused sweep (DYNPR_TRACE)
-  uint32_t hot;  // new ids < hot: contributions kept L1-resident (evict_last)
   // iteration state
   double alpha, teleport, tf, tp;
   const double* rank_prev;
