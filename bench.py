@@ -311,7 +311,7 @@ def run_ours(args, world, rank, local):
         return st
 
     def dfp_dev(gF, gT, b):
-        (ds, dd), (is_, id_) = b.deletions, b.insertions
+        ds, dd, is_, id_ = b.deletions.src, b.deletions.dst, b.insertions.src, b.insertions.dst
         st = N.Stats()
         dp._check(L.dynpr_dynamic_frontier(
             N.C.c_void_p(ctx.h), N.C.c_void_p(gF.h), N.C.c_void_p(gT.h), dp._p(ds), dp._p(dd), len(ds),

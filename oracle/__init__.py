@@ -92,7 +92,9 @@ def _u8(a) -> np.ndarray:
 
 
 def split_edges(edges):
-    """list of (u, v) | (src, dst) arrays -> (src uint32, dst uint32)."""
+    """list of (u, v) | (src, dst) arrays | object with .src/.dst -> (src uint32, dst uint32)."""
+    if hasattr(edges, "src") and hasattr(edges, "dst"):
+        return _u32(edges.src), _u32(edges.dst)
     if isinstance(edges, tuple) and len(edges) == 2 and isinstance(edges[0], np.ndarray):
         return _u32(edges[0]), _u32(edges[1])
     arr = np.asarray(list(edges), dtype=np.uint64).reshape(-1, 2)

@@ -27,7 +27,7 @@ from . import _native as N
 from ._native import NativeUnavailable
 
 __all__ = [
-    "BatchUpdate", "BatchApplyStats", "Context", "CsrGraph", "DegreePartition", "EngineConfig",
+    "BatchUpdate", "BatchApplyStats", "EdgeArray", "Context", "CsrGraph", "DegreePartition", "EngineConfig",
     "PartitionStrategy", "RankMode", "RankResult", "SizingError", "NativeUnavailable",
     "add_self_loops", "apply_batch", "apply_batch_pair", "build_csr", "default_context",
     "dynamic_frontier", "dynamic_frontier_from_flags", "expand_affected", "initial_affected",
@@ -95,6 +95,49 @@ class RankResult:  # engine.hpp:16-22
 class DegreePartition:  # partition.hpp:12-15
     order: np.ndarray
     low_count: int
+
+
+class EdgeArray:
+    """An EdgeList (graph.hpp:10, a list of (source, target) pairs in the
+    reference's Python binding) held as two uint32 arrays: it compares,
+    indexes and iterates like the reference's list of tuples, while the
+    engines take `src` / `dst` without a conversion."""
+
+    __slots__ = ("src", "dst")
+
+    def __init__(self, src, dst):
+        self.src = np.ascontiguousarray(np.asarray(src, dtype=np.uint32).reshape(-1))
+        self.dst = np.ascontiguousarray(np.asarray(dst, dtype=np.uint32).reshape(-1))
+        if len(self.src) != len(self.dst):
+            raise ValueError("EdgeArray: src and dst lengths differ")
+
+    def __len__(self):
+        return len(self.src)
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return EdgeArray(self.src[i], self.dst[i])
+        return (int(self.src[i]), int(self.dst[i]))
+
+    def __iter__(self):
+        return iter(zip(self.src.tolist(), self.dst.tolist()))
+
+    def tolist(self):
+        return list(zip(self.src.tolist(), self.dst.tolist()))
+
+    def __eq__(self, other):
+        if isinstance(other, EdgeArray):
+            return np.array_equal(self.src, other.src) and np.array_equal(self.dst, other.dst)
+        try:
+            return self.tolist() == [tuple(x) for x in other]
+        except TypeError:
+            return NotImplemented
+
+    __hash__ = None
+
+    def __repr__(self):
+        head = ", ".join(f"({u}, {v})" for u, v in zip(self.src[:4].tolist(), self.dst[:4].tolist()))
+        return f"EdgeArray([{head}{', ...' if len(self) > 4 else ''}], len={len(self)})"
 
 
 @dataclass
@@ -272,7 +315,9 @@ def _arr(a, dtype) -> np.ndarray:
 
 
 def _edges(edges):
-    """[(u, v), ...] | (src, dst) arrays | (k, 2) array -> uint32 src, dst."""
+    """EdgeArray | [(u, v), ...] | (src, dst) arrays | (k, 2) array -> uint32 src, dst."""
+    if isinstance(edges, EdgeArray):
+        return edges.src, edges.dst
     if isinstance(edges, tuple) and len(edges) == 2 and not np.isscalar(edges[0]) and \
             isinstance(edges[0], np.ndarray):
         return _arr(edges[0], np.uint32), _arr(edges[1], np.uint32)
@@ -513,8 +558,8 @@ def generate_random_batch(g: CsrGraph, total_size: int, insert_fraction: float =
     _check(N.lib().dynpr_generate_random_batch(C.c_void_p(g.ctx.h), C.c_void_p(g.h), int(total_size),
                                                float(insert_fraction), int(seed), _p(is_), _p(id_),
                                                C.byref(ni), _p(ds), _p(dd), C.byref(nd)))
-    return BatchUpdate(deletions=(ds[: nd.value].copy(), dd[: nd.value].copy()),
-                       insertions=(is_[: ni.value].copy(), id_[: ni.value].copy()))
+    return BatchUpdate(deletions=EdgeArray(ds[: nd.value], dd[: nd.value]),
+                       insertions=EdgeArray(is_[: ni.value], id_[: ni.value]))
 
 
 # ---- primitives ------------------------------------------------------------------

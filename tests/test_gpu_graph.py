@@ -193,8 +193,8 @@ def test_generate_random_batch_matches_reference(dp, oracle_lib, scale, frac, in
     assert dp.derive_seed(seed, 5) == s
     dels, inss = oracle_lib.generate_random_batch(og, size, ins, s)
     b = dp.generate_random_batch(dp.rmat_graph(scale), size, ins, s)
-    assert np.array_equal(b.deletions[0], dels[0]) and np.array_equal(b.deletions[1], dels[1])
-    assert np.array_equal(b.insertions[0], inss[0]) and np.array_equal(b.insertions[1], inss[1])
+    assert np.array_equal(b.deletions.src, dels[0]) and np.array_equal(b.deletions.dst, dels[1])
+    assert np.array_equal(b.insertions.src, inss[0]) and np.array_equal(b.insertions.dst, inss[1])
 
 
 def test_generate_random_batch_errors(dp):
