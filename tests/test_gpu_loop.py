@@ -114,3 +114,28 @@ def test_device_resident_arrays(dp, oracle_lib):
         dp.naive_dynamic(gt2, g2, out.float())
     with pytest.raises(ValueError, match="exactly vertex_count"):
         dp.static_pagerank(gt, g, out=out[:10])
+
+
+@pytest.mark.parametrize("threshold", [0, 1, 300, 1000])
+@pytest.mark.parametrize("sweep", ["fused", "split"])
+def test_engines_any_low_degree_threshold(dp, oracle_lib, monkeypatch, threshold, sweep):
+    """lowDegreeThreshold moves the flat / 256-chunk accumulation boundary
+    (rank.cpp:42-75: flat when in-degree <= T) and the expansion split; every
+    value must stay bitwise, including T > 256 (single segments longer than a
+    chunk) on an RMAT graph whose hubs exceed T."""
+    import oracle
+    monkeypatch.setenv("DYNPR_SWEEP", sweep)
+    O = oracle_lib
+    src, dst = O.rmat_edges(13, 16 << 13)
+    og = O.add_self_loops(O.build_csr((src, dst), 1 << 13))
+    ogt = O.transpose(og)
+    ocfg = oracle.default_config(low_degree_threshold=threshold)
+    cfg = dp.EngineConfig(low_degree_threshold=threshold)
+    base = O.static(ogt, og, ocfg)
+    dels, ins = O.generate_random_batch(og, 120, 0.8, 3)
+    og2, _, _ = O.apply_batch(og, dels, ins)
+    ogt2 = O.transpose(og2)
+    g2, gt2 = to_dev(dp, og2), to_dev(dp, ogt2)
+    _same(dp.static_pagerank(gt2, g2, cfg), O.static(ogt2, og2, ocfg))
+    _same(dp.dynamic_frontier(g2, gt2, dels, ins, base.ranks, cfg, True),
+          O.dynamic_frontier(og2, ogt2, dels, ins, base.ranks, ocfg, pruning=True))
