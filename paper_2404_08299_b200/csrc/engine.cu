@@ -167,8 +167,7 @@ LoopGraph& loop_graph(dynpr_context* ctx, const SweepPlan& plan, int frontier, L
   DYNPR_CK(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
   try {
     for (int k = 0; k < 2; ++k) {
-      DYNPR_CK(cudaMemsetAsync(red, 0, sizeof(SweepRed), st));
-      launch_sweep_ind(ctx, plan, k, tick);
+      launch_sweep_ind(ctx, plan, k, tick);  // the record is zero: before the launch, then k_loop_end
       launch_loop_end(ctx, dc, red, cond, k == 1);
       if (frontier) {
         launch_expand_ind(ctx, k, &dc->pend_low, &dc->expand);
@@ -231,6 +230,7 @@ void run_device_loop(dynpr_context* ctx, const SolveSpec& sp, const SweepArgs& a
   std::memcpy(stage + 1024, &h, sizeof h);
   std::memcpy(stage + 2048, half, sizeof half);
   DYNPR_CK(cudaMemcpyAsync(dc, stage + 1024, sizeof h, cudaMemcpyHostToDevice, st));
+  DYNPR_CK(cudaMemsetAsync(red, 0, sizeof(SweepRed), st));
   upload_loop_args(ctx, reinterpret_cast<const SweepArgs*>(stage + 2048));
   DYNPR_CK(cudaGraphLaunch(lg.exec, st));
   DYNPR_CK(cudaMemcpyAsync(stage + 1024, dc, sizeof h, cudaMemcpyDeviceToHost, st));

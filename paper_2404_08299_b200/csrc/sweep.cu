@@ -661,6 +661,9 @@ __device__ __forceinline__ void fused_body(const SweepArgs& a) {
   }
   if (a.npeers) __threadfence_system();  // peer stores visible before the team barrier
   block_reduce_commit(acc, a.red);
+  // every warp of the block is past its last grab: the block's heavy-item
+  // counter is zero again for the next sweep (no memset per sweep)
+  if (threadIdx.x == 0) a.tick_sm[blockIdx.x] = 0;
 }
 
 // 16-deep heavy chains at 4 CTAs per SM.  (A 5-CTA, 8-deep variant was
@@ -944,9 +947,10 @@ __global__ void k_expand_high_c(const unsigned* counts, const int* gate) {
 }
 
 // ---- device-driven loop bookkeeping (engine.cpp:71-92) --------------------------------
-__global__ void k_loop_end(LoopCtl* c, const SweepRed* red, cudaGraphConditionalHandle h, int set_cond) {
+__global__ void k_loop_end(LoopCtl* c, SweepRed* red, cudaGraphConditionalHandle h, int set_cond) {
   if (!c->done) {
     const SweepRed r = *red;
+    *red = SweepRed{};  // zeroed for the next sweep (no memset node per iteration)
     const double delta = __longlong_as_double((long long)r.delta_bits);
     c->iterations += 1;
     c->affected += c->flagged ? r.processed : c->n;
@@ -1309,7 +1313,7 @@ static void launch_sweep_c(dynpr_context* ctx, const SweepPlan& p, uint32_t* tic
   do {                                                                                           \
     if (!p.split) {                                                                              \
       if (p.g_fused) {                                                                           \
-        DYNPR_CK(cudaMemsetAsync(tick, 0, kMaxBlocks * sizeof(uint32_t), st));                   \
+        (void)tick; /* zero between sweeps: each block resets its own counter */                \
         k_sweep_fused_c<F, C, H><<<p.g_fused, kSweepThreads, 0, st>>>();                         \
         ++launched;                                                                              \
       }                                                                                          \
@@ -1365,10 +1369,16 @@ void upload_loop_args(dynpr_context* ctx, const SweepArgs* host_pinned_half2) {
                                    ctx->stream));
 }
 
-uint32_t* sweep_tick(dynpr_context* ctx) { return ctx->tick.as<uint32_t>(kMaxBlocks); }
+uint32_t* sweep_tick(dynpr_context* ctx) {
+  if (!ctx->tick.p) {  // zeroed once; the fused sweep leaves it zero
+    uint32_t* t = ctx->tick.as<uint32_t>(kMaxBlocks);
+    DYNPR_CK(cudaMemsetAsync(t, 0, ctx->tick.cap, ctx->stream));
+  }
+  return ctx->tick.as<uint32_t>(kMaxBlocks);
+}
 
 void prepare_sweep_launch(dynpr_context* ctx) {
-  ctx->tick.as<uint32_t>(kMaxBlocks);
+  sweep_tick(ctx);
   persistent_grid(ctx, k_sweep_fused<false, false>, 1);
   persistent_grid(ctx, k_sweep_fused<true, false>, 1);
   persistent_grid(ctx, k_sweep_fused<false, true>, 1);
@@ -1443,7 +1453,7 @@ void launch_expand(dynpr_context* ctx, const uint64_t* off, const uint32_t* tgt,
   }
 }
 
-void launch_loop_end(dynpr_context* ctx, LoopCtl* c, const SweepRed* red, cudaGraphConditionalHandle h,
+void launch_loop_end(dynpr_context* ctx, LoopCtl* c, SweepRed* red, cudaGraphConditionalHandle h,
                      int set_cond) {
   k_loop_end<<<1, 1, 0, ctx->stream>>>(c, red, h, set_cond);
   check_launch();

@@ -86,7 +86,7 @@ struct LoopCtl {
 // One iteration's bookkeeping (single thread): count, delta, convergence,
 // max-iterations, expansion direction; `set_cond` also sets the WHILE
 // node's condition to !done.
-void launch_loop_end(dynpr_context* ctx, LoopCtl* c, const SweepRed* red, cudaGraphConditionalHandle h,
+void launch_loop_end(dynpr_context* ctx, LoopCtl* c, SweepRed* red, cudaGraphConditionalHandle h,
                      int set_cond);
 // Push expansion with device-resident list sizes (counts[0] low, counts[1]
 // high), optionally gated on *gate == kExpandPush; fixed grids.
