@@ -269,10 +269,21 @@ __global__ void k_new_degrees(const uint64_t* off, uint32_t n,
 // Untouched slices keep their content and only shift: a warp per 32-vertex
 // tile copies the whole contiguous range when no vertex of the tile is
 // touched (the common case), else slice by slice skipping touched ones.
-// Copy of one CSR row range [b, e) to d.. with 8 loads in flight per lane
-// (the source and destination offsets differ by an arbitrary shift, so the
-// copy stays 4-byte granular; the depth gives the memory-level parallelism).
-__device__ __forceinline__ void warp_copy_range(const uint32_t* __restrict__ tgt, uint32_t* __restrict__ ntgt,
+// Copy of one CSR row range [b, e) to d..: 16-byte stores at 16-byte
+// aligned destinations, the source realigned in registers -- each lane loads
+// one aligned 16-byte source block, takes its neighbour's with a shuffle and
+// funnels the four words the destination block needs (the source/destination
+// shift is arbitrary: it is the running balance of inserted and deleted
+// edges).  Heads, tails and short ranges go 4 bytes at a time.
+__device__ __forceinline__ uint4 funnel4(uint4 a, uint4 b, unsigned r) {
+  switch (r) {
+    case 1: return make_uint4(a.y, a.z, a.w, b.x);
+    case 2: return make_uint4(a.z, a.w, b.x, b.y);
+    case 3: return make_uint4(a.w, b.x, b.y, b.z);
+    default: return a;
+  }
+}
+__device__ __forceinline__ void warp_copy_words(const uint32_t* __restrict__ tgt, uint32_t* __restrict__ ntgt,
                                                 uint64_t b, uint64_t e, uint64_t d, unsigned lane) {
   for (uint64_t i = b + lane; i < e; i += 32 * 8) {
     uint32_t x[8];
@@ -282,6 +293,48 @@ __device__ __forceinline__ void warp_copy_range(const uint32_t* __restrict__ tgt
     for (int q = 0; q < 8; ++q)
       if (i + 32 * q < e) __stcs(ntgt + d + (i + 32 * q - b), x[q]);
   }
+}
+__device__ __forceinline__ void warp_copy_range(const uint32_t* __restrict__ tgt, uint32_t* __restrict__ ntgt,
+                                                uint64_t b, uint64_t e, uint64_t d, unsigned lane) {
+  if (e - b < 512) {
+    warp_copy_words(tgt, ntgt, b, e, d, lane);
+    return;
+  }
+  const uint64_t head = (4 - (d & 3)) & 3;  // words until the destination is 16-byte aligned
+  const uint64_t S = b + head, D = d + head;
+  const unsigned r = (unsigned)(S & 3);
+  const uint64_t A = S - r;  // aligned source block of the first destination block
+  // vector blocks j with source blocks j and j + 1 both inside [A, e)
+  const uint64_t nblk = (e - A) / 4 >= 1 ? (e - A) / 4 - 1 : 0;
+  const uint4* src4 = reinterpret_cast<const uint4*>(tgt + A);
+  uint4* dst4 = reinterpret_cast<uint4*>(ntgt + D);
+  if (lane < head) ntgt[d + lane] = tgt[b + lane];
+  constexpr int U = 4;  // blocks in flight per lane (2 KB per warp)
+  for (uint64_t j0 = 0; j0 < nblk; j0 += 32 * U) {
+    uint4 a[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      const uint64_t j = j0 + 32 * q + lane;
+      a[q] = j < nblk ? __ldcs(src4 + j) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      const uint64_t j = j0 + 32 * q + lane;
+      // block j + 1: the next lane's block, lane 0's of the next group for
+      // lane 31; loaded directly at the end of the round or of the range
+      const unsigned srcl = (lane + 1) & 31;
+      const uint4 from = (lane == 0 && q + 1 < U) ? a[q + 1 < U ? q + 1 : q] : a[q];  // lane 31 reads lane 0's
+      uint4 nx;
+      nx.x = __shfl_sync(0xffffffffu, from.x, srcl);
+      nx.y = __shfl_sync(0xffffffffu, from.y, srcl);
+      nx.z = __shfl_sync(0xffffffffu, from.z, srcl);
+      nx.w = __shfl_sync(0xffffffffu, from.w, srcl);
+      if (j < nblk && ((lane == 31 && q + 1 == U) || j + 1 >= nblk)) nx = __ldcs(src4 + j + 1);
+      if (j < nblk) __stcs(dst4 + j, funnel4(a[q], nx, r));
+    }
+  }
+  // tail: the words after the last vector block
+  warp_copy_words(tgt, ntgt, S + 4 * nblk, e, D + 4 * nblk, lane);
 }
 
 // Rows without batch entries keep their slices: warp per 32-vertex tile,
