@@ -126,6 +126,7 @@ struct dynpr_context {
   void* pinned = nullptr;
   cudaStream_t side = nullptr;  // deferred uploads / validation (created on first use)
   cudaEvent_t ev_side = nullptr;
+  cudaEvent_t ev_rec[2] = {nullptr, nullptr};  // speculative team loop: per-record readiness
   // instantiated device-loop graphs (engine.cu LoopGraphCache), keyed by
   // sweep plan; owned
   void* loop_graphs = nullptr;

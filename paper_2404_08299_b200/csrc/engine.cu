@@ -378,7 +378,61 @@ void solve(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynpr_sta
     run_device_loop(ctx, sp, a, R, CB, L, red, res);
     cur = res.iterations & 1;
   }
-  for (int iter = 0; !device_loop && iter < c.max_iterations; ++iter) {
+  // Multi-GPU team, no observer / profiling: the host-driven loop runs one
+  // iteration ahead -- iteration k+1 (sweep, collectives, pull expansion) is
+  // enqueued before iteration k's record is read back, so no host round trip
+  // sits between two sweeps.  Safe because nothing enqueued depends on a host
+  // decision: teams always expand by pull, and an iteration enqueued after
+  // convergence only overwrites the buffers of the iterate before last (the
+  // result R[iterations & 1] is untouched; flags are not results).  The
+  // stream-ordered record all-reduce stays the team barrier of the fused
+  // exchange.  Every rank enqueues the same sequence of collectives.
+  const bool speculative = !device_loop && dist && !obs && !ctx->profiling;
+  if (speculative) {
+    for (int k = 0; k < 2; ++k)
+      if (!ctx->ev_rec[k]) DYNPR_CK(cudaEventCreateWithFlags(&ctx->ev_rec[k], cudaEventDisableTiming));
+    auto* slot = reinterpret_cast<SweepRed*>(static_cast<char*>(ctx->pinned) + 512);  // 2 records
+    auto enqueue = [&](int k) {
+      SweepRed* rk = red + (k & 1);
+      const int cu = k & 1;
+      DYNPR_CK(cudaMemsetAsync(rk, 0, sizeof(SweepRed), st));
+      SweepArgs ak = a;
+      ak.red = rk;
+      ak.rank_prev = R[cu];
+      ak.rank_cur = R[cu ^ 1];
+      ak.contrib_prev = CB[cu];
+      ak.contrib_cur = CB[cu ^ 1];
+      ak.npeers = 0;
+      if (fused)
+        for (int q = 0; q < comm->world; ++q)
+          if (q != comm->rank) ak.peer_cur[ak.npeers++] = ctx->peer_cb[cu ^ 1][q];
+      launch_sweep(ctx, ak, sp.flagged, sp.closed);
+      comm->allreduce_red(rk, st);
+      if (!fused) comm->allgatherv(CB[cu ^ 1], off_c.data(), st);
+      if (sp.flagged && !sp.traversal) comm->allgatherv(np, off_f.data(), st);
+      DYNPR_CK(cudaMemcpyAsync(slot + (k & 1), rk, sizeof(SweepRed), cudaMemcpyDeviceToHost, st));
+      DYNPR_CK(cudaEventRecord(ctx->ev_rec[k & 1], st));
+      if (sp.flagged && !sp.traversal) launch_pull_expand(ctx, ak);
+    };
+    enqueue(0);
+    for (int iter = 0; iter < c.max_iterations; ++iter) {
+      if (iter + 1 < c.max_iterations) enqueue(iter + 1);
+      DYNPR_CK(cudaEventSynchronize(ctx->ev_rec[iter & 1]));
+      SweepRed r;
+      std::memcpy(&r, slot + (iter & 1), sizeof r);
+      const double delta = bits_to_double(r.delta_bits);
+      res.iterations = iter + 1;
+      res.affected_vertex_iterations += sp.flagged ? r.processed : (uint64_t)n;
+      res.processed_edges += r.edges;
+      res.final_delta = delta;
+      if (!c.convergence_check_disabled && delta <= c.iteration_tolerance) {
+        res.converged = 1;
+        break;
+      }
+    }
+    cur = res.iterations & 1;
+  }
+  for (int iter = 0; !device_loop && !speculative && iter < c.max_iterations; ++iter) {
     DYNPR_CK(cudaMemsetAsync(red, 0, sizeof(SweepRed), st));
     if (obs && sp.flagged) {
       uint8_t* snap = obs_flags + n;  // owned entries are current on each rank
@@ -615,6 +669,8 @@ dynpr_status dynpr_context_destroy(dynpr_context* ctx) {
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->side) cudaStreamDestroy(ctx->side);
     if (ctx->ev_side) cudaEventDestroy(ctx->ev_side);
+    for (auto& e : ctx->ev_rec)
+      if (e) cudaEventDestroy(e);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
   });

@@ -140,3 +140,36 @@ def test_partitioned_observer_sees_full_iterates(dp, oracle_lib):
         assert len(seen) == len(seen_single)
         for a, b in zip(seen, seen_single):
             assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("fused", [False, True], ids=["allgather", "fused-peer-stores"])
+@pytest.mark.parametrize("max_it,check_off", [(1, False), (2, False), (5, True), (6, True), (500, False)])
+def test_team_speculative_loop_limits(dp, oracle_lib, fused, max_it, check_off):
+    """The team loop enqueues iteration k+1 before reading iteration k's
+    record: every exit (convergence on either parity, max iterations, check
+    disabled) must still return exactly the single-GPU result."""
+    O = oracle_lib
+    og, ogt = rand_pair(O, 29, 4000, 50000)
+    off, tgt = og.csr()
+    n = og.n
+    dels, ins = O.generate_random_batch(og, 40, 0.8, 11)
+    og2, _, _ = O.apply_batch(og, dels, ins)
+    off2, tgt2 = og2.csr()
+    cfg = dp.EngineConfig(max_iterations=max_it, convergence_check_disabled=check_off)
+    g = dp.CsrGraph.from_csr(n, off, tgt)
+    base = dp.static_pagerank(dp.transpose(g), g)
+    g2 = dp.CsrGraph.from_csr(n, off2, tgt2)
+    gt2 = dp.transpose(g2)
+    single = {"static": dp.static_pagerank(gt2, g2, cfg),
+              "dfp": dp.dynamic_frontier(g2, gt2, dels, ins, base.ranks, cfg, True)}
+
+    def fn(ctx, r):
+        h2 = dp.CsrGraph.from_csr(n, off2, tgt2, ctx=ctx)
+        ht2 = dp.transpose(h2)
+        return {"static": dp.static_pagerank(ht2, h2, cfg),
+                "dfp": dp.dynamic_frontier(h2, ht2, dels, ins, base.ranks, cfg, True)}
+
+    out, _ = run_team(dp, 3, fn, fused_n=n if fused else 0)
+    for r in range(3):
+        for k in single:
+            same(out[r][k], single[k])
