@@ -416,7 +416,10 @@ def run_ours(args, world, rank, local):
             "dfp": {"ms_per_solve": dfp_ms, "iterations": statistics.mean(rec["dfp_it"]),
                     "affected_vertex_iterations": statistics.mean(rec["dfp_aff"]),
                     "processed_gteps": sum(rec["dfp_edges"]) / (sum(rec["dfp_ms"]) * 1e-3) / 1e9,
-                    "speedup_vs_static": st_ms / dfp_ms},
+                    "speedup_vs_static": st_ms / dfp_ms,
+                    "speedup_incl_ingest": st_ms / (dfp_ms + statistics.mean(rec["ingest_ms"])),
+                    "note": "speedup_incl_ingest charges DF-P with the batch ingest (applyBatch pair + engine "
+                            "layout) that the reference's timed region excludes (harness.cpp:203-204)"},
             "ingest": {"ms_per_batch": statistics.mean(rec["ingest_ms"]),
                        "layout_ms": statistics.mean(rec["layout_ms"]),
                        "note": "applyBatch on forward + transpose + engine layout of the new snapshot "
