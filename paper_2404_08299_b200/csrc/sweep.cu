@@ -38,6 +38,7 @@
 // pending in-neighbour) when pushing would touch more edges.  Both produce
 // exactly vertexAffected |= out(pending).
 #include <cstdlib>
+#include <mutex>
 #include <string>
 #include <utility>
 
@@ -1069,6 +1070,8 @@ template <class K>
 unsigned persistent_grid(dynpr_context* ctx, K kernel, uint64_t work_blocks) {
   static const void* keys[32] = {};
   static int vals[32] = {};
+  static std::mutex lock;  // contexts on several host threads (LocalTeam, concurrent solves)
+  std::lock_guard<std::mutex> guard(lock);
   int per_sm = -1;
   for (int i = 0; i < 32 && keys[i]; ++i)
     if (keys[i] == (const void*)kernel) per_sm = vals[i];

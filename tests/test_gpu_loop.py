@@ -139,3 +139,38 @@ def test_engines_any_low_degree_threshold(dp, oracle_lib, monkeypatch, threshold
     _same(dp.static_pagerank(gt2, g2, cfg), O.static(ogt2, og2, ocfg))
     _same(dp.dynamic_frontier(g2, gt2, dels, ins, base.ranks, cfg, True),
           O.dynamic_frontier(og2, ogt2, dels, ins, base.ranks, ocfg, pruning=True))
+
+
+def test_concurrent_contexts_device_loops(dp, oracle_lib):
+    """Independent contexts solving on separate host threads (reference
+    SPEC: distinct instances on distinct graphs may run concurrently): the
+    device loop's constant-bank argument slots are serialised per device, and
+    every result stays bitwise."""
+    import threading
+    O = oracle_lib
+    cases = []
+    for seed in (61, 62, 63, 64):
+        og, ogt = rand_pair(O, seed, 3000, 30000)
+        cases.append((og, ogt, O.static(ogt, og)))
+    out = [None] * len(cases)
+    errors = []
+
+    def work(i):
+        try:
+            ctx = dp.Context(0)
+            og, ogt, _ = cases[i]
+            g = dp.CsrGraph.from_csr(og.n, *og.csr(), ctx=ctx)
+            gt = dp.CsrGraph.from_csr(ogt.n, *ogt.csr(), ctx=ctx)
+            out[i] = [dp.static_pagerank(gt, g) for _ in range(3)]
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(e)
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(len(cases))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors
+    for (og, ogt, ref), res in zip(cases, out):
+        for r in res:
+            _same(r, ref)
