@@ -1068,17 +1068,18 @@ __global__ void k_l1_final(const double* partials, uint64_t nb, double* out) {
 // Persistent grid: resident blocks per SM x SMs (queried once per kernel).
 template <class K>
 unsigned persistent_grid(dynpr_context* ctx, K kernel, uint64_t work_blocks) {
-  static const void* keys[32] = {};
-  static int vals[32] = {};
+  constexpr int kSlots = 128;  // > the 36 persistent kernel instantiations
+  static const void* keys[kSlots] = {};
+  static int vals[kSlots] = {};
   static std::mutex lock;  // contexts on several host threads (LocalTeam, concurrent solves)
   std::lock_guard<std::mutex> guard(lock);
   int per_sm = -1;
-  for (int i = 0; i < 32 && keys[i]; ++i)
+  for (int i = 0; i < kSlots && keys[i]; ++i)
     if (keys[i] == (const void*)kernel) per_sm = vals[i];
   if (per_sm < 0) {
     int b = 0;
-    // these kernels use ~200 B of shared memory: give the SM's unified
-    // L1/shared SRAM to L1 (it holds the hot contribution prefix)
+    // these kernels use little shared memory: give the SM's unified
+    // L1/shared SRAM to L1 (it holds the hot contributions)
     cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
     cudaGetLastError();
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, kThreads, 0) != cudaSuccess || b < 1) {
@@ -1086,7 +1087,7 @@ unsigned persistent_grid(dynpr_context* ctx, K kernel, uint64_t work_blocks) {
       b = 1;
     }
     per_sm = b;
-    for (int i = 0; i < 32; ++i)
+    for (int i = 0; i < kSlots; ++i)
       if (!keys[i]) {
         keys[i] = (const void*)kernel;
         vals[i] = b;
