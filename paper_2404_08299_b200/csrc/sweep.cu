@@ -467,7 +467,7 @@ __global__ void __launch_bounds__(kThreads) k_sweep_mfinal_c() {
 //    the partials in chunk order (rank.cpp:72) with a warp-wide load and a
 //    shuffle-broadcast sequential sum, and runs the epilogue.
 // Every vertex's sum and epilogue are exactly those of the split kernels.
-constexpr unsigned kLightGrab = 4;
+constexpr unsigned kLightGrab = 2;
 // Above this many slices per resident warp the sweep is throughput-bound and
 // the split kernels are used.
 constexpr uint64_t kSplitSlicesPerWarp = 64;
