@@ -257,6 +257,7 @@ __constant__ SweepArgs c_loop_args[2];
 // Sweep kernels: persistent grids of 256-thread CTAs at full occupancy.
 constexpr int kSweepThreads = kThreads;
 constexpr int kSweepWarps = kSweepThreads / 32;
+constexpr unsigned kSplitGrab = 4;  // k_sweep_single: slices per dynamic grab
 
 // ---- single-segment vertices: warp per 32-vertex slice ------------------------
 template <bool FLAGGED, bool CLOSED>
@@ -264,8 +265,15 @@ __device__ __forceinline__ void b_sweep_single(const SweepArgs& a) {
   if (a.done && *a.done) return;
   Acc acc;
   const unsigned lane = lane_id();
-  const uint64_t nw = (uint64_t)gridDim.x * kSweepWarps;
-  for (uint64_t s = a.ss_lo + ((uint64_t)blockIdx.x * kSweepThreads + threadIdx.x) / 32; s < a.ss_hi; s += nw) {
+  // slices grabbed dynamically, kSplitGrab at a time (counter in the record)
+  for (;;) {
+    unsigned g = 0;
+    if (lane == 0) g = atomicAdd(&a.red->ticket_light, kSplitGrab);
+    g = __shfl_sync(kFull, g, 0);
+    const uint64_t s0 = a.ss_lo + g;
+    if (s0 >= a.ss_hi) break;
+    const uint64_t s1 = s0 + kSplitGrab < a.ss_hi ? s0 + kSplitGrab : a.ss_hi;
+  for (uint64_t s = s0; s < s1; ++s) {
     const uint64_t vv = (uint64_t)a.M + s * 32 + lane;
     const bool valid = vv < a.n;
     const uint32_t v = (uint32_t)vv;
@@ -294,6 +302,7 @@ __device__ __forceinline__ void b_sweep_single(const SweepArgs& a) {
       }
     }
     if (FLAGGED && a.pend_low) warp_append(pend, lowout, v, od, a.pend_low, a.pend_high, a.red);
+  }
   }
   if (a.npeers) __threadfence_system();  // peer stores visible before the team barrier
   block_reduce_commit(acc, a.red);
