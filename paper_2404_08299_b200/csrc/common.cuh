@@ -127,6 +127,10 @@ struct dynpr_context {
   cudaStream_t side = nullptr;  // deferred uploads / validation (created on first use)
   cudaEvent_t ev_side = nullptr;
   cudaEvent_t ev_rec[2] = {nullptr, nullptr};  // speculative team loop: per-record readiness
+  // split sweep: the multi-chunk kernel runs on `aux`, concurrently with the
+  // single-vertex kernel (fork / join events)
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // instantiated device-loop graphs (engine.cu LoopGraphCache), keyed by
   // sweep plan; owned
   void* loop_graphs = nullptr;

@@ -182,6 +182,25 @@ LoopGraph& loop_graph(dynpr_context* ctx, const SweepPlan& plan, int frontier, L
   }
   cudaGraph_t captured = nullptr;
   DYNPR_CK(cudaStreamEndCapture(st, &captured));
+  {  // the multi-chunk sweep branch first: highest node priority
+    size_t cnt = 0;
+    DYNPR_CK(cudaGraphGetNodes(body, nullptr, &cnt));
+    std::vector<cudaGraphNode_t> nodes(cnt);
+    DYNPR_CK(cudaGraphGetNodes(body, nodes.data(), &cnt));
+    int lo = 0, hi = 0;
+    DYNPR_CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    for (cudaGraphNode_t nd : nodes) {
+      cudaGraphNodeType t;
+      DYNPR_CK(cudaGraphNodeGetType(nd, &t));
+      if (t != cudaGraphNodeTypeKernel) continue;
+      cudaKernelNodeParams kp{};
+      DYNPR_CK(cudaGraphKernelNodeGetParams(nd, &kp));
+      if (!is_priority_sweep_kernel(kp.func)) continue;
+      cudaLaunchAttributeValue v{};
+      v.priority = hi;
+      DYNPR_CK(cudaGraphKernelNodeSetAttribute(nd, cudaLaunchAttributePriority, &v));
+    }
+  }
   DYNPR_CK(cudaGraphInstantiate(&lg.exec, lg.g, 0));
   lg.launches_per_body = ctx->launches - launches0;
   ctx->launches = launches0;
@@ -271,7 +290,14 @@ void solve(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynpr_sta
   // Device-driven loop (CUDA graph WHILE node, no host round trip per
   // iteration) unless the caller needs the host in the loop: an observer,
   // a multi-GPU team (host-orchestrated collectives), per-sweep profiling.
-  const bool device_loop = !obs && !dist && !ctx->profiling && !host_loop_forced();
+  // Large graphs (split sweep) keep the host-driven loop: there the
+  // multi-chunk kernel runs on a second stream concurrently with the
+  // single-vertex kernel, launched first, and inside a captured graph the two
+  // branches lose that order (RMAT-24: 1.09 vs 1.05 ms per iteration, the
+  // host round trip being ~25 µs of it) -- DYNPR_DEVICE_LOOP=1 overrides.
+  const char* dl = std::getenv("DYNPR_DEVICE_LOOP");
+  const bool big_split = sweep_is_split(ctx, L) && !(dl && dl[0] == '1');
+  const bool device_loop = !obs && !dist && !ctx->profiling && !host_loop_forced() && !big_split;
   double* partials = ctx->partials.as<double>(L->n_mseg + 1);
   SweepRed* red = ctx->red.as<SweepRed>(2);
   uint8_t* va = nullptr;
@@ -668,6 +694,12 @@ dynpr_status dynpr_context_destroy(dynpr_context* ctx) {
     ctx->loop_graphs = nullptr;
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->side) cudaStreamDestroy(ctx->side);
+    if (ctx->aux) {
+      cudaStreamSynchronize(ctx->aux);
+      cudaStreamDestroy(ctx->aux);
+    }
+    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+    if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     if (ctx->ev_side) cudaEventDestroy(ctx->ev_side);
     for (auto& e : ctx->ev_rec)
       if (e) cudaEventDestroy(e);

@@ -1215,6 +1215,27 @@ unsigned sweep_grid(dynpr_context* ctx, K kernel, uint64_t slices, size_t smem) 
   return persistent_grid(ctx, kernel, (slices + kSweepWarps - 1) / kSweepWarps);
 }
 
+// Fork / join of the context's aux stream (capturable: the aux stream joins
+// a capture through the fork event and rejoins through the join event).
+static cudaStream_t fork_aux(dynpr_context* ctx) {
+  if (!ctx->aux) {
+    // highest priority: the multi-chunk slices hold the longest lane chains,
+    // so their blocks go first (captured into the loop graph's kernel node)
+    int lo = 0, hi = 0;
+    DYNPR_CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    DYNPR_CK(cudaStreamCreateWithPriority(&ctx->aux, cudaStreamNonBlocking, hi));
+    DYNPR_CK(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+    DYNPR_CK(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+  }
+  DYNPR_CK(cudaEventRecord(ctx->ev_fork, ctx->stream));
+  DYNPR_CK(cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0));
+  return ctx->aux;
+}
+static void join_aux(dynpr_context* ctx) {
+  DYNPR_CK(cudaEventRecord(ctx->ev_join, ctx->aux));
+  DYNPR_CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
+}
+
 void launch_sweep(dynpr_context* ctx, const SweepArgs& a, bool flagged, bool closed) {
   cudaStream_t st = ctx->stream;
   const uint64_t mv = (a.M < a.v_hi ? a.M : a.v_hi) > a.v_lo ? (a.M < a.v_hi ? a.M : a.v_hi) - a.v_lo : 0;
@@ -1224,9 +1245,11 @@ void launch_sweep(dynpr_context* ctx, const SweepArgs& a, bool flagged, bool clo
   unsigned launched = 0;
 #define DYNPR_SWEEP(F, C)                                                                           \
   do {                                                                                              \
+    const bool par = n_ms && n_ss;  /* multi chunks on aux, concurrent with the single slices */   \
     if (n_ms) {                                                                                     \
+      cudaStream_t ms = par ? fork_aux(ctx) : st;                                                   \
       k_sweep_mseg<F><<<sweep_grid(ctx, k_sweep_mseg<F>, n_ms, smem), kSweepThreads, smem,          \
-                        st>>>(a);                                                                   \
+                        ms>>>(a);                                                                   \
       ++launched;                                                                                   \
     }                                                                                               \
     if (n_ss) {                                                                                     \
@@ -1234,6 +1257,7 @@ void launch_sweep(dynpr_context* ctx, const SweepArgs& a, bool flagged, bool clo
                              smem, st>>>(a);                                                        \
       ++launched;                                                                                   \
     }                                                                                               \
+    if (par) join_aux(ctx);                                                                         \
     if (mv) {                                                                                       \
       k_sweep_mfinal<F, C><<<g_mfinal, kThreads, 0, st>>>(a);                                       \
       ++launched;                                                                                   \
@@ -1331,8 +1355,14 @@ static void launch_sweep_c(dynpr_context* ctx, const SweepPlan& p, uint32_t* tic
         ++launched;                                                                              \
       }                                                                                          \
     } else {                                                                                     \
-      if (p.g_mseg) { k_sweep_mseg_c<F, H><<<p.g_mseg, kSweepThreads, 0, st>>>(); ++launched; }   \
+      const bool par = p.g_mseg && p.g_single;                                                  \
+      if (p.g_mseg) {                                                                            \
+        cudaStream_t ms = par ? fork_aux(ctx) : st;                                              \
+        k_sweep_mseg_c<F, H><<<p.g_mseg, kSweepThreads, 0, ms>>>();                              \
+        ++launched;                                                                              \
+      }                                                                                          \
       if (p.g_single) { k_sweep_single_c<F, C, H><<<p.g_single, kSweepThreads, 0, st>>>(); ++launched; } \
+      if (par) join_aux(ctx);                                                                    \
       if (p.g_mfinal) { k_sweep_mfinal_c<F, C, H><<<p.g_mfinal, kThreads, 0, st>>>(); ++launched; } \
     }                                                                                            \
   } while (0)
@@ -1375,6 +1405,19 @@ void launch_expand_ind(dynpr_context* ctx, int half, const unsigned* counts, con
   }
   check_launch();
   count_launch(ctx, 2);
+}
+
+bool sweep_is_split(dynpr_context* ctx, const Layout* L) {
+  const char* mode = std::getenv("DYNPR_SWEEP");
+  const std::string m = mode ? mode : "";
+  const uint64_t resident_warps = (uint64_t)ctx->num_sms * 32;
+  const bool big = (L->n_mslices + L->n_sslices) > kSplitSlicesPerWarp * resident_warps;
+  return m == "split" || (m != "fused" && big);
+}
+
+bool is_priority_sweep_kernel(const void* f) {
+  return f == (const void*)k_sweep_mseg_c<false, 0> || f == (const void*)k_sweep_mseg_c<false, 1> ||
+         f == (const void*)k_sweep_mseg_c<true, 0> || f == (const void*)k_sweep_mseg_c<true, 1>;
 }
 
 void upload_loop_args(dynpr_context* ctx, const SweepArgs* host_pinned_half2) {

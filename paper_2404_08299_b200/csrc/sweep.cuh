@@ -117,6 +117,11 @@ void launch_sweep_ind(dynpr_context* ctx, const SweepPlan& p, int half, uint32_t
 void launch_pull_ind(dynpr_context* ctx, const SweepPlan& p, int half);
 void launch_expand_ind(dynpr_context* ctx, int half, const unsigned* counts, const int* gate);
 void upload_loop_args(dynpr_context* ctx, const SweepArgs* host_pinned_half2);
+// The multi-chunk sweep kernels, whose nodes get the highest launch priority
+// in the loop graph (they run concurrently with the single-vertex kernel).
+bool is_priority_sweep_kernel(const void* f);
+// Whether a whole-graph sweep of this layout takes the split kernels.
+bool sweep_is_split(dynpr_context* ctx, const Layout* L);
 uint32_t* sweep_tick(dynpr_context* ctx);
 // Allocates the sweep launch workspace and resolves every kernel's persistent
 // grid, so launch_sweep / launch_pull_expand can be stream-captured.
