@@ -1252,16 +1252,16 @@ void launch_sweep(dynpr_context* ctx, const SweepArgs& a, bool flagged, bool clo
                         ms>>>(a);                                                                   \
       ++launched;                                                                                   \
     }                                                                                               \
+    if (mv) { /* the ordered combine follows the chunks on the same stream */                     \
+      k_sweep_mfinal<F, C><<<g_mfinal, kThreads, 0, par ? ctx->aux : st>>>(a);                     \
+      ++launched;                                                                                   \
+    }                                                                                               \
     if (n_ss) {                                                                                     \
       k_sweep_single<F, C><<<sweep_grid(ctx, k_sweep_single<F, C>, n_ss, smem), kSweepThreads,      \
                              smem, st>>>(a);                                                        \
       ++launched;                                                                                   \
     }                                                                                               \
     if (par) join_aux(ctx);                                                                         \
-    if (mv) {                                                                                       \
-      k_sweep_mfinal<F, C><<<g_mfinal, kThreads, 0, st>>>(a);                                       \
-      ++launched;                                                                                   \
-    }                                                                                               \
   } while (0)
   // Latency-bound graphs (few slices per resident warp) take the fused
   // kernel; throughput-bound ones the split kernels (measured A/B,
@@ -1361,9 +1361,12 @@ static void launch_sweep_c(dynpr_context* ctx, const SweepPlan& p, uint32_t* tic
         k_sweep_mseg_c<F, H><<<p.g_mseg, kSweepThreads, 0, ms>>>();                              \
         ++launched;                                                                              \
       }                                                                                          \
+      if (p.g_mfinal) {                                                                          \
+        k_sweep_mfinal_c<F, C, H><<<p.g_mfinal, kThreads, 0, par ? ctx->aux : st>>>();           \
+        ++launched;                                                                              \
+      }                                                                                          \
       if (p.g_single) { k_sweep_single_c<F, C, H><<<p.g_single, kSweepThreads, 0, st>>>(); ++launched; } \
       if (par) join_aux(ctx);                                                                    \
-      if (p.g_mfinal) { k_sweep_mfinal_c<F, C, H><<<p.g_mfinal, kThreads, 0, st>>>(); ++launched; } \
     }                                                                                            \
   } while (0)
   if (p.flagged) {
