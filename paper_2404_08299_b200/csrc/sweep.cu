@@ -321,8 +321,11 @@ template <bool FLAGGED>
 __device__ __forceinline__ void b_sweep_mseg(const SweepArgs& a) {
   if (a.done && *a.done) return;
   const unsigned lane = lane_id();
-  const uint64_t nw = (uint64_t)gridDim.x * kSweepWarps;
-  for (uint64_t s = a.ms_lo + ((uint64_t)blockIdx.x * kSweepThreads + threadIdx.x) / 32; s < a.ms_hi; s += nw) {
+  for (;;) {  // slices grabbed dynamically (counter in the record)
+    unsigned g = 0;
+    if (lane == 0) g = atomicAdd(&a.red->ticket_heavy, 1u);
+    const uint64_t s = a.ms_lo + __shfl_sync(kFull, g, 0);
+    if (s >= a.ms_hi) break;
     const uint64_t seg = s * 32 + lane;
     uint32_t len = 0, v = 0xffffffffu;
     if (seg < a.n_mseg) {
