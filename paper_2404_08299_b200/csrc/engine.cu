@@ -290,14 +290,7 @@ void solve(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynpr_sta
   // Device-driven loop (CUDA graph WHILE node, no host round trip per
   // iteration) unless the caller needs the host in the loop: an observer,
   // a multi-GPU team (host-orchestrated collectives), per-sweep profiling.
-  // Large graphs (split sweep) keep the host-driven loop: there the
-  // multi-chunk kernel runs on a second stream concurrently with the
-  // single-vertex kernel, launched first, and inside a captured graph the two
-  // branches lose that order (RMAT-24: 1.09 vs 1.05 ms per iteration, the
-  // host round trip being ~25 µs of it) -- DYNPR_DEVICE_LOOP=1 overrides.
-  const char* dl = std::getenv("DYNPR_DEVICE_LOOP");
-  const bool big_split = sweep_is_split(ctx, L) && !(dl && dl[0] == '1');
-  const bool device_loop = !obs && !dist && !ctx->profiling && !host_loop_forced() && !big_split;
+  const bool device_loop = !obs && !dist && !ctx->profiling && !host_loop_forced();
   double* partials = ctx->partials.as<double>(L->n_mseg + 1);
   SweepRed* red = ctx->red.as<SweepRed>(2);
   uint8_t* va = nullptr;

@@ -1359,16 +1359,18 @@ static void launch_sweep_c(dynpr_context* ctx, const SweepPlan& p, uint32_t* tic
       }                                                                                          \
     } else {                                                                                     \
       const bool par = p.g_mseg && p.g_single;                                                  \
+      /* in the captured graph: the chunks + combine on the origin stream, the */                 \
+      /* single slices on the aux branch (forked after the chunk launch)       */                 \
+      cudaStream_t ss = par ? fork_aux(ctx) : st;                                                \
       if (p.g_mseg) {                                                                            \
-        cudaStream_t ms = par ? fork_aux(ctx) : st;                                              \
-        k_sweep_mseg_c<F, H><<<p.g_mseg, kSweepThreads, 0, ms>>>();                              \
+        k_sweep_mseg_c<F, H><<<p.g_mseg, kSweepThreads, 0, st>>>();                              \
         ++launched;                                                                              \
       }                                                                                          \
       if (p.g_mfinal) {                                                                          \
-        k_sweep_mfinal_c<F, C, H><<<p.g_mfinal, kThreads, 0, par ? ctx->aux : st>>>();           \
+        k_sweep_mfinal_c<F, C, H><<<p.g_mfinal, kThreads, 0, st>>>();                            \
         ++launched;                                                                              \
       }                                                                                          \
-      if (p.g_single) { k_sweep_single_c<F, C, H><<<p.g_single, kSweepThreads, 0, st>>>(); ++launched; } \
+      if (p.g_single) { k_sweep_single_c<F, C, H><<<p.g_single, kSweepThreads, 0, ss>>>(); ++launched; } \
       if (par) join_aux(ctx);                                                                    \
     }                                                                                            \
   } while (0)

@@ -14,9 +14,7 @@ for scale in (18, 20, 22, 24):
     os.environ["DYNPR_HOST_LOOP"] = "1"
     rh = dp.static_pagerank(gt, g)
     os.environ["DYNPR_HOST_LOOP"] = "0"
-    os.environ["DYNPR_DEVICE_LOOP"] = "1"
     rd = dp.static_pagerank(gt, g)
-    os.environ["DYNPR_DEVICE_LOOP"] = "0"
     ctx.set_profiling(True)
     r = dp.static_pagerank(gt, g)
     sw = ctx.sweep_times()
