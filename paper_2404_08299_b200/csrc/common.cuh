@@ -97,6 +97,8 @@ struct SweepRed {
   unsigned int pend_high;         // 1024-edge expansion items of the others
   unsigned int ticket_heavy;      // fused sweep work queues (dynamic scheduling)
   unsigned int ticket_light;
+  unsigned int ticket_pull;       // pull expansion work queue
+  unsigned int pad_;
 };
 
 // Out-edges per expansion work item of a high out-degree vertex.

@@ -695,13 +695,19 @@ __global__ void __launch_bounds__(kSweepThreads, 4) k_sweep_fused_c() {
 __device__ __forceinline__ void b_pull_single(const SweepArgs& a) {
   if (a.expand && *a.expand != kExpandPull) return;
   const unsigned lane = lane_id();
-  const uint64_t nw = (uint64_t)gridDim.x * kWarps;
-  for (uint64_t s = a.ss_lo + ((uint64_t)blockIdx.x * kThreads + threadIdx.x) / 32; s < a.ss_hi; s += nw) {
+  for (;;) {  // slices grabbed dynamically, kSplitGrab at a time
+    unsigned g = 0;
+    if (lane == 0) g = atomicAdd(&a.red->ticket_pull, kSplitGrab);
+    const uint64_t s0 = a.ss_lo + __shfl_sync(kFull, g, 0);
+    if (s0 >= a.ss_hi) break;
+    const uint64_t s1 = s0 + kSplitGrab < a.ss_hi ? s0 + kSplitGrab : a.ss_hi;
+  for (uint64_t s = s0; s < s1; ++s) {
     const uint64_t vv = (uint64_t)a.M + s * 32 + lane;
     const bool need = vv < a.n && !a.va[vv];
     const uint32_t len = need ? a.indeg[vv] : 0u;
     if (!__any_sync(kFull, len != 0)) continue;
     if (segment_any_pending(a.sell_s, a.sbase[s], lane, len, a.np)) a.va[vv] = 1;
+  }
   }
 }
 __global__ void __launch_bounds__(kThreads) k_pull_single(SweepArgs a) { b_pull_single(a); }
