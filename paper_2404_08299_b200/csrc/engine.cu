@@ -328,8 +328,7 @@ void solve(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynpr_sta
     } else if (sp.traversal) {
       // markReachable over the relabelled forward CSR (frontier.cpp:86-121)
       DYNPR_CK(cudaMemsetAsync(va, 0, n, st));
-      uint32_t* fb = ctx->perm_stage.as<uint32_t>((uint64_t)n + 1);
-      mark_reachable(ctx, L->offF, L->tgtF, n, L->inv, sp.seeds, sp.nseeds, va, pl, fb);
+      mark_reachable(ctx, L->offF, L->tgtF, n, L->m, L->inv, sp.seeds, sp.nseeds, va);
     } else {
       // initialAffected + the one expandAffected before the loop
       // (engine.cpp:199-200)
@@ -1047,9 +1046,7 @@ dynpr_status dynpr_mark_reachable(dynpr_context* ctx, const dynpr_graph* g, cons
     if (any_bad_ids(ctx, s, s, n_seeds, n)) invalid("markReachable: seed out of range");
     uint8_t* flags = ctx->flags_va.as<uint8_t>((uint64_t)n + 4);
     DYNPR_CK(cudaMemsetAsync(flags, 0, (size_t)n + 4, ctx->stream));
-    uint32_t* fa = ctx->pend_low.as<uint32_t>((uint64_t)n + 1);
-    uint32_t* fb = ctx->perm_stage.as<uint32_t>((uint64_t)n + 1);
-    mark_reachable(ctx, g->off, g->tgt, n, nullptr, s, n_seeds, flags, fa, fb);
+    mark_reachable(ctx, g->off, g->tgt, n, g->m, nullptr, s, n_seeds, flags);
     if (n) DYNPR_CK(cudaMemcpyAsync(vertex_affected, flags, n, cudaMemcpyDefault, ctx->stream));
     sync(ctx);
   });

@@ -1004,46 +1004,69 @@ __device__ __forceinline__ bool claim_byte(uint8_t* flags, uint32_t w) {
   return ((old >> sh) & 0xffu) == 0u;
 }
 
-__device__ __forceinline__ void warp_push(bool take, uint32_t v, uint32_t* out, unsigned* cnt) {
-  const unsigned mask = __ballot_sync(kFull, take);
-  if (!mask) return;
+// Frontier entries are (vertex, 1024-edge chunk) items, so a hub reached
+// at some level is scanned by ceil(outdeg / 1024) warps instead of one (a
+// warp per frontier vertex left a single warp walking a 4e5-edge RMAT-24 hub
+// while the rest of the GPU idled).  Newly claimed vertices append their
+// items with a warp-aggregated atomic.
+constexpr uint32_t kBfsChunk = 1024;
+__device__ __forceinline__ void warp_push_items(bool take, uint32_t w, uint32_t items, uint2* out, unsigned* cnt) {
+  const unsigned lane = lane_id();
+  unsigned incl = take ? items : 0u;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(kFull, incl, o);
+    if ((int)lane >= o) incl += y;
+  }
+  const unsigned total = __shfl_sync(kFull, incl, 31);
+  if (!total) return;
   unsigned base = 0;
-  if (lane_id() == 0) base = atomicAdd(cnt, (unsigned)__popc(mask));
+  if (lane == 0) base = atomicAdd(cnt, total);
   base = __shfl_sync(kFull, base, 0);
-  if (take) out[base + __popc(mask & ((1u << lane_id()) - 1u))] = v;
+  if (take)
+    for (unsigned j = 0, b = base + incl - items; j < items; ++j) out[b + j] = make_uint2(w, j);
 }
 
-__global__ void k_bfs_seed(const uint32_t* inv, const uint32_t* seeds, uint64_t ns, uint8_t* flags, uint32_t* out,
-                           unsigned* cnt) {
+__device__ __forceinline__ uint32_t bfs_items(const uint64_t* off, uint32_t w) {
+  const uint64_t d = off[w + 1] - off[w];
+  return d ? (uint32_t)((d + kBfsChunk - 1) / kBfsChunk) : 0u;
+}
+
+__global__ void k_bfs_seed(const uint64_t* off, const uint32_t* inv, const uint32_t* seeds, uint64_t ns,
+                           uint8_t* flags, uint2* out, unsigned* cnt) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x; b < ns; b += stride) {
     const uint64_t i = b + threadIdx.x;
-    uint32_t v = 0;
+    uint32_t v = 0, items = 0;
     bool take = false;
     if (i < ns) {
       v = inv ? inv[seeds[i]] : seeds[i];
       take = claim_byte(flags, v);
+      if (take) items = bfs_items(off, v);
     }
-    warp_push(take, v, out, cnt);
+    warp_push_items(take && items, v, items, out, cnt);
   }
 }
 
-// warp per frontier vertex, lanes stride over its out-edges
-__global__ void k_bfs_level(const uint64_t* off, const uint32_t* tgt, const uint32_t* fr, uint32_t nf, uint8_t* flags,
-                            uint32_t* out, unsigned* cnt) {
+// warp per frontier item: lanes stride over the chunk's out-edges
+__global__ void k_bfs_level(const uint64_t* off, const uint32_t* tgt, const uint2* fr, uint32_t nf, uint8_t* flags,
+                            uint2* out, unsigned* cnt) {
   const uint64_t nw = (uint64_t)gridDim.x * blockDim.x / 32;
   for (uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; i < nf; i += nw) {
-    const uint32_t u = fr[i];
-    const uint64_t b = off[u], e = off[u + 1];
+    const uint2 it = fr[i];
+    const uint64_t b = off[it.x] + (uint64_t)kBfsChunk * it.y;
+    const uint64_t e0 = off[it.x + 1];
+    const uint64_t e = b + kBfsChunk < e0 ? b + kBfsChunk : e0;
     for (uint64_t k0 = b; k0 < e; k0 += 32) {
       const uint64_t k = k0 + lane_id();
-      uint32_t w = 0;
+      uint32_t w = 0, items = 0;
       bool take = false;
       if (k < e) {
         w = tgt[k];
         take = claim_byte(flags, w);
+        if (take) items = bfs_items(off, w);
       }
-      warp_push(take, w, out, cnt);
+      warp_push_items(take && items, w, items, out, cnt);
     }
   }
 }
@@ -1540,14 +1563,17 @@ void launch_expand_dev(dynpr_context* ctx, const uint64_t* off, const uint32_t* 
   count_launch(ctx, 2);
 }
 
-uint64_t mark_reachable(dynpr_context* ctx, const uint64_t* off, const uint32_t* tgt, uint32_t n, const uint32_t* inv,
-                        const uint32_t* seeds, uint64_t ns, uint8_t* flags, uint32_t* fa, uint32_t* fb) {
+uint64_t mark_reachable(dynpr_context* ctx, const uint64_t* off, const uint32_t* tgt, uint32_t n, uint64_t m,
+                        const uint32_t* inv, const uint32_t* seeds, uint64_t ns, uint8_t* flags) {
   cudaStream_t st = ctx->stream;
   auto* cnt = reinterpret_cast<unsigned*>(ctx->scratch32a.as<unsigned>(2));
-  uint64_t reached = 0;
+  uint64_t items_total = 0;
   if (!ns || !n) return 0;
+  const uint64_t cap = (uint64_t)n + m / kBfsChunk + 1;  // every vertex's items, once
+  uint2* fa = ctx->bfs_a.as<uint2>(cap);
+  uint2* fb = ctx->bfs_b.as<uint2>(cap);
   DYNPR_CK(cudaMemsetAsync(cnt, 0, 4, st));
-  k_bfs_seed<<<grid_for(ns, kThreads, ctx->num_sms * 16), kThreads, 0, st>>>(inv, seeds, ns, flags, fa, cnt);
+  k_bfs_seed<<<grid_for(ns, kThreads, ctx->num_sms * 16), kThreads, 0, st>>>(off, inv, seeds, ns, flags, fa, cnt);
   check_launch();
   count_launch(ctx);
   for (;;) {
@@ -1555,7 +1581,7 @@ uint64_t mark_reachable(dynpr_context* ctx, const uint64_t* off, const uint32_t*
     DYNPR_CK(cudaMemcpyAsync(ctx->pinned, cnt, 4, cudaMemcpyDeviceToHost, st));
     sync(ctx);
     std::memcpy(&nf, ctx->pinned, 4);
-    reached += nf;
+    items_total += nf;
     if (!nf) break;
     DYNPR_CK(cudaMemsetAsync(cnt, 0, 4, st));
     k_bfs_level<<<grid_for((uint64_t)nf * 32, kThreads, ctx->num_sms * 16), kThreads, 0, st>>>(off, tgt, fa, nf, flags,
@@ -1564,7 +1590,7 @@ uint64_t mark_reachable(dynpr_context* ctx, const uint64_t* off, const uint32_t*
     count_launch(ctx);
     std::swap(fa, fb);
   }
-  return reached;
+  return items_total;
 }
 
 void launch_linf(dynpr_context* ctx, const double* a, const double* b, uint64_t n, unsigned long long* out_bits) {

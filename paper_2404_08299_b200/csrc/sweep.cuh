@@ -145,11 +145,11 @@ void launch_expand(dynpr_context* ctx, const uint64_t* off, const uint32_t* tgt,
 void launch_pull_expand(dynpr_context* ctx, const SweepArgs& a);
 
 // markReachable (frontier.cpp:86-121): flags |= everything reachable from
-// the seeds over the CSR (off, tgt); seed ids mapped through `inv` when given;
-// fa/fb are frontier buffers of n entries.  Returns the number of vertices
-// newly claimed.
-uint64_t mark_reachable(dynpr_context* ctx, const uint64_t* off, const uint32_t* tgt, uint32_t n, const uint32_t* inv,
-                        const uint32_t* seeds, uint64_t ns, uint8_t* flags, uint32_t* fa, uint32_t* fb);
+// the seeds over the CSR (off, tgt; m edges); seed ids mapped through `inv`
+// when given.  Level-synchronous; frontier items are (vertex, 1024-edge
+// chunk).  Returns the number of frontier items processed.
+uint64_t mark_reachable(dynpr_context* ctx, const uint64_t* off, const uint32_t* tgt, uint32_t n, uint64_t m,
+                        const uint32_t* inv, const uint32_t* seeds, uint64_t ns, uint8_t* flags);
 
 // Norms (rank.cpp:142-152).
 void launch_linf(dynpr_context* ctx, const double* a, const double* b, uint64_t n, unsigned long long* out_bits);
