@@ -45,6 +45,19 @@ bool is_device_ptr(const void* p) {
 
 bool any_bad_ids(dynpr_context* ctx, const uint32_t* d_s, const uint32_t* d_d, uint64_t cnt, uint32_t n);
 
+// Range check of a batch list: on the host when the caller's arrays are host
+// memory (no device round trip), else on the device (staged arrays).
+bool batch_ids_bad(dynpr_context* ctx, const uint32_t* user_s, const uint32_t* user_d, const uint32_t* dev_s,
+                   const uint32_t* dev_d, uint64_t cnt, uint32_t n) {
+  if (!cnt) return false;
+  if (user_s && user_d && !is_device_ptr(user_s) && !is_device_ptr(user_d)) {
+    for (uint64_t i = 0; i < cnt; ++i)
+      if (user_s[i] >= n || user_d[i] >= n) return true;
+    return false;
+  }
+  return any_bad_ids(ctx, dev_s, dev_d, cnt, n);
+}
+
 namespace {
 
 void validate_config(const dynpr_config* c) {  // rank.cpp:11-20
@@ -988,8 +1001,10 @@ dynpr_status dynpr_dynamic_frontier(dynpr_context* ctx, const dynpr_graph* gF, c
     sp.nd = n_del;
     sp.ni = n_ins;
     // initialAffected range checks (frontier.cpp:36-37)
-    if (any_bad_ids(ctx, sp.ds, sp.dd, n_del, gT->n)) invalid("initialAffected deletions: vertex id out of range");
-    if (any_bad_ids(ctx, sp.is, id, n_ins, gT->n)) invalid("initialAffected insertions: vertex id out of range");
+    if (batch_ids_bad(ctx, del_src, del_dst, sp.ds, sp.dd, n_del, gT->n))
+      invalid("initialAffected deletions: vertex id out of range");
+    if (batch_ids_bad(ctx, ins_src, ins_dst, sp.is, id, n_ins, gT->n))
+      invalid("initialAffected insertions: vertex id out of range");
     sp.flagged = true;
     sp.closed = pruning != 0;
     solve(ctx, sp, ranks_out, stats, observer, observer_user);
