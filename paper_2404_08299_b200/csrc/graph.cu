@@ -337,29 +337,43 @@ __device__ __forceinline__ void warp_copy_range(const uint32_t* __restrict__ tgt
   warp_copy_words(tgt, ntgt, S + 4 * nblk, e, D + 4 * nblk, lane);
 }
 
-// Rows without batch entries keep their slices: warp per 32-vertex tile,
-// one contiguous copy when the whole tile is untouched.
-__global__ void k_copy_untouched(const uint64_t* off, const uint32_t* tgt,
-                                 const uint64_t* noff, uint32_t* ntgt,
-                                 uint32_t n, const uint8_t* touched) {
-  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / 32;
-  const unsigned lane = threadIdx.x & 31;
-  const uint64_t nwarps = (uint64_t)gridDim.x * blockDim.x / 32;
-  const uint64_t ntiles = ((uint64_t)n + 31) / 32;
-  for (uint64_t t = warp; t < ntiles; t += nwarps) {
-    const uint64_t v0 = t * 32;
-    const uint64_t v1 = v0 + 32 < n ? v0 + 32 : n;
-    const uint64_t v = v0 + lane;
-    const bool mine = v < v1 && touched[v];
-    const unsigned any = __ballot_sync(0xffffffffu, mine);
-    if (!any) {
-      warp_copy_range(tgt, ntgt, off[v0], off[v1], noff[v0], lane);
-    } else {
-      for (uint64_t w = v0; w < v1; ++w) {
-        if ((any >> (w - v0)) & 1u) continue;
-        warp_copy_range(tgt, ntgt, off[w], off[w + 1], noff[w], lane);
-      }
+
+// Untouched rows as runs: the rows between two consecutive touched rows
+// keep their slices and their order, so each run is ONE contiguous copy with
+// a constant source/destination shift.  Runs are cut into kRunPiece-word
+// pieces, warp per piece (grid-stride over the pieces), which keeps every
+// warp streaming ~32 KB instead of re-reading row metadata every 32 rows.
+constexpr uint64_t kRunPiece = 8192;
+__global__ void k_run_pieces(const uint32_t* T, const unsigned long long* nt_ptr, uint32_t n, const uint64_t* off,
+                             uint32_t* pieces) {
+  const uint64_t nt = *nt_ptr;
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j <= nt + 1;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t c = 0;
+    if (j <= nt) {
+      const uint64_t a = j == 0 ? 0 : (uint64_t)T[j - 1] + 1;
+      const uint64_t b = j == nt ? n : T[j];
+      const uint64_t words = b > a ? off[b] - off[a] : 0;
+      c = (uint32_t)((words + kRunPiece - 1) / kRunPiece);
     }
+    pieces[j] = c;  // entry nt + 1 stays 0: the exclusive scan's total
+  }
+}
+__global__ void k_copy_runs(const uint32_t* T, const unsigned long long* nt_ptr, const uint32_t* pstart, uint32_t n,
+                            const uint64_t* off, const uint32_t* tgt, const uint64_t* noff, uint32_t* ntgt) {
+  const uint64_t nt = *nt_ptr;
+  const uint32_t total = pstart[nt + 1];
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / 32;
+  const uint64_t nwarps = (uint64_t)gridDim.x * blockDim.x / 32;
+  const unsigned lane = threadIdx.x & 31;
+  for (uint64_t t = warp; t < total; t += nwarps) {
+    const uint64_t j = upper_bound_u32(pstart, nt + 2, (uint32_t)t) - 1;  // run of piece t
+    const uint64_t k = t - pstart[j];
+    const uint64_t a = j == 0 ? 0 : (uint64_t)T[j - 1] + 1;
+    const uint64_t b = j == nt ? n : T[j];
+    const uint64_t sb = off[a] + k * kRunPiece, se0 = off[b];
+    const uint64_t se = sb + kRunPiece < se0 ? sb + kRunPiece : se0;
+    warp_copy_range(tgt, ntgt, sb, se, noff[a] + k * kRunPiece, lane);
   }
 }
 
@@ -720,14 +734,25 @@ void graph_apply_batch_impl(dynpr_context* ctx, const dynpr_graph* g,
     cub_call(ctx, [&](void* t, size_t& b) {
       return cub::DeviceScan::ExclusiveSum(t, b, istart, istart, (int64_t)n + 1, st);
     });
-    const uint64_t tiles = ((uint64_t)n + 31) / 32;
-    k_copy_untouched<<<grid_for(tiles * 32, 256, 1 << 16), 256, 0, st>>>(g->off, g->tgt, r->off, r->tgt, n,
-                                                                          touched);
+    // touched rows in order -> runs of untouched rows -> pieces -> copies
+    uint32_t* T = ctx->run_list.as<uint32_t>((uint64_t)n + 1);
+    uint32_t* pcs = ctx->run_pieces.as<uint32_t>((uint64_t)n + 3);
+    auto* nt = reinterpret_cast<unsigned long long*>(ctx->scratch64a.as<unsigned long long>(4)) + 2;
+    cub::CountingInputIterator<uint32_t> iota(0);
+    cub_call(ctx, [&](void* t, size_t& b) {
+      return cub::DeviceSelect::Flagged(t, b, iota, touched, T, nt, (int64_t)n, st);
+    });
+    k_run_pieces<<<grid_for((uint64_t)n + 2, 256, 1 << 16), 256, 0, st>>>(T, nt, n, g->off, pcs);
+    check_launch();
+    cub_call(ctx, [&](void* t, size_t& b) {
+      return cub::DeviceScan::ExclusiveSum(t, b, pcs, pcs, (int64_t)n + 3, st);
+    });
+    k_copy_runs<<<(unsigned)ctx->num_sms * 32, 256, 0, st>>>(T, nt, pcs, n, g->off, g->tgt, r->off, r->tgt);
     check_launch();
     k_merge_touched<<<(unsigned)ctx->num_sms * 16, 256, 0, st>>>(istart, n, g->off, g->tgt, r->off, r->tgt, dp,
                                                                  ndp, nw, nnw, sb, mask, need);
     check_launch();
-    count_launch(ctx, 4);
+    count_launch(ctx, 5);
   }
   unsigned long long hc[2];
   DYNPR_CK(cudaMemcpyAsync(ctx->pinned, counters, 16, cudaMemcpyDeviceToHost, st));
