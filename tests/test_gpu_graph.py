@@ -248,3 +248,48 @@ def test_static_pagerank_csr_host_pair(dp, oracle_lib):
     assert rc == N.DYNPR_INVALID_ARGUMENT and "out of range" in N.last_error()
     rc, r2, _ = run(offT, tgtT, offF, tgtF)  # the context is still healthy
     assert rc == 0 and np.array_equal(r2[:n], ref.ranks)
+
+
+@pytest.mark.parametrize("case", ["empty", "first_last", "every_row", "hub_rows"])
+def test_apply_batch_pair_run_boundaries(dp, oracle_lib, case):
+    """The ingest copies untouched rows as runs between touched rows: batches
+    touching the first / last row, every row, no row, or only hub rows must
+    still give the reference's bytes for both the forward and the transpose."""
+    O = oracle_lib
+    src, dst = O.rmat_edges(12, 16 << 12)
+    og = O.add_self_loops(O.build_csr((src, dst), 1 << 12))
+    n = og.n
+    off, tgt = og.csr()
+    rng = np.random.default_rng(5)
+    if case == "empty":
+        dels, ins = [], []
+    elif case == "first_last":
+        dels = [(0, int(t)) for t in tgt[off[0]:off[1]] if t != 0][:3] + \
+               [(n - 1, int(t)) for t in tgt[off[n - 1]:off[n]] if t != n - 1][:1]
+        ins = [(0, n - 1), (n - 1, 0), (n - 1, 1)]
+        ins = [e for e in ins if not og_has(off, tgt, *e)]
+    elif case == "every_row":
+        ins = [(u, int((u * 7 + 3) % n)) for u in range(n)]
+        ins = [e for e in ins if e[0] != e[1] and not og_has(off, tgt, *e)]
+        dels = []
+    else:
+        deg = np.diff(off)
+        hubs = np.argsort(-deg)[:4]
+        dels = [(int(h), int(t)) for h in hubs for t in tgt[off[h]:off[h + 1]][::7] if t != h]
+        ins = []
+    og2, miss1, dup1 = O.apply_batch(og, dels, ins)
+    g = dp.CsrGraph.from_csr(n, off, tgt)
+    gt = dp.transpose(g)
+    st = dp.BatchApplyStats()
+    g2, gt2 = dp.apply_batch_pair(g, gt, dp.BatchUpdate(dels, ins), st)
+    o2, t2 = og2.csr()
+    ot2, tt2 = O.transpose(og2).csr()
+    assert np.array_equal(g2.offsets, o2) and np.array_equal(g2.targets, t2)
+    assert np.array_equal(gt2.offsets, ot2) and np.array_equal(gt2.targets, tt2)
+    assert (st.missing_deletions, st.duplicate_insertions) == (miss1, dup1)
+
+
+def og_has(off, tgt, u, v):
+    row = tgt[off[u]:off[u + 1]]
+    i = np.searchsorted(row, v)
+    return i < len(row) and row[i] == v
