@@ -74,6 +74,7 @@ __device__ __forceinline__ void block_reduce_commit(Acc acc, SweepRed* red) {
     s_e[w] = acc.edges;
     s_q[w] = acc.pedges;
   }
+  __syncwarp();  // reconverge the warp after the lane-divergent store
   __syncthreads();
   if (threadIdx.x == 0) {
     double d = 0.0;
@@ -390,6 +391,7 @@ __device__ __forceinline__ void b_sweep_mfinal(const SweepArgs& a) {
     }
     s_mb = lo;
   }
+  __syncwarp();  // reconverge the warp after the lane-divergent store
   __syncthreads();
   const uint64_t mb = s_mb;
   // phase 1: warp per heavy multi vertex
@@ -751,6 +753,7 @@ __device__ __forceinline__ unsigned block_exclusive_scan(unsigned x, unsigned& t
     if ((int)lane >= o) inc += y;
   }
   if (lane == 31) s_w[w] = inc;
+  __syncwarp();  // reconverge the warp after the lane-divergent store
   __syncthreads();
   unsigned pre = 0;
   total = 0;
@@ -1082,6 +1085,7 @@ __global__ void k_linf(const double* a, const double* b, uint64_t n, unsigned lo
   m = warp_max(m);
   __shared__ double s[kWarps];
   if (lane_id() == 0) s[threadIdx.x >> 5] = m;
+  __syncwarp();  // reconverge the warp after the lane-divergent store
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int i = 1; i < kWarps; ++i) m = fmax(m, s[i]);
