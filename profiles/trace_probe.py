@@ -1,4 +1,7 @@
-"""Per-warp timeline of one fused sweep (DYNPR_TRACE=1)."""
+"""Per-warp timeline of one fused sweep (DYNPR_TRACE=1): the last sweep of a
+3-sweep Static solve, or with a second argument `dfp [fraction]` the last
+sweep of a DF-P solve after a random batch of that size.
+    python profiles/trace_probe.py SCALE [dfp [1e-7]]"""
 import os, sys, ctypes as C
 import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -8,8 +11,18 @@ import paper_2404_08299_b200 as dp
 from paper_2404_08299_b200 import _native as N
 scale = int(sys.argv[1])
 g = dp.rmat_graph(scale); gt = dp.transpose(g); dp.prepare(gt, g)
-cfg = dp.EngineConfig(max_iterations=3, convergence_check_disabled=True)
-dp.static_pagerank(gt, g, cfg)
+if len(sys.argv) > 2 and sys.argv[2] == "dfp":
+    frac = float(sys.argv[3]) if len(sys.argv) > 3 else 1e-7
+    base = dp.static_pagerank(gt, g)
+    b = dp.generate_random_batch(g, dp.batch_size_from_fraction(frac, g.edge_count), 0.8, 5)
+    g, gt = dp.apply_batch_pair(g, gt, b)
+    dp.prepare(gt, g)
+    for _ in range(2):
+        d = dp.dynamic_frontier(g, gt, b.deletions, b.insertions, base.ranks, pruning=True)
+    print("dfp iterations", d.iterations, "affected", d.affected_vertex_iterations, "device_ms %.3f" % d.device_ms)
+else:
+    cfg = dp.EngineConfig(max_iterations=3, convergence_check_disabled=True)
+    dp.static_pagerank(gt, g, cfg)
 cnt = C.c_uint64()
 N.lib().dynpr_debug_sweep_trace(None, 0, C.byref(cnt))
 buf = np.zeros(cnt.value, np.uint64)
