@@ -371,7 +371,7 @@ def _out_ranks(out, n: int):
     the caller's device array `out` (n float64) so chained solves never
     leave the GPU."""
     if out is None:
-        r = np.zeros(max(n, 1), np.float64)
+        r = np.empty(max(n, 1), np.float64)  # every entry is written
         return _p(r), r
     ptr, length, keep = _in_array(out, np.float64)
     if length != n:
@@ -741,7 +741,7 @@ def dynamic_frontier_from_flags(g_forward: CsrGraph, g_transpose: CsrGraph, vert
     va = _arr(vertex_affected, np.uint8)
     np_ = _arr(neighbors_pending, np.uint8)
     prev = _arr(previous_ranks, np.float64)
-    ranks = np.zeros(max(g_transpose.vertex_count, 1), np.float64)
+    ranks = np.empty(max(g_transpose.vertex_count, 1), np.float64)
     st = N.Stats()
     obs, keep = _observer(observer)
     _check(N.lib().dynpr_dynamic_frontier_from_flags(C.c_void_p(g_forward.ctx.h), C.c_void_p(g_forward.h),

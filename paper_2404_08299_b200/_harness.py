@@ -185,7 +185,7 @@ def compute_reference_ranks(g_transpose, g_forward, config=None) -> np.ndarray:
     max_iterations sweeps with the convergence check disabled, on the GPU."""
     from . import EngineConfig, _p
     cfg = (config or EngineConfig())._c()
-    ranks = np.zeros(max(g_transpose.vertex_count, 1), np.float64)
+    ranks = np.empty(max(g_transpose.vertex_count, 1), np.float64)
     _check(N.lib().dynpr_compute_reference_ranks(C.c_void_p(g_transpose.ctx.h), C.c_void_p(g_transpose.h),
                                                  C.c_void_p(g_forward.h), C.byref(cfg), _p(ranks)))
     return ranks[: g_transpose.vertex_count]
