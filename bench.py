@@ -297,7 +297,8 @@ def run_ours(args, world, rank, local):
     base_dev = torch.from_numpy(base.ranks).to(f"cuda:{local}")
     size = dp.batch_size_from_fraction(args.batch_frac, m0)
     total = args.warmup + args.steps
-    batches = [dp.generate_random_batch(g0, size, 0.8, dp.derive_seed(args.seed + rank, 1000003 + k))
+    # the same batches on every rank: a team shares one replicated graph
+    batches = [dp.generate_random_batch(g0, size, 0.8, dp.derive_seed(args.seed, 1000003 + k))
                for k in range(total)]
     ranks_dev = torch.empty(n, dtype=torch.float64, device=f"cuda:{local}")
     cfg = dp.EngineConfig()._c()

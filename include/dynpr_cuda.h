@@ -103,6 +103,10 @@ dynpr_status dynpr_config_validate(const dynpr_config* cfg);
 
 /* ---- context ------------------------------------------------------------ */
 dynpr_status dynpr_context_create(int device, dynpr_context** out);
+/* Graphs live in their context's device memory pool: destroying a context
+ * whose graphs are still alive defers the teardown until the last of them
+ * is destroyed (any order of the two calls is safe; using a graph after its
+ * context's destroy is not supported). */
 dynpr_status dynpr_context_destroy(dynpr_context* ctx);
 /* Kernel-launch counter (every kernel this library launched). */
 uint64_t dynpr_context_launches(const dynpr_context* ctx);

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -141,6 +142,13 @@ struct dynpr_context {
       pend_low, pend_high, pend_flags, partials, perm_stage,
       tile_counts, red, stage_a, stage_b, stage_c, stage_d, stage_e, stage_f,
       cub_tmp, tick, loopctl, layout_tmp, side_err, bfs_a, bfs_b, run_list, run_pieces, scratch64a, scratch64b, scratch32a, scratch32b, scratch8a, batch[4];
+  // lifetime: graphs are allocated from this context's stream-ordered pool.
+  // dynpr_context_destroy with graphs still alive (e.g. a garbage-collected
+  // binding finalising both in arbitrary order) defers the teardown to the
+  // last graph's destroy.
+  std::atomic<uint64_t> live_graphs{0};
+  std::atomic<bool> closing{false};
+  std::atomic<bool> torn_down{false};
 };
 
 namespace dynpr_b200 {
@@ -298,6 +306,8 @@ inline int bits_for(uint64_t x) {
 dynpr_graph* new_graph_struct(dynpr_context* ctx, uint32_t n);
 dynpr_graph* make_graph(dynpr_context* ctx, uint32_t n, uint64_t m);
 void destroy_graph(dynpr_graph* g);
+// releases every resource of a context (engine.cu); called exactly once
+void context_teardown(dynpr_context* ctx);
 
 // A host CSR uploaded with its targets' transfer + validation deferred to
 // the context's side stream (dynpr_static_pagerank_csr): the graph is usable

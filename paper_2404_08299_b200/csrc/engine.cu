@@ -91,6 +91,33 @@ SweepRed read_red(dynpr_context* ctx, const SweepRed* d) {
   return h;
 }
 
+// A team shares one replicated graph: every rank must hold the same pair,
+// or the ranges it sweeps belong to different graphs.  The content
+// fingerprint of the pair (both CSRs) is computed once per layout; every
+// team solve all-reduces it (max and sum agree only if all ranks match).
+void team_check_graph(dynpr_context* ctx, Comm* comm, Layout* L, const dynpr_graph* gT, const dynpr_graph* gF,
+                      SweepRed* red) {
+  if (!L->fingerprint) {
+    DYNPR_CK(cudaMemsetAsync(red, 0, sizeof(SweepRed), ctx->stream));
+    auto* acc = reinterpret_cast<unsigned long long*>(&red->delta_bits);
+    launch_fingerprint(ctx, reinterpret_cast<const uint32_t*>(gT->off), 2 * ((uint64_t)gT->n + 1), 1ull << 40, acc);
+    launch_fingerprint(ctx, gT->tgt, gT->m, 2ull << 40, acc);
+    launch_fingerprint(ctx, reinterpret_cast<const uint32_t*>(gF->off), 2 * ((uint64_t)gF->n + 1), 3ull << 40, acc);
+    launch_fingerprint(ctx, gF->tgt, gF->m, 4ull << 40, acc);
+    const uint64_t fp = read_red(ctx, red).delta_bits;
+    L->fingerprint = fp ? fp : 1;
+  }
+  SweepRed rec{};
+  rec.delta_bits = L->fingerprint;
+  rec.processed = L->fingerprint;
+  std::memcpy(ctx->pinned, &rec, sizeof rec);
+  DYNPR_CK(cudaMemcpyAsync(red, ctx->pinned, sizeof rec, cudaMemcpyHostToDevice, ctx->stream));
+  comm->allreduce_red(red, ctx->stream);
+  const SweepRed t = read_red(ctx, red);
+  if (t.processed != t.delta_bits * (uint64_t)comm->world)
+    throw Error(DYNPR_INVALID_ARGUMENT, "team: the ranks hold different graphs (a team sweeps one replicated graph)");
+}
+
 struct SolveSpec {
   const dynpr_graph* gT = nullptr;
   const dynpr_graph* gF = nullptr;
@@ -394,6 +421,7 @@ void solve(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynpr_sta
     off_c[comm->world] = 8ull * n;
     off_f[comm->world] = n;
   }
+  if (dist) team_check_graph(ctx, comm, const_cast<Layout*>(L), gT, gF, red);
 
   if (fused) {
     // Team barrier: no rank may store into a peer's buffers before that
@@ -551,6 +579,33 @@ void solve(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynpr_sta
 
 using namespace dynpr_b200;
 
+void dynpr_b200::context_teardown(dynpr_context* ctx) {
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->side) cudaStreamSynchronize(ctx->side);
+  delete ctx->comm;
+  ctx->comm = nullptr;
+  if (ctx->ev_a) cudaEventDestroy(ctx->ev_a);
+  if (ctx->ev_b) cudaEventDestroy(ctx->ev_b);
+  if (ctx->ev_s0) cudaEventDestroy(ctx->ev_s0);
+  if (ctx->ev_s1) cudaEventDestroy(ctx->ev_s1);
+  delete static_cast<LoopGraphCache*>(ctx->loop_graphs);
+  ctx->loop_graphs = nullptr;
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  if (ctx->side) cudaStreamDestroy(ctx->side);
+  if (ctx->aux) {
+    cudaStreamSynchronize(ctx->aux);
+    cudaStreamDestroy(ctx->aux);
+  }
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+  if (ctx->ev_side) cudaEventDestroy(ctx->ev_side);
+  for (auto& e : ctx->ev_rec)
+    if (e) cudaEventDestroy(e);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
 extern "C" {
 
 const char* dynpr_last_error(void) { return g_last_error.c_str(); }
@@ -686,32 +741,12 @@ dynpr_status dynpr_context_rank(const dynpr_context* ctx, int* rank, int* world)
 dynpr_status dynpr_context_destroy(dynpr_context* ctx) {
   return api_guard([&] {
     if (!ctx) return;
-    cudaSetDevice(ctx->device);
-    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
-    if (ctx->side) cudaStreamSynchronize(ctx->side);
-    delete ctx->comm;
-    ctx->comm = nullptr;
-    if (ctx->ev_a) cudaEventDestroy(ctx->ev_a);
-    if (ctx->ev_b) cudaEventDestroy(ctx->ev_b);
-    if (ctx->ev_s0) cudaEventDestroy(ctx->ev_s0);
-    if (ctx->ev_s1) cudaEventDestroy(ctx->ev_s1);
-    delete static_cast<LoopGraphCache*>(ctx->loop_graphs);
-    ctx->loop_graphs = nullptr;
-    if (ctx->pinned) cudaFreeHost(ctx->pinned);
-    if (ctx->side) cudaStreamDestroy(ctx->side);
-    if (ctx->aux) {
-      cudaStreamSynchronize(ctx->aux);
-      cudaStreamDestroy(ctx->aux);
-    }
-    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
-    if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
-    if (ctx->ev_side) cudaEventDestroy(ctx->ev_side);
-    for (auto& e : ctx->ev_rec)
-      if (e) cudaEventDestroy(e);
-    if (ctx->stream) cudaStreamDestroy(ctx->stream);
-    delete ctx;
+    ctx->closing.store(true);
+    // graphs still alive: the last one's destroy tears the context down
+    if (ctx->live_graphs.load() == 0 && !ctx->torn_down.exchange(true)) context_teardown(ctx);
   });
 }
+
 
 uint64_t dynpr_context_launches(const dynpr_context* ctx) { return ctx ? ctx->launches : 0; }
 

@@ -545,6 +545,7 @@ dynpr_graph* new_graph_struct(dynpr_context* ctx, uint32_t n) {
   g->id = next_id.fetch_add(1);
   g->ctx = ctx;
   g->n = n;
+  if (ctx) ctx->live_graphs.fetch_add(1);
   return g;
 }
 
@@ -564,9 +565,13 @@ dynpr_graph* make_graph(dynpr_context* ctx, uint32_t n, uint64_t m) {
 void destroy_graph(dynpr_graph* g) {
   if (!g) return;
   if (g->layout) destroy_layout(g->layout);
-  pool_free(g->ctx, g->off);
-  pool_free(g->ctx, g->tgt);
+  dynpr_context* ctx = g->ctx;
+  pool_free(ctx, g->off);
+  pool_free(ctx, g->tgt);
   delete g;
+  // the context's own destroy came first: its teardown waited for us
+  if (ctx && ctx->live_graphs.fetch_sub(1) == 1 && ctx->closing.load() && !ctx->torn_down.exchange(true))
+    context_teardown(ctx);
 }
 
 // buildCsr on device from device edge arrays (validation already done).

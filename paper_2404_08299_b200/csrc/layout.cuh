@@ -79,6 +79,8 @@ struct Layout {
   // multi-GPU partition cache (sweep.cu plan_ranges)
   int plan_world = 0;
   std::vector<RankRange> plan;
+  // content fingerprint of the graph pair (team identity check), 0 = not yet
+  uint64_t fingerprint = 0;
   ~Layout();
 };
 

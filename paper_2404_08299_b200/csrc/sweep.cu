@@ -1074,6 +1074,25 @@ __global__ void k_bfs_level(const uint64_t* off, const uint32_t* tgt, const uint
   }
 }
 
+// ---- team graph fingerprint ----------------------------------------------------
+// Order-free sum of position-salted SplitMix64 finalisers of 32-bit words:
+// equal arrays give equal sums on every rank, a differing word changes the
+// sum (up to 2^-64 collisions).
+__device__ __forceinline__ uint64_t fp_mix(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+__global__ void k_fingerprint(const uint32_t* w, uint64_t count, uint64_t salt, unsigned long long* out) {
+  uint64_t h = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    h += fp_mix((i + salt) * 0x9e3779b97f4a7c15ull ^ w[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(kFull, h, o);
+  if (lane_id() == 0 && h) atomicAdd(out, (unsigned long long)h);
+}
+
 // ---- norms ------------------------------------------------------------------
 __global__ void k_linf(const double* a, const double* b, uint64_t n, unsigned long long* out) {
   double m = 0.0;
@@ -1595,6 +1614,14 @@ uint64_t mark_reachable(dynpr_context* ctx, const uint64_t* off, const uint32_t*
     std::swap(fa, fb);
   }
   return items_total;
+}
+
+void launch_fingerprint(dynpr_context* ctx, const uint32_t* words, uint64_t count, uint64_t salt,
+                        unsigned long long* acc) {
+  if (!count) return;
+  k_fingerprint<<<grid_for(count, kThreads, ctx->num_sms * 8), kThreads, 0, ctx->stream>>>(words, count, salt, acc);
+  check_launch();
+  count_launch(ctx);
 }
 
 void launch_linf(dynpr_context* ctx, const double* a, const double* b, uint64_t n, unsigned long long* out_bits) {

@@ -152,6 +152,9 @@ uint64_t mark_reachable(dynpr_context* ctx, const uint64_t* off, const uint32_t*
                         const uint32_t* inv, const uint32_t* seeds, uint64_t ns, uint8_t* flags);
 
 // Norms (rank.cpp:142-152).
+// adds the fingerprint of `count` 32-bit words to *acc (team graph identity check)
+void launch_fingerprint(dynpr_context* ctx, const uint32_t* words, uint64_t count, uint64_t salt,
+                        unsigned long long* acc);
 void launch_linf(dynpr_context* ctx, const double* a, const double* b, uint64_t n, unsigned long long* out_bits);
 void launch_l1(dynpr_context* ctx, const double* a, const double* b, uint64_t n, double* partials, double* out);
 

@@ -293,3 +293,26 @@ def og_has(off, tgt, u, v):
     row = tgt[off[u]:off[u + 1]]
     i = np.searchsorted(row, v)
     return i < len(row) and row[i] == v
+
+
+def test_context_destroyed_before_its_graphs(dp):
+    """Finalisers of a garbage cycle run in any order: a context destroyed
+    while graphs still live defers its teardown to the last graph's
+    destroy (include/dynpr_cuda.h), so neither order crashes."""
+    for order in ("ctx_first", "graphs_first"):
+        ctx = dp.Context(0)
+        g = dp.build_csr([(0, 1), (1, 2), (2, 0)], 3, ctx=ctx)
+        gt = dp.transpose(g)
+        r = dp.static_pagerank(gt, g)
+        assert r.converged
+        if order == "ctx_first":
+            ctx._fin()
+            g._fin()
+            gt._fin()
+        else:
+            gt._fin()
+            g._fin()
+            ctx._fin()
+    # the default context is unaffected
+    g = dp.add_self_loops(dp.build_csr([(0, 1)], 2))
+    assert dp.static_pagerank(dp.transpose(g), g).converged

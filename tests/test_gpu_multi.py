@@ -173,3 +173,38 @@ def test_team_speculative_loop_limits(dp, oracle_lib, fused, max_it, check_off):
     for r in range(3):
         for k in single:
             same(out[r][k], single[k])
+
+
+@pytest.mark.parametrize("fused", [False, True], ids=["allgather", "fused-peer-stores"])
+def test_team_rejects_ranks_with_different_graphs(dp, oracle_lib, fused):
+    """A team sweeps ONE replicated graph.  Ranks holding different graphs of
+    the same size (same n and m, one edge moved) must all fail the solve
+    instead of combining ranges of different graphs; identical graphs pass."""
+    O = oracle_lib
+    og, _ = rand_pair(O, 31, 3000, 30000)
+    off, tgt = og.csr()
+    n = og.n
+    tgt_b = np.array(tgt, copy=True)
+    # move one edge of vertex 0 to a target it does not have yet (same n, m)
+    row = set(tgt_b[off[0]:off[1]].tolist())
+    new_t = next(t for t in range(1, n) if t not in row)
+    k = int(off[0]) + next(i for i, t in enumerate(tgt_b[off[0]:off[1]].tolist()) if t != 0)
+    tgt_b[k] = new_t
+    tgt_b[off[0]:off[1]] = np.sort(tgt_b[off[0]:off[1]])
+
+    def fn_for(graphs):
+        def fn(ctx, r):
+            h = dp.CsrGraph.from_csr(n, off, graphs[r], ctx=ctx)
+            ht = dp.transpose(h)
+            try:
+                return dp.static_pagerank(ht, h)
+            except ValueError as e:
+                return e
+        return fn
+
+    out, _ = run_team(dp, 2, fn_for([tgt, tgt_b]), fused_n=n if fused else 0)
+    assert all(isinstance(o, ValueError) and "different graphs" in str(o) for o in out), out
+    out, _ = run_team(dp, 2, fn_for([tgt, tgt]), fused_n=n if fused else 0)
+    single = dp.static_pagerank(dp.transpose(dp.CsrGraph.from_csr(n, off, tgt)), dp.CsrGraph.from_csr(n, off, tgt))
+    for o in out:
+        same(o, single)
