@@ -248,7 +248,7 @@ def run_reference(args, world, rank, local):
     line = {
         "impl": "reference", "metric": baseline_metric(), "value": value, "unit": "GTEPS", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / len(times),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic RMAT (Graph500 a=.57 b=c=.19, edge factor 16, seed %d, dedup + self-loops)" % args.seed,
         "config": {"workload": desc, "scale": scale, "n": n, "m": m, "alpha": 0.85, "tol": 1e-10},
         "cpu_baseline": {"value": value, "unit": "GTEPS", "cores": threads if kind == "reference" else 1,
