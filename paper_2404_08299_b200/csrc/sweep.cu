@@ -878,11 +878,10 @@ __global__ void k_collect_pending(const uint32_t* outdeg, const uint64_t* off, u
 // Push expansion (frontier.cpp:55-84) split by out-degree: thread per low
 // pending vertex, warp per 1024-edge item of a high one.  Byte stores of 1
 // are idempotent; the read-before-write keeps dense frontiers
-// from turning into L2 write traffic.
-__global__ void k_expand_low(const uint64_t* off, const uint32_t* tgt, const uint32_t* list, uint32_t cnt,
-                             uint8_t* va, const unsigned* dcnt, const int* gate) {
-  if (gate && *gate != kExpandPush) return;
-  if (dcnt) cnt = dcnt[0];
+// from turning into L2 write traffic.  (An 8-deep variant with more loads in
+// flight per thread was measured slower: profiles/r01/README.md.)
+__device__ __forceinline__ void expand_low_body(const uint64_t* off, const uint32_t* tgt, const uint32_t* list,
+                                                uint64_t cnt, uint8_t* va) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cnt;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t u = list[i];
@@ -893,10 +892,8 @@ __global__ void k_expand_low(const uint64_t* off, const uint32_t* tgt, const uin
     }
   }
 }
-__global__ void k_expand_high(const uint64_t* off, const uint32_t* tgt, const uint2* items, uint32_t cnt,
-                              uint8_t* va, const unsigned* dcnt, const int* gate) {
-  if (gate && *gate != kExpandPush) return;
-  if (dcnt) cnt = dcnt[1];
+__device__ __forceinline__ void expand_high_body(const uint64_t* off, const uint32_t* tgt, const uint2* items,
+                                                 uint64_t cnt, uint8_t* va) {
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / 32;
   const uint64_t nw = (uint64_t)gridDim.x * blockDim.x / 32;
   const unsigned lane = lane_id();
@@ -918,54 +915,28 @@ __global__ void k_expand_high(const uint64_t* off, const uint32_t* tgt, const ui
     }
   }
 }
+__global__ void k_expand_low(const uint64_t* off, const uint32_t* tgt, const uint32_t* list, uint32_t cnt,
+                             uint8_t* va, const unsigned* dcnt, const int* gate) {
+  if (gate && *gate != kExpandPush) return;
+  expand_low_body(off, tgt, list, dcnt ? dcnt[0] : cnt, va);
+}
+__global__ void k_expand_high(const uint64_t* off, const uint32_t* tgt, const uint2* items, uint32_t cnt,
+                              uint8_t* va, const unsigned* dcnt, const int* gate) {
+  if (gate && *gate != kExpandPush) return;
+  expand_high_body(off, tgt, items, dcnt ? dcnt[1] : cnt, va);
+}
+// device-loop variants: arguments from the constant-bank slot of half H
 template <int H>
 __global__ void k_expand_low_c(const unsigned* counts, const int* gate) {
   const SweepArgs* ap = &c_loop_args[H];
   if (gate && *gate != kExpandPush) return;
-  const unsigned cnt = counts[0];
-  const uint64_t* off = ap->offF;
-  const uint32_t* tgt = ap->tgtF;
-  const uint32_t* list = ap->pend_low;
-  uint8_t* va = ap->va;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cnt;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t u = list[i];
-    const uint64_t b = off[u], e = off[u + 1];
-    for (uint64_t k = b; k < e; ++k) {
-      const uint32_t w = tgt[k];
-      if (!va[w]) va[w] = 1;
-    }
-  }
+  expand_low_body(ap->offF, ap->tgtF, ap->pend_low, counts[0], ap->va);
 }
 template <int H>
 __global__ void k_expand_high_c(const unsigned* counts, const int* gate) {
   const SweepArgs* ap = &c_loop_args[H];
   if (gate && *gate != kExpandPush) return;
-  const unsigned cnt = counts[1];
-  const uint64_t* off = ap->offF;
-  const uint32_t* tgt = ap->tgtF;
-  const uint2* items = ap->pend_high;
-  uint8_t* va = ap->va;
-  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / 32;
-  const uint64_t nw = (uint64_t)gridDim.x * blockDim.x / 32;
-  const unsigned lane = lane_id();
-  for (uint64_t i = warp; i < cnt; i += nw) {
-    const uint2 it = items[i];
-    const uint64_t b = off[it.x] + (uint64_t)kExpandChunk * it.y;
-    const uint64_t e0 = off[it.x + 1];
-    const uint64_t e = b + kExpandChunk < e0 ? b + kExpandChunk : e0;
-    for (uint64_t k = b + lane; k < e; k += 32 * 4) {
-      uint32_t w[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) w[q] = k + 32 * q < e ? tgt[k + 32 * q] : 0xffffffffu;
-      uint8_t f[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) f[q] = w[q] != 0xffffffffu ? va[w[q]] : 1;
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (!f[q]) va[w[q]] = 1;
-    }
-  }
+  expand_high_body(ap->offF, ap->tgtF, ap->pend_high, counts[1], ap->va);
 }
 
 // ---- device-driven loop bookkeeping (engine.cpp:71-92) --------------------------------
