@@ -143,6 +143,13 @@ bool host_loop_forced() {
   const char* e = std::getenv("DYNPR_HOST_LOOP");
   return e && e[0] && e[0] != '0';
 }
+// Test hook: a 1-rank NCCL / LocalTeam context takes the team path (range
+// plan, collectives, speculative host loop) instead of the single-GPU one,
+// so the real transport code runs on a one-GPU box.
+bool team_forced() {
+  const char* e = std::getenv("DYNPR_FORCE_TEAM");
+  return e && e[0] && e[0] != '0';
+}
 
 // convergeLoop (engine.cpp:61-95) run entirely on the device: one CUDA graph
 // whose WHILE node repeats a two-iteration body (even sweep R0->R1, odd
@@ -323,7 +330,7 @@ void solve(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynpr_sta
   // peer-mapped buffers and each sweep stores its new values straight into
   // every rank's copy (fused exchange); otherwise they are all-gathered.
   Comm* comm = ctx->comm;
-  const bool dist = comm && comm->world > 1;
+  const bool dist = comm && (comm->world > 1 || team_forced());
   const bool fused = dist && (int)ctx->peer_cb[0].size() == comm->world && ctx->peer_capacity >= n;
   double* CB[2] = {fused ? ctx->peer_cb[0][comm->rank] : ctx->contrib[0].as<double>(n),
                    fused ? ctx->peer_cb[1][comm->rank] : ctx->contrib[1].as<double>(n)};

@@ -9,6 +9,7 @@ the reference's (tests/test_gpu_engine.py).  NCCL cannot put two ranks on
 one GPU, so the NCCL transport itself is exercised only on multi-GPU boxes
 (bench.py --gpus N).
 """
+import os
 import threading
 
 import numpy as np
@@ -208,3 +209,45 @@ def test_team_rejects_ranks_with_different_graphs(dp, oracle_lib, fused):
     single = dp.static_pagerank(dp.transpose(dp.CsrGraph.from_csr(n, off, tgt)), dp.CsrGraph.from_csr(n, off, tgt))
     for o in out:
         same(o, single)
+
+
+def test_nccl_context_single_rank(dp, oracle_lib):
+    """The NCCL plumbing of the one-process-per-GPU path on this one-GPU box:
+    libnccl is found, a 1-rank communicator initialises and is torn down
+    with its context, and solves through it equal the plain context's
+    (a 1-rank team sweeps the whole vertex range, no collectives)."""
+    ctx = dp.Context.nccl(0, 0, 1, dp.nccl_unique_id())
+    assert (ctx.rank, ctx.world) == (0, 1)
+    O = oracle_lib
+    og, _ = rand_pair(O, 37, 2000, 20000)
+    off, tgt = og.csr()
+    n = og.n
+    g = dp.CsrGraph.from_csr(n, off, tgt, ctx=ctx)
+    gt = dp.transpose(g)
+    p = dp.CsrGraph.from_csr(n, off, tgt)
+    pt = dp.transpose(p)
+    same(dp.static_pagerank(gt, g), dp.static_pagerank(pt, p))
+    # DYNPR_FORCE_TEAM: the 1-rank communicator takes the team path, so the
+    # real NCCL collectives (record all-reduce, broadcast-based all-gather,
+    # graph identity check) and the speculative host loop run here too
+    dels, ins = O.generate_random_batch(og, 30, 0.8, 5)
+    og2, _, _ = O.apply_batch(og, dels, ins)
+    off2, tgt2 = og2.csr()
+    g2 = dp.CsrGraph.from_csr(n, off2, tgt2, ctx=ctx)
+    gt2 = dp.transpose(g2)
+    p2 = dp.CsrGraph.from_csr(n, off2, tgt2)
+    pt2 = dp.transpose(p2)
+    base = dp.static_pagerank(pt, p)
+    want = {"static": dp.static_pagerank(pt2, p2),
+            "dfp": dp.dynamic_frontier(p2, pt2, dels, ins, base.ranks, pruning=True),
+            "dt": dp.dynamic_traversal(p2, pt2, dels, ins, base.ranks)}
+    os.environ["DYNPR_FORCE_TEAM"] = "1"
+    try:
+        got = {"static": dp.static_pagerank(gt2, g2),
+               "dfp": dp.dynamic_frontier(g2, gt2, dels, ins, base.ranks, pruning=True),
+               "dt": dp.dynamic_traversal(g2, gt2, dels, ins, base.ranks)}
+    finally:
+        del os.environ["DYNPR_FORCE_TEAM"]
+    for k in want:
+        same(got[k], want[k])
+    del g, gt, g2, gt2
