@@ -123,12 +123,23 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+# DYNPR_FORCE_TEAM=1 (a test hook of the library, engine.cu team_forced):
+# at N = 1 the bench still builds the NCCL team context and the fused
+# exchange, and the library runs its team path, so the code the driver's
+# N > 1 runs depend on is exercised on a one-GPU box.  Not a bench number.
+FORCE_TEAM = os.environ.get("DYNPR_FORCE_TEAM", "0") not in ("", "0")
+
+
 def dist_setup(backend: str):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if world > 1 or (FORCE_TEAM and backend == "nccl"):
         import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        os.environ.setdefault("RANK", str(rank))
+        os.environ.setdefault("WORLD_SIZE", str(world))
         dist.init_process_group(backend)
     return world, rank, local
 
@@ -273,7 +284,8 @@ def run_ours(args, world, rank, local):
     # vertex range; contributions / pending flags are all-gathered over
     # NVLink after every sweep.  Same graph for every N: strong
     # scaling.
-    ctx = dp.Context(local) if world == 1 else dp.context_from_process_group(local)
+    team = world > 1 or FORCE_TEAM
+    ctx = dp.context_from_process_group(local) if team else dp.Context(local)
     L = N.lib()
 
     # ---- setup (untimed): base graph pair, base ranks, batches ---------------
@@ -282,7 +294,7 @@ def run_ours(args, world, rank, local):
     n, m0 = g0.vertex_count, g0.edge_count
     exchange = "none (single GPU)"
     symm_keep = None
-    if world > 1:
+    if team:
         # fused exchange: contributions stored straight into every rank's
         # peer-mapped buffer by the sweep epilogue (torch symmetric memory
         # for the IPC plumbing); the NCCL all-gather is the fallback
@@ -509,7 +521,7 @@ def main():
         run_reference(args, world, rank, local)
     else:
         run_ours(args, world, rank, local)
-    if world > 1:
+    if world > 1 or (FORCE_TEAM and args.impl != "reference"):
         import torch.distributed as dist
         dist.destroy_process_group()
 

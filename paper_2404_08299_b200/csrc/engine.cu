@@ -95,18 +95,22 @@ SweepRed read_red(dynpr_context* ctx, const SweepRed* d) {
 // or the ranges it sweeps belong to different graphs.  The content
 // fingerprint of the pair (both CSRs) is computed once per layout; every
 // team solve all-reduces it (max and sum agree only if all ranks match).
+void ensure_fingerprint(dynpr_context* ctx, Layout* L, const dynpr_graph* gT, const dynpr_graph* gF) {
+  if (L->fingerprint) return;
+  SweepRed* red = ctx->red.as<SweepRed>(2);
+  DYNPR_CK(cudaMemsetAsync(red, 0, sizeof(SweepRed), ctx->stream));
+  auto* acc = reinterpret_cast<unsigned long long*>(&red->delta_bits);
+  launch_fingerprint(ctx, reinterpret_cast<const uint32_t*>(gT->off), 2 * ((uint64_t)gT->n + 1), 1ull << 40, acc);
+  launch_fingerprint(ctx, gT->tgt, gT->m, 2ull << 40, acc);
+  launch_fingerprint(ctx, reinterpret_cast<const uint32_t*>(gF->off), 2 * ((uint64_t)gF->n + 1), 3ull << 40, acc);
+  launch_fingerprint(ctx, gF->tgt, gF->m, 4ull << 40, acc);
+  const uint64_t fp = read_red(ctx, red).delta_bits;
+  L->fingerprint = fp ? fp : 1;
+}
+
 void team_check_graph(dynpr_context* ctx, Comm* comm, Layout* L, const dynpr_graph* gT, const dynpr_graph* gF,
                       SweepRed* red) {
-  if (!L->fingerprint) {
-    DYNPR_CK(cudaMemsetAsync(red, 0, sizeof(SweepRed), ctx->stream));
-    auto* acc = reinterpret_cast<unsigned long long*>(&red->delta_bits);
-    launch_fingerprint(ctx, reinterpret_cast<const uint32_t*>(gT->off), 2 * ((uint64_t)gT->n + 1), 1ull << 40, acc);
-    launch_fingerprint(ctx, gT->tgt, gT->m, 2ull << 40, acc);
-    launch_fingerprint(ctx, reinterpret_cast<const uint32_t*>(gF->off), 2 * ((uint64_t)gF->n + 1), 3ull << 40, acc);
-    launch_fingerprint(ctx, gF->tgt, gF->m, 4ull << 40, acc);
-    const uint64_t fp = read_red(ctx, red).delta_bits;
-    L->fingerprint = fp ? fp : 1;
-  }
+  ensure_fingerprint(ctx, L, gT, gF);
   SweepRed rec{};
   rec.delta_bits = L->fingerprint;
   rec.processed = L->fingerprint;
@@ -797,6 +801,12 @@ dynpr_status dynpr_graph_prepare(dynpr_context* ctx, const dynpr_graph* gT, cons
     bind_device(ctx);
     const Layout* L = get_layout(ctx, gT, gF, threshold, with_forward != 0);
     if (build_ms) *build_ms = L->build_ms;
+    // a team's per-snapshot work (edge-balanced range plan, graph
+    // fingerprint) belongs to the snapshot build, not to the first solve
+    if (ctx->comm && (ctx->comm->world > 1 || team_forced())) {
+      plan_ranges(ctx, const_cast<Layout*>(L), ctx->comm->world);
+      ensure_fingerprint(ctx, const_cast<Layout*>(L), gT, gF);
+    }
   });
 }
 

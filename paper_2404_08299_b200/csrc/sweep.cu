@@ -42,6 +42,9 @@
 #include <string>
 #include <utility>
 
+#include <cub/device/device_scan.cuh>
+#include <cub/iterator/transform_input_iterator.cuh>
+
 #include "sweep.cuh"
 
 namespace dynpr_b200 {
@@ -1192,28 +1195,57 @@ SweepArgs layout_args(const Layout* L, double* partials) {
   return a;
 }
 
+struct WidenU32 {
+  __host__ __device__ unsigned long long operator()(uint32_t x) const { return x; }
+};
+// cut[r] (0 < r < world): after the first vertex v whose inclusive in-degree
+// prefix reaches r/world of the edges, rounded up to a whole single-region
+// slice; n if none does.
+__global__ void k_plan_cuts(const unsigned long long* prefix, uint32_t n, uint32_t M, uint64_t m, int world,
+                            uint32_t* cut) {
+  const int r = (int)threadIdx.x + 1;
+  if (r >= world) return;
+  const unsigned long long goal = (unsigned long long)m * (unsigned long long)r;
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint32_t mid = lo + (hi - lo) / 2;
+    if (prefix[mid] * (unsigned long long)world >= goal) hi = mid; else lo = mid + 1;
+  }
+  uint32_t c = n;
+  if (lo < n) {
+    c = lo + 1;
+    if (c > M) c = M + ((c - M + 31) / 32) * 32;
+    if (c > n) c = n;
+  }
+  cut[r] = c;
+}
+
 std::vector<RankRange> plan_ranges(dynpr_context* ctx, Layout* L, int world) {
   if (L->plan_world == world) return L->plan;
   const uint32_t n = L->n, M = L->M;
-  std::vector<uint32_t> indeg(n), pbase((size_t)M + 1);
-  DYNPR_CK(cudaMemcpy(indeg.data(), L->indeg, (size_t)n * 4, cudaMemcpyDeviceToHost));
-  DYNPR_CK(cudaMemcpy(pbase.data(), L->pbase, ((size_t)M + 1) * 4, cudaMemcpyDeviceToHost));
-  (void)ctx;
-  // boundaries at equal shares of the in-edges (each owned edge is one gather)
-  std::vector<uint32_t> cut(world + 1, 0);
+  // boundaries at equal shares of the in-edges (each owned edge is one
+  // gather): an in-degree prefix scan and one binary search per boundary on
+  // the device; only the world + 1 cuts and the multi-vertex chunk bases
+  // come back
+  std::vector<uint32_t> cut(world + 1, 0), pbase((size_t)M + 1);
   cut[world] = n;
-  uint64_t acc = 0;
-  int r = 1;
-  for (uint32_t v = 0; v < n && r < world; ++v) {
-    acc += indeg[v];
-    while (r < world && acc * (uint64_t)world >= L->m * (uint64_t)r) {
-      uint32_t c = v + 1;
-      if (c > M) c = M + ((c - M + 31) / 32) * 32;  // whole single-region slices
-      if (c > n) c = n;
-      cut[r++] = c;
-    }
+  if (world > 1 && n) {
+    auto* prefix = ctx->plan_prefix.as<unsigned long long>((uint64_t)n + 64);
+    auto* dcut = reinterpret_cast<uint32_t*>(prefix + n);
+    if (world > 128) throw Error(DYNPR_INVALID_ARGUMENT, "team larger than 128 ranks");
+    // 64-bit accumulation (m may exceed 2^32)
+    cub::TransformInputIterator<unsigned long long, WidenU32, const uint32_t*> deg(L->indeg, WidenU32{});
+    size_t bytes = 0;
+    DYNPR_CK(cub::DeviceScan::InclusiveSum(nullptr, bytes, deg, prefix, (int64_t)n, ctx->stream));
+    void* tmp = ctx->cub_tmp.ensure(bytes);
+    DYNPR_CK(cub::DeviceScan::InclusiveSum(tmp, bytes, deg, prefix, (int64_t)n, ctx->stream));
+    k_plan_cuts<<<1, 128, 0, ctx->stream>>>(prefix, n, M, L->m, world, dcut);
+    check_launch();
+    DYNPR_CK(cudaMemcpyAsync(cut.data() + 1, dcut + 1, (size_t)(world - 1) * 4, cudaMemcpyDeviceToHost,
+                             ctx->stream));
   }
-  while (r < world) cut[r++] = n;
+  DYNPR_CK(cudaMemcpyAsync(pbase.data(), L->pbase, ((size_t)M + 1) * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  DYNPR_CK(cudaStreamSynchronize(ctx->stream));
   for (int i = 1; i <= world; ++i)
     if (cut[i] < cut[i - 1]) cut[i] = cut[i - 1];
   std::vector<RankRange> plan(world);
