@@ -251,3 +251,22 @@ def test_nccl_context_single_rank(dp, oracle_lib):
     for k in want:
         same(got[k], want[k])
     del g, gt, g2, gt2
+
+
+@pytest.mark.parametrize("n", [1, 5, 40, 97])
+def test_tiny_graphs_on_a_wide_team(dp, n):
+    """Range plan edge cases (device prefix scan + binary search): fewer
+    vertices or slices than ranks leaves trailing ranks empty; every rank
+    still returns exactly the single-GPU result."""
+    edges = [(u, (u * 7 + 3) % n) for u in range(n)] + [(u, (u + 1) % n) for u in range(0, n, 3)]
+    g = dp.add_self_loops(dp.build_csr(edges, n))
+    gt = dp.transpose(g)
+    single = dp.static_pagerank(gt, g)
+
+    def fn(ctx, r):
+        h = dp.add_self_loops(dp.build_csr(edges, n, ctx=ctx))
+        return dp.static_pagerank(dp.transpose(h), h)
+
+    out, _ = run_team(dp, 4, fn)
+    for o in out:
+        same(o, single)
