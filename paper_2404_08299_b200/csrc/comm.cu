@@ -114,6 +114,7 @@ struct LocalTeam {
   uint64_t generation = 0;
   void* staging = nullptr;
   size_t staging_bytes = 0;
+  bool aborted = false;
   std::vector<SweepRed> reds;
   explicit LocalTeam(int w) : world(w), reds(w) {}
   ~LocalTeam() {
@@ -121,14 +122,21 @@ struct LocalTeam {
   }
   void barrier() {
     std::unique_lock<std::mutex> lk(m);
+    if (aborted) throw Error(DYNPR_RUNTIME_ERROR, "team: another rank failed");
     const uint64_t gen = generation;
     if (++arrived == world) {
       arrived = 0;
       ++generation;
       cv.notify_all();
     } else {
-      cv.wait(lk, [&] { return generation != gen; });
+      cv.wait(lk, [&] { return generation != gen || aborted; });
+      if (generation == gen) throw Error(DYNPR_RUNTIME_ERROR, "team: another rank failed");
     }
+  }
+  void abort() {
+    std::lock_guard<std::mutex> lk(m);
+    aborted = true;
+    cv.notify_all();
   }
 };
 
@@ -183,6 +191,7 @@ class LocalComm final : public Comm {
     DYNPR_CK(cudaStreamSynchronize(st));
   }
   void barrier() override { team_->barrier(); }
+  void abort() override { team_->abort(); }
 
  private:
   std::shared_ptr<LocalTeam> team_;

@@ -30,6 +30,10 @@ class Comm {
   // In place on a device SweepRed: delta_bits max, the counters summed.
   virtual void allreduce_red(SweepRed* red, cudaStream_t st) = 0;
   virtual void barrier() = 0;
+  // A rank that fails between collectives calls abort(): ranks blocked in
+  // (or later entering) a host-side barrier of the team throw instead of
+  // waiting forever.  No-op for NCCL (its collectives are stream-ordered).
+  virtual void abort() {}
 };
 
 // 128-byte NCCL unique id (ncclUniqueId) from the rank-0 process.

@@ -317,8 +317,8 @@ void run_device_loop(dynpr_context* ctx, const SolveSpec& sp, const SweepArgs& a
 
 // convergeLoop (engine.cu:61-95) on the device, in the layout's new-id
 // space; inputs are permuted in and the result permuted back out.
-void solve(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynpr_stats* stats,
-           dynpr_observer obs, void* user) {
+void solve_impl(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynpr_stats* stats,
+                dynpr_observer obs, void* user) {
   const dynpr_graph* gT = sp.gT;
   const dynpr_graph* gF = sp.gF;
   const dynpr_config& c = *sp.cfg;
@@ -583,6 +583,18 @@ void solve(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynpr_sta
   DYNPR_CK(cudaEventElapsedTime(&ms, ctx->ev_a, ctx->ev_b));
   res.device_ms = ms;
   if (stats) *stats = res;
+}
+
+// A team rank that fails mid-solve releases the others (host-side barriers
+// of the team throw instead of waiting for it), then rethrows.
+void solve(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynpr_stats* stats, dynpr_observer obs,
+           void* user) {
+  try {
+    solve_impl(ctx, sp, ranks_out, stats, obs, user);
+  } catch (...) {
+    if (ctx->comm && (ctx->comm->world > 1 || team_forced())) ctx->comm->abort();
+    throw;
+  }
 }
 
 }  // namespace
@@ -998,6 +1010,10 @@ dynpr_status dynpr_static_pagerank_csr(dynpr_context* ctx, uint32_t n, const uin
       gF.finish();  // an invalid gF would have failed at construction, first
       throw;
     }
+    // A team fingerprints both CSRs of the pair (team_check_graph) on the
+    // main stream: gF's targets must have landed (and be valid) first, so a
+    // team joins the side upload before the solve instead of after it.
+    if (ctx->comm && (ctx->comm->world > 1 || team_forced())) gF.finish();
     SolveSpec sp;
     sp.gT = gT;
     sp.gF = gF.g;

@@ -838,116 +838,141 @@ struct Runner {
   }
 };
 
-// harness.cpp:56-66
-double geometric_mean(const std::vector<double>& values) {
-  if (values.empty()) return 0.0;
-  double log_sum = 0.0;
-  for (double v : values) {
-    if (!(v > 0.0)) return 0.0;
-    log_sum += std::log(v);
-  }
-  return std::exp(log_sum / static_cast<double>(values.size()));
-}
+// summarizeRows (harness.cpp:56-113): one summary row per (approach, batch
+// size spec), in order of first appearance.  Means are accumulated in row
+// order as the rows stream past: the geometric means as running log sums
+// (exp(sum / count), 0 once a non-positive value is seen), the counters as
+// running sums rounded at the end; NaN errors are left out of the error mean
+// and a group without errors reports NaN.
+struct RunningSummary {
+  std::string graph, approach, spec;
+  uint64_t rows = 0;
+  double log_runtime = 0.0;
+  bool runtime_nonpositive = false;
+  uint64_t errors = 0;
+  double log_error = 0.0;
+  bool error_nonpositive = false;
+  double iterations = 0.0, affected = 0.0;
+  bool converged = true;
 
-// harness.cpp:68-113 summarizeRows
+  static void add_log(double v, double& log_sum, bool& nonpositive) {
+    if (v > 0.0)
+      log_sum += std::log(v);
+    else
+      nonpositive = true;
+  }
+  void add(const dynpr_report::Row& r) {
+    ++rows;
+    add_log(r.runtime, log_runtime, runtime_nonpositive);
+    if (!std::isnan(r.l1)) {
+      ++errors;
+      add_log(r.l1, log_error, error_nonpositive);
+    }
+    iterations += static_cast<double>(r.iterations);
+    affected += static_cast<double>(r.affected);
+    converged = converged && r.converged;
+  }
+  static double geo(uint64_t count, double log_sum, bool nonpositive) {
+    return (count == 0 || nonpositive) ? 0.0 : std::exp(log_sum / static_cast<double>(count));
+  }
+  dynpr_report::Row row() const {
+    dynpr_report::Row s;
+    s.graph = graph;
+    s.approach = approach;
+    s.spec = spec;
+    s.batch_index = -1;
+    s.runtime = geo(rows, log_runtime, runtime_nonpositive);
+    s.l1 = errors ? geo(errors, log_error, error_nonpositive) : std::nan("");
+    s.iterations = static_cast<int64_t>(std::llround(iterations / static_cast<double>(rows)));
+    s.affected = static_cast<uint64_t>(std::llround(affected / static_cast<double>(rows)));
+    s.converged = converged;
+    return s;
+  }
+};
+
 std::vector<dynpr_report::Row> summarize(const std::vector<dynpr_report::Row>& rows) {
-  std::vector<std::pair<std::string, std::string>> order;
-  std::map<std::pair<std::string, std::string>, std::vector<const dynpr_report::Row*>> groups;
+  std::vector<RunningSummary> groups;  // a handful: (approach, spec) pairs
   for (const auto& r : rows) {
-    auto key = std::make_pair(r.approach, r.spec);
-    auto [it, inserted] = groups.emplace(key, std::vector<const dynpr_report::Row*>{});
-    if (inserted) order.push_back(key);
-    it->second.push_back(&r);
+    auto g = std::find_if(groups.begin(), groups.end(),
+                          [&](const RunningSummary& x) { return x.approach == r.approach && x.spec == r.spec; });
+    if (g == groups.end()) {
+      groups.emplace_back();
+      g = groups.end() - 1;
+      g->graph = r.graph;
+      g->approach = r.approach;
+      g->spec = r.spec;
+    }
+    g->add(r);
   }
   std::vector<dynpr_report::Row> out;
-  for (const auto& key : order) {
-    const auto& g = groups[key];
-    dynpr_report::Row s;
-    s.graph = g.front()->graph;
-    s.approach = key.first;
-    s.spec = key.second;
-    s.batch_index = -1;
-    std::vector<double> runtimes, errors;
-    double iter_sum = 0.0, affected_sum = 0.0;
-    bool all = true;
-    for (const auto* r : g) {
-      runtimes.push_back(r->runtime);
-      if (!std::isnan(r->l1)) errors.push_back(r->l1);
-      iter_sum += static_cast<double>(r->iterations);
-      affected_sum += static_cast<double>(r->affected);
-      all = all && r->converged;
-    }
-    s.runtime = geometric_mean(runtimes);
-    s.l1 = errors.empty() ? std::nan("") : geometric_mean(errors);
-    s.iterations = static_cast<int64_t>(std::llround(iter_sum / static_cast<double>(g.size())));
-    s.affected = static_cast<uint64_t>(std::llround(affected_sum / static_cast<double>(g.size())));
-    s.converged = all;
-    out.push_back(std::move(s));
-  }
+  out.reserve(groups.size());
+  for (const auto& g : groups) out.push_back(g.row());
   return out;
 }
 
-void fmt_double(std::string& out, double v) {  // harness.cpp:272-276
-  char buf[64];
+// Report schema (proj/README.md:89-115; writers harness.cpp:241-352): nine
+// columns, floats as %.17g, a NaN error as an empty CSV field / JSON null.
+// Each row is first turned into its nine (name, text, quoted) cells; the CSV
+// and JSON writers only differ in how they join them.
+struct Cell {
+  const char* name;
+  std::string text;
+  bool quoted;  // JSON string value
+};
+
+std::string g17(double v) {
+  char buf[40];
   std::snprintf(buf, sizeof buf, "%.17g", v);
-  out += buf;
+  return buf;
 }
 
-std::string escape_json(const std::string& s) {
-  std::string out;
+std::vector<Cell> cells_of(const dynpr_report::Row& r) {
+  return {{"graphName", r.graph, true},
+          {"approach", r.approach, true},
+          {"batchSizeSpec", r.spec, true},
+          {"batchIndex", std::to_string(r.batch_index), false},
+          {"runtimeMillis", g17(r.runtime), false},
+          {"iterations", std::to_string(r.iterations), false},
+          {"affectedVertexIterations", std::to_string(r.affected), false},
+          {"l1ErrorVsReference", std::isnan(r.l1) ? std::string() : g17(r.l1), false},
+          {"converged", r.converged ? "true" : "false", false}};
+}
+
+std::string json_quote(const std::string& s) {
+  std::string q = "\"";
   for (char c : s) {
-    if (c == '"' || c == '\\') out += '\\';
-    out += c;
+    if (c == '"' || c == '\\') q += '\\';
+    q += c;
   }
-  return out;
+  return q + '"';
 }
 
-// harness.cpp:287-316 writeCsv / 318-352 writeJson
 std::string render(const std::vector<dynpr_report::Row>& rows, int32_t format) {
+  const bool csv = format == DYNPR_REPORT_CSV;
   std::string out;
-  if (format == DYNPR_REPORT_CSV) {
-    out += "graphName,approach,batchSizeSpec,batchIndex,runtimeMillis,"
-           "iterations,affectedVertexIterations,l1ErrorVsReference,converged\n";
-    for (const auto& r : rows) {
-      out += r.graph;
-      out += ',';
-      out += r.approach;
-      out += ',';
-      out += r.spec;
-      out += ',';
-      out += std::to_string(r.batch_index);
-      out += ',';
-      fmt_double(out, r.runtime);
-      out += ',';
-      out += std::to_string(r.iterations);
-      out += ',';
-      out += std::to_string(r.affected);
-      out += ',';
-      if (!std::isnan(r.l1)) fmt_double(out, r.l1);
-      out += ',';
-      out += r.converged ? "true" : "false";
-      out += '\n';
-    }
+  if (csv) {
+    const dynpr_report::Row header_row{};
+    const auto header = cells_of(header_row);
+    for (size_t i = 0; i < header.size(); ++i) out += std::string(i ? "," : "") + header[i].name;
+    out += '\n';
   } else {
     out += "[\n";
-    for (size_t i = 0; i < rows.size(); ++i) {
-      const auto& r = rows[i];
-      out += "  {\"graphName\":\"" + escape_json(r.graph) + "\",\"approach\":\"" + escape_json(r.approach) +
-             "\",\"batchSizeSpec\":\"" + escape_json(r.spec) + "\",\"batchIndex\":" +
-             std::to_string(r.batch_index) + ",\"runtimeMillis\":";
-      fmt_double(out, r.runtime);
-      out += ",\"iterations\":" + std::to_string(r.iterations) +
-             ",\"affectedVertexIterations\":" + std::to_string(r.affected) + ",\"l1ErrorVsReference\":";
-      if (std::isnan(r.l1))
-        out += "null";
-      else
-        fmt_double(out, r.l1);
-      out += ",\"converged\":";
-      out += r.converged ? "true" : "false";
-      out += i + 1 < rows.size() ? "},\n" : "}\n";
-    }
-    out += "]\n";
   }
+  for (size_t k = 0; k < rows.size(); ++k) {
+    const auto cells = cells_of(rows[k]);
+    if (!csv) out += "  {";
+    for (size_t i = 0; i < cells.size(); ++i) {
+      if (i) out += ',';
+      if (csv) {
+        out += cells[i].text;
+      } else {
+        out += json_quote(cells[i].name) + ':';
+        out += cells[i].quoted ? json_quote(cells[i].text) : (cells[i].text.empty() ? "null" : cells[i].text);
+      }
+    }
+    out += csv ? "\n" : (k + 1 < rows.size() ? "},\n" : "}\n");
+  }
+  if (!csv) out += "]\n";
   return out;
 }
 

@@ -16,10 +16,12 @@ void cub_call(dynpr_context* ctx, F&& f) {
   DYNPR_CK(f(tmp, bytes));
 }
 
-dynpr_context* g_alloc_ctx = nullptr;  // set for the duration of a build
+// Layout arrays come from the building context's pool (explicit, so
+// contexts building layouts concurrently on several host threads never
+// share allocation state).
 template <class T>
-T* dalloc(uint64_t count) {
-  return pool_alloc_n<T>(g_alloc_ctx, count ? count : 1);
+T* dalloc(dynpr_context* ctx, uint64_t count) {
+  return pool_alloc_n<T>(ctx, count ? count : 1);
 }
 
 #define GRID_STRIDE(i, count)                                                      \
@@ -214,9 +216,8 @@ uint64_t read_u64(dynpr_context* ctx, const void* d) {
 
 void build_forward(dynpr_context* ctx, Layout* L, const dynpr_graph* gF) {
   cudaStream_t st = ctx->stream;
-  g_alloc_ctx = ctx;
-  L->offF = dalloc<uint64_t>((uint64_t)L->n + 1);
-  L->tgtF = dalloc<uint32_t>(L->m);
+  L->offF = dalloc<uint64_t>(ctx, (uint64_t)L->n + 1);
+  L->tgtF = dalloc<uint32_t>(ctx, L->m);
   k_outdeg64<<<grid(ctx, (uint64_t)L->n + 1), 256, 0, st>>>(L->outdeg, L->n, L->offF);
   check_launch();
   cub_call(ctx, [&](void* t, size_t& b) {
@@ -234,17 +235,16 @@ Layout* build_layout(dynpr_context* ctx, const dynpr_graph* gT, const dynpr_grap
   const uint32_t n = gT->n;
   auto* L = new Layout();
   L->ctx = ctx;
-  g_alloc_ctx = ctx;
   uint32_t* tmp = nullptr;
   try {
     L->n = n;
     L->m = gT->m;
     L->T = T;
     L->gF_id = gF->id;
-    L->perm = dalloc<uint32_t>(n);
-    L->inv = dalloc<uint32_t>(n);
-    L->indeg = dalloc<uint32_t>(n);
-    L->outdeg = dalloc<uint32_t>(n);
+    L->perm = dalloc<uint32_t>(ctx, n);
+    L->inv = dalloc<uint32_t>(ctx, n);
+    L->indeg = dalloc<uint32_t>(ctx, n);
+    L->outdeg = dalloc<uint32_t>(ctx, n);
     // temporaries from the pool (the context's stage buffers may hold the
     // caller's staged inputs when the build happens inside an engine call)
     // temporaries in a context-owned grow-only buffer: a pool allocation of
@@ -296,20 +296,20 @@ Layout* build_layout(dynpr_context* ctx, const dynpr_graph* gT, const dynpr_grap
       const uint32_t nh = (uint32_t)(read_u64(ctx, cnt) & 0xffffffffu);
       L->n_hslices = nh > M ? ((uint64_t)(nh - M) + 31) / 32 : 0;
     }
-    L->mcount = dalloc<uint32_t>((uint64_t)M + 1);
+    L->mcount = dalloc<uint32_t>(ctx, (uint64_t)M + 1);
     DYNPR_CK(cudaMemsetAsync(L->mcount, 0, ((size_t)M + 1) * 4, st));
     // single region slices
     L->n_sslices = ((uint64_t)(n - M) + 31) / 32;
-    L->sbase = dalloc<uint64_t>(L->n_sslices + 1);
+    L->sbase = dalloc<uint64_t>(ctx, L->n_sslices + 1);
     k_single_slice_len<<<grid(ctx, L->n_sslices + 1), 256, 0, st>>>(L->indeg, M, n, L->n_sslices, L->sbase);
     check_launch();
     cub_call(ctx, [&](void* t, size_t& b) {
       return cub::DeviceScan::ExclusiveSum(t, b, L->sbase, L->sbase, (int64_t)L->n_sslices + 1, st);
     });
     const uint64_t sell_s_len = read_u64(ctx, L->sbase + L->n_sslices);
-    L->sell_s = dalloc<uint32_t>(sell_s_len);
+    L->sell_s = dalloc<uint32_t>(ctx, sell_s_len);
     // multi region segments
-    L->pbase = dalloc<uint32_t>((uint64_t)M + 1);
+    L->pbase = dalloc<uint32_t>(ctx, (uint64_t)M + 1);
     k_multi_nch<<<grid(ctx, (uint64_t)M + 1), 256, 0, st>>>(L->indeg, M, L->pbase);
     check_launch();
     cub_call(ctx, [&](void* t, size_t& b) {
@@ -322,10 +322,10 @@ Layout* build_layout(dynpr_context* ctx, const dynpr_graph* gT, const dynpr_grap
       std::memcpy(&h, ctx->pinned, 4);
       L->n_mseg = h;
     }
-    L->mseg_v = dalloc<uint32_t>(L->n_mseg);
-    L->mseg_len = dalloc<uint32_t>(L->n_mseg);
+    L->mseg_v = dalloc<uint32_t>(ctx, L->n_mseg);
+    L->mseg_len = dalloc<uint32_t>(ctx, L->n_mseg);
     L->n_mslices = (L->n_mseg + 31) / 32;
-    L->mbase = dalloc<uint64_t>(L->n_mslices + 1);
+    L->mbase = dalloc<uint64_t>(ctx, L->n_mslices + 1);
     if (M) {
       k_multi_segments<<<grid(ctx, M), 256, 0, st>>>(L->indeg, M, L->pbase, L->mseg_v, L->mseg_len);
       check_launch();
@@ -337,7 +337,7 @@ Layout* build_layout(dynpr_context* ctx, const dynpr_graph* gT, const dynpr_grap
       return cub::DeviceScan::ExclusiveSum(t, b, L->mbase, L->mbase, (int64_t)L->n_mslices + 1, st);
     });
     const uint64_t sell_m_len = read_u64(ctx, L->mbase + L->n_mslices);
-    L->sell_m = dalloc<uint32_t>(sell_m_len);
+    L->sell_m = dalloc<uint32_t>(ctx, sell_m_len);
     if (L->n_sslices) {
       k_fill_single<<<grid(ctx, L->n_sslices * 32), 256, 0, st>>>(gT->off, gT->tgt, L->perm, L->inv, L->indeg, M, n,
                                                                  L->n_sslices, L->sbase, L->sell_s);
@@ -368,6 +368,10 @@ Layout::~Layout() {
 void destroy_layout(Layout* L) { delete L; }
 
 Layout* get_layout(dynpr_context* ctx, const dynpr_graph* gT, const dynpr_graph* gF, uint32_t T, bool need_forward) {
+  // The layout is cached on gT and freed with it through its context's pool:
+  // build it only with the context that owns both graphs (a layout built by
+  // another context could outlive that context, or sit on another device).
+  if (gT->ctx != ctx || gF->ctx != ctx) invalid("engine: the graphs belong to another context");
   Layout* L = gT->layout;
   if (!L || L->gF_id != gF->id || L->T != T) {
     if (L) {
