@@ -23,7 +23,13 @@ DF-P PageRank (warm-started from the base ranks) solve the updated graph.
              on a bounded sample of the same workload
 
 --impl reference runs the unmodified reference CPU library through its own
-public API (staticPageRank) on the box's host cores, same metric and unit.
+public API (staticPageRank) on the box's host cores, same metric and unit, on
+the graph the device arm solves at its first timed step, built without the
+product library (oracle/bench_input.c); see run_reference.
+
+--gpus N > 1 outside torchrun re-launches this script under
+torch.distributed.run with N ranks (one GPU each); it fails if fewer GPUs
+are visible, and under torchrun WORLD_SIZE must equal N.
 """
 from __future__ import annotations
 
@@ -196,75 +202,130 @@ def barrier(world: int):
 
 
 # ---------------------------------------------------------------------------
-def cpu_reference_static(gF_host, gT_host, sweeps: int, threads: int):
-    """The reference library on host cores: `sweeps` static sweeps of
-    staticPageRank (maxIterations bounds the sample).  Returns
-    (GTEPS, ms, kind, ranks)."""
+def _ref_oracle(threads: int):
     import oracle
     kind = "reference" if oracle.available("ref") else "port"
     O = oracle.Oracle("ref" if kind == "reference" else "port")
     O.set_threads(threads)
+    return O, kind, (threads if kind == "reference" else 1)
+
+
+def workload_config(args, n, m_base, size):
+    scale, desc = WORKLOADS[args.workload]
+    return {"workload": desc, "scale": scale, "n": n, "m_base": m_base, "alpha": 0.85, "tol": 1e-10,
+            "batch_fraction": args.batch_frac, "batch_size": size,
+            "l2": "inputs larger than L2 (graph pair %.2f GB vs 126 MB L2); no flush needed"
+                  % ((2 * (8 * (n + 1) + 4 * m_base)) / 1e9)}
+
+
+def cpu_reference_full(gF_host, gT_host, base_ranks, batch, threads: int):
+    """The reference library on the host cores (cpu_baseline leg): ONE full
+    converged staticPageRank on the step's updated graph (partition, init and
+    every sweep inside the timed call, harness.cpp:222-224), then one
+    dynamicFrontier(pruning) on it from the base ranks.  Returns a dict."""
+    O, kind, cores = _ref_oracle(threads)
     n = len(gF_host[0]) - 1
     gF = O.graph_from_csr(n, *gF_host)
     gT = O.graph_from_csr(n, *gT_host)
-    cfg = oracle.default_config(max_iterations=sweeps, convergence_check_disabled=1)
-    O.static(gT, gF, cfg)  # warm-up (page-in)
     t0 = time.perf_counter()
-    r = O.static(gT, gF, cfg)
-    ms = (time.perf_counter() - t0) * 1e3
-    gteps = gF.m * r.iterations / (ms * 1e-3) / 1e9
-    return gteps, ms, kind, r.ranks, (threads if kind == "reference" else 1)
+    r = O.static(gT, gF)
+    st_ms = (time.perf_counter() - t0) * 1e3
+    (ds, dd), (is_, id_) = batch
+    t0 = time.perf_counter()
+    d = O.dynamic_frontier(gF, gT, (ds, dd), (is_, id_), base_ranks, pruning=True)
+    dfp_ms = (time.perf_counter() - t0) * 1e3
+    return {"kind": kind, "cores": cores, "static_ms": st_ms, "static_it": r.iterations, "ranks": r.ranks,
+            "gteps": gF.m * r.iterations / (st_ms * 1e-3) / 1e9, "dfp_ms": dfp_ms, "dfp_it": d.iterations,
+            "dfp_ranks": d.ranks}
 
 
 def run_reference(args, world, rank, local):
-    """--impl reference: the unmodified reference CPU library, rank 0 only."""
+    """--impl reference: the unmodified reference CPU library (oracle/_ref,
+    OpenMP, every host core) through its public API, rank 0 only.  Its input
+    is built without the product library: the oracle's multithreaded RMAT
+    generator + buildCsr/addSelfLoops restatement (oracle/bench_input.c, the
+    bytes of the device generator), handed to the reference through its
+    validating CsrGraph(n, offsets, targets) constructor; the batch is the
+    reference's own generateRandomBatch and applyBatch.  The graph solved is
+    the one the device arm solves at its first timed step.
+
+    Per step: staticPageRank (partition + init + sweeps inside the call) with
+    maxIterations bounded so the K timed steps take about --ref-budget-s
+    seconds; before them, one full converged staticPageRank on the updated
+    graph and one full dynamicFrontier(pruning) are timed once and reported."""
     if rank != 0:
         return
-    import numpy as np
-
     import oracle
-    import paper_2404_08299_b200 as dp
     scale, desc = WORKLOADS[args.workload]
     threads = os.cpu_count() or 1
-    # Input preparation only (not timed, not the reference's code path): the
-    # RMAT graph is generated on the device and handed over through the
-    # reference's validating CsrGraph(n, offsets, targets) constructor
-    # (BASELINE.md "Kronecker-27 CPU run": hand the graph over from the GPU).
-    ctx = dp.Context(local)
-    g = dp.rmat_graph(scale, seed=args.seed, ctx=ctx)
-    gt = dp.transpose(g)
-    gF_host = (g.offsets.copy(), g.targets.copy())
-    gT_host = (gt.offsets.copy(), gt.targets.copy())
-    n, m = g.vertex_count, g.edge_count
-    del g, gt
-    gc.collect()
-    kind = "reference" if oracle.available("ref") else "port"
-    O = oracle.Oracle("ref" if kind == "reference" else "port")
-    O.set_threads(threads)
-    gF = O.graph_from_csr(n, *gF_host)
-    gT = O.graph_from_csr(n, *gT_host)
-    cfg = oracle.default_config(max_iterations=args.ref_sweeps, convergence_check_disabled=1)
+    t_setup = time.perf_counter()
+    n, off0, tgt0 = oracle.par_rmat_csr(scale, seed=args.seed)
+    O, kind, cores = _ref_oracle(threads)
+    g0 = O.graph_from_csr(n, off0, tgt0)
+    m0 = g0.m
+    toff0, ttgt0 = oracle.par_transpose(n, off0, tgt0)
+    gt0 = O.graph_from_csr(n, toff0, ttgt0)
+    del off0, tgt0, toff0, ttgt0
+    size = O.batch_size_from_fraction(args.batch_frac, m0)
+    k_ref = args.warmup  # the device arm's first timed step
+    dels, ins = O.generate_random_batch(g0, size, 0.8, O.derive_seed(args.seed, 1000003 + k_ref))
+    g, _, _ = O.apply_batch(g0, dels, ins)
+    off, tgt = g.csr()
+    toff, ttgt = oracle.par_transpose(n, off, tgt)
+    gt = O.graph_from_csr(n, toff, ttgt)
+    del off, tgt, toff, ttgt
+    setup_s = time.perf_counter() - t_setup
+    from oracle import default_config
+    # one full converged solve of each engine (reported, not the per-step value)
+    t0 = time.perf_counter()
+    base = O.static(gt0, g0)
+    base_ms = (time.perf_counter() - t0) * 1e3
+    del gt0
+    t0 = time.perf_counter()
+    full = O.static(gt, g)
+    full_ms = (time.perf_counter() - t0) * 1e3
+    t0 = time.perf_counter()
+    d = O.dynamic_frontier(g, gt, dels, ins, base.ranks, pruning=True)
+    dfp_ms = (time.perf_counter() - t0) * 1e3
+    # bounded per-step samples
+    per_sweep_s = full_ms * 1e-3 / max(1, full.iterations)
+    sweeps = int(max(5, min(full.iterations, args.ref_budget_s / max(1, args.steps) / per_sweep_s)))
+    warm_cfg = default_config(max_iterations=2, convergence_check_disabled=1)
+    cfg = default_config(max_iterations=sweeps)
     times, iters = [], []
     for step in range(args.warmup + args.steps):
+        if step < args.warmup:
+            O.static(gt, g, warm_cfg)
+            continue
         t0 = time.perf_counter()
-        r = O.static(gT, gF, cfg)  # staticPageRank, harness.cpp:222-224 style timing
-        ms = (time.perf_counter() - t0) * 1e3
-        if step >= args.warmup:
-            times.append(ms)
-            iters.append(r.iterations)
+        r = O.static(gt, g, cfg)  # staticPageRank, timed like harness.cpp:222-224
+        times.append((time.perf_counter() - t0) * 1e3)
+        iters.append(r.iterations)
     total_ms = sum(times)
-    value = m * sum(iters) / (total_ms * 1e-3) / 1e9
-    sample = (f"{args.ref_sweeps} static sweeps per step (staticPageRank, maxIterations={args.ref_sweeps}, "
-              f"convergence check disabled) on the base RMAT-{scale} graph")
+    value = g.m * sum(iters) / (total_ms * 1e-3) / 1e9
+    sample = (f"per step: staticPageRank (partition + init + sweeps in the timed call) with maxIterations="
+              f"{sweeps} of the full solve's {full.iterations}, on the RMAT-{scale} graph updated by the device "
+              f"arm's first timed batch (same bytes)")
     line = {
         "impl": "reference", "metric": baseline_metric(), "value": value, "unit": "GTEPS", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / len(times),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic RMAT (Graph500 a=.57 b=c=.19, edge factor 16, seed %d, dedup + self-loops)" % args.seed,
-        "config": {"workload": desc, "scale": scale, "n": n, "m": m, "alpha": 0.85, "tol": 1e-10},
-        "cpu_baseline": {"value": value, "unit": "GTEPS", "cores": threads if kind == "reference" else 1,
-                         "kind": kind, "sample": sample},
+        "data": "synthetic RMAT (Graph500 a=.57 b=c=.19, edge factor 16, seed %d, dedup + self-loops, built on "
+                "the host by the oracle's multithreaded generator -- no product code); random 80/20 batch from "
+                "the reference's generateRandomBatch + applyBatch" % args.seed,
+        "config": workload_config(args, n, m0, size),
+        "cpu_baseline": {"value": value, "unit": "GTEPS", "cores": cores, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "full_solve": {"static_ms": full_ms, "static_iterations": full.iterations,
+                       "static_gteps": g.m * full.iterations / (full_ms * 1e-3) / 1e9,
+                       "dfp_ms": dfp_ms, "dfp_iterations": d.iterations,
+                       "dfp_affected_vertex_iterations": d.affected_vertex_iterations,
+                       "dfp_speedup_vs_static": full_ms / dfp_ms, "base_static_ms": base_ms,
+                       "note": "one converged solve of each engine on the updated graph (DF-P from the base "
+                               "graph's converged Static ranks)"},
+        "setup_s": setup_s,
+        "native_libraries": "oracle/_ref/libdynpr_ref.so (reference), oracle/_build/libdynpr_oracle.so "
+                            "(input builders); libdynpr_cuda.so is never loaded",
     }
     print(json.dumps(line))
 
@@ -416,16 +477,20 @@ def run_ours(args, world, rank, local):
             "data": "synthetic RMAT (Graph500 a=.57 b=c=.19, edge factor 16, seed %d, dedup + self-loops, "
                     "generated on device); random 80/20 batches from the reference generateRandomBatch "
                     "algorithm" % args.seed,
-            "config": {"workload": desc, "scale": scale, "n": n, "m_base": m0, "alpha": 0.85, "tol": 1e-10,
-                       "batch_fraction": args.batch_frac, "batch_size": size,
-                       "l2": "inputs larger than L2 (graph pair %.2f GB vs 126 MB L2); no flush needed"
-                             % ((2 * (8 * (n + 1) + 4 * m0)) / 1e9),
-                       "parallelism": "single GPU" if world == 1 else
-                       "vertex-range partitioned over %d GPUs (edge-balanced; NCCL all-reduce of the "
-                       "sweep record per iteration)" % world,
-                       "exchange": exchange},
+            "config": dict(workload_config(args, n, m0, size), **{
+                "parallelism": "single GPU" if world == 1 else
+                "vertex-range partitioned over %d GPUs (edge-balanced; NCCL all-reduce of the sweep record "
+                "per iteration)" % world,
+                "exchange": exchange}),
             "static": {"ms_per_solve": st_ms, "iterations": statistics.mean(rec["static_it"]),
-                       "gteps": local_gteps},
+                       "gteps": local_gteps,
+                       "ms_per_solve_incl_layout": st_ms + statistics.mean(rec["layout_ms"]),
+                       "note": "ms_per_solve_incl_layout adds the per-snapshot engine layout (degree relabel + "
+                               "SELL segments, dynpr_graph_prepare), this engine's counterpart of the partition "
+                               "the reference's staticPageRank builds inside its timed call (engine.cpp:99-108); "
+                               "the layout is built once per snapshot and shared by every solve on it"},
+            "value_incl_layout": static_edges / ((static_ms_total + sum(rec["layout_ms"])) * 1e-3) / 1e9
+                                 if world == 1 else None,
             "dfp": {"ms_per_solve": dfp_ms, "iterations": statistics.mean(rec["dfp_it"]),
                     "affected_vertex_iterations": statistics.mean(rec["dfp_aff"]),
                     "processed_gteps": sum(rec["dfp_edges"]) / (sum(rec["dfp_ms"]) * 1e-3) / 1e9,
@@ -485,20 +550,43 @@ def run_ours(args, world, rank, local):
                               "wall clock, %d steps" % e2e_steps}
 
     # ---- CPU baseline: the reference library on the host cores (rank 0, N=1) ---
+    # One full converged staticPageRank + one dynamicFrontier(pruning) of the
+    # reference on the last step's updated graph (the same bytes), and the
+    # device's full solve of that graph compared with it bit for bit.
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        gteps, ms, kind, ref_ranks, cores = cpu_reference_static(
-            (g.offsets, g.targets), (gt.offsets, gt.targets), args.ref_sweeps, threads)
-        out["cpu_baseline"] = {"value": gteps, "unit": "GTEPS", "cores": cores, "kind": kind,
-                               "sample": f"{args.ref_sweeps} static sweeps (staticPageRank, maxIterations="
-                                         f"{args.ref_sweeps}) on the last step's updated RMAT-{scale} graph, "
-                                         f"{ms:.0f} ms"}
-        st = static_dev(gt, g, max_iter=args.ref_sweeps)
+        b_last = batches[-1]
+        batch = ((b_last.deletions.src, b_last.deletions.dst), (b_last.insertions.src, b_last.insertions.dst))
+        c = cpu_reference_full((g.offsets, g.targets), (gt.offsets, gt.targets), base.ranks, batch, threads)
+        out["cpu_baseline"] = {"value": c["gteps"], "unit": "GTEPS", "cores": c["cores"], "kind": c["kind"],
+                               "sample": "one full converged staticPageRank (%d sweeps, partition + init inside the "
+                                         "timed call) on the last step's updated RMAT-%d graph: %.0f ms; "
+                                         "dynamicFrontier(pruning) on it: %.0f ms (%d it)"
+                                         % (c["static_it"], scale, c["static_ms"], c["dfp_ms"], c["dfp_it"]),
+                               "static_ms": c["static_ms"], "dfp_ms": c["dfp_ms"]}
+        st = static_dev(gt, g)
         mine = ranks_dev.cpu().numpy()
-        out["parity_sample"] = {"sweeps": args.ref_sweeps, "ranks_bitwise_equal": bool(np.array_equal(mine, ref_ranks)),
-                                "linf": float(np.max(np.abs(mine - ref_ranks)))}
+        sd = dfp_dev(g, gt, b_last)
+        mine_d = ranks_dev.cpu().numpy()
+        out["parity_sample"] = {"what": "full Static and DF-P solves of the last step's graph vs the reference",
+                                "static_iterations_equal": st.iterations == c["static_it"],
+                                "static_ranks_bitwise_equal": bool(np.array_equal(mine, c["ranks"])),
+                                "static_linf": float(np.max(np.abs(mine - c["ranks"]))),
+                                "dfp_iterations_equal": sd.iterations == c["dfp_it"],
+                                "dfp_ranks_bitwise_equal": bool(np.array_equal(mine_d, c["dfp_ranks"]))}
     if rank == 0:
         print(json.dumps(out))
+
+
+def relaunch_under_torchrun(n: int) -> int:
+    """--gpus N > 1 without a torchrun environment: launch N ranks here."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -510,18 +598,32 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="rmat24")
     ap.add_argument("--batch-frac", type=float, default=1e-4)
     ap.add_argument("--seed", type=int, default=42)
-    ap.add_argument("--ref-sweeps", type=int, default=5)
+    ap.add_argument("--ref-budget-s", type=float, default=90.0,
+                    help="reference arm: seconds of timed CPU work over all steps")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    world, rank, local = dist_setup("gloo" if args.impl == "reference" else "nccl")
+    if args.gpus < 1:
+        sys.exit("bench.py: --gpus must be >= 1")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        if args.impl == "ours":
+            import torch
+            have = torch.cuda.device_count()
+            if have < args.gpus:
+                sys.exit(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) visible")
+        sys.exit(relaunch_under_torchrun(args.gpus))
+    world_env = int(os.environ.get("WORLD_SIZE", "1"))
+    if world_env != args.gpus and not (args.gpus == 1 and FORCE_TEAM):
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world_env}")
     if args.impl == "reference":
-        run_reference(args, world, rank, local)
-    else:
-        run_ours(args, world, rank, local)
-    if world > 1 or (FORCE_TEAM and args.impl != "reference"):
+        # rank 0 alone runs the CPU reference; no process group is needed
+        run_reference(args, world_env, int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0")))
+        return
+    world, rank, local = dist_setup("nccl")
+    run_ours(args, world, rank, local)
+    if world > 1 or FORCE_TEAM:
         import torch.distributed as dist
         dist.destroy_process_group()
 

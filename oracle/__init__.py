@@ -607,6 +607,46 @@ class RefRng:
         return float(self.lib.L.ref_rng_next_double(C.c_void_p(self.h)))
 
 
+# ---- bench input for the CPU arms (oracle/bench_input.c, OpenMP) ------------------
+def _port_lib():
+    L = C.CDLL(PORT_LIB)
+    L.orc_par_rmat_edges.argtypes = [C.c_uint32, C.c_uint64, C.c_double, C.c_double, C.c_double, C.c_uint64,
+                                     _u32p, _u32p]
+    L.orc_par_build_csr.argtypes = [C.c_uint32, _u32p, _u32p, C.c_uint64, C.c_int, _u64p, _u32p]
+    L.orc_par_build_csr.restype = C.c_uint64
+    L.orc_par_transpose.argtypes = [C.c_uint32, _u64p, _u32p, _u64p, _u32p]
+    return L
+
+
+def par_rmat_csr(scale: int, edge_factor: int = 16, seed: int = 42, a=0.57, b=0.19, c=0.19):
+    """RMAT forward CSR (buildCsr + addSelfLoops of edge_factor << scale
+    pairs) built on all host cores: the bytes of Oracle("port").rmat_edges ->
+    build_csr -> add_self_loops (and of the device generator), without the
+    product library.  Returns (n, offsets u64[n+1], targets u32[m])."""
+    L = _port_lib()
+    n = 1 << scale
+    count = edge_factor << scale
+    src = np.empty(count, np.uint32)
+    dst = np.empty(count, np.uint32)
+    L.orc_par_rmat_edges(scale, count, a, b, c, seed, _ptr(src, _u32p), _ptr(dst, _u32p))
+    off = np.empty(n + 1, np.uint64)
+    tgt = np.empty(count + n, np.uint32)
+    m = L.orc_par_build_csr(n, _ptr(src, _u32p), _ptr(dst, _u32p), count, 1, _ptr(off, _u64p), _ptr(tgt, _u32p))
+    del src, dst
+    return n, off, np.ascontiguousarray(tgt[:m])
+
+
+def par_transpose(n: int, off, tgt):
+    """transpose (graph.cpp:70-83) of a sorted, deduplicated CSR on all host cores."""
+    L = _port_lib()
+    off = np.ascontiguousarray(off, dtype=np.uint64)
+    tgt = np.ascontiguousarray(tgt, dtype=np.uint32)
+    toff = np.empty(n + 1, np.uint64)
+    ttgt = np.empty(max(len(tgt), 1), np.uint32)
+    L.orc_par_transpose(n, _ptr(off, _u64p), _ptr(tgt, _u32p), _ptr(toff, _u64p), _ptr(ttgt, _u32p))
+    return toff, ttgt[: len(tgt)]
+
+
 def available(kind: str) -> bool:
     return os.path.exists(PORT_LIB if kind == "port" else REF_LIB)
 
