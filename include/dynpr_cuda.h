@@ -360,6 +360,13 @@ dynpr_status dynpr_edge_list_copy(const dynpr_edge_list* e, uint64_t first,
                                   uint64_t count, uint32_t* src, uint32_t* dst,
                                   int64_t* ts);
 dynpr_status dynpr_edge_list_destroy(dynpr_edge_list* e);
+/* A caller-built edge list (e.g. the reference's TemporalEdgeList entries,
+ * workload.hpp:26-36): `count` pairs, timestamps optional (ts NULL = not a
+ * temporal stream).  Ids are not checked (the reference's lists are plain
+ * values). */
+dynpr_status dynpr_edge_list_create(uint32_t vertex_count, const uint32_t* src,
+                                    const uint32_t* dst, const int64_t* ts,
+                                    uint64_t count, dynpr_edge_list** out);
 
 /* ---- experiment harness (harness.hpp:12-79, harness.cpp:68-399) --------- */
 /* computeReferenceRanks (harness.cpp:340-349): Static with the convergence

@@ -157,6 +157,7 @@ PROTOTYPES = {
     "dynpr_edge_list_info": (_i, [_vp, _u32p, _u64p, _ip]),
     "dynpr_edge_list_copy": (_i, [_vp, _u64, _u64, _vp, _vp, _vp]),
     "dynpr_edge_list_destroy": (_i, [_vp]),
+    "dynpr_edge_list_create": (_i, [_u32, _vp, _vp, _vp, _u64, _vp]),
     "dynpr_compute_reference_ranks": (_i, [_vp, _vp, _vp, _cfgp, _vp]),
     "dynpr_experiment_spec_default": (None, [C.POINTER(ExperimentSpec)]),
     "dynpr_run_experiment": (_i, [_vp, C.POINTER(ExperimentSpec), _pvp]),

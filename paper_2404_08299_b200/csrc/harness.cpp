@@ -1017,6 +1017,23 @@ dynpr_status dynpr_edge_list_info(const dynpr_edge_list* e, uint32_t* vertex_cou
   });
 }
 
+dynpr_status dynpr_edge_list_create(uint32_t vertex_count, const uint32_t* src, const uint32_t* dst,
+                                    const int64_t* ts, uint64_t count, dynpr_edge_list** out) {
+  return api_guard([&] {
+    if (!out) invalid("null argument");
+    if (count && (!src || !dst)) invalid("null array argument");
+    auto e = std::make_unique<dynpr_edge_list>();
+    e->n = vertex_count;
+    e->src.assign(src, src + count);
+    e->dst.assign(dst, dst + count);
+    if (ts) {
+      e->ts.assign(ts, ts + count);
+      e->temporal = true;
+    }
+    *out = e.release();
+  });
+}
+
 dynpr_status dynpr_edge_list_copy(const dynpr_edge_list* e, uint64_t first, uint64_t count, uint32_t* src,
                                   uint32_t* dst, int64_t* ts) {
   return api_guard([&] {
