@@ -140,6 +140,35 @@ dynpr_status dynpr_context_create_team(int device, dynpr_team* team, int rank,
                                        dynpr_context** out);
 dynpr_status dynpr_context_rank(const dynpr_context* ctx, int* rank,
                                 int* world);
+/* The same partitioned engine over a caller-supplied host transport (any
+ * process-group library: torch.distributed gloo, MPI, ...).  The engine
+ * stages every collective through pinned host memory and calls these on the
+ * solving thread, identically ordered on every rank; a nonzero return fails
+ * the solve with DYNPR_RUNTIME_ERROR.  Ranks may share a GPU (NCCL refuses
+ * that), which is how the cross-process path is tested on one GPU. */
+typedef struct dynpr_comm_ops {
+  /* in place on host data[count]: element-wise over the ranks, op 0 = sum
+   * (mod 2^64), op 1 = max (unsigned) */
+  int (*allreduce_u64)(uint64_t* data, uint64_t count, int op, void* user);
+  /* in place on host buf: rank r contributes bytes [offsets[r],
+   * offsets[r+1]) and receives all offsets[world] bytes */
+  int (*allgatherv)(void* buf, const uint64_t* offsets, int world,
+                    void* user);
+  int (*barrier)(void* user);
+} dynpr_comm_ops;
+dynpr_status dynpr_context_create_hostcomm(int device, int rank, int world,
+                                           const dynpr_comm_ops* ops,
+                                           void* user, dynpr_context** out);
+/* Device buffers shareable across processes (CUDA IPC) for the fused
+ * exchange: dynpr_ipc_alloc returns a device buffer and its 64-byte handle;
+ * another process maps it with dynpr_ipc_open (same or peer GPU) and unmaps
+ * with dynpr_ipc_close; the owner releases it with dynpr_ipc_free. */
+dynpr_status dynpr_ipc_alloc(dynpr_context* ctx, uint64_t bytes, void** dptr,
+                             uint8_t* handle64);
+dynpr_status dynpr_ipc_open(dynpr_context* ctx, const uint8_t* handle64,
+                            void** dptr);
+dynpr_status dynpr_ipc_close(dynpr_context* ctx, void* dptr);
+dynpr_status dynpr_ipc_free(dynpr_context* ctx, void* dptr);
 /* Fused exchange: ptrs0[r] / ptrs1[r] are rank r's two contribution buffers
  * (`capacity` doubles each) mapped into this process -- CUDA IPC / torch
  * symmetric memory across processes, plain device pointers for a LocalTeam.

@@ -34,7 +34,7 @@ __all__ = [
     "l1_norm_delta", "linf_norm_delta", "naive_dynamic", "partition_by_degree", "rmat_graph",
     "static_pagerank", "transpose", "update_ranks", "generate_random_batch", "batch_size_from_fraction",
     "derive_seed", "prepare", "LocalTeam", "nccl_unique_id", "share_nccl_unique_id",
-    "context_from_process_group", "attach_symmetric_exchange", "dynamic_traversal", "mark_reachable",
+    "context_from_process_group", "attach_symmetric_exchange", "TorchDistTransport", "IpcExchange", "dynamic_traversal", "mark_reachable",
     "ParseError", "Approach", "ExperimentMode", "ChainMode", "ReportFormat", "ExperimentRow", "ExperimentSpec",
     "approach_name", "approach_from_name", "load_matrix_market", "load_matrix_market_arrays",
     "load_temporal_edge_list", "load_temporal_edge_list_arrays", "split_temporal", "compute_reference_ranks",
@@ -197,6 +197,16 @@ class Context:
         _check(N.lib().dynpr_context_create_nccl(int(device), int(rank), int(world), buf, C.byref(h)))
         return cls(device, _handle=h.value)
 
+    @classmethod
+    def hostcomm(cls, device: int, transport: "TorchDistTransport") -> "Context":
+        """Rank `transport.rank` of a team whose collectives go through a host
+        transport (dynpr_context_create_hostcomm) -- any number of processes,
+        several per GPU allowed."""
+        h = C.c_void_p()
+        _check(N.lib().dynpr_context_create_hostcomm(int(device), int(transport.rank), int(transport.world),
+                                                     C.byref(transport.ops), None, C.byref(h)))
+        return cls(device, _handle=h.value, _keep=transport)
+
     def attach_peers(self, ptrs0: Sequence[int], ptrs1: Sequence[int], capacity: int) -> None:
         """Fused exchange: every rank's two contribution buffers (device
         addresses valid in this process, `capacity` doubles each); [] detaches.
@@ -268,12 +278,134 @@ def attach_symmetric_exchange(ctx: Context, n: int, group=None):
     return keep
 
 
-def context_from_process_group(device: int, group=None) -> Context:
-    """One process per GPU (torchrun): this process's rank of an NCCL team
-    spanning the torch.distributed process group."""
+def context_from_process_group(device: int, group=None, transport: str = "nccl") -> Context:
+    """One process per GPU (torchrun): this process's rank of a team spanning
+    the torch.distributed process group -- over NCCL (default), or with
+    transport="host" over the group itself (TorchDistTransport: gloo/MPI,
+    several processes per GPU allowed)."""
     import torch.distributed as dist
+    if transport == "host":
+        return Context.hostcomm(device, TorchDistTransport(group))
+    if transport != "nccl":
+        raise ValueError(f"unknown transport {transport!r}")
     uid = share_nccl_unique_id(group)
     return Context.nccl(device, dist.get_rank(group), dist.get_world_size(group), uid)
+
+
+class TorchDistTransport:
+    """dynpr_comm_ops over a torch.distributed process group whose backend
+    takes CPU tensors (gloo, or MPI): the host transport of
+    `Context.hostcomm`.  Collectives run on the thread that called the engine,
+    in the same order on every rank.  The callbacks must not raise into C: a
+    failure is recorded in `error` and returned as a nonzero status, which
+    the engine turns into a RuntimeError."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.error: Optional[str] = None
+        self.calls = 0
+        self.ops = N.CommOps(N.ALLREDUCE_U64(self._allreduce), N.ALLGATHERV(self._allgatherv),
+                             N.BARRIER(self._barrier))
+
+    def _guard(self, fn) -> int:
+        try:
+            self.calls += 1
+            fn()
+            return 0
+        except Exception:  # noqa: BLE001 -- reported through the engine's status
+            import traceback
+            self.error = traceback.format_exc()
+            return 1
+
+    def _allreduce(self, data, count, op, _user):
+        def run():
+            import torch
+            import torch.distributed as dist
+            view = np.ctypeslib.as_array(data, shape=(int(count),))
+            mine = torch.from_numpy(view.copy().view(np.int64))
+            parts = [torch.empty_like(mine) for _ in range(self.world)]
+            dist.all_gather(parts, mine, group=self.group)
+            st = np.stack([p.numpy().view(np.uint64) for p in parts])
+            view[:] = st.max(axis=0) if op == 1 else st.sum(axis=0, dtype=np.uint64)  # mod 2^64
+        return self._guard(run)
+
+    def _allgatherv(self, buf, offsets, world, _user):
+        def run():
+            import torch
+            import torch.distributed as dist
+            off = [int(offsets[i]) for i in range(world + 1)]
+            host = np.ctypeslib.as_array((C.c_uint8 * max(off[-1], 1)).from_address(buf))
+            sizes = [off[r + 1] - off[r] for r in range(world)]
+            width = max(max(sizes), 1)
+            send = torch.zeros(width, dtype=torch.uint8)
+            me = self.rank
+            send[:sizes[me]] = torch.from_numpy(host[off[me]:off[me + 1]].copy())
+            parts = [torch.empty(width, dtype=torch.uint8) for _ in range(world)]
+            dist.all_gather(parts, send, group=self.group)
+            for r in range(world):
+                if r != me and sizes[r]:
+                    host[off[r]:off[r + 1]] = parts[r].numpy()[:sizes[r]]
+        return self._guard(run)
+
+    def _barrier(self, _user):
+        def run():
+            import torch.distributed as dist
+            dist.barrier(group=self.group)
+        return self._guard(run)
+
+
+class IpcExchange:
+    """The fused exchange across processes without torch symmetric memory:
+    each rank's two contribution buffers are CUDA IPC allocations of this
+    library, their handles all-gathered over the process group and mapped by
+    every rank (peers on the same or another GPU), then attached to the
+    context.  Keep the object alive while the context solves; close() (or
+    garbage collection) detaches, unmaps and frees in that order."""
+
+    def __init__(self, ctx: "Context", n: int, group=None):
+        import torch.distributed as dist
+        self.ctx = ctx
+        self.group = group
+        self.own = []
+        self.opened = []
+        handles = []
+        lib = N.lib()
+        for _ in range(2):
+            p = C.c_void_p()
+            h = (C.c_uint8 * 64)()
+            _check(lib.dynpr_ipc_alloc(C.c_void_p(ctx.h), 8 * max(n, 1), C.byref(p), h))
+            self.own.append(p.value)
+            handles.append(bytes(h))
+        allh = [None] * dist.get_world_size(group)
+        dist.all_gather_object(allh, handles, group=group)
+        me = dist.get_rank(group)
+        ptrs = [[], []]
+        for r, hs in enumerate(allh):
+            for k in range(2):
+                if r == me:
+                    ptrs[k].append(self.own[k])
+                    continue
+                p = C.c_void_p()
+                _check(lib.dynpr_ipc_open(C.c_void_p(ctx.h), (C.c_uint8 * 64).from_buffer_copy(hs[k]), C.byref(p)))
+                self.opened.append(p.value)
+                ptrs[k].append(p.value)
+        ctx.attach_peers(ptrs[0], ptrs[1], max(n, 1))
+
+    def close(self) -> None:
+        if self.ctx is None:
+            return
+        import torch.distributed as dist
+        lib = N.lib()
+        self.ctx.attach_peers([], [], 0)
+        for p in self.opened:
+            _check(lib.dynpr_ipc_close(C.c_void_p(self.ctx.h), C.c_void_p(p)))
+        dist.barrier(group=self.group)  # every peer unmapped before the owners free
+        for p in self.own:
+            _check(lib.dynpr_ipc_free(C.c_void_p(self.ctx.h), C.c_void_p(p)))
+        self.ctx = None
 
 
 class LocalTeam:

@@ -87,6 +87,16 @@ class ExperimentRow(C.Structure):  # dynpr_experiment_row
 OBSERVER = C.CFUNCTYPE(None, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_uint8),
                        C.c_uint64, C.c_void_p)
 
+# dynpr_comm_ops (caller-supplied host transport)
+ALLREDUCE_U64 = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_uint64), C.c_uint64, C.c_int, C.c_void_p)
+ALLGATHERV = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_uint64), C.c_int, C.c_void_p)
+BARRIER = C.CFUNCTYPE(C.c_int, C.c_void_p)
+
+
+class CommOps(C.Structure):
+    _fields_ = [("allreduce_u64", ALLREDUCE_U64), ("allgatherv", ALLGATHERV), ("barrier", BARRIER)]
+
+
 _vp = C.c_void_p
 _pvp = C.POINTER(C.c_void_p)
 _u32p = C.POINTER(C.c_uint32)
@@ -119,6 +129,11 @@ PROTOTYPES = {
     "dynpr_context_create_team": (_i, [_i, _vp, _i, _pvp]),
     "dynpr_context_rank": (_i, [_vp, _ip, _ip]),
     "dynpr_context_attach_peers": (_i, [_vp, _i, _vp, _vp, _u64]),
+    "dynpr_context_create_hostcomm": (_i, [_i, _i, _i, C.POINTER(CommOps), _vp, _pvp]),
+    "dynpr_ipc_alloc": (_i, [_vp, _u64, _pvp, _vp]),
+    "dynpr_ipc_open": (_i, [_vp, _vp, _pvp]),
+    "dynpr_ipc_close": (_i, [_vp, _vp]),
+    "dynpr_ipc_free": (_i, [_vp, _vp]),
     "dynpr_graph_from_csr": (_i, [_vp, _u32, _vp, _vp, _u64, _pvp]),
     "dynpr_graph_build": (_i, [_vp, _u32, _vp, _vp, _u64, _pvp]),
     "dynpr_graph_add_self_loops": (_i, [_vp, _vp, _pvp]),

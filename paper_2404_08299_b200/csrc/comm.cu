@@ -198,7 +198,134 @@ class LocalComm final : public Comm {
   int device_;
 };
 
+// ---- HostComm: caller-supplied host transport -------------------------------
+class HostComm final : public Comm {
+ public:
+  HostComm(int r, int w, const dynpr_comm_ops& ops, void* user) : ops_(ops), user_(user) {
+    rank = r;
+    world = w;
+    DYNPR_CK(cudaMallocHost(&small_, 4096));
+  }
+  ~HostComm() override {
+    if (host_) cudaFreeHost(host_);
+    if (small_) cudaFreeHost(small_);
+  }
+  void allgatherv(void* buf, const uint64_t* off, cudaStream_t st) override {
+    const uint64_t total = off[world];
+    if (total > host_bytes_) {
+      if (host_) DYNPR_CK(cudaFreeHost(host_));
+      host_ = nullptr;
+      host_bytes_ = 0;
+      DYNPR_CK(cudaMallocHost(&host_, total));
+      host_bytes_ = total;
+    }
+    auto* h = static_cast<uint8_t*>(host_);
+    auto* b = static_cast<uint8_t*>(buf);
+    const uint64_t lo = off[rank], hi = off[rank + 1];
+    if (hi > lo) DYNPR_CK(cudaMemcpyAsync(h + lo, b + lo, hi - lo, cudaMemcpyDeviceToHost, st));
+    DYNPR_CK(cudaStreamSynchronize(st));
+    call(ops_.allgatherv(host_, off, world, user_), "allgatherv");
+    if (lo) DYNPR_CK(cudaMemcpyAsync(b, h, lo, cudaMemcpyHostToDevice, st));
+    if (total > hi) DYNPR_CK(cudaMemcpyAsync(b + hi, h + hi, total - hi, cudaMemcpyHostToDevice, st));
+    // the staging buffer is reused by the next collective
+    DYNPR_CK(cudaStreamSynchronize(st));
+  }
+  void allreduce_red(SweepRed* red, cudaStream_t st) override {
+    auto* h = static_cast<SweepRed*>(small_);
+    DYNPR_CK(cudaMemcpyAsync(h, red, sizeof(SweepRed), cudaMemcpyDeviceToHost, st));
+    DYNPR_CK(cudaStreamSynchronize(st));
+    uint64_t mx[1] = {h->delta_bits};
+    uint64_t sm[5] = {h->processed, h->edges, h->pend_edges, h->pend_low, h->pend_high};
+    call(ops_.allreduce_u64(mx, 1, 1, user_), "allreduce (max)");
+    call(ops_.allreduce_u64(sm, 5, 0, user_), "allreduce (sum)");
+    h->delta_bits = mx[0];
+    h->processed = sm[0];
+    h->edges = sm[1];
+    h->pend_edges = sm[2];
+    h->pend_low = static_cast<unsigned>(sm[3]);
+    h->pend_high = static_cast<unsigned>(sm[4]);
+    DYNPR_CK(cudaMemcpyAsync(red, h, sizeof(SweepRed), cudaMemcpyHostToDevice, st));
+    DYNPR_CK(cudaStreamSynchronize(st));
+  }
+  void barrier() override { call(ops_.barrier(user_), "barrier"); }
+
+ private:
+  void call(int rc, const char* what) {
+    if (rc != 0) throw Error(DYNPR_RUNTIME_ERROR, std::string("team: host transport ") + what + " failed");
+  }
+  dynpr_comm_ops ops_;
+  void* user_;
+  void* host_ = nullptr;
+  uint64_t host_bytes_ = 0;
+  void* small_ = nullptr;
+};
+
+// ---- pending-flag bitmap ------------------------------------------------------
+__global__ void k_pack_flags(const uint8_t* __restrict__ flags, uint32_t lo, uint32_t hi,
+                             uint32_t* __restrict__ seg) {
+  const uint32_t w0 = lo >> 5;
+  const uint64_t v = ((uint64_t)w0 << 5) + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool in = v >= lo && v < hi;
+  const unsigned bits = __ballot_sync(0xffffffffu, in && flags[in ? v : lo]);
+  if ((threadIdx.x & 31) == 0 && v < hi) seg[(v >> 5) - w0] = bits;  // v = the word's first vertex
+}
+
+// bounds: lo_0..lo_world (lo_world = n), then seg_0..seg_world (word offsets)
+__global__ void k_unpack_flags(const uint32_t* __restrict__ bits, const uint32_t* __restrict__ bounds, int world,
+                               int me, uint32_t n, uint8_t* __restrict__ flags) {
+  const uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= n) return;
+  if (v >= bounds[me] && v < bounds[me + 1]) return;  // own range: already current
+  int a = 0, b = world;  // owner q: lo_q <= v < lo_{q+1}
+  while (b - a > 1) {
+    const int mid = (a + b) >> 1;
+    if (v >= bounds[mid]) a = mid; else b = mid;
+  }
+  const uint32_t word = bounds[world + 1 + a] + (uint32_t)((v >> 5) - (bounds[a] >> 5));
+  flags[v] = (uint8_t)((bits[word] >> (v & 31)) & 1u);
+}
+
 }  // namespace
+
+FlagBitmapPlan make_flag_bitmap_plan(const std::vector<uint32_t>& v_lo, uint32_t n) {
+  const int world = (int)v_lo.size();
+  FlagBitmapPlan p;
+  p.host_bounds.assign(2 * (world + 1), 0);
+  p.byte_off.assign(world + 1, 0);
+  uint64_t seg = 0;
+  for (int r = 0; r < world; ++r) {
+    const uint32_t lo = v_lo[r], hi = r + 1 < world ? v_lo[r + 1] : n;
+    p.host_bounds[r] = lo;
+    p.host_bounds[world + 1 + r] = (uint32_t)seg;
+    p.byte_off[r] = 4 * seg;
+    if (hi > lo) seg += ((uint64_t)hi + 31) / 32 - lo / 32;
+  }
+  p.host_bounds[world] = n;
+  p.host_bounds[2 * world + 1] = (uint32_t)seg;
+  p.byte_off[world] = 4 * seg;
+  p.words = seg;
+  return p;
+}
+
+void launch_pack_flags(dynpr_context* ctx, const uint8_t* flags, uint32_t lo, uint32_t hi, uint32_t* seg_words) {
+  if (hi <= lo) return;
+  const uint64_t span = (((uint64_t)hi + 31) / 32 - lo / 32) * 32;
+  k_pack_flags<<<(unsigned)((span + 255) / 256), 256, 0, ctx->stream>>>(flags, lo, hi, seg_words);
+  ctx->launches += 1;
+  check_launch();
+}
+
+void launch_unpack_flags(dynpr_context* ctx, const uint32_t* bits, const uint32_t* bounds, int world, int me,
+                         uint32_t n, uint8_t* flags) {
+  if (!n) return;
+  k_unpack_flags<<<(n + 255) / 256, 256, 0, ctx->stream>>>(bits, bounds, world, me, n, flags);
+  ctx->launches += 1;
+  check_launch();
+}
+
+std::unique_ptr<Comm> make_host_comm(int rank, int world, const dynpr_comm_ops& ops, void* user) {
+  return std::make_unique<HostComm>(rank, world, ops, user);
+}
 
 dynpr_status nccl_unique_id(void* out128) {
   return api_guard([&] {

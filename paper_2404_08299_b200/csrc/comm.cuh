@@ -15,6 +15,7 @@
 #pragma once
 
 #include <memory>
+#include <vector>
 
 #include "common.cuh"
 
@@ -46,5 +47,27 @@ struct LocalTeam;
 std::shared_ptr<LocalTeam> make_local_team(int world);
 int local_team_world(const LocalTeam& t);
 std::unique_ptr<Comm> make_local_comm(std::shared_ptr<LocalTeam> team, int rank, int device);
+
+// Caller-supplied host transport (dynpr_comm_ops, e.g. torch.distributed
+// gloo, MPI): the collectives are staged through pinned host memory.  Any
+// number of processes on any devices -- including several processes on one
+// GPU, which NCCL refuses -- so the cross-process engine runs on one GPU.
+std::unique_ptr<Comm> make_host_comm(int rank, int world, const dynpr_comm_ops& ops, void* user);
+
+// DF/DF-P pending-flag exchange as a bitmap (n/8 bytes per sweep instead of
+// n): rank r packs the flags of its vertex range [lo_r, hi_r) into words
+// [lo_r/32, ceil(hi_r/32)) of its segment of the bit buffer (segments
+// concatenated in rank order); after the all-gather every rank unpacks the
+// other ranks' ranges into its byte flags.
+struct FlagBitmapPlan {
+  std::vector<uint64_t> byte_off;    // allgatherv offsets of the segments (world + 1)
+  std::vector<uint32_t> host_bounds; // lo_0..lo_world (= n), seg_0..seg_world (word offsets)
+  uint64_t words = 0;                // total words of the bit buffer
+};
+FlagBitmapPlan make_flag_bitmap_plan(const std::vector<uint32_t>& v_lo, uint32_t n);
+// `bounds` = device copy of host_bounds
+void launch_pack_flags(dynpr_context* ctx, const uint8_t* flags, uint32_t lo, uint32_t hi, uint32_t* seg_words);
+void launch_unpack_flags(dynpr_context* ctx, const uint32_t* bits, const uint32_t* bounds, int world, int me,
+                         uint32_t n, uint8_t* flags);
 
 }  // namespace dynpr_b200

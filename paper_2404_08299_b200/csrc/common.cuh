@@ -141,7 +141,8 @@ struct dynpr_context {
   dynpr_b200::DevBuf rank[2], contrib[2], flags_va, flags_np, flags_written,
       pend_low, pend_high, pend_flags, partials, perm_stage,
       tile_counts, red, stage_a, stage_b, stage_c, stage_d, stage_e, stage_f,
-      cub_tmp, tick, loopctl, layout_tmp, plan_prefix, side_err, bfs_a, bfs_b, run_list, run_pieces, scratch64a, scratch64b, scratch32a, scratch32b, scratch8a, batch[4];
+      cub_tmp, tick, loopctl, layout_tmp, plan_prefix, side_err, bfs_a, bfs_b, run_list, run_pieces, scratch64a, scratch64b, scratch32a, scratch32b, scratch8a, batch[4],
+      flag_bits, flag_bounds;  // team pending-flag bitmap exchange
   // lifetime: graphs are allocated from this context's stream-ordered pool.
   // dynpr_context_destroy with graphs still alive (e.g. a garbage-collected
   // binding finalising both in arbitrary order) defers the teardown to the

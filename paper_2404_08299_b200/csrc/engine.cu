@@ -414,6 +414,9 @@ void solve_impl(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynp
   // every sweep and the reduction record all-reduced, so every rank takes
   // the same convergence / expansion decisions.
   std::vector<uint64_t> off_c, off_f;  // allgatherv byte offsets: f64 / u8 per vertex
+  FlagBitmapPlan fplan;
+  uint32_t* fbits = nullptr;
+  uint32_t* fbounds = nullptr;
   if (dist) {
     const std::vector<RankRange> plan = plan_ranges(ctx, const_cast<Layout*>(L), comm->world);
     const RankRange& me = plan[comm->rank];
@@ -431,7 +434,25 @@ void solve_impl(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynp
     }
     off_c[comm->world] = 8ull * n;
     off_f[comm->world] = n;
+    if (sp.flagged && !sp.traversal) {
+      std::vector<uint32_t> lo(comm->world);
+      for (int r = 0; r < comm->world; ++r) lo[r] = plan[r].v_lo;
+      fplan = make_flag_bitmap_plan(lo, n);
+      fbits = ctx->flag_bits.as<uint32_t>(fplan.words + 1);
+      fbounds = ctx->flag_bounds.as<uint32_t>(fplan.host_bounds.size());
+      DYNPR_CK(cudaMemcpyAsync(fbounds, fplan.host_bounds.data(), 4 * fplan.host_bounds.size(),
+                               cudaMemcpyHostToDevice, st));
+    }
   }
+  // DF/DF-P pending flags: packed to bits, all-gathered, unpacked into the
+  // other ranks' ranges (n/8 bytes per sweep on the wire)
+  auto exchange_flags = [&] {
+    const int me = comm->rank;
+    launch_pack_flags(ctx, np, fplan.host_bounds[me], fplan.host_bounds[me + 1],
+                      fbits + fplan.host_bounds[comm->world + 1 + me]);
+    comm->allgatherv(fbits, fplan.byte_off.data(), st);
+    launch_unpack_flags(ctx, fbits, fbounds, comm->world, me, n, np);
+  };
   if (dist) team_check_graph(ctx, comm, const_cast<Layout*>(L), gT, gF, red);
 
   if (fused) {
@@ -479,7 +500,7 @@ void solve_impl(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynp
       launch_sweep(ctx, ak, sp.flagged, sp.closed);
       comm->allreduce_red(rk, st);
       if (!fused) comm->allgatherv(CB[cu ^ 1], off_c.data(), st);
-      if (sp.flagged && !sp.traversal) comm->allgatherv(np, off_f.data(), st);
+      if (sp.flagged && !sp.traversal) exchange_flags();
       DYNPR_CK(cudaMemcpyAsync(slot + (k & 1), rk, sizeof(SweepRed), cudaMemcpyDeviceToHost, st));
       DYNPR_CK(cudaEventRecord(ctx->ev_rec[k & 1], st));
       if (sp.flagged && !sp.traversal) launch_pull_expand(ctx, ak);
@@ -526,7 +547,7 @@ void solve_impl(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynp
     if (dist) {
       comm->allreduce_red(red, st);  // also the team barrier of the fused exchange
       if (!fused) comm->allgatherv(CB[cur ^ 1], off_c.data(), st);
-      if (sp.flagged && !sp.traversal) comm->allgatherv(np, off_f.data(), st);
+      if (sp.flagged && !sp.traversal) exchange_flags();
       if (obs) comm->allgatherv(R[cur ^ 1], off_c.data(), st);
     }
     const SweepRed r = read_red(ctx, red);
@@ -731,6 +752,72 @@ dynpr_status dynpr_context_create_team(int device, dynpr_team* team, int rank, d
     *out = nullptr;
   }
   return st;
+}
+
+dynpr_status dynpr_context_create_hostcomm(int device, int rank, int world, const dynpr_comm_ops* ops, void* user,
+                                           dynpr_context** out) {
+  if (!out) {
+    set_last_error("null argument");
+    return DYNPR_INVALID_ARGUMENT;
+  }
+  *out = nullptr;
+  if (world < 1 || rank < 0 || rank >= world || !ops || !ops->allreduce_u64 || !ops->allgatherv || !ops->barrier) {
+    set_last_error("dynpr_context_create_hostcomm: bad rank/world or missing transport callback");
+    return DYNPR_INVALID_ARGUMENT;
+  }
+  dynpr_status st = dynpr_context_create(device, out);
+  if (st != DYNPR_OK) return st;
+  st = api_guard([&] { (*out)->comm = make_host_comm(rank, world, *ops, user).release(); });
+  if (st != DYNPR_OK) {
+    dynpr_context_destroy(*out);
+    *out = nullptr;
+  }
+  return st;
+}
+
+static_assert(sizeof(cudaIpcMemHandle_t) == 64, "CUDA IPC handles are 64 bytes");
+
+dynpr_status dynpr_ipc_alloc(dynpr_context* ctx, uint64_t bytes, void** dptr, uint8_t* handle64) {
+  return api_guard([&] {
+    if (!ctx || !dptr || !handle64 || !bytes) invalid("dynpr_ipc_alloc: null argument or zero size");
+    DYNPR_CK(cudaSetDevice(ctx->device));
+    void* p = nullptr;
+    DYNPR_CK(cudaMalloc(&p, bytes));  // IPC needs a plain cudaMalloc allocation (not the stream pool)
+    cudaIpcMemHandle_t h;
+    const cudaError_t e = cudaIpcGetMemHandle(&h, p);
+    if (e != cudaSuccess) {
+      cudaFree(p);
+      DYNPR_CK(e);
+    }
+    std::memcpy(handle64, &h, 64);
+    *dptr = p;
+  });
+}
+
+dynpr_status dynpr_ipc_open(dynpr_context* ctx, const uint8_t* handle64, void** dptr) {
+  return api_guard([&] {
+    if (!ctx || !dptr || !handle64) invalid("dynpr_ipc_open: null argument");
+    DYNPR_CK(cudaSetDevice(ctx->device));
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, 64);
+    DYNPR_CK(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess));
+  });
+}
+
+dynpr_status dynpr_ipc_close(dynpr_context* ctx, void* dptr) {
+  return api_guard([&] {
+    if (!ctx || !dptr) invalid("dynpr_ipc_close: null argument");
+    DYNPR_CK(cudaSetDevice(ctx->device));
+    DYNPR_CK(cudaIpcCloseMemHandle(dptr));
+  });
+}
+
+dynpr_status dynpr_ipc_free(dynpr_context* ctx, void* dptr) {
+  return api_guard([&] {
+    if (!ctx || !dptr) invalid("dynpr_ipc_free: null argument");
+    DYNPR_CK(cudaSetDevice(ctx->device));
+    DYNPR_CK(cudaFree(dptr));
+  });
 }
 
 dynpr_status dynpr_context_attach_peers(dynpr_context* ctx, int world, const uint64_t* ptrs0, const uint64_t* ptrs1,

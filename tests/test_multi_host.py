@@ -103,6 +103,25 @@ def worker(rank, port, q):
         res["ranks_equal"] = bool(np.array_equal(ranks, ref.ranks))
         res["iters_equal"] = iters == ref.iterations
 
+        # the host transport of the cross-process team engine
+        # (Context.hostcomm): the C callbacks dynpr_comm_ops, called exactly
+        # as libdynpr_cuda.so's HostComm calls them
+        import ctypes as C
+        t = dp.TorchDistTransport()
+        mx = (C.c_uint64 * 2)(2**63 + rank, 7)
+        sm = (C.c_uint64 * 3)(rank + 1, 2**64 - 1, 10)
+        rc = [t.ops.allreduce_u64(mx, 2, 1, None), t.ops.allreduce_u64(sm, 3, 0, None)]
+        res["allreduce"] = (rc, list(mx), list(sm))
+        gathered = []
+        for off in ([0, 3, 8], [0, 0, 4], [0, 5, 5]):
+            buf = (C.c_uint8 * max(off[-1], 1))()
+            for i in range(off[rank], off[rank + 1]):
+                buf[i] = 10 * rank + i
+            o = (C.c_uint64 * 3)(*off)
+            rc = t.ops.allgatherv(C.addressof(buf), o, WORLD, None)
+            gathered.append((rc, list(buf)[: off[-1]]))
+        res["allgatherv"] = gathered
+        res["barrier"] = t.ops.barrier(None)
         res["max_over_ranks"] = bench.max_over_ranks(float(rank + 1), WORLD)
         res["sum_over_ranks"] = bench.sum_over_ranks(float(rank + 1), WORLD)
         q.put((rank, res))
@@ -126,5 +145,14 @@ def test_multi_rank_host_protocol_gloo():
         assert got[r]["uid_ok"]
         assert got[r]["ranks_equal"]
         assert got[r]["iters_equal"]
+        rc, mx, sm = got[r]["allreduce"]
+        assert rc == [0, 0]
+        assert mx == [2**63 + 1, 7]  # unsigned max
+        assert sm == [3, 2**64 - 2, 20]  # sum mod 2^64
+        expect = []
+        for off in ([0, 3, 8], [0, 0, 4], [0, 5, 5]):
+            expect.append((0, [10 * q + i for q in range(WORLD) for i in range(off[q], off[q + 1])]))
+        assert got[r]["allgatherv"] == expect
+        assert got[r]["barrier"] == 0
         assert got[r]["max_over_ranks"] == float(WORLD)
         assert got[r]["sum_over_ranks"] == float(WORLD * (WORLD + 1) // 2)
