@@ -34,7 +34,7 @@ __all__ = [
     "l1_norm_delta", "linf_norm_delta", "naive_dynamic", "partition_by_degree", "rmat_graph",
     "static_pagerank", "transpose", "update_ranks", "generate_random_batch", "batch_size_from_fraction",
     "derive_seed", "prepare", "LocalTeam", "nccl_unique_id", "share_nccl_unique_id",
-    "context_from_process_group", "attach_symmetric_exchange", "TorchDistTransport", "IpcExchange", "dynamic_traversal", "mark_reachable",
+    "context_from_process_group", "attach_symmetric_exchange", "TorchDistTransport", "IpcExchange", "layout_info", "dynamic_traversal", "mark_reachable",
     "ParseError", "Approach", "ExperimentMode", "ChainMode", "ReportFormat", "ExperimentRow", "ExperimentSpec",
     "approach_name", "approach_from_name", "load_matrix_market", "load_matrix_market_arrays",
     "load_temporal_edge_list", "load_temporal_edge_list_arrays", "split_temporal", "compute_reference_ranks",
@@ -659,6 +659,16 @@ def prepare(g_transpose: CsrGraph, g_forward: CsrGraph, config: Optional[EngineC
                                        C.c_void_p(g_forward.h), int(cfg.low_degree_threshold), int(frontier),
                                        C.byref(ms)))
     return ms.value
+
+
+def layout_info(g_transpose: CsrGraph) -> dict:
+    """The engine layout cached on a transpose graph (dynpr_graph_layout_info):
+    SELL words held by its context, the owned vertex range in relabelled
+    order, and whether the relabelled forward CSR is built."""
+    w, lo, hi, fw = C.c_uint64(), C.c_uint32(), C.c_uint32(), C.c_int()
+    _check(N.lib().dynpr_graph_layout_info(C.c_void_p(g_transpose.h), C.byref(w), C.byref(lo), C.byref(hi),
+                                           C.byref(fw)))
+    return {"sell_words": w.value, "v_lo": lo.value, "v_hi": hi.value, "has_forward": bool(fw.value)}
 
 
 def rmat_graph(scale: int, edge_factor: int = 16, a: float = 0.57, b: float = 0.19, c: float = 0.19,

@@ -37,6 +37,12 @@ class Comm {
   virtual void abort() {}
 };
 
+// A context of a range-partitioned team (world > 1, or the DYNPR_FORCE_TEAM
+// test hook on a 1-rank team): its layouts hold only the rank's rows and its
+// engines exchange after every sweep.
+bool team_forced();
+bool is_team(const dynpr_context* ctx);
+
 // 128-byte NCCL unique id (ncclUniqueId) from the rank-0 process.
 dynpr_status nccl_unique_id(void* out128);
 std::unique_ptr<Comm> make_nccl_comm(int rank, int world, const void* id128);

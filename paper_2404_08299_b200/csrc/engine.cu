@@ -30,6 +30,15 @@
 
 namespace dynpr_b200 {
 
+// Test hook: a 1-rank NCCL / LocalTeam context takes the team path (range
+// plan, collectives, speculative host loop) instead of the single-GPU one,
+// so the real transport code runs on a one-GPU box.
+bool team_forced() {
+  const char* e = std::getenv("DYNPR_FORCE_TEAM");
+  return e && e[0] && e[0] != '0';
+}
+bool is_team(const dynpr_context* ctx) { return ctx->comm && (ctx->comm->world > 1 || team_forced()); }
+
 thread_local std::string g_last_error;
 void set_last_error(const std::string& m) { g_last_error = m; }
 
@@ -145,13 +154,6 @@ struct SolveSpec {
 
 bool host_loop_forced() {
   const char* e = std::getenv("DYNPR_HOST_LOOP");
-  return e && e[0] && e[0] != '0';
-}
-// Test hook: a 1-rank NCCL / LocalTeam context takes the team path (range
-// plan, collectives, speculative host loop) instead of the single-GPU one,
-// so the real transport code runs on a one-GPU box.
-bool team_forced() {
-  const char* e = std::getenv("DYNPR_FORCE_TEAM");
   return e && e[0] && e[0] != '0';
 }
 
@@ -327,7 +329,9 @@ void solve_impl(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynp
   // The engine layout is part of the device graph format (built at ingest
   // or by dynpr_graph_prepare); an uncached build is timed with the solve.
   DYNPR_CK(cudaEventRecord(ctx->ev_a, st));
-  const Layout* L = get_layout(ctx, gT, gF, c.low_degree_threshold, sp.flagged);
+  // a team expands by pull over its own in-lists: only the traversal engine
+  // (markReachable) reads the relabelled forward CSR there
+  const Layout* L = get_layout(ctx, gT, gF, c.low_degree_threshold, is_team(ctx) ? sp.traversal : sp.flagged);
   // workspace (allocation is excluded from the timed region)
   double* R[2] = {ctx->rank[0].as<double>(n), ctx->rank[1].as<double>(n)};
   // Multi-GPU with attached peer buffers: contributions live in the
@@ -387,12 +391,14 @@ void solve_impl(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynp
       DYNPR_CK(cudaMemsetAsync(np, 0, n, st));
       DYNPR_CK(cudaMemsetAsync(red + 1, 0, sizeof(SweepRed), st));
       launch_init_affected(ctx, L->inv, sp.ds, sp.dd, sp.nd, sp.is, sp.ni, va, np);
-      launch_collect_pending(ctx, L->outdeg, nullptr, n, np, c.low_degree_threshold, pl, ph, red + 1);
-      if (device_loop) {  // list sizes stay on the device
-        launch_expand_dev(ctx, L->offF, L->tgtF, va, pl, ph, &red[1].pend_low, nullptr);
-      } else {
-        const SweepRed r0 = read_red(ctx, red + 1);
-        launch_expand(ctx, L->offF, L->tgtF, va, pl, r0.pend_low, ph, r0.pend_high);
+      if (!dist) {  // (a team expands by pull into its own rows, below)
+        launch_collect_pending(ctx, L->outdeg, nullptr, n, np, c.low_degree_threshold, pl, ph, red + 1);
+        if (device_loop) {  // list sizes stay on the device
+          launch_expand_dev(ctx, L->offF, L->tgtF, va, pl, ph, &red[1].pend_low, nullptr);
+        } else {
+          const SweepRed r0 = read_red(ctx, red + 1);
+          launch_expand(ctx, L->offF, L->tgtF, va, pl, r0.pend_low, ph, r0.pend_high);
+        }
       }
     }
   }
@@ -454,6 +460,13 @@ void solve_impl(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynp
     launch_unpack_flags(ctx, fbits, fbounds, comm->world, me, n, np);
   };
   if (dist) team_check_graph(ctx, comm, const_cast<Layout*>(L), gT, gF, red);
+  if (dist && sp.flagged && !sp.traversal && !sp.flags_in) {
+    // initial expandAffected (engine.cpp:199-200) as a pull: every rank holds
+    // the batch's pending flags (replicated), and marks its own rows
+    SweepArgs a0 = a;
+    a0.red = red + 1;  // zeroed above: the pull work queue starts at 0
+    launch_pull_expand(ctx, a0);
+  }
 
   if (fused) {
     // Team barrier: no rank may store into a peer's buffers before that
@@ -613,7 +626,7 @@ void solve(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynpr_sta
   try {
     solve_impl(ctx, sp, ranks_out, stats, obs, user);
   } catch (...) {
-    if (ctx->comm && (ctx->comm->world > 1 || team_forced())) ctx->comm->abort();
+    if (is_team(ctx)) ctx->comm->abort();
     throw;
   }
 }
@@ -898,14 +911,29 @@ dynpr_status dynpr_graph_prepare(dynpr_context* ctx, const dynpr_graph* gT, cons
     if (!ctx) invalid("null context");
     check_pair(gT, gF);
     bind_device(ctx);
-    const Layout* L = get_layout(ctx, gT, gF, threshold, with_forward != 0);
+    // team engines expand by pull: the forward CSR is left to the traversal
+    // engine, which builds it on first use
+    const Layout* L = get_layout(ctx, gT, gF, threshold, with_forward != 0 && !is_team(ctx));
     if (build_ms) *build_ms = L->build_ms;
     // a team's per-snapshot work (edge-balanced range plan, graph
     // fingerprint) belongs to the snapshot build, not to the first solve
-    if (ctx->comm && (ctx->comm->world > 1 || team_forced())) {
+    if (is_team(ctx)) {
       plan_ranges(ctx, const_cast<Layout*>(L), ctx->comm->world);
       ensure_fingerprint(ctx, const_cast<Layout*>(L), gT, gF);
     }
+  });
+}
+
+dynpr_status dynpr_graph_layout_info(const dynpr_graph* gT, uint64_t* sell_words, uint32_t* v_lo, uint32_t* v_hi,
+                                     int* has_forward) {
+  return api_guard([&] {
+    if (!gT) invalid("null graph");
+    const Layout* L = gT->layout;
+    if (!L) invalid("dynpr_graph_layout_info: the graph has no engine layout yet (dynpr_graph_prepare)");
+    if (sell_words) *sell_words = L->sell_words;
+    if (v_lo) *v_lo = L->owned ? L->own.v_lo : 0u;
+    if (v_hi) *v_hi = L->owned ? L->own.v_hi : L->n;
+    if (has_forward) *has_forward = L->has_forward ? 1 : 0;
   });
 }
 
@@ -921,6 +949,8 @@ dynpr_status dynpr_update_ranks(dynpr_context* ctx, const dynpr_graph* gT, const
     if (n == 0) return;
     if (gF->n != n) invalid("engine: graph pair is not mutually transposed (count mismatch)");
     const Layout* L = get_layout(ctx, gT, gF, cfg->low_degree_threshold, false);
+    if (L->owned)
+      invalid("updateRanks: a team context holds only its rank's rows; call it on a single-GPU context");
     const double* prev = stage_in(ctx, ctx->stage_b, previous, n);
     double* R0 = ctx->rank[0].as<double>(n);
     double* R1 = ctx->rank[1].as<double>(n);
@@ -1100,7 +1130,7 @@ dynpr_status dynpr_static_pagerank_csr(dynpr_context* ctx, uint32_t n, const uin
     // A team fingerprints both CSRs of the pair (team_check_graph) on the
     // main stream: gF's targets must have landed (and be valid) first, so a
     // team joins the side upload before the solve instead of after it.
-    if (ctx->comm && (ctx->comm->world > 1 || team_forced())) gF.finish();
+    if (is_team(ctx)) gF.finish();
     SolveSpec sp;
     sp.gT = gT;
     sp.gF = gF.g;

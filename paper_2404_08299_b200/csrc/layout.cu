@@ -2,7 +2,9 @@
 // SELL-32 segment slices, relabelled forward CSR.
 #include <cub/cub.cuh>
 
+#include "comm.cuh"
 #include "layout.cuh"
+#include "sweep.cuh"
 
 namespace dynpr_b200 {
 
@@ -101,12 +103,12 @@ __device__ __forceinline__ void fill_lane(uint32_t* sell, uint64_t base, unsigne
 
 // SELL fill, single region: warp per slice, lane per vertex
 __global__ void k_fill_single(const uint64_t* offT, const uint32_t* tgtT, const uint32_t* perm, const uint32_t* inv,
-                              const uint32_t* indeg, uint32_t M, uint32_t n, uint64_t S, const uint64_t* sbase,
-                              uint32_t* sell) {
+                              const uint32_t* indeg, uint32_t M, uint32_t n, uint64_t s_lo, uint64_t s_hi,
+                              const uint64_t* sbase, uint32_t* sell) {
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / 32;
   const unsigned lane = threadIdx.x & 31;
   const uint64_t nw = (uint64_t)gridDim.x * blockDim.x / 32;
-  for (uint64_t s = warp; s < S; s += nw) {
+  for (uint64_t s = s_lo + warp; s < s_hi; s += nw) {
     const uint64_t vn = M + s * 32 + lane;
     const bool valid = vn < n;
     const uint32_t deg = valid ? indeg[vn] : 0u;
@@ -119,11 +121,11 @@ __global__ void k_fill_single(const uint64_t* offT, const uint32_t* tgtT, const 
 // SELL fill, multi region: warp per slice, lane per 256-edge segment
 __global__ void k_fill_multi(const uint64_t* offT, const uint32_t* tgtT, const uint32_t* perm, const uint32_t* inv,
                              const uint32_t* pbase, const uint32_t* mseg_v, const uint32_t* mseg_len, uint64_t nseg,
-                             uint64_t S, const uint64_t* mbase, uint32_t* sell) {
+                             uint64_t s_lo, uint64_t s_hi, const uint64_t* mbase, uint32_t* sell) {
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / 32;
   const unsigned lane = threadIdx.x & 31;
   const uint64_t nw = (uint64_t)gridDim.x * blockDim.x / 32;
-  for (uint64_t s = warp; s < S; s += nw) {
+  for (uint64_t s = s_lo + warp; s < s_hi; s += nw) {
     const uint64_t seg = s * 32 + lane;
     const bool valid = seg < nseg;
     uint32_t len = 0;
@@ -306,8 +308,6 @@ Layout* build_layout(dynpr_context* ctx, const dynpr_graph* gT, const dynpr_grap
     cub_call(ctx, [&](void* t, size_t& b) {
       return cub::DeviceScan::ExclusiveSum(t, b, L->sbase, L->sbase, (int64_t)L->n_sslices + 1, st);
     });
-    const uint64_t sell_s_len = read_u64(ctx, L->sbase + L->n_sslices);
-    L->sell_s = dalloc<uint32_t>(ctx, sell_s_len);
     // multi region segments
     L->pbase = dalloc<uint32_t>(ctx, (uint64_t)M + 1);
     k_multi_nch<<<grid(ctx, (uint64_t)M + 1), 256, 0, st>>>(L->indeg, M, L->pbase);
@@ -336,17 +336,33 @@ Layout* build_layout(dynpr_context* ctx, const dynpr_graph* gT, const dynpr_grap
     cub_call(ctx, [&](void* t, size_t& b) {
       return cub::DeviceScan::ExclusiveSum(t, b, L->mbase, L->mbase, (int64_t)L->n_mslices + 1, st);
     });
-    const uint64_t sell_m_len = read_u64(ctx, L->mbase + L->n_mslices);
-    L->sell_m = dalloc<uint32_t>(ctx, sell_m_len);
-    if (L->n_sslices) {
-      k_fill_single<<<grid(ctx, L->n_sslices * 32), 256, 0, st>>>(gT->off, gT->tgt, L->perm, L->inv, L->indeg, M, n,
-                                                                 L->n_sslices, L->sbase, L->sell_s);
+    // the slices this context sweeps: all of them, or on a team context
+    // the rank's edge-balanced range (its in-CSR rows only)
+    uint64_t ss_lo = 0, ss_hi = L->n_sslices, ms_lo = 0, ms_hi = L->n_mslices;
+    if (is_team(ctx)) {
+      L->owned = true;
+      L->own = plan_ranges(ctx, L, ctx->comm->world)[ctx->comm->rank];
+      ss_lo = L->own.ss_lo;
+      ss_hi = L->own.ss_hi;
+      ms_lo = L->own.ms_lo;
+      ms_hi = L->own.ms_hi;
+    }
+    const uint64_t s_w0 = read_u64(ctx, L->sbase + ss_lo), s_w1 = read_u64(ctx, L->sbase + ss_hi);
+    const uint64_t m_w0 = read_u64(ctx, L->mbase + ms_lo), m_w1 = read_u64(ctx, L->mbase + ms_hi);
+    L->sell_s_alloc = dalloc<uint32_t>(ctx, s_w1 - s_w0);
+    L->sell_m_alloc = dalloc<uint32_t>(ctx, m_w1 - m_w0);
+    L->sell_s = L->sell_s_alloc - s_w0;  // indexed by sbase[s], s in the owned range
+    L->sell_m = L->sell_m_alloc - m_w0;
+    L->sell_words = (s_w1 - s_w0) + (m_w1 - m_w0);
+    if (ss_hi > ss_lo) {
+      k_fill_single<<<grid(ctx, (ss_hi - ss_lo) * 32), 256, 0, st>>>(gT->off, gT->tgt, L->perm, L->inv, L->indeg, M,
+                                                                     n, ss_lo, ss_hi, L->sbase, L->sell_s);
       check_launch();
     }
-    if (L->n_mslices) {
-      k_fill_multi<<<grid(ctx, L->n_mslices * 32), 256, 0, st>>>(gT->off, gT->tgt, L->perm, L->inv, L->pbase,
-                                                                L->mseg_v, L->mseg_len, L->n_mseg, L->n_mslices,
-                                                                L->mbase, L->sell_m);
+    if (ms_hi > ms_lo) {
+      k_fill_multi<<<grid(ctx, (ms_hi - ms_lo) * 32), 256, 0, st>>>(gT->off, gT->tgt, L->perm, L->inv, L->pbase,
+                                                                    L->mseg_v, L->mseg_len, L->n_mseg, ms_lo, ms_hi,
+                                                                    L->mbase, L->sell_m);
       check_launch();
     }
     count_launch(ctx, 6);
@@ -360,8 +376,9 @@ Layout* build_layout(dynpr_context* ctx, const dynpr_graph* gT, const dynpr_grap
 }  // namespace
 
 Layout::~Layout() {
-  for (void* p : {(void*)perm, (void*)inv, (void*)indeg, (void*)outdeg, (void*)sbase, (void*)sell_s, (void*)mbase,
-                  (void*)mseg_v, (void*)mseg_len, (void*)pbase, (void*)sell_m, (void*)mcount, (void*)offF, (void*)tgtF})
+  for (void* p : {(void*)perm, (void*)inv, (void*)indeg, (void*)outdeg, (void*)sbase, (void*)sell_s_alloc,
+                  (void*)mbase, (void*)mseg_v, (void*)mseg_len, (void*)pbase, (void*)sell_m_alloc, (void*)mcount,
+                  (void*)offF, (void*)tgtF})
     pool_free(ctx, p);
 }
 

@@ -70,6 +70,15 @@ struct Layout {
   uint32_t* mseg_len = nullptr;
   uint32_t* pbase = nullptr;   // first segment of multi vertex v (M + 1)
   uint32_t* sell_m = nullptr;
+  // Multi-GPU team layouts hold only this rank's rows: sell_s / sell_m are
+  // then virtual bases (valid for the owned slices [own.ss_lo, own.ss_hi) /
+  // [own.ms_lo, own.ms_hi) only) into the allocations below (SURVEY 8e:
+  // per-rank in-CSR rows; the O(n) vertex arrays stay whole).
+  bool owned = false;
+  RankRange own{};
+  uint32_t* sell_s_alloc = nullptr;
+  uint32_t* sell_m_alloc = nullptr;
+  uint64_t sell_words = 0;  // SELL words held on this rank (both regions)
   uint32_t* mcount = nullptr;  // per multi vertex: chunks finished this sweep (0 between sweeps)
   // relabelled forward CSR (frontier engines)
   bool has_forward = false;
@@ -85,7 +94,8 @@ struct Layout {
 };
 
 // Returns the cached layout of (gT, gF, T), building it if needed.  When
-// `need_forward` the relabelled forward CSR is built too.
+// `need_forward` the relabelled forward CSR is built too.  On a team context
+// (multi-GPU) the layout holds only the calling rank's rows.
 Layout* get_layout(dynpr_context* ctx, const dynpr_graph* gT, const dynpr_graph* gF, uint32_t T,
                    bool need_forward);
 void destroy_layout(Layout* L);

@@ -270,3 +270,50 @@ def test_tiny_graphs_on_a_wide_team(dp, n):
     out, _ = run_team(dp, 4, fn)
     for o in out:
         same(o, single)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_team_layout_holds_only_owned_rows(dp, world):
+    """SURVEY 8e ownership: a team rank's engine layout holds only its own
+    in-CSR rows (SELL slices of its edge-balanced vertex range), so the
+    per-rank layout memory is ~1/world of the single-GPU one; the owned
+    ranges tile the vertex space; team DF/DF-P expand by pull and never
+    build the relabelled forward CSR."""
+    scale = 14
+    g = dp.rmat_graph(scale)
+    gt = dp.transpose(g)
+    dp.prepare(gt, g)
+    whole = dp.layout_info(gt)
+    assert whole["v_lo"] == 0 and whole["v_hi"] == g.vertex_count and whole["has_forward"]
+
+    def fn(ctx, r):
+        h = dp.rmat_graph(scale, ctx=ctx)
+        ht = dp.transpose(h)
+        dp.prepare(ht, h)
+        info = dp.layout_info(ht)
+        batch = dp.generate_random_batch(h, 200, 0.8, 3)
+        h2, ht2 = dp.apply_batch_pair(h, ht, batch)
+        b = dp.static_pagerank(ht, h)
+        d = dp.dynamic_frontier(h2, ht2, batch.deletions, batch.insertions, b.ranks, pruning=True)
+        with pytest.raises(ValueError, match="team context"):
+            dp.update_ranks(ht, h, b.ranks)
+        return info, dp.layout_info(ht2), d
+
+    out, _ = run_team(dp, world, fn)
+    infos = [o[0] for o in out]
+    assert infos[0]["v_lo"] == 0 and infos[-1]["v_hi"] == g.vertex_count
+    for a, b in zip(infos, infos[1:]):
+        assert a["v_hi"] == b["v_lo"]
+    total = sum(i["sell_words"] for i in infos)
+    assert whole["sell_words"] <= total <= whole["sell_words"] * 1.02  # boundary slices only
+    for i in infos:
+        assert i["sell_words"] <= whole["sell_words"] / world * 1.25
+        assert not i["has_forward"]
+    for _, after, _ in out:
+        assert not after["has_forward"]
+    batch = dp.generate_random_batch(g, 200, 0.8, 3)
+    g2, gt2 = dp.apply_batch_pair(g, gt, batch)
+    single = dp.dynamic_frontier(g2, gt2, batch.deletions, batch.insertions, dp.static_pagerank(gt, g).ranks,
+                                 pruning=True)
+    for _, _, d in out:
+        same(d, single)
