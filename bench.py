@@ -366,6 +366,9 @@ def run_ours(args, world, rank, local):
                 exchange = "fused: sweep epilogue stores contributions into all peers over NVLink"
             except Exception as e:  # plumbing unavailable: keep the all-gather transport
                 exchange += " (fused exchange unavailable: %s)" % str(e).splitlines()[0][:120]
+    # the base snapshot's engine layout, with the relabelled forward CSR the
+    # frontier engines read: every batch's snapshot derives its layout from it
+    dp.prepare(gt0, g0)
     base = dp.static_pagerank(gt0, g0)
     base_dev = torch.from_numpy(base.ranks).to(f"cuda:{local}")
     size = dp.batch_size_from_fraction(args.batch_frac, m0)

@@ -245,12 +245,15 @@ dynpr_status dynpr_graph_prepare(dynpr_context* ctx, const dynpr_graph* gT,
 /* The cached engine layout of gT (after dynpr_graph_prepare or a solve):
  * SELL words held by this context (a team rank holds only its own rows:
  * about 1/world of the single-GPU figure), the owned vertex range
- * [v_lo, v_hi) in the layout's relabelled order (everything on one GPU), and
- * whether the relabelled forward CSR is built.  DYNPR_INVALID_ARGUMENT if
- * gT has no layout yet.  Any output may be null. */
+ * [v_lo, v_hi) in the layout's relabelled order (everything on one GPU),
+ * whether the relabelled forward CSR is built, and its generation: 0 for a
+ * layout built from scratch, k for one derived incrementally k batches after
+ * (dynpr_graph_apply_batch_pair of a prepared pair seeds the derivation).
+ * DYNPR_INVALID_ARGUMENT if gT has no layout yet.  Outputs may be null. */
 dynpr_status dynpr_graph_layout_info(const dynpr_graph* gT,
                                      uint64_t* sell_words, uint32_t* v_lo,
-                                     uint32_t* v_hi, int* has_forward);
+                                     uint32_t* v_hi, int* has_forward,
+                                     int* generation);
 
 /* ---- workload (workload.hpp:189-197, rng.hpp:44-47) --------------------- */
 /* batchSizeFromFraction (workload.cpp:245-249): round half up, floor 1. */

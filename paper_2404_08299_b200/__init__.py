@@ -664,11 +664,13 @@ def prepare(g_transpose: CsrGraph, g_forward: CsrGraph, config: Optional[EngineC
 def layout_info(g_transpose: CsrGraph) -> dict:
     """The engine layout cached on a transpose graph (dynpr_graph_layout_info):
     SELL words held by its context, the owned vertex range in relabelled
-    order, and whether the relabelled forward CSR is built."""
-    w, lo, hi, fw = C.c_uint64(), C.c_uint32(), C.c_uint32(), C.c_int()
+    order, whether the relabelled forward CSR is built, and the generation
+    (0 = built from scratch, k = derived incrementally k batches after)."""
+    w, lo, hi, fw, gen = C.c_uint64(), C.c_uint32(), C.c_uint32(), C.c_int(), C.c_int()
     _check(N.lib().dynpr_graph_layout_info(C.c_void_p(g_transpose.h), C.byref(w), C.byref(lo), C.byref(hi),
-                                           C.byref(fw)))
-    return {"sell_words": w.value, "v_lo": lo.value, "v_hi": hi.value, "has_forward": bool(fw.value)}
+                                           C.byref(fw), C.byref(gen)))
+    return {"sell_words": w.value, "v_lo": lo.value, "v_hi": hi.value, "has_forward": bool(fw.value),
+            "generation": gen.value}
 
 
 def rmat_graph(scale: int, edge_factor: int = 16, a: float = 0.57, b: float = 0.19, c: float = 0.19,

@@ -130,7 +130,7 @@ PROTOTYPES = {
     "dynpr_context_rank": (_i, [_vp, _ip, _ip]),
     "dynpr_context_attach_peers": (_i, [_vp, _i, _vp, _vp, _u64]),
     "dynpr_context_create_hostcomm": (_i, [_i, _i, _i, C.POINTER(CommOps), _vp, _pvp]),
-    "dynpr_graph_layout_info": (_i, [_vp, _u64p, _u32p, _u32p, _ip]),
+    "dynpr_graph_layout_info": (_i, [_vp, _u64p, _u32p, _u32p, _ip, _ip]),
     "dynpr_ipc_alloc": (_i, [_vp, _u64, _pvp, _vp]),
     "dynpr_ipc_open": (_i, [_vp, _vp, _pvp]),
     "dynpr_ipc_close": (_i, [_vp, _vp]),

@@ -10,6 +10,7 @@
 
 #include <cstdint>
 #include <cstring>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -154,11 +155,16 @@ struct dynpr_context {
 
 namespace dynpr_b200 {
 struct Layout;
+struct LayoutSeed;
 }
 
 struct dynpr_graph {
   uint64_t id = 0;          // unique per snapshot (layout cache key)
-  dynpr_b200::Layout* layout = nullptr;  // cached engine layout (transpose side)
+  std::shared_ptr<dynpr_b200::Layout> layout;  // cached engine layout (transpose side)
+  // set by apply_batch_pair on the new transpose: the parent snapshot's
+  // layout + the rows the batch touched, from which the new layout is
+  // derived incrementally (layout.cu) instead of rebuilt
+  std::shared_ptr<dynpr_b200::LayoutSeed> seed;
   dynpr_context* ctx = nullptr;
   uint32_t n = 0;
   uint64_t m = 0;
@@ -326,6 +332,8 @@ struct DeferredCsr {
 cudaStream_t side_stream(dynpr_context* ctx);
 void upload_csr_deferred(dynpr_context* ctx, uint32_t n, const uint64_t* offsets, const uint32_t* targets,
                          uint64_t m, cudaEvent_t after, DeferredCsr& d);
+uint32_t* copy_untouched_rows(dynpr_context* ctx, const uint8_t* touched, uint32_t n, const uint64_t* off,
+                              const uint32_t* tgt, const uint64_t* noff, uint32_t* ntgt, unsigned long long* nt);
 void graph_apply_batch_impl(dynpr_context* ctx, const dynpr_graph* g,
                             const uint32_t* d_ds, const uint32_t* d_dd,
                             uint64_t nd, const uint32_t* d_is,
@@ -333,6 +341,7 @@ void graph_apply_batch_impl(dynpr_context* ctx, const dynpr_graph* g,
                             const uint32_t* h_ds, const uint32_t* h_dd,
                             const uint32_t* h_is, const uint32_t* h_id,
                             dynpr_graph** out, uint64_t* missing,
-                            uint64_t* duplicate);
+                            uint64_t* duplicate, uint32_t** rows_out = nullptr,
+                            uint64_t* nrows_out = nullptr);
 
 }  // namespace dynpr_b200

@@ -925,15 +925,16 @@ dynpr_status dynpr_graph_prepare(dynpr_context* ctx, const dynpr_graph* gT, cons
 }
 
 dynpr_status dynpr_graph_layout_info(const dynpr_graph* gT, uint64_t* sell_words, uint32_t* v_lo, uint32_t* v_hi,
-                                     int* has_forward) {
+                                     int* has_forward, int* generation) {
   return api_guard([&] {
     if (!gT) invalid("null graph");
-    const Layout* L = gT->layout;
+    const Layout* L = gT->layout.get();
     if (!L) invalid("dynpr_graph_layout_info: the graph has no engine layout yet (dynpr_graph_prepare)");
     if (sell_words) *sell_words = L->sell_words;
     if (v_lo) *v_lo = L->owned ? L->own.v_lo : 0u;
     if (v_hi) *v_hi = L->owned ? L->own.v_hi : L->n;
     if (has_forward) *has_forward = L->has_forward ? 1 : 0;
+    if (generation) *generation = L->generation;
   });
 }
 

@@ -564,7 +564,8 @@ dynpr_graph* make_graph(dynpr_context* ctx, uint32_t n, uint64_t m) {
 
 void destroy_graph(dynpr_graph* g) {
   if (!g) return;
-  if (g->layout) destroy_layout(g->layout);
+  g->layout.reset();  // (freed through the context's pool: before its teardown)
+  g->seed.reset();
   dynpr_context* ctx = g->ctx;
   pool_free(ctx, g->off);
   pool_free(ctx, g->tgt);
@@ -601,6 +602,30 @@ static dynpr_graph* build_from_device_edges(dynpr_context* ctx, uint32_t n,
   return g;
 }
 
+// Rows of `touched` (flags, n entries) listed in order, and every run of
+// untouched rows between them copied from (off, tgt) to (noff, ntgt) in
+// 8K-word pieces: the part of a CSR rebuild that is a plain copy.  `nt` =
+// device count of touched rows; the list is left in ctx->run_list.
+uint32_t* copy_untouched_rows(dynpr_context* ctx, const uint8_t* touched, uint32_t n, const uint64_t* off,
+                              const uint32_t* tgt, const uint64_t* noff, uint32_t* ntgt, unsigned long long* nt) {
+  cudaStream_t st = ctx->stream;
+  uint32_t* T = ctx->run_list.as<uint32_t>((uint64_t)n + 1);
+  uint32_t* pcs = ctx->run_pieces.as<uint32_t>((uint64_t)n + 3);
+  cub::CountingInputIterator<uint32_t> iota(0);
+  cub_call(ctx, [&](void* t, size_t& b) {
+    return cub::DeviceSelect::Flagged(t, b, iota, touched, T, nt, (int64_t)n, st);
+  });
+  k_run_pieces<<<grid_for((uint64_t)n + 2, 256, 1 << 16), 256, 0, st>>>(T, nt, n, off, pcs);
+  check_launch();
+  cub_call(ctx, [&](void* t, size_t& b) {
+    return cub::DeviceScan::ExclusiveSum(t, b, pcs, pcs, (int64_t)n + 3, st);
+  });
+  k_copy_runs<<<(unsigned)ctx->num_sms * 32, 256, 0, st>>>(T, nt, pcs, n, off, tgt, noff, ntgt);
+  check_launch();
+  count_launch(ctx, 2);
+  return T;
+}
+
 void graph_apply_batch_impl(dynpr_context* ctx, const dynpr_graph* g,
                             const uint32_t* d_ds, const uint32_t* d_dd,
                             uint64_t nd, const uint32_t* d_is,
@@ -608,7 +633,8 @@ void graph_apply_batch_impl(dynpr_context* ctx, const dynpr_graph* g,
                             const uint32_t* h_ds, const uint32_t* h_dd,
                             const uint32_t* h_is, const uint32_t* h_id,
                             dynpr_graph** out, uint64_t* missing_out,
-                            uint64_t* duplicate_out) {
+                            uint64_t* duplicate_out, uint32_t** rows_out,
+                            uint64_t* nrows_out) {
   const uint32_t n = g->n;
   cudaStream_t st = ctx->stream;
   if (validate) {  // graph.cpp:116-120, in the reference's order
@@ -740,24 +766,19 @@ void graph_apply_batch_impl(dynpr_context* ctx, const dynpr_graph* g,
       return cub::DeviceScan::ExclusiveSum(t, b, istart, istart, (int64_t)n + 1, st);
     });
     // touched rows in order -> runs of untouched rows -> pieces -> copies
-    uint32_t* T = ctx->run_list.as<uint32_t>((uint64_t)n + 1);
-    uint32_t* pcs = ctx->run_pieces.as<uint32_t>((uint64_t)n + 3);
     auto* nt = reinterpret_cast<unsigned long long*>(ctx->scratch64a.as<unsigned long long>(4)) + 2;
-    cub::CountingInputIterator<uint32_t> iota(0);
-    cub_call(ctx, [&](void* t, size_t& b) {
-      return cub::DeviceSelect::Flagged(t, b, iota, touched, T, nt, (int64_t)n, st);
-    });
-    k_run_pieces<<<grid_for((uint64_t)n + 2, 256, 1 << 16), 256, 0, st>>>(T, nt, n, g->off, pcs);
-    check_launch();
-    cub_call(ctx, [&](void* t, size_t& b) {
-      return cub::DeviceScan::ExclusiveSum(t, b, pcs, pcs, (int64_t)n + 3, st);
-    });
-    k_copy_runs<<<(unsigned)ctx->num_sms * 32, 256, 0, st>>>(T, nt, pcs, n, g->off, g->tgt, r->off, r->tgt);
-    check_launch();
+    uint32_t* T = copy_untouched_rows(ctx, touched, n, g->off, g->tgt, r->off, r->tgt, nt);
     k_merge_touched<<<(unsigned)ctx->num_sms * 16, 256, 0, st>>>(istart, n, g->off, g->tgt, r->off, r->tgt, dp,
                                                                  ndp, nw, nnw, sb, mask, need);
     check_launch();
-    count_launch(ctx, 5);
+    count_launch(ctx, 3);
+    if (rows_out) {  // the touched rows, for an incremental engine layout (layout.cu)
+      const uint64_t cnt = read_u64(ctx, nt);
+      uint32_t* rows = pool_alloc_n<uint32_t>(ctx, cnt ? cnt : 1);
+      if (cnt) DYNPR_CK(cudaMemcpyAsync(rows, T, cnt * 4, cudaMemcpyDeviceToDevice, st));
+      *rows_out = rows;
+      *nrows_out = cnt;
+    }
   }
   unsigned long long hc[2];
   DYNPR_CK(cudaMemcpyAsync(ctx->pinned, counters, 16, cudaMemcpyDeviceToHost, st));
@@ -1001,19 +1022,34 @@ static dynpr_status apply_batch_common(dynpr_context* ctx, const dynpr_graph* gF
     const uint32_t* d_is = stage_in(ctx, ctx->batch[2], is, ni);
     const uint32_t* d_id = stage_in(ctx, ctx->batch[3], id, ni);
     const bool hd = nd && !is_device_ptr(ds), hi = ni && !is_device_ptr(is);
+    // The new pair's engine layout can be derived from the parent's when the
+    // parent pair has one (single-GPU layouts; both graphs carry every
+    // self-loop, so only the batch's rows change): record the touched rows.
+    const bool seeded = gT && gT->layout && !gT->layout->owned && gT->layout->gF_id == gF->id &&
+                        gF->all_loops && gT->all_loops && gT->ctx == ctx && gF->ctx == ctx;
+    auto seed = seeded ? std::make_shared<LayoutSeed>() : nullptr;
+    if (seed) {
+      seed->ctx = ctx;
+      seed->parent = gT->layout;
+    }
     dynpr_graph* f = nullptr;
     graph_apply_batch_impl(ctx, gF, d_ds, d_dd, nd, d_is, d_id, ni, true, hd ? ds : nullptr,
                            hd ? dd : nullptr, hi ? is : nullptr, hi ? id : nullptr, &f, missing,
-                           duplicate);
+                           duplicate, seed ? &seed->rows_F : nullptr, seed ? &seed->n_F : nullptr);
     if (gT) {
       dynpr_graph* t = nullptr;
       try {
         // reversed batch on the transpose (ids already validated)
         graph_apply_batch_impl(ctx, gT, d_dd, d_ds, nd, d_id, d_is, ni, false, nullptr, nullptr,
-                               nullptr, nullptr, &t, nullptr, nullptr);
+                               nullptr, nullptr, &t, nullptr, nullptr, seed ? &seed->rows_T : nullptr,
+                               seed ? &seed->n_T : nullptr);
       } catch (...) {
         destroy_graph(f);
         throw;
+      }
+      if (seed) {
+        seed->gF_id = f->id;
+        t->seed = std::move(seed);
       }
       *outT = t;
     }

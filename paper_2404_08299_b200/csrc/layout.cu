@@ -206,6 +206,147 @@ __global__ void k_scatter_inv_u8(const uint32_t* inv, uint32_t n, const uint8_t*
   GRID_STRIDE(o, n) dst[o] = src[inv[o]];
 }
 
+
+// A SELL block owned (shared) by layout L: freed when the last layout
+// reading it goes.
+uint32_t* new_block(dynpr_context* ctx, Layout* L, uint64_t words) {
+  uint32_t* p = dalloc<uint32_t>(ctx, words);
+  L->blocks.emplace_back(p, [ctx](uint32_t* q) { pool_free(ctx, q); });
+  return p;
+}
+// 64-bit element offset of `p` from base `b` (two's complement when p < b):
+// `b + offset` addresses p
+uint64_t rel_words(const uint32_t* b, const uint32_t* p) {
+  const int64_t bytes = (int64_t)((uintptr_t)p - (uintptr_t)b);
+  return (uint64_t)(bytes / 4);
+}
+
+// ---- incremental derivation (build_incremental) --------------------------------
+// touched rows (old ids): flag in the relabelled space + the new degree
+__global__ void k_mark_rows(const uint32_t* rows, uint64_t cnt, const uint32_t* inv, const uint64_t* off,
+                            uint8_t* flag, uint32_t* deg) {
+  GRID_STRIDE(i, cnt) {
+    const uint32_t u = rows[i], w = inv[u];
+    flag[w] = 1;
+    deg[w] = (uint32_t)(off[u + 1] - off[u]);
+  }
+}
+// single region, stale order: slice length = the longest of its 32 segments
+__global__ void k_single_slice_len_max(const uint32_t* indeg, uint32_t M, uint32_t n, uint64_t S, uint64_t* len32) {
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / 32;
+  const unsigned lane = threadIdx.x & 31;
+  const uint64_t nw = (uint64_t)gridDim.x * blockDim.x / 32;
+  for (uint64_t s = warp; s <= S; s += nw) {
+    const uint64_t v = (uint64_t)M + 32 * s + lane;
+    const unsigned d = (s < S && v < n) ? indeg[v] : 0u;
+    const unsigned mx = __reduce_max_sync(0xffffffffu, d);
+    if (lane == 0) len32[s] = 32ull * ((mx + 3u) & ~3u);
+  }
+}
+// One lane's segment copied from its position in the parent layout (column
+// ids are in the same relabelled space): 16-byte groups, zero padding.
+__device__ __forceinline__ void copy_lane(uint32_t* sell, uint64_t base, unsigned lane, uint32_t L, uint32_t len,
+                                          const uint32_t* old, uint64_t obase, unsigned olane) {
+  for (uint32_t k = 0; k < L; k += 4) {
+    const uint4 w = k < len ? *reinterpret_cast<const uint4*>(old + sell_pos(obase, olane, k)) : make_uint4(0, 0, 0, 0);
+    *reinterpret_cast<uint4*>(sell + sell_pos(base, lane, k)) = w;
+  }
+}
+// single region, copy-on-write: a slice is re-built iff one of its vertices'
+// in-lists changed; its length is then the longest of its 32 new segments
+// (the relabelling is no longer sorted), else it is shared.
+__global__ void k_slice_touched_len(const uint32_t* indeg, const uint8_t* touched, uint32_t M, uint32_t n,
+                                    uint64_t S, uint64_t* len32) {
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / 32;
+  const unsigned lane = threadIdx.x & 31;
+  const uint64_t nw = (uint64_t)gridDim.x * blockDim.x / 32;
+  for (uint64_t s = warp; s <= S; s += nw) {
+    const uint64_t v = (uint64_t)M + 32 * s + lane;
+    const bool in = s < S && v < n;
+    const unsigned d = in ? indeg[v] : 0u;
+    const bool any = __any_sync(0xffffffffu, in && touched[v]);
+    const unsigned mx = __reduce_max_sync(0xffffffffu, d);
+    if (lane == 0) len32[s] = any ? 32ull * ((mx + 3u) & ~3u) : 0ull;
+  }
+}
+__global__ void k_sbase_cow(const uint64_t* sbase0, const uint64_t* len32, const uint64_t* dpos, uint64_t S,
+                            uint64_t rel, uint64_t* sbase) {
+  GRID_STRIDE(s, S + 1) sbase[s] = (s < S && len32[s]) ? rel + dpos[s] : sbase0[s];
+}
+__global__ void k_fill_single_cow(const uint64_t* offT, const uint32_t* tgtT, const uint32_t* perm,
+                                  const uint32_t* inv, const uint32_t* indeg, uint32_t M, uint32_t n, uint64_t S,
+                                  const uint64_t* len32, const uint64_t* sbase, uint32_t* sell,
+                                  const uint8_t* touched, const uint64_t* sbase0) {
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / 32;
+  const unsigned lane = threadIdx.x & 31;
+  const uint64_t nw = (uint64_t)gridDim.x * blockDim.x / 32;
+  for (uint64_t s = warp; s < S; s += nw) {
+    const uint32_t L = (uint32_t)(len32[s] / 32);
+    if (!L) continue;  // shared with the parent
+    const uint64_t vn = M + s * 32 + lane;
+    const bool valid = vn < n;
+    const uint32_t deg = valid ? indeg[vn] : 0u;
+    if (valid && touched[vn])
+      fill_lane(sell, sbase[s], lane, L, deg, tgtT + offT[perm[vn]], inv);
+    else
+      copy_lane(sell, sbase[s], lane, L, deg, sell, sbase0[s], lane);
+  }
+}
+// multi region, copy-on-write: the chunks of a vertex whose in-list changed
+// are retired in place (length 0: every sweep skips them) and re-built as
+// new segments appended after the parent's (from a slice boundary on); the
+// vertex's pbase points to them.  Untouched vertices keep their slices.
+__global__ void k_multi_touched_nch(const uint32_t* indeg, const uint8_t* touched, uint32_t M, uint32_t* nch) {
+  GRID_STRIDE(v, (uint64_t)M + 1) nch[v] = (v < M && touched[v]) ? (indeg[v] + 255u) / 256u : 0u;
+}
+__global__ void k_multi_cow_segments(const uint32_t* indeg, const uint32_t* indeg0, const uint8_t* touched,
+                                     uint32_t M, const uint32_t* apos, uint64_t first, const uint32_t* pbase0,
+                                     uint32_t* pbase, uint32_t* mseg_v, uint32_t* mseg_len) {
+  GRID_STRIDE(v, M) {
+    if (!touched[v]) continue;
+    const uint32_t d0 = indeg0[v], p0 = pbase0[v];
+    for (uint32_t j = 0; j < (d0 + 255u) / 256u; ++j) mseg_len[p0 + j] = 0u;  // retired
+    const uint32_t d = indeg[v], b = (uint32_t)(first + apos[v]);
+    const uint32_t nch = (d + 255u) / 256u;
+    pbase[v] = b;
+    for (uint32_t j = 0; j < nch; ++j) {
+      mseg_v[b + j] = (uint32_t)v;
+      mseg_len[b + j] = (j + 1 < nch) ? 256u : d - 256u * j;
+    }
+  }
+}
+__global__ void k_mbase_append(uint64_t* mbase, uint64_t s0, uint64_t cnt, uint64_t rel) {
+  GRID_STRIDE(i, cnt + 1) mbase[s0 + i] += rel;
+}
+
+// relabelled forward CSR, touched rows (the untouched ones are copied as
+// runs, graph.cu copy_untouched_rows): rows cut into 4K-element items so a
+// touched hub spreads over many warps; item t -> row by binary search of the
+// items' exclusive scan
+constexpr uint64_t kRowItem = 4096;
+__global__ void k_row_items(const uint32_t* rows, const unsigned long long* cnt, const uint32_t* deg,
+                            uint32_t* items) {
+  const uint64_t c = *cnt;
+  GRID_STRIDE(i, c + 1) items[i] = i < c ? (uint32_t)((deg[rows[i]] + kRowItem - 1) / kRowItem) : 0u;
+}
+__global__ void k_refill_rows(const uint32_t* rows, const unsigned long long* cnt, const uint32_t* istart,
+                              const uint64_t* offF, const uint32_t* tgtF, const uint32_t* perm, const uint32_t* inv,
+                              const uint64_t* noff, uint32_t* ntgt) {
+  const uint64_t c = *cnt;
+  const uint32_t total = istart[c];
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / 32;
+  const unsigned lane = threadIdx.x & 31;
+  const uint64_t nw = (uint64_t)gridDim.x * blockDim.x / 32;
+  for (uint64_t t = warp; t < total; t += nw) {
+    const uint64_t j = upper_bound_u32(istart, c + 1, (uint32_t)t) - 1;
+    const uint32_t w = rows[j];
+    const uint64_t len = noff[w + 1] - noff[w];
+    const uint64_t k0 = (t - istart[j]) * kRowItem, k1 = k0 + kRowItem < len ? k0 + kRowItem : len;
+    const uint32_t* src = tgtF + offF[perm[w]];
+    for (uint64_t k = k0 + lane; k < k1; k += 32) ntgt[noff[w] + k] = inv[src[k]];
+  }
+}
+
 unsigned grid(dynpr_context* ctx, uint64_t items) { return grid_for(items, 256, ctx->num_sms * 32); }
 
 uint64_t read_u64(dynpr_context* ctx, const void* d) {
@@ -349,10 +490,10 @@ Layout* build_layout(dynpr_context* ctx, const dynpr_graph* gT, const dynpr_grap
     }
     const uint64_t s_w0 = read_u64(ctx, L->sbase + ss_lo), s_w1 = read_u64(ctx, L->sbase + ss_hi);
     const uint64_t m_w0 = read_u64(ctx, L->mbase + ms_lo), m_w1 = read_u64(ctx, L->mbase + ms_hi);
-    L->sell_s_alloc = dalloc<uint32_t>(ctx, s_w1 - s_w0);
-    L->sell_m_alloc = dalloc<uint32_t>(ctx, m_w1 - m_w0);
-    L->sell_s = L->sell_s_alloc - s_w0;  // indexed by sbase[s], s in the owned range
-    L->sell_m = L->sell_m_alloc - m_w0;
+    uint32_t* sa = new_block(ctx, L, s_w1 - s_w0);
+    uint32_t* ma = new_block(ctx, L, m_w1 - m_w0);
+    L->sell_s = sa - s_w0;  // indexed by sbase[s], s in the owned range
+    L->sell_m = ma - m_w0;
     L->sell_words = (s_w1 - s_w0) + (m_w1 - m_w0);
     if (ss_hi > ss_lo) {
       k_fill_single<<<grid(ctx, (ss_hi - ss_lo) * 32), 256, 0, st>>>(gT->off, gT->tgt, L->perm, L->inv, L->indeg, M,
@@ -373,31 +514,209 @@ Layout* build_layout(dynpr_context* ctx, const dynpr_graph* gT, const dynpr_grap
   return L;
 }
 
+
+// The layout of a snapshot pair derived from its parent pair's (same vertex
+// relabelling, so every column id already stored stays valid): in-lists the
+// batch did not touch are copied segment by segment from the parent's SELL
+// slices, touched ones re-gathered from the new transpose; the forward CSR
+// likewise by rows.  Degrees, slice lengths and the multi-region chunk
+// metadata are recomputed (O(n)).  The relabelling is no longer exactly
+// sorted, which only affects scheduling: a slice's length is the maximum of
+// its segments, and a vertex whose in-degree grew past the flat limit while
+// in a single slice is summed by its lane in 256-element chunks (sweep.cu
+// folds), bit-identical to the reference's chunked path.  nullptr = build
+// from scratch instead (T above 256, team layouts, many derivations).
+Layout* build_incremental(dynpr_context* ctx, const dynpr_graph* gT, const dynpr_graph* gF, uint32_t T,
+                          const LayoutSeed& seed) {
+  const Layout* P = seed.parent.get();
+  constexpr int kMaxGenerations = 32;  // then rebuild (sorted order, tight slices)
+  if (!P || P->ctx != ctx || P->owned || is_team(ctx) || P->T != T || T > 256u || P->n != gT->n ||
+      P->generation >= kMaxGenerations || !gT->n)
+    return nullptr;
+  cudaStream_t st = ctx->stream;
+  const uint32_t n = gT->n, M = P->M;
+  auto* L = new Layout();
+  L->ctx = ctx;
+  try {
+    L->n = n;
+    L->m = gT->m;
+    L->T = T;
+    L->gF_id = gF->id;
+    L->M = M;
+    L->generation = P->generation + 1;
+    L->n_hslices = P->n_hslices;  // scheduling hint only
+    L->perm = dalloc<uint32_t>(ctx, n);
+    L->inv = dalloc<uint32_t>(ctx, n);
+    L->indeg = dalloc<uint32_t>(ctx, n);
+    L->outdeg = dalloc<uint32_t>(ctx, n);
+    DYNPR_CK(cudaMemcpyAsync(L->perm, P->perm, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
+    DYNPR_CK(cudaMemcpyAsync(L->inv, P->inv, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
+    DYNPR_CK(cudaMemcpyAsync(L->indeg, P->indeg, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
+    DYNPR_CK(cudaMemcpyAsync(L->outdeg, P->outdeg, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
+    // touched rows in the relabelled space, in-lists (T) and out-lists (F),
+    // and their new degrees
+    auto* flagT = reinterpret_cast<uint8_t*>(ctx->layout_tmp.as<uint32_t>(((uint64_t)n + 4) / 2 + 2));
+    uint8_t* flagF = flagT + n + 4;
+    DYNPR_CK(cudaMemsetAsync(flagT, 0, 2 * ((size_t)n + 4), st));
+    if (seed.n_T)
+      k_mark_rows<<<grid(ctx, seed.n_T), 256, 0, st>>>(seed.rows_T, seed.n_T, L->inv, gT->off, flagT, L->indeg);
+    if (seed.n_F)
+      k_mark_rows<<<grid(ctx, seed.n_F), 256, 0, st>>>(seed.rows_F, seed.n_F, L->inv, gF->off, flagF, L->outdeg);
+    check_launch();
+    count_launch(ctx, 2);
+    L->mcount = dalloc<uint32_t>(ctx, (uint64_t)M + 1);
+    DYNPR_CK(cudaMemsetAsync(L->mcount, 0, ((size_t)M + 1) * 4, st));
+    L->blocks = P->blocks;  // shared slices (copy-on-write)
+    L->sell_s = P->sell_s;
+    L->sell_m = P->sell_m;
+    // single region: re-built slices into a new block
+    const uint64_t S = P->n_sslices;
+    L->n_sslices = S;
+    L->sbase = dalloc<uint64_t>(ctx, S + 1);
+    auto* len32 = reinterpret_cast<uint64_t*>(ctx->scratch64b.as<unsigned long long>(2 * (S + 1)));
+    uint64_t* dpos = len32 + S + 1;
+    k_slice_touched_len<<<grid(ctx, (S + 1) * 32), 256, 0, st>>>(L->indeg, flagT, M, n, S, len32);
+    check_launch();
+    cub_call(ctx, [&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, len32, dpos, (int64_t)S + 1, st); });
+    const uint64_t s_new = read_u64(ctx, dpos + S);
+    uint32_t* ds = new_block(ctx, L, s_new);
+    k_sbase_cow<<<grid(ctx, S + 1), 256, 0, st>>>(P->sbase, len32, dpos, S, rel_words(L->sell_s, ds), L->sbase);
+    check_launch();
+    if (s_new) {
+      k_fill_single_cow<<<grid(ctx, S * 32), 256, 0, st>>>(gT->off, gT->tgt, L->perm, L->inv, L->indeg, M, n, S,
+                                                           len32, L->sbase, L->sell_s, flagT, P->sbase);
+      check_launch();
+    }
+    count_launch(ctx, 3);
+    // multi region: touched vertices' chunks retired and appended
+    uint32_t* apos = ctx->scratch32a.as<uint32_t>((uint64_t)M + 2);
+    k_multi_touched_nch<<<grid(ctx, (uint64_t)M + 1), 256, 0, st>>>(L->indeg, flagT, M, apos);
+    check_launch();
+    cub_call(ctx, [&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, apos, apos, (int64_t)M + 1, st); });
+    uint64_t appended = 0, retired = 0;
+    {
+      uint32_t h = 0;
+      DYNPR_CK(cudaMemcpyAsync(ctx->pinned, apos + M, 4, cudaMemcpyDeviceToHost, st));
+      sync(ctx);
+      std::memcpy(&h, ctx->pinned, 4);
+      appended = h;
+    }
+    const uint64_t first = P->n_mslices * 32;  // appended segments start a slice
+    L->n_mseg = first + appended;
+    L->n_mslices = (L->n_mseg + 31) / 32;
+    L->pbase = dalloc<uint32_t>(ctx, (uint64_t)M + 1);
+    L->mseg_v = dalloc<uint32_t>(ctx, L->n_mseg);
+    L->mseg_len = dalloc<uint32_t>(ctx, L->n_mseg);
+    L->mbase = dalloc<uint64_t>(ctx, L->n_mslices + 1);
+    DYNPR_CK(cudaMemcpyAsync(L->pbase, P->pbase, ((size_t)M + 1) * 4, cudaMemcpyDeviceToDevice, st));
+    DYNPR_CK(cudaMemsetAsync(L->mseg_v, 0, L->n_mseg * 4, st));
+    DYNPR_CK(cudaMemsetAsync(L->mseg_len, 0, L->n_mseg * 4, st));
+    if (P->n_mseg) {
+      DYNPR_CK(cudaMemcpyAsync(L->mseg_v, P->mseg_v, P->n_mseg * 4, cudaMemcpyDeviceToDevice, st));
+      DYNPR_CK(cudaMemcpyAsync(L->mseg_len, P->mseg_len, P->n_mseg * 4, cudaMemcpyDeviceToDevice, st));
+    }
+    DYNPR_CK(cudaMemcpyAsync(L->mbase, P->mbase, (P->n_mslices + 1) * 8, cudaMemcpyDeviceToDevice, st));
+    if (M) {
+      k_multi_cow_segments<<<grid(ctx, M), 256, 0, st>>>(L->indeg, P->indeg, flagT, M, apos, first, P->pbase,
+                                                         L->pbase, L->mseg_v, L->mseg_len);
+      check_launch();
+    }
+    DYNPR_CK(cudaMemcpyAsync(L->pbase + M, &L->n_mseg, 4, cudaMemcpyHostToDevice, st));  // (pageable: synchronous)
+    const uint64_t s_lo = P->n_mslices, s_hi = L->n_mslices;
+    if (s_hi > s_lo) {
+      // the appended slices' lengths -> bases within a new block
+      k_multi_slice_len<<<grid(ctx, (s_hi - s_lo + 1) * 32), 256, 0, st>>>(L->mseg_len + first, appended,
+                                                                           s_hi - s_lo, L->mbase + s_lo);
+      check_launch();
+      cub_call(ctx, [&](void* t, size_t& b) {
+        return cub::DeviceScan::ExclusiveSum(t, b, L->mbase + s_lo, L->mbase + s_lo, (int64_t)(s_hi - s_lo) + 1, st);
+      });
+      const uint64_t m_new = read_u64(ctx, L->mbase + s_hi);
+      uint32_t* dm = new_block(ctx, L, m_new);
+      k_mbase_append<<<grid(ctx, s_hi - s_lo + 1), 256, 0, st>>>(L->mbase, s_lo, s_hi - s_lo, rel_words(L->sell_m, dm));
+      check_launch();
+      k_fill_multi<<<grid(ctx, (s_hi - s_lo) * 32), 256, 0, st>>>(gT->off, gT->tgt, L->perm, L->inv, L->pbase,
+                                                                  L->mseg_v, L->mseg_len, L->n_mseg, s_lo, s_hi,
+                                                                  L->mbase, L->sell_m);
+      check_launch();
+      count_launch(ctx, 4);
+      L->sell_words = P->sell_words + s_new + m_new;
+    } else {
+      L->sell_words = P->sell_words + s_new;
+    }
+    {  // retired segments (old chunks of touched vertices + the slice padding)
+      auto* cnt = reinterpret_cast<unsigned*>(ctx->scratch64a.as<unsigned long long>(2));
+      DYNPR_CK(cudaMemsetAsync(cnt, 0, 8, st));
+      k_count_above<<<grid(ctx, L->n_mseg), 256, 0, st>>>(L->mseg_len, (uint32_t)L->n_mseg, 0u, cnt);
+      check_launch();
+      count_launch(ctx, 2);
+      retired = L->n_mseg - (read_u64(ctx, cnt) & 0xffffffffu);
+      L->dead_segs = retired;
+    }
+    if (L->dead_segs > L->n_mseg / 4 + 64) {  // too fragmented: rebuild from scratch
+      destroy_layout(L);
+      return nullptr;
+    }
+    if (P->has_forward) {
+      L->offF = dalloc<uint64_t>(ctx, (uint64_t)n + 1);
+      L->tgtF = dalloc<uint32_t>(ctx, L->m);
+      k_outdeg64<<<grid(ctx, (uint64_t)n + 1), 256, 0, st>>>(L->outdeg, n, L->offF);
+      check_launch();
+      cub_call(ctx, [&](void* t, size_t& b) {
+        return cub::DeviceScan::ExclusiveSum(t, b, L->offF, L->offF, (int64_t)n + 1, st);
+      });
+      auto* cnt = reinterpret_cast<unsigned long long*>(ctx->scratch64a.as<unsigned long long>(4)) + 3;
+      const uint32_t* rows = copy_untouched_rows(ctx, flagF, n, P->offF, P->tgtF, L->offF, L->tgtF, cnt);
+      uint32_t* items = ctx->scratch32a.as<uint32_t>(seed.n_F + 2);
+      k_row_items<<<grid(ctx, seed.n_F + 1), 256, 0, st>>>(rows, cnt, L->outdeg, items);
+      check_launch();
+      cub_call(ctx, [&](void* t, size_t& b) {
+        return cub::DeviceScan::ExclusiveSum(t, b, items, items, (int64_t)seed.n_F + 1, st);
+      });
+      k_refill_rows<<<(unsigned)ctx->num_sms * 16, 256, 0, st>>>(rows, cnt, items, gF->off, gF->tgt, L->perm, L->inv,
+                                                                 L->offF, L->tgtF);
+      check_launch();
+      count_launch(ctx, 3);
+      L->has_forward = true;
+    }
+  } catch (...) {
+    destroy_layout(L);
+    throw;
+  }
+  return L;
+}
 }  // namespace
 
 Layout::~Layout() {
-  for (void* p : {(void*)perm, (void*)inv, (void*)indeg, (void*)outdeg, (void*)sbase, (void*)sell_s_alloc,
-                  (void*)mbase, (void*)mseg_v, (void*)mseg_len, (void*)pbase, (void*)sell_m_alloc, (void*)mcount,
-                  (void*)offF, (void*)tgtF})
+  for (void* p : {(void*)perm, (void*)inv, (void*)indeg, (void*)outdeg, (void*)sbase, (void*)mbase,
+                  (void*)mseg_v, (void*)mseg_len, (void*)pbase, (void*)mcount, (void*)offF, (void*)tgtF})
     pool_free(ctx, p);
 }
 
 void destroy_layout(Layout* L) { delete L; }
+
+std::shared_ptr<Layout> share_layout(Layout* L) { return std::shared_ptr<Layout>(L, destroy_layout); }
+
+LayoutSeed::~LayoutSeed() {
+  pool_free(ctx, rows_T);
+  pool_free(ctx, rows_F);
+}
 
 Layout* get_layout(dynpr_context* ctx, const dynpr_graph* gT, const dynpr_graph* gF, uint32_t T, bool need_forward) {
   // The layout is cached on gT and freed with it through its context's pool:
   // build it only with the context that owns both graphs (a layout built by
   // another context could outlive that context, or sit on another device).
   if (gT->ctx != ctx || gF->ctx != ctx) invalid("engine: the graphs belong to another context");
-  Layout* L = gT->layout;
+  auto* g = const_cast<dynpr_graph*>(gT);
+  Layout* L = g->layout.get();
   if (!L || L->gF_id != gF->id || L->T != T) {
-    if (L) {
-      destroy_layout(L);
-      const_cast<dynpr_graph*>(gT)->layout = nullptr;
-    }
+    g->layout.reset();
     DYNPR_CK(cudaEventRecord(ctx->ev_s0, ctx->stream));
-    L = build_layout(ctx, gT, gF, T);
-    const_cast<dynpr_graph*>(gT)->layout = L;
+    L = nullptr;
+    if (g->seed && g->seed->gF_id == gF->id) L = build_incremental(ctx, gT, gF, T, *g->seed);
+    if (!L) L = build_layout(ctx, gT, gF, T);
+    g->seed.reset();  // releases the parent layout
+    g->layout = share_layout(L);
     DYNPR_CK(cudaEventRecord(ctx->ev_s1, ctx->stream));
     sync(ctx);
     float ms = 0.f;

@@ -76,9 +76,15 @@ struct Layout {
   // per-rank in-CSR rows; the O(n) vertex arrays stay whole).
   bool owned = false;
   RankRange own{};
-  uint32_t* sell_s_alloc = nullptr;
-  uint32_t* sell_m_alloc = nullptr;
-  uint64_t sell_words = 0;  // SELL words held on this rank (both regions)
+  // SELL storage this layout reads.  A layout derived incrementally
+  // (layout.cu build_incremental) shares its parent's slices copy-on-write:
+  // sell_s / sell_m stay the root build's base pointers and sbase / mbase of
+  // re-built slices point into later blocks (64-bit offsets relative to the
+  // base, wrapping when a block sits below it), so the blocks of the whole
+  // chain stay alive with every layout that reads them.
+  std::vector<std::shared_ptr<uint32_t>> blocks;
+  uint64_t sell_words = 0;  // SELL words held on this rank (both regions, incl. shared)
+  uint64_t dead_segs = 0;   // multi-region segments retired by derivations (len 0)
   uint32_t* mcount = nullptr;  // per multi vertex: chunks finished this sweep (0 between sweeps)
   // relabelled forward CSR (frontier engines)
   bool has_forward = false;
@@ -90,8 +96,26 @@ struct Layout {
   std::vector<RankRange> plan;
   // content fingerprint of the graph pair (team identity check), 0 = not yet
   uint64_t fingerprint = 0;
+  // derivations since the last full build (layout.cu build_incremental)
+  int generation = 0;
   ~Layout();
 };
+
+// What an incremental layout build needs (graph.cu apply_batch_pair): the
+// parent pair's layout and the rows the batch touched, old ids, in the
+// pool of `ctx`.  rows_T: in-lists that changed (batch destinations),
+// rows_F: out-lists (batch sources).
+struct LayoutSeed {
+  dynpr_context* ctx = nullptr;
+  std::shared_ptr<Layout> parent;
+  uint64_t gF_id = 0;  // the new forward snapshot of the pair
+  uint32_t* rows_T = nullptr;
+  uint64_t n_T = 0;
+  uint32_t* rows_F = nullptr;
+  uint64_t n_F = 0;
+  ~LayoutSeed();
+};
+std::shared_ptr<Layout> share_layout(Layout* L);
 
 // Returns the cached layout of (gT, gF, T), building it if needed.  When
 // `need_forward` the relabelled forward CSR is built too.  On a team context

@@ -202,16 +202,29 @@ __device__ __forceinline__ double ld_contrib(const double* __restrict__ contrib,
   return u == self ? cself : __ldg(contrib + u);
 }
 
+// A single-region segment longer than the flat limit max(T, 256) belongs to
+// a chunked vertex (rank.cpp:59-75) that an incrementally derived layout left
+// in its single slice (layout.cu): its lane folds the running partial into
+// the total at every 256-element boundary -- c = ((0 + p0) + p1) + ..., the
+// reference's chunk order exactly.  Never true in a freshly built layout.
+__device__ __forceinline__ bool folds(const SweepArgs& a, uint32_t len) {
+#ifdef DYNPR_NO_FOLD  // A/B builds only (profiles/ab_static_layouts.py)
+  return false;
+#endif
+  return len > (a.T > kAccumChunk ? a.T : kAccumChunk);
+}
+
 // Lane-sequential sum of one SELL-32x4 segment (layout.cuh sell_pos):
 // elements 4j..4j+3 of this lane arrive with one 16-byte load.  Index loads
 // for the next 8 elements are issued before the adds of the current 8
-// (software pipelining); the adds stay in segment order.
+// (software pipelining); the adds stay in segment order.  `fold`: chunked
+// accumulation (see folds()).
 __device__ __forceinline__ double segment_sum(const uint32_t* __restrict__ sell, uint64_t base, unsigned lane,
                                               uint32_t len, uint32_t Lw, const double* __restrict__ contrib,
-                                              uint32_t self, double cself) {
+                                              uint32_t self, double cself, bool fold = false) {
   const uint32_t* p = sell + base + 4u * lane;  // element k at p + 32*k (k % 4 == 0)
   const uint4 z = make_uint4(0, 0, 0, 0);
-  double c = 0.0;
+  double c = 0.0, tot = 0.0;
   uint4 a = len > 0 ? ld_idx4(p) : z;
   uint4 b = len > 4 ? ld_idx4(p + 128) : z;
   for (uint32_t k = 0; k < Lw; k += 8) {
@@ -222,11 +235,15 @@ __device__ __forceinline__ double segment_sum(const uint32_t* __restrict__ sell,
       x[q] = (k + q < len) ? ld_contrib(contrib, u[q], self, cself) : 0.0;
     a = (k + 8 < len) ? ld_idx4(p + 32ull * (k + 8)) : z;
     b = (k + 12 < len) ? ld_idx4(p + 32ull * (k + 12)) : z;
+    if (fold && k != 0 && (k & (kAccumChunk - 1)) == 0 && k < len) {
+      tot = __dadd_rn(tot, c);
+      c = 0.0;
+    }
 #pragma unroll
     for (uint32_t q = 0; q < 8; ++q)
       if (k + q < len) c = __dadd_rn(c, x[q]);
   }
-  return c;
+  return fold ? __dadd_rn(tot, c) : c;
 }
 
 // Does any element of this lane's SELL segment hit a pending vertex?
@@ -294,7 +311,7 @@ __device__ __forceinline__ void b_sweep_single(const SweepArgs& a) {
       cself = a.contrib_prev[v];
     }
     double c = 0.0;
-    if (Lw) c = segment_sum(a.sell_s, a.sbase[s], lane, len, Lw, a.contrib_prev, v, cself);
+    if (Lw) c = segment_sum(a.sell_s, a.sbase[s], lane, len, Lw, a.contrib_prev, v, cself, folds(a, len));
     bool pend = false, lowout = false;
     if (valid) {
       if (!aff) {
@@ -509,11 +526,12 @@ __device__ __forceinline__ unsigned smid() {
 template <int Q>
 __device__ __forceinline__ double segment_sum_deep(const uint32_t* __restrict__ sell, uint64_t base, unsigned lane,
                                                    uint32_t len, uint32_t Lw, const double* __restrict__ contrib,
-                                                   uint32_t self, double cself) {
+                                                   uint32_t self, double cself, bool fold = false) {
   constexpr uint32_t D = 4 * Q;  // elements in flight per lane
+  static_assert(kAccumChunk % D == 0, "a chunk boundary starts a group");
   const uint32_t* p = sell + base + 4u * lane;
   const uint4 z = make_uint4(0, 0, 0, 0);
-  double c = 0.0;
+  double c = 0.0, tot = 0.0;
   uint4 ix[Q];
 #pragma unroll
   for (int j = 0; j < Q; ++j) ix[j] = (4u * j < len) ? ld_idx4(p + 128ull * j) : z;
@@ -528,11 +546,15 @@ __device__ __forceinline__ double segment_sum_deep(const uint32_t* __restrict__ 
     }
 #pragma unroll
     for (int j = 0; j < Q; ++j) ix[j] = (k + D + 4 * j < len) ? ld_idx4(p + 32ull * (k + D + 4 * j)) : z;
+    if (fold && k != 0 && (k & (kAccumChunk - 1)) == 0 && k < len) {
+      tot = __dadd_rn(tot, c);
+      c = 0.0;
+    }
 #pragma unroll
     for (uint32_t q = 0; q < D; ++q)
       if (k + q < len) c = __dadd_rn(c, x[q]);
   }
-  return c;
+  return fold ? __dadd_rn(tot, c) : c;
 }
 
 // One single-region slice (the body of k_sweep_single).
@@ -554,7 +576,7 @@ __device__ __forceinline__ void single_slice(const SweepArgs& a, uint64_t s, uns
     cself = a.contrib_prev[v];
   }
   double c = 0.0;
-  if (Lw) c = segment_sum_deep<Q>(a.sell_s, a.sbase[s], lane, len, Lw, a.contrib_prev, v, cself);
+  if (Lw) c = segment_sum_deep<Q>(a.sell_s, a.sbase[s], lane, len, Lw, a.contrib_prev, v, cself, folds(a, len));
   bool pend = false, lowout = false;
   if (valid) {
     if (!aff) {
@@ -603,7 +625,9 @@ __device__ __forceinline__ void multi_slice(const SweepArgs& a, uint64_t s, unsi
     const int L = __ffs(lm) - 1;
     lm &= lm - 1;
     const uint32_t w = __shfl_sync(kFull, v, L);
-    const uint32_t pb = a.pbase[w], nch = a.pbase[w + 1] - pb;
+    // (chunk count from the in-degree: a derived layout's chunks of w need
+    // not be followed by w + 1's, layout.cu build_incremental)
+    const uint32_t pb = a.pbase[w], nch = (a.indeg[w] + kAccumChunk - 1) / kAccumChunk;
     double sum = 0.0;
     for (uint32_t g = 0; g < nch; g += 32) {
       const double x = (g + lane < nch) ? __ldcg(a.partials + pb + g + lane) : 0.0;
