@@ -492,6 +492,11 @@ dynpr_status dynpr_report_destroy(dynpr_report* r);
  * {smid, start ns, end ns, heavy items | light items << 32, first heavy item,
  * end of heavy phase ns} of the latest sweep; copies up to `cap` words. */
 dynpr_status dynpr_debug_sweep_trace(uint64_t* out, uint64_t cap, uint64_t* count);
+/* Per-iteration trace of the last device-loop solve: 4 words per iteration
+ * {globaltimer ns at the end of the sweep, gathered edges, processed
+ * vertices, pending out-edges | expansion direction << 62 (1 push, 2 pull)}.
+ * Diagnostics only (profiles/dfp_iter_probe.py). */
+dynpr_status dynpr_debug_loop_trace(uint64_t* out, uint64_t cap, uint64_t* count);
 
 #ifdef __cplusplus
 }

@@ -15,9 +15,22 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "dynpr_cuda.h"
 
 namespace dynpr_b200 {
+
+// NVTX range for the span of a scope (tracing): every C-ABI entry
+// point and the solve / ingest / layout phases inside it, so an nsys or ncu
+// NVTX view attributes kernels to the API call that launched them.
+// (nvtx3 is header-only: without an attached tool a range costs a branch.)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // ---- error model -----------------------------------------------------------
 // Internal code throws; every extern "C" entry point converts to a status and

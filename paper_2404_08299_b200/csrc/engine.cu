@@ -224,7 +224,7 @@ LoopGraph& loop_graph(dynpr_context* ctx, const SweepPlan& plan, int frontier, L
       launch_loop_end(ctx, dc, red, cond, k == 1);
       if (frontier) {
         launch_expand_ind(ctx, k, &dc->pend_low, &dc->expand);
-        launch_pull_ind(ctx, plan, k);
+        if (!plan.pull_fused) launch_pull_ind(ctx, plan, k);  // (else: inside the next sweep)
       }
     }
   } catch (...) {
@@ -293,7 +293,18 @@ void run_device_loop(dynpr_context* ctx, const SolveSpec& sp, const SweepArgs& a
     half[k].tgtF = L->tgtF;
     half[k].tick_sm = sweep_tick(ctx);
   }
+  // In-sweep pull (SweepArgs::pull_fused) with the split kernels: a pull-mode
+  // expansion is folded into the next sweep's gathers, pending flags ride in
+  // the contributions' sign bits (no pull pass, no pending byte array).
+  // DYNPR_PULL_FUSED=0 keeps the separate pull kernels (A/B).
+  const char* pf = std::getenv("DYNPR_PULL_FUSED");
+  const bool want_pf = h.frontier && !(pf && pf[0] == '0');
+  for (int k = 0; k < 2; ++k) half[k].pull_fused = want_pf ? 1 : 0;
   const SweepPlan plan = plan_sweep(ctx, half[0], sp.flagged, sp.closed);
+  for (int k = 0; k < 2; ++k) {
+    half[k].pull_fused = plan.pull_fused;
+    if (plan.pull_fused) half[k].np = nullptr;
+  }
   LoopGraph& lg = loop_graph(ctx, plan, h.frontier, dc, red);
 
   // per-solve state: loop control + both halves' arguments, one upload
@@ -331,7 +342,10 @@ void solve_impl(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynp
   DYNPR_CK(cudaEventRecord(ctx->ev_a, st));
   // a team expands by pull over its own in-lists: only the traversal engine
   // (markReachable) reads the relabelled forward CSR there
-  const Layout* L = get_layout(ctx, gT, gF, c.low_degree_threshold, is_team(ctx) ? sp.traversal : sp.flagged);
+  const Layout* L = [&] {
+    NvtxRange r("dynpr layout");
+    return get_layout(ctx, gT, gF, c.low_degree_threshold, is_team(ctx) ? sp.traversal : sp.flagged);
+  }();
   // workspace (allocation is excluded from the timed region)
   double* R[2] = {ctx->rank[0].as<double>(n), ctx->rank[1].as<double>(n)};
   // Multi-GPU with attached peer buffers: contributions live in the
@@ -479,6 +493,7 @@ void solve_impl(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynp
   dynpr_stats res{};
   int cur = 0;  // R[cur] holds the latest iterate ("previous")
   if (device_loop) {
+    NvtxRange r("dynpr device loop");
     run_device_loop(ctx, sp, a, R, CB, L, red, res);
     cur = res.iterations & 1;
   }
@@ -895,6 +910,7 @@ dynpr_status dynpr_context_sweep_times(dynpr_context* ctx, double* total_ms, uin
 // ---- primitives ---------------------------------------------------------------
 dynpr_status dynpr_partition_by_degree(dynpr_context* ctx, const dynpr_graph* g, uint32_t threshold,
                                        uint32_t* order, uint32_t* low_count) {
+  NvtxRange nvtx__("dynpr_partition_by_degree");
   return api_guard([&] {
     if (!ctx || !g || !low_count) invalid("null argument");
     bind_device(ctx);
@@ -907,6 +923,7 @@ dynpr_status dynpr_partition_by_degree(dynpr_context* ctx, const dynpr_graph* g,
 
 dynpr_status dynpr_graph_prepare(dynpr_context* ctx, const dynpr_graph* gT, const dynpr_graph* gF,
                                  uint32_t threshold, int with_forward, double* build_ms) {
+  NvtxRange nvtx__("dynpr_graph_prepare");
   return api_guard([&] {
     if (!ctx) invalid("null context");
     check_pair(gT, gF);
@@ -941,6 +958,7 @@ dynpr_status dynpr_graph_layout_info(const dynpr_graph* gT, uint64_t* sell_words
 dynpr_status dynpr_update_ranks(dynpr_context* ctx, const dynpr_graph* gT, const dynpr_graph* gF,
                                 uint8_t* vertex_affected, uint8_t* neighbors_pending, const double* previous,
                                 double* current, const dynpr_config* cfg, int mode) {
+  NvtxRange nvtx__("dynpr_update_ranks");
   return api_guard([&] {
     if (!ctx || !gT || !gF || !cfg) invalid("null argument");
     if ((vertex_affected == nullptr) != (neighbors_pending == nullptr))
@@ -1060,6 +1078,7 @@ dynpr_status dynpr_initial_affected(dynpr_context* ctx, const dynpr_graph* g, co
 
 dynpr_status dynpr_expand_affected(dynpr_context* ctx, const dynpr_graph* g, uint8_t* vertex_affected,
                                    const uint8_t* neighbors_pending, uint32_t threshold) {
+  NvtxRange nvtx__("dynpr_expand_affected");
   return api_guard([&] {
     if (!ctx || !g) invalid("null argument");
     bind_device(ctx);
@@ -1084,6 +1103,7 @@ dynpr_status dynpr_expand_affected(dynpr_context* ctx, const dynpr_graph* g, uin
 dynpr_status dynpr_static_pagerank(dynpr_context* ctx, const dynpr_graph* gT, const dynpr_graph* gF,
                                    const dynpr_config* cfg, double* ranks_out, dynpr_stats* stats,
                                    dynpr_observer observer, void* observer_user) {
+  NvtxRange nvtx__("dynpr_static_pagerank");
   return api_guard([&] {
     if (!ctx) invalid("null context");
     validate_config(cfg);
@@ -1108,6 +1128,7 @@ dynpr_status dynpr_static_pagerank_csr(dynpr_context* ctx, uint32_t n, const uin
                                        const uint64_t* offF, const uint32_t* tgtF, uint64_t m,
                                        const dynpr_config* cfg, double* ranks_out, dynpr_stats* stats,
                                        dynpr_observer observer, void* observer_user) {
+  NvtxRange nvtx__("dynpr_static_pagerank_csr");
   dynpr_graph* gT = nullptr;
   const dynpr_status st = dynpr_graph_from_csr(ctx, n, offT, tgtT, m, &gT);
   if (st != DYNPR_OK) return st;
@@ -1145,6 +1166,7 @@ dynpr_status dynpr_naive_dynamic(dynpr_context* ctx, const dynpr_graph* gT, cons
                                  const double* previous, uint64_t n_previous, const dynpr_config* cfg,
                                  double* ranks_out, dynpr_stats* stats, dynpr_observer observer,
                                  void* observer_user) {
+  NvtxRange nvtx__("dynpr_naive_dynamic");
   return api_guard([&] {
     if (!ctx) invalid("null context");
     validate_config(cfg);
@@ -1167,6 +1189,7 @@ dynpr_status dynpr_dynamic_frontier(dynpr_context* ctx, const dynpr_graph* gF, c
                                     const double* previous, uint64_t n_previous, const dynpr_config* cfg,
                                     int pruning, double* ranks_out, dynpr_stats* stats, dynpr_observer observer,
                                     void* observer_user) {
+  NvtxRange nvtx__("dynpr_dynamic_frontier");
   return api_guard([&] {
     if (!ctx) invalid("null context");
     // checkFrontierInputs (engine.cpp:155-162)
@@ -1203,6 +1226,7 @@ dynpr_status dynpr_dynamic_traversal(dynpr_context* ctx, const dynpr_graph* gF, 
                                      const double* previous, uint64_t n_previous, const dynpr_config* cfg,
                                      double* ranks_out, dynpr_stats* stats, dynpr_observer observer,
                                      void* observer_user) {
+  NvtxRange nvtx__("dynpr_dynamic_traversal");
   return api_guard([&] {
     if (!ctx) invalid("null context");
     validate_config(cfg);
@@ -1239,6 +1263,7 @@ dynpr_status dynpr_dynamic_traversal(dynpr_context* ctx, const dynpr_graph* gF, 
 
 dynpr_status dynpr_mark_reachable(dynpr_context* ctx, const dynpr_graph* g, const uint32_t* seeds, uint64_t n_seeds,
                                   uint8_t* vertex_affected) {
+  NvtxRange nvtx__("dynpr_mark_reachable");
   return api_guard([&] {
     if (!ctx || !g) invalid("null argument");
     bind_device(ctx);
@@ -1258,6 +1283,7 @@ dynpr_status dynpr_dynamic_frontier_from_flags(dynpr_context* ctx, const dynpr_g
                                                uint64_t n_flags, const double* previous, uint64_t n_previous,
                                                const dynpr_config* cfg, int pruning, double* ranks_out,
                                                dynpr_stats* stats, dynpr_observer observer, void* observer_user) {
+  NvtxRange nvtx__("dynpr_dynamic_frontier_from_flags");
   return api_guard([&] {
     if (!ctx) invalid("null context");
     validate_config(cfg);

@@ -917,6 +917,7 @@ dynpr_status dynpr_graph_from_csr(dynpr_context* ctx, uint32_t n,
                                   const uint64_t* offsets,
                                   const uint32_t* targets, uint64_t m,
                                   dynpr_graph** out) {
+  NvtxRange nvtx__("dynpr_graph_from_csr");
   return api_guard([&] {
     if (!ctx || !out) invalid("null argument");
     bind_device(ctx);
@@ -968,6 +969,7 @@ dynpr_status dynpr_graph_add_self_loops(dynpr_context* ctx, const dynpr_graph* g
 }
 
 dynpr_status dynpr_graph_transpose(dynpr_context* ctx, const dynpr_graph* g, dynpr_graph** out) {
+  NvtxRange nvtx__("dynpr_graph_transpose");
   return api_guard([&] {
     if (!ctx || !g || !out) invalid("null argument");
     bind_device(ctx);
@@ -1061,6 +1063,7 @@ dynpr_status dynpr_graph_apply_batch(dynpr_context* ctx, const dynpr_graph* g, c
                                      const uint32_t* del_dst, uint64_t n_del, const uint32_t* ins_src,
                                      const uint32_t* ins_dst, uint64_t n_ins, dynpr_graph** out,
                                      uint64_t* missing, uint64_t* duplicate) {
+  NvtxRange nvtx__("dynpr_graph_apply_batch");
   return apply_batch_common(ctx, g, nullptr, del_src, del_dst, n_del, ins_src, ins_dst, n_ins, out,
                             nullptr, missing, duplicate);
 }
@@ -1071,6 +1074,7 @@ dynpr_status dynpr_graph_apply_batch_pair(dynpr_context* ctx, const dynpr_graph*
                                           const uint32_t* ins_src, const uint32_t* ins_dst,
                                           uint64_t n_ins, dynpr_graph** out_gF, dynpr_graph** out_gT,
                                           uint64_t* missing, uint64_t* duplicate) {
+  NvtxRange nvtx__("dynpr_graph_apply_batch_pair");
   if (!gT || !out_gT) {
     set_last_error("null argument");
     return DYNPR_INVALID_ARGUMENT;
@@ -1129,6 +1133,7 @@ dynpr_status dynpr_graph_destroy(dynpr_graph* g) {
 
 dynpr_status dynpr_graph_rmat(dynpr_context* ctx, uint32_t scale, uint32_t edge_factor, double a,
                               double b, double c, uint64_t seed, dynpr_graph** out) {
+  NvtxRange nvtx__("dynpr_graph_rmat");
   return api_guard([&] {
     if (!ctx || !out) invalid("null argument");
     if (scale < 1 || scale > 31) invalid("rmat: scale must be in [1,31]");

@@ -1056,6 +1056,7 @@ dynpr_status dynpr_edge_list_destroy(dynpr_edge_list* e) {
 
 dynpr_status dynpr_compute_reference_ranks(dynpr_context* ctx, const dynpr_graph* gT, const dynpr_graph* gF,
                                            const dynpr_config* cfg, double* ranks_out) {
+  NvtxRange nvtx__("dynpr_compute_reference_ranks");
   return api_guard([&] {
     if (!cfg) invalid("null config");
     dynpr_config c = *cfg;  // harness.cpp:340-349
@@ -1080,6 +1081,7 @@ void dynpr_experiment_spec_default(dynpr_experiment_spec* s) {
 
 // harness.cpp:351-381 runExperiment
 dynpr_status dynpr_run_experiment(dynpr_context* ctx, const dynpr_experiment_spec* spec, dynpr_report** out) {
+  NvtxRange nvtx__("dynpr_run_experiment");
   return api_guard([&] {
     if (!ctx || !spec || !out) invalid("null argument");
     ck(dynpr_config_validate(&spec->config));

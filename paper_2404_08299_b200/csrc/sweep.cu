@@ -63,9 +63,13 @@ struct Acc {
 };
 
 // ---- block reductions ----------------------------------------------------
+// (kWarps-sized arrays: with the L1-preferring carveout the SM keeps an 8 KB
+// shared-memory configuration, and 1 KB of static shared memory per block
+// (+1 KB reserved by the driver) capped the 48-register single-slice kernel
+// at 4 blocks per SM -- 32 warps -- instead of its register limit of 5.)
 __device__ __forceinline__ void block_reduce_commit(Acc acc, SweepRed* red) {
-  __shared__ double s_d[32];
-  __shared__ unsigned long long s_p[32], s_e[32], s_q[32];
+  __shared__ double s_d[kWarps];
+  __shared__ unsigned long long s_p[kWarps], s_e[kWarps], s_q[kWarps];
   acc.dmax = warp_max(acc.dmax);
   acc.proc = warp_sum(acc.proc);
   acc.edges = warp_sum(acc.edges);
@@ -82,7 +86,7 @@ __device__ __forceinline__ void block_reduce_commit(Acc acc, SweepRed* red) {
   if (threadIdx.x == 0) {
     double d = 0.0;
     unsigned long long p = 0, e = 0, q = 0;
-    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+    for (int i = 0; i < kWarps; ++i) {  // every caller runs kThreads-thread blocks
       d = fmax(d, s_d[i]);
       p += s_p[i];
       e += s_e[i];
@@ -138,19 +142,20 @@ __device__ __forceinline__ void copy_through(const SweepArgs& a, uint32_t v) {
   if (a.copy_all) {
     a.rank_cur[v] = a.rank_prev[v];
     if (a.contrib_cur) a.contrib_cur[v] = a.contrib_prev[v];
-  } else if (a.written[v]) {
+  } else if (const uint8_t w = a.written[v]) {
     a.rank_cur[v] = a.rank_prev[v];
-    store_contrib(a, v, a.contrib_prev[v]);
-    a.written[v] = 0;
+    store_contrib(a, v, fabs(a.contrib_prev[v]));  // (clears an in-sweep-pull pending bit)
+    a.written[v] = w - 1;
   }
   if (a.np && !a.np_accumulate) a.np[v] = 0;
 }
 
 // Fused epilogue: rank formula (rank.cpp:97-106), next contribution, delta,
 // flags (rank.cpp:108-115).
+// `newly`: the vertex became affected in this sweep's in-sweep pull.
 template <bool FLAGGED, bool CLOSED>
 __device__ __forceinline__ void finalize(const SweepArgs& a, uint32_t v, double c, double pv, uint32_t od,
-                                         Acc& acc, bool& pend, bool& lowout) {
+                                         Acc& acc, bool& pend, bool& lowout, bool newly = false) {
   const double d = (double)od;
   double r;
   if (CLOSED) {
@@ -160,13 +165,17 @@ __device__ __forceinline__ void finalize(const SweepArgs& a, uint32_t v, double 
     r = __dadd_rn(a.teleport, __dmul_rn(a.alpha, c));
   }
   a.rank_cur[v] = r;
-  if (a.contrib_cur) store_contrib(a, v, __ddiv_rn(r, d));
   const double dr = fabs(__dsub_rn(r, pv));
   if (dr > acc.dmax) acc.dmax = dr;  // NaN never wins, like blockMax (parallel.hpp:66-73)
+  bool signbit = false;
   if (FLAGGED) {
     const double denom = r > pv ? r : pv;
     const double rel = denom > 0.0 ? __ddiv_rn(dr, denom) : 0.0;
-    if (CLOSED && rel <= a.tp) a.va[v] = 0;
+    if (CLOSED && rel <= a.tp) {
+      a.va[v] = 0;
+    } else if (newly) {
+      a.va[v] = 1;
+    }
     pend = rel > a.tf;
     if (a.np) {
       if (a.np_accumulate) {
@@ -177,7 +186,12 @@ __device__ __forceinline__ void finalize(const SweepArgs& a, uint32_t v, double 
     }
     lowout = od <= a.T;
     if (pend) acc.pedges += od;
-    if (a.written) a.written[v] = 1;
+    signbit = a.pull_fused && pend;
+    if (a.written) a.written[v] = signbit ? 2 : 1;
+  }
+  if (a.contrib_cur) {
+    const double q = __ddiv_rn(r, d);
+    store_contrib(a, v, signbit ? -q : q);
   }
 }
 
@@ -219,9 +233,15 @@ __device__ __forceinline__ bool folds(const SweepArgs& a, uint32_t len) {
 // for the next 8 elements are issued before the adds of the current 8
 // (software pipelining); the adds stay in segment order.  `fold`: chunked
 // accumulation (see folds()).
+// Contributions are summed as |x| (the sign bit may carry an in-sweep-pull
+// pending flag, see SweepArgs::pull_fused); NEG also ORs the sign bits of the
+// gathered values into *neg (bit 31).
+template <bool NEG = false>
 __device__ __forceinline__ double segment_sum(const uint32_t* __restrict__ sell, uint64_t base, unsigned lane,
                                               uint32_t len, uint32_t Lw, const double* __restrict__ contrib,
-                                              uint32_t self, double cself, bool fold = false) {
+                                              uint32_t self, double cself, bool fold = false,
+                                              unsigned* neg = nullptr) {
+  unsigned nb = 0;
   const uint32_t* p = sell + base + 4u * lane;  // element k at p + 32*k (k % 4 == 0)
   const uint4 z = make_uint4(0, 0, 0, 0);
   double c = 0.0, tot = 0.0;
@@ -240,9 +260,12 @@ __device__ __forceinline__ double segment_sum(const uint32_t* __restrict__ sell,
       c = 0.0;
     }
 #pragma unroll
-    for (uint32_t q = 0; q < 8; ++q)
-      if (k + q < len) c = __dadd_rn(c, x[q]);
+    for (uint32_t q = 0; q < 8; ++q) {
+      if (k + q < len) c = __dadd_rn(c, fabs(x[q]));
+      if (NEG) nb |= (unsigned)__double2hiint(x[q]);  // (0.0 past the end)
+    }
   }
+  if (NEG) *neg = nb >> 31;
   return fold ? __dadd_rn(tot, c) : c;
 }
 
@@ -281,11 +304,18 @@ constexpr int kSweepWarps = kSweepThreads / 32;
 constexpr unsigned kSplitGrab = 4;  // k_sweep_single: slices per dynamic grab
 
 // ---- single-segment vertices: warp per 32-vertex slice ------------------------
+// In-sweep pull (SweepArgs::pull_fused): this sweep follows an expansion
+// decided as a pull.
+__device__ __forceinline__ bool pull_now(const SweepArgs& a) {
+  return a.pull_fused && a.expand && *a.expand == kExpandPull;
+}
+
 template <bool FLAGGED, bool CLOSED>
 __device__ __forceinline__ void b_sweep_single(const SweepArgs& a) {
   if (a.done && *a.done) return;
   Acc acc;
   const unsigned lane = lane_id();
+  const bool pull = FLAGGED && pull_now(a);
   // slices grabbed dynamically, kSplitGrab at a time (counter in the record)
   for (;;) {
     unsigned g = 0;
@@ -301,23 +331,31 @@ __device__ __forceinline__ void b_sweep_single(const SweepArgs& a) {
     const uint32_t deg = valid ? a.indeg[v] : 0u;
     bool aff = valid;
     if (FLAGGED) aff = valid && a.va[v];
-    const uint32_t len = aff ? deg : 0u;
+    const bool scan = pull && valid && !aff;  // in-sweep pull: any pending in-neighbour?
+    const uint32_t len = (aff || scan) ? deg : 0u;
     const uint32_t Lw = __reduce_max_sync(kFull, len);
     double pv = 0.0, cself = 0.0;
     uint32_t od = 0;
-    if (aff) {  // prefetch the epilogue operands (and the self-loop term)
+    if (aff || scan) {  // prefetch the epilogue operands (and the self-loop term)
       pv = a.rank_prev[v];
       od = a.outdeg[v];
       cself = a.contrib_prev[v];
     }
     double c = 0.0;
-    if (Lw) c = segment_sum(a.sell_s, a.sbase[s], lane, len, Lw, a.contrib_prev, v, cself, folds(a, len));
+    unsigned neg = 0;
+    if (Lw) {
+      if (pull)
+        c = segment_sum<true>(a.sell_s, a.sbase[s], lane, len, Lw, a.contrib_prev, v, cself, folds(a, len), &neg);
+      else
+        c = segment_sum(a.sell_s, a.sbase[s], lane, len, Lw, a.contrib_prev, v, cself, folds(a, len));
+    }
+    const bool newly = scan && neg;
     bool pend = false, lowout = false;
     if (valid) {
-      if (!aff) {
+      if (!aff && !newly) {
         copy_through(a, v);
       } else {
-        finalize<FLAGGED, CLOSED>(a, v, c, pv, od, acc, pend, lowout);
+        finalize<FLAGGED, CLOSED>(a, v, c, pv, od, acc, pend, lowout, newly);
         ++acc.proc;
         acc.edges += deg;
       }
@@ -342,6 +380,7 @@ template <bool FLAGGED>
 __device__ __forceinline__ void b_sweep_mseg(const SweepArgs& a) {
   if (a.done && *a.done) return;
   const unsigned lane = lane_id();
+  const bool pull = FLAGGED && pull_now(a);
   for (;;) {  // slices grabbed dynamically (counter in the record)
     unsigned g = 0;
     if (lane == 0) g = atomicAdd(&a.red->ticket_heavy, 1u);
@@ -353,14 +392,20 @@ __device__ __forceinline__ void b_sweep_mseg(const SweepArgs& a) {
       len = a.mseg_len[seg];
       v = a.mseg_v[seg];
       if (v < a.v_lo || v >= a.v_hi) len = 0;  // another rank's vertex
-      if (FLAGGED && !a.va[v]) len = 0;
+      if (FLAGGED && !pull && !a.va[v]) len = 0;
     }
     const uint32_t Lw = __reduce_max_sync(kFull, len);
     if (!Lw) continue;
     // (a multi vertex's self-loop is one gather among >256: not special-cased)
-    const double c = segment_sum(a.sell_m, a.mbase[s], lane, len, Lw, a.contrib_prev, 0xffffffffu,
-                                 0.0);
-    if (len) a.partials[seg] = c;
+    if (pull) {  // the chunk's "any pending source" rides in the partial's sign bit
+      unsigned neg = 0;
+      const double c =
+          segment_sum<true>(a.sell_m, a.mbase[s], lane, len, Lw, a.contrib_prev, 0xffffffffu, 0.0, false, &neg);
+      if (len) a.partials[seg] = neg ? -c : c;
+    } else {
+      const double c = segment_sum(a.sell_m, a.mbase[s], lane, len, Lw, a.contrib_prev, 0xffffffffu, 0.0);
+      if (len) a.partials[seg] = c;
+    }
   }
 }
 template <bool FLAGGED>
@@ -377,19 +422,24 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_mseg_c() {
 // per 32 partials, then a shuffle-broadcast sequential sum whose shuffles are
 // independent of the add chain (full groups unrolled), so the critical path
 // is n dependent DADDs instead of n dependent loads.
-__device__ __forceinline__ double warp_ordered_sum(const double* __restrict__ p, uint32_t n) {
+// Partials are summed as |x|; *neg = OR of their sign bits (in-sweep pull).
+__device__ __forceinline__ double warp_ordered_sum(const double* __restrict__ p, uint32_t n, bool* neg) {
   const unsigned lane = lane_id();
   double sum = 0.0;
+  unsigned nb = 0;
   uint32_t g = 0;
   for (; g + 32 <= n; g += 32) {
     const double x = p[g + lane];
+    nb |= (unsigned)__double2hiint(x);
 #pragma unroll
-    for (int j = 0; j < 32; ++j) sum = __dadd_rn(sum, __shfl_sync(kFull, x, j));
+    for (int j = 0; j < 32; ++j) sum = __dadd_rn(sum, fabs(__shfl_sync(kFull, x, j)));
   }
   if (g < n) {
     const double x = g + lane < n ? p[g + lane] : 0.0;
-    for (uint32_t j = 0; j < n - g; ++j) sum = __dadd_rn(sum, __shfl_sync(kFull, x, j));
+    nb |= (unsigned)__double2hiint(x);
+    for (uint32_t j = 0; j < n - g; ++j) sum = __dadd_rn(sum, fabs(__shfl_sync(kFull, x, j)));
   }
+  *neg = (__reduce_or_sync(kFull, nb) >> 31) != 0;
   return sum;
 }
 
@@ -399,6 +449,7 @@ template <bool FLAGGED, bool CLOSED>
 __device__ __forceinline__ void b_sweep_mfinal(const SweepArgs& a) {
   if (a.done && *a.done) return;
   Acc acc;
+  const bool pull = FLAGGED && pull_now(a);
   const uint64_t vend = a.M < a.v_hi ? a.M : a.v_hi;
   // the multi vertices are sorted by in-degree (descending): [0, Mb) have
   // more than kWarpCombineChunks partials
@@ -423,17 +474,24 @@ __device__ __forceinline__ void b_sweep_mfinal(const SweepArgs& a) {
       const uint32_t v = (uint32_t)vv;
       bool pend = false, lowout = false;
       uint32_t od = 0;
-      if (FLAGGED && !a.va[v]) {
+      const bool aff = !FLAGGED || a.va[v];
+      if (!aff && !pull) {
         if (lane_id() == 0) copy_through(a, v);
       } else {
         const uint32_t deg = a.indeg[v];
         const uint32_t pb = a.pbase[v];
-        const double c = warp_ordered_sum(a.partials + pb, (deg + kAccumChunk - 1) / kAccumChunk);
+        bool neg = false;
+        const double c = warp_ordered_sum(a.partials + pb, (deg + kAccumChunk - 1) / kAccumChunk, &neg);
+        const bool newly = !aff && neg;
         if (lane_id() == 0) {
-          od = a.outdeg[v];
-          finalize<FLAGGED, CLOSED>(a, v, c, a.rank_prev[v], od, acc, pend, lowout);
-          ++acc.proc;
-          acc.edges += deg;
+          if (!aff && !newly) {
+            copy_through(a, v);
+          } else {
+            od = a.outdeg[v];
+            finalize<FLAGGED, CLOSED>(a, v, c, a.rank_prev[v], od, acc, pend, lowout, newly);
+            ++acc.proc;
+            acc.edges += deg;
+          }
         }
       }
       if (FLAGGED && a.pend_low) warp_append(pend, lowout, v, od, a.pend_low, a.pend_high, a.red);
@@ -448,25 +506,34 @@ __device__ __forceinline__ void b_sweep_mfinal(const SweepArgs& a) {
     const uint32_t v = (uint32_t)vv;
     uint32_t od = 0;
     if (vv < vend) {
-      if (FLAGGED && !a.va[v]) {
+      const bool aff = !FLAGGED || a.va[v];
+      if (!aff && !pull) {
         copy_through(a, v);
       } else {
         const uint32_t deg = a.indeg[v];
         const uint32_t nch = (deg + kAccumChunk - 1) / kAccumChunk;
         const double* p = a.partials + a.pbase[v];
         double c = 0.0;
+        unsigned nb = 0;
         for (uint32_t q = 0; q < nch; q += 8) {
           double x[8];
 #pragma unroll
           for (uint32_t j = 0; j < 8; ++j) x[j] = q + j < nch ? p[q + j] : 0.0;
 #pragma unroll
-          for (uint32_t j = 0; j < 8; ++j)
-            if (q + j < nch) c = __dadd_rn(c, x[j]);
+          for (uint32_t j = 0; j < 8; ++j) {
+            if (q + j < nch) c = __dadd_rn(c, fabs(x[j]));
+            nb |= (unsigned)__double2hiint(x[j]);
+          }
         }
-        od = a.outdeg[v];
-        finalize<FLAGGED, CLOSED>(a, v, c, a.rank_prev[v], od, acc, pend, lowout);
-        ++acc.proc;
-        acc.edges += deg;
+        const bool newly = !aff && (nb >> 31);
+        if (!aff && !newly) {
+          copy_through(a, v);
+        } else {
+          od = a.outdeg[v];
+          finalize<FLAGGED, CLOSED>(a, v, c, a.rank_prev[v], od, acc, pend, lowout, newly);
+          ++acc.proc;
+          acc.edges += deg;
+        }
       }
     }
     if (FLAGGED && a.pend_low) warp_append(pend, lowout, v, od, a.pend_low, a.pend_high, a.red);
@@ -967,6 +1034,13 @@ __global__ void k_expand_high_c(const unsigned* counts, const int* gate) {
 }
 
 // ---- device-driven loop bookkeeping (engine.cpp:71-92) --------------------------------
+// Per-iteration trace of the last device-loop solve (read with
+// dynpr_debug_loop_trace): {globaltimer ns at the end of the iteration's
+// sweep, gathered edges, processed vertices, pending out-edges | expansion
+// direction << 62}.  One thread writes 32 bytes per iteration.
+constexpr int kLoopTraceIters = 1024;
+__device__ unsigned long long g_loop_trace[kLoopTraceIters * 4];
+
 __global__ void k_loop_end(LoopCtl* c, SweepRed* red, cudaGraphConditionalHandle h, int set_cond) {
   if (!c->done) {
     const SweepRed r = *red;
@@ -988,6 +1062,15 @@ __global__ void k_loop_end(LoopCtl* c, SweepRed* red, cudaGraphConditionalHandle
       c->expand = r.pend_edges > pull_bound ? kExpandPull : kExpandPush;
       c->pend_low = r.pend_low;
       c->pend_high = r.pend_high;
+    }
+    if (c->iterations <= kLoopTraceIters) {
+      unsigned long long* t = g_loop_trace + 4 * (c->iterations - 1);
+      unsigned long long now;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      t[0] = now;
+      t[1] = r.edges;
+      t[2] = r.processed;
+      t[3] = r.pend_edges | ((unsigned long long)c->expand << 62);
     }
   }
   if (set_cond) cudaGraphSetConditional(h, c->done ? 0u : 1u);
@@ -1419,6 +1502,7 @@ SweepPlan plan_sweep(dynpr_context* ctx, const SweepArgs& a, bool flagged, bool 
     if (closed) DYNPR_PLAN(false, true); else DYNPR_PLAN(false, false);
   }
 #undef DYNPR_PLAN
+  p.pull_fused = a.pull_fused && p.split;
   if (n_ms) p.g_pull_m = pgrid(ctx, k_pull_mseg_c<0>, (n_ms + kWarps - 1) / kWarps);
   if (n_ss) p.g_pull_s = pgrid(ctx, k_pull_single_c<0>, (n_ss + kWarps - 1) / kWarps);
   return p;
@@ -1671,6 +1755,15 @@ void launch_l1(dynpr_context* ctx, const double* a, const double* b, uint64_t n,
 }
 
 }  // namespace dynpr_b200
+
+extern "C" dynpr_status dynpr_debug_loop_trace(uint64_t* out, uint64_t cap, uint64_t* count) {
+  dynpr_b200::NvtxRange nvtx__("dynpr_debug_loop_trace");
+  return dynpr_b200::api_guard([&] {
+    const uint64_t n = 4ull * dynpr_b200::kLoopTraceIters;
+    if (count) *count = n;
+    if (out && cap) DYNPR_CK(cudaMemcpyFromSymbol(out, dynpr_b200::g_loop_trace, (cap < n ? cap : n) * 8));
+  });
+}
 
 extern "C" dynpr_status dynpr_debug_sweep_trace(uint64_t* out, uint64_t cap, uint64_t* count) {
   return dynpr_b200::api_guard([&] {

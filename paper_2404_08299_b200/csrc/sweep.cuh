@@ -54,6 +54,14 @@ struct SweepArgs {
   uint2* pend_high;            // (vertex, 1024-edge chunk) items, out-degree > T
   SweepRed* red;
   int np_accumulate;  // updateRanks primitive: np |= pend, untouched otherwise
+  // In-sweep pull (device loop, split sweep): each new contribution carries
+  // its vertex's pending decision in the sign bit (contributions are >= 0,
+  // every gather sums |x|), and a sweep that follows a pull-mode expansion
+  // decision gathers the in-lists of the unaffected vertices too -- a vertex
+  // with a pending in-neighbour is affected (frontier.cpp:55-84) and its sum
+  // is already in hand.  `written` then counts the copy-throughs still owed
+  // (2 after a pending write: the older buffer's sign bit must be cleared).
+  int pull_fused;
   int copy_all;       // updateRanks primitive: copy-through every unaffected
   // owned work (multi-GPU rank; the whole graph on one GPU): vertices
   // [v_lo, v_hi), single slices [ss_lo, ss_hi), multi slices [ms_lo, ms_hi)
@@ -106,7 +114,7 @@ void launch_sweep(dynpr_context* ctx, const SweepArgs& a, bool flagged, bool clo
 // Launch plan of one sweep for the cached device-loop graph: kernel choice
 // (fused / split) and every grid.  Plans compare bytewise.
 struct SweepPlan {
-  int flagged, closed, split;
+  int flagged, closed, split, pull_fused;
   unsigned g_fused, g_mseg, g_single, g_mfinal, g_pull_m, g_pull_s;
 };
 SweepPlan plan_sweep(dynpr_context* ctx, const SweepArgs& a, bool flagged, bool closed);

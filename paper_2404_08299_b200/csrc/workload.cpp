@@ -74,6 +74,7 @@ dynpr_status dynpr_generate_random_batch(dynpr_context* ctx, const dynpr_graph* 
                                          double insert_fraction, uint64_t seed, uint32_t* ins_src,
                                          uint32_t* ins_dst, uint64_t* n_ins, uint32_t* del_src, uint32_t* del_dst,
                                          uint64_t* n_del) {
+  NvtxRange nvtx__("dynpr_generate_random_batch");
   return api_guard([&] {
     if (!ctx || !g || !n_ins || !n_del) invalid("null argument");
     if (total < 1) invalid("generateRandomBatch: totalSize must be >= 1");
