@@ -293,9 +293,9 @@ void run_device_loop(dynpr_context* ctx, const SolveSpec& sp, const SweepArgs& a
     half[k].tgtF = L->tgtF;
     half[k].tick_sm = sweep_tick(ctx);
   }
-  // In-sweep pull (SweepArgs::pull_fused) with the split kernels: a pull-mode
-  // expansion is folded into the next sweep's gathers, pending flags ride in
-  // the contributions' sign bits (no pull pass, no pending byte array).
+  // In-sweep pull (SweepArgs::pull_fused): a pull-mode expansion is folded
+  // into the next sweep's gathers, pending flags ride in the contributions'
+  // sign bits (no pull pass, no pending byte array).
   // DYNPR_PULL_FUSED=0 keeps the separate pull kernels (A/B).
   const char* pf = std::getenv("DYNPR_PULL_FUSED");
   const bool want_pf = h.frontier && !(pf && pf[0] == '0');

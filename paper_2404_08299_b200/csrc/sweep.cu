@@ -590,11 +590,14 @@ __device__ __forceinline__ unsigned smid() {
   return r;
 }
 
-template <int Q>
+// (|x| sums and the optional sign-bit OR as in segment_sum)
+template <int Q, bool NEG = false>
 __device__ __forceinline__ double segment_sum_deep(const uint32_t* __restrict__ sell, uint64_t base, unsigned lane,
                                                    uint32_t len, uint32_t Lw, const double* __restrict__ contrib,
-                                                   uint32_t self, double cself, bool fold = false) {
+                                                   uint32_t self, double cself, bool fold = false,
+                                                   unsigned* neg = nullptr) {
   constexpr uint32_t D = 4 * Q;  // elements in flight per lane
+  unsigned nb = 0;
   static_assert(kAccumChunk % D == 0, "a chunk boundary starts a group");
   const uint32_t* p = sell + base + 4u * lane;
   const uint4 z = make_uint4(0, 0, 0, 0);
@@ -618,38 +621,52 @@ __device__ __forceinline__ double segment_sum_deep(const uint32_t* __restrict__ 
       c = 0.0;
     }
 #pragma unroll
-    for (uint32_t q = 0; q < D; ++q)
-      if (k + q < len) c = __dadd_rn(c, x[q]);
+    for (uint32_t q = 0; q < D; ++q) {
+      if (k + q < len) c = __dadd_rn(c, fabs(x[q]));
+      if (NEG) nb |= (unsigned)__double2hiint(x[q]);
+    }
   }
+  if (NEG) *neg = nb >> 31;
   return fold ? __dadd_rn(tot, c) : c;
 }
 
 // One single-region slice (the body of k_sweep_single).
+// `pull`: in-sweep pull (SweepArgs::pull_fused) -- unaffected lanes gather
+// too and become affected on a pending source.
 template <bool FLAGGED, bool CLOSED, int Q>
-__device__ __forceinline__ void single_slice(const SweepArgs& a, uint64_t s, unsigned lane, Acc& acc) {
+__device__ __forceinline__ void single_slice(const SweepArgs& a, uint64_t s, unsigned lane, Acc& acc, bool pull) {
   const uint64_t vv = (uint64_t)a.M + s * 32 + lane;
   const bool valid = vv < a.n;
   const uint32_t v = (uint32_t)vv;
   const uint32_t deg = valid ? a.indeg[v] : 0u;
   bool aff = valid;
   if (FLAGGED) aff = valid && a.va[v];
-  const uint32_t len = aff ? deg : 0u;
+  const bool scan = FLAGGED && pull && valid && !aff;
+  const uint32_t len = (aff || scan) ? deg : 0u;
   const uint32_t Lw = __reduce_max_sync(kFull, len);
   double pv = 0.0, cself = 0.0;
   uint32_t od = 0;
-  if (aff) {
+  if (aff || scan) {
     pv = a.rank_prev[v];
     od = a.outdeg[v];
     cself = a.contrib_prev[v];
   }
   double c = 0.0;
-  if (Lw) c = segment_sum_deep<Q>(a.sell_s, a.sbase[s], lane, len, Lw, a.contrib_prev, v, cself, folds(a, len));
+  unsigned neg = 0;
+  if (Lw) {
+    if (FLAGGED && pull)
+      c = segment_sum_deep<Q, true>(a.sell_s, a.sbase[s], lane, len, Lw, a.contrib_prev, v, cself, folds(a, len),
+                                    &neg);
+    else
+      c = segment_sum_deep<Q>(a.sell_s, a.sbase[s], lane, len, Lw, a.contrib_prev, v, cself, folds(a, len));
+  }
+  const bool newly = scan && neg;
   bool pend = false, lowout = false;
   if (valid) {
-    if (!aff) {
+    if (!aff && !newly) {
       copy_through(a, v);
     } else {
-      finalize<FLAGGED, CLOSED>(a, v, c, pv, od, acc, pend, lowout);
+      finalize<FLAGGED, CLOSED>(a, v, c, pv, od, acc, pend, lowout, newly);
       ++acc.proc;
       acc.edges += deg;
     }
@@ -660,7 +677,7 @@ __device__ __forceinline__ void single_slice(const SweepArgs& a, uint64_t s, uns
 // One multi-chunk slice: 32 chunk partials; the warp that completes a
 // vertex's last chunk combines and finalises it.
 template <bool FLAGGED, bool CLOSED, int Q>
-__device__ __forceinline__ void multi_slice(const SweepArgs& a, uint64_t s, unsigned lane, Acc& acc) {
+__device__ __forceinline__ void multi_slice(const SweepArgs& a, uint64_t s, unsigned lane, Acc& acc, bool pull) {
   const uint64_t seg = s * 32 + lane;
   uint32_t len = 0, v = 0xffffffffu;
   if (seg < a.n_mseg) {
@@ -668,14 +685,22 @@ __device__ __forceinline__ void multi_slice(const SweepArgs& a, uint64_t s, unsi
     len = a.mseg_len[seg];
     if (v < a.v_lo || v >= a.v_hi) {
       len = 0;  // another rank's vertex
-    } else if (FLAGGED && !a.va[v]) {
+    } else if (FLAGGED && !pull && !a.va[v]) {
       len = 0;
       if (seg == a.pbase[v]) copy_through(a, v);  // first chunk's lane does the copy-through
     }
   }
   const uint32_t Lw = __reduce_max_sync(kFull, len);
   if (!Lw) return;
-  const double c = segment_sum_deep<Q>(a.sell_m, a.mbase[s], lane, len, Lw, a.contrib_prev, 0xffffffffu, 0.0);
+  double c;
+  if (FLAGGED && pull) {  // the chunk's "any pending source" rides in the partial's sign bit
+    unsigned neg = 0;
+    c = segment_sum_deep<Q, true>(a.sell_m, a.mbase[s], lane, len, Lw, a.contrib_prev, 0xffffffffu, 0.0, false,
+                                  &neg);
+    if (neg) c = -c;
+  } else {
+    c = segment_sum_deep<Q>(a.sell_m, a.mbase[s], lane, len, Lw, a.contrib_prev, 0xffffffffu, 0.0);
+  }
   bool last = false;
   if (len) {
     __stcg(a.partials + seg, c);
@@ -688,6 +713,7 @@ __device__ __forceinline__ void multi_slice(const SweepArgs& a, uint64_t s, unsi
   if (!lm) return;
   __syncwarp();
   double cfin = 0.0;
+  bool negfin = false;
   while (lm) {
     const int L = __ffs(lm) - 1;
     lm &= lm - 1;
@@ -696,23 +722,33 @@ __device__ __forceinline__ void multi_slice(const SweepArgs& a, uint64_t s, unsi
     // not be followed by w + 1's, layout.cu build_incremental)
     const uint32_t pb = a.pbase[w], nch = (a.indeg[w] + kAccumChunk - 1) / kAccumChunk;
     double sum = 0.0;
+    unsigned nb = 0;
     for (uint32_t g = 0; g < nch; g += 32) {
       const double x = (g + lane < nch) ? __ldcg(a.partials + pb + g + lane) : 0.0;
+      nb |= (unsigned)__double2hiint(x);
       const uint32_t cnt = nch - g < 32 ? nch - g : 32;
-      for (uint32_t j = 0; j < cnt; ++j) sum = __dadd_rn(sum, __shfl_sync(kFull, x, j));
+      for (uint32_t j = 0; j < cnt; ++j) sum = __dadd_rn(sum, fabs(__shfl_sync(kFull, x, j)));
     }
+    nb = __reduce_or_sync(kFull, nb);
     if ((int)lane == L) {
       cfin = sum;
+      negfin = (nb >> 31) != 0;
       a.mcount[w] = 0;  // ready for the next sweep
     }
   }
   bool pend = false, lowout = false;
   uint32_t od = 0;
   if (last) {
-    od = a.outdeg[v];
-    finalize<FLAGGED, CLOSED>(a, v, cfin, a.rank_prev[v], od, acc, pend, lowout);
-    ++acc.proc;
-    acc.edges += a.indeg[v];
+    const bool aff = !FLAGGED || !pull || a.va[v];
+    const bool newly = !aff && negfin;
+    if (!aff && !newly) {
+      copy_through(a, v);
+    } else {
+      od = a.outdeg[v];
+      finalize<FLAGGED, CLOSED>(a, v, cfin, a.rank_prev[v], od, acc, pend, lowout, newly);
+      ++acc.proc;
+      acc.edges += a.indeg[v];
+    }
   }
   if (FLAGGED && a.pend_low) warp_append(pend, lowout, v, od, a.pend_low, a.pend_high, a.red);
 }
@@ -722,6 +758,7 @@ __device__ __forceinline__ void fused_body(const SweepArgs& a) {
   if (a.done && *a.done) return;
   Acc acc;
   const unsigned lane = lane_id();
+  const bool pull = FLAGGED && pull_now(a);
   const uint64_t n_ms = a.ms_hi - a.ms_lo;
   const uint64_t hs_hi = a.ss_heavy < a.ss_hi ? a.ss_heavy : a.ss_hi;
   const uint64_t n_hs = hs_hi > a.ss_lo ? hs_hi - a.ss_lo : 0;
@@ -740,9 +777,9 @@ __device__ __forceinline__ void fused_body(const SweepArgs& a) {
     ++nh;
     if (first == ~0ull) first = t;
     if (t < n_ms)
-      multi_slice<FLAGGED, CLOSED, QH>(a, a.ms_lo + t, lane, acc);
+      multi_slice<FLAGGED, CLOSED, QH>(a, a.ms_lo + t, lane, acc, pull);
     else
-      single_slice<FLAGGED, CLOSED, QH>(a, a.ss_lo + (t - n_ms), lane, acc);
+      single_slice<FLAGGED, CLOSED, QH>(a, a.ss_lo + (t - n_ms), lane, acc, pull);
   }
   if (a.trace) th = gtimer();
   const uint64_t l_lo = a.ss_lo + n_hs;
@@ -754,7 +791,7 @@ __device__ __forceinline__ void fused_body(const SweepArgs& a) {
     if (t >= n_light) break;
     const uint64_t e = t + kLightGrab < n_light ? t + kLightGrab : n_light;
     nl += e - t;
-    for (uint64_t i = t; i < e; ++i) single_slice<FLAGGED, CLOSED, 2>(a, l_lo + i, lane, acc);
+    for (uint64_t i = t; i < e; ++i) single_slice<FLAGGED, CLOSED, 2>(a, l_lo + i, lane, acc, pull);
   }
   if (a.trace && lane == 0) {
     const uint64_t w = ((uint64_t)blockIdx.x * kSweepThreads + threadIdx.x) / 32;
@@ -1502,7 +1539,7 @@ SweepPlan plan_sweep(dynpr_context* ctx, const SweepArgs& a, bool flagged, bool 
     if (closed) DYNPR_PLAN(false, true); else DYNPR_PLAN(false, false);
   }
 #undef DYNPR_PLAN
-  p.pull_fused = a.pull_fused && p.split;
+  p.pull_fused = a.pull_fused;
   if (n_ms) p.g_pull_m = pgrid(ctx, k_pull_mseg_c<0>, (n_ms + kWarps - 1) / kWarps);
   if (n_ss) p.g_pull_s = pgrid(ctx, k_pull_single_c<0>, (n_ss + kWarps - 1) / kWarps);
   return p;

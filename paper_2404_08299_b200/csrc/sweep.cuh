@@ -54,7 +54,7 @@ struct SweepArgs {
   uint2* pend_high;            // (vertex, 1024-edge chunk) items, out-degree > T
   SweepRed* red;
   int np_accumulate;  // updateRanks primitive: np |= pend, untouched otherwise
-  // In-sweep pull (device loop, split sweep): each new contribution carries
+  // In-sweep pull (device loop): each new contribution carries
   // its vertex's pending decision in the sign bit (contributions are >= 0,
   // every gather sums |x|), and a sweep that follows a pull-mode expansion
   // decision gathers the in-lists of the unaffected vertices too -- a vertex

@@ -1,6 +1,6 @@
-"""In-sweep pull (sweep.cuh SweepArgs::pull_fused): with the split sweep
-kernels the device loop folds a pull-mode expandAffected (frontier.cpp:55-84)
-into the next sweep -- pending flags ride in the contributions' sign bits,
+"""In-sweep pull (sweep.cuh SweepArgs::pull_fused): with either sweep kernel
+(split or fused latency mode) the device loop folds a pull-mode
+expandAffected (frontier.cpp:55-84) into the next sweep -- pending flags ride in the contributions' sign bits,
 unaffected vertices gather their in-lists and become affected when one
 source is pending.  Compared bit for bit with the separate pull kernels
 (DYNPR_PULL_FUSED=0), the host-driven loop and the reference library, on
@@ -32,9 +32,10 @@ def rmat16(dp, oracle_lib):
     return og, ogt, g, gt, O.static(ogt, og)
 
 
+@pytest.mark.parametrize("sweep", ["split", "fused"])
 @pytest.mark.parametrize("frac", [1e-4, 1e-3, 1e-2, 0.1])
 @pytest.mark.parametrize("pruning", [True, False])
-def test_in_sweep_pull_matches_reference(dp, oracle_lib, monkeypatch, rmat16, frac, pruning):
+def test_in_sweep_pull_matches_reference(dp, oracle_lib, monkeypatch, rmat16, frac, pruning, sweep):
     O = oracle_lib
     og, ogt, g, gt, base = rmat16
     size = O.batch_size_from_fraction(frac, og.m)
@@ -43,7 +44,7 @@ def test_in_sweep_pull_matches_reference(dp, oracle_lib, monkeypatch, rmat16, fr
     ogt2 = O.transpose(og2)
     g2, gt2 = dp.apply_batch_pair(g, gt, dp.BatchUpdate(dels, ins))
     ref = O.dynamic_frontier(og2, ogt2, dels, ins, base.ranks, pruning=pruning)
-    monkeypatch.setenv("DYNPR_SWEEP", "split")
+    monkeypatch.setenv("DYNPR_SWEEP", sweep)
     runs = {}
     for mode, env in (("fused", {"DYNPR_HOST_LOOP": "0", "DYNPR_PULL_FUSED": "1"}),
                       ("separate", {"DYNPR_HOST_LOOP": "0", "DYNPR_PULL_FUSED": "0"}),
@@ -61,8 +62,9 @@ def test_in_sweep_pull_matches_reference(dp, oracle_lib, monkeypatch, rmat16, fr
     _same(dp.static_pagerank(gt2, g2), O.static(ogt2, og2))
 
 
+@pytest.mark.parametrize("sweep", ["split", "fused"])
 @pytest.mark.parametrize("threshold", [0, 40, 1000])
-def test_in_sweep_pull_thresholds(dp, oracle_lib, monkeypatch, rmat16, threshold):
+def test_in_sweep_pull_thresholds(dp, oracle_lib, monkeypatch, rmat16, threshold, sweep):
     """lowDegreeThreshold moves vertices between the flat single slices and
     the 256-chunk multi path (and the push lists between low / high)."""
     import oracle
@@ -76,7 +78,7 @@ def test_in_sweep_pull_thresholds(dp, oracle_lib, monkeypatch, rmat16, threshold
     og2, _, _ = O.apply_batch(og, dels, ins)
     ogt2 = O.transpose(og2)
     g2, gt2 = dp.apply_batch_pair(g, gt, dp.BatchUpdate(dels, ins))
-    monkeypatch.setenv("DYNPR_SWEEP", "split")
+    monkeypatch.setenv("DYNPR_SWEEP", sweep)
     monkeypatch.setenv("DYNPR_HOST_LOOP", "0")
     for pruning in (True, False):
         ref = O.dynamic_frontier(og2, ogt2, dels, ins, base.ranks, ocfg, pruning=pruning)
