@@ -155,7 +155,7 @@ struct dynpr_context {
   dynpr_b200::DevBuf rank[2], contrib[2], flags_va, flags_np, flags_written,
       pend_low, pend_high, pend_flags, partials, perm_stage,
       tile_counts, red, stage_a, stage_b, stage_c, stage_d, stage_e, stage_f,
-      cub_tmp, tick, loopctl, layout_tmp, plan_prefix, side_err, bfs_a, bfs_b, run_list, run_pieces, scratch64a, scratch64b, scratch32a, scratch32b, scratch8a, batch[4],
+      prims_tmp, sort_hist, ingest_state[2], tick, loopctl, layout_tmp, plan_prefix, side_err, bfs_a, bfs_b, run_list, run_pieces, scratch64a, scratch64b, scratch32a, scratch32b, scratch8a, batch[4],
       flag_bits, flag_bounds;  // team pending-flag bitmap exchange
   // lifetime: graphs are allocated from this context's stream-ordered pool.
   // dynpr_context_destroy with graphs still alive (e.g. a garbage-collected
@@ -345,8 +345,12 @@ struct DeferredCsr {
 cudaStream_t side_stream(dynpr_context* ctx);
 void upload_csr_deferred(dynpr_context* ctx, uint32_t n, const uint64_t* offsets, const uint32_t* targets,
                          uint64_t m, cudaEvent_t after, DeferredCsr& d);
-uint32_t* copy_untouched_rows(dynpr_context* ctx, const uint8_t* touched, uint32_t n, const uint64_t* off,
-                              const uint32_t* tgt, const uint64_t* noff, uint32_t* ntgt, unsigned long long* nt);
+void graph_apply_batch_multi(dynpr_context* ctx, int count, const dynpr_graph* const* gs,
+                             const uint32_t* const* ds, const uint32_t* const* dd, uint64_t nd,
+                             const uint32_t* const* is, const uint32_t* const* id, uint64_t ni, bool validate,
+                             const uint32_t* h_ds, const uint32_t* h_dd, const uint32_t* h_is,
+                             const uint32_t* h_id, dynpr_graph** outs, uint64_t* missing_out,
+                             uint64_t* duplicate_out, uint32_t** rows_out, uint64_t* nrows_out);
 void graph_apply_batch_impl(dynpr_context* ctx, const dynpr_graph* g,
                             const uint32_t* d_ds, const uint32_t* d_dd,
                             uint64_t nd, const uint32_t* d_is,

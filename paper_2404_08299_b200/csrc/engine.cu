@@ -289,7 +289,7 @@ void run_device_loop(dynpr_context* ctx, const SolveSpec& sp, const SweepArgs& a
     half[k].npeers = 0;
     half[k].done = &dc->done;
     half[k].expand = &dc->expand;
-    half[k].offF = L->offF;
+    half[k].begF = L->begF;
     half[k].tgtF = L->tgtF;
     half[k].tick_sm = sweep_tick(ctx);
   }
@@ -388,8 +388,10 @@ void solve_impl(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynp
     }
   }
   // initRanksUniform / initRanksFrom (rank.cpp:22-37) + contributions
-  if (sp.prev) launch_gather_perm_f64(ctx, L, sp.prev, R[0]);
-  launch_init_ranks(ctx, L, sp.prev ? R[0] : nullptr, 1.0 / (double)n, R[0], R[1], CB[0], CB[1]);
+  // (the second buffers only where a sweep may leave vertices unwritten:
+  // frontier engines; a plain sweep writes every owned vertex)
+  launch_init_ranks(ctx, L, sp.prev, 1.0 / (double)n, R[0], sp.flagged ? R[1] : nullptr, CB[0],
+                    sp.flagged ? CB[1] : nullptr);
   if (sp.flagged) {
     DYNPR_CK(cudaMemsetAsync(written, 0, n, st));
     if (sp.flags_in) {
@@ -397,7 +399,7 @@ void solve_impl(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynp
     } else if (sp.traversal) {
       // markReachable over the relabelled forward CSR (frontier.cpp:86-121)
       DYNPR_CK(cudaMemsetAsync(va, 0, n, st));
-      mark_reachable(ctx, L->offF, L->tgtF, n, L->m, L->inv, sp.seeds, sp.nseeds, va);
+      mark_reachable(ctx, Rows{L->begF, L->outdeg, L->tgtF}, n, L->m, L->inv, sp.seeds, sp.nseeds, va);
     } else {
       // initialAffected + the one expandAffected before the loop
       // (engine.cpp:199-200)
@@ -408,10 +410,10 @@ void solve_impl(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynp
       if (!dist) {  // (a team expands by pull into its own rows, below)
         launch_collect_pending(ctx, L->outdeg, nullptr, n, np, c.low_degree_threshold, pl, ph, red + 1);
         if (device_loop) {  // list sizes stay on the device
-          launch_expand_dev(ctx, L->offF, L->tgtF, va, pl, ph, &red[1].pend_low, nullptr);
+          launch_expand_dev(ctx, Rows{L->begF, L->outdeg, L->tgtF}, va, pl, ph, &red[1].pend_low, nullptr);
         } else {
           const SweepRed r0 = read_red(ctx, red + 1);
-          launch_expand(ctx, L->offF, L->tgtF, va, pl, r0.pend_low, ph, r0.pend_high);
+          launch_expand(ctx, Rows{L->begF, L->outdeg, L->tgtF}, va, pl, r0.pend_low, ph, r0.pend_high);
         }
       }
     }
@@ -615,7 +617,7 @@ void solve_impl(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynp
         launch_pull_expand(ctx, a);
         ctx->pull_expansions += 1;
       } else {
-        launch_expand(ctx, L->offF, L->tgtF, va, pl, r.pend_low, ph, r.pend_high);
+        launch_expand(ctx, Rows{L->begF, L->outdeg, L->tgtF}, va, pl, r.pend_low, ph, r.pend_high);
       }
     }
   }
@@ -720,7 +722,7 @@ dynpr_status dynpr_context_create(int device, dynpr_context** out) {
       DYNPR_CK(cudaEventCreate(&ctx->ev_b));
       DYNPR_CK(cudaEventCreate(&ctx->ev_s0));
       DYNPR_CK(cudaEventCreate(&ctx->ev_s1));
-      DYNPR_CK(cudaMallocHost(&ctx->pinned, 4096));
+      DYNPR_CK(cudaMallocHost(&ctx->pinned, 8192));  // [4096, 8192): ingest status slots (graph.cu)
     } catch (...) {
       dynpr_context_destroy(ctx);
       throw;
@@ -974,8 +976,7 @@ dynpr_status dynpr_update_ranks(dynpr_context* ctx, const dynpr_graph* gT, const
     double* R0 = ctx->rank[0].as<double>(n);
     double* R1 = ctx->rank[1].as<double>(n);
     double* C0 = ctx->contrib[0].as<double>(n);
-    launch_gather_perm_f64(ctx, L, prev, R0);
-    launch_init_ranks(ctx, L, R0, 0.0, R0, nullptr, C0, nullptr);
+    launch_init_ranks(ctx, L, prev, 0.0, R0, nullptr, C0, nullptr);
     const bool flagged = vertex_affected != nullptr;
     uint8_t* va = nullptr;
     uint8_t* np = nullptr;
@@ -1094,7 +1095,7 @@ dynpr_status dynpr_expand_affected(dynpr_context* ctx, const dynpr_graph* g, uin
     DYNPR_CK(cudaMemsetAsync(red, 0, sizeof(SweepRed), ctx->stream));
     launch_collect_pending(ctx, nullptr, g->off, n, np, threshold, pl, ph, red);
     const SweepRed r = read_red(ctx, red);
-    launch_expand(ctx, g->off, g->tgt, va.dev, pl, r.pend_low, ph, r.pend_high);
+    launch_expand(ctx, Rows{g->off, nullptr, g->tgt}, va.dev, pl, r.pend_low, ph, r.pend_high);
     va.commit();
   });
 }
@@ -1272,7 +1273,7 @@ dynpr_status dynpr_mark_reachable(dynpr_context* ctx, const dynpr_graph* g, cons
     if (any_bad_ids(ctx, s, s, n_seeds, n)) invalid("markReachable: seed out of range");
     uint8_t* flags = ctx->flags_va.as<uint8_t>((uint64_t)n + 4);
     DYNPR_CK(cudaMemsetAsync(flags, 0, (size_t)n + 4, ctx->stream));
-    mark_reachable(ctx, g->off, g->tgt, n, g->m, nullptr, s, n_seeds, flags);
+    mark_reachable(ctx, Rows{g->off, nullptr, g->tgt}, n, g->m, nullptr, s, n_seeds, flags);
     if (n) DYNPR_CK(cudaMemcpyAsync(vertex_affected, flags, n, cudaMemcpyDefault, ctx->stream));
     sync(ctx);
   });

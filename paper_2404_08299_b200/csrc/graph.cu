@@ -14,10 +14,9 @@
 // deduplicated slices) and validation errors carry the reference messages.
 #include <atomic>
 
-#include <cub/cub.cuh>
-
 #include "common.cuh"
 #include "layout.cuh"
+#include "prims.cuh"
 
 namespace dynpr_b200 {
 
@@ -188,12 +187,66 @@ __global__ void k_validate_edges(const uint32_t* tgt, uint64_t elim, uint32_t n,
 }
 
 // ---- applyBatch kernels ----------------------------------------------------
-__global__ void k_overlap(const uint64_t* ins, uint64_t ni, const uint64_t* dels,
-                          uint64_t nd, int* flag) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ni;
+// The ingest is two-phase (see graph_apply_batch_impl): phase A sorts and
+// classifies the batch and derives the new offsets without a host round
+// trip; one readback of an IngestStatus record then sizes the new target
+// array and carries every validation result; phase B copies and merges.
+// Per-vertex state (deletion / insertion counts, touched / loop / need
+// flags) lives in context arrays that stay zero between ingests: phase B
+// clears exactly the touched rows again, so no O(n) memset runs per batch.
+struct IngestStatus {
+  unsigned long long bad_del, bad_ins, self_del;  // first offending list index (kNone: none)
+  unsigned long long overlap;                     // an edge both deleted and inserted
+  unsigned long long missing, dup;                // deletions not present / insertions already present
+  unsigned long long ndu, nu;                     // unique deletions / unique batch entries
+  unsigned long long ndp, nnw;                    // present deletions / fresh insertions
+  unsigned long long nt;                          // touched rows
+  unsigned long long m_new;                       // edge count of the new snapshot
+};
+
+// Per-vertex ingest state of one CSR, zero between ingests.
+struct VertexState {
+  unsigned* ddel;
+  unsigned* dins;
+  uint8_t* touched;
+  uint8_t* loop_ins;
+  uint8_t* need;
+};
+
+__global__ void k_status_init(IngestStatus* s) {
+  *s = IngestStatus{kNone, kNone, kNone, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+}
+
+// graph.cpp:116-120: ids in range (both lists), no self-loop deletion; the
+// first offending index of each kind.
+__global__ void k_batch_check(const uint32_t* ds, const uint32_t* dd, uint64_t nd, const uint32_t* is,
+                              const uint32_t* id, uint64_t ni, uint32_t n, IngestStatus* st) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nd + ni;
        i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t p = lower_bound_dev<uint64_t, uint64_t>(dels, 0, nd, ins[i]);
-    if (p < nd && dels[p] == ins[i]) atomicExch(flag, 1);
+    if (i < nd) {
+      const uint32_t u = ds[i], v = dd[i];
+      if (u >= n || v >= n) atomicMin(&st->bad_del, (unsigned long long)i);
+      if (u == v) atomicMin(&st->self_del, (unsigned long long)i);
+    } else {
+      const uint64_t k = i - nd;
+      if (is[k] >= n || id[k] >= n) atomicMin(&st->bad_ins, (unsigned long long)k);
+    }
+  }
+}
+
+// Deletions then insertions as one key list: tag (0 / 1) above the packed
+// (u, v).  Out-of-range ids (reported through the status) are clamped so
+// the rest of phase A stays in bounds.
+__global__ void k_pack_batch(const uint32_t* ds, const uint32_t* dd, uint64_t nd, const uint32_t* is,
+                             const uint32_t* id, uint64_t ni, uint32_t n, int sb, uint64_t* keys) {
+  const uint32_t top = n ? n - 1 : 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nd + ni;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const bool del = i < nd;
+    uint32_t u = del ? ds[i] : is[i - nd], v = del ? dd[i] : id[i - nd];
+    u = u < top ? u : top;
+    v = v < top ? v : top;
+    keys[i] = ((uint64_t)(del ? 0 : 1) << (2 * sb)) | ((uint64_t)u << sb) | v;
   }
 }
 
@@ -204,65 +257,144 @@ __device__ __forceinline__ bool slice_has(const uint64_t* off, const uint32_t* t
   return p < e && tgt[p] == v;
 }
 
-// Unique deletions: found ones shrink their source slice, absent ones are
-// tallied as missing (graph.cpp:174-191).
-__global__ void k_del_effect(const uint64_t* dels, uint64_t nd, int sb,
-                             uint64_t mask, const uint64_t* off,
-                             const uint32_t* tgt, uint8_t* found,
-                             unsigned* ddel, uint8_t* touched,
-                             unsigned long long* missing) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nd;
+// Unique batch entries (graph.cpp:122-191): a deletion present in the graph
+// shrinks its row, an absent one is missing; an insertion already present
+// is a duplicate, a fresh one grows its row; an insertion that is also a
+// deletion is the overlap error (graph.cpp:130-138).  keep[i] marks the
+// entries the merge applies.
+__global__ void k_batch_effect(const uint64_t* keys, const unsigned long long* nu_dev, int sb, const uint64_t* off,
+                               const uint32_t* tgt, uint8_t* keep, VertexState vs, IngestStatus* st) {
+  const uint64_t nu = *nu_dev;
+  const uint64_t tag = 1ull << (2 * sb), mask = (1ull << sb) - 1;
+  unsigned long long missing = 0, dup = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nu;
        i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t u = (uint32_t)(dels[i] >> sb), v = (uint32_t)(dels[i] & mask);
-    const bool f = slice_has(off, tgt, u, v);
-    found[i] = f;
-    if (f) {
-      atomicAdd(&ddel[u], 1u);
-      touched[u] = 1;
-    } else {
-      atomicAdd(missing, 1ull);
-    }
-  }
-}
-// Unique insertions: present ones are duplicates (graph.cpp:168-171).
-__global__ void k_ins_effect(const uint64_t* ins, uint64_t ni, int sb,
-                             uint64_t mask, const uint64_t* off,
-                             const uint32_t* tgt, uint8_t* fresh,
-                             unsigned* dins, uint8_t* touched,
-                             uint8_t* loop_ins, unsigned long long* dup) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ni;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t u = (uint32_t)(ins[i] >> sb), v = (uint32_t)(ins[i] & mask);
+    const uint64_t k = keys[i];
+    const bool ins = (k & tag) != 0;
+    const uint32_t u = (uint32_t)((k >> sb) & mask), v = (uint32_t)(k & mask);
+    if (!ins && (i + 1 == nu || (keys[i + 1] & tag))) st->ndu = i + 1;  // last deletion
     const bool present = slice_has(off, tgt, u, v);
-    fresh[i] = !present;
-    if (present) {
-      atomicAdd(dup, 1ull);
+    bool kp;
+    if (!ins) {
+      kp = present;
+      if (present) {
+        atomicAdd(vs.ddel + u, 1u);
+        vs.touched[u] = 1;
+      } else {
+        ++missing;
+      }
     } else {
-      atomicAdd(&dins[u], 1u);
-      touched[u] = 1;
-      if (u == v) loop_ins[u] = 1;
+      kp = !present;
+      if (present) {
+        ++dup;
+      } else {
+        atomicAdd(vs.dins + u, 1u);
+        vs.touched[u] = 1;
+        if (u == v) vs.loop_ins[u] = 1;
+      }
+      const uint64_t dk = k & ~tag;  // the same edge as a deletion?
+      const uint64_t p = lower_bound_dev<uint64_t, uint64_t>(keys, 0, i, dk);
+      if (p < i && keys[p] == dk) st->overlap = 1;
     }
+    keep[i] = kp;
+  }
+  missing = warp_sum(missing);
+  dup = warp_sum(dup);
+  if ((threadIdx.x & 31) == 0) {
+    if (missing) atomicAdd(&st->missing, missing);
+    if (dup) atomicAdd(&st->dup, dup);
   }
 }
+
 // Vertices lacking their loop get one (graph.cpp:155-163,193).
-__global__ void k_need_loop(const uint64_t* off, const uint32_t* tgt, uint32_t n,
-                            const uint8_t* loop_ins, uint8_t* need,
-                            uint8_t* touched) {
+__global__ void k_need_loop(const uint64_t* off, const uint32_t* tgt, uint32_t n, VertexState vs) {
   for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
        v += (uint64_t)gridDim.x * blockDim.x) {
-    const bool has = slice_has(off, tgt, (uint32_t)v, (uint32_t)v);
-    const bool nl = !has && !loop_ins[v];
-    need[v] = nl;
-    if (nl) touched[v] = 1;
+    const bool nl = !vs.loop_ins[v] && !slice_has(off, tgt, (uint32_t)v, (uint32_t)v);
+    if (nl) {
+      vs.need[v] = 1;
+      vs.touched[v] = 1;
+    }
   }
 }
-__global__ void k_new_degrees(const uint64_t* off, uint32_t n,
-                              const unsigned* ddel, const unsigned* dins,
-                              const uint8_t* need, uint64_t* noff) {
-  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v <= n;
-       v += (uint64_t)gridDim.x * blockDim.x) {
-    if (v == n) { noff[v] = 0; continue; }
-    noff[v] = (off[v + 1] - off[v]) - ddel[v] + dins[v] + need[v];
+
+// The merge lists: present deletions (tag 0, keep) / fresh insertions (tag
+// 1, keep), untagged and still sorted.
+struct KeepTag {
+  const uint64_t* keys;
+  const uint8_t* keep;
+  uint64_t tag;
+  bool ins;
+  __device__ __forceinline__ bool operator()(uint64_t i) const {
+    return keep[i] && (((keys[i] & tag) != 0) == ins);
+  }
+};
+struct Untag {
+  const uint64_t* keys;
+  uint64_t tag;
+  __device__ __forceinline__ uint64_t operator()(uint64_t i) const { return keys[i] & ~tag; }
+};
+// Row delta of the j-th touched row (0 past the list).
+struct RowDelta {
+  const uint32_t* T;
+  const unsigned long long* nt;
+  VertexState vs;
+  __device__ __forceinline__ long long operator()(uint64_t j) const {
+    if (j >= *nt) return 0;
+    const uint32_t u = T[j];
+    return (long long)vs.dins[u] + vs.need[u] - (long long)vs.ddel[u];
+  }
+};
+
+// New offsets: noff[v] = off[v] + D[#touched rows < v].  Block per 2048
+// vertices: cs[c] = #touched rows below chunk c (k_chunk_starts, one
+// binary search per chunk), the chunk's touched rows (few) are staged in
+// shared memory and each thread counts those below its vertex.
+constexpr int kOffChunk = 2048;
+__global__ void k_chunk_starts(const uint32_t* T, const unsigned long long* nt_dev, uint64_t nchunks, uint32_t* cs) {
+  const uint64_t nt = *nt_dev;
+  for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c <= nchunks;
+       c += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t x = c * kOffChunk;
+    uint64_t lo = 0, hi = nt;
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (T[mid] < x) lo = mid + 1; else hi = mid;
+    }
+    cs[c] = (uint32_t)lo;
+  }
+}
+__global__ void __launch_bounds__(256) k_new_offsets(const uint64_t* off, uint32_t n, const uint32_t* T,
+                                                     const uint32_t* cs, const long long* D, uint64_t* noff,
+                                                     IngestStatus* st) {
+  __shared__ uint32_t s_t[kOffChunk];
+  const uint64_t c0 = (uint64_t)blockIdx.x * kOffChunk;
+  const uint64_t c1 = c0 + kOffChunk < (uint64_t)n + 1 ? c0 + kOffChunk : (uint64_t)n + 1;
+  const uint32_t j0 = cs[blockIdx.x], k = cs[blockIdx.x + 1] - j0;  // <= kOffChunk (distinct rows)
+  for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) s_t[i] = T[j0 + i];
+  __syncthreads();
+  for (uint64_t v = c0 + threadIdx.x; v < c1; v += blockDim.x) {
+    uint32_t lo = 0, hi = k;  // staged rows < v
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (s_t[mid] < v) lo = mid + 1; else hi = mid;
+    }
+    const uint64_t o = (uint64_t)((long long)off[v] + D[j0 + lo]);
+    noff[v] = o;
+    if (v == n) st->m_new = o;
+  }
+}
+
+// Phase B: clear the touched rows' state (the zero invariant).
+__global__ void k_clear_rows(const uint32_t* T, uint64_t nt, VertexState vs) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < nt;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t u = T[j];
+    vs.ddel[u] = 0;
+    vs.dins[u] = 0;
+    vs.touched[u] = 0;
+    vs.loop_ins[u] = 0;
+    vs.need[u] = 0;
   }
 }
 
@@ -344,10 +476,10 @@ __device__ __forceinline__ void warp_copy_range(const uint32_t* __restrict__ tgt
 // pieces, warp per piece (grid-stride over the pieces), which keeps every
 // warp streaming ~32 KB instead of re-reading row metadata every 32 rows.
 constexpr uint64_t kRunPiece = 8192;
-__global__ void k_run_pieces(const uint32_t* T, const unsigned long long* nt_ptr, uint32_t n, const uint64_t* off,
-                             uint32_t* pieces) {
+__global__ void k_run_pieces(const uint32_t* T, const unsigned long long* nt_ptr, uint64_t upper, uint32_t n,
+                             const uint64_t* off, uint32_t* pieces) {
   const uint64_t nt = *nt_ptr;
-  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j <= nt + 1;
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < upper + 2;
        j += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t c = 0;
     if (j <= nt) {
@@ -356,7 +488,7 @@ __global__ void k_run_pieces(const uint32_t* T, const unsigned long long* nt_ptr
       const uint64_t words = b > a ? off[b] - off[a] : 0;
       c = (uint32_t)((words + kRunPiece - 1) / kRunPiece);
     }
-    pieces[j] = c;  // entry nt + 1 stays 0: the exclusive scan's total
+    pieces[j] = c;  // entries past nt stay 0: the exclusive scan at nt + 1 is the total
   }
 }
 __global__ void k_copy_runs(const uint32_t* T, const unsigned long long* nt_ptr, const uint32_t* pstart, uint32_t n,
@@ -377,41 +509,57 @@ __global__ void k_copy_runs(const uint32_t* T, const unsigned long long* nt_ptr,
   }
 }
 
+// The runs of untouched rows around the ascending touched-row list T (*nt_dev
+// entries, at most nt_upper) copied from (off, tgt) to (noff, ntgt); pieces
+// holds nt_upper + 3 words of workspace.
+void copy_runs(dynpr_context* ctx, const uint32_t* T, const unsigned long long* nt_dev, uint64_t nt_upper, uint32_t n,
+               const uint64_t* off, const uint32_t* tgt, const uint64_t* noff, uint32_t* ntgt, uint32_t* pieces) {
+  cudaStream_t st = ctx->stream;
+  k_run_pieces<<<grid_for(nt_upper + 2, 256, (unsigned)ctx->num_sms * 8), 256, 0, st>>>(T, nt_dev, nt_upper, n, off,
+                                                                                       pieces);
+  check_launch();
+  prims::scan_array<uint32_t>(ctx, pieces, pieces, nt_upper + 2, st);
+  k_copy_runs<<<(unsigned)ctx->num_sms * 32, 256, 0, st>>>(T, nt_dev, pieces, n, off, tgt, noff, ntgt);
+  check_launch();
+  count_launch(ctx, 2);
+}
+
 // Merge work items of the touched rows: a row of old degree d is split into
 // max(1, ceil(d / kMergeChunk)) items so a touched hub (RMAT-24: ~4e5 edges)
 // is spread over many warps instead of serialising one.
 constexpr uint64_t kMergeChunk = 2048;
-__global__ void k_merge_items(const uint8_t* touched, const uint64_t* off, uint32_t n, uint32_t* items) {
-  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v <= n;
-       v += (uint64_t)gridDim.x * blockDim.x) {
-    uint32_t c = 0;
-    if (v < n && touched[v]) {
-      const uint64_t d = off[v + 1] - off[v];
-      c = d > kMergeChunk ? (uint32_t)((d + kMergeChunk - 1) / kMergeChunk) : 1u;
-    }
-    items[v] = c;
+struct RowItems {
+  const uint32_t* T;
+  const uint64_t* off;
+  uint64_t nt;
+  __device__ __forceinline__ uint32_t operator()(uint64_t j) const {
+    if (j >= nt) return 0;
+    const uint64_t d = off[T[j] + 1] - off[T[j]];
+    return d > kMergeChunk ? (uint32_t)((d + kMergeChunk - 1) / kMergeChunk) : 1u;
   }
-}
+};
 
-// Rows with batch entries: every surviving old target and every fresh
-// insertion is written at its final position (old index - deletions before
-// it + insertions before it + the re-ensured self-loop when it precedes),
-// so the items of one row are independent.  Item t -> row through the
-// exclusive scan `istart` (n + 1 entries, istart[n] = total items).
-__global__ void k_merge_touched(const uint32_t* istart, uint32_t n,
-                                const uint64_t* off, const uint32_t* tgt,
-                                const uint64_t* noff, uint32_t* ntgt,
-                                const uint64_t* dp, uint64_t ndp,
-                                const uint64_t* nw, uint64_t nnw, int sb,
-                                uint64_t mask, const uint8_t* need) {
+// Touched rows: every surviving old target and every fresh insertion is
+// written at its final position (old index - deletions before it +
+// insertions before it + the re-ensured self-loop when it precedes), so
+// the items of one row are independent.  Item t -> touched row j through
+// the exclusive scan `istart` (nt + 1 entries).  Old targets are loaded
+// kMergeIlp at a time per lane (independent loads in flight; the searches
+// in the row's few batch entries then run on registers).
+constexpr int kMergeIlp = 8;
+__global__ void k_merge_touched(const uint32_t* istart, const uint32_t* T, uint64_t nt, const uint64_t* off,
+                                const uint32_t* tgt, const uint64_t* noff, uint32_t* ntgt, const uint64_t* dp,
+                                const unsigned long long* ndp_dev, const uint64_t* nw,
+                                const unsigned long long* nnw_dev, int sb, uint64_t mask, const uint8_t* need) {
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / 32;
   const unsigned lane = threadIdx.x & 31;
   const uint64_t nwarps = (uint64_t)gridDim.x * blockDim.x / 32;
-  const uint32_t total = istart[n];
+  const uint32_t total = istart[nt];
+  const uint64_t ndp = *ndp_dev, nnw = *nnw_dev;
   for (uint64_t t = warp; t < total; t += nwarps) {
-    // row u: the last u with istart[u] <= t (rows with no items share a start)
-    const uint32_t u = (uint32_t)(upper_bound_u32(istart, (uint64_t)n + 1, (uint32_t)t) - 1);
-    const uint64_t c = t - istart[u];
+    const uint64_t j = upper_bound_u32(istart, nt + 1, (uint32_t)t) - 1;
+    const uint32_t u = T[j];
+    const uint64_t c = t - istart[j];
     const uint64_t so = off[u], se = off[u + 1], base = noff[u];
     const uint64_t cb = so + c * kMergeChunk, ce = cb + kMergeChunk < se ? cb + kMergeChunk : se;
     const uint64_t klo = (uint64_t)u << sb, khi = ((uint64_t)u + 1) << sb;
@@ -420,13 +568,29 @@ __global__ void k_merge_touched(const uint32_t* istart, uint32_t n,
     const uint64_t nlo = lower_bound_dev<uint64_t, uint64_t>(nw, 0, nnw, klo);
     const uint64_t nhi = lower_bound_dev<uint64_t, uint64_t>(nw, nlo, nnw, khi);
     const bool nl = need[u];
-    for (uint64_t k = cb - so + lane; k < ce - so; k += 32) {
-      const uint32_t x = tgt[so + k];
-      const uint64_t key = klo | x;
-      const uint64_t q = lower_bound_dev<uint64_t, uint64_t>(dp, dlo, dhi, key);
-      if (q < dhi && dp[q] == key) continue;
-      const uint64_t r = lower_bound_dev<uint64_t, uint64_t>(nw, nlo, nhi, key) - nlo;
-      ntgt[base + k - (q - dlo) + r + ((nl && u < x) ? 1 : 0)] = x;
+    // the batch entries inside the chunk's value range (usually none)
+    const uint64_t kf = cb < ce ? (klo | tgt[cb]) : klo, kl = cb < ce ? (klo | tgt[ce - 1]) + 1 : klo;
+    const uint64_t d0 = lower_bound_dev<uint64_t, uint64_t>(dp, dlo, dhi, kf);
+    const uint64_t d1 = lower_bound_dev<uint64_t, uint64_t>(dp, d0, dhi, kl);
+    const uint64_t n0 = lower_bound_dev<uint64_t, uint64_t>(nw, nlo, nhi, kf);
+    const uint64_t n1 = lower_bound_dev<uint64_t, uint64_t>(nw, n0, nhi, kl);
+    for (uint64_t k0 = cb; k0 < ce; k0 += 32 * kMergeIlp) {
+      uint32_t x[kMergeIlp];
+#pragma unroll
+      for (int q = 0; q < kMergeIlp; ++q) {
+        const uint64_t k = k0 + 32 * q + lane;
+        x[q] = k < ce ? tgt[k] : 0u;
+      }
+#pragma unroll
+      for (int q = 0; q < kMergeIlp; ++q) {
+        const uint64_t k = k0 + 32 * q + lane;
+        if (k >= ce) continue;
+        const uint64_t key = klo | x[q];
+        const uint64_t qd = d1 > d0 ? lower_bound_dev<uint64_t, uint64_t>(dp, d0, d1, key) : d0;
+        if (qd < d1 && dp[qd] == key) continue;
+        const uint64_t r = (n1 > n0 ? lower_bound_dev<uint64_t, uint64_t>(nw, n0, n1, key) : n0) - nlo;
+        ntgt[base + (k - so) - (qd - dlo) + r + ((nl && u < x[q]) ? 1 : 0)] = x[q];
+      }
     }
     if (c != 0) continue;
     for (uint64_t k = lane; k < nhi - nlo; k += 32) {
@@ -445,6 +609,7 @@ __global__ void k_merge_touched(const uint32_t* istart, uint32_t n,
     }
   }
 }
+
 
 // ---- helpers -------------------------------------------------------------
 int key_shift(uint32_t n) {
@@ -497,34 +662,22 @@ void check_ids(dynpr_context* ctx, const uint32_t* d_s, const uint32_t* d_d,
   }
 }
 
-template <class F>
-void cub_call(dynpr_context* ctx, F&& f) {
-  size_t bytes = 0;
-  DYNPR_CK(f(nullptr, bytes));
-  void* tmp = ctx->cub_tmp.ensure(bytes);
-  DYNPR_CK(f(tmp, bytes));
-}
-
-// Sorts + dedupes packed keys; returns the unique count (keys end in `out`).
-uint64_t sort_unique(dynpr_context* ctx, uint64_t* keys, uint64_t* alt,
-                     uint64_t cnt, int end_bit, uint64_t** out) {
+// Sorts + dedupes packed keys (end_bit significant bits); returns the unique
+// count (keys end in `*out`, one of the two buffers).
+uint64_t sort_unique(dynpr_context* ctx, uint64_t* keys, uint64_t* alt, uint64_t cnt, int end_bit, uint64_t** out) {
   if (cnt == 0) {
     *out = keys;
     return 0;
   }
-  cub::DoubleBuffer<uint64_t> db(keys, alt);
-  cub_call(ctx, [&](void* t, size_t& b) {
-    return cub::DeviceRadixSort::SortKeys(t, b, db, cnt, 0, end_bit, ctx->stream);
-  });
-  uint64_t* sorted = db.Current();
-  uint64_t* uniq = db.Alternate();
-  auto* num = reinterpret_cast<unsigned long long*>(ctx->scratch64a.as<unsigned long long>(1));
-  cub_call(ctx, [&](void* t, size_t& b) {
-    return cub::DeviceSelect::Unique(t, b, sorted, uniq, num, (int64_t)cnt, ctx->stream);
-  });
+  uint64_t* sorted = prims::radix_sort<uint64_t, uint32_t>(ctx, keys, alt, nullptr, nullptr, cnt, 0, end_bit,
+                                                           ctx->stream);
+  uint64_t* uniq = sorted == keys ? alt : keys;
+  auto* num = ctx->scratch64a.as<unsigned long long>(1);
+  prims::unique_sorted<uint64_t>(ctx, sorted, cnt, uniq, num, ctx->stream);
   *out = uniq;
   return read_u64(ctx, num);
 }
+
 
 }  // namespace
 
@@ -602,28 +755,223 @@ static dynpr_graph* build_from_device_edges(dynpr_context* ctx, uint32_t n,
   return g;
 }
 
-// Rows of `touched` (flags, n entries) listed in order, and every run of
-// untouched rows between them copied from (off, tgt) to (noff, ntgt) in
-// 8K-word pieces: the part of a CSR rebuild that is a plain copy.  `nt` =
-// device count of touched rows; the list is left in ctx->run_list.
-uint32_t* copy_untouched_rows(dynpr_context* ctx, const uint8_t* touched, uint32_t n, const uint64_t* off,
-                              const uint32_t* tgt, const uint64_t* noff, uint32_t* ntgt, unsigned long long* nt) {
+namespace {
+
+// Device temporaries of one CSR's ingest, carved from one pool block.
+struct IngestPlan {
+  const dynpr_graph* g = nullptr;
+  dynpr_graph* r = nullptr;
+  uint32_t n = 0;
+  int sb = 1;
+  uint64_t nd = 0, ni = 0, nb = 0, t_cap = 0;
+  VertexState vs{};
+  void* block = nullptr;
+  uint64_t *keys = nullptr, *keys2 = nullptr, *ukeys = nullptr, *dp = nullptr, *nw = nullptr;
+  uint8_t* keep = nullptr;
+  uint32_t *T = nullptr, *pieces = nullptr, *istart = nullptr, *cs = nullptr;
+  long long* D = nullptr;
+  IngestStatus* st = nullptr;   // device
+  IngestStatus* host = nullptr; // pinned readback slot
+};
+
+template <class T>
+T* carve(char*& p, uint64_t count) {
+  T* r = reinterpret_cast<T*>(p);
+  p += ((count * sizeof(T) + 255) / 256) * 256;
+  return r;
+}
+
+// Per-vertex ingest state `set` (0: the forward CSR, 1: the transpose of a
+// pair): zeroed when (re)allocated, kept zero by phase B.
+VertexState vertex_state(dynpr_context* ctx, int set, uint32_t n) {
+  DevBuf& b = ctx->ingest_state[set];
+  const uint64_t words = (uint64_t)n + 1;
+  const size_t need = words * (4 + 4 + 1 + 1 + 1) + 64;
+  void* before = b.p;
+  const size_t cap_before = b.cap;
+  char* p = static_cast<char*>(b.ensure(need));
+  if (p != before || cap_before < need) DYNPR_CK(cudaMemsetAsync(p, 0, b.cap, ctx->stream));
+  VertexState vs;
+  vs.ddel = reinterpret_cast<unsigned*>(p);
+  vs.dins = vs.ddel + words;
+  vs.touched = reinterpret_cast<uint8_t*>(vs.dins + words);
+  vs.loop_ins = vs.touched + words;
+  vs.need = vs.loop_ins + words;
+  return vs;
+}
+
+// Phase A: validation (optional), sort + unique + classification of the
+// batch, touched rows, their deltas and the new offsets; ends with the
+// status record copied to its pinned slot (no host wait).
+void ingest_phase_a(dynpr_context* ctx, IngestPlan& P, const dynpr_graph* g, int set, const uint32_t* ds,
+                    const uint32_t* dd, uint64_t nd, const uint32_t* is, const uint32_t* id, uint64_t ni,
+                    bool validate, IngestStatus* host_slot) {
   cudaStream_t st = ctx->stream;
-  uint32_t* T = ctx->run_list.as<uint32_t>((uint64_t)n + 1);
-  uint32_t* pcs = ctx->run_pieces.as<uint32_t>((uint64_t)n + 3);
-  cub::CountingInputIterator<uint32_t> iota(0);
-  cub_call(ctx, [&](void* t, size_t& b) {
-    return cub::DeviceSelect::Flagged(t, b, iota, touched, T, nt, (int64_t)n, st);
-  });
-  k_run_pieces<<<grid_for((uint64_t)n + 2, 256, 1 << 16), 256, 0, st>>>(T, nt, n, off, pcs);
+  const uint32_t n = g->n;
+  P.g = g;
+  P.n = n;
+  P.sb = key_shift(n);
+  if (2 * P.sb + 1 > 64) invalid("applyBatch: vertex ids too wide for the batch keys");
+  P.nd = nd;
+  P.ni = ni;
+  P.nb = nd + ni;
+  P.vs = vertex_state(ctx, set, n);
+  // touched rows: batch sources, plus every row lacking its loop
+  P.t_cap = g->all_loops ? (P.nb < (uint64_t)n ? P.nb : (uint64_t)n) : (uint64_t)n;
+  const uint64_t nb1 = P.nb + 1, t1 = P.t_cap + 2;
+  const uint64_t nchunks1 = ((uint64_t)n + 1 + kOffChunk - 1) / kOffChunk + 1;
+  const size_t bytes = 5 * (((nb1 * 8) + 255) / 256) * 256 + ((nb1 + 255) / 256) * 256 +
+                       2 * (((t1 * 4) + 255) / 256) * 256 + (((t1 + 1) * 4 + 255) / 256) * 256 +
+                       (((t1 * 8) + 255) / 256) * 256 + ((nchunks1 * 4 + 255) / 256) * 256 + 256;
+  P.block = pool_alloc(ctx, bytes);
+  char* p = static_cast<char*>(P.block);
+  P.keys = carve<uint64_t>(p, nb1);
+  P.keys2 = carve<uint64_t>(p, nb1);
+  P.ukeys = carve<uint64_t>(p, nb1);
+  P.dp = carve<uint64_t>(p, nb1);
+  P.nw = carve<uint64_t>(p, nb1);
+  P.keep = carve<uint8_t>(p, nb1);
+  P.T = carve<uint32_t>(p, t1);
+  P.istart = carve<uint32_t>(p, t1);
+  P.pieces = carve<uint32_t>(p, t1 + 1);
+  P.D = carve<long long>(p, t1);
+  P.cs = carve<uint32_t>(p, nchunks1);
+  P.st = carve<IngestStatus>(p, 1);
+  P.host = host_slot;
+  k_status_init<<<1, 1, 0, st>>>(P.st);
+  if (validate && P.nb) {
+    k_batch_check<<<grid_for(P.nb, 256, 4096), 256, 0, st>>>(ds, dd, nd, is, id, ni, n, P.st);
+  }
+  const uint64_t tag = 1ull << (2 * P.sb);
+  unsigned long long* nu = &P.st->nu;
+  if (P.nb) {
+    k_pack_batch<<<grid_for(P.nb, 256, 4096), 256, 0, st>>>(ds, dd, nd, is, id, ni, n, P.sb, P.keys);
+    uint64_t* sorted = prims::radix_sort<uint64_t, uint32_t>(ctx, P.keys, P.keys2, nullptr, nullptr, P.nb, 0,
+                                                             2 * P.sb + 1, st);
+    prims::unique_sorted<uint64_t>(ctx, sorted, P.nb, P.ukeys, nu, st);
+    k_batch_effect<<<grid_for(P.nb, 256, 4096), 256, 0, st>>>(P.ukeys, nu, P.sb, g->off, g->tgt, P.keep, P.vs,
+                                                              P.st);
+    count_launch(ctx, 2);
+  }
+  if (!g->all_loops && n) {
+    k_need_loop<<<grid_for(n, 256, 1 << 16), 256, 0, st>>>(g->off, g->tgt, n, P.vs);
+    count_launch(ctx);
+  }
   check_launch();
-  cub_call(ctx, [&](void* t, size_t& b) {
-    return cub::DeviceScan::ExclusiveSum(t, b, pcs, pcs, (int64_t)n + 3, st);
-  });
-  k_copy_runs<<<(unsigned)ctx->num_sms * 32, 256, 0, st>>>(T, nt, pcs, n, off, tgt, noff, ntgt);
+  unsigned long long* nt = &P.st->nt;
+  if (P.t_cap)
+    prims::select_if<uint32_t>(ctx, prims::Nonzero<uint8_t>{P.vs.touched}, prims::Iota32{}, n, P.T, nt, st);
+  if (P.nb) {
+    prims::select_if<uint64_t>(ctx, KeepTag{P.ukeys, P.keep, tag, false}, Untag{P.ukeys, tag}, P.nb, P.dp,
+                               &P.st->ndp, st, nu);
+    prims::select_if<uint64_t>(ctx, KeepTag{P.ukeys, P.keep, tag, true}, Untag{P.ukeys, tag}, P.nb, P.nw,
+                               &P.st->nnw, st, nu);
+  }
+  // D[j] = sum of the deltas of touched rows 0..j-1 (j <= nt)
+  prims::scan_exclusive<long long>(ctx, RowDelta{P.T, nt, P.vs}, P.D, P.t_cap + 1, st);
+  P.r = new_graph_struct(ctx, n);
+  P.r->off = pool_alloc_n<uint64_t>(ctx, (uint64_t)n + 1);
+  const uint64_t nchunks = ((uint64_t)n + 1 + kOffChunk - 1) / kOffChunk;
+  k_chunk_starts<<<grid_for(nchunks + 1, 256, 4096), 256, 0, st>>>(P.T, nt, nchunks, P.cs);
+  k_new_offsets<<<(unsigned)nchunks, 256, 0, st>>>(g->off, n, P.T, P.cs, P.D, P.r->off, P.st);
   check_launch();
   count_launch(ctx, 2);
-  return T;
+  DYNPR_CK(cudaMemcpyAsync(P.host, P.st, sizeof(IngestStatus), cudaMemcpyDeviceToHost, st));
+}
+
+// Phase B: the new targets -- runs of untouched rows copied, touched rows
+// merged -- and the per-vertex state cleared again.
+void ingest_phase_b(dynpr_context* ctx, IngestPlan& P, uint32_t** rows_out, uint64_t* nrows_out) {
+  cudaStream_t st = ctx->stream;
+  const IngestStatus& h = *P.host;
+  dynpr_graph* r = P.r;
+  r->m = h.m_new;
+  r->tgt = pool_alloc_n<uint32_t>(ctx, r->m ? r->m : 1);
+  const uint64_t nt = h.nt;
+  copy_runs(ctx, P.T, &P.st->nt, nt, P.n, P.g->off, P.g->tgt, r->off, r->tgt, P.pieces);
+  if (nt) {
+    prims::scan_exclusive<uint32_t>(ctx, RowItems{P.T, P.g->off, nt}, P.istart, nt + 1, st);
+    const uint64_t mask = (1ull << P.sb) - 1;
+    k_merge_touched<<<(unsigned)ctx->num_sms * 16, 256, 0, st>>>(P.istart, P.T, nt, P.g->off, P.g->tgt, r->off,
+                                                                  r->tgt, P.dp, &P.st->ndp, P.nw, &P.st->nnw, P.sb,
+                                                                  mask, P.vs.need);
+    k_clear_rows<<<grid_for(nt, 256, 4096), 256, 0, st>>>(P.T, nt, P.vs);
+    check_launch();
+    count_launch(ctx, 2);
+  }
+  if (rows_out) {  // the touched rows, for an incremental engine layout (layout.cu)
+    uint32_t* rows = pool_alloc_n<uint32_t>(ctx, nt ? nt : 1);
+    if (nt) DYNPR_CK(cudaMemcpyAsync(rows, P.T, nt * 4, cudaMemcpyDeviceToDevice, st));
+    *rows_out = rows;
+    *nrows_out = nt;
+  }
+  r->all_loops = true;
+  pool_free(ctx, P.block);
+  P.block = nullptr;
+}
+
+// Error path: the result (if any) and the temporaries freed, and the
+// per-vertex state zeroed wholesale (phase A may have marked rows that no
+// readback listed).
+void ingest_abort(dynpr_context* ctx, IngestPlan& P, int set) {
+  if (P.r) destroy_graph(P.r);
+  P.r = nullptr;
+  if (P.block) pool_free(ctx, P.block);
+  P.block = nullptr;
+  DevBuf& b = ctx->ingest_state[set];
+  if (b.p) cudaMemsetAsync(b.p, 0, b.cap, ctx->stream);
+  cudaGetLastError();
+}
+
+// The reference's error order (graph.cpp:116-138), from the status record.
+void ingest_throw_if_invalid(dynpr_context* ctx, const IngestStatus& h, const uint32_t* d_ds, const uint32_t* d_dd,
+                             const uint32_t* d_is, const uint32_t* d_id, const uint32_t* h_ds, const uint32_t* h_dd,
+                             const uint32_t* h_is, const uint32_t* h_id, uint32_t n) {
+  auto bad = [&](const char* what, const uint32_t* ds, const uint32_t* dd, const uint32_t* hs, const uint32_t* hd,
+                 unsigned long long i) {
+    auto [u, v] = fetch_pair(ctx, ds, dd, hs, hd, i);
+    invalid(std::string(what) + ": vertex id out of range (" + std::to_string(u) + "," + std::to_string(v) +
+            ") for |V|=" + std::to_string(n));
+  };
+  if (h.bad_del != kNone) bad("applyBatch deletions", d_ds, d_dd, h_ds, h_dd, h.bad_del);
+  if (h.bad_ins != kNone) bad("applyBatch insertions", d_is, d_id, h_is, h_id, h.bad_ins);
+  if (h.self_del != kNone) invalid("applyBatch: self-loops cannot be deleted");
+  if (h.overlap) invalid("applyBatch: edge appears in both deletions and insertions");
+}
+
+}  // namespace
+
+// applyBatch of one CSR or of a mutually transposed pair (the transpose
+// receives the reversed batch, ids already validated through the first):
+// both phase A's, ONE host wait for both status records, both phase B's.
+void graph_apply_batch_multi(dynpr_context* ctx, int count, const dynpr_graph* const* gs,
+                             const uint32_t* const* ds, const uint32_t* const* dd, uint64_t nd,
+                             const uint32_t* const* is, const uint32_t* const* id, uint64_t ni, bool validate,
+                             const uint32_t* h_ds, const uint32_t* h_dd, const uint32_t* h_is,
+                             const uint32_t* h_id, dynpr_graph** outs, uint64_t* missing_out,
+                             uint64_t* duplicate_out, uint32_t** rows_out, uint64_t* nrows_out) {
+  IngestPlan P[2];
+  auto* slots = reinterpret_cast<IngestStatus*>(static_cast<char*>(ctx->pinned) + 4096);
+  static_assert(2 * sizeof(IngestStatus) <= 1024, "pinned status slots");
+  try {
+    for (int c = 0; c < count; ++c)
+      ingest_phase_a(ctx, P[c], gs[c], c, ds[c], dd[c], nd, is[c], id[c], ni, validate && c == 0, slots + c);
+    sync(ctx);
+    if (validate) ingest_throw_if_invalid(ctx, *P[0].host, ds[0], dd[0], is[0], id[0], h_ds, h_dd, h_is, h_id,
+                                          gs[0]->n);
+    for (int c = 0; c < count; ++c)
+      ingest_phase_b(ctx, P[c], rows_out ? rows_out + c : nullptr, nrows_out ? nrows_out + c : nullptr);
+  } catch (...) {
+    for (int c = 0; c < count; ++c) ingest_abort(ctx, P[c], c);
+    throw;
+  }
+  const IngestStatus& h = *P[0].host;
+  if (missing_out) *missing_out += (nd - h.ndu) + h.missing;
+  if (duplicate_out) *duplicate_out += (ni - (h.nu - h.ndu)) + h.dup;
+  for (int c = 0; c < count; ++c) {
+    outs[c] = P[c].r;
+    P[c].r = nullptr;
+  }
 }
 
 void graph_apply_batch_impl(dynpr_context* ctx, const dynpr_graph* g,
@@ -635,162 +983,11 @@ void graph_apply_batch_impl(dynpr_context* ctx, const dynpr_graph* g,
                             dynpr_graph** out, uint64_t* missing_out,
                             uint64_t* duplicate_out, uint32_t** rows_out,
                             uint64_t* nrows_out) {
-  const uint32_t n = g->n;
-  cudaStream_t st = ctx->stream;
-  if (validate) {  // graph.cpp:116-120, in the reference's order
-    check_ids(ctx, d_ds, d_dd, nd, n, "applyBatch deletions", h_ds, h_dd);
-    check_ids(ctx, d_is, d_id, ni, n, "applyBatch insertions", h_is, h_id);
-    if (nd) {
-      auto* first = scratch_u64(ctx, ctx->scratch64b, 1, kNone);
-      k_first_self_pair<<<grid_for(nd, 256, 4096), 256, 0, st>>>(d_ds, d_dd, nd, first);
-      check_launch();
-      count_launch(ctx);
-      if (read_u64(ctx, first) != kNone)
-        invalid("applyBatch: self-loops cannot be deleted");
-    }
-  }
-  const int sb = key_shift(n);
-  const uint64_t mask = (1ull << sb) - 1;
-  // sort + unique both lists (graph.cpp:122-127)
-  uint64_t* dk = ctx->stage_c.as<uint64_t>(nd + 1);
-  uint64_t* dk2 = ctx->stage_d.as<uint64_t>(nd + 1);
-  uint64_t* ik = ctx->stage_e.as<uint64_t>(ni + 1);
-  uint64_t* ik2 = ctx->stage_f.as<uint64_t>(ni + 1);
-  if (nd) {
-    k_pack<<<grid_for(nd, 256, 4096), 256, 0, st>>>(d_ds, d_dd, nd, sb, dk);
-    check_launch();
-    count_launch(ctx);
-  }
-  if (ni) {
-    k_pack<<<grid_for(ni, 256, 4096), 256, 0, st>>>(d_is, d_id, ni, sb, ik);
-    check_launch();
-    count_launch(ctx);
-  }
-  uint64_t *du = dk, *iu = ik;
-  const uint64_t ndu = sort_unique(ctx, dk, dk2, nd, 2 * sb, &du);
-  const uint64_t niu = sort_unique(ctx, ik, ik2, ni, 2 * sb, &iu);
-  uint64_t missing = nd - ndu, duplicate = ni - niu;
-  if (validate && ndu && niu) {  // graph.cpp:130-138
-    auto* flag = reinterpret_cast<int*>(scratch_u64(ctx, ctx->scratch64b, 1, 0));
-    k_overlap<<<grid_for(niu, 256, 4096), 256, 0, st>>>(iu, niu, du, ndu, flag);
-    check_launch();
-    count_launch(ctx);
-    if (read_u64(ctx, reinterpret_cast<unsigned long long*>(flag)) != 0)
-      invalid("applyBatch: edge appears in both deletions and insertions");
-  }
-  // per-vertex deltas
-  unsigned* ddel = ctx->scratch32a.as<unsigned>(2 * (uint64_t)n + 2);
-  unsigned* dins = ddel + n + 1;
-  uint8_t* v8 = ctx->scratch8a.as<uint8_t>(3 * (uint64_t)n + 3);
-  uint8_t* touched = v8;
-  uint8_t* loop_ins = v8 + n + 1;
-  uint8_t* need = v8 + 2 * ((uint64_t)n + 1);
-  DYNPR_CK(cudaMemsetAsync(ddel, 0, (2 * (uint64_t)n + 2) * sizeof(unsigned), st));
-  DYNPR_CK(cudaMemsetAsync(v8, 0, 3 * (uint64_t)n + 3, st));
-  auto* counters = scratch_u64(ctx, ctx->scratch64b, 4, 0);  // missing, dup, touched
-  uint8_t* found = ctx->stage_a.as<uint8_t>(ndu + niu + 2);
-  uint8_t* fresh = found + ndu + 1;
-  if (ndu) {
-    k_del_effect<<<grid_for(ndu, 256, 8192), 256, 0, st>>>(du, ndu, sb, mask, g->off, g->tgt, found,
-                                                           ddel, touched, counters + 0);
-    check_launch();
-    count_launch(ctx);
-  }
-  if (niu) {
-    k_ins_effect<<<grid_for(niu, 256, 8192), 256, 0, st>>>(iu, niu, sb, mask, g->off, g->tgt, fresh,
-                                                           dins, touched, loop_ins, counters + 1);
-    check_launch();
-    count_launch(ctx);
-  }
-  if (!g->all_loops && n) {
-    k_need_loop<<<grid_for(n, 256, 1 << 16), 256, 0, st>>>(g->off, g->tgt, n, loop_ins, need, touched);
-    check_launch();
-    count_launch(ctx);
-  }
-  // new offsets
-  dynpr_graph* r = new_graph_struct(ctx, n);
-  try {
-    r->off = pool_alloc_n<uint64_t>(ctx, (uint64_t)n + 1);
-  } catch (...) {
-    destroy_graph(r);
-    throw;
-  }
-  k_new_degrees<<<grid_for((uint64_t)n + 1, 256, 1 << 16), 256, 0, st>>>(g->off, n, ddel, dins, need, r->off);
-  check_launch();
-  count_launch(ctx);
-  cub_call(ctx, [&](void* t, size_t& b) {
-    return cub::DeviceScan::ExclusiveSum(t, b, r->off, r->off, (int64_t)n + 1, st);
-  });
-  uint64_t m_new = 0;
-  DYNPR_CK(cudaMemcpyAsync(ctx->pinned, r->off + n, 8, cudaMemcpyDeviceToHost, st));
+  graph_apply_batch_multi(ctx, 1, &g, &d_ds, &d_dd, nd, &d_is, &d_id, ni, validate, h_ds, h_dd, h_is, h_id, out,
+                          missing_out, duplicate_out, rows_out, nrows_out);
   sync(ctx);
-  std::memcpy(&m_new, ctx->pinned, 8);
-  r->m = m_new;
-  try {
-    r->tgt = pool_alloc_n<uint32_t>(ctx, m_new ? m_new : 1);
-  } catch (...) {
-    destroy_graph(r);
-    throw;
-  }
-  // compact present deletions / fresh insertions
-  uint64_t* dp = ctx->stage_d.as<uint64_t>(ndu + 1);
-  uint64_t* nw = ctx->stage_f.as<uint64_t>(niu + 1);
-  auto* nsel = reinterpret_cast<unsigned long long*>(ctx->scratch64a.as<unsigned long long>(2));
-  uint64_t ndp = 0, nnw = 0;
-  if (ndu) {
-    if (du == dp) {  // sort_unique left the result in stage_d: move it aside
-      DYNPR_CK(cudaMemcpyAsync(dk, du, ndu * 8, cudaMemcpyDeviceToDevice, st));
-      du = dk;
-    }
-    cub_call(ctx, [&](void* t, size_t& b) {
-      return cub::DeviceSelect::Flagged(t, b, du, found, dp, nsel, (int64_t)ndu, st);
-    });
-    ndp = read_u64(ctx, nsel);
-  }
-  if (niu) {
-    if (iu == nw) {
-      DYNPR_CK(cudaMemcpyAsync(ik, iu, niu * 8, cudaMemcpyDeviceToDevice, st));
-      iu = ik;
-    }
-    cub_call(ctx, [&](void* t, size_t& b) {
-      return cub::DeviceSelect::Flagged(t, b, iu, fresh, nw, nsel + 1, (int64_t)niu, st);
-    });
-    nnw = read_u64(ctx, nsel + 1);
-  }
-  // copies of the untouched rows + chunked merge of the touched ones
-  if (n) {
-    uint32_t* istart = ctx->scratch32b.as<uint32_t>((uint64_t)n + 1);
-    k_merge_items<<<grid_for((uint64_t)n + 1, 256, 1 << 16), 256, 0, st>>>(touched, g->off, n, istart);
-    check_launch();
-    cub_call(ctx, [&](void* t, size_t& b) {
-      return cub::DeviceScan::ExclusiveSum(t, b, istart, istart, (int64_t)n + 1, st);
-    });
-    // touched rows in order -> runs of untouched rows -> pieces -> copies
-    auto* nt = reinterpret_cast<unsigned long long*>(ctx->scratch64a.as<unsigned long long>(4)) + 2;
-    uint32_t* T = copy_untouched_rows(ctx, touched, n, g->off, g->tgt, r->off, r->tgt, nt);
-    k_merge_touched<<<(unsigned)ctx->num_sms * 16, 256, 0, st>>>(istart, n, g->off, g->tgt, r->off, r->tgt, dp,
-                                                                 ndp, nw, nnw, sb, mask, need);
-    check_launch();
-    count_launch(ctx, 3);
-    if (rows_out) {  // the touched rows, for an incremental engine layout (layout.cu)
-      const uint64_t cnt = read_u64(ctx, nt);
-      uint32_t* rows = pool_alloc_n<uint32_t>(ctx, cnt ? cnt : 1);
-      if (cnt) DYNPR_CK(cudaMemcpyAsync(rows, T, cnt * 4, cudaMemcpyDeviceToDevice, st));
-      *rows_out = rows;
-      *nrows_out = cnt;
-    }
-  }
-  unsigned long long hc[2];
-  DYNPR_CK(cudaMemcpyAsync(ctx->pinned, counters, 16, cudaMemcpyDeviceToHost, st));
-  sync(ctx);
-  std::memcpy(hc, ctx->pinned, 16);
-  missing += hc[0];
-  duplicate += hc[1];
-  r->all_loops = true;
-  if (missing_out) *missing_out += missing;
-  if (duplicate_out) *duplicate_out += duplicate;
-  *out = r;
 }
+
 
 }  // namespace dynpr_b200
 
@@ -986,15 +1183,12 @@ dynpr_status dynpr_graph_transpose(dynpr_context* ctx, const dynpr_graph* g, dyn
         k_expand_sources<<<grid_for((uint64_t)n * 32, 256, 1 << 16), 256, 0, st>>>(g->off, n, vals);
         check_launch();
         count_launch(ctx);
-        cub::DoubleBuffer<uint32_t> kb(keys, keys2);
-        cub::DoubleBuffer<uint32_t> vb(vals, t->tgt);
         const int eb = key_shift(n);
-        cub_call(ctx, [&](void* tmp, size_t& b) {
-          return cub::DeviceRadixSort::SortPairs(tmp, b, kb, vb, m, 0, eb, st);
-        });
-        if (vb.Current() != t->tgt)
-          DYNPR_CK(cudaMemcpyAsync(t->tgt, vb.Current(), m * 4, cudaMemcpyDeviceToDevice, st));
-        k_offsets_from_keys32<<<grid_for(m + 1, 256, 1 << 16), 256, 0, st>>>(kb.Current(), m, n, t->off);
+        uint32_t* vsorted = nullptr;
+        uint32_t* ksorted = prims::radix_sort<uint32_t, uint32_t>(ctx, keys, keys2, vals, t->tgt, m, 0, eb, st,
+                                                                  &vsorted);
+        if (vsorted != t->tgt) DYNPR_CK(cudaMemcpyAsync(t->tgt, vsorted, m * 4, cudaMemcpyDeviceToDevice, st));
+        k_offsets_from_keys32<<<grid_for(m + 1, 256, 1 << 16), 256, 0, st>>>(ksorted, m, n, t->off);
       } else {
         k_offsets_from_keys32<<<1, 256, 0, st>>>(keys, 0, n, t->off);
       }
@@ -1034,26 +1228,35 @@ static dynpr_status apply_batch_common(dynpr_context* ctx, const dynpr_graph* gF
       seed->ctx = ctx;
       seed->parent = gT->layout;
     }
-    dynpr_graph* f = nullptr;
-    graph_apply_batch_impl(ctx, gF, d_ds, d_dd, nd, d_is, d_id, ni, true, hd ? ds : nullptr,
-                           hd ? dd : nullptr, hi ? is : nullptr, hi ? id : nullptr, &f, missing,
-                           duplicate, seed ? &seed->rows_F : nullptr, seed ? &seed->n_F : nullptr);
+    // forward + transpose (reversed batch, ids validated through the
+    // forward): both phase A's, one host wait, both phase B's
+    const int cnt = gT ? 2 : 1;
+    const dynpr_graph* gs[2] = {gF, gT};
+    const uint32_t* ls[2] = {d_ds, d_dd};
+    const uint32_t* ld[2] = {d_dd, d_ds};
+    const uint32_t* lis[2] = {d_is, d_id};
+    const uint32_t* lid[2] = {d_id, d_is};
+    dynpr_graph* outs[2] = {nullptr, nullptr};
+    uint32_t* rows[2] = {nullptr, nullptr};
+    uint64_t nrows[2] = {0, 0};
+    graph_apply_batch_multi(ctx, cnt, gs, ls, ld, nd, lis, lid, ni, true, hd ? ds : nullptr, hd ? dd : nullptr,
+                            hi ? is : nullptr, hi ? id : nullptr, outs, missing, duplicate, seed ? rows : nullptr,
+                            seed ? nrows : nullptr);
+    sync(ctx);  // calls are synchronous on return (the C-ABI contract)
+    dynpr_graph* f = outs[0];
     if (gT) {
-      dynpr_graph* t = nullptr;
-      try {
-        // reversed batch on the transpose (ids already validated)
-        graph_apply_batch_impl(ctx, gT, d_dd, d_ds, nd, d_id, d_is, ni, false, nullptr, nullptr,
-                               nullptr, nullptr, &t, nullptr, nullptr, seed ? &seed->rows_T : nullptr,
-                               seed ? &seed->n_T : nullptr);
-      } catch (...) {
-        destroy_graph(f);
-        throw;
-      }
+      dynpr_graph* t = outs[1];
       if (seed) {
+        seed->rows_F = rows[0];
+        seed->n_F = nrows[0];
+        seed->rows_T = rows[1];
+        seed->n_T = nrows[1];
         seed->gF_id = f->id;
         t->seed = std::move(seed);
       }
       *outT = t;
+    } else if (seed) {
+      pool_free(ctx, rows[0]);
     }
     *outF = f;
   });

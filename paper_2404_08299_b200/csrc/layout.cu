@@ -1,22 +1,13 @@
 // Builder of the engine layout (see layout.cuh): degree sort, relabelling,
 // SELL-32 segment slices, relabelled forward CSR.
-#include <cub/cub.cuh>
-
 #include "comm.cuh"
 #include "layout.cuh"
+#include "prims.cuh"
 #include "sweep.cuh"
 
 namespace dynpr_b200 {
 
 namespace {
-
-template <class F>
-void cub_call(dynpr_context* ctx, F&& f) {
-  size_t bytes = 0;
-  DYNPR_CK(f(nullptr, bytes));
-  void* tmp = ctx->cub_tmp.ensure(bytes);
-  DYNPR_CK(f(tmp, bytes));
-}
 
 // Layout arrays come from the building context's pool (explicit, so
 // contexts building layouts concurrently on several host threads never
@@ -89,15 +80,20 @@ __global__ void k_multi_slice_len(const uint32_t* mseg_len, uint64_t nseg, uint6
 }
 // One lane's segment into SELL-32x4: 4 consecutive elements per 16-byte
 // store, so each warp store covers 512 contiguous bytes.
+// 16 elements per round: the 16 source loads, then the 16 relabel gathers,
+// are independent (one round trip each instead of one per element pair)
 __device__ __forceinline__ void fill_lane(uint32_t* sell, uint64_t base, unsigned lane, uint32_t L, uint32_t len,
                                           const uint32_t* src, const uint32_t* inv) {
-  for (uint32_t k = 0; k < L; k += 4) {
-    uint4 w;
-    w.x = k < len ? inv[src[k]] : 0u;
-    w.y = k + 1 < len ? inv[src[k + 1]] : 0u;
-    w.z = k + 2 < len ? inv[src[k + 2]] : 0u;
-    w.w = k + 3 < len ? inv[src[k + 3]] : 0u;
-    *reinterpret_cast<uint4*>(sell + sell_pos(base, lane, k)) = w;
+  for (uint32_t k = 0; k < L; k += 16) {
+    uint32_t x[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) x[q] = k + q < len ? src[k + q] : 0u;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) x[q] = k + q < len ? inv[x[q]] : 0u;
+#pragma unroll
+    for (int q = 0; q < 16; q += 4)
+      if (k + q < L) *reinterpret_cast<uint4*>(sell + sell_pos(base, lane, k + q)) =
+          make_uint4(x[q], x[q + 1], x[q + 2], x[q + 3]);
   }
 }
 
@@ -322,28 +318,64 @@ __global__ void k_mbase_append(uint64_t* mbase, uint64_t s0, uint64_t cnt, uint6
 // relabelled forward CSR, touched rows (the untouched ones are copied as
 // runs, graph.cu copy_untouched_rows): rows cut into 4K-element items so a
 // touched hub spreads over many warps; item t -> row by binary search of the
-// items' exclusive scan
+// items' exclusive scan.  rows: old ids of the touched forward rows.
 constexpr uint64_t kRowItem = 4096;
-__global__ void k_row_items(const uint32_t* rows, const unsigned long long* cnt, const uint32_t* deg,
-                            uint32_t* items) {
-  const uint64_t c = *cnt;
-  GRID_STRIDE(i, c + 1) items[i] = i < c ? (uint32_t)((deg[rows[i]] + kRowItem - 1) / kRowItem) : 0u;
-}
-__global__ void k_refill_rows(const uint32_t* rows, const unsigned long long* cnt, const uint32_t* istart,
-                              const uint64_t* offF, const uint32_t* tgtF, const uint32_t* perm, const uint32_t* inv,
-                              const uint64_t* noff, uint32_t* ntgt) {
-  const uint64_t c = *cnt;
+struct RowWords {  // new out-degree of touched row j (0 past the list)
+  const uint32_t* rows;
+  const uint32_t* inv;
+  const uint32_t* outdeg;
+  uint64_t c;
+  __device__ __forceinline__ unsigned long long operator()(uint64_t j) const {
+    return j < c ? (unsigned long long)outdeg[inv[rows[j]]] : 0ull;
+  }
+};
+struct RowChunks {
+  const uint32_t* rows;
+  const uint32_t* inv;
+  const uint32_t* outdeg;
+  uint64_t c;
+  __device__ __forceinline__ uint32_t operator()(uint64_t j) const {
+    return j < c ? (uint32_t)((outdeg[inv[rows[j]]] + kRowItem - 1) / kRowItem) : 0u;
+  }
+};
+// Touched row j (old id u, new id w) rewritten into the new block at
+// wpos[j]: relabelled targets of the new forward graph's row u; the first
+// item of the row re-points begF[w] (blk_rel: the block's offset from the
+// shared base).
+__global__ void k_refill_rows(const uint32_t* rows, uint64_t c, const uint32_t* istart, const unsigned long long* wpos,
+                              const uint64_t* offF, const uint32_t* tgtF, const uint32_t* inv, uint64_t blk_rel,
+                              const uint32_t* base, uint64_t* begF, uint32_t* blk) {
   const uint32_t total = istart[c];
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / 32;
   const unsigned lane = threadIdx.x & 31;
   const uint64_t nw = (uint64_t)gridDim.x * blockDim.x / 32;
+  (void)base;
   for (uint64_t t = warp; t < total; t += nw) {
     const uint64_t j = upper_bound_u32(istart, c + 1, (uint32_t)t) - 1;
-    const uint32_t w = rows[j];
-    const uint64_t len = noff[w + 1] - noff[w];
+    const uint32_t u = rows[j], w = inv[u];
+    const uint64_t len = offF[u + 1] - offF[u];
     const uint64_t k0 = (t - istart[j]) * kRowItem, k1 = k0 + kRowItem < len ? k0 + kRowItem : len;
-    const uint32_t* src = tgtF + offF[perm[w]];
-    for (uint64_t k = k0 + lane; k < k1; k += 32) ntgt[noff[w] + k] = inv[src[k]];
+    const uint32_t* src = tgtF + offF[u];
+    uint32_t* dst = blk + wpos[j];
+    if (k0 == 0 && lane == 0) begF[w] = blk_rel + wpos[j];
+    for (uint64_t kb = k0; kb < k1; kb += 32 * 8) {  // 8 loads, then 8 gathers, in flight per lane
+      uint32_t x[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint64_t k = kb + 32 * q + lane;
+        x[q] = k < k1 ? src[k] : 0u;
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint64_t k = kb + 32 * q + lane;
+        if (k < k1) x[q] = inv[x[q]];
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint64_t k = kb + 32 * q + lane;
+        if (k < k1) dst[k] = x[q];
+      }
+    }
   }
 }
 
@@ -357,17 +389,19 @@ uint64_t read_u64(dynpr_context* ctx, const void* d) {
   return h;
 }
 
+// The relabelled forward graph of a full build: CSR order, so begF is the
+// exclusive scan of the out-degrees (n + 1 entries); its target array is a
+// shared block that derived layouts keep reading (copy-on-write rows).
 void build_forward(dynpr_context* ctx, Layout* L, const dynpr_graph* gF) {
   cudaStream_t st = ctx->stream;
-  L->offF = dalloc<uint64_t>(ctx, (uint64_t)L->n + 1);
-  L->tgtF = dalloc<uint32_t>(ctx, L->m);
-  k_outdeg64<<<grid(ctx, (uint64_t)L->n + 1), 256, 0, st>>>(L->outdeg, L->n, L->offF);
+  L->begF = dalloc<uint64_t>(ctx, (uint64_t)L->n + 1);
+  L->tgtF = new_block(ctx, L, L->m);
+  L->fwd_words = L->m;
+  k_outdeg64<<<grid(ctx, (uint64_t)L->n + 1), 256, 0, st>>>(L->outdeg, L->n, L->begF);
   check_launch();
-  cub_call(ctx, [&](void* t, size_t& b) {
-    return cub::DeviceScan::ExclusiveSum(t, b, L->offF, L->offF, (int64_t)L->n + 1, st);
-  });
+  prims::scan_array(ctx, L->begF, L->begF, (uint64_t)L->n + 1, st);
   k_fill_forward<<<grid(ctx, (L->m + kFillChunk - 1) / kFillChunk * 32), 256, 0, st>>>(
-      gF->off, gF->tgt, L->perm, L->inv, L->n, L->offF, L->tgtF);
+      gF->off, gF->tgt, L->perm, L->inv, L->n, L->begF, L->tgtF);
   check_launch();
   count_launch(ctx, 2);
   L->has_forward = true;
@@ -384,8 +418,10 @@ Layout* build_layout(dynpr_context* ctx, const dynpr_graph* gT, const dynpr_grap
     L->m = gT->m;
     L->T = T;
     L->gF_id = gF->id;
-    L->perm = dalloc<uint32_t>(ctx, n);
-    L->inv = dalloc<uint32_t>(ctx, n);
+    L->loops = gT->all_loops;
+    // the relabelling: shared blocks (derived layouts keep the order)
+    L->perm = new_block(ctx, L, n);
+    L->inv = new_block(ctx, L, n);
     L->indeg = dalloc<uint32_t>(ctx, n);
     L->outdeg = dalloc<uint32_t>(ctx, n);
     // temporaries from the pool (the context's stage buffers may hold the
@@ -403,20 +439,17 @@ Layout* build_layout(dynpr_context* ctx, const dynpr_graph* gT, const dynpr_grap
     check_launch();
     // max in-degree -> descending sort keys
     auto* mx = reinterpret_cast<uint32_t*>(ctx->scratch64a.as<unsigned long long>(2));
-    cub_call(ctx, [&](void* t, size_t& b) { return cub::DeviceReduce::Max(t, b, indeg_old, mx, (int64_t)n, st); });
+    prims::reduce_max_u32(ctx, indeg_old, n, mx, st);
     const uint32_t maxdeg = (uint32_t)(read_u64(ctx, mx) & 0xffffffffu);
     k_desc_keys<<<grid(ctx, n), 256, 0, st>>>(indeg_old, n, maxdeg, keys);
     check_launch();
     count_launch(ctx, 2);
     const int eb = bits_for(maxdeg);
     if (eb > 0) {
-      cub::DoubleBuffer<uint32_t> kb(keys, keys2);
-      cub::DoubleBuffer<uint32_t> vb(iota, L->perm);
-      cub_call(ctx, [&](void* t, size_t& b) {
-        return cub::DeviceRadixSort::SortPairs(t, b, kb, vb, (int64_t)n, 0, eb, st);
-      });
-      if (vb.Current() != L->perm)
-        DYNPR_CK(cudaMemcpyAsync(L->perm, vb.Current(), (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
+      uint32_t* vsorted = nullptr;
+      prims::radix_sort<uint32_t, uint32_t>(ctx, keys, keys2, iota, L->perm, n, 0, eb, st, &vsorted);
+      if (vsorted != L->perm)
+        DYNPR_CK(cudaMemcpyAsync(L->perm, vsorted, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
     } else {
       DYNPR_CK(cudaMemcpyAsync(L->perm, iota, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
     }
@@ -446,16 +479,12 @@ Layout* build_layout(dynpr_context* ctx, const dynpr_graph* gT, const dynpr_grap
     L->sbase = dalloc<uint64_t>(ctx, L->n_sslices + 1);
     k_single_slice_len<<<grid(ctx, L->n_sslices + 1), 256, 0, st>>>(L->indeg, M, n, L->n_sslices, L->sbase);
     check_launch();
-    cub_call(ctx, [&](void* t, size_t& b) {
-      return cub::DeviceScan::ExclusiveSum(t, b, L->sbase, L->sbase, (int64_t)L->n_sslices + 1, st);
-    });
+    prims::scan_array(ctx, L->sbase, L->sbase, (uint64_t)L->n_sslices + 1, st);
     // multi region segments
     L->pbase = dalloc<uint32_t>(ctx, (uint64_t)M + 1);
     k_multi_nch<<<grid(ctx, (uint64_t)M + 1), 256, 0, st>>>(L->indeg, M, L->pbase);
     check_launch();
-    cub_call(ctx, [&](void* t, size_t& b) {
-      return cub::DeviceScan::ExclusiveSum(t, b, L->pbase, L->pbase, (int64_t)M + 1, st);
-    });
+    prims::scan_array(ctx, L->pbase, L->pbase, (uint64_t)M + 1, st);
     {
       uint32_t h = 0;  // pbase is uint32: read exactly 4 bytes
       DYNPR_CK(cudaMemcpyAsync(ctx->pinned, L->pbase + M, 4, cudaMemcpyDeviceToHost, st));
@@ -474,9 +503,7 @@ Layout* build_layout(dynpr_context* ctx, const dynpr_graph* gT, const dynpr_grap
     k_multi_slice_len<<<grid(ctx, (L->n_mslices + 1) * 32), 256, 0, st>>>(L->mseg_len, L->n_mseg, L->n_mslices,
                                                                           L->mbase);
     check_launch();
-    cub_call(ctx, [&](void* t, size_t& b) {
-      return cub::DeviceScan::ExclusiveSum(t, b, L->mbase, L->mbase, (int64_t)L->n_mslices + 1, st);
-    });
+    prims::scan_array(ctx, L->mbase, L->mbase, (uint64_t)L->n_mslices + 1, st);
     // the slices this context sweeps: all of them, or on a team context
     // the rank's edge-balanced range (its in-CSR rows only)
     uint64_t ss_lo = 0, ss_hi = L->n_sslices, ms_lo = 0, ms_hi = L->n_mslices;
@@ -542,15 +569,15 @@ Layout* build_incremental(dynpr_context* ctx, const dynpr_graph* gT, const dynpr
     L->m = gT->m;
     L->T = T;
     L->gF_id = gF->id;
+    L->loops = gT->all_loops;
     L->M = M;
     L->generation = P->generation + 1;
     L->n_hslices = P->n_hslices;  // scheduling hint only
-    L->perm = dalloc<uint32_t>(ctx, n);
-    L->inv = dalloc<uint32_t>(ctx, n);
+    L->blocks = P->blocks;  // shared relabelling, slices and forward rows (copy-on-write)
+    L->perm = P->perm;
+    L->inv = P->inv;
     L->indeg = dalloc<uint32_t>(ctx, n);
     L->outdeg = dalloc<uint32_t>(ctx, n);
-    DYNPR_CK(cudaMemcpyAsync(L->perm, P->perm, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
-    DYNPR_CK(cudaMemcpyAsync(L->inv, P->inv, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
     DYNPR_CK(cudaMemcpyAsync(L->indeg, P->indeg, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
     DYNPR_CK(cudaMemcpyAsync(L->outdeg, P->outdeg, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
     // touched rows in the relabelled space, in-lists (T) and out-lists (F),
@@ -566,7 +593,6 @@ Layout* build_incremental(dynpr_context* ctx, const dynpr_graph* gT, const dynpr
     count_launch(ctx, 2);
     L->mcount = dalloc<uint32_t>(ctx, (uint64_t)M + 1);
     DYNPR_CK(cudaMemsetAsync(L->mcount, 0, ((size_t)M + 1) * 4, st));
-    L->blocks = P->blocks;  // shared slices (copy-on-write)
     L->sell_s = P->sell_s;
     L->sell_m = P->sell_m;
     // single region: re-built slices into a new block
@@ -577,7 +603,7 @@ Layout* build_incremental(dynpr_context* ctx, const dynpr_graph* gT, const dynpr
     uint64_t* dpos = len32 + S + 1;
     k_slice_touched_len<<<grid(ctx, (S + 1) * 32), 256, 0, st>>>(L->indeg, flagT, M, n, S, len32);
     check_launch();
-    cub_call(ctx, [&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, len32, dpos, (int64_t)S + 1, st); });
+    prims::scan_array<uint64_t>(ctx, len32, dpos, S + 1, st);
     const uint64_t s_new = read_u64(ctx, dpos + S);
     uint32_t* ds = new_block(ctx, L, s_new);
     k_sbase_cow<<<grid(ctx, S + 1), 256, 0, st>>>(P->sbase, len32, dpos, S, rel_words(L->sell_s, ds), L->sbase);
@@ -592,7 +618,7 @@ Layout* build_incremental(dynpr_context* ctx, const dynpr_graph* gT, const dynpr
     uint32_t* apos = ctx->scratch32a.as<uint32_t>((uint64_t)M + 2);
     k_multi_touched_nch<<<grid(ctx, (uint64_t)M + 1), 256, 0, st>>>(L->indeg, flagT, M, apos);
     check_launch();
-    cub_call(ctx, [&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, apos, apos, (int64_t)M + 1, st); });
+    prims::scan_array(ctx, apos, apos, (uint64_t)M + 1, st);
     uint64_t appended = 0, retired = 0;
     {
       uint32_t h = 0;
@@ -628,9 +654,7 @@ Layout* build_incremental(dynpr_context* ctx, const dynpr_graph* gT, const dynpr
       k_multi_slice_len<<<grid(ctx, (s_hi - s_lo + 1) * 32), 256, 0, st>>>(L->mseg_len + first, appended,
                                                                            s_hi - s_lo, L->mbase + s_lo);
       check_launch();
-      cub_call(ctx, [&](void* t, size_t& b) {
-        return cub::DeviceScan::ExclusiveSum(t, b, L->mbase + s_lo, L->mbase + s_lo, (int64_t)(s_hi - s_lo) + 1, st);
-      });
+      prims::scan_array(ctx, L->mbase + s_lo, L->mbase + s_lo, (uint64_t)(s_hi - s_lo) + 1, st);
       const uint64_t m_new = read_u64(ctx, L->mbase + s_hi);
       uint32_t* dm = new_block(ctx, L, m_new);
       k_mbase_append<<<grid(ctx, s_hi - s_lo + 1), 256, 0, st>>>(L->mbase, s_lo, s_hi - s_lo, rel_words(L->sell_m, dm));
@@ -658,25 +682,28 @@ Layout* build_incremental(dynpr_context* ctx, const dynpr_graph* gT, const dynpr
       return nullptr;
     }
     if (P->has_forward) {
-      L->offF = dalloc<uint64_t>(ctx, (uint64_t)n + 1);
-      L->tgtF = dalloc<uint32_t>(ctx, L->m);
-      k_outdeg64<<<grid(ctx, (uint64_t)n + 1), 256, 0, st>>>(L->outdeg, n, L->offF);
-      check_launch();
-      cub_call(ctx, [&](void* t, size_t& b) {
-        return cub::DeviceScan::ExclusiveSum(t, b, L->offF, L->offF, (int64_t)n + 1, st);
-      });
-      auto* cnt = reinterpret_cast<unsigned long long*>(ctx->scratch64a.as<unsigned long long>(4)) + 3;
-      const uint32_t* rows = copy_untouched_rows(ctx, flagF, n, P->offF, P->tgtF, L->offF, L->tgtF, cnt);
-      uint32_t* items = ctx->scratch32a.as<uint32_t>(seed.n_F + 2);
-      k_row_items<<<grid(ctx, seed.n_F + 1), 256, 0, st>>>(rows, cnt, L->outdeg, items);
-      check_launch();
-      cub_call(ctx, [&](void* t, size_t& b) {
-        return cub::DeviceScan::ExclusiveSum(t, b, items, items, (int64_t)seed.n_F + 1, st);
-      });
-      k_refill_rows<<<(unsigned)ctx->num_sms * 16, 256, 0, st>>>(rows, cnt, items, gF->off, gF->tgt, L->perm, L->inv,
-                                                                 L->offF, L->tgtF);
-      check_launch();
-      count_launch(ctx, 3);
+      // copy-on-write forward rows: untouched rows keep their words in the
+      // parent's blocks, the touched ones (batch sources) are rewritten into
+      // one new block; begF is the parent's with those rows re-pointed
+      L->tgtF = P->tgtF;
+      L->begF = dalloc<uint64_t>(ctx, (uint64_t)n + 1);
+      DYNPR_CK(cudaMemcpyAsync(L->begF, P->begF, ((size_t)n + 1) * 8, cudaMemcpyDeviceToDevice, st));
+      const uint64_t c = seed.n_F;
+      uint64_t words = 0;
+      if (c) {
+        auto* wpos = ctx->scratch64b.as<unsigned long long>(c + 1);
+        uint32_t* items = ctx->scratch32a.as<uint32_t>(c + 2);
+        prims::scan_exclusive<unsigned long long>(ctx, RowWords{seed.rows_F, L->inv, L->outdeg, c}, wpos, c + 1, st);
+        words = read_u64(ctx, wpos + c);
+        uint32_t* blk = new_block(ctx, L, words);
+        prims::scan_exclusive<uint32_t>(ctx, RowChunks{seed.rows_F, L->inv, L->outdeg, c}, items, c + 1, st);
+        k_refill_rows<<<(unsigned)ctx->num_sms * 16, 256, 0, st>>>(seed.rows_F, c, items, wpos, gF->off, gF->tgt,
+                                                                   L->inv, rel_words(L->tgtF, blk), L->tgtF,
+                                                                   L->begF, blk);
+        check_launch();
+        count_launch(ctx);
+      }
+      L->fwd_words = P->fwd_words + words;
       L->has_forward = true;
     }
   } catch (...) {
@@ -688,8 +715,9 @@ Layout* build_incremental(dynpr_context* ctx, const dynpr_graph* gT, const dynpr
 }  // namespace
 
 Layout::~Layout() {
-  for (void* p : {(void*)perm, (void*)inv, (void*)indeg, (void*)outdeg, (void*)sbase, (void*)mbase,
-                  (void*)mseg_v, (void*)mseg_len, (void*)pbase, (void*)mcount, (void*)offF, (void*)tgtF})
+  // (perm, inv, the SELL storage and the forward rows are shared blocks)
+  for (void* p : {(void*)indeg, (void*)outdeg, (void*)sbase, (void*)mbase, (void*)mseg_v, (void*)mseg_len,
+                  (void*)pbase, (void*)mcount, (void*)begF})
     pool_free(ctx, p);
 }
 

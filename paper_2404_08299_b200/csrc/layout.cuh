@@ -19,7 +19,8 @@
 //    loads and every lane sums its own segment in order -- the reference's
 //    accumulation order, bit for bit, with no shared-memory staging.
 //  * For the frontier engines the forward graph is also relabelled (rows and
-//    columns) for push expansion in new-id space.
+//    columns) for push expansion in new-id space; derived snapshots share
+//    its untouched rows copy-on-write.
 #pragma once
 
 #include "common.cuh"
@@ -57,6 +58,7 @@ struct Layout {
   uint32_t* indeg = nullptr;   // new order
   uint32_t* outdeg = nullptr;  // new order
   uint32_t M = 0;              // multi-segment vertices are [0, M)
+  bool loops = false;          // every in-list holds its own vertex (gT carries all self-loops)
   // single-segment region: vertices [M, n), slice s = vertices M+32s..+31
   uint64_t n_sslices = 0;
   uint64_t n_hslices = 0;      // leading single slices with in-degree > kHeavyDeg
@@ -86,10 +88,16 @@ struct Layout {
   uint64_t sell_words = 0;  // SELL words held on this rank (both regions, incl. shared)
   uint64_t dead_segs = 0;   // multi-region segments retired by derivations (len 0)
   uint32_t* mcount = nullptr;  // per multi vertex: chunks finished this sweep (0 between sweeps)
-  // relabelled forward CSR (frontier engines)
+  // relabelled forward graph (frontier engines): row v = outdeg[v] words at
+  // tgtF + begF[v] (a 64-bit word offset from the shared base, wrapping when
+  // a derived layout's block sits below it).  A full build stores the rows in
+  // CSR order (begF = exclusive scan of outdeg, n + 1 entries); a derived
+  // layout re-points only the rows the batch touched (copy-on-write, the
+  // blocks held in `blocks`)
   bool has_forward = false;
-  uint64_t* offF = nullptr;
+  uint64_t* begF = nullptr;
   uint32_t* tgtF = nullptr;
+  uint64_t fwd_words = 0;  // forward words allocated along this layout's chain
   double build_ms = 0.0;       // device time of the last (re)build
   // multi-GPU partition cache (sweep.cu plan_ranges)
   int plan_world = 0;

@@ -42,9 +42,7 @@
 #include <string>
 #include <utility>
 
-#include <cub/device/device_scan.cuh>
-#include <cub/iterator/transform_input_iterator.cuh>
-
+#include "prims.cuh"
 #include "sweep.cuh"
 
 namespace dynpr_b200 {
@@ -343,7 +341,12 @@ __device__ __forceinline__ void b_sweep_single(const SweepArgs& a) {
     }
     double c = 0.0;
     unsigned neg = 0;
-    if (Lw) {
+    if (Lw == 1 && a.loops) {  // self-loops only: 0.0 + |cself| (rank.cpp:45-54)
+      if (len) {
+        c = fabs(cself);
+        neg = (unsigned)__double2hiint(cself) >> 31;
+      }
+    } else if (Lw) {
       if (pull)
         c = segment_sum<true>(a.sell_s, a.sbase[s], lane, len, Lw, a.contrib_prev, v, cself, folds(a, len), &neg);
       else
@@ -653,7 +656,12 @@ __device__ __forceinline__ void single_slice(const SweepArgs& a, uint64_t s, uns
   }
   double c = 0.0;
   unsigned neg = 0;
-  if (Lw) {
+  if (Lw == 1 && a.loops) {  // self-loops only (see b_sweep_single)
+    if (len) {
+      c = fabs(cself);
+      neg = (unsigned)__double2hiint(cself) >> 31;
+    }
+  } else if (Lw) {
     if (FLAGGED && pull)
       c = segment_sum_deep<Q, true>(a.sell_s, a.sbase[s], lane, len, Lw, a.contrib_prev, v, cself, folds(a, len),
                                     &neg);
@@ -957,11 +965,13 @@ __global__ void __launch_bounds__(kThreads) k_part_scatter(const uint64_t* off, 
 }
 
 // ---- init / frontier kernels -------------------------------------------------
-__global__ void k_init_ranks(const uint32_t* outdeg, uint32_t n, const double* init, double uniform, double* r0,
-                             double* r1, double* c0, double* c1) {
+// init: the previous ranks in old-id order (gathered through perm), or null
+// for uniform; r1 / c1 may be null when the first sweep writes every vertex.
+__global__ void k_init_ranks(const uint32_t* outdeg, const uint32_t* perm, uint32_t n, const double* init,
+                             double uniform, double* r0, double* r1, double* c0, double* c1) {
   for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
        v += (uint64_t)gridDim.x * blockDim.x) {
-    const double r = init ? init[v] : uniform;
+    const double r = init ? init[perm[v]] : uniform;
     const double c = __ddiv_rn(r, (double)outdeg[v]);
     r0[v] = r;
     if (r1) r1[v] = r;
@@ -1011,32 +1021,32 @@ __global__ void k_collect_pending(const uint32_t* outdeg, const uint64_t* off, u
 // are idempotent; the read-before-write keeps dense frontiers
 // from turning into L2 write traffic.  (An 8-deep variant with more loads in
 // flight per thread was measured slower: profiles/r01/README.md.)
-__device__ __forceinline__ void expand_low_body(const uint64_t* off, const uint32_t* tgt, const uint32_t* list,
-                                                uint64_t cnt, uint8_t* va) {
+__device__ __forceinline__ void expand_low_body(Rows rows, const uint32_t* list, uint64_t cnt, uint8_t* va) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cnt;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t u = list[i];
-    const uint64_t b = off[u], e = off[u + 1];
-    for (uint64_t k = b; k < e; ++k) {
-      const uint32_t w = tgt[k];
+    const uint32_t* r = rows.row(u);
+    const uint64_t len = rows.len(u);
+    for (uint64_t k = 0; k < len; ++k) {
+      const uint32_t w = r[k];
       if (!va[w]) va[w] = 1;
     }
   }
 }
-__device__ __forceinline__ void expand_high_body(const uint64_t* off, const uint32_t* tgt, const uint2* items,
-                                                 uint64_t cnt, uint8_t* va) {
+__device__ __forceinline__ void expand_high_body(Rows rows, const uint2* items, uint64_t cnt, uint8_t* va) {
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / 32;
   const uint64_t nw = (uint64_t)gridDim.x * blockDim.x / 32;
   const unsigned lane = lane_id();
   for (uint64_t i = warp; i < cnt; i += nw) {
     const uint2 it = items[i];
-    const uint64_t b = off[it.x] + (uint64_t)kExpandChunk * it.y;
-    const uint64_t e0 = off[it.x + 1];
-    const uint64_t e = b + kExpandChunk < e0 ? b + kExpandChunk : e0;
+    const uint32_t* r = rows.row(it.x);
+    const uint64_t len = rows.len(it.x);
+    const uint64_t b = (uint64_t)kExpandChunk * it.y;
+    const uint64_t e = b + kExpandChunk < len ? b + kExpandChunk : len;
     for (uint64_t k = b + lane; k < e; k += 32 * 4) {
       uint32_t w[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) w[q] = k + 32 * q < e ? tgt[k + 32 * q] : 0xffffffffu;
+      for (int q = 0; q < 4; ++q) w[q] = k + 32 * q < e ? r[k + 32 * q] : 0xffffffffu;
       uint8_t f[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) f[q] = w[q] != 0xffffffffu ? va[w[q]] : 1;
@@ -1046,28 +1056,28 @@ __device__ __forceinline__ void expand_high_body(const uint64_t* off, const uint
     }
   }
 }
-__global__ void k_expand_low(const uint64_t* off, const uint32_t* tgt, const uint32_t* list, uint32_t cnt,
-                             uint8_t* va, const unsigned* dcnt, const int* gate) {
+__global__ void k_expand_low(Rows rows, const uint32_t* list, uint32_t cnt, uint8_t* va, const unsigned* dcnt,
+                             const int* gate) {
   if (gate && *gate != kExpandPush) return;
-  expand_low_body(off, tgt, list, dcnt ? dcnt[0] : cnt, va);
+  expand_low_body(rows, list, dcnt ? dcnt[0] : cnt, va);
 }
-__global__ void k_expand_high(const uint64_t* off, const uint32_t* tgt, const uint2* items, uint32_t cnt,
-                              uint8_t* va, const unsigned* dcnt, const int* gate) {
+__global__ void k_expand_high(Rows rows, const uint2* items, uint32_t cnt, uint8_t* va, const unsigned* dcnt,
+                              const int* gate) {
   if (gate && *gate != kExpandPush) return;
-  expand_high_body(off, tgt, items, dcnt ? dcnt[1] : cnt, va);
+  expand_high_body(rows, items, dcnt ? dcnt[1] : cnt, va);
 }
 // device-loop variants: arguments from the constant-bank slot of half H
 template <int H>
 __global__ void k_expand_low_c(const unsigned* counts, const int* gate) {
   const SweepArgs* ap = &c_loop_args[H];
   if (gate && *gate != kExpandPush) return;
-  expand_low_body(ap->offF, ap->tgtF, ap->pend_low, counts[0], ap->va);
+  expand_low_body(Rows{ap->begF, ap->outdeg, ap->tgtF}, ap->pend_low, counts[0], ap->va);
 }
 template <int H>
 __global__ void k_expand_high_c(const unsigned* counts, const int* gate) {
   const SweepArgs* ap = &c_loop_args[H];
   if (gate && *gate != kExpandPush) return;
-  expand_high_body(ap->offF, ap->tgtF, ap->pend_high, counts[1], ap->va);
+  expand_high_body(Rows{ap->begF, ap->outdeg, ap->tgtF}, ap->pend_high, counts[1], ap->va);
 }
 
 // ---- device-driven loop bookkeeping (engine.cpp:71-92) --------------------------------
@@ -1148,12 +1158,12 @@ __device__ __forceinline__ void warp_push_items(bool take, uint32_t w, uint32_t 
     for (unsigned j = 0, b = base + incl - items; j < items; ++j) out[b + j] = make_uint2(w, j);
 }
 
-__device__ __forceinline__ uint32_t bfs_items(const uint64_t* off, uint32_t w) {
-  const uint64_t d = off[w + 1] - off[w];
+__device__ __forceinline__ uint32_t bfs_items(Rows rows, uint32_t w) {
+  const uint64_t d = rows.len(w);
   return d ? (uint32_t)((d + kBfsChunk - 1) / kBfsChunk) : 0u;
 }
 
-__global__ void k_bfs_seed(const uint64_t* off, const uint32_t* inv, const uint32_t* seeds, uint64_t ns,
+__global__ void k_bfs_seed(Rows rows, const uint32_t* inv, const uint32_t* seeds, uint64_t ns,
                            uint8_t* flags, uint2* out, unsigned* cnt) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x; b < ns; b += stride) {
@@ -1163,29 +1173,29 @@ __global__ void k_bfs_seed(const uint64_t* off, const uint32_t* inv, const uint3
     if (i < ns) {
       v = inv ? inv[seeds[i]] : seeds[i];
       take = claim_byte(flags, v);
-      if (take) items = bfs_items(off, v);
+      if (take) items = bfs_items(rows, v);
     }
     warp_push_items(take && items, v, items, out, cnt);
   }
 }
 
 // warp per frontier item: lanes stride over the chunk's out-edges
-__global__ void k_bfs_level(const uint64_t* off, const uint32_t* tgt, const uint2* fr, uint32_t nf, uint8_t* flags,
-                            uint2* out, unsigned* cnt) {
+__global__ void k_bfs_level(Rows rows, const uint2* fr, uint32_t nf, uint8_t* flags, uint2* out, unsigned* cnt) {
   const uint64_t nw = (uint64_t)gridDim.x * blockDim.x / 32;
   for (uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; i < nf; i += nw) {
     const uint2 it = fr[i];
-    const uint64_t b = off[it.x] + (uint64_t)kBfsChunk * it.y;
-    const uint64_t e0 = off[it.x + 1];
-    const uint64_t e = b + kBfsChunk < e0 ? b + kBfsChunk : e0;
+    const uint32_t* r = rows.row(it.x);
+    const uint64_t len = rows.len(it.x);
+    const uint64_t b = (uint64_t)kBfsChunk * it.y;
+    const uint64_t e = b + kBfsChunk < len ? b + kBfsChunk : len;
     for (uint64_t k0 = b; k0 < e; k0 += 32) {
       const uint64_t k = k0 + lane_id();
       uint32_t w = 0, items = 0;
       bool take = false;
       if (k < e) {
-        w = tgt[k];
+        w = r[k];
         take = claim_byte(flags, w);
-        if (take) items = bfs_items(off, w);
+        if (take) items = bfs_items(rows, w);
       }
       warp_push_items(take && items, w, items, out, cnt);
     }
@@ -1312,6 +1322,7 @@ SweepArgs layout_args(const Layout* L, double* partials) {
   SweepArgs a{};
   a.n = L->n;
   a.M = L->M;
+  a.loops = L->loops ? 1 : 0;
   a.T = L->T;
   a.indeg = L->indeg;
   a.outdeg = L->outdeg;
@@ -1339,8 +1350,13 @@ SweepArgs layout_args(const Layout* L, double* partials) {
   return a;
 }
 
-struct WidenU32 {
-  __host__ __device__ unsigned long long operator()(uint32_t x) const { return x; }
+// in-degree i widened to 64 bits, 0 past the end
+struct IndegAt {
+  const uint32_t* indeg;
+  uint32_t n;
+  __device__ __forceinline__ unsigned long long operator()(uint64_t i) const {
+    return i < n ? (unsigned long long)indeg[i] : 0ull;
+  }
 };
 // cut[r] (0 < r < world): after the first vertex v whose inclusive in-degree
 // prefix reaches r/world of the edges, rounded up to a whole single-region
@@ -1374,16 +1390,13 @@ std::vector<RankRange> plan_ranges(dynpr_context* ctx, Layout* L, int world) {
   std::vector<uint32_t> cut(world + 1, 0), pbase((size_t)M + 1);
   cut[world] = n;
   if (world > 1 && n) {
-    auto* prefix = ctx->plan_prefix.as<unsigned long long>((uint64_t)n + 64);
-    auto* dcut = reinterpret_cast<uint32_t*>(prefix + n);
+    auto* prefix = ctx->plan_prefix.as<unsigned long long>((uint64_t)n + 72);
+    auto* dcut = reinterpret_cast<uint32_t*>(prefix + n + 1);
     if (world > 128) throw Error(DYNPR_INVALID_ARGUMENT, "team larger than 128 ranks");
-    // 64-bit accumulation (m may exceed 2^32)
-    cub::TransformInputIterator<unsigned long long, WidenU32, const uint32_t*> deg(L->indeg, WidenU32{});
-    size_t bytes = 0;
-    DYNPR_CK(cub::DeviceScan::InclusiveSum(nullptr, bytes, deg, prefix, (int64_t)n, ctx->stream));
-    void* tmp = ctx->cub_tmp.ensure(bytes);
-    DYNPR_CK(cub::DeviceScan::InclusiveSum(tmp, bytes, deg, prefix, (int64_t)n, ctx->stream));
-    k_plan_cuts<<<1, 128, 0, ctx->stream>>>(prefix, n, M, L->m, world, dcut);
+    // 64-bit accumulation (m may exceed 2^32); the exclusive prefix over
+    // n + 1 entries shifted by one is the inclusive prefix
+    prims::scan_exclusive<unsigned long long>(ctx, IndegAt{L->indeg, n}, prefix, (uint64_t)n + 1, ctx->stream);
+    k_plan_cuts<<<1, 128, 0, ctx->stream>>>(prefix + 1, n, M, L->m, world, dcut);
     check_launch();
     DYNPR_CK(cudaMemcpyAsync(cut.data() + 1, dcut + 1, (size_t)(world - 1) * 4, cudaMemcpyDeviceToHost,
                              ctx->stream));
@@ -1673,11 +1686,11 @@ void launch_pull_expand(dynpr_context* ctx, const SweepArgs& a) {
   count_launch(ctx, launched);
 }
 
-void launch_init_ranks(dynpr_context* ctx, const Layout* L, const double* init, double uniform, double* r0,
+void launch_init_ranks(dynpr_context* ctx, const Layout* L, const double* init_old, double uniform, double* r0,
                        double* r1, double* c0, double* c1) {
   if (!L->n) return;
-  k_init_ranks<<<grid_for(L->n, kThreads, ctx->num_sms * 16), kThreads, 0, ctx->stream>>>(L->outdeg, L->n, init,
-                                                                                         uniform, r0, r1, c0, c1);
+  k_init_ranks<<<grid_for(L->n, kThreads, ctx->num_sms * 16), kThreads, 0, ctx->stream>>>(
+      L->outdeg, L->perm, L->n, init_old, uniform, r0, r1, c0, c1);
   check_launch();
   count_launch(ctx);
 }
@@ -1700,18 +1713,17 @@ void launch_collect_pending(dynpr_context* ctx, const uint32_t* outdeg, const ui
   count_launch(ctx);
 }
 
-void launch_expand(dynpr_context* ctx, const uint64_t* off, const uint32_t* tgt, uint8_t* va,
-                   const uint32_t* pend_low, uint32_t n_low, const uint2* pend_high, uint32_t n_high) {
+void launch_expand(dynpr_context* ctx, Rows rows, uint8_t* va, const uint32_t* pend_low, uint32_t n_low,
+                   const uint2* pend_high, uint32_t n_high) {
   if (n_low) {
-    k_expand_low<<<grid_for(n_low, kThreads, ctx->num_sms * 16), kThreads, 0, ctx->stream>>>(off, tgt, pend_low,
-                                                                                            n_low, va, nullptr,
-                                                                                            nullptr);
+    k_expand_low<<<grid_for(n_low, kThreads, ctx->num_sms * 16), kThreads, 0, ctx->stream>>>(rows, pend_low, n_low,
+                                                                                            va, nullptr, nullptr);
     check_launch();
     count_launch(ctx);
   }
   if (n_high) {
     k_expand_high<<<grid_for((uint64_t)n_high * 32, kThreads, ctx->num_sms * 16), kThreads, 0, ctx->stream>>>(
-        off, tgt, pend_high, n_high, va, nullptr, nullptr);
+        rows, pend_high, n_high, va, nullptr, nullptr);
     check_launch();
     count_launch(ctx);
   }
@@ -1724,17 +1736,17 @@ void launch_loop_end(dynpr_context* ctx, LoopCtl* c, SweepRed* red, cudaGraphCon
   count_launch(ctx);
 }
 
-void launch_expand_dev(dynpr_context* ctx, const uint64_t* off, const uint32_t* tgt, uint8_t* va,
-                       const uint32_t* pend_low, const uint2* pend_high, const unsigned* counts, const int* gate) {
+void launch_expand_dev(dynpr_context* ctx, Rows rows, uint8_t* va, const uint32_t* pend_low, const uint2* pend_high,
+                       const unsigned* counts, const int* gate) {
   const unsigned g = (unsigned)ctx->num_sms * 16;
-  k_expand_low<<<g, kThreads, 0, ctx->stream>>>(off, tgt, pend_low, 0, va, counts, gate);
+  k_expand_low<<<g, kThreads, 0, ctx->stream>>>(rows, pend_low, 0, va, counts, gate);
   check_launch();
-  k_expand_high<<<g, kThreads, 0, ctx->stream>>>(off, tgt, pend_high, 0, va, counts, gate);
+  k_expand_high<<<g, kThreads, 0, ctx->stream>>>(rows, pend_high, 0, va, counts, gate);
   check_launch();
   count_launch(ctx, 2);
 }
 
-uint64_t mark_reachable(dynpr_context* ctx, const uint64_t* off, const uint32_t* tgt, uint32_t n, uint64_t m,
+uint64_t mark_reachable(dynpr_context* ctx, Rows rows, uint32_t n, uint64_t m,
                         const uint32_t* inv, const uint32_t* seeds, uint64_t ns, uint8_t* flags) {
   cudaStream_t st = ctx->stream;
   auto* cnt = reinterpret_cast<unsigned*>(ctx->scratch32a.as<unsigned>(2));
@@ -1744,7 +1756,7 @@ uint64_t mark_reachable(dynpr_context* ctx, const uint64_t* off, const uint32_t*
   uint2* fa = ctx->bfs_a.as<uint2>(cap);
   uint2* fb = ctx->bfs_b.as<uint2>(cap);
   DYNPR_CK(cudaMemsetAsync(cnt, 0, 4, st));
-  k_bfs_seed<<<grid_for(ns, kThreads, ctx->num_sms * 16), kThreads, 0, st>>>(off, inv, seeds, ns, flags, fa, cnt);
+  k_bfs_seed<<<grid_for(ns, kThreads, ctx->num_sms * 16), kThreads, 0, st>>>(rows, inv, seeds, ns, flags, fa, cnt);
   check_launch();
   count_launch(ctx);
   for (;;) {
@@ -1755,7 +1767,7 @@ uint64_t mark_reachable(dynpr_context* ctx, const uint64_t* off, const uint32_t*
     items_total += nf;
     if (!nf) break;
     DYNPR_CK(cudaMemsetAsync(cnt, 0, 4, st));
-    k_bfs_level<<<grid_for((uint64_t)nf * 32, kThreads, ctx->num_sms * 16), kThreads, 0, st>>>(off, tgt, fa, nf, flags,
+    k_bfs_level<<<grid_for((uint64_t)nf * 32, kThreads, ctx->num_sms * 16), kThreads, 0, st>>>(rows, fa, nf, flags,
                                                                                            fb, cnt);
     check_launch();
     count_launch(ctx);

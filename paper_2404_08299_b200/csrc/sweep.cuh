@@ -22,6 +22,20 @@ struct Schedule {
 };
 Schedule build_partition(dynpr_context* ctx, const dynpr_graph* g, uint32_t thr, uint32_t* order);
 
+// Out-rows of a graph for push expansion / markReachable: a canonical CSR
+// (deg null: row u = tgt[beg[u] .. beg[u+1])) or the engine layout's
+// copy-on-write relabelled forward graph (row u = deg[u] words from
+// tgt + beg[u], beg a 64-bit word offset that may wrap below tgt).
+struct Rows {
+  const uint64_t* beg;
+  const uint32_t* deg;
+  const uint32_t* tgt;
+  __device__ __forceinline__ const uint32_t* row(uint32_t u) const { return tgt + beg[u]; }
+  __device__ __forceinline__ uint64_t len(uint32_t u) const {
+    return deg ? (uint64_t)deg[u] : beg[u + 1] - beg[u];
+  }
+};
+
 struct SweepArgs {
   // engine layout (new-id space)
   uint32_t n, M, T;
@@ -41,6 +55,10 @@ struct SweepArgs {
   uint32_t* mcount;      // per multi vertex chunk-completion counters (fused sweep)
   uint64_t ss_heavy;     // single slices [0, ss_heavy) are heavy (layout n_hslices)
   int trace;     // debug: record per-warp timelines of the fused sweep (DYNPR_TRACE)
+  // every in-list holds its own vertex: an in-degree-1 segment is the
+  // self-loop alone, summed from the vertex's own contribution (no index or
+  // gather load)
+  int loops;
   // iteration state
   double alpha, teleport, tf, tp;
   const double* rank_prev;
@@ -76,8 +94,9 @@ struct SweepArgs {
   // when *expand == kExpandPull.  Null in the host-driven loop.
   const int* done;
   const int* expand;
-  // relabelled forward CSR for the device loop's push expansion
-  const uint64_t* offF;
+  // relabelled forward graph for the device loop's push expansion
+  // (Rows{begF, outdeg, tgtF})
+  const uint64_t* begF;
   const uint32_t* tgtF;
 };
 
@@ -98,7 +117,7 @@ void launch_loop_end(dynpr_context* ctx, LoopCtl* c, SweepRed* red, cudaGraphCon
                      int set_cond);
 // Push expansion with device-resident list sizes (counts[0] low, counts[1]
 // high), optionally gated on *gate == kExpandPush; fixed grids.
-void launch_expand_dev(dynpr_context* ctx, const uint64_t* off, const uint32_t* tgt, uint8_t* va,
+void launch_expand_dev(dynpr_context* ctx, Rows rows, uint8_t* va,
                        const uint32_t* pend_low, const uint2* pend_high, const unsigned* counts, const int* gate);
 
 // Edge-balanced partition of the layout's vertex space over `world` ranks
@@ -135,9 +154,10 @@ uint32_t* sweep_tick(dynpr_context* ctx);
 // grid, so launch_sweep / launch_pull_expand can be stream-captured.
 void prepare_sweep_launch(dynpr_context* ctx);
 
-// rank / contribution initialisation in new-id order: r = init (already in
-// new order) or `uniform`; c = r / outdeg.
-void launch_init_ranks(dynpr_context* ctx, const Layout* L, const double* init, double uniform, double* r0,
+// rank / contribution initialisation in new-id order: r = init_old[perm[v]]
+// (the previous ranks in old-id order) or `uniform`; c = r / outdeg; r1 / c1
+// (copies) may be null.
+void launch_init_ranks(dynpr_context* ctx, const Layout* L, const double* init_old, double uniform, double* r0,
                        double* r1, double* c0, double* c1);
 
 // Frontier (frontier.cpp).  initialAffected marks the batch endpoints
@@ -148,7 +168,7 @@ void launch_init_affected(dynpr_context* ctx, const uint32_t* inv, const uint32_
                           uint64_t nd, const uint32_t* is, uint64_t ni, uint8_t* va, uint8_t* np);
 void launch_collect_pending(dynpr_context* ctx, const uint32_t* outdeg, const uint64_t* off, uint32_t n,
                             const uint8_t* np, uint32_t T, uint32_t* pend_low, uint2* pend_high, SweepRed* red);
-void launch_expand(dynpr_context* ctx, const uint64_t* off, const uint32_t* tgt, uint8_t* va,
+void launch_expand(dynpr_context* ctx, Rows rows, uint8_t* va,
                    const uint32_t* pend_low, uint32_t n_low, const uint2* pend_high, uint32_t n_high);
 void launch_pull_expand(dynpr_context* ctx, const SweepArgs& a);
 
@@ -156,7 +176,7 @@ void launch_pull_expand(dynpr_context* ctx, const SweepArgs& a);
 // the seeds over the CSR (off, tgt; m edges); seed ids mapped through `inv`
 // when given.  Level-synchronous; frontier items are (vertex, 1024-edge
 // chunk).  Returns the number of frontier items processed.
-uint64_t mark_reachable(dynpr_context* ctx, const uint64_t* off, const uint32_t* tgt, uint32_t n, uint64_t m,
+uint64_t mark_reachable(dynpr_context* ctx, Rows rows, uint32_t n, uint64_t m,
                         const uint32_t* inv, const uint32_t* seeds, uint64_t ns, uint8_t* flags);
 
 // Norms (rank.cpp:142-152).
