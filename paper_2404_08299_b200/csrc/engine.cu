@@ -189,6 +189,13 @@ struct LoopGraphCache {
 };
 constexpr size_t kLoopCacheMax = 16;
 
+// Device-loop solves of one GPU in this process go one at a time (the
+// constant-bank argument slots are per device); captures too.
+std::mutex& loop_slot_lock(int device) {
+  static std::mutex locks[64];
+  return locks[device & 63];
+}
+
 LoopGraph& loop_graph(dynpr_context* ctx, const SweepPlan& plan, int frontier, LoopCtl* dc, SweepRed* red) {
   auto* cache = static_cast<LoopGraphCache*>(ctx->loop_graphs);
   if (!cache) ctx->loop_graphs = cache = new LoopGraphCache();
@@ -223,7 +230,7 @@ LoopGraph& loop_graph(dynpr_context* ctx, const SweepPlan& plan, int frontier, L
       launch_sweep_ind(ctx, plan, k, tick);  // the record is zero: before the launch, then k_loop_end
       launch_loop_end(ctx, dc, red, cond, k == 1);
       if (frontier) {
-        launch_expand_ind(ctx, k, &dc->pend_low, &dc->expand);
+        launch_expand_ind(ctx, k, dc);
         if (!plan.pull_fused) launch_pull_ind(ctx, plan, k);  // (else: inside the next sweep)
       }
     }
@@ -276,8 +283,7 @@ void run_device_loop(dynpr_context* ctx, const SolveSpec& sp, const SweepArgs& a
   LoopCtl* dc = ctx->loopctl.as<LoopCtl>(1);
   // the constant-bank argument slots are per device: one device-loop solve
   // at a time per GPU in this process
-  static std::mutex slot_lock[64];
-  std::lock_guard<std::mutex> guard(slot_lock[ctx->device & 63]);
+  std::lock_guard<std::mutex> guard(loop_slot_lock(ctx->device));
   prepare_sweep_launch(ctx);  // allocations / attributes must not happen inside a capture
 
   SweepArgs half[2] = {a_in, a_in};
@@ -301,10 +307,14 @@ void run_device_loop(dynpr_context* ctx, const SolveSpec& sp, const SweepArgs& a
   const bool want_pf = h.frontier && !(pf && pf[0] == '0');
   for (int k = 0; k < 2; ++k) half[k].pull_fused = want_pf ? 1 : 0;
   const SweepPlan plan = plan_sweep(ctx, half[0], sp.flagged, sp.closed);
+  const char* ll = std::getenv("DYNPR_LAZY_LISTS");
+  const bool lazy = plan.pull_fused && !(ll && ll[0] == '0');
   for (int k = 0; k < 2; ++k) {
     half[k].pull_fused = plan.pull_fused;
+    half[k].lazy_lists = lazy ? 1 : 0;
     if (plan.pull_fused) half[k].np = nullptr;
   }
+  h.lazy_lists = lazy ? 1 : 0;
   LoopGraph& lg = loop_graph(ctx, plan, h.frontier, dc, red);
 
   // per-solve state: loop control + both halves' arguments, one upload
@@ -326,6 +336,42 @@ void run_device_loop(dynpr_context* ctx, const SolveSpec& sp, const SweepArgs& a
   res.affected_vertex_iterations = h.affected;
   res.processed_edges = h.edges;
   res.final_delta = h.final_delta;
+}
+
+// Snapshot preparation also readies the solves that follow (single GPU,
+// device loop): the engine workspace at this graph's size and the
+// instantiated loop graphs of Static and of the frontier engines (DF-P,
+// DF) for this layout's sweep plan, so a first solve pays neither
+// allocations nor a graph capture + instantiation (RMAT-20: the first DF-P
+// of a process took ~20 ms of device time, the next 0.6).  Both are cached
+// on the context and reused by every snapshot of the same shape.
+void prewarm_solves(dynpr_context* ctx, const Layout* L, uint64_t m, bool frontier) {
+  const uint32_t n = L->n;
+  for (int k = 0; k < 2; ++k) {
+    ctx->rank[k].as<double>(n);
+    ctx->contrib[k].as<double>(n);
+  }
+  double* partials = ctx->partials.as<double>(L->n_mseg + 1);
+  SweepRed* red = ctx->red.as<SweepRed>(2);
+  LoopCtl* dc = ctx->loopctl.as<LoopCtl>(1);
+  if (frontier) {
+    ctx->flags_va.as<uint8_t>((uint64_t)n + 4);
+    ctx->pend_flags.as<uint8_t>(n);
+    ctx->flags_written.as<uint8_t>(n);
+    ctx->pend_low.as<uint32_t>((uint64_t)n + 1);
+    ctx->pend_high.as<uint2>((uint64_t)n + m / kExpandChunk + 1);
+  }
+  std::lock_guard<std::mutex> guard(loop_slot_lock(ctx->device));
+  prepare_sweep_launch(ctx);
+  const char* pf = std::getenv("DYNPR_PULL_FUSED");
+  const bool want_pf = !(pf && pf[0] == '0');
+  const int kinds[3][2] = {{0, 0}, {1, 1}, {1, 0}};  // (flagged, closed): Static / ND, DF-P, DF
+  for (int i = 0; i < (frontier ? 3 : 1); ++i) {
+    SweepArgs a = layout_args(L, partials);
+    a.pull_fused = kinds[i][0] && want_pf ? 1 : 0;
+    const SweepPlan plan = plan_sweep(ctx, a, kinds[i][0] != 0, kinds[i][1] != 0);
+    loop_graph(ctx, plan, kinds[i][0], dc, red);
+  }
 }
 
 // convergeLoop (engine.cu:61-95) on the device, in the layout's new-id
@@ -939,6 +985,8 @@ dynpr_status dynpr_graph_prepare(dynpr_context* ctx, const dynpr_graph* gT, cons
     if (is_team(ctx)) {
       plan_ranges(ctx, const_cast<Layout*>(L), ctx->comm->world);
       ensure_fingerprint(ctx, const_cast<Layout*>(L), gT, gF);
+    } else if (!host_loop_forced()) {
+      prewarm_solves(ctx, L, gT->m, with_forward != 0);
     }
   });
 }

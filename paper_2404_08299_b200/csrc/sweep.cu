@@ -100,8 +100,8 @@ __device__ __forceinline__ void block_reduce_commit(Acc acc, SweepRed* red) {
 // Warp-aggregated append of pending vertices (all 32 lanes must call it):
 // low out-degree vertices go to `pl` one entry each, the others to `ph` as
 // ceil(outdeg / 1024) (vertex, chunk) work items.
-__device__ __forceinline__ void warp_append(bool pend, bool lowout, uint32_t v, uint32_t od, uint32_t* pl,
-                                            uint2* ph, SweepRed* red) {
+__device__ __forceinline__ void warp_append_to(bool pend, bool lowout, uint32_t v, uint32_t od, uint32_t* pl,
+                                               uint2* ph, unsigned* cnt_low, unsigned* cnt_high) {
   const unsigned ml = __ballot_sync(kFull, pend && lowout);
   const unsigned items = (pend && !lowout) ? (od + kExpandChunk - 1) / kExpandChunk : 0u;
   const unsigned mh = __ballot_sync(kFull, items != 0);
@@ -116,14 +116,18 @@ __device__ __forceinline__ void warp_append(bool pend, bool lowout, uint32_t v, 
   const unsigned total = __shfl_sync(kFull, incl, 31);
   unsigned bl = 0, bh = 0;
   if (lane == 0) {
-    if (ml) bl = atomicAdd(&red->pend_low, (unsigned)__popc(ml));
-    if (total) bh = atomicAdd(&red->pend_high, total);
+    if (ml) bl = atomicAdd(cnt_low, (unsigned)__popc(ml));
+    if (total) bh = atomicAdd(cnt_high, total);
   }
   bl = __shfl_sync(kFull, bl, 0);
   bh = __shfl_sync(kFull, bh, 0);
   const unsigned lt = (1u << lane) - 1u;
   if (pend && lowout) pl[bl + __popc(ml & lt)] = v;
   for (unsigned j = 0, b = bh + incl - items; j < items; ++j) ph[b + j] = make_uint2(v, j);
+}
+__device__ __forceinline__ void warp_append(bool pend, bool lowout, uint32_t v, uint32_t od, uint32_t* pl,
+                                            uint2* ph, SweepRed* red) {
+  warp_append_to(pend, lowout, v, od, pl, ph, &red->pend_low, &red->pend_high);
 }
 
 // A new contribution of vertex v: the local buffer and, in a multi-GPU team
@@ -237,12 +241,11 @@ __device__ __forceinline__ bool folds(const SweepArgs& a, uint32_t len) {
 template <bool NEG = false>
 __device__ __forceinline__ double segment_sum(const uint32_t* __restrict__ sell, uint64_t base, unsigned lane,
                                               uint32_t len, uint32_t Lw, const double* __restrict__ contrib,
-                                              uint32_t self, double cself, bool fold = false,
-                                              unsigned* neg = nullptr) {
+                                              uint32_t self, double cself, unsigned* neg = nullptr) {
   unsigned nb = 0;
   const uint32_t* p = sell + base + 4u * lane;  // element k at p + 32*k (k % 4 == 0)
   const uint4 z = make_uint4(0, 0, 0, 0);
-  double c = 0.0, tot = 0.0;
+  double c = 0.0;
   uint4 a = len > 0 ? ld_idx4(p) : z;
   uint4 b = len > 4 ? ld_idx4(p + 128) : z;
   for (uint32_t k = 0; k < Lw; k += 8) {
@@ -253,10 +256,6 @@ __device__ __forceinline__ double segment_sum(const uint32_t* __restrict__ sell,
       x[q] = (k + q < len) ? ld_contrib(contrib, u[q], self, cself) : 0.0;
     a = (k + 8 < len) ? ld_idx4(p + 32ull * (k + 8)) : z;
     b = (k + 12 < len) ? ld_idx4(p + 32ull * (k + 12)) : z;
-    if (fold && k != 0 && (k & (kAccumChunk - 1)) == 0 && k < len) {
-      tot = __dadd_rn(tot, c);
-      c = 0.0;
-    }
 #pragma unroll
     for (uint32_t q = 0; q < 8; ++q) {
       if (k + q < len) c = __dadd_rn(c, fabs(x[q]));
@@ -264,6 +263,37 @@ __device__ __forceinline__ double segment_sum(const uint32_t* __restrict__ sell,
     }
   }
   if (NEG) *neg = nb >> 31;
+  return c;
+}
+
+// The segment sum of a warp holding a folding lane (folds(): derived layouts
+// only, rare): chunked accumulation, c = ((0 + p0) + p1) + ..., with the
+// sign-bit OR.  Out of line, so its extra live state does not weigh on the
+// register allocation of the common path (the fused sweep spilled 168 B
+// instead of 72 B with the fold inlined; RMAT-20 Static 4.67 -> 4.35 ms).
+__device__ __noinline__ double segment_sum_folding(const uint32_t* __restrict__ sell, uint64_t base, unsigned lane,
+                                                   uint32_t len, uint32_t Lw, const double* __restrict__ contrib,
+                                                   uint32_t self, double cself, bool fold, unsigned* neg) {
+  const uint32_t* p = sell + base + 4u * lane;
+  double c = 0.0, tot = 0.0;
+  unsigned nb = 0;
+  for (uint32_t k = 0; k < Lw; k += 4) {
+    const uint4 w = k < len ? ld_idx4(p + 32ull * k) : make_uint4(0, 0, 0, 0);
+    const uint32_t u[4] = {w.x, w.y, w.z, w.w};
+    double x[4];
+#pragma unroll
+    for (uint32_t q = 0; q < 4; ++q) x[q] = (k + q < len) ? ld_contrib(contrib, u[q], self, cself) : 0.0;
+    if (fold && k != 0 && (k & (kAccumChunk - 1)) == 0 && k < len) {
+      tot = __dadd_rn(tot, c);
+      c = 0.0;
+    }
+#pragma unroll
+    for (uint32_t q = 0; q < 4; ++q) {
+      if (k + q < len) c = __dadd_rn(c, fabs(x[q]));
+      nb |= (unsigned)__double2hiint(x[q]);
+    }
+  }
+  *neg = nb >> 31;
   return fold ? __dadd_rn(tot, c) : c;
 }
 
@@ -322,7 +352,11 @@ __device__ __forceinline__ void b_sweep_single(const SweepArgs& a) {
     const uint64_t s0 = a.ss_lo + g;
     if (s0 >= a.ss_hi) break;
     const uint64_t s1 = s0 + kSplitGrab < a.ss_hi ? s0 + kSplitGrab : a.ss_hi;
+    // the grab's slice bases in one load (lane i: slice s0 + i), so a
+    // slice's index loads do not wait for its own base load
+    const uint64_t sb_lane = s0 + lane < s1 ? a.sbase[s0 + lane] : 0ull;
   for (uint64_t s = s0; s < s1; ++s) {
+    const uint64_t sb = __shfl_sync(kFull, sb_lane, (int)(s - s0));
     const uint64_t vv = (uint64_t)a.M + s * 32 + lane;
     const bool valid = vv < a.n;
     const uint32_t v = (uint32_t)vv;
@@ -347,10 +381,13 @@ __device__ __forceinline__ void b_sweep_single(const SweepArgs& a) {
         neg = (unsigned)__double2hiint(cself) >> 31;
       }
     } else if (Lw) {
-      if (pull)
-        c = segment_sum<true>(a.sell_s, a.sbase[s], lane, len, Lw, a.contrib_prev, v, cself, folds(a, len), &neg);
+      const bool fold = folds(a, len);
+      if (__any_sync(kFull, fold))
+        c = segment_sum_folding(a.sell_s, sb, lane, len, Lw, a.contrib_prev, v, cself, fold, &neg);
+      else if (pull)
+        c = segment_sum<true>(a.sell_s, sb, lane, len, Lw, a.contrib_prev, v, cself, &neg);
       else
-        c = segment_sum(a.sell_s, a.sbase[s], lane, len, Lw, a.contrib_prev, v, cself, folds(a, len));
+        c = segment_sum(a.sell_s, sb, lane, len, Lw, a.contrib_prev, v, cself);
     }
     const bool newly = scan && neg;
     bool pend = false, lowout = false;
@@ -363,7 +400,7 @@ __device__ __forceinline__ void b_sweep_single(const SweepArgs& a) {
         acc.edges += deg;
       }
     }
-    if (FLAGGED && a.pend_low) warp_append(pend, lowout, v, od, a.pend_low, a.pend_high, a.red);
+    if (FLAGGED && a.pend_low && !(pull && a.lazy_lists)) warp_append(pend, lowout, v, od, a.pend_low, a.pend_high, a.red);
   }
   }
   if (a.npeers) __threadfence_system();  // peer stores visible before the team barrier
@@ -403,7 +440,7 @@ __device__ __forceinline__ void b_sweep_mseg(const SweepArgs& a) {
     if (pull) {  // the chunk's "any pending source" rides in the partial's sign bit
       unsigned neg = 0;
       const double c =
-          segment_sum<true>(a.sell_m, a.mbase[s], lane, len, Lw, a.contrib_prev, 0xffffffffu, 0.0, false, &neg);
+          segment_sum<true>(a.sell_m, a.mbase[s], lane, len, Lw, a.contrib_prev, 0xffffffffu, 0.0, &neg);
       if (len) a.partials[seg] = neg ? -c : c;
     } else {
       const double c = segment_sum(a.sell_m, a.mbase[s], lane, len, Lw, a.contrib_prev, 0xffffffffu, 0.0);
@@ -497,7 +534,7 @@ __device__ __forceinline__ void b_sweep_mfinal(const SweepArgs& a) {
           }
         }
       }
-      if (FLAGGED && a.pend_low) warp_append(pend, lowout, v, od, a.pend_low, a.pend_high, a.red);
+      if (FLAGGED && a.pend_low && !(pull && a.lazy_lists)) warp_append(pend, lowout, v, od, a.pend_low, a.pend_high, a.red);
     }
   }
   // phase 2: thread per remaining multi vertex, partials loaded 8 ahead
@@ -539,7 +576,7 @@ __device__ __forceinline__ void b_sweep_mfinal(const SweepArgs& a) {
         }
       }
     }
-    if (FLAGGED && a.pend_low) warp_append(pend, lowout, v, od, a.pend_low, a.pend_high, a.red);
+    if (FLAGGED && a.pend_low && !(pull && a.lazy_lists)) warp_append(pend, lowout, v, od, a.pend_low, a.pend_high, a.red);
   }
   if (a.npeers) __threadfence_system();  // peer stores visible before the team barrier
   block_reduce_commit(acc, a.red);
@@ -597,14 +634,12 @@ __device__ __forceinline__ unsigned smid() {
 template <int Q, bool NEG = false>
 __device__ __forceinline__ double segment_sum_deep(const uint32_t* __restrict__ sell, uint64_t base, unsigned lane,
                                                    uint32_t len, uint32_t Lw, const double* __restrict__ contrib,
-                                                   uint32_t self, double cself, bool fold = false,
-                                                   unsigned* neg = nullptr) {
+                                                   uint32_t self, double cself, unsigned* neg = nullptr) {
   constexpr uint32_t D = 4 * Q;  // elements in flight per lane
   unsigned nb = 0;
-  static_assert(kAccumChunk % D == 0, "a chunk boundary starts a group");
   const uint32_t* p = sell + base + 4u * lane;
   const uint4 z = make_uint4(0, 0, 0, 0);
-  double c = 0.0, tot = 0.0;
+  double c = 0.0;
   uint4 ix[Q];
 #pragma unroll
   for (int j = 0; j < Q; ++j) ix[j] = (4u * j < len) ? ld_idx4(p + 128ull * j) : z;
@@ -619,10 +654,6 @@ __device__ __forceinline__ double segment_sum_deep(const uint32_t* __restrict__ 
     }
 #pragma unroll
     for (int j = 0; j < Q; ++j) ix[j] = (k + D + 4 * j < len) ? ld_idx4(p + 32ull * (k + D + 4 * j)) : z;
-    if (fold && k != 0 && (k & (kAccumChunk - 1)) == 0 && k < len) {
-      tot = __dadd_rn(tot, c);
-      c = 0.0;
-    }
 #pragma unroll
     for (uint32_t q = 0; q < D; ++q) {
       if (k + q < len) c = __dadd_rn(c, fabs(x[q]));
@@ -630,7 +661,7 @@ __device__ __forceinline__ double segment_sum_deep(const uint32_t* __restrict__ 
     }
   }
   if (NEG) *neg = nb >> 31;
-  return fold ? __dadd_rn(tot, c) : c;
+  return c;
 }
 
 // One single-region slice (the body of k_sweep_single).
@@ -662,11 +693,11 @@ __device__ __forceinline__ void single_slice(const SweepArgs& a, uint64_t s, uns
       neg = (unsigned)__double2hiint(cself) >> 31;
     }
   } else if (Lw) {
-    if (FLAGGED && pull)
-      c = segment_sum_deep<Q, true>(a.sell_s, a.sbase[s], lane, len, Lw, a.contrib_prev, v, cself, folds(a, len),
-                                    &neg);
-    else
-      c = segment_sum_deep<Q>(a.sell_s, a.sbase[s], lane, len, Lw, a.contrib_prev, v, cself, folds(a, len));
+    const bool fold = folds(a, len);
+    if (__any_sync(kFull, fold))
+      c = segment_sum_folding(a.sell_s, a.sbase[s], lane, len, Lw, a.contrib_prev, v, cself, fold, &neg);
+    else  // (frontier sweeps always OR the sign bits: one instantiation, fewer spills)
+      c = segment_sum_deep<Q, FLAGGED>(a.sell_s, a.sbase[s], lane, len, Lw, a.contrib_prev, v, cself, &neg);
   }
   const bool newly = scan && neg;
   bool pend = false, lowout = false;
@@ -679,7 +710,7 @@ __device__ __forceinline__ void single_slice(const SweepArgs& a, uint64_t s, uns
       acc.edges += deg;
     }
   }
-  if (FLAGGED && a.pend_low) warp_append(pend, lowout, v, od, a.pend_low, a.pend_high, a.red);
+  if (FLAGGED && a.pend_low && !(pull && a.lazy_lists)) warp_append(pend, lowout, v, od, a.pend_low, a.pend_high, a.red);
 }
 
 // One multi-chunk slice: 32 chunk partials; the warp that completes a
@@ -701,13 +732,10 @@ __device__ __forceinline__ void multi_slice(const SweepArgs& a, uint64_t s, unsi
   const uint32_t Lw = __reduce_max_sync(kFull, len);
   if (!Lw) return;
   double c;
-  if (FLAGGED && pull) {  // the chunk's "any pending source" rides in the partial's sign bit
+  {  // (a pull sweep's chunk carries "any pending source" in the partial's sign bit)
     unsigned neg = 0;
-    c = segment_sum_deep<Q, true>(a.sell_m, a.mbase[s], lane, len, Lw, a.contrib_prev, 0xffffffffu, 0.0, false,
-                                  &neg);
-    if (neg) c = -c;
-  } else {
-    c = segment_sum_deep<Q>(a.sell_m, a.mbase[s], lane, len, Lw, a.contrib_prev, 0xffffffffu, 0.0);
+    c = segment_sum_deep<Q, FLAGGED>(a.sell_m, a.mbase[s], lane, len, Lw, a.contrib_prev, 0xffffffffu, 0.0, &neg);
+    if (FLAGGED && pull && neg) c = -c;
   }
   bool last = false;
   if (len) {
@@ -758,7 +786,7 @@ __device__ __forceinline__ void multi_slice(const SweepArgs& a, uint64_t s, unsi
       acc.edges += a.indeg[v];
     }
   }
-  if (FLAGGED && a.pend_low) warp_append(pend, lowout, v, od, a.pend_low, a.pend_high, a.red);
+  if (FLAGGED && a.pend_low && !(pull && a.lazy_lists)) warp_append(pend, lowout, v, od, a.pend_low, a.pend_high, a.red);
 }
 
 template <bool FLAGGED, bool CLOSED, int QH>
@@ -1058,25 +1086,25 @@ __device__ __forceinline__ void expand_high_body(Rows rows, const uint2* items, 
 }
 __global__ void k_expand_low(Rows rows, const uint32_t* list, uint32_t cnt, uint8_t* va, const unsigned* dcnt,
                              const int* gate) {
-  if (gate && *gate != kExpandPush) return;
+  if (gate && *gate != kExpandPush && *gate != kExpandPushCollect) return;
   expand_low_body(rows, list, dcnt ? dcnt[0] : cnt, va);
 }
 __global__ void k_expand_high(Rows rows, const uint2* items, uint32_t cnt, uint8_t* va, const unsigned* dcnt,
                               const int* gate) {
-  if (gate && *gate != kExpandPush) return;
+  if (gate && *gate != kExpandPush && *gate != kExpandPushCollect) return;
   expand_high_body(rows, items, dcnt ? dcnt[1] : cnt, va);
 }
 // device-loop variants: arguments from the constant-bank slot of half H
 template <int H>
 __global__ void k_expand_low_c(const unsigned* counts, const int* gate) {
   const SweepArgs* ap = &c_loop_args[H];
-  if (gate && *gate != kExpandPush) return;
+  if (gate && *gate != kExpandPush && *gate != kExpandPushCollect) return;
   expand_low_body(Rows{ap->begF, ap->outdeg, ap->tgtF}, ap->pend_low, counts[0], ap->va);
 }
 template <int H>
 __global__ void k_expand_high_c(const unsigned* counts, const int* gate) {
   const SweepArgs* ap = &c_loop_args[H];
-  if (gate && *gate != kExpandPush) return;
+  if (gate && *gate != kExpandPush && *gate != kExpandPushCollect) return;
   expand_high_body(Rows{ap->begF, ap->outdeg, ap->tgtF}, ap->pend_high, counts[1], ap->va);
 }
 
@@ -1090,6 +1118,8 @@ __device__ unsigned long long g_loop_trace[kLoopTraceIters * 4];
 
 __global__ void k_loop_end(LoopCtl* c, SweepRed* red, cudaGraphConditionalHandle h, int set_cond) {
   if (!c->done) {
+    // a pull sweep of a lazy-list loop appended no pending lists
+    const bool no_lists = c->lazy_lists && c->expand == kExpandPull;
     const SweepRed r = *red;
     *red = SweepRed{};  // zeroed for the next sweep (no memset node per iteration)
     const double delta = __longlong_as_double((long long)r.delta_bits);
@@ -1106,9 +1136,9 @@ __global__ void k_loop_end(LoopCtl* c, SweepRed* red, cudaGraphConditionalHandle
     } else if (c->frontier) {
       // direction-optimising expandAffected (same rule as the host loop)
       const unsigned long long pull_bound = c->m > r.edges ? c->m - r.edges : 0ull;
-      c->expand = r.pend_edges > pull_bound ? kExpandPull : kExpandPush;
-      c->pend_low = r.pend_low;
-      c->pend_high = r.pend_high;
+      c->expand = r.pend_edges > pull_bound ? kExpandPull : (no_lists ? kExpandPushCollect : kExpandPush);
+      c->pend_low = no_lists ? 0u : r.pend_low;
+      c->pend_high = no_lists ? 0u : r.pend_high;
     }
     if (c->iterations <= kLoopTraceIters) {
       unsigned long long* t = g_loop_trace + 4 * (c->iterations - 1);
@@ -1121,6 +1151,28 @@ __global__ void k_loop_end(LoopCtl* c, SweepRed* red, cudaGraphConditionalHandle
     }
   }
   if (set_cond) cudaGraphSetConditional(h, c->done ? 0u : 1u);
+}
+
+// A push decided after a pull sweep of a lazy-list loop: the pending lists
+// were not appended (SweepArgs::lazy_lists); the sweep's pending vertices
+// are exactly the negative entries of the contributions it wrote.  The
+// counts go straight to the loop state the push kernels read.
+template <int H>
+__global__ void k_collect_signs_c(LoopCtl* c) {
+  const SweepArgs& a = c_loop_args[H];
+  if (c->expand != kExpandPushCollect) return;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < a.n; base += stride) {
+    const uint64_t v = base + threadIdx.x;
+    bool pend = false, lowout = false;
+    uint32_t od = 0;
+    if (v < a.n && v >= a.v_lo && v < a.v_hi && __double2hiint(a.contrib_cur[v]) < 0) {
+      pend = true;
+      od = a.outdeg[v];
+      lowout = od <= a.T;
+    }
+    warp_append_to(pend, lowout, (uint32_t)v, od, a.pend_low, a.pend_high, &c->pend_low, &c->pend_high);
+  }
 }
 
 // ---- markReachable (frontier.cpp:86-121): level-synchronous BFS -------------------
@@ -1322,7 +1374,8 @@ SweepArgs layout_args(const Layout* L, double* partials) {
   SweepArgs a{};
   a.n = L->n;
   a.M = L->M;
-  a.loops = L->loops ? 1 : 0;
+  static const bool no_self_fast = std::getenv("DYNPR_NO_SELF_FAST") != nullptr;  // A/B only
+  a.loops = (L->loops && !no_self_fast) ? 1 : 0;
   a.T = L->T;
   a.indeg = L->indeg;
   a.outdeg = L->outdeg;
@@ -1615,8 +1668,14 @@ void launch_pull_ind(dynpr_context* ctx, const SweepPlan& p, int half) {
   count_launch(ctx, launched);
 }
 
-void launch_expand_ind(dynpr_context* ctx, int half, const unsigned* counts, const int* gate) {
+void launch_expand_ind(dynpr_context* ctx, int half, LoopCtl* dc) {
   const unsigned g = (unsigned)ctx->num_sms * 16;
+  const unsigned* counts = &dc->pend_low;
+  const int* gate = &dc->expand;
+  // (returns at once unless a lazy-list loop pushes after a pull sweep)
+  if (half) k_collect_signs_c<1><<<g, kThreads, 0, ctx->stream>>>(dc);
+  else k_collect_signs_c<0><<<g, kThreads, 0, ctx->stream>>>(dc);
+  count_launch(ctx);
   if (half) {
     k_expand_low_c<1><<<g, kThreads, 0, ctx->stream>>>(counts, gate);
     k_expand_high_c<1><<<g, kThreads, 0, ctx->stream>>>(counts, gate);

@@ -80,6 +80,10 @@ struct SweepArgs {
   // is already in hand.  `written` then counts the copy-throughs still owed
   // (2 after a pending write: the older buffer's sign bit must be cleared).
   int pull_fused;
+  // With pull_fused: a pull sweep does not append the push-expansion lists
+  // (the next expansion is usually a pull again); a push decided after it
+  // collects them from the contributions' sign bits (k_collect_signs_c).
+  int lazy_lists;
   int copy_all;       // updateRanks primitive: copy-through every unaffected
   // owned work (multi-GPU rank; the whole graph on one GPU): vertices
   // [v_lo, v_hi), single slices [ss_lo, ss_hi), multi slices [ms_lo, ms_hi)
@@ -102,10 +106,11 @@ struct SweepArgs {
 
 // Device-driven convergence loop state (convergeLoop's bookkeeping,
 // engine.cpp:71-92, kept on the device so no iteration waits on the host).
-enum { kExpandNone = 0, kExpandPush = 1, kExpandPull = 2 };
+enum { kExpandNone = 0, kExpandPush = 1, kExpandPull = 2, kExpandPushCollect = 3 };
 struct LoopCtl {
   int done, converged, iterations, max_iter;
   int check, frontier, flagged, expand;
+  int lazy_lists, pad_;  // pull sweeps skip the pending-list appends (SweepArgs::lazy_lists)
   unsigned pend_low, pend_high;  // push-expansion list sizes of the last sweep
   double tol, final_delta;
   unsigned long long affected, edges, m, n;
@@ -142,7 +147,7 @@ SweepPlan plan_sweep(dynpr_context* ctx, const SweepArgs& a, bool flagged, bool 
 // bank (upload_loop_args, stream-ordered), for capture into the loop graph.
 void launch_sweep_ind(dynpr_context* ctx, const SweepPlan& p, int half, uint32_t* tick);
 void launch_pull_ind(dynpr_context* ctx, const SweepPlan& p, int half);
-void launch_expand_ind(dynpr_context* ctx, int half, const unsigned* counts, const int* gate);
+void launch_expand_ind(dynpr_context* ctx, int half, LoopCtl* dc);
 void upload_loop_args(dynpr_context* ctx, const SweepArgs* host_pinned_half2);
 // The multi-chunk sweep kernels, whose nodes get the highest launch priority
 // in the loop graph (they run concurrently with the single-vertex kernel).

@@ -46,13 +46,17 @@ def test_in_sweep_pull_matches_reference(dp, oracle_lib, monkeypatch, rmat16, fr
     ref = O.dynamic_frontier(og2, ogt2, dels, ins, base.ranks, pruning=pruning)
     monkeypatch.setenv("DYNPR_SWEEP", sweep)
     runs = {}
+    # DYNPR_LAZY_LISTS=0: pull sweeps append the push lists anyway (default:
+    # they are collected from the sign bits when a push follows a pull)
     for mode, env in (("fused", {"DYNPR_HOST_LOOP": "0", "DYNPR_PULL_FUSED": "1"}),
+                      ("fused-eager-lists", {"DYNPR_HOST_LOOP": "0", "DYNPR_LAZY_LISTS": "0"}),
                       ("separate", {"DYNPR_HOST_LOOP": "0", "DYNPR_PULL_FUSED": "0"}),
                       ("host", {"DYNPR_HOST_LOOP": "1"})):
         for k, v in env.items():
             monkeypatch.setenv(k, v)
         runs[mode] = dp.dynamic_frontier(g2, gt2, dels, ins, base.ranks, pruning=pruning)
         monkeypatch.delenv("DYNPR_PULL_FUSED", raising=False)
+        monkeypatch.delenv("DYNPR_LAZY_LISTS", raising=False)
     for r in runs.values():
         _same(r, ref)
     # a second solve on the same context (stale sign bits in the reused
