@@ -232,6 +232,13 @@ dynpr_status dynpr_graph_destroy(dynpr_graph* g);
 dynpr_status dynpr_graph_rmat(dynpr_context* ctx, uint32_t scale,
                               uint32_t edge_factor, double a, double b,
                               double c, uint64_t seed, dynpr_graph** out);
+/* Kronecker graph in the Graph500 style: the RMAT draws above with the
+ * Graph500 initiator (a, b, c) = (0.57, 0.19, 0.19), then every vertex id
+ * mapped through a seeded bijection of [0, 2^scale) (odd multiplications,
+ * an added constant and xor-shifts modulo 2^scale) so the hubs are spread
+ * over the id space; buildCsr + addSelfLoops. */
+dynpr_status dynpr_graph_kronecker(dynpr_context* ctx, uint32_t scale, uint32_t edge_factor, uint64_t seed,
+                                   dynpr_graph** out);
 
 /* Builds (or reuses) the engine layout of the pair (gT, gF) for degree
  * threshold `threshold`: vertices relabelled by in-degree, SELL-32 segment

@@ -179,6 +179,7 @@ class Oracle:
             L.orc_rng_double.restype = C.c_double
             L.orc_linf.argtypes = [_dp, _dp, C.c_uint64]
             L.orc_l1.argtypes = [_dp, _dp, C.c_uint64]
+            L.orc_kronecker_edges.argtypes = [C.c_uint32, C.c_uint64, C.c_uint64, _u32p, _u32p]
             L.orc_rmat_edges.argtypes = [C.c_uint32, C.c_uint64, C.c_double, C.c_double,
                                          C.c_double, C.c_uint64, _u32p, _u32p]
         else:
@@ -298,6 +299,15 @@ class Oracle:
 
     def rng(self, seed: int):
         return PortRng(self, seed) if self.kind == "port" else RefRng(self, seed)
+
+    def kronecker_edges(self, scale: int, count: int, seed=42):
+        """Graph500-style Kronecker edges: RMAT draws + the seeded id bijection
+        of the device generator (dynpr_graph_kronecker)."""
+        src = np.zeros(max(count, 1), np.uint32)
+        dst = np.zeros(max(count, 1), np.uint32)
+        port = self if self.kind == "port" else Oracle("port")
+        port.L.orc_kronecker_edges(scale, count, seed, _ptr(src, _u32p), _ptr(dst, _u32p))
+        return src[:count], dst[:count]
 
     def rmat_edges(self, scale: int, count: int, a=0.57, b=0.19, c=0.19, seed=42):
         src = np.zeros(max(count, 1), np.uint32)

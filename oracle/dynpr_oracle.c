@@ -763,6 +763,33 @@ orc_graph* orc_random_graph(uint64_t* state, uint32_t n, uint64_t pairs) {
   return g;
 }
 
+/* Graph500-style Kronecker edge list (no reference counterpart): the RMAT
+ * draws of orc_rmat_edges with (a, b, c) = (0.57, 0.19, 0.19), every id
+ * mapped through the seeded bijection of [0, 2^scale) the CUDA generator
+ * uses (graph.cu Scramble: keys from a SplitMix64 stream of
+ * deriveSeed(seed, 2^40), odd multipliers, xor-shifts by ceil(s/2), ceil(s/3)). */
+static uint32_t orc_scramble(uint32_t x, uint64_t k1, uint64_t k2, uint64_t k3, uint64_t mask, uint32_t sh1,
+                             uint32_t sh2) {
+  uint64_t y = ((uint64_t)x * k1) & mask;
+  y ^= y >> sh1;
+  y = (y * k2 + k3) & mask;
+  y ^= y >> sh2;
+  return (uint32_t)y;
+}
+void orc_rmat_edges(uint32_t scale, uint64_t count, double a, double b, double c, uint64_t seed, uint32_t* src,
+                    uint32_t* dst);
+void orc_kronecker_edges(uint32_t scale, uint64_t count, uint64_t seed, uint32_t* src, uint32_t* dst) {
+  orc_rmat_edges(scale, count, 0.57, 0.19, 0.19, seed, src, dst);
+  orc_rng key = {orc_derive_seed(seed, 1ull << 40)};
+  const uint64_t k1 = rng_next(&key) | 1ull, k2 = rng_next(&key) | 1ull, k3 = rng_next(&key);
+  const uint64_t mask = (1ull << scale) - 1;
+  const uint32_t sh1 = (scale + 1) / 2, sh2 = (scale + 2) / 3;
+  for (uint64_t i = 0; i < count; ++i) {
+    src[i] = orc_scramble(src[i], k1, k2, k3, mask, sh1, sh2);
+    dst[i] = orc_scramble(dst[i], k1, k2, k3, mask, sh1, sh2);
+  }
+}
+
 /* Synthetic RMAT edge list (no reference counterpart): edge i
  * draws `scale` quadrants from SplitMix64(deriveSeed(seed, i)) with
  * cumulative thresholds t1=a, t2=a+b, t3=a+b+c.  Same as the CUDA generator. */

@@ -682,6 +682,14 @@ def rmat_graph(scale: int, edge_factor: int = 16, a: float = 0.57, b: float = 0.
                       float(c), int(seed))
 
 
+def kronecker_graph(scale: int, edge_factor: int = 16, seed: int = 42, ctx: Optional[Context] = None) -> CsrGraph:
+    """Graph500-style Kronecker graph generated on the device: the RMAT draws
+    of rmat_graph with the Graph500 initiator, vertex ids scrambled by a
+    seeded bijection (dynpr_graph_kronecker), self-loops added."""
+    ctx = _ctx(ctx)
+    return _new_graph(N.lib().dynpr_graph_kronecker, ctx, int(scale), int(edge_factor), int(seed))
+
+
 # ---- workload (workload.hpp:189-197) --------------------------------------------
 def batch_size_from_fraction(fraction: float, total: int) -> int:
     return int(N.lib().dynpr_batch_size_from_fraction(float(fraction), int(total)))

@@ -147,6 +147,7 @@ PROTOTYPES = {
     "dynpr_graph_has_edge": (_i, [_vp, _vp, _u32, _u32, _ip]),
     "dynpr_graph_destroy": (_i, [_vp]),
     "dynpr_graph_rmat": (_i, [_vp, _u32, _u32, _d, _d, _d, _u64, _pvp]),
+    "dynpr_graph_kronecker": (_i, [_vp, _u32, _u32, _u64, _pvp]),
     "dynpr_graph_prepare": (_i, [_vp, _vp, _vp, _u32, _i, _dp]),
     "dynpr_batch_size_from_fraction": (_u64, [_d, _u64]),
     "dynpr_derive_seed": (_u64, [_u64, _u64]),

@@ -189,6 +189,20 @@ struct LoopGraphCache {
 };
 constexpr size_t kLoopCacheMax = 16;
 
+// expandAffected direction (both loops): pull when push_cost x the pending
+// vertices' out-edges exceed the in-edges of the vertices the sweep left
+// unaffected (what a pull scans).  A pushed edge is a dependent id load plus
+// a flag read-modify-write, a pulled one a gather the in-sweep pull merges
+// into the sweep it precedes: push_cost 4 (profiles/r02/push_cost_ab.txt:
+// RMAT-20 1e-7 0.75 -> 0.50 ms, 1e-5 1.00 -> 0.83, uniform n=2^20 1e-4 /
+// 1e-3 0.85 -> 0.63 / 0.94 -> 0.74, RMAT-24 unchanged).  DYNPR_PUSH_COST
+// overrides (A/B).
+int push_cost_factor() {
+  const char* e = std::getenv("DYNPR_PUSH_COST");
+  const long v = e ? std::strtol(e, nullptr, 10) : 4L;
+  return v > 0 ? (int)v : 1;
+}
+
 // Device-loop solves of one GPU in this process go one at a time (the
 // constant-bank argument slots are per device); captures too.
 std::mutex& loop_slot_lock(int device) {
@@ -315,6 +329,7 @@ void run_device_loop(dynpr_context* ctx, const SolveSpec& sp, const SweepArgs& a
     if (plan.pull_fused) half[k].np = nullptr;
   }
   h.lazy_lists = lazy ? 1 : 0;
+  h.push_cost = push_cost_factor();
   LoopGraph& lg = loop_graph(ctx, plan, h.frontier, dc, red);
 
   // per-solve state: loop control + both halves' arguments, one upload
@@ -659,7 +674,7 @@ void solve_impl(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynp
       const uint64_t pull_bound = gT->m > r.edges ? gT->m - r.edges : 0;
       // multi-GPU: pending flags are replicated, each rank pulls into its
       // own rows (no remote writes)
-      if (dist || r.pend_edges > pull_bound) {
+      if (dist || r.pend_edges * (uint64_t)push_cost_factor() > pull_bound) {
         launch_pull_expand(ctx, a);
         ctx->pull_expansions += 1;
       } else {

@@ -33,8 +33,45 @@ __device__ __forceinline__ uint64_t splitmix_next(uint64_t& s) {
   return z ^ (z >> 31);
 }
 
+// Graph500-style vertex scrambling for the Kronecker generator: a seeded
+// bijection of [0, 2^scale) (odd multiplications, an added constant and
+// xor-shifts, all modulo 2^scale), so hub ids are spread over the id space
+// instead of sitting at the small ids RMAT favours.
+struct Scramble {
+  uint64_t k1, k2, k3, mask;
+  uint32_t sh1, sh2;
+  __host__ __device__ uint32_t operator()(uint32_t x) const {
+    uint64_t y = ((uint64_t)x * k1) & mask;
+    y ^= y >> sh1;
+    y = (y * k2 + k3) & mask;
+    y ^= y >> sh2;
+    return (uint32_t)y;
+  }
+};
+
+// The keys of the bijection from the seed (SplitMix64 stream seeded with
+// deriveSeed(seed, 2^40), rng.hpp:44-47); multipliers forced odd.
+Scramble kronecker_scramble(uint32_t scale, uint64_t seed) {
+  uint64_t st = seed ^ (0xD1B54A32D192ED03ULL * ((1ull << 40) + 1));
+  auto next = [&st] {
+    uint64_t z = (st += 0x9E3779B97F4A7C15ULL);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+  };
+  st = next();  // deriveSeed(seed, 2^40): the stream's seed
+  Scramble sc;
+  sc.k1 = next() | 1ull;
+  sc.k2 = next() | 1ull;
+  sc.k3 = next();
+  sc.mask = scale >= 64 ? ~0ull : (1ull << scale) - 1;
+  sc.sh1 = (scale + 1) / 2;
+  sc.sh2 = (scale + 2) / 3;
+  return sc;
+}
+
 __global__ void k_rmat(uint64_t count, uint32_t scale, double t1, double t2,
-                       double t3, uint64_t seed, uint32_t* src, uint32_t* dst) {
+                       double t3, uint64_t seed, uint32_t* src, uint32_t* dst, int scramble, Scramble sc) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
        i += (uint64_t)gridDim.x * blockDim.x) {
     uint64_t s0 = seed ^ (0xD1B54A32D192ED03ULL * (i + 1));
@@ -47,8 +84,8 @@ __global__ void k_rmat(uint64_t count, uint32_t scale, double t1, double t2,
       u = (u << 1) | bu;
       v = (v << 1) | bv;
     }
-    src[i] = u;
-    dst[i] = v;
+    src[i] = scramble ? sc(u) : u;
+    dst[i] = scramble ? sc(v) : v;
   }
 }
 
@@ -1334,37 +1371,47 @@ dynpr_status dynpr_graph_destroy(dynpr_graph* g) {
   });
 }
 
+static void generate_rmat(dynpr_context* ctx, uint32_t scale, uint32_t edge_factor, double a, double b, double c,
+                          uint64_t seed, bool scramble, dynpr_graph** out) {
+  if (!ctx || !out) invalid("null argument");
+  if (scale < 1 || scale > 31) invalid("rmat: scale must be in [1,31]");
+  if (!(a >= 0 && b >= 0 && c >= 0 && a + b + c <= 1.0)) invalid("rmat: bad probabilities");
+  bind_device(ctx);
+  const uint32_t n = 1u << scale;
+  const uint64_t cnt = (uint64_t)edge_factor << scale;
+  uint32_t* s = ctx->stage_a.as<uint32_t>(cnt + 1);
+  uint32_t* d = ctx->stage_b.as<uint32_t>(cnt + 1);
+  Scramble sc = kronecker_scramble(scale, seed);
+  if (cnt) {
+    k_rmat<<<grid_for(cnt, 256, 1 << 18), 256, 0, ctx->stream>>>(cnt, scale, a, a + b, a + b + c, seed, s, d,
+                                                                 scramble ? 1 : 0, sc);
+    check_launch();
+    count_launch(ctx);
+  }
+  dynpr_graph* raw = build_from_device_edges(ctx, n, s, d, cnt);
+  // free the generator's staging before the self-loop pass needs memory
+  dynpr_graph* looped = nullptr;
+  try {
+    graph_apply_batch_impl(ctx, raw, nullptr, nullptr, 0, nullptr, nullptr, 0, false, nullptr, nullptr,
+                           nullptr, nullptr, &looped, nullptr, nullptr);
+  } catch (...) {
+    destroy_graph(raw);
+    throw;
+  }
+  destroy_graph(raw);
+  *out = looped;
+}
+
 dynpr_status dynpr_graph_rmat(dynpr_context* ctx, uint32_t scale, uint32_t edge_factor, double a,
                               double b, double c, uint64_t seed, dynpr_graph** out) {
   NvtxRange nvtx__("dynpr_graph_rmat");
-  return api_guard([&] {
-    if (!ctx || !out) invalid("null argument");
-    if (scale < 1 || scale > 31) invalid("rmat: scale must be in [1,31]");
-    if (!(a >= 0 && b >= 0 && c >= 0 && a + b + c <= 1.0)) invalid("rmat: bad probabilities");
-    bind_device(ctx);
-    const uint32_t n = 1u << scale;
-    const uint64_t cnt = (uint64_t)edge_factor << scale;
-    uint32_t* s = ctx->stage_a.as<uint32_t>(cnt + 1);
-    uint32_t* d = ctx->stage_b.as<uint32_t>(cnt + 1);
-    if (cnt) {
-      k_rmat<<<grid_for(cnt, 256, 1 << 18), 256, 0, ctx->stream>>>(cnt, scale, a, a + b, a + b + c, seed, s,
-                                                                   d);
-      check_launch();
-      count_launch(ctx);
-    }
-    dynpr_graph* raw = build_from_device_edges(ctx, n, s, d, cnt);
-    // free the generator's staging before the self-loop pass needs memory
-    dynpr_graph* looped = nullptr;
-    try {
-      graph_apply_batch_impl(ctx, raw, nullptr, nullptr, 0, nullptr, nullptr, 0, false, nullptr, nullptr,
-                             nullptr, nullptr, &looped, nullptr, nullptr);
-    } catch (...) {
-      destroy_graph(raw);
-      throw;
-    }
-    destroy_graph(raw);
-    *out = looped;
-  });
+  return api_guard([&] { generate_rmat(ctx, scale, edge_factor, a, b, c, seed, false, out); });
+}
+
+dynpr_status dynpr_graph_kronecker(dynpr_context* ctx, uint32_t scale, uint32_t edge_factor, uint64_t seed,
+                                   dynpr_graph** out) {
+  NvtxRange nvtx__("dynpr_graph_kronecker");
+  return api_guard([&] { generate_rmat(ctx, scale, edge_factor, 0.57, 0.19, 0.19, seed, true, out); });
 }
 
 }  // extern "C"

@@ -241,11 +241,12 @@ __device__ __forceinline__ bool folds(const SweepArgs& a, uint32_t len) {
 template <bool NEG = false>
 __device__ __forceinline__ double segment_sum(const uint32_t* __restrict__ sell, uint64_t base, unsigned lane,
                                               uint32_t len, uint32_t Lw, const double* __restrict__ contrib,
-                                              uint32_t self, double cself, unsigned* neg = nullptr) {
+                                              uint32_t self, double cself, unsigned* neg = nullptr,
+                                              bool fold = false) {
   unsigned nb = 0;
   const uint32_t* p = sell + base + 4u * lane;  // element k at p + 32*k (k % 4 == 0)
   const uint4 z = make_uint4(0, 0, 0, 0);
-  double c = 0.0;
+  double c = 0.0, tot = 0.0;
   uint4 a = len > 0 ? ld_idx4(p) : z;
   uint4 b = len > 4 ? ld_idx4(p + 128) : z;
   for (uint32_t k = 0; k < Lw; k += 8) {
@@ -256,6 +257,10 @@ __device__ __forceinline__ double segment_sum(const uint32_t* __restrict__ sell,
       x[q] = (k + q < len) ? ld_contrib(contrib, u[q], self, cself) : 0.0;
     a = (k + 8 < len) ? ld_idx4(p + 32ull * (k + 8)) : z;
     b = (k + 12 < len) ? ld_idx4(p + 32ull * (k + 12)) : z;
+    if (fold && k != 0 && (k & (kAccumChunk - 1)) == 0 && k < len) {
+      tot = __dadd_rn(tot, c);
+      c = 0.0;
+    }
 #pragma unroll
     for (uint32_t q = 0; q < 8; ++q) {
       if (k + q < len) c = __dadd_rn(c, fabs(x[q]));
@@ -263,7 +268,7 @@ __device__ __forceinline__ double segment_sum(const uint32_t* __restrict__ sell,
     }
   }
   if (NEG) *neg = nb >> 31;
-  return c;
+  return fold ? __dadd_rn(tot, c) : c;
 }
 
 // The segment sum of a warp holding a folding lane (folds(): derived layouts
@@ -381,13 +386,11 @@ __device__ __forceinline__ void b_sweep_single(const SweepArgs& a) {
         neg = (unsigned)__double2hiint(cself) >> 31;
       }
     } else if (Lw) {
-      const bool fold = folds(a, len);
-      if (__any_sync(kFull, fold))
-        c = segment_sum_folding(a.sell_s, sb, lane, len, Lw, a.contrib_prev, v, cself, fold, &neg);
-      else if (pull)
-        c = segment_sum<true>(a.sell_s, sb, lane, len, Lw, a.contrib_prev, v, cself, &neg);
+      // (the split kernel keeps the fold inline: 48 registers either way)
+      if (pull)
+        c = segment_sum<true>(a.sell_s, sb, lane, len, Lw, a.contrib_prev, v, cself, &neg, folds(a, len));
       else
-        c = segment_sum(a.sell_s, sb, lane, len, Lw, a.contrib_prev, v, cself);
+        c = segment_sum(a.sell_s, sb, lane, len, Lw, a.contrib_prev, v, cself, nullptr, folds(a, len));
     }
     const bool newly = scan && neg;
     bool pend = false, lowout = false;
@@ -1136,7 +1139,8 @@ __global__ void k_loop_end(LoopCtl* c, SweepRed* red, cudaGraphConditionalHandle
     } else if (c->frontier) {
       // direction-optimising expandAffected (same rule as the host loop)
       const unsigned long long pull_bound = c->m > r.edges ? c->m - r.edges : 0ull;
-      c->expand = r.pend_edges > pull_bound ? kExpandPull : (no_lists ? kExpandPushCollect : kExpandPush);
+      const unsigned long long cost = c->push_cost > 0 ? (unsigned long long)c->push_cost : 1ull;
+      c->expand = r.pend_edges * cost > pull_bound ? kExpandPull : (no_lists ? kExpandPushCollect : kExpandPush);
       c->pend_low = no_lists ? 0u : r.pend_low;
       c->pend_high = no_lists ? 0u : r.pend_high;
     }
@@ -1504,6 +1508,27 @@ static void join_aux(dynpr_context* ctx) {
   DYNPR_CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
 }
 
+// The two concurrently launched split kernels share every SM: their
+// persistent grids are capped at kMsegPerSm / kSinglePerSm blocks per SM
+// (both fit one SM's registers), instead of the first launched kernel
+// filling the GPU at full occupancy and the other running in its tail.
+// The multi-chunk slices are request-bound and need few warps, the single
+// slices are latency-bound and take the rest (profiles/r02/grid_ab_*.txt:
+// RMAT-24 Static 60.4 -> 56.0 ms, RMAT-26 259.5 -> 256.2, Kronecker-25
+// 121.4 -> 118.5).  DYNPR_MSEG_BPS / DYNPR_SINGLE_BPS override (0: no cap).
+constexpr unsigned kMsegPerSm = 2, kSinglePerSm = 3;
+static void cap_blocks(dynpr_context* ctx, const char* var, unsigned def_bps, unsigned& grid) {
+  const char* e = std::getenv(var);
+  const unsigned bps = e ? (unsigned)std::strtoul(e, nullptr, 10) : def_bps;
+  const unsigned cap = bps * (unsigned)ctx->num_sms;
+  if (grid && cap && grid > cap) grid = cap;
+}
+static void cap_split_grids(dynpr_context* ctx, unsigned& g_mseg, unsigned& g_single) {
+  if (!g_mseg || !g_single) return;  // one kernel alone: full occupancy
+  cap_blocks(ctx, "DYNPR_MSEG_BPS", kMsegPerSm, g_mseg);
+  cap_blocks(ctx, "DYNPR_SINGLE_BPS", kSinglePerSm, g_single);
+}
+
 void launch_sweep(dynpr_context* ctx, const SweepArgs& a, bool flagged, bool closed) {
   cudaStream_t st = ctx->stream;
   const uint64_t mv = (a.M < a.v_hi ? a.M : a.v_hi) > a.v_lo ? (a.M < a.v_hi ? a.M : a.v_hi) - a.v_lo : 0;
@@ -1514,10 +1539,12 @@ void launch_sweep(dynpr_context* ctx, const SweepArgs& a, bool flagged, bool clo
 #define DYNPR_SWEEP(F, C)                                                                           \
   do {                                                                                              \
     const bool par = n_ms && n_ss;  /* multi chunks on aux, concurrent with the single slices */   \
+    unsigned gm = n_ms ? sweep_grid(ctx, k_sweep_mseg<F>, n_ms, smem) : 0u;                         \
+    unsigned gs = n_ss ? sweep_grid(ctx, k_sweep_single<F, C>, n_ss, smem) : 0u;                    \
+    cap_split_grids(ctx, gm, gs);                                                                   \
     if (n_ms) {                                                                                     \
       cudaStream_t ms = par ? fork_aux(ctx) : st;                                                   \
-      k_sweep_mseg<F><<<sweep_grid(ctx, k_sweep_mseg<F>, n_ms, smem), kSweepThreads, smem,          \
-                        ms>>>(a);                                                                   \
+      k_sweep_mseg<F><<<gm, kSweepThreads, smem, ms>>>(a);                                         \
       ++launched;                                                                                   \
     }                                                                                               \
     if (mv) { /* the ordered combine follows the chunks on the same stream */                     \
@@ -1525,8 +1552,7 @@ void launch_sweep(dynpr_context* ctx, const SweepArgs& a, bool flagged, bool clo
       ++launched;                                                                                   \
     }                                                                                               \
     if (n_ss) {                                                                                     \
-      k_sweep_single<F, C><<<sweep_grid(ctx, k_sweep_single<F, C>, n_ss, smem), kSweepThreads,      \
-                             smem, st>>>(a);                                                        \
+      k_sweep_single<F, C><<<gs, kSweepThreads, smem, st>>>(a);                                     \
       ++launched;                                                                                   \
     }                                                                                               \
     if (par) join_aux(ctx);                                                                         \
@@ -1596,6 +1622,7 @@ SweepPlan plan_sweep(dynpr_context* ctx, const SweepArgs& a, bool flagged, bool 
     } else {                                                                             \
       if (n_ms) p.g_mseg = pgrid(ctx, k_sweep_mseg_c<F, 0>, wms);                        \
       if (n_ss) p.g_single = pgrid(ctx, k_sweep_single_c<F, C, 0>, wss);                 \
+      cap_split_grids(ctx, p.g_mseg, p.g_single);                                        \
       if (mv) p.g_mfinal = grid_for(mv, kThreads);                                       \
     }                                                                                    \
   } while (0)

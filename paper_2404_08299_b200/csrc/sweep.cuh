@@ -110,7 +110,8 @@ enum { kExpandNone = 0, kExpandPush = 1, kExpandPull = 2, kExpandPushCollect = 3
 struct LoopCtl {
   int done, converged, iterations, max_iter;
   int check, frontier, flagged, expand;
-  int lazy_lists, pad_;  // pull sweeps skip the pending-list appends (SweepArgs::lazy_lists)
+  int lazy_lists;        // pull sweeps skip the pending-list appends (SweepArgs::lazy_lists)
+  int push_cost;         // direction rule: push when push_cost * pending out-edges <= unaffected in-edges
   unsigned pend_low, pend_high;  // push-expansion list sizes of the last sweep
   double tol, final_delta;
   unsigned long long affected, edges, m, n;

@@ -11,7 +11,9 @@ cores) on the same inputs, with a parity check on the compared solves.
               reference generator), 5 reps per size: DF-P and Static ms/solve
               on the same updated graph; the reference's DF-P + Static for the
               first rep of every size (parity: iterations, ranks bitwise).
-  configs[3]  Static + DF-P (1e-4 batch) on Kronecker scale-27 (~2.1 B edges)
+  configs[3]  Static + DF-P (1e-4 batch) on Kronecker scale-27 (~2.1 B edges;
+              Graph500 initiator with the seeded vertex-id scramble,
+              dynpr_graph_kronecker)
               on ONE B200 (the box has one GPU; the partitioned engine is
               exercised by bench.py --gpus N); reference: a bounded sample of
               static sweeps.
@@ -132,7 +134,7 @@ def config1(O, kind, cores, reps=5, seed=42):
 
 def config3(O, kind, cores, scale=27, seed=42, ref_sweeps=3):
     t0 = time.perf_counter()
-    g0 = dp.rmat_graph(scale, seed=seed)
+    g0 = dp.kronecker_graph(scale, seed=seed)  # Graph500 initiator + id scramble
     gt0 = dp.transpose(g0)
     build_s = time.perf_counter() - t0
     n, m = g0.vertex_count, g0.edge_count
@@ -160,7 +162,8 @@ def config3(O, kind, cores, scale=27, seed=42, ref_sweeps=3):
     ds = sorted((dp.dynamic_frontier(g, gt, b.deletions, b.insertions, prev_dev, pruning=True) for _ in range(3)),
                 key=lambda r: r.device_ms)
     s, d = ss[1], ds[1]
-    out = {"workload": "configs[3] Kronecker-%d on one B200" % scale, "n": n, "m": m,
+    out = {"workload": "configs[3] Kronecker-%d (Graph500 initiator, scrambled ids) on one B200" % scale,
+           "n": n, "m": m,
            "build_s": build_s, "ingest_ms": ingest_ms, "layout_ms": lay,
            "ingest_cold_ms": ingest_cold_ms, "layout_cold_ms": lay_cold,
            "static": {"ms_per_solve": s.device_ms, "iterations": s.iterations,

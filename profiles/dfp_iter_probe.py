@@ -12,11 +12,21 @@ import numpy as np
 import paper_2404_08299_b200 as dp
 from paper_2404_08299_b200 import _native as N
 
-scale = int(sys.argv[1]) if len(sys.argv) > 1 else 24
+arg = sys.argv[1] if len(sys.argv) > 1 else "24"
 frac = float(sys.argv[2]) if len(sys.argv) > 2 else 1e-4
 if len(sys.argv) > 3:
     os.environ["DYNPR_SWEEP"] = sys.argv[3]  # split | fused
-g = dp.rmat_graph(scale); gt = dp.transpose(g)
+if arg.startswith("u"):  # uniform random graph (configs[4]'s kind): 2^S vertices, 16 x 2^S pairs + self-loops
+    scale = int(arg[1:])
+    rng = np.random.default_rng(1)
+    nv = 1 << scale
+    src = rng.integers(0, nv, 16 * nv, dtype=np.uint32)
+    dst = rng.integers(0, nv, 16 * nv, dtype=np.uint32)
+    g = dp.add_self_loops(dp.build_csr((src, dst), nv))
+else:
+    scale = int(arg)
+    g = dp.rmat_graph(scale)
+gt = dp.transpose(g)
 base = dp.static_pagerank(gt, g)
 b = dp.generate_random_batch(g, dp.batch_size_from_fraction(frac, g.edge_count), 0.8, dp.derive_seed(42, 0))
 g2, gt2 = dp.apply_batch_pair(g, gt, b)

@@ -7,10 +7,20 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import paper_2404_08299_b200 as dp
 
-scale, frac, reps = int(sys.argv[1]), float(sys.argv[2]), int(sys.argv[3])
+arg, frac, reps = sys.argv[1], float(sys.argv[2]), int(sys.argv[3])
 var, vals = sys.argv[4].split("=")
 vals = vals.split(",")
-g = dp.rmat_graph(scale); gt = dp.transpose(g)
+if arg.startswith("u"):  # uniform random graph, 2^S vertices, 16 x 2^S pairs + self-loops
+    import numpy as np
+    scale = int(arg[1:])
+    rng = np.random.default_rng(1)
+    src = rng.integers(0, 1 << scale, 16 << scale, dtype=np.uint32)
+    dst = rng.integers(0, 1 << scale, 16 << scale, dtype=np.uint32)
+    g = dp.add_self_loops(dp.build_csr((src, dst), 1 << scale))
+else:
+    scale = int(arg)
+    g = dp.rmat_graph(scale)
+gt = dp.transpose(g)
 base = dp.static_pagerank(gt, g)
 b = dp.generate_random_batch(g, dp.batch_size_from_fraction(frac, g.edge_count), 0.8, dp.derive_seed(42, 0))
 g2, gt2 = dp.apply_batch_pair(g, gt, b)

@@ -159,6 +159,20 @@ def test_rmat_generator_matches_oracle(dp, oracle_lib, scale):
     assert same_csr(dp.rmat_graph(scale), og)
 
 
+@pytest.mark.parametrize("scale", [1, 6, 13])
+def test_kronecker_generator_matches_oracle(dp, oracle_lib, scale):
+    """Graph500-style Kronecker (RMAT draws + seeded id bijection) on the
+    device == the C port's edges through the reference buildCsr/addSelfLoops;
+    the scramble permutes ids, so the degree multisets equal RMAT's."""
+    src, dst = oracle_lib.kronecker_edges(scale, 16 << scale, seed=7)
+    og = oracle_lib.add_self_loops(oracle_lib.build_csr((src, dst), 1 << scale))
+    kg = dp.kronecker_graph(scale, seed=7)
+    assert same_csr(kg, og)
+    rg = dp.rmat_graph(scale, seed=7)
+    assert kg.edge_count == rg.edge_count
+    assert np.array_equal(np.sort(np.diff(kg.offsets)), np.sort(np.diff(rg.offsets)))
+
+
 @pytest.mark.parametrize("n,off,tgt,msg", [
     (2, [0, 1, 3], [1, 0], "malformed offsets"),
     (3, [0, 1, 0, 2], [1, 0], "non-decreasing"),
