@@ -1508,8 +1508,9 @@ static void join_aux(dynpr_context* ctx) {
   DYNPR_CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
 }
 
-// The two concurrently launched split kernels share every SM: their
-// persistent grids are capped at kMsegPerSm / kSinglePerSm blocks per SM
+// In the device-loop graph the two concurrently launched split kernels share
+// every SM: their persistent grids are capped at kMsegPerSm / kSinglePerSm
+// blocks per SM
 // (both fit one SM's registers), instead of the first launched kernel
 // filling the GPU at full occupancy and the other running in its tail.
 // The multi-chunk slices are request-bound and need few warps, the single
@@ -1539,12 +1540,12 @@ void launch_sweep(dynpr_context* ctx, const SweepArgs& a, bool flagged, bool clo
 #define DYNPR_SWEEP(F, C)                                                                           \
   do {                                                                                              \
     const bool par = n_ms && n_ss;  /* multi chunks on aux, concurrent with the single slices */   \
-    unsigned gm = n_ms ? sweep_grid(ctx, k_sweep_mseg<F>, n_ms, smem) : 0u;                         \
-    unsigned gs = n_ss ? sweep_grid(ctx, k_sweep_single<F, C>, n_ss, smem) : 0u;                    \
-    cap_split_grids(ctx, gm, gs);                                                                   \
+    /* (uncapped grids here: the grid caps of the loop graph made the  */                          \
+    /* host-driven sweep slower, 0.95 -> 1.16 ms on RMAT-24)            */                          \
     if (n_ms) {                                                                                     \
       cudaStream_t ms = par ? fork_aux(ctx) : st;                                                   \
-      k_sweep_mseg<F><<<gm, kSweepThreads, smem, ms>>>(a);                                         \
+      k_sweep_mseg<F><<<sweep_grid(ctx, k_sweep_mseg<F>, n_ms, smem), kSweepThreads, smem,          \
+                        ms>>>(a);                                                                   \
       ++launched;                                                                                   \
     }                                                                                               \
     if (mv) { /* the ordered combine follows the chunks on the same stream */                     \
@@ -1552,7 +1553,8 @@ void launch_sweep(dynpr_context* ctx, const SweepArgs& a, bool flagged, bool clo
       ++launched;                                                                                   \
     }                                                                                               \
     if (n_ss) {                                                                                     \
-      k_sweep_single<F, C><<<gs, kSweepThreads, smem, st>>>(a);                                     \
+      k_sweep_single<F, C><<<sweep_grid(ctx, k_sweep_single<F, C>, n_ss, smem), kSweepThreads,      \
+                             smem, st>>>(a);                                                        \
       ++launched;                                                                                   \
     }                                                                                               \
     if (par) join_aux(ctx);                                                                         \
