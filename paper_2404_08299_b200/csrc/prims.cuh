@@ -333,6 +333,92 @@ __global__ void __launch_bounds__(kPT) k_radix_scatter(const K* __restrict__ key
   }
 }
 
+// Staged scatter (large inputs): the tile is first ordered by digit in
+// shared memory, then written out as runs -- consecutive threads write
+// consecutive positions of one digit bucket, so the stores coalesce (the
+// direct scatter wrote 8-byte keys at up to 32 buckets per warp
+// instruction).  Same stable order as k_radix_scatter.
+template <class K, class V, bool HASV, int RI>
+__global__ void __launch_bounds__(kPT) k_radix_scatter_staged(const K* __restrict__ keys, const V* __restrict__ vals,
+                                                              uint64_t n, int shift, const uint32_t* hist,
+                                                              uint64_t ntiles, K* __restrict__ okeys,
+                                                              V* __restrict__ ovals) {
+  extern __shared__ unsigned char s_dyn[];
+  K* s_k = reinterpret_cast<K*>(s_dyn);
+  V* s_v = reinterpret_cast<V*>(s_dyn + sizeof(K) * kPT * RI);
+  __shared__ uint32_t h[kPW][256];
+  __shared__ uint32_t s_start[256];  // tile-local start of each digit
+  __shared__ uint32_t s_gbase[256];  // global start of each digit for this tile
+  __shared__ uint32_t s_w[kPW];
+  for (int i = threadIdx.x; i < kPW * 256; i += kPT) (&h[0][0])[i] = 0;
+  __syncthreads();
+  const unsigned lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint64_t tb = (uint64_t)blockIdx.x * (kPT * RI);
+  const uint64_t wb = tb + (uint64_t)w * (32 * RI);
+  K k[RI];
+  V v[RI];
+#pragma unroll
+  for (int r = 0; r < RI; ++r) {
+    const uint64_t i = wb + 32 * r + lane;
+    k[r] = i < n ? keys[i] : K(0);
+    if (HASV) v[r] = i < n ? vals[i] : V(0);
+  }
+#pragma unroll
+  for (int r = 0; r < RI; ++r) {
+    const bool valid = wb + 32 * r + lane < n;
+    const unsigned d = valid ? digit_of(k[r], shift) : 0x100u;
+    const unsigned peers = __match_any_sync(kAll, d);
+    if (valid && (int)lane == __ffs(peers) - 1) h[w][d] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  {  // thread t = digit t: tile total, exclusive scan over digits, warps' starts
+    uint32_t tot = 0;
+#pragma unroll
+    for (int j = 0; j < kPW; ++j) tot += h[j][threadIdx.x];
+    const uint32_t inc = warp_incl_scan(tot);
+    if (lane == 31) s_w[w] = inc;
+    __syncthreads();
+    uint32_t off = 0;
+    for (unsigned j = 0; j < w; ++j) off += s_w[j];
+    uint32_t run = off + inc - tot;
+    s_start[threadIdx.x] = run;
+    s_gbase[threadIdx.x] = hist[(uint64_t)threadIdx.x * ntiles + blockIdx.x];
+#pragma unroll
+    for (int j = 0; j < kPW; ++j) {
+      const uint32_t c = h[j][threadIdx.x];
+      h[j][threadIdx.x] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int r = 0; r < RI; ++r) {
+    const bool valid = wb + 32 * r + lane < n;
+    const unsigned d = valid ? digit_of(k[r], shift) : 0x100u;
+    const unsigned peers = __match_any_sync(kAll, d);
+    uint32_t pos = 0;
+    if (valid) pos = h[w][d] + __popc(peers & lt);
+    __syncwarp();
+    if (valid && (int)lane == __ffs(peers) - 1) h[w][d] += __popc(peers);
+    __syncwarp();
+    if (valid) {
+      s_k[pos] = k[r];
+      if (HASV) s_v[pos] = v[r];
+    }
+  }
+  __syncthreads();
+  const uint32_t cnt = n - tb < (uint64_t)(kPT * RI) ? (uint32_t)(n - tb) : (uint32_t)(kPT * RI);
+  for (uint32_t i = threadIdx.x; i < cnt; i += kPT) {
+    const K key = s_k[i];
+    const unsigned d = digit_of(key, shift);
+    const uint32_t g = s_gbase[d] + (i - s_start[d]);
+    okeys[g] = key;
+    if (HASV) ovals[g] = s_v[i];
+  }
+}
+
 }  // namespace
 
 // ---- host entry points ------------------------------------------------------------------
@@ -403,10 +489,16 @@ void radix_pass(dynpr_context* ctx, const K* ks, const V* vs, uint64_t n, int sh
       k_radix_scatter<K, V, false, RI, true><<<(unsigned)ntiles, kPT, 0, st>>>(ks, vs, n, shift, hist, ntiles, kd, vd);
   } else {
     scan_array<uint32_t>(ctx, hist, hist, 256 * ntiles, st);
-    if (vs)
-      k_radix_scatter<K, V, true, RI, false><<<(unsigned)ntiles, kPT, 0, st>>>(ks, vs, n, shift, hist, ntiles, kd, vd);
-    else
-      k_radix_scatter<K, V, false, RI, false><<<(unsigned)ntiles, kPT, 0, st>>>(ks, vs, n, shift, hist, ntiles, kd, vd);
+    const size_t smem = (size_t)kPT * RI * (sizeof(K) + (vs ? sizeof(V) : 0));
+    if (vs) {
+      auto kern = k_radix_scatter_staged<K, V, true, RI>;
+      DYNPR_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      kern<<<(unsigned)ntiles, kPT, smem, st>>>(ks, vs, n, shift, hist, ntiles, kd, vd);
+    } else {
+      auto kern = k_radix_scatter_staged<K, V, false, RI>;
+      DYNPR_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      kern<<<(unsigned)ntiles, kPT, smem, st>>>(ks, vs, n, shift, hist, ntiles, kd, vd);
+    }
   }
   check_launch();
   count_launch(ctx);

@@ -138,6 +138,7 @@ def config3(O, kind, cores, scale=27, seed=42, ref_sweeps=3):
     gt0 = dp.transpose(g0)
     build_s = time.perf_counter() - t0
     n, m = g0.vertex_count, g0.edge_count
+    dp.prepare(gt0, g0)  # the base snapshot of a DF-P stream: layout + relabelled forward rows
     base = dp.static_pagerank(gt0, g0)
     size = dp.batch_size_from_fraction(1e-4, m)
     b = dp.generate_random_batch(g0, size, 0.8, dp.derive_seed(seed, 1000003))

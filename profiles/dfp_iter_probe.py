@@ -53,6 +53,6 @@ for name, fn in (("static", lambda: dp.static_pagerank(gt2, g2)),
         d = dt[i - 1] if i else float("nan")
         w = int(t[i, 3])
         pend = w & ((1 << 62) - 1)
-        ex = {0: "-", 1: "push", 2: "pull"}[(w >> 62) & 3]
+        ex = {0: "-", 1: "push", 2: "pull", 3: "push (lists collected)"}[(w >> 62) & 3]
         print("  it %2d  %7.3f ms  edges %11d (%.2f m)  processed %9d  pending-out %11d  -> %s" % (
             i + 1, d, int(t[i, 1]), int(t[i, 1]) / g2.edge_count, int(t[i, 2]), pend, ex))

@@ -1,6 +1,6 @@
 """Cold vs warm ingest + layout on a Kronecker graph (configs[3]).  Prints
 per-repetition apply_batch_pair / prepare times and free device memory;
-run with DYNPR_ALLOC_DEBUG=1 to see slow pool growth.
+run with DYNPR_ALLOC_DEBUG=1 to see slow pool growth; KRON=0 for RMAT.
     python profiles/kron_ingest_probe.py [scale] [reps]"""
 import os
 import sys
@@ -19,7 +19,7 @@ def free_gb():
     return torch.cuda.mem_get_info()[0] / 2**30
 
 
-g0 = dp.rmat_graph(scale)
+g0 = dp.kronecker_graph(scale) if os.environ.get("KRON", "1") == "1" else dp.rmat_graph(scale)
 gt0 = dp.transpose(g0)
 print("built n=%d m=%d free=%.1f GB" % (g0.vertex_count, g0.edge_count, free_gb()), flush=True)
 t0 = time.perf_counter()
