@@ -203,6 +203,11 @@ int push_cost_factor() {
   return v > 0 ? (int)v : 1;
 }
 
+bool pull_fused_enabled() {
+  const char* pf = std::getenv("DYNPR_PULL_FUSED");
+  return !(pf && pf[0] == '0');
+}
+
 // Device-loop solves of one GPU in this process go one at a time (the
 // constant-bank argument slots are per device); captures too.
 std::mutex& loop_slot_lock(int device) {
@@ -317,8 +322,7 @@ void run_device_loop(dynpr_context* ctx, const SolveSpec& sp, const SweepArgs& a
   // into the next sweep's gathers, pending flags ride in the contributions'
   // sign bits (no pull pass, no pending byte array).
   // DYNPR_PULL_FUSED=0 keeps the separate pull kernels (A/B).
-  const char* pf = std::getenv("DYNPR_PULL_FUSED");
-  const bool want_pf = h.frontier && !(pf && pf[0] == '0');
+  const bool want_pf = h.frontier && pull_fused_enabled();
   for (int k = 0; k < 2; ++k) half[k].pull_fused = want_pf ? 1 : 0;
   const SweepPlan plan = plan_sweep(ctx, half[0], sp.flagged, sp.closed);
   const char* ll = std::getenv("DYNPR_LAZY_LISTS");
@@ -378,8 +382,7 @@ void prewarm_solves(dynpr_context* ctx, const Layout* L, uint64_t m, bool fronti
   }
   std::lock_guard<std::mutex> guard(loop_slot_lock(ctx->device));
   prepare_sweep_launch(ctx);
-  const char* pf = std::getenv("DYNPR_PULL_FUSED");
-  const bool want_pf = !(pf && pf[0] == '0');
+  const bool want_pf = pull_fused_enabled();
   const int kinds[3][2] = {{0, 0}, {1, 1}, {1, 0}};  // (flagged, closed): Static / ND, DF-P, DF
   for (int i = 0; i < (frontier ? 3 : 1); ++i) {
     SweepArgs a = layout_args(L, partials);
@@ -553,6 +556,29 @@ void solve_impl(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynp
     comm->allreduce_red(red, st);
   }
 
+  // The in-sweep pull in the host-driven loop too (single GPU and teams;
+  // not with an observer, which is shown the affected set before each sweep
+  // -- an in-sweep pull completes it only during the sweep): the pending
+  // flags ride in the contributions' sign bits, which a team's contribution
+  // exchange already carries, so a team exchanges no pending-flag bitmap and
+  // runs no separate pull pass.  The decision for the next sweep is a device
+  // int the sweeps read (LoopCtl::expand).
+  const bool host_pf = !device_loop && sp.flagged && !sp.traversal && !obs && pull_fused_enabled();
+  int* expand_dev = nullptr;
+  if (host_pf) {
+    expand_dev = &ctx->loopctl.as<LoopCtl>(1)->expand;
+    launch_set_expand(ctx, expand_dev, kExpandNone);
+    a.pull_fused = 1;
+    a.expand = expand_dev;
+    a.np = nullptr;  // (the batch's flags served the expansion before the loop)
+    if (dist) {
+      a.pend_low = nullptr;  // a team never pushes
+      a.pend_high = nullptr;
+    } else {
+      a.lazy_lists = 1;
+    }
+  }
+
   dynpr_stats res{};
   int cur = 0;  // R[cur] holds the latest iterate ("previous")
   if (device_loop) {
@@ -591,10 +617,16 @@ void solve_impl(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynp
       launch_sweep(ctx, ak, sp.flagged, sp.closed);
       comm->allreduce_red(rk, st);
       if (!fused) comm->allgatherv(CB[cu ^ 1], off_c.data(), st);
-      if (sp.flagged && !sp.traversal) exchange_flags();
+      if (sp.flagged && !sp.traversal && !host_pf) exchange_flags();
       DYNPR_CK(cudaMemcpyAsync(slot + (k & 1), rk, sizeof(SweepRed), cudaMemcpyDeviceToHost, st));
       DYNPR_CK(cudaEventRecord(ctx->ev_rec[k & 1], st));
-      if (sp.flagged && !sp.traversal) launch_pull_expand(ctx, ak);
+      if (sp.flagged && !sp.traversal) {
+        if (host_pf) {
+          if (k == 0) launch_set_expand(ctx, expand_dev, kExpandPull);  // every later sweep pulls
+        } else {
+          launch_pull_expand(ctx, ak);
+        }
+      }
     };
     enqueue(0);
     for (int iter = 0; iter < c.max_iterations; ++iter) {
@@ -614,6 +646,7 @@ void solve_impl(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynp
     }
     cur = res.iterations & 1;
   }
+  bool prev_pull = false;  // the last expansion was a pull (host_pf: the next sweep appends no lists)
   for (int iter = 0; !device_loop && !speculative && iter < c.max_iterations; ++iter) {
     DYNPR_CK(cudaMemsetAsync(red, 0, sizeof(SweepRed), st));
     if (obs && sp.flagged) {
@@ -638,7 +671,7 @@ void solve_impl(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynp
     if (dist) {
       comm->allreduce_red(red, st);  // also the team barrier of the fused exchange
       if (!fused) comm->allgatherv(CB[cur ^ 1], off_c.data(), st);
-      if (sp.flagged && !sp.traversal) exchange_flags();
+      if (sp.flagged && !sp.traversal && !host_pf) exchange_flags();
       if (obs) comm->allgatherv(R[cur ^ 1], off_c.data(), st);
     }
     const SweepRed r = read_red(ctx, red);
@@ -674,12 +707,26 @@ void solve_impl(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynp
       const uint64_t pull_bound = gT->m > r.edges ? gT->m - r.edges : 0;
       // multi-GPU: pending flags are replicated, each rank pulls into its
       // own rows (no remote writes)
-      if (dist || r.pend_edges * (uint64_t)push_cost_factor() > pull_bound) {
+      const bool pull = dist || r.pend_edges * (uint64_t)push_cost_factor() > pull_bound;
+      if (host_pf) {  // a pull happens inside the next sweep
+        if (pull) {
+          launch_set_expand(ctx, expand_dev, kExpandPull);
+        } else {
+          SweepRed lists = r;
+          if (prev_pull) {  // a pull sweep appended no lists: collect them from the sign bits
+            launch_collect_signs(ctx, a, red + 1);
+            lists = read_red(ctx, red + 1);
+          }
+          launch_expand(ctx, Rows{L->begF, L->outdeg, L->tgtF}, va, pl, lists.pend_low, ph, lists.pend_high);
+          launch_set_expand(ctx, expand_dev, kExpandPush);
+        }
+        prev_pull = pull;
+      } else if (pull) {
         launch_pull_expand(ctx, a);
-        ctx->pull_expansions += 1;
       } else {
         launch_expand(ctx, Rows{L->begF, L->outdeg, L->tgtF}, va, pl, r.pend_low, ph, r.pend_high);
       }
+      if (pull) ctx->pull_expansions += 1;
     }
   }
   // result back to old ids (R[cur ^ 1] is free and receives the permuted copy

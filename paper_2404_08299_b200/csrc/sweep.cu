@@ -1161,10 +1161,7 @@ __global__ void k_loop_end(LoopCtl* c, SweepRed* red, cudaGraphConditionalHandle
 // were not appended (SweepArgs::lazy_lists); the sweep's pending vertices
 // are exactly the negative entries of the contributions it wrote.  The
 // counts go straight to the loop state the push kernels read.
-template <int H>
-__global__ void k_collect_signs_c(LoopCtl* c) {
-  const SweepArgs& a = c_loop_args[H];
-  if (c->expand != kExpandPushCollect) return;
+__device__ __forceinline__ void collect_signs_body(const SweepArgs& a, unsigned* cnt_low, unsigned* cnt_high) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < a.n; base += stride) {
     const uint64_t v = base + threadIdx.x;
@@ -1175,9 +1172,15 @@ __global__ void k_collect_signs_c(LoopCtl* c) {
       od = a.outdeg[v];
       lowout = od <= a.T;
     }
-    warp_append_to(pend, lowout, (uint32_t)v, od, a.pend_low, a.pend_high, &c->pend_low, &c->pend_high);
+    warp_append_to(pend, lowout, (uint32_t)v, od, a.pend_low, a.pend_high, cnt_low, cnt_high);
   }
 }
+template <int H>
+__global__ void k_collect_signs_c(LoopCtl* c) {
+  if (c->expand != kExpandPushCollect) return;
+  collect_signs_body(c_loop_args[H], &c->pend_low, &c->pend_high);
+}
+__global__ void k_collect_signs(SweepArgs a, SweepRed* out) { collect_signs_body(a, &out->pend_low, &out->pend_high); }
 
 // ---- markReachable (frontier.cpp:86-121): level-synchronous BFS -------------------
 // Claims a flag byte exactly once (the containing 32-bit word is or-ed, the
@@ -1820,6 +1823,20 @@ void launch_expand(dynpr_context* ctx, Rows rows, uint8_t* va, const uint32_t* p
 void launch_loop_end(dynpr_context* ctx, LoopCtl* c, SweepRed* red, cudaGraphConditionalHandle h,
                      int set_cond) {
   k_loop_end<<<1, 1, 0, ctx->stream>>>(c, red, h, set_cond);
+  check_launch();
+  count_launch(ctx);
+}
+
+__global__ void k_set_int(int* p, int v) { *p = v; }
+void launch_set_expand(dynpr_context* ctx, int* p, int v) {
+  k_set_int<<<1, 1, 0, ctx->stream>>>(p, v);
+  check_launch();
+  count_launch(ctx);
+}
+
+void launch_collect_signs(dynpr_context* ctx, const SweepArgs& a, SweepRed* out) {
+  DYNPR_CK(cudaMemsetAsync(out, 0, sizeof(SweepRed), ctx->stream));
+  k_collect_signs<<<(unsigned)ctx->num_sms * 16, kThreads, 0, ctx->stream>>>(a, out);
   check_launch();
   count_launch(ctx);
 }

@@ -177,6 +177,12 @@ void launch_collect_pending(dynpr_context* ctx, const uint32_t* outdeg, const ui
 void launch_expand(dynpr_context* ctx, Rows rows, uint8_t* va,
                    const uint32_t* pend_low, uint32_t n_low, const uint2* pend_high, uint32_t n_high);
 void launch_pull_expand(dynpr_context* ctx, const SweepArgs& a);
+// Host-loop lazy lists: the pending vertices of the sweep that wrote
+// a.contrib_cur (negative entries) -> a.pend_low / a.pend_high, counts into
+// out->pend_low / pend_high (zeroed here).
+void launch_collect_signs(dynpr_context* ctx, const SweepArgs& a, SweepRed* out);
+// *p = v on the stream (the host loop's expansion decision for the next sweep)
+void launch_set_expand(dynpr_context* ctx, int* p, int v);
 
 // markReachable (frontier.cpp:86-121): flags |= everything reachable from
 // the seeds over the CSR (off, tgt; m edges); seed ids mapped through `inv`

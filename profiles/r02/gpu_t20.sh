@@ -1,0 +1,3 @@
+set -x
+timeout 1200 python -m pytest tests/test_gpu_engine.py tests/test_gpu_loop.py tests/test_gpu_pull.py tests/test_gpu_rank.py -q -x 2>&1 | tail -2
+timeout 1500 python profiles/r02/dfp_bisect_ab.py 24:1e-4,20:1e-4,20:1e-3,18:1e-4 _ab_head .
