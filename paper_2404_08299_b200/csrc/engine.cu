@@ -158,14 +158,14 @@ bool host_loop_forced() {
 }
 
 // convergeLoop (engine.cpp:61-95) run entirely on the device: one CUDA graph
-// whose WHILE node repeats a two-iteration body (even sweep R0->R1, odd
-// sweep R1->R0, so the ping-pong buffers are baked in) --
-//   zero record -> sweep -> k_loop_end -> [push expand | pull expand]
-// -- where k_loop_end does the count / delta / convergence / max-iterations
-// bookkeeping of engine.cpp:79-91 on the device, picks the expansion
-// direction, and sets the loop condition.  Kernels of an iteration after
-// convergence return immediately (done flag), so the odd half of the last
-// body is free.  The host waits once, at the end.
+// whose WHILE node repeats a body of body_sweeps() iterations (even sweeps
+// R0->R1, odd sweeps R1->R0, so the ping-pong buffers are baked in), each
+//   sweep -> k_loop_end -> [collect | push expand]
+// where k_loop_end does the count / delta / convergence / max-iterations
+// bookkeeping of engine.cpp:79-91 on the device, zeroes the record, picks
+// the expansion direction, and sets the loop condition.  Kernels of an
+// iteration after convergence return immediately (done flag), so the rest
+// of the last body is free.  The host waits once, at the end.
 //
 // The kernels read their SweepArgs from constant-bank slots written per solve,
 // so an instantiated graph depends only on the sweep plan (kernel choice and
@@ -188,6 +188,11 @@ struct LoopGraphCache {
   }
 };
 constexpr size_t kLoopCacheMax = 16;
+// Sweeps per WHILE body: the body's re-evaluation costs ~17 us, paid once
+// per body -- 4 for the latency-mode (fused) sweeps of small graphs
+// (RMAT-18 Static 3.03 -> 2.94 ms, RMAT-20 4.25 -> 4.18), 2 for the split
+// sweeps (4 made RMAT-24 Static 56.0 -> 59.8 ms).
+int body_sweeps(const SweepPlan& p) { return p.split ? 2 : 4; }
 
 // expandAffected direction (both loops): pull when push_cost x the pending
 // vertices' out-edges exceed the in-edges of the vertices the sweep left
@@ -245,12 +250,16 @@ LoopGraph& loop_graph(dynpr_context* ctx, const SweepPlan& plan, int frontier, L
   cudaGraph_t body = np.conditional.phGraph_out[0];
   DYNPR_CK(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
   try {
-    for (int k = 0; k < 2; ++k) {
-      launch_sweep_ind(ctx, plan, k, tick);  // the record is zero: before the launch, then k_loop_end
-      launch_loop_end(ctx, dc, red, cond, k == 1);
+    // body_sweeps() per body (an even number: the ping-pong parity of every
+    // position is fixed)
+    const int nb = body_sweeps(plan);
+    for (int k = 0; k < nb; ++k) {
+      const int half = k & 1;
+      launch_sweep_ind(ctx, plan, half, tick);  // the record is zero: before the launch, then k_loop_end
+      launch_loop_end(ctx, dc, red, cond, k == nb - 1);
       if (frontier) {
-        launch_expand_ind(ctx, k, dc);
-        if (!plan.pull_fused) launch_pull_ind(ctx, plan, k);  // (else: inside the next sweep)
+        launch_expand_ind(ctx, half, dc);
+        if (!plan.pull_fused) launch_pull_ind(ctx, plan, half);  // (else: inside the next sweep)
       }
     }
   } catch (...) {
@@ -349,7 +358,7 @@ void run_device_loop(dynpr_context* ctx, const SolveSpec& sp, const SweepArgs& a
   sync(ctx);
   std::memcpy(&h, stage + 1024, sizeof h);
   // launches: the captured body (two iterations) ran once per two sweeps
-  ctx->launches += lg.launches_per_body * (uint64_t)((h.iterations + 1) / 2);
+  ctx->launches += lg.launches_per_body * (uint64_t)((h.iterations + body_sweeps(plan) - 1) / body_sweeps(plan));
   res.iterations = h.iterations;
   res.converged = h.converged;
   res.affected_vertex_iterations = h.affected;
