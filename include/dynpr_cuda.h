@@ -504,6 +504,13 @@ dynpr_status dynpr_debug_sweep_trace(uint64_t* out, uint64_t cap, uint64_t* coun
  * vertices, pending out-edges | expansion direction << 62 (1 push, 2 pull)}.
  * Diagnostics only (profiles/dfp_iter_probe.py). */
 dynpr_status dynpr_debug_loop_trace(uint64_t* out, uint64_t cap, uint64_t* count);
+/* Unit-test entry for the hand-written device primitives (csrc/prims.cuh)
+ * on host arrays: op 0 radix sort of u64 keys (bits = key width), 1 radix
+ * sort of (u32 key, u32 value) pairs, 2 exclusive scan of u64 (total in
+ * *out_count), 3 indices of the nonzero bytes, 4 unique of sorted u64
+ * (count in *out_count). */
+dynpr_status dynpr_debug_prims(dynpr_context* ctx, int op, const void* in, const void* in2, uint64_t count,
+                               int bits, void* out, void* out2, uint64_t* out_count);
 
 #ifdef __cplusplus
 }

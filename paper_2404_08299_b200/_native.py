@@ -187,6 +187,7 @@ PROTOTYPES = {
     "dynpr_report_destroy": (_i, [_vp]),
     "dynpr_debug_sweep_trace": (_i, [_vp, _u64, _u64p]),
     "dynpr_debug_loop_trace": (_i, [_vp, _u64, _u64p]),
+    "dynpr_debug_prims": (_i, [_vp, C.c_int, _vp, _vp, _u64, C.c_int, _vp, _vp, _u64p]),
 }
 
 _lib = None

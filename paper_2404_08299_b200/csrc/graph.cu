@@ -1327,6 +1327,81 @@ dynpr_status dynpr_graph_apply_batch_pair(dynpr_context* ctx, const dynpr_graph*
                             out_gT, missing, duplicate);
 }
 
+// Unit-test entry for the device primitives (prims.cuh) on host arrays.
+dynpr_status dynpr_debug_prims(dynpr_context* ctx, int op, const void* in, const void* in2, uint64_t count,
+                               int bits, void* out, void* out2, uint64_t* out_count) {
+  return api_guard([&] {
+    if (!ctx) invalid("null context");
+    bind_device(ctx);
+    cudaStream_t st = ctx->stream;
+    const uint64_t c1 = count ? count : 1;
+    auto up = [&](const void* h, size_t bytes) {
+      void* d = pool_alloc(ctx, bytes ? bytes : 16);
+      if (bytes) DYNPR_CK(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st));
+      return d;
+    };
+    std::vector<void*> held;
+    auto hold = [&](void* p) { held.push_back(p); return p; };
+    try {
+      auto* num = ctx->scratch64a.as<unsigned long long>(1);
+      uint64_t n_out = count;
+      switch (op) {
+        case 0: {  // radix sort of u64 keys on bits [0, bits)
+          auto* k = static_cast<uint64_t*>(hold(up(in, count * 8)));
+          auto* k2 = static_cast<uint64_t*>(hold(pool_alloc(ctx, c1 * 8)));
+          uint64_t* r = prims::radix_sort<uint64_t, uint32_t>(ctx, k, k2, nullptr, nullptr, count, 0, bits, st);
+          if (count) DYNPR_CK(cudaMemcpyAsync(out, r, count * 8, cudaMemcpyDeviceToHost, st));
+          break;
+        }
+        case 1: {  // radix sort of (u32 key, u32 value) pairs on bits [0, bits)
+          auto* k = static_cast<uint32_t*>(hold(up(in, count * 4)));
+          auto* v = static_cast<uint32_t*>(hold(up(in2, count * 4)));
+          auto* k2 = static_cast<uint32_t*>(hold(pool_alloc(ctx, c1 * 4)));
+          auto* v2 = static_cast<uint32_t*>(hold(pool_alloc(ctx, c1 * 4)));
+          uint32_t* vo = nullptr;
+          uint32_t* r = prims::radix_sort<uint32_t, uint32_t>(ctx, k, k2, v, v2, count, 0, bits, st, &vo);
+          if (count) {
+            DYNPR_CK(cudaMemcpyAsync(out, r, count * 4, cudaMemcpyDeviceToHost, st));
+            DYNPR_CK(cudaMemcpyAsync(out2, vo, count * 4, cudaMemcpyDeviceToHost, st));
+          }
+          break;
+        }
+        case 2: {  // exclusive scan of u64, total in *out_count
+          auto* a = static_cast<uint64_t*>(hold(up(in, count * 8)));
+          prims::scan_array<uint64_t>(ctx, a, a, count, st, reinterpret_cast<uint64_t*>(num));
+          if (count) DYNPR_CK(cudaMemcpyAsync(out, a, count * 8, cudaMemcpyDeviceToHost, st));
+          n_out = read_u64(ctx, num);
+          break;
+        }
+        case 3: {  // indices of the nonzero bytes
+          auto* f = static_cast<uint8_t*>(hold(up(in, count)));
+          auto* o = static_cast<uint32_t*>(hold(pool_alloc(ctx, c1 * 4)));
+          prims::select_if<uint32_t>(ctx, prims::Nonzero<uint8_t>{f}, prims::Iota32{}, count, o, num, st);
+          n_out = read_u64(ctx, num);
+          if (n_out) DYNPR_CK(cudaMemcpyAsync(out, o, n_out * 4, cudaMemcpyDeviceToHost, st));
+          break;
+        }
+        case 4: {  // unique of sorted u64
+          auto* k = static_cast<uint64_t*>(hold(up(in, count * 8)));
+          auto* o = static_cast<uint64_t*>(hold(pool_alloc(ctx, c1 * 8)));
+          prims::unique_sorted<uint64_t>(ctx, k, count, o, num, st);
+          n_out = read_u64(ctx, num);
+          if (n_out) DYNPR_CK(cudaMemcpyAsync(out, o, n_out * 8, cudaMemcpyDeviceToHost, st));
+          break;
+        }
+        default:
+          invalid("dynpr_debug_prims: unknown op");
+      }
+      sync(ctx);
+      if (out_count) *out_count = n_out;
+    } catch (...) {
+      for (void* p : held) pool_free(ctx, p);
+      throw;
+    }
+    for (void* p : held) pool_free(ctx, p);
+  });
+}
+
 dynpr_status dynpr_graph_info(const dynpr_graph* g, uint32_t* n, uint64_t* m) {
   return api_guard([&] {
     if (!g) invalid("null graph");

@@ -227,6 +227,29 @@ def test_rmat_static_and_dfp_bitwise(dp, oracle_lib, scale, frac):
         assert np.array_equal(f, rf)
 
 
+@pytest.mark.parametrize("scale,frac", [(14, 1e-3), (16, 1e-4)])
+def test_kronecker_static_and_dfp_bitwise(dp, oracle_lib, scale, frac):
+    """Graph500-style Kronecker graph (scrambled ids: hubs spread over the
+    id space, so the degree relabel and the SELL slices mix ids unlike
+    RMAT's) -- Static and DF-P bitwise vs the reference."""
+    src, dst = oracle_lib.kronecker_edges(scale, 16 << scale, seed=5)
+    og = oracle_lib.add_self_loops(oracle_lib.build_csr((src, dst), 1 << scale))
+    ogt = oracle_lib.transpose(og)
+    g = dp.kronecker_graph(scale, seed=5)
+    gt = dp.transpose(g)
+    base_ref = oracle_lib.static(ogt, og)
+    base = dp.static_pagerank(gt, g)
+    assert_same_result(base, base_ref)
+    size = oracle_lib.batch_size_from_fraction(frac, og.m)
+    dels, ins = oracle_lib.generate_random_batch(og, size, 0.8, oracle_lib.derive_seed(5, 1))
+    og2, _, _ = oracle_lib.apply_batch(og, dels, ins)
+    ogt2 = oracle_lib.transpose(og2)
+    dp.prepare(gt, g)
+    g2, gt2 = dp.apply_batch_pair(g, gt, dp.BatchUpdate(dels, ins))
+    ref = oracle_lib.dynamic_frontier(og2, ogt2, dels, ins, base_ref.ranks, pruning=True)
+    assert_same_result(dp.dynamic_frontier(g2, gt2, dels, ins, base.ranks, pruning=True), ref)
+
+
 # ---- dynamicTraversal / markReachable (engine.cpp:124-151, frontier.cpp:86-121) ----
 @pytest.mark.parametrize("case", [(131, 400, 4000, 8, 0.8, 2024), (137, 300, 1200, 3, 1.0, 77),
                                   (139, 150, 2500, 6, 0.8, 5), (3, 20000, 200000, 200, 0.8, 9)])
