@@ -1,6 +1,6 @@
 """DF-P device ms (min / median of 6 warm solves, same batch) for several
 package builds, one process per (build, graph, fraction), interleaved.
-    python profiles/r02/dfp_bisect_ab.py scale:frac[,scale:frac] DIR [DIR ...]"""
+    python profiles/r02/dfp_bisect_ab.py scale:frac[,scale:frac] DIR[:VAR=value] ..."""
 import os, subprocess, sys
 CHILD = r'''
 import sys, statistics
@@ -16,7 +16,12 @@ print("%.3f %.3f" % (min(ms), statistics.median(ms)))
 cases = [c.split(":") for c in sys.argv[1].split(",")]
 for scale, frac in cases:
     for rep in range(2):
-        for d in sys.argv[2:]:
+        for spec in sys.argv[2:]:
+            d, _, kv = spec.partition(":")
+            env = dict(os.environ)
+            if kv:
+                k, v = kv.split("=")
+                env[k] = v
             out = subprocess.run([sys.executable, "-c", CHILD, os.path.abspath(d), scale, frac], capture_output=True,
-                                 text=True, cwd="/tmp")
-            print(scale, frac, d, out.stdout.strip() or out.stderr[-300:], flush=True)
+                                 text=True, cwd="/tmp", env=env)
+            print(scale, frac, spec, out.stdout.strip() or out.stderr[-300:], flush=True)
