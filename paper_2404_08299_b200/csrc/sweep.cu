@@ -612,6 +612,12 @@ __global__ void __launch_bounds__(kThreads) k_sweep_mfinal_c() {
 //    shuffle-broadcast sequential sum, and runs the epilogue.
 // Every vertex's sum and epilogue are exactly those of the split kernels.
 constexpr unsigned kLightGrab = 2;
+// Lanes per segment in the heavy items (segment_sum_group): 2 on the most
+// latency-bound graphs (at most kGroupSlicesPerWarp slices per resident warp:
+// the heavy chains halve, RMAT-18 static 2.94 -> 2.51 ms), 1 above (the extra
+// shuffles and spills cost 15-20% on RMAT-20/22; profiles/r02/README.md).
+// DYNPR_HEAVY_LANES=1|2 overrides.
+constexpr uint64_t kGroupSlicesPerWarp = 3;
 // Above this many slices per resident warp the sweep is throughput-bound and
 // the split kernels are used.
 constexpr uint64_t kSplitSlicesPerWarp = 64;
@@ -667,12 +673,72 @@ __device__ __forceinline__ double segment_sum_deep(const uint32_t* __restrict__ 
   return c;
 }
 
+// G lanes per segment (column `col` of a SELL slice) for the heavy items of
+// the latency-mode sweep: in every round of 16G elements the lane of role r
+// gathers elements [16r, 16r + 16) of the round, and the owner (role 0) adds
+// its own 16 and then, in order, each other role's 16 received by shuffles
+// -- the reference's sequential order with G times fewer dependent gather
+// rounds on the chain (a 256-element segment: 16 rounds at G = 1).  Only
+// the owner's return value is the sum; *neg is the group's sign-bit OR.
+template <int G, bool NEG>
+__device__ __forceinline__ double segment_sum_group(const uint32_t* __restrict__ sell, uint64_t base, unsigned col,
+                                                    unsigned role, uint32_t len, uint32_t Lw,
+                                                    const double* __restrict__ contrib, uint32_t self,
+                                                    double cself, unsigned* neg) {
+  const uint32_t* p = sell + base + 4u * col;  // element k at p + 32*k (k % 4 == 0)
+  const uint4 z = make_uint4(0, 0, 0, 0);
+  const unsigned owner = lane_id() - role;
+  double c = 0.0;
+  unsigned nb = 0;
+  uint4 ix[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) ix[j] = (16u * role + 4u * j < len) ? ld_idx4(p + 32ull * (16u * role + 4u * j)) : z;
+  for (uint32_t k = 0; k < Lw; k += 16u * G) {
+    const uint32_t kb = k + 16u * role;
+    double x[16];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t u[4] = {ix[j].x, ix[j].y, ix[j].z, ix[j].w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        x[4 * j + q] = (kb + 4 * j + q < len) ? ld_contrib(contrib, u[q], self, cself) : 0.0;
+    }
+    const uint32_t kn = kb + 16u * G;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) ix[j] = (kn + 4u * j < len) ? ld_idx4(p + 32ull * (kn + 4u * j)) : z;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      if (NEG) nb |= (unsigned)__double2hiint(x[q]);
+      if (role == 0 && k + q < len) c = __dadd_rn(c, fabs(x[q]));
+    }
+#pragma unroll
+    for (int r = 1; r < G; ++r) {
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const double y = __shfl_sync(kFull, x[q], owner + r);
+        if (role == 0 && k + 16u * r + q < len) c = __dadd_rn(c, fabs(y));
+      }
+    }
+  }
+  if (NEG) {
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) nb |= __shfl_xor_sync(kFull, nb, o);
+    *neg = nb >> 31;
+  }
+  return c;
+}
+
 // One single-region slice (the body of k_sweep_single).
 // `pull`: in-sweep pull (SweepArgs::pull_fused) -- unaffected lanes gather
 // too and become affected on a pending source.
-template <bool FLAGGED, bool CLOSED, int Q>
-__device__ __forceinline__ void single_slice(const SweepArgs& a, uint64_t s, unsigned lane, Acc& acc, bool pull) {
-  const uint64_t vv = (uint64_t)a.M + s * 32 + lane;
+// G > 1: the heavy-item form -- part `part` of the slice, its 32/G columns
+// with G lanes each (segment_sum_group); the owner lanes finish the vertices.
+template <bool FLAGGED, bool CLOSED, int Q, int G = 1>
+__device__ __forceinline__ void single_slice(const SweepArgs& a, uint64_t s, unsigned lane, Acc& acc, bool pull,
+                                             unsigned part = 0) {
+  const unsigned col = G == 1 ? lane : part * (32u / G) + lane / G;
+  const unsigned role = G == 1 ? 0u : lane % G;
+  const uint64_t vv = (uint64_t)a.M + s * 32 + col;
   const bool valid = vv < a.n;
   const uint32_t v = (uint32_t)vv;
   const uint32_t deg = valid ? a.indeg[v] : 0u;
@@ -697,14 +763,16 @@ __device__ __forceinline__ void single_slice(const SweepArgs& a, uint64_t s, uns
     }
   } else if (Lw) {
     const bool fold = folds(a, len);
-    if (__any_sync(kFull, fold))
-      c = segment_sum_folding(a.sell_s, a.sbase[s], lane, len, Lw, a.contrib_prev, v, cself, fold, &neg);
-    else  // (frontier sweeps always OR the sign bits: one instantiation, fewer spills)
+    if (__any_sync(kFull, fold))  // (every lane of a group computes its column's sum)
+      c = segment_sum_folding(a.sell_s, a.sbase[s], col, len, Lw, a.contrib_prev, v, cself, fold, &neg);
+    else if (G == 1)  // (frontier sweeps always OR the sign bits: one instantiation, fewer spills)
       c = segment_sum_deep<Q, FLAGGED>(a.sell_s, a.sbase[s], lane, len, Lw, a.contrib_prev, v, cself, &neg);
+    else
+      c = segment_sum_group<G, FLAGGED>(a.sell_s, a.sbase[s], col, role, len, Lw, a.contrib_prev, v, cself, &neg);
   }
   const bool newly = scan && neg;
   bool pend = false, lowout = false;
-  if (valid) {
+  if (valid && role == 0) {
     if (!aff && !newly) {
       copy_through(a, v);
     } else {
@@ -718,9 +786,12 @@ __device__ __forceinline__ void single_slice(const SweepArgs& a, uint64_t s, uns
 
 // One multi-chunk slice: 32 chunk partials; the warp that completes a
 // vertex's last chunk combines and finalises it.
-template <bool FLAGGED, bool CLOSED, int Q>
-__device__ __forceinline__ void multi_slice(const SweepArgs& a, uint64_t s, unsigned lane, Acc& acc, bool pull) {
-  const uint64_t seg = s * 32 + lane;
+template <bool FLAGGED, bool CLOSED, int Q, int G = 1>
+__device__ __forceinline__ void multi_slice(const SweepArgs& a, uint64_t s, unsigned lane, Acc& acc, bool pull,
+                                            unsigned part = 0) {
+  const unsigned col = G == 1 ? lane : part * (32u / G) + lane / G;
+  const unsigned role = G == 1 ? 0u : lane % G;
+  const uint64_t seg = s * 32 + col;
   uint32_t len = 0, v = 0xffffffffu;
   if (seg < a.n_mseg) {
     v = a.mseg_v[seg];
@@ -729,7 +800,7 @@ __device__ __forceinline__ void multi_slice(const SweepArgs& a, uint64_t s, unsi
       len = 0;  // another rank's vertex
     } else if (FLAGGED && !pull && !a.va[v]) {
       len = 0;
-      if (seg == a.pbase[v]) copy_through(a, v);  // first chunk's lane does the copy-through
+      if (seg == a.pbase[v] && role == 0) copy_through(a, v);  // first chunk's owner does the copy-through
     }
   }
   const uint32_t Lw = __reduce_max_sync(kFull, len);
@@ -737,11 +808,15 @@ __device__ __forceinline__ void multi_slice(const SweepArgs& a, uint64_t s, unsi
   double c;
   {  // (a pull sweep's chunk carries "any pending source" in the partial's sign bit)
     unsigned neg = 0;
-    c = segment_sum_deep<Q, FLAGGED>(a.sell_m, a.mbase[s], lane, len, Lw, a.contrib_prev, 0xffffffffu, 0.0, &neg);
+    if (G == 1)
+      c = segment_sum_deep<Q, FLAGGED>(a.sell_m, a.mbase[s], lane, len, Lw, a.contrib_prev, 0xffffffffu, 0.0, &neg);
+    else
+      c = segment_sum_group<G, FLAGGED>(a.sell_m, a.mbase[s], col, role, len, Lw, a.contrib_prev, 0xffffffffu, 0.0,
+                                        &neg);
     if (FLAGGED && pull && neg) c = -c;
   }
   bool last = false;
-  if (len) {
+  if (len && role == 0) {
     __stcg(a.partials + seg, c);
     __threadfence();
     const uint32_t nch = (a.indeg[v] + kAccumChunk - 1) / kAccumChunk;
@@ -792,7 +867,7 @@ __device__ __forceinline__ void multi_slice(const SweepArgs& a, uint64_t s, unsi
   if (FLAGGED && a.pend_low && !(pull && a.lazy_lists)) warp_append(pend, lowout, v, od, a.pend_low, a.pend_high, a.red);
 }
 
-template <bool FLAGGED, bool CLOSED, int QH>
+template <bool FLAGGED, bool CLOSED, int QH, int G>
 __device__ __forceinline__ void fused_body(const SweepArgs& a) {
   if (a.done && *a.done) return;
   Acc acc;
@@ -801,7 +876,7 @@ __device__ __forceinline__ void fused_body(const SweepArgs& a) {
   const uint64_t n_ms = a.ms_hi - a.ms_lo;
   const uint64_t hs_hi = a.ss_heavy < a.ss_hi ? a.ss_heavy : a.ss_hi;
   const uint64_t n_hs = hs_hi > a.ss_lo ? hs_hi - a.ss_lo : 0;
-  const uint64_t n_heavy = n_ms + n_hs;
+  const uint64_t n_heavy = (n_ms + n_hs) * G;  // items: (slice, part of G)
   const unsigned long long t0 = a.trace ? gtimer() : 0ull;
   unsigned long long nh = 0, nl = 0, first = ~0ull, th = 0;
   // heavy items are dealt round-robin to the (all resident) blocks -- item =
@@ -815,10 +890,12 @@ __device__ __forceinline__ void fused_body(const SweepArgs& a) {
     if (t >= n_heavy) break;
     ++nh;
     if (first == ~0ull) first = t;
-    if (t < n_ms)
-      multi_slice<FLAGGED, CLOSED, QH>(a, a.ms_lo + t, lane, acc, pull);
+    const uint64_t item = t / G;
+    const unsigned part = (unsigned)(t % G);
+    if (item < n_ms)
+      multi_slice<FLAGGED, CLOSED, QH, G>(a, a.ms_lo + item, lane, acc, pull, part);
     else
-      single_slice<FLAGGED, CLOSED, QH>(a, a.ss_lo + (t - n_ms), lane, acc, pull);
+      single_slice<FLAGGED, CLOSED, QH, G>(a, a.ss_lo + (item - n_ms), lane, acc, pull, part);
   }
   if (a.trace) th = gtimer();
   const uint64_t l_lo = a.ss_lo + n_hs;
@@ -854,13 +931,13 @@ __device__ __forceinline__ void fused_body(const SweepArgs& a) {
 // 16-deep heavy chains at 4 CTAs per SM.  (A 5-CTA, 8-deep variant was
 // measured: it spills and is no faster on large graphs, where the split
 // kernels win -- profiles/ab_probe.py.)
-template <bool FLAGGED, bool CLOSED>
+template <bool FLAGGED, bool CLOSED, int G>
 __global__ void __launch_bounds__(kSweepThreads, 4) k_sweep_fused(SweepArgs a) {
-  fused_body<FLAGGED, CLOSED, 4>(a);
+  fused_body<FLAGGED, CLOSED, 4, G>(a);
 }
-template <bool FLAGGED, bool CLOSED, int H>
+template <bool FLAGGED, bool CLOSED, int H, int G>
 __global__ void __launch_bounds__(kSweepThreads, 4) k_sweep_fused_c() {
-  fused_body<FLAGGED, CLOSED, 4>(c_loop_args[H]);
+  fused_body<FLAGGED, CLOSED, 4, G>(c_loop_args[H]);
 }
 
 // ---- pull expansion over the SELL in-lists ------------------------------------------
@@ -1317,6 +1394,15 @@ __global__ void k_l1_final(const double* partials, uint64_t nb, double* out) {
 }
 
 // Persistent grid: resident blocks per SM x SMs (queried once per kernel).
+// Lanes per heavy segment for a fused sweep over n_slices slices (see
+// kGroupSlicesPerWarp).
+static int heavy_lanes(dynpr_context* ctx, uint64_t n_slices) {
+  const char* e = std::getenv("DYNPR_HEAVY_LANES");
+  const int forced = e ? std::atoi(e) : 0;
+  if (forced == 1 || forced == 2) return forced;
+  return n_slices <= kGroupSlicesPerWarp * (uint64_t)ctx->num_sms * 32 ? 2 : 1;
+}
+
 template <class K>
 unsigned persistent_grid(dynpr_context* ctx, K kernel, uint64_t work_blocks) {
   constexpr int kSlots = 128;  // > the 36 persistent kernel instantiations
@@ -1577,8 +1663,14 @@ void launch_sweep(dynpr_context* ctx, const SweepArgs& a, bool flagged, bool clo
     af.tick_sm = ctx->tick.as<uint32_t>(kMaxBlocks);
     DYNPR_CK(cudaMemsetAsync(af.tick_sm, 0, kMaxBlocks * sizeof(uint32_t), st));
     const uint64_t wb = (n_ms + n_ss + kSweepWarps - 1) / kSweepWarps;
-#define DYNPR_FUSED(F, C) \
-  k_sweep_fused<F, C><<<persistent_grid(ctx, k_sweep_fused<F, C>, wb), kSweepThreads, 0, st>>>(af)
+    const bool grouped = heavy_lanes(ctx, n_ms + n_ss) == 2;
+#define DYNPR_FUSED(F, C)                                                                      \
+  do {                                                                                         \
+    if (grouped)                                                                               \
+      k_sweep_fused<F, C, 2><<<persistent_grid(ctx, k_sweep_fused<F, C, 2>, wb), kSweepThreads, 0, st>>>(af); \
+    else                                                                                       \
+      k_sweep_fused<F, C, 1><<<persistent_grid(ctx, k_sweep_fused<F, C, 1>, wb), kSweepThreads, 0, st>>>(af); \
+  } while (0)
     if (n_ms + n_ss) {
       if (flagged) {
         if (closed) DYNPR_FUSED(true, true); else DYNPR_FUSED(true, false);
@@ -1619,11 +1711,14 @@ SweepPlan plan_sweep(dynpr_context* ctx, const SweepArgs& a, bool flagged, bool 
   const uint64_t resident_warps = (uint64_t)ctx->num_sms * 32;
   const bool big = (n_ms + n_ss) > kSplitSlicesPerWarp * resident_warps;
   p.split = m == "split" || (m != "fused" && big);
+  p.grouped = !p.split && heavy_lanes(ctx, n_ms + n_ss) == 2;
   const uint64_t wms = (n_ms + kSweepWarps - 1) / kSweepWarps, wss = (n_ss + kSweepWarps - 1) / kSweepWarps;
 #define DYNPR_PLAN(F, C)                                                                 \
   do {                                                                                   \
     if (!p.split) {                                                                      \
-      if (n_ms + n_ss) p.g_fused = pgrid(ctx, k_sweep_fused_c<F, C, 0>, (n_ms + n_ss + kSweepWarps - 1) / kSweepWarps); \
+      if (n_ms + n_ss)                                                                   \
+        p.g_fused = p.grouped ? pgrid(ctx, k_sweep_fused_c<F, C, 0, 2>, (n_ms + n_ss + kSweepWarps - 1) / kSweepWarps) \
+                              : pgrid(ctx, k_sweep_fused_c<F, C, 0, 1>, (n_ms + n_ss + kSweepWarps - 1) / kSweepWarps); \
     } else {                                                                             \
       if (n_ms) p.g_mseg = pgrid(ctx, k_sweep_mseg_c<F, 0>, wms);                        \
       if (n_ss) p.g_single = pgrid(ctx, k_sweep_single_c<F, C, 0>, wss);                 \
@@ -1652,7 +1747,8 @@ static void launch_sweep_c(dynpr_context* ctx, const SweepPlan& p, uint32_t* tic
     if (!p.split) {                                                                              \
       if (p.g_fused) {                                                                           \
         (void)tick; /* zero between sweeps: each block resets its own counter */                \
-        k_sweep_fused_c<F, C, H><<<p.g_fused, kSweepThreads, 0, st>>>();                         \
+        if (p.grouped) k_sweep_fused_c<F, C, H, 2><<<p.g_fused, kSweepThreads, 0, st>>>();       \
+        else k_sweep_fused_c<F, C, H, 1><<<p.g_fused, kSweepThreads, 0, st>>>();                 \
         ++launched;                                                                              \
       }                                                                                          \
     } else {                                                                                     \
@@ -1747,10 +1843,14 @@ uint32_t* sweep_tick(dynpr_context* ctx) {
 
 void prepare_sweep_launch(dynpr_context* ctx) {
   sweep_tick(ctx);
-  persistent_grid(ctx, k_sweep_fused<false, false>, 1);
-  persistent_grid(ctx, k_sweep_fused<true, false>, 1);
-  persistent_grid(ctx, k_sweep_fused<false, true>, 1);
-  persistent_grid(ctx, k_sweep_fused<true, true>, 1);
+  persistent_grid(ctx, k_sweep_fused<false, false, 1>, 1);
+  persistent_grid(ctx, k_sweep_fused<true, false, 1>, 1);
+  persistent_grid(ctx, k_sweep_fused<false, true, 1>, 1);
+  persistent_grid(ctx, k_sweep_fused<true, true, 1>, 1);
+  persistent_grid(ctx, k_sweep_fused<false, false, 2>, 1);
+  persistent_grid(ctx, k_sweep_fused<true, false, 2>, 1);
+  persistent_grid(ctx, k_sweep_fused<false, true, 2>, 1);
+  persistent_grid(ctx, k_sweep_fused<true, true, 2>, 1);
   persistent_grid(ctx, k_sweep_mseg<false>, 1);
   persistent_grid(ctx, k_sweep_mseg<true>, 1);
   persistent_grid(ctx, k_sweep_single<false, false>, 1);

@@ -139,7 +139,7 @@ void launch_sweep(dynpr_context* ctx, const SweepArgs& a, bool flagged, bool clo
 // Launch plan of one sweep for the cached device-loop graph: kernel choice
 // (fused / split) and every grid.  Plans compare bytewise.
 struct SweepPlan {
-  int flagged, closed, split, pull_fused;
+  int flagged, closed, split, pull_fused, grouped;
   unsigned g_fused, g_mseg, g_single, g_mfinal, g_pull_m, g_pull_s;
 };
 SweepPlan plan_sweep(dynpr_context* ctx, const SweepArgs& a, bool flagged, bool closed);
