@@ -152,6 +152,29 @@ __device__ __forceinline__ void copy_through(const SweepArgs& a, uint32_t v) {
   if (a.np && !a.np_accumulate) a.np[v] = 0;
 }
 
+// The same with the vertex's `written` count and previous rank / contribution
+// already loaded (with its flags, one round trip earlier): the split
+// single-slice sweep (RMAT-24 DF-P 1e-4 13.51 -> 13.19 ms with the 4-deep
+// k_init_ranks; the latency-mode sweep was 2-5% slower with it and keeps
+// copy_through).
+__device__ __forceinline__ void copy_through_loaded(const SweepArgs& a, uint32_t v, unsigned wr, double pv,
+                                                    double cprev) {
+  if (a.copy_all) {
+    copy_through(a, v);
+    return;
+  }
+  if (wr) {
+    a.rank_cur[v] = pv;
+    store_contrib(a, v, fabs(cprev));
+    a.written[v] = (uint8_t)(wr - 1);
+  }
+  if (a.np && !a.np_accumulate) a.np[v] = 0;
+}
+// Is v owed a copy-through (see copy_through)?  Loaded with the flags.
+__device__ __forceinline__ unsigned written_of(const SweepArgs& a, uint32_t v, bool valid) {
+  return (valid && a.written && !a.copy_all) ? a.written[v] : 0u;
+}
+
 // Fused epilogue: rank formula (rank.cpp:97-106), next contribution, delta,
 // flags (rank.cpp:108-115).
 // `newly`: the vertex became affected in this sweep's in-sweep pull.
@@ -367,7 +390,11 @@ __device__ __forceinline__ void b_sweep_single(const SweepArgs& a) {
     const uint32_t v = (uint32_t)vv;
     const uint32_t deg = valid ? a.indeg[v] : 0u;
     bool aff = valid;
-    if (FLAGGED) aff = valid && a.va[v];
+    unsigned wr = 0;
+    if (FLAGGED) {
+      aff = valid && a.va[v];
+      wr = written_of(a, v, valid);
+    }
     const bool scan = pull && valid && !aff;  // in-sweep pull: any pending in-neighbour?
     const uint32_t len = (aff || scan) ? deg : 0u;
     const uint32_t Lw = __reduce_max_sync(kFull, len);
@@ -376,6 +403,9 @@ __device__ __forceinline__ void b_sweep_single(const SweepArgs& a) {
     if (aff || scan) {  // prefetch the epilogue operands (and the self-loop term)
       pv = a.rank_prev[v];
       od = a.outdeg[v];
+      cself = a.contrib_prev[v];
+    } else if (FLAGGED && wr) {  // a copy-through's operands
+      pv = a.rank_prev[v];
       cself = a.contrib_prev[v];
     }
     double c = 0.0;
@@ -396,7 +426,7 @@ __device__ __forceinline__ void b_sweep_single(const SweepArgs& a) {
     bool pend = false, lowout = false;
     if (valid) {
       if (!aff && !newly) {
-        copy_through(a, v);
+        copy_through_loaded(a, v, wr, pv, cself);
       } else {
         finalize<FLAGGED, CLOSED>(a, v, c, pv, od, acc, pend, lowout, newly);
         ++acc.proc;
@@ -1077,14 +1107,26 @@ __global__ void __launch_bounds__(kThreads) k_part_scatter(const uint64_t* off, 
 // for uniform; r1 / c1 may be null when the first sweep writes every vertex.
 __global__ void k_init_ranks(const uint32_t* outdeg, const uint32_t* perm, uint32_t n, const double* init,
                              double uniform, double* r0, double* r1, double* c0, double* c1) {
-  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
-       v += (uint64_t)gridDim.x * blockDim.x) {
-    const double r = init ? init[perm[v]] : uniform;
-    const double c = __ddiv_rn(r, (double)outdeg[v]);
-    r0[v] = r;
-    if (r1) r1[v] = r;
-    c0[v] = c;
-    if (c1) c1[v] = c;
+  // 4 vertices per thread per round, so 4 of the (random) old-order rank
+  // gathers are in flight at once
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t v0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v0 < n; v0 += 4 * stride) {
+    double r[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint64_t v = v0 + j * stride;
+      r[j] = v < n ? (init ? init[perm[v]] : uniform) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint64_t v = v0 + j * stride;
+      if (v >= n) break;
+      const double c = __ddiv_rn(r[j], (double)outdeg[v]);
+      r0[v] = r[j];
+      if (r1) r1[v] = r[j];
+      c0[v] = c;
+      if (c1) c1[v] = c;
+    }
   }
 }
 
