@@ -148,6 +148,8 @@ struct dynpr_context {
   // single-vertex kernel (fork / join events)
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // captures the IF bodies of the device-loop graph (never launched on)
+  cudaStream_t capture_aux = nullptr;
   // instantiated device-loop graphs (engine.cu LoopGraphCache), keyed by
   // sweep plan; owned
   void* loop_graphs = nullptr;

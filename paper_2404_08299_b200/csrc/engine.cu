@@ -176,7 +176,8 @@ struct LoopGraph {
   int frontier;
   cudaGraph_t g = nullptr;
   cudaGraphExec_t exec = nullptr;
-  uint64_t launches_per_body = 0;
+  uint64_t launches_per_body = 0;  // (without the push expansions' IF bodies)
+  uint64_t launches_per_push = 0;
 };
 struct LoopGraphCache {
   std::vector<LoopGraph> items;
@@ -248,23 +249,55 @@ LoopGraph& loop_graph(dynpr_context* ctx, const SweepPlan& plan, int frontier, L
   cudaGraphNode_t node;
   DYNPR_CK(cudaGraphAddNode(&node, lg.g, nullptr, 0, &np));
   cudaGraph_t body = np.conditional.phGraph_out[0];
+  // A frontier loop's push expansion sits in an IF node that k_loop_end
+  // arms only when a push follows: pull iterations (and the last one) launch
+  // no expansion kernels at all (before: three gated-off 16-CTA/SM grids
+  // per iteration, ~13 us of an RMAT-20 sweep's ~62).
+  const int nb = body_sweeps(plan);
+  std::vector<cudaGraphConditionalHandle> hpush(frontier ? nb : 0);
+  for (auto& x : hpush) DYNPR_CK(cudaGraphConditionalHandleCreate(&x, body, 0u, cudaGraphCondAssignDefault));
+  if (frontier && !ctx->capture_aux)
+    DYNPR_CK(cudaStreamCreateWithFlags(&ctx->capture_aux, cudaStreamNonBlocking));
+  uint64_t push_launches = 0;
+  std::vector<cudaGraphNode_t> if_nodes;  // (cudaGraphNodeGetType fails on them: skipped below)
   DYNPR_CK(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
   try {
     // body_sweeps() per body (an even number: the ping-pong parity of every
     // position is fixed)
-    const int nb = body_sweeps(plan);
     for (int k = 0; k < nb; ++k) {
       const int half = k & 1;
       launch_sweep_ind(ctx, plan, half, tick);  // the record is zero: before the launch, then k_loop_end
-      launch_loop_end(ctx, dc, red, cond, k == nb - 1);
+      launch_loop_end(ctx, dc, red, cond, k == nb - 1, frontier ? hpush[k] : 0, frontier);
       if (frontier) {
-        launch_expand_ind(ctx, half, dc);
+        cudaStreamCaptureStatus cs;
+        cudaGraph_t cg = nullptr;
+        const cudaGraphNode_t* deps = nullptr;
+        size_t nd = 0;
+        DYNPR_CK(cudaStreamGetCaptureInfo(st, &cs, nullptr, &cg, &deps, &nd));
+        cudaGraphNodeParams ip{};
+        ip.type = cudaGraphNodeTypeConditional;
+        ip.conditional.handle = hpush[k];
+        ip.conditional.type = cudaGraphCondTypeIf;
+        ip.conditional.size = 1;
+        cudaGraphNode_t ifn;
+        DYNPR_CK(cudaGraphAddNode(&ifn, cg, deps, nd, &ip));
+        if_nodes.push_back(ifn);
+        DYNPR_CK(cudaStreamUpdateCaptureDependencies(st, &ifn, 1, cudaStreamSetCaptureDependencies));
+        const uint64_t l0 = ctx->launches;
+        DYNPR_CK(cudaStreamBeginCaptureToGraph(ctx->capture_aux, ip.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                               cudaStreamCaptureModeThreadLocal));
+        launch_expand_ind(ctx, half, dc, ctx->capture_aux);
+        cudaGraph_t ib = nullptr;
+        DYNPR_CK(cudaStreamEndCapture(ctx->capture_aux, &ib));
+        push_launches = ctx->launches - l0;
+        ctx->launches = l0;
         if (!plan.pull_fused) launch_pull_ind(ctx, plan, half);  // (else: inside the next sweep)
       }
     }
   } catch (...) {
     cudaGraph_t junk = nullptr;
     cudaStreamEndCapture(st, &junk);
+    if (ctx->capture_aux) cudaStreamEndCapture(ctx->capture_aux, &junk);
     cudaGetLastError();
     throw;  // (the half-built graph is leaked: destroying it crashes in the driver)
   }
@@ -278,6 +311,7 @@ LoopGraph& loop_graph(dynpr_context* ctx, const SweepPlan& plan, int frontier, L
     int lo = 0, hi = 0;
     DYNPR_CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     for (cudaGraphNode_t nd : nodes) {
+      if (std::find(if_nodes.begin(), if_nodes.end(), nd) != if_nodes.end()) continue;
       cudaGraphNodeType t;
       DYNPR_CK(cudaGraphNodeGetType(nd, &t));
       if (t != cudaGraphNodeTypeKernel) continue;
@@ -291,6 +325,7 @@ LoopGraph& loop_graph(dynpr_context* ctx, const SweepPlan& plan, int frontier, L
   }
   DYNPR_CK(cudaGraphInstantiate(&lg.exec, lg.g, 0));
   lg.launches_per_body = ctx->launches - launches0;
+  lg.launches_per_push = push_launches;
   ctx->launches = launches0;
   cache->items.push_back(lg);
   return cache->items.back();
@@ -358,7 +393,8 @@ void run_device_loop(dynpr_context* ctx, const SolveSpec& sp, const SweepArgs& a
   sync(ctx);
   std::memcpy(&h, stage + 1024, sizeof h);
   // launches: the captured body (two iterations) ran once per two sweeps
-  ctx->launches += lg.launches_per_body * (uint64_t)((h.iterations + body_sweeps(plan) - 1) / body_sweeps(plan));
+  ctx->launches += lg.launches_per_body * (uint64_t)((h.iterations + body_sweeps(plan) - 1) / body_sweeps(plan)) +
+                   lg.launches_per_push * h.pushes;
   res.iterations = h.iterations;
   res.converged = h.converged;
   res.affected_vertex_iterations = h.affected;
@@ -784,6 +820,7 @@ void dynpr_b200::context_teardown(dynpr_context* ctx) {
   ctx->loop_graphs = nullptr;
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   if (ctx->side) cudaStreamDestroy(ctx->side);
+  if (ctx->capture_aux) cudaStreamDestroy(ctx->capture_aux);
   if (ctx->aux) {
     cudaStreamSynchronize(ctx->aux);
     cudaStreamDestroy(ctx->aux);

@@ -1238,7 +1238,8 @@ __global__ void k_expand_high_c(const unsigned* counts, const int* gate) {
 constexpr int kLoopTraceIters = 1024;
 __device__ unsigned long long g_loop_trace[kLoopTraceIters * 4];
 
-__global__ void k_loop_end(LoopCtl* c, SweepRed* red, cudaGraphConditionalHandle h, int set_cond) {
+__global__ void k_loop_end(LoopCtl* c, SweepRed* red, cudaGraphConditionalHandle h, int set_cond,
+                           cudaGraphConditionalHandle hpush, int has_push) {
   if (!c->done) {
     // a pull sweep of a lazy-list loop appended no pending lists
     const bool no_lists = c->lazy_lists && c->expand == kExpandPull;
@@ -1274,6 +1275,11 @@ __global__ void k_loop_end(LoopCtl* c, SweepRed* red, cudaGraphConditionalHandle
     }
   }
   if (set_cond) cudaGraphSetConditional(h, c->done ? 0u : 1u);
+  if (has_push) {
+    const bool push = !c->done && (c->expand == kExpandPush || c->expand == kExpandPushCollect);
+    c->pushes += push ? 1u : 0u;
+    cudaGraphSetConditional(hpush, push ? 1u : 0u);
+  }
 }
 
 // A push decided after a pull sweep of a lazy-list loop: the pending lists
@@ -1838,20 +1844,20 @@ void launch_pull_ind(dynpr_context* ctx, const SweepPlan& p, int half) {
   count_launch(ctx, launched);
 }
 
-void launch_expand_ind(dynpr_context* ctx, int half, LoopCtl* dc) {
+void launch_expand_ind(dynpr_context* ctx, int half, LoopCtl* dc, cudaStream_t stream) {
   const unsigned g = (unsigned)ctx->num_sms * 16;
   const unsigned* counts = &dc->pend_low;
   const int* gate = &dc->expand;
   // (returns at once unless a lazy-list loop pushes after a pull sweep)
-  if (half) k_collect_signs_c<1><<<g, kThreads, 0, ctx->stream>>>(dc);
-  else k_collect_signs_c<0><<<g, kThreads, 0, ctx->stream>>>(dc);
+  if (half) k_collect_signs_c<1><<<g, kThreads, 0, stream>>>(dc);
+  else k_collect_signs_c<0><<<g, kThreads, 0, stream>>>(dc);
   count_launch(ctx);
   if (half) {
-    k_expand_low_c<1><<<g, kThreads, 0, ctx->stream>>>(counts, gate);
-    k_expand_high_c<1><<<g, kThreads, 0, ctx->stream>>>(counts, gate);
+    k_expand_low_c<1><<<g, kThreads, 0, stream>>>(counts, gate);
+    k_expand_high_c<1><<<g, kThreads, 0, stream>>>(counts, gate);
   } else {
-    k_expand_low_c<0><<<g, kThreads, 0, ctx->stream>>>(counts, gate);
-    k_expand_high_c<0><<<g, kThreads, 0, ctx->stream>>>(counts, gate);
+    k_expand_low_c<0><<<g, kThreads, 0, stream>>>(counts, gate);
+    k_expand_high_c<0><<<g, kThreads, 0, stream>>>(counts, gate);
   }
   check_launch();
   count_launch(ctx, 2);
@@ -1963,8 +1969,8 @@ void launch_expand(dynpr_context* ctx, Rows rows, uint8_t* va, const uint32_t* p
 }
 
 void launch_loop_end(dynpr_context* ctx, LoopCtl* c, SweepRed* red, cudaGraphConditionalHandle h,
-                     int set_cond) {
-  k_loop_end<<<1, 1, 0, ctx->stream>>>(c, red, h, set_cond);
+                     int set_cond, cudaGraphConditionalHandle hpush, int has_push) {
+  k_loop_end<<<1, 1, 0, ctx->stream>>>(c, red, h, set_cond, hpush, has_push);
   check_launch();
   count_launch(ctx);
 }

@@ -113,14 +113,16 @@ struct LoopCtl {
   int lazy_lists;        // pull sweeps skip the pending-list appends (SweepArgs::lazy_lists)
   int push_cost;         // direction rule: push when push_cost * pending out-edges <= unaffected in-edges
   unsigned pend_low, pend_high;  // push-expansion list sizes of the last sweep
+  unsigned pushes;               // push expansions run (their IF bodies executed)
   double tol, final_delta;
   unsigned long long affected, edges, m, n;
 };
 // One iteration's bookkeeping (single thread): count, delta, convergence,
 // max-iterations, expansion direction; `set_cond` also sets the WHILE
-// node's condition to !done.
+// node's condition to !done, `has_push` the IF node `hpush` (around the push
+// expansion) to "a push follows".
 void launch_loop_end(dynpr_context* ctx, LoopCtl* c, SweepRed* red, cudaGraphConditionalHandle h,
-                     int set_cond);
+                     int set_cond, cudaGraphConditionalHandle hpush = 0, int has_push = 0);
 // Push expansion with device-resident list sizes (counts[0] low, counts[1]
 // high), optionally gated on *gate == kExpandPush; fixed grids.
 void launch_expand_dev(dynpr_context* ctx, Rows rows, uint8_t* va,
@@ -148,7 +150,7 @@ SweepPlan plan_sweep(dynpr_context* ctx, const SweepArgs& a, bool flagged, bool 
 // bank (upload_loop_args, stream-ordered), for capture into the loop graph.
 void launch_sweep_ind(dynpr_context* ctx, const SweepPlan& p, int half, uint32_t* tick);
 void launch_pull_ind(dynpr_context* ctx, const SweepPlan& p, int half);
-void launch_expand_ind(dynpr_context* ctx, int half, LoopCtl* dc);
+void launch_expand_ind(dynpr_context* ctx, int half, LoopCtl* dc, cudaStream_t stream);
 void upload_loop_args(dynpr_context* ctx, const SweepArgs* host_pinned_half2);
 // The multi-chunk sweep kernels, whose nodes get the highest launch priority
 // in the loop graph (they run concurrently with the single-vertex kernel).

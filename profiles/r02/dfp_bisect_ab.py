@@ -1,12 +1,20 @@
 """DF-P device ms (min / median of 6 warm solves, same batch) for several
 package builds, one process per (build, graph, fraction), interleaved.
-    python profiles/r02/dfp_bisect_ab.py scale:frac[,scale:frac] DIR[:VAR=value] ..."""
+    python profiles/r02/dfp_bisect_ab.py scale:frac[,scale:frac] DIR[:VAR=value] ...
+(scale uS: a uniform random graph of 2^S vertices)"""
 import os, subprocess, sys
 CHILD = r'''
 import sys, statistics
 sys.path.insert(0, sys.argv[1])
 import paper_2404_08299_b200 as dp
-g = dp.rmat_graph(int(sys.argv[2])); gt = dp.transpose(g)
+if sys.argv[2].startswith("u"):  # uniform: 2^S vertices, 16 x 2^S random pairs + self-loops
+    import numpy as np
+    S = int(sys.argv[2][1:]); rng = np.random.default_rng(1)
+    g = dp.add_self_loops(dp.build_csr((rng.integers(0, 1 << S, 16 << S, dtype=np.uint32),
+                                        rng.integers(0, 1 << S, 16 << S, dtype=np.uint32)), 1 << S))
+else:
+    g = dp.rmat_graph(int(sys.argv[2]))
+gt = dp.transpose(g)
 base = dp.static_pagerank(gt, g)
 b = dp.generate_random_batch(g, dp.batch_size_from_fraction(float(sys.argv[3]), g.edge_count), 0.8, 11)
 g2, gt2 = dp.apply_batch_pair(g, gt, b); dp.prepare(gt2, g2)
