@@ -1177,12 +1177,28 @@ __device__ __forceinline__ void expand_low_body(Rows rows, const uint32_t* list,
     const uint32_t u = list[i];
     const uint32_t* r = rows.row(u);
     const uint64_t len = rows.len(u);
-    for (uint64_t k = 0; k < len; ++k) {
-      const uint32_t w = r[k];
-      if (!va[w]) va[w] = 1;
+    // 8 targets, then their 8 flags, then the stores: 2 dependent round
+    // trips per 8 edges instead of per edge (a byte store may alias the
+    // target list, so the compiler cannot hoist the next loads by itself)
+    for (uint64_t k = 0; k < len; k += 8) {
+      uint32_t w[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) w[q] = k + q < len ? __ldg(r + k + q) : 0xffffffffu;
+      uint8_t f[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) f[q] = w[q] != 0xffffffffu ? va[w[q]] : 1;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (!f[q]) va[w[q]] = 1;
     }
   }
 }
+#ifndef DYNPR_EXPAND_DEPTH
+#define DYNPR_EXPAND_DEPTH 4
+#endif
+// edges per lane per round of a 1024-edge item (8 measured no faster:
+// profiles/r02/expand_batch_ab.txt)
+constexpr int kExpandDepth = DYNPR_EXPAND_DEPTH;
 __device__ __forceinline__ void expand_high_body(Rows rows, const uint2* items, uint64_t cnt, uint8_t* va) {
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / 32;
   const uint64_t nw = (uint64_t)gridDim.x * blockDim.x / 32;
@@ -1193,15 +1209,15 @@ __device__ __forceinline__ void expand_high_body(Rows rows, const uint2* items, 
     const uint64_t len = rows.len(it.x);
     const uint64_t b = (uint64_t)kExpandChunk * it.y;
     const uint64_t e = b + kExpandChunk < len ? b + kExpandChunk : len;
-    for (uint64_t k = b + lane; k < e; k += 32 * 4) {
-      uint32_t w[4];
+    for (uint64_t k = b + lane; k < e; k += 32 * kExpandDepth) {
+      uint32_t w[kExpandDepth];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) w[q] = k + 32 * q < e ? r[k + 32 * q] : 0xffffffffu;
-      uint8_t f[4];
+      for (int q = 0; q < kExpandDepth; ++q) w[q] = k + 32 * q < e ? __ldg(r + k + 32 * q) : 0xffffffffu;
+      uint8_t f[kExpandDepth];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) f[q] = w[q] != 0xffffffffu ? va[w[q]] : 1;
+      for (int q = 0; q < kExpandDepth; ++q) f[q] = w[q] != 0xffffffffu ? va[w[q]] : 1;
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < kExpandDepth; ++q)
         if (!f[q]) va[w[q]] = 1;
     }
   }
