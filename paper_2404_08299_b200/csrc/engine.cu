@@ -20,6 +20,7 @@
 #include <cstdio>
 #include <cmath>
 #include <cstdlib>
+#include <functional>
 #include <string>
 #include <mutex>
 #include <vector>
@@ -178,6 +179,7 @@ struct LoopGraph {
   cudaGraphExec_t exec = nullptr;
   uint64_t launches_per_body = 0;  // (without the push expansions' IF bodies)
   uint64_t launches_per_push = 0;
+  uint64_t launches_per_empty_check = 0;
 };
 struct LoopGraphCache {
   std::vector<LoopGraph> items;
@@ -254,12 +256,45 @@ LoopGraph& loop_graph(dynpr_context* ctx, const SweepPlan& plan, int frontier, L
   // no expansion kernels at all (before: three gated-off 16-CTA/SM grids
   // per iteration, ~13 us of an RMAT-20 sweep's ~62).
   const int nb = body_sweeps(plan);
-  std::vector<cudaGraphConditionalHandle> hpush(frontier ? nb : 0);
+  // The DF-P end-game check (launch_empty_check) in its own IF node: split
+  // plans only -- an empty sweep there costs ~0.2-0.3 ms (RMAT-24), while on
+  // the latency-mode plans a second IF node per iteration cost more than the
+  // empty sweeps it saves (profiles/r02/empty_check_ab.txt).
+  const bool end_check = frontier && plan.split && plan.closed;
+  std::vector<cudaGraphConditionalHandle> hpush(frontier ? nb : 0), hempty(end_check ? nb : 0);
   for (auto& x : hpush) DYNPR_CK(cudaGraphConditionalHandleCreate(&x, body, 0u, cudaGraphCondAssignDefault));
+  for (auto& x : hempty) DYNPR_CK(cudaGraphConditionalHandleCreate(&x, body, 0u, cudaGraphCondAssignDefault));
   if (frontier && !ctx->capture_aux)
     DYNPR_CK(cudaStreamCreateWithFlags(&ctx->capture_aux, cudaStreamNonBlocking));
-  uint64_t push_launches = 0;
+  uint64_t push_launches = 0, empty_launches = 0;
   std::vector<cudaGraphNode_t> if_nodes;  // (cudaGraphNodeGetType fails on them: skipped below)
+  // an IF node after the captured work so far; its body captured from `fill`
+  // on the capture-only stream; returns the kernels launched in it
+  auto add_if = [&](cudaGraphConditionalHandle hc, const std::function<void(cudaStream_t)>& fill) {
+    cudaStreamCaptureStatus cs;
+    cudaGraph_t cg = nullptr;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    DYNPR_CK(cudaStreamGetCaptureInfo(st, &cs, nullptr, &cg, &deps, &nd));
+    cudaGraphNodeParams ip{};
+    ip.type = cudaGraphNodeTypeConditional;
+    ip.conditional.handle = hc;
+    ip.conditional.type = cudaGraphCondTypeIf;
+    ip.conditional.size = 1;
+    cudaGraphNode_t ifn;
+    DYNPR_CK(cudaGraphAddNode(&ifn, cg, deps, nd, &ip));
+    if_nodes.push_back(ifn);
+    DYNPR_CK(cudaStreamUpdateCaptureDependencies(st, &ifn, 1, cudaStreamSetCaptureDependencies));
+    const uint64_t l0 = ctx->launches;
+    DYNPR_CK(cudaStreamBeginCaptureToGraph(ctx->capture_aux, ip.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeThreadLocal));
+    fill(ctx->capture_aux);
+    cudaGraph_t ib = nullptr;
+    DYNPR_CK(cudaStreamEndCapture(ctx->capture_aux, &ib));
+    const uint64_t used = ctx->launches - l0;
+    ctx->launches = l0;
+    return used;
+  };
   DYNPR_CK(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
   try {
     // body_sweeps() per body (an even number: the ping-pong parity of every
@@ -267,30 +302,14 @@ LoopGraph& loop_graph(dynpr_context* ctx, const SweepPlan& plan, int frontier, L
     for (int k = 0; k < nb; ++k) {
       const int half = k & 1;
       launch_sweep_ind(ctx, plan, half, tick);  // the record is zero: before the launch, then k_loop_end
-      launch_loop_end(ctx, dc, red, cond, k == nb - 1, frontier ? hpush[k] : 0, frontier);
+      launch_loop_end(ctx, dc, red, cond, k == nb - 1, frontier ? hpush[k] : 0, frontier,
+                      end_check ? hempty[k] : 0, end_check);
       if (frontier) {
-        cudaStreamCaptureStatus cs;
-        cudaGraph_t cg = nullptr;
-        const cudaGraphNode_t* deps = nullptr;
-        size_t nd = 0;
-        DYNPR_CK(cudaStreamGetCaptureInfo(st, &cs, nullptr, &cg, &deps, &nd));
-        cudaGraphNodeParams ip{};
-        ip.type = cudaGraphNodeTypeConditional;
-        ip.conditional.handle = hpush[k];
-        ip.conditional.type = cudaGraphCondTypeIf;
-        ip.conditional.size = 1;
-        cudaGraphNode_t ifn;
-        DYNPR_CK(cudaGraphAddNode(&ifn, cg, deps, nd, &ip));
-        if_nodes.push_back(ifn);
-        DYNPR_CK(cudaStreamUpdateCaptureDependencies(st, &ifn, 1, cudaStreamSetCaptureDependencies));
-        const uint64_t l0 = ctx->launches;
-        DYNPR_CK(cudaStreamBeginCaptureToGraph(ctx->capture_aux, ip.conditional.phGraph_out[0], nullptr, nullptr, 0,
-                                               cudaStreamCaptureModeThreadLocal));
-        launch_expand_ind(ctx, half, dc, ctx->capture_aux);
-        cudaGraph_t ib = nullptr;
-        DYNPR_CK(cudaStreamEndCapture(ctx->capture_aux, &ib));
-        push_launches = ctx->launches - l0;
-        ctx->launches = l0;
+        push_launches = add_if(hpush[k], [&](cudaStream_t s) { launch_expand_ind(ctx, half, dc, s); });
+        if (end_check)
+          empty_launches = add_if(hempty[k], [&](cudaStream_t s) {
+            launch_empty_check(ctx, dc, half, s, cond, k == nb - 1);
+          });
         if (!plan.pull_fused) launch_pull_ind(ctx, plan, half);  // (else: inside the next sweep)
       }
     }
@@ -326,12 +345,15 @@ LoopGraph& loop_graph(dynpr_context* ctx, const SweepPlan& plan, int frontier, L
   DYNPR_CK(cudaGraphInstantiate(&lg.exec, lg.g, 0));
   lg.launches_per_body = ctx->launches - launches0;
   lg.launches_per_push = push_launches;
+  lg.launches_per_empty_check = empty_launches;
   ctx->launches = launches0;
   cache->items.push_back(lg);
   return cache->items.back();
 }
 
-void run_device_loop(dynpr_context* ctx, const SolveSpec& sp, const SweepArgs& a_in, double* const R[2],
+// Returns true when the last iteration was accounted without its sweep
+// (k_loop_end: nothing left affected); the result is then R[(iterations - 1) & 1].
+bool run_device_loop(dynpr_context* ctx, const SolveSpec& sp, const SweepArgs& a_in, double* const R[2],
                      double* const CB[2], const Layout* L, SweepRed* red, dynpr_stats& res) {
   const dynpr_config& c = *sp.cfg;
   cudaStream_t st = ctx->stream;
@@ -394,12 +416,13 @@ void run_device_loop(dynpr_context* ctx, const SolveSpec& sp, const SweepArgs& a
   std::memcpy(&h, stage + 1024, sizeof h);
   // launches: the captured body (two iterations) ran once per two sweeps
   ctx->launches += lg.launches_per_body * (uint64_t)((h.iterations + body_sweeps(plan) - 1) / body_sweeps(plan)) +
-                   lg.launches_per_push * h.pushes;
+                   lg.launches_per_push * h.pushes + lg.launches_per_empty_check * h.empty_checks;
   res.iterations = h.iterations;
   res.converged = h.converged;
   res.affected_vertex_iterations = h.affected;
   res.processed_edges = h.edges;
   res.final_delta = h.final_delta;
+  return h.skipped != 0;
 }
 
 // Snapshot preparation also readies the solves that follow (single GPU,
@@ -628,8 +651,8 @@ void solve_impl(dynpr_context* ctx, const SolveSpec& sp, double* ranks_out, dynp
   int cur = 0;  // R[cur] holds the latest iterate ("previous")
   if (device_loop) {
     NvtxRange r("dynpr device loop");
-    run_device_loop(ctx, sp, a, R, CB, L, red, res);
-    cur = res.iterations & 1;
+    const bool skipped = run_device_loop(ctx, sp, a, R, CB, L, red, res);
+    cur = (res.iterations - (skipped ? 1 : 0)) & 1;
   }
   // Multi-GPU team, no observer / profiling: the host-driven loop runs one
   // iteration ahead -- iteration k+1 (sweep, collectives, pull expansion) is

@@ -1255,7 +1255,8 @@ constexpr int kLoopTraceIters = 1024;
 __device__ unsigned long long g_loop_trace[kLoopTraceIters * 4];
 
 __global__ void k_loop_end(LoopCtl* c, SweepRed* red, cudaGraphConditionalHandle h, int set_cond,
-                           cudaGraphConditionalHandle hpush, int has_push) {
+                           cudaGraphConditionalHandle hpush, int has_push, cudaGraphConditionalHandle hempty,
+                           int has_empty) {
   if (!c->done) {
     // a pull sweep of a lazy-list loop appended no pending lists
     const bool no_lists = c->lazy_lists && c->expand == kExpandPull;
@@ -1279,6 +1280,10 @@ __global__ void k_loop_end(LoopCtl* c, SweepRed* red, cudaGraphConditionalHandle
       c->expand = r.pend_edges * cost > pull_bound ? kExpandPull : (no_lists ? kExpandPushCollect : kExpandPush);
       c->pend_low = no_lists ? 0u : r.pend_low;
       c->pend_high = no_lists ? 0u : r.pend_high;
+      // nothing pending: no expansion; with pruning the affected set may now
+      // be empty (checked by the IF node `hempty`)
+      if (r.pend_edges == 0) c->expand = kExpandNone;
+      c->check_empty = has_empty && c->check && r.pend_edges == 0 ? 1 : 0;
     }
     if (c->iterations <= kLoopTraceIters) {
       unsigned long long* t = g_loop_trace + 4 * (c->iterations - 1);
@@ -1296,6 +1301,48 @@ __global__ void k_loop_end(LoopCtl* c, SweepRed* red, cudaGraphConditionalHandle
     c->pushes += push ? 1u : 0u;
     cudaGraphSetConditional(hpush, push ? 1u : 0u);
   }
+  if (has_empty) {
+    const bool chk = !c->done && c->check_empty;
+    c->empty_checks += chk ? 1u : 0u;
+    cudaGraphSetConditional(hempty, chk ? 1u : 0u);
+  }
+}
+
+// Any vertex still affected (a delta-V byte set)?  16-byte loads; a block
+// stops once another found one.
+template <int H>
+__global__ void k_any_affected(LoopCtl* c) {
+  const uint8_t* va = c_loop_args[H].va;  // (the solve's flags, from its argument slot)
+  const uint64_t n = c_loop_args[H].n;
+  const uint64_t nv = n / 16;
+  const uint4* v4 = reinterpret_cast<const uint4*>(va);
+  bool found = false;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nv && !found;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint4 x = v4[i];
+    found = (x.x | x.y | x.z | x.w) != 0u;
+  }
+  if (blockIdx.x == 0 && threadIdx.x < n % 16) found = found || va[nv * 16 + threadIdx.x] != 0;
+  if (__syncthreads_or(found) && threadIdx.x == 0) atomicOr(&c->kept, 1u);
+}
+__global__ void k_empty_finish(LoopCtl* c, cudaGraphConditionalHandle h, int set_cond) {
+  if (!c->done && !c->kept) {
+    c->iterations += 1;  // all copied through: delta 0 (engine.cpp:79-91)
+    c->final_delta = 0.0;
+    c->converged = 0.0 <= c->tol ? 1 : 0;
+    c->done = 1;
+    c->skipped = 1;
+    if (c->iterations <= kLoopTraceIters) {
+      unsigned long long* t = g_loop_trace + 4 * (c->iterations - 1);
+      unsigned long long now;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      t[0] = now;
+      t[1] = t[2] = t[3] = 0ull;
+    }
+  }
+  c->kept = 0u;
+  c->check_empty = 0;
+  if (set_cond) cudaGraphSetConditional(h, c->done ? 0u : 1u);
 }
 
 // A push decided after a pull sweep of a lazy-list loop: the pending lists
@@ -1984,9 +2031,19 @@ void launch_expand(dynpr_context* ctx, Rows rows, uint8_t* va, const uint32_t* p
   }
 }
 
+void launch_empty_check(dynpr_context* ctx, LoopCtl* c, int half, cudaStream_t stream, cudaGraphConditionalHandle h,
+                        int set_cond) {
+  if (half) k_any_affected<1><<<ctx->num_sms * 4, kThreads, 0, stream>>>(c);
+  else k_any_affected<0><<<ctx->num_sms * 4, kThreads, 0, stream>>>(c);
+  k_empty_finish<<<1, 1, 0, stream>>>(c, h, set_cond);
+  check_launch();
+  count_launch(ctx, 2);
+}
+
 void launch_loop_end(dynpr_context* ctx, LoopCtl* c, SweepRed* red, cudaGraphConditionalHandle h,
-                     int set_cond, cudaGraphConditionalHandle hpush, int has_push) {
-  k_loop_end<<<1, 1, 0, ctx->stream>>>(c, red, h, set_cond, hpush, has_push);
+                     int set_cond, cudaGraphConditionalHandle hpush, int has_push, cudaGraphConditionalHandle hempty,
+                     int has_empty) {
+  k_loop_end<<<1, 1, 0, ctx->stream>>>(c, red, h, set_cond, hpush, has_push, hempty, has_empty);
   check_launch();
   count_launch(ctx);
 }

@@ -114,6 +114,10 @@ struct LoopCtl {
   int push_cost;         // direction rule: push when push_cost * pending out-edges <= unaffected in-edges
   unsigned pend_low, pend_high;  // push-expansion list sizes of the last sweep
   unsigned pushes;               // push expansions run (their IF bodies executed)
+  unsigned empty_checks;         // DF-P end-game checks run (their IF bodies executed)
+  int check_empty;               // no vertex pending after the sweep: is any still affected?
+  unsigned kept;                 // (k_any_affected: some vertex still affected)
+  int skipped;                   // the last iteration was accounted without its (empty) sweep
   double tol, final_delta;
   unsigned long long affected, edges, m, n;
 };
@@ -122,7 +126,15 @@ struct LoopCtl {
 // node's condition to !done, `has_push` the IF node `hpush` (around the push
 // expansion) to "a push follows".
 void launch_loop_end(dynpr_context* ctx, LoopCtl* c, SweepRed* red, cudaGraphConditionalHandle h,
-                     int set_cond, cudaGraphConditionalHandle hpush = 0, int has_push = 0);
+                     int set_cond, cudaGraphConditionalHandle hpush = 0, int has_push = 0,
+                     cudaGraphConditionalHandle hempty = 0, int has_empty = 0);
+// DF-P end game (the body of the IF node `hempty` that k_loop_end arms when a
+// sweep leaves no vertex pending): if no vertex is still affected either,
+// the next iteration would affect nothing -- it is accounted without its
+// sweep (iterations + 1, delta 0, converged, LoopCtl::skipped) and the loop
+// ends; `set_cond` also clears the WHILE node's condition `h`.
+void launch_empty_check(dynpr_context* ctx, LoopCtl* c, int half, cudaStream_t stream, cudaGraphConditionalHandle h,
+                        int set_cond);
 // Push expansion with device-resident list sizes (counts[0] low, counts[1]
 // high), optionally gated on *gate == kExpandPush; fixed grids.
 void launch_expand_dev(dynpr_context* ctx, Rows rows, uint8_t* va,
