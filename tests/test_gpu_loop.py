@@ -174,3 +174,49 @@ def test_concurrent_contexts_device_loops(dp, oracle_lib):
     for (og, ogt, ref), res in zip(cases, out):
         for r in res:
             _same(r, ref)
+
+
+def _loop_trace(n_it):
+    import ctypes as C
+    from paper_2404_08299_b200 import _native as N
+    cnt = C.c_uint64()
+    N.lib().dynpr_debug_loop_trace(None, 0, C.byref(cnt))
+    buf = np.zeros(cnt.value, np.uint64)
+    N.lib().dynpr_debug_loop_trace(buf.ctypes.data, cnt.value, None)
+    return buf.reshape(-1, 4)[:n_it]
+
+
+def test_dfp_end_game_accounts_the_empty_iteration(dp, oracle_lib, monkeypatch):
+    """DF-P on a split plan: when a sweep leaves nothing pending and nothing
+    affected, the device loop accounts the next (empty) iteration without
+    its sweep (engine.cu end_check).  Same counts, delta and ranks as the
+    host loop, which runs that sweep, and as the reference; also with
+    max_iterations cutting the loop right before and at that iteration."""
+    import oracle
+    O = oracle_lib
+    monkeypatch.setenv("DYNPR_SWEEP", "split")
+    src, dst = O.rmat_edges(16, 16 << 16)
+    og = O.add_self_loops(O.build_csr((src, dst), 1 << 16))
+    ogt = O.transpose(og)
+    g0 = dp.rmat_graph(16)
+    gt0 = dp.transpose(g0)
+    base = O.static(ogt, og)
+    empty_ends = 0
+    for k, frac in enumerate((1e-5, 1e-4, 1e-3, 1e-4, 1e-5, 1e-3)):
+        size = O.batch_size_from_fraction(frac, og.m)
+        dels, ins = O.generate_random_batch(og, size, 0.8, O.derive_seed(5, k))
+        og2, _, _ = O.apply_batch(og, dels, ins)
+        ogt2 = O.transpose(og2)
+        g, gt = dp.apply_batch_pair(g0, gt0, dp.BatchUpdate(dels, ins))
+        ref = O.dynamic_frontier(og2, ogt2, dels, ins, base.ranks, pruning=True)
+        dev = _both(monkeypatch, lambda: dp.dynamic_frontier(g, gt, dels, ins, base.ranks, pruning=True))
+        _same(dev, ref)
+        t = _loop_trace(dev.iterations)
+        if dev.iterations > 1 and t[-1][1] == 0 and t[-1][2] == 0:
+            empty_ends += 1
+            for cut in (dev.iterations - 1, dev.iterations):
+                ocfg = oracle.default_config(max_iterations=cut)
+                cfg = dp.EngineConfig(max_iterations=cut)
+                r = O.dynamic_frontier(og2, ogt2, dels, ins, base.ranks, ocfg, pruning=True)
+                _same(_both(monkeypatch, lambda: dp.dynamic_frontier(g, gt, dels, ins, base.ranks, cfg, True)), r)
+    assert empty_ends > 0, "no case ended with an empty iteration"
