@@ -239,6 +239,7 @@ struct IngestStatus {
   unsigned long long ndp, nnw;                    // present deletions / fresh insertions
   unsigned long long nt;                          // touched rows
   unsigned long long m_new;                       // edge count of the new snapshot
+  unsigned long long nrd, nri, nrm;               // touched rows among the deletions / insertions / both
 };
 
 // Per-vertex ingest state of one CSR, zero between ingests.
@@ -251,7 +252,7 @@ struct VertexState {
 };
 
 __global__ void k_status_init(IngestStatus* s) {
-  *s = IngestStatus{kNone, kNone, kNone, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  *s = IngestStatus{kNone, kNone, kNone, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 }
 
 // graph.cpp:116-120: ids in range (both lists), no self-loop deletion; the
@@ -371,6 +372,48 @@ struct Untag {
   uint64_t tag;
   __device__ __forceinline__ uint64_t operator()(uint64_t i) const { return keys[i] & ~tag; }
 };
+// Touched rows from the batch (every row with a loop: only batch sources
+// change): the first entry of each row within the sorted deletions
+// [0, ndu) or the sorted insertions [ndu, nu), kept if the row changes.
+struct RowHead {
+  const uint64_t* keys;
+  const unsigned long long* ndu;
+  const uint8_t* touched;
+  int sb;
+  uint64_t mask;
+  bool ins;
+  __device__ __forceinline__ bool operator()(uint64_t i) const {
+    const uint64_t d = *ndu;
+    if (ins ? i < d : i >= d) return false;
+    const uint32_t u = (uint32_t)((keys[i] >> sb) & mask);
+    if (i != (ins ? d : 0ull) && (uint32_t)((keys[i - 1] >> sb) & mask) == u) return false;
+    return touched[u] != 0;
+  }
+};
+struct RowOf {
+  const uint64_t* keys;
+  int sb;
+  uint64_t mask;
+  __device__ __forceinline__ uint32_t operator()(uint64_t i) const { return (uint32_t)((keys[i] >> sb) & mask); }
+};
+// Merge of the two sorted touched-row lists (duplicates kept adjacent, the
+// deletion side first); *nm = na + nb for the unique pass that follows.
+__global__ void k_merge_row_lists(const uint32_t* A, const unsigned long long* na_d, const uint32_t* B,
+                                  const unsigned long long* nb_d, uint32_t* out, unsigned long long* nm) {
+  const uint64_t na = *na_d, nb = *nb_d;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *nm = na + nb;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < na + nb;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    if (i < na) {
+      const uint32_t x = A[i];
+      out[i + lower_bound_dev<uint32_t, uint64_t>(B, 0, nb, x)] = x;  // B entries < x
+    } else {
+      const uint32_t x = B[i - na];
+      out[(i - na) + lower_bound_dev<uint32_t, uint64_t>(A, 0, na, x + 1)] = x;  // A entries <= x
+    }
+  }
+}
+
 // Row delta of the j-th touched row (0 past the list).
 struct RowDelta {
   const uint32_t* T;
@@ -896,8 +939,25 @@ void ingest_phase_a(dynpr_context* ctx, IngestPlan& P, const dynpr_graph* g, int
   }
   check_launch();
   unsigned long long* nt = &P.st->nt;
-  if (P.t_cap)
+  if (P.t_cap && g->all_loops) {
+    // O(batch): the rows the batch changes, from its sorted keys (the
+    // deletion and insertion runs merged, then deduplicated) -- not a
+    // selection over all n vertices (Kronecker-27: ~0.3 ms per CSR)
+    const uint64_t mask = (1ull << P.sb) - 1;
+    auto* A = reinterpret_cast<uint32_t*>(P.keys);  // (free after the sort + unique)
+    uint32_t* B = A + nb1;
+    auto* Mg = reinterpret_cast<uint32_t*>(P.keys2);
+    prims::select_if<uint32_t>(ctx, RowHead{P.ukeys, &P.st->ndu, P.vs.touched, P.sb, mask, false},
+                               RowOf{P.ukeys, P.sb, mask}, P.nb, A, &P.st->nrd, st, nu);
+    prims::select_if<uint32_t>(ctx, RowHead{P.ukeys, &P.st->ndu, P.vs.touched, P.sb, mask, true},
+                               RowOf{P.ukeys, P.sb, mask}, P.nb, B, &P.st->nri, st, nu);
+    k_merge_row_lists<<<grid_for(P.nb, 256, 4096), 256, 0, st>>>(A, &P.st->nrd, B, &P.st->nri, Mg, &P.st->nrm);
+    check_launch();
+    count_launch(ctx);
+    prims::unique_sorted<uint32_t>(ctx, Mg, 2 * P.nb, P.T, nt, st, &P.st->nrm);
+  } else if (P.t_cap) {
     prims::select_if<uint32_t>(ctx, prims::Nonzero<uint8_t>{P.vs.touched}, prims::Iota32{}, n, P.T, nt, st);
+  }
   if (P.nb) {
     prims::select_if<uint64_t>(ctx, KeepTag{P.ukeys, P.keep, tag, false}, Untag{P.ukeys, tag}, P.nb, P.dp,
                                &P.st->ndp, st, nu);

@@ -109,6 +109,9 @@ __global__ void __launch_bounds__(kPT) k_tile_sum(Load load, uint64_t count, con
 }
 
 // One block: exclusive scan of the tile totals in place; *total = their sum.
+// Each thread takes kScanR consecutive totals per round (8192 per round), so
+// a 134 M-item scan (65536 tiles) runs 8 block rounds instead of 64.
+constexpr int kScanR = 8;
 template <class T>
 __global__ void __launch_bounds__(1024) k_scan_tiles(T* partial, uint64_t ntiles, T* total) {
   __shared__ T s_w[32];
@@ -116,10 +119,16 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(T* partial, uint64_t ntiles
   const unsigned lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (threadIdx.x == 0) s_carry = T(0);
   __syncthreads();
-  for (uint64_t b = 0; b < ntiles; b += 1024) {
-    const uint64_t i = b + threadIdx.x;
-    const T x = i < ntiles ? partial[i] : T(0);
-    const T inc = warp_incl_scan(x);
+  for (uint64_t b = 0; b < ntiles; b += 1024 * kScanR) {
+    const uint64_t i0 = b + (uint64_t)threadIdx.x * kScanR;
+    T x[kScanR];
+    T sum = T(0);
+#pragma unroll
+    for (int r = 0; r < kScanR; ++r) {
+      x[r] = i0 + r < ntiles ? partial[i0 + r] : T(0);
+      sum += x[r];
+    }
+    const T inc = warp_incl_scan(sum);
     if (lane == 31) s_w[w] = inc;
     __syncthreads();
     if (w == 0) {
@@ -127,10 +136,14 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(T* partial, uint64_t ntiles
       s_w[lane] = warp_incl_scan(y) - y;
     }
     __syncthreads();
-    const T ex = s_carry + s_w[w] + inc - x;
-    if (i < ntiles) partial[i] = ex;
+    T ex = s_carry + s_w[w] + inc - sum;
+#pragma unroll
+    for (int r = 0; r < kScanR; ++r) {
+      if (i0 + r < ntiles) partial[i0 + r] = ex;
+      ex += x[r];
+    }
     __syncthreads();
-    if (threadIdx.x == 1023) s_carry = ex + x;
+    if (threadIdx.x == 1023) s_carry = ex;
     __syncthreads();
   }
   if (threadIdx.x == 0 && total) *total = s_carry;

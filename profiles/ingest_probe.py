@@ -4,6 +4,7 @@ incrementally, layout.cu build_incremental), and the same with the base
 unprepared (layout built from scratch)."""
 import os, sys, time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.environ.get("DYNPR_PKG_ROOT", ROOT)  # (A/B: another build of the package)
 sys.path.insert(0, ROOT)
 import torch
 import paper_2404_08299_b200 as dp

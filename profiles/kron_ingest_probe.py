@@ -7,6 +7,7 @@ import sys
 import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.environ.get("DYNPR_PKG_ROOT", ROOT)  # (A/B: another build of the package)
 sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 import paper_2404_08299_b200 as dp  # noqa: E402

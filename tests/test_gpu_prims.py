@@ -2,7 +2,8 @@
 (csrc/prims.cuh: LSD radix sort, exclusive scan, stable select, unique)
 against numpy, through dynpr_debug_prims, at the sizes where their code
 paths change: empty, single element, tile edges (1024-key small-sort tiles,
-2048-item scan / select tiles, 4096-key large-sort tiles), the 64-tile
+2048-item scan / select tiles, 4096-key large-sort tiles, the 8192-tile
+rounds of the tile-total scan), the 64-tile
 limit of the in-scatter base scan, the 2^18 small / large sort switch, and
 multi-pass keys (all digits), constant keys and already-sorted input
 (stability is checked through the values)."""
@@ -15,6 +16,8 @@ pytestmark = pytest.mark.gpu
 
 SIZES = [0, 1, 2, 31, 1023, 1024, 1025, 2047, 2048, 2049, 4095, 4096, 4097, 65535, 65536, 65537,
          (1 << 18), (1 << 18) + 1, 300001, 1 << 21]
+# the tile-total scan takes 8192 tiles (of 2048 items) per block round
+BIG = [8192 * 2048, 8192 * 2048 + 1, 2 * 8192 * 2048 + 2049]
 
 
 def _call(dp, op, a, b=None, bits=0, out_dtype=None, out2_dtype=None, n_out=None):
@@ -57,7 +60,7 @@ def test_radix_sort_pairs_is_stable(dp, n):
     assert np.array_equal(ko[:n], wide[order]) and np.array_equal(vo[:n], vals[order])
 
 
-@pytest.mark.parametrize("n", SIZES)
+@pytest.mark.parametrize("n", SIZES + BIG)
 def test_exclusive_scan_u64(dp, n):
     rng = np.random.default_rng(n + 11)
     a = rng.integers(0, 1 << 40, n, dtype=np.uint64)
@@ -67,7 +70,7 @@ def test_exclusive_scan_u64(dp, n):
     assert total == int(a.sum(dtype=np.uint64)) if n else total == 0
 
 
-@pytest.mark.parametrize("n", SIZES)
+@pytest.mark.parametrize("n", SIZES + BIG)
 def test_select_nonzero_indices(dp, n):
     rng = np.random.default_rng(n + 13)
     for density in (0.0, 0.01, 0.5, 1.0):
