@@ -251,35 +251,45 @@ __device__ __forceinline__ void copy_lane(uint32_t* sell, uint64_t base, unsigne
 // single region, copy-on-write: a slice is re-built iff one of its vertices'
 // in-lists changed; its length is then the longest of its 32 new segments
 // (the relabelling is no longer sorted), else it is shared.
-__global__ void k_slice_touched_len(const uint32_t* indeg, const uint8_t* touched, uint32_t M, uint32_t n,
-                                    uint64_t S, uint64_t* len32) {
+// Driven by the touched rows (old ids), O(batch) instead of a pass over
+// every slice: a warp per touched single-region vertex computes its slice's
+// length (len32 zeroed before; two touched vertices of one slice write the
+// same value).
+__global__ void k_slice_touched_len_rows(const uint32_t* rows, uint64_t cnt, const uint32_t* inv,
+                                         const uint32_t* indeg, uint32_t M, uint32_t n, uint64_t* len32) {
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / 32;
   const unsigned lane = threadIdx.x & 31;
   const uint64_t nw = (uint64_t)gridDim.x * blockDim.x / 32;
-  for (uint64_t s = warp; s <= S; s += nw) {
+  for (uint64_t i = warp; i < cnt; i += nw) {
+    const uint32_t vn = inv[rows[i]];
+    if (vn < M) continue;  // (warp-uniform) multi region
+    const uint64_t s = (vn - (uint64_t)M) / 32;
     const uint64_t v = (uint64_t)M + 32 * s + lane;
-    const bool in = s < S && v < n;
-    const unsigned d = in ? indeg[v] : 0u;
-    const bool any = __any_sync(0xffffffffu, in && touched[v]);
+    const unsigned d = v < n ? indeg[v] : 0u;
     const unsigned mx = __reduce_max_sync(0xffffffffu, d);
-    if (lane == 0) len32[s] = any ? 32ull * ((mx + 3u) & ~3u) : 0ull;
+    if (lane == 0) len32[s] = 32ull * ((mx + 3u) & ~3u);
   }
 }
 __global__ void k_sbase_cow(const uint64_t* sbase0, const uint64_t* len32, const uint64_t* dpos, uint64_t S,
                             uint64_t rel, uint64_t* sbase) {
   GRID_STRIDE(s, S + 1) sbase[s] = (s < S && len32[s]) ? rel + dpos[s] : sbase0[s];
 }
-__global__ void k_fill_single_cow(const uint64_t* offT, const uint32_t* tgtT, const uint32_t* perm,
-                                  const uint32_t* inv, const uint32_t* indeg, uint32_t M, uint32_t n, uint64_t S,
-                                  const uint64_t* len32, const uint64_t* sbase, uint32_t* sell,
-                                  const uint8_t* touched, const uint64_t* sbase0) {
+// A warp per touched single-region vertex rebuilds its slice: touched lanes
+// re-gathered, the others copied from the parent (a slice holding several
+// touched vertices is rebuilt once per vertex, with identical words).
+__global__ void k_fill_single_cow_rows(const uint32_t* rows, uint64_t cnt, const uint64_t* offT, const uint32_t* tgtT,
+                                       const uint32_t* perm, const uint32_t* inv, const uint32_t* indeg, uint32_t M,
+                                       uint32_t n, const uint64_t* len32, const uint64_t* sbase, uint32_t* sell,
+                                       const uint8_t* touched, const uint64_t* sbase0) {
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / 32;
   const unsigned lane = threadIdx.x & 31;
   const uint64_t nw = (uint64_t)gridDim.x * blockDim.x / 32;
-  for (uint64_t s = warp; s < S; s += nw) {
+  for (uint64_t i = warp; i < cnt; i += nw) {
+    const uint32_t w = inv[rows[i]];
+    if (w < M) continue;  // (warp-uniform) multi region
+    const uint64_t s = (w - (uint64_t)M) / 32;
     const uint32_t L = (uint32_t)(len32[s] / 32);
-    if (!L) continue;  // shared with the parent
-    const uint64_t vn = M + s * 32 + lane;
+    const uint64_t vn = (uint64_t)M + s * 32 + lane;
     const bool valid = vn < n;
     const uint32_t deg = valid ? indeg[vn] : 0u;
     if (valid && touched[vn])
@@ -295,18 +305,25 @@ __global__ void k_fill_single_cow(const uint64_t* offT, const uint32_t* tgtT, co
 __global__ void k_multi_touched_nch(const uint32_t* indeg, const uint8_t* touched, uint32_t M, uint32_t* nch) {
   GRID_STRIDE(v, (uint64_t)M + 1) nch[v] = (v < M && touched[v]) ? (indeg[v] + 255u) / 256u : 0u;
 }
-__global__ void k_multi_cow_segments(const uint32_t* indeg, const uint32_t* indeg0, const uint8_t* touched,
-                                     uint32_t M, const uint32_t* apos, uint64_t first, const uint32_t* pbase0,
-                                     uint32_t* pbase, uint32_t* mseg_v, uint32_t* mseg_len) {
-  GRID_STRIDE(v, M) {
-    if (!touched[v]) continue;
+// A warp per touched multi vertex, its lanes striding over the chunks (a
+// hub's thousands of chunks are not one thread's serial loop).
+__global__ void k_multi_cow_segments_rows(const uint32_t* rows, uint64_t cnt, const uint32_t* inv,
+                                          const uint32_t* indeg, const uint32_t* indeg0, uint32_t M,
+                                          const uint32_t* apos, uint64_t first, const uint32_t* pbase0,
+                                          uint32_t* pbase, uint32_t* mseg_v, uint32_t* mseg_len) {
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / 32;
+  const unsigned lane = threadIdx.x & 31;
+  const uint64_t nw = (uint64_t)gridDim.x * blockDim.x / 32;
+  for (uint64_t i = warp; i < cnt; i += nw) {
+    const uint32_t v = inv[rows[i]];
+    if (v >= M) continue;  // (warp-uniform) single region
     const uint32_t d0 = indeg0[v], p0 = pbase0[v];
-    for (uint32_t j = 0; j < (d0 + 255u) / 256u; ++j) mseg_len[p0 + j] = 0u;  // retired
+    for (uint32_t j = lane; j < (d0 + 255u) / 256u; j += 32) mseg_len[p0 + j] = 0u;  // retired
     const uint32_t d = indeg[v], b = (uint32_t)(first + apos[v]);
     const uint32_t nch = (d + 255u) / 256u;
-    pbase[v] = b;
-    for (uint32_t j = 0; j < nch; ++j) {
-      mseg_v[b + j] = (uint32_t)v;
+    if (lane == 0) pbase[v] = b;
+    for (uint32_t j = lane; j < nch; j += 32) {
+      mseg_v[b + j] = v;
       mseg_len[b + j] = (j + 1 < nch) ? 256u : d - 256u * j;
     }
   }
@@ -601,7 +618,11 @@ Layout* build_incremental(dynpr_context* ctx, const dynpr_graph* gT, const dynpr
     L->sbase = dalloc<uint64_t>(ctx, S + 1);
     auto* len32 = reinterpret_cast<uint64_t*>(ctx->scratch64b.as<unsigned long long>(2 * (S + 1)));
     uint64_t* dpos = len32 + S + 1;
-    k_slice_touched_len<<<grid(ctx, (S + 1) * 32), 256, 0, st>>>(L->indeg, flagT, M, n, S, len32);
+    // (the touched rows drive the slice passes: O(batch), not O(slices))
+    DYNPR_CK(cudaMemsetAsync(len32, 0, (S + 1) * 8, st));
+    if (seed.n_T)
+      k_slice_touched_len_rows<<<grid(ctx, seed.n_T * 32), 256, 0, st>>>(seed.rows_T, seed.n_T, L->inv, L->indeg,
+                                                                          M, n, len32);
     check_launch();
     prims::scan_array<uint64_t>(ctx, len32, dpos, S + 1, st);
     const uint64_t s_new = read_u64(ctx, dpos + S);
@@ -609,8 +630,9 @@ Layout* build_incremental(dynpr_context* ctx, const dynpr_graph* gT, const dynpr
     k_sbase_cow<<<grid(ctx, S + 1), 256, 0, st>>>(P->sbase, len32, dpos, S, rel_words(L->sell_s, ds), L->sbase);
     check_launch();
     if (s_new) {
-      k_fill_single_cow<<<grid(ctx, S * 32), 256, 0, st>>>(gT->off, gT->tgt, L->perm, L->inv, L->indeg, M, n, S,
-                                                           len32, L->sbase, L->sell_s, flagT, P->sbase);
+      k_fill_single_cow_rows<<<grid(ctx, seed.n_T * 32), 256, 0, st>>>(seed.rows_T, seed.n_T, gT->off, gT->tgt,
+                                                                        L->perm, L->inv, L->indeg, M, n, len32,
+                                                                        L->sbase, L->sell_s, flagT, P->sbase);
       check_launch();
     }
     count_launch(ctx, 3);
@@ -642,9 +664,10 @@ Layout* build_incremental(dynpr_context* ctx, const dynpr_graph* gT, const dynpr
       DYNPR_CK(cudaMemcpyAsync(L->mseg_len, P->mseg_len, P->n_mseg * 4, cudaMemcpyDeviceToDevice, st));
     }
     DYNPR_CK(cudaMemcpyAsync(L->mbase, P->mbase, (P->n_mslices + 1) * 8, cudaMemcpyDeviceToDevice, st));
-    if (M) {
-      k_multi_cow_segments<<<grid(ctx, M), 256, 0, st>>>(L->indeg, P->indeg, flagT, M, apos, first, P->pbase,
-                                                         L->pbase, L->mseg_v, L->mseg_len);
+    if (M && seed.n_T) {
+      k_multi_cow_segments_rows<<<grid(ctx, seed.n_T * 32), 256, 0, st>>>(seed.rows_T, seed.n_T, L->inv, L->indeg,
+                                                                           P->indeg, M, apos, first, P->pbase,
+                                                                           L->pbase, L->mseg_v, L->mseg_len);
       check_launch();
     }
     DYNPR_CK(cudaMemcpyAsync(L->pbase + M, &L->n_mseg, 4, cudaMemcpyHostToDevice, st));  // (pageable: synchronous)
