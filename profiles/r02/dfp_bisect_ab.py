@@ -27,8 +27,8 @@ for scale, frac in cases:
         for spec in sys.argv[2:]:
             d, _, kv = spec.partition(":")
             env = dict(os.environ)
-            if kv:
-                k, v = kv.split("=")
+            for item in filter(None, kv.split("+")):  # VAR=value[+VAR2=value2]
+                k, v = item.split("=")
                 env[k] = v
             out = subprocess.run([sys.executable, "-c", CHILD, os.path.abspath(d), scale, frac], capture_output=True,
                                  text=True, cwd="/tmp", env=env)
