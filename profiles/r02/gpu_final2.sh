@@ -1,9 +1,9 @@
 # round 2 session 4: full GPU suite, smoke, bench, reference arm
 set -x
-mkdir -p gpurun_out/r2s4
+mkdir -p gpurun_out/r2s4b
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
-timeout 2400 python -m pytest tests -q -m gpu -x --durations=25 > gpurun_out/r2s4/gputest.log 2>&1; echo "pytest exit $?" >> gpurun_out/r2s4/gputest.log
-timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2s4/smoke.log 2>&1; echo "smoke exit $?" >> gpurun_out/r2s4/smoke.log
-timeout 900 python bench.py > gpurun_out/r2s4/bench.log 2>&1
-timeout 900 python bench.py --impl reference > gpurun_out/r2s4/bench_ref.log 2>&1
-tail -3 gpurun_out/r2s4/gputest.log; tail -1 gpurun_out/r2s4/smoke.log; tail -c 1500 gpurun_out/r2s4/bench.log; tail -c 600 gpurun_out/r2s4/bench_ref.log
+timeout 2400 python -m pytest tests -q -m gpu -x --durations=25 > gpurun_out/r2s4b/gputest.log 2>&1; echo "pytest exit $?" >> gpurun_out/r2s4b/gputest.log
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2s4b/smoke.log 2>&1; echo "smoke exit $?" >> gpurun_out/r2s4b/smoke.log
+timeout 900 python bench.py > gpurun_out/r2s4b/bench.log 2>&1
+timeout 900 python bench.py --impl reference > gpurun_out/r2s4b/bench_ref.log 2>&1
+tail -3 gpurun_out/r2s4b/gputest.log; tail -1 gpurun_out/r2s4b/smoke.log; tail -c 1500 gpurun_out/r2s4b/bench.log; tail -c 600 gpurun_out/r2s4b/bench_ref.log
