@@ -7,6 +7,7 @@ processed vertices, pending out-edges and the expansion decided after it.
 import ctypes as C
 import os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.environ.get("DYNPR_PKG_ROOT", ROOT)  # (A/B: another build of the package)
 sys.path.insert(0, ROOT)
 import numpy as np
 import paper_2404_08299_b200 as dp
