@@ -357,15 +357,14 @@ __constant__ SweepArgs c_loop_args[2];
 // Sweep kernels: persistent grids of 256-thread CTAs at full occupancy.
 constexpr int kSweepThreads = kThreads;
 constexpr int kSweepWarps = kSweepThreads / 32;
-// k_sweep_single: slices per dynamic grab -- 4 for Static, 8 for the
-// frontier sweeps (profiles/r02/s5/frontier_split_grab_ab.txt: RMAT-24 DF-P
-// 1e-6 / 1e-5 / 1e-4 / 1e-3 6.21 -> 6.16, 6.43 -> 6.37, 13.06 -> 13.00,
-// 27.47 -> 27.35 ms, RMAT-26 1e-4 61.3 -> 61.0; 16 was 10-17% slower).  The
-// latency-mode sweep's light grabs stay at 2 for both (4 made RMAT-20 DF-P
-// 1e-7 19% slower, frontier_grab_ab.txt).
-constexpr unsigned kSplitGrab = 4;
-template <bool FLAGGED>
-constexpr unsigned kSplitGrabOf = FLAGGED ? 8u : kSplitGrab;
+// k_sweep_single: slices per dynamic grab, 8 (was 4; measured in the loop
+// graph, profiles/r02/s5/*split_grab_ab.txt: Static RMAT-24 55.93 -> 55.62
+// ms, RMAT-25 117.7 -> 116.7, RMAT-26 within noise, 2 was 5-7% slower;
+// DF-P RMAT-24 1e-6 / 1e-5 / 1e-4 / 1e-3 6.21 -> 6.16, 6.43 -> 6.37,
+// 13.06 -> 13.00, 27.47 -> 27.35 ms, RMAT-26 1e-4 61.3 -> 61.0; 16 was
+// 10-17% slower).  The latency-mode sweep's light grabs stay at 2 (4 made
+// RMAT-20 DF-P 1e-7 19% slower, frontier_grab_ab.txt).
+constexpr unsigned kSplitGrab = 8;
 
 // ---- single-segment vertices: warp per 32-vertex slice ------------------------
 // In-sweep pull (SweepArgs::pull_fused): this sweep follows an expansion
@@ -383,11 +382,11 @@ __device__ __forceinline__ void b_sweep_single(const SweepArgs& a) {
   // slices grabbed dynamically, kSplitGrab at a time (counter in the record)
   for (;;) {
     unsigned g = 0;
-    if (lane == 0) g = atomicAdd(&a.red->ticket_light, kSplitGrabOf<FLAGGED>);
+    if (lane == 0) g = atomicAdd(&a.red->ticket_light, kSplitGrab);
     g = __shfl_sync(kFull, g, 0);
     const uint64_t s0 = a.ss_lo + g;
     if (s0 >= a.ss_hi) break;
-    const uint64_t s1 = s0 + kSplitGrabOf<FLAGGED> < a.ss_hi ? s0 + kSplitGrabOf<FLAGGED> : a.ss_hi;
+    const uint64_t s1 = s0 + kSplitGrab < a.ss_hi ? s0 + kSplitGrab : a.ss_hi;
     // the grab's slice bases in one load (lane i: slice s0 + i), so a
     // slice's index loads do not wait for its own base load
     const uint64_t sb_lane = s0 + lane < s1 ? a.sbase[s0 + lane] : 0ull;
